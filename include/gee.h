@@ -1,0 +1,174 @@
+/*
+ * gee.h -- C ABI of libgee.so, the B200 (sm_100a) sparse Graph Encoder
+ * Embedding hot path (arXiv 2406.03726).
+ *
+ * Plain pointers, sizes and a cudaStream_t passed as void*; no C++ or torch
+ * types cross this boundary.  All array pointers are DEVICE pointers unless
+ * a name says _host.  Every call is stream-ordered, never synchronises the
+ * host, never allocates device memory (workspaces are caller-provided after
+ * a *_workspace size query) and is re-entrant across streams.
+ *
+ * Each entry point replaces one reference interface of the `graphee` 0.1.0
+ * package (paths relative to /root/reference/pkg/src/graphee):
+ *
+ *   gee_label_hist           LabelVector.class_counts  embedding.py:68-71
+ *                            + build_weight_matrix     embedding.py:92-107
+ *   gee_csr_build            EdgeList.to_csr           graph_io.py:78-92
+ *                            -> _kernels.coo_to_csr    _kernels.py:39-130, :314/:321
+ *   gee_degree               degree_vector             sparse.py:193-196
+ *                            (of A, or of add_identity(A) sparse.py:184-190)
+ *                            + the scale of laplacian_normalize sparse.py:211-215
+ *   gee_add_identity         _kernels.add_identity_kernel _kernels.py:137-198, :315/:322
+ *   gee_laplacian_normalize  laplacian_normalize       sparse.py:199-226
+ *   gee_embed                spmm(A', build_weight_matrix(Y)).to_dense()
+ *                            sparse.py:166-181 -> _kernels.spmm_kernel _kernels.py:208-307
+ *                            + correlate_rows          embedding.py:134-143
+ *   gee_encode_edges         encode(EdgeList.to_csr(), labels, opts)
+ *                            embedding.py:110-131 (the reference's timed region,
+ *                            cli.py:170-180)
+ *
+ * Errors.  Host-detectable argument problems return a status synchronously
+ * (GEE_E_ARG, GEE_E_WORKSPACE) and launch failures return GEE_E_CUDA.
+ * Data-dependent problems are detected on the device and OR-ed into the
+ * caller's device word `err` as GEE_ERR_* bits; the caller reads it once
+ * after synchronising and raises the reference's exception class:
+ *   GEE_ERR_NEG_DEGREE  -> NumericalDomainError  (sparse.py:211-212)
+ *   GEE_ERR_NONFINITE   -> NumericalDomainError  (embedding.py:137-138)
+ *   GEE_ERR_LABEL       -> StructuralError       (embedding.py:45-51)
+ *   GEE_ERR_EDGE_RANGE  -> StructuralError       (graph_io.py:65-70)
+ *   GEE_ERR_EDGE_WEIGHT -> StructuralError       (graph_io.py:71-72)
+ */
+#ifndef GEE_H
+#define GEE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* synchronous status codes */
+#define GEE_OK 0
+#define GEE_E_ARG 1
+#define GEE_E_WORKSPACE 2
+#define GEE_E_CUDA 3
+
+/* device error bits (OR-ed into *err) */
+#define GEE_ERR_NEG_DEGREE 1
+#define GEE_ERR_NONFINITE 2
+#define GEE_ERR_LABEL 4
+#define GEE_ERR_EDGE_RANGE 8
+#define GEE_ERR_EDGE_WEIGHT 16
+
+/* EmbedOptions (embedding.py:74-89) as a bit set */
+#define GEE_LAPLACIAN 1u
+#define GEE_DIAGONAL 2u
+#define GEE_CORRELATION 4u
+
+/* edge-weight element types */
+#define GEE_W_UNIT 0 /* w == NULL: every weight is 1.0 */
+#define GEE_W_F64 1
+#define GEE_W_F32 2 /* promoted to f64 exactly, as EdgeList does (graph_io.py:61) */
+
+const char *gee_version(void);
+const char *gee_status_string(int status);
+/* last CUDA error text seen by this thread (for GEE_E_CUDA) */
+const char *gee_last_error_string(void);
+
+/* Validate an edge list on the device: 0 <= rows,cols < n and finite
+ * weights (EdgeList.__post_init__, graph_io.py:58-72). */
+int gee_validate_edges(const int64_t *rows, const int64_t *cols, const void *w, int w_type,
+                       int64_t n_edges, int64_t n_nodes, int32_t *err, void *stream);
+
+/* K1: labels int64[n] in {-1..k-1} -> y32 int32[n], counts int64[k]
+ * (bit-exact n_k) and inv_nk f64[k] = 1.0/n_k (0 for empty classes, which
+ * are never read).  Bad labels set GEE_ERR_LABEL. */
+int gee_label_hist(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_t *counts,
+                   double *inv_nk, int32_t *err, void *stream);
+
+/* K2: edge list -> CSR with the reference's exact structure and values:
+ * undirected lists are symmetrised in the order [originals, reversed
+ * off-diagonals]; entries are ordered by (row, col); duplicates are summed
+ * left to right in that stream order; exact-zero sums are dropped.
+ *   capacity of col/val: n_edges (directed) or 2*n_edges (undirected)
+ *   row_ptr int64[n_rows+1], *nnz (device int64) = row_ptr[n_rows]
+ * deg_flags: 0, or GEE_LAPLACIAN [| GEE_DIAGONAL] to also produce, fused,
+ * the degree vector of A (or A+I) and scale = 1/sqrt(deg) (0 where deg==0)
+ * into deg/scale (f64[n_rows]); requires n_rows == n_cols.
+ * compact = 0 leaves each row's unique entries at the start of its
+ * pre-dedup slot range (row i: [slot_ptr[i], slot_ptr[i]+row_cnt[i])) and
+ * only gee_embed may consume it; compact = 1 produces a standard CSR. */
+int gee_csr_build_workspace(int64_t n_edges, int64_t n_rows, int64_t n_cols, int directed,
+                            size_t *ws_bytes);
+int gee_csr_build(const int64_t *rows, const int64_t *cols, const void *w, int w_type,
+                  int64_t n_edges, int64_t n_rows, int64_t n_cols, int directed, int compact,
+                  int64_t *row_ptr, uint32_t *row_cnt, int32_t *col, double *val, int64_t *nnz,
+                  unsigned deg_flags, double *deg, double *scale, void *ws, size_t ws_bytes,
+                  int32_t *err, void *stream);
+
+/* K3: degree of A (flags 0) or of A+I (GEE_DIAGONAL) for a square CSR,
+ * folded per row in storage order exactly as np.bincount does, plus
+ * scale = 1/sqrt(deg).  deg < 0 sets GEE_ERR_NEG_DEGREE. */
+int gee_degree(const int64_t *row_ptr, const int32_t *col, const double *val, int64_t n,
+               unsigned flags, double *deg, double *scale, int32_t *err, void *stream);
+
+/* Materialised A+I (the reference seam; the embed path fuses it instead).
+ * Two phases: counts -> (caller scans nothing; *nnz_out on device) then fill.
+ * out capacity nnz + n. */
+int gee_add_identity(const int64_t *row_ptr, const int32_t *col, const double *val, int64_t n,
+                     int64_t *out_row_ptr, int32_t *out_col, double *out_val, int64_t *nnz_out,
+                     void *ws, size_t ws_bytes, void *stream);
+int gee_add_identity_workspace(int64_t n, size_t *ws_bytes);
+
+/* Materialised D^-1/2 A D^-1/2 with zero pruning (bit-exact with
+ * sparse.py:217: (v*s_r)*s_c).  deg < 0 sets GEE_ERR_NEG_DEGREE. */
+int gee_laplacian_normalize(const int64_t *row_ptr, const int32_t *col, const double *val,
+                            int64_t n, const double *deg, int64_t *out_row_ptr,
+                            int32_t *out_col, double *out_val, int64_t *nnz_out, void *ws,
+                            size_t ws_bytes, int32_t *err, void *stream);
+int gee_laplacian_normalize_workspace(int64_t n, size_t *ws_bytes);
+
+/* K4: Z[r - row_begin, :] for r in [row_begin, row_end):
+ *   Z[r, c] = sum over stored (r, j) with Y_j == c of a'_rj * inv_nk[c]
+ * with a' = a (+1 on the diagonal under GEE_DIAGONAL, inserted if absent)
+ * and, under GEE_LAPLACIAN, a' <- (a' * scale_r) * scale_j; under
+ * GEE_CORRELATION each nonzero row is divided by its 2-norm (non-finite
+ * rows set GEE_ERR_NONFINITE).  row_cnt may be NULL (standard CSR) or the
+ * uncompacted counts from gee_csr_build(compact=0).  val may be NULL for
+ * unit weights.  z is dense row-major with leading dimension ldz >= k. */
+int gee_embed_workspace(int64_t n_rows, size_t *ws_bytes);
+int gee_embed(const int64_t *row_ptr, const uint32_t *row_cnt, const int32_t *col,
+              const double *val, int64_t row_begin, int64_t row_end, const int32_t *y32,
+              const double *inv_nk, const double *scale, int32_t k, unsigned flags, double *z,
+              int64_t ldz, void *ws, size_t ws_bytes, int32_t *err, void *stream);
+
+/* The whole reference timed region on the device: edge list + labels ->
+ * Z (N x K, f64).  Optionally also returns the uncompacted CSR through
+ * the workspace (not exposed).  One stream, no host synchronisation. */
+int gee_encode_edges_workspace(int64_t n_edges, int64_t n_nodes, int32_t k, int directed,
+                               size_t *ws_bytes);
+int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, int w_type,
+                     int64_t n_edges, int64_t n_nodes, int directed, const int64_t *labels,
+                     int32_t k, unsigned flags, double *z, void *ws, size_t ws_bytes,
+                     int32_t *err, void *stream);
+
+/* Launch statistics: number of kernels this thread launched through the
+ * library since the last reset (for bench.py's gpu_launches). */
+uint64_t gee_launch_count(void);
+void gee_reset_launch_count(void);
+
+/* Per-kernel timing for the benchmark: after gee_profile_start(stream) the
+ * calling thread's launches are each followed by an event record on their
+ * stream; gee_profile_stop() ends recording and returns the mark count;
+ * gee_profile_read() synchronises on the last mark and returns, per launch,
+ * the elapsed ms since the previous mark and the kernel name. */
+int gee_profile_start(void *stream);
+int gee_profile_stop(void);
+int gee_profile_read(float *ms, const char **names, int cap);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GEE_H */

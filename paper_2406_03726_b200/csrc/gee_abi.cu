@@ -1,0 +1,275 @@
+// gee_abi.cu -- the extern "C" boundary of libgee.so (declared in include/gee.h).
+#include <mutex>
+#include <stdio.h>
+#include <string.h>
+
+#include "gee_common.cuh"
+
+#define GEE_VERSION "gee-b200 0.1.0 (sm_100a)"
+
+namespace gee {
+
+static thread_local uint64_t t_launches = 0;
+static thread_local char t_last_error[256] = "";
+
+uint64_t &launch_counter() { return t_launches; }
+
+// ---- per-kernel timing marks (bench.py only) --------------------------------
+constexpr int kMaxMarks = 4096;
+struct Profile {
+    bool on = false;
+    int n = 0;
+    cudaEvent_t ev[kMaxMarks + 1] = {};
+    const char *name[kMaxMarks + 1] = {};
+};
+static thread_local Profile t_prof;
+
+void profile_mark(const char *name, cudaStream_t st) {
+    Profile &p = t_prof;
+    if (!p.on || p.n >= kMaxMarks) return;
+    if (!p.ev[p.n]) cudaEventCreate(&p.ev[p.n]);
+    cudaEventRecord(p.ev[p.n], st);
+    p.name[p.n] = name;
+    ++p.n;
+}
+
+int cuda_status(cudaError_t e) {
+    snprintf(t_last_error, sizeof(t_last_error), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+    return GEE_E_CUDA;
+}
+
+int num_sms() {
+    static int cache[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return kSMs;
+    if (!cache[dev]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+            v = kSMs;
+        cache[dev] = v;
+    }
+    return cache[dev];
+}
+
+int label_hist(const int64_t *, int64_t, int32_t, int32_t *, int64_t *, double *, int32_t *, cudaStream_t);
+size_t csr_build_workspace(int64_t E, int64_t n_rows, int directed);
+int csr_build(const int64_t *, const int64_t *, const void *, int, int64_t, int64_t, int64_t, int, int,
+              int64_t *, unsigned *, int32_t *, double *, int64_t *, unsigned, double *, double *, void *,
+              size_t, int32_t *, cudaStream_t);
+int degree(const int64_t *, const int32_t *, const double *, int64_t, unsigned, double *, double *,
+           int32_t *, cudaStream_t);
+size_t add_identity_workspace(int64_t n);
+int add_identity(const int64_t *, const int32_t *, const double *, int64_t, int64_t *, int32_t *, double *,
+                 int64_t *, void *, size_t, cudaStream_t);
+size_t laplacian_workspace(int64_t n);
+int laplacian_normalize(const int64_t *, const int32_t *, const double *, int64_t, const double *, int64_t *,
+                        int32_t *, double *, int64_t *, void *, size_t, int32_t *, cudaStream_t);
+size_t embed_workspace(int64_t n_rows);
+int embed(const int64_t *, const unsigned *, const int32_t *, const double *, int64_t, int64_t,
+          const int32_t *, const double *, const double *, int, unsigned, double *, int64_t, void *, size_t,
+          int32_t *, cudaStream_t);
+int validate_edges(const int64_t *, const int64_t *, const void *, int, int64_t, int64_t, int32_t *,
+                   cudaStream_t);
+
+static bool index_ok(int64_t x) { return x >= 0 && x < ((int64_t)1 << 31); }
+static bool wt_ok(int wt, const void *w) {
+    if (wt == GEE_W_UNIT) return true;
+    return (wt == GEE_W_F64 || wt == GEE_W_F32) && w != nullptr;
+}
+
+// Pipeline workspace: everything encode needs between K1 and K4.
+struct EncodeWs {
+    int32_t *y32;
+    int64_t *counts;
+    double *inv, *deg, *scale;
+    int64_t *row_ptr;
+    unsigned *row_cnt;
+    int32_t *col;
+    double *val;
+    void *csr_ws;
+    size_t csr_bytes;
+    void *emb_ws;
+    size_t emb_bytes;
+};
+
+static size_t carve_encode(Carver &cv, EncodeWs &w, int64_t E, int64_t n, int32_t k, int directed) {
+    const int64_t M = directed ? E : 2 * E;
+    w.y32 = cv.take<int32_t>((size_t)n + 1);
+    w.counts = cv.take<int64_t>((size_t)k);
+    w.inv = cv.take<double>((size_t)k);
+    w.deg = cv.take<double>((size_t)n + 1);
+    w.scale = cv.take<double>((size_t)n + 1);
+    w.row_ptr = cv.take<int64_t>((size_t)n + 1);
+    w.row_cnt = cv.take<unsigned>((size_t)n + 1);
+    w.col = cv.take<int32_t>((size_t)(M > 0 ? M : 1));
+    w.val = cv.take<double>((size_t)(M > 0 ? M : 1));
+    w.csr_bytes = csr_build_workspace(E, n, directed);
+    w.csr_ws = cv.take<char>(w.csr_bytes);
+    w.emb_bytes = embed_workspace(n);
+    w.emb_ws = cv.take<char>(w.emb_bytes);
+    return cv.bytes();
+}
+
+}  // namespace gee
+
+using namespace gee;
+
+extern "C" {
+
+const char *gee_version(void) { return GEE_VERSION; }
+
+const char *gee_status_string(int s) {
+    switch (s) {
+        case GEE_OK: return "ok";
+        case GEE_E_ARG: return "invalid argument";
+        case GEE_E_WORKSPACE: return "workspace too small";
+        case GEE_E_CUDA: return "CUDA error";
+        default: return "unknown status";
+    }
+}
+
+const char *gee_last_error_string(void) { return t_last_error; }
+
+uint64_t gee_launch_count(void) { return t_launches; }
+void gee_reset_launch_count(void) { t_launches = 0; }
+
+int gee_profile_start(void *stream) {
+    Profile &p = t_prof;
+    p.on = true;
+    p.n = 0;
+    profile_mark("start", (cudaStream_t)stream);
+    return GEE_OK;
+}
+
+int gee_profile_stop(void) {
+    t_prof.on = false;
+    return t_prof.n;
+}
+
+int gee_profile_read(float *ms, const char **names, int cap) {
+    Profile &p = t_prof;
+    if (p.n < 1) return 0;
+    GEE_CHECK_CUDA(cudaEventSynchronize(p.ev[p.n - 1]));
+    int m = 0;
+    for (int i = 1; i < p.n && m < cap; ++i, ++m) {
+        float t = 0.f;
+        GEE_CHECK_CUDA(cudaEventElapsedTime(&t, p.ev[i - 1], p.ev[i]));
+        ms[m] = t;
+        names[m] = p.name[i];
+    }
+    return m;
+}
+
+int gee_validate_edges(const int64_t *rows, const int64_t *cols, const void *w, int w_type, int64_t n_edges,
+                       int64_t n_nodes, int32_t *err, void *stream) {
+    if (n_edges < 0 || n_nodes < 0 || !wt_ok(w_type, w) || !err) return GEE_E_ARG;
+    return validate_edges(rows, cols, w, w_type, n_edges, n_nodes, err, (cudaStream_t)stream);
+}
+
+int gee_label_hist(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_t *counts, double *inv_nk,
+                   int32_t *err, void *stream) {
+    if (n < 0 || k < 1 || !index_ok(n) || !y32 || !counts || !inv_nk) return GEE_E_ARG;
+    if (n > 0 && !labels) return GEE_E_ARG;
+    return label_hist(labels, n, k, y32, counts, inv_nk, err, (cudaStream_t)stream);
+}
+
+int gee_csr_build_workspace(int64_t n_edges, int64_t n_rows, int64_t n_cols, int directed, size_t *ws_bytes) {
+    if (!ws_bytes || n_edges < 0 || !index_ok(n_edges) || !index_ok(n_rows) || !index_ok(n_cols))
+        return GEE_E_ARG;
+    *ws_bytes = csr_build_workspace(n_edges, n_rows, directed);
+    return GEE_OK;
+}
+
+int gee_csr_build(const int64_t *rows, const int64_t *cols, const void *w, int w_type, int64_t n_edges,
+                  int64_t n_rows, int64_t n_cols, int directed, int compact, int64_t *row_ptr, uint32_t *row_cnt,
+                  int32_t *col, double *val, int64_t *nnz, unsigned deg_flags, double *deg, double *scale,
+                  void *ws, size_t ws_bytes, int32_t *err, void *stream) {
+    if (!index_ok(n_edges) || !index_ok(n_rows) || !index_ok(n_cols) || !wt_ok(w_type, w)) return GEE_E_ARG;
+    if (!row_ptr || (!compact && !row_cnt) || (n_edges > 0 && (!rows || !cols || !col || !val)))
+        return GEE_E_ARG;
+    if (!directed && n_rows != n_cols) return GEE_E_ARG;
+    if (deg_flags && (n_rows != n_cols || !deg || ((deg_flags & GEE_LAPLACIAN) && !scale)))
+        return GEE_E_ARG;
+    return csr_build(rows, cols, w, w_type, n_edges, n_rows, n_cols, directed, compact, row_ptr, row_cnt, col, val,
+                     nnz, deg_flags, deg, scale, ws, ws_bytes, err, (cudaStream_t)stream);
+}
+
+int gee_degree(const int64_t *row_ptr, const int32_t *col, const double *val, int64_t n, unsigned flags,
+               double *deg, double *scale, int32_t *err, void *stream) {
+    if (!index_ok(n) || !row_ptr || !deg) return GEE_E_ARG;
+    return degree(row_ptr, col, val, n, flags, deg, scale, err, (cudaStream_t)stream);
+}
+
+int gee_add_identity_workspace(int64_t n, size_t *ws_bytes) {
+    if (!ws_bytes || !index_ok(n)) return GEE_E_ARG;
+    *ws_bytes = add_identity_workspace(n);
+    return GEE_OK;
+}
+
+int gee_add_identity(const int64_t *row_ptr, const int32_t *col, const double *val, int64_t n,
+                     int64_t *out_row_ptr, int32_t *out_col, double *out_val, int64_t *nnz_out, void *ws,
+                     size_t ws_bytes, void *stream) {
+    if (!index_ok(n) || !row_ptr || !out_row_ptr) return GEE_E_ARG;
+    return add_identity(row_ptr, col, val, n, out_row_ptr, out_col, out_val, nnz_out, ws, ws_bytes,
+                        (cudaStream_t)stream);
+}
+
+int gee_laplacian_normalize_workspace(int64_t n, size_t *ws_bytes) {
+    if (!ws_bytes || !index_ok(n)) return GEE_E_ARG;
+    *ws_bytes = laplacian_workspace(n);
+    return GEE_OK;
+}
+
+int gee_laplacian_normalize(const int64_t *row_ptr, const int32_t *col, const double *val, int64_t n,
+                            const double *deg, int64_t *out_row_ptr, int32_t *out_col, double *out_val,
+                            int64_t *nnz_out, void *ws, size_t ws_bytes, int32_t *err, void *stream) {
+    if (!index_ok(n) || !row_ptr || !deg || !out_row_ptr) return GEE_E_ARG;
+    return laplacian_normalize(row_ptr, col, val, n, deg, out_row_ptr, out_col, out_val, nnz_out, ws, ws_bytes,
+                               err, (cudaStream_t)stream);
+}
+
+int gee_embed_workspace(int64_t n_rows, size_t *ws_bytes) {
+    if (!ws_bytes || !index_ok(n_rows)) return GEE_E_ARG;
+    *ws_bytes = embed_workspace(n_rows);
+    return GEE_OK;
+}
+
+int gee_embed(const int64_t *row_ptr, const uint32_t *row_cnt, const int32_t *col, const double *val,
+              int64_t row_begin, int64_t row_end, const int32_t *y32, const double *inv_nk, const double *scale,
+              int32_t k, unsigned flags, double *z, int64_t ldz, void *ws, size_t ws_bytes, int32_t *err,
+              void *stream) {
+    if (k < 1 || ldz < k || row_begin < 0 || row_end < row_begin || !index_ok(row_end)) return GEE_E_ARG;
+    if (row_end > row_begin && (!row_ptr || !y32 || !inv_nk || !z)) return GEE_E_ARG;
+    if ((flags & GEE_LAPLACIAN) && !scale) return GEE_E_ARG;
+    return embed(row_ptr, row_cnt, col, val, row_begin, row_end, y32, inv_nk, scale, k, flags, z, ldz, ws,
+                 ws_bytes, err, (cudaStream_t)stream);
+}
+
+int gee_encode_edges_workspace(int64_t n_edges, int64_t n_nodes, int32_t k, int directed, size_t *ws_bytes) {
+    if (!ws_bytes || !index_ok(n_edges) || !index_ok(n_nodes) || k < 1) return GEE_E_ARG;
+    Carver cv(nullptr);
+    EncodeWs w;
+    *ws_bytes = carve_encode(cv, w, n_edges, n_nodes, k, directed);
+    return GEE_OK;
+}
+
+int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, int w_type, int64_t n_edges,
+                     int64_t n_nodes, int directed, const int64_t *labels, int32_t k, unsigned flags, double *z,
+                     void *ws, size_t ws_bytes, int32_t *err, void *stream) {
+    if (!index_ok(n_edges) || !index_ok(n_nodes) || k < 1 || !wt_ok(w_type, w) || !z) return GEE_E_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    Carver cv(ws);
+    EncodeWs W;
+    size_t need = carve_encode(cv, W, n_edges, n_nodes, k, directed);
+    if (ws_bytes < need || !ws) return GEE_E_WORKSPACE;
+    int rc = label_hist(labels, n_nodes, k, W.y32, W.counts, W.inv, err, st);
+    if (rc) return rc;
+    const unsigned deg_flags = (flags & GEE_LAPLACIAN) ? (GEE_LAPLACIAN | (flags & GEE_DIAGONAL)) : 0u;
+    rc = csr_build(rows, cols, w, w_type, n_edges, n_nodes, n_nodes, directed, 0, W.row_ptr, W.row_cnt, W.col,
+                   W.val, nullptr, deg_flags, W.deg, W.scale, W.csr_ws, W.csr_bytes, err, st);
+    if (rc) return rc;
+    return embed(W.row_ptr, W.row_cnt, W.col, W.val, 0, n_nodes, W.y32, W.inv,
+                 (flags & GEE_LAPLACIAN) ? W.scale : nullptr, k, flags, z, k, W.emb_ws, W.emb_bytes, err, st);
+}
+
+}  // extern "C"

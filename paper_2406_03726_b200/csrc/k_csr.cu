@@ -1,0 +1,841 @@
+// k_csr.cu -- K2: edge list -> CSR with the reference's exact structure, and
+// the fused K3 degree of A / A+I for the rows it assembles.
+//
+// Reference semantics (bitwise):
+//   * EdgeList.to_csr (graph_io.py:78-92): undirected lists become the stream
+//     [originals..., reversed off-diagonals...]; self-loops contribute once.
+//   * _coo_to_csr_loops (_kernels.py:73-130): stable by (row, col); duplicate
+//     runs summed LEFT TO RIGHT IN STREAM ORDER; sums equal to 0.0 dropped.
+//   * degree_vector (sparse.py:193-196): per-row left fold in column order,
+//     of A or of add_identity(A) (_kernels.py:169-198, diagonal merged as one
+//     v+1.0 term or inserted as 1.0 at its sorted position).
+//
+// B200 design: stream entry e of the symmetrised list is identified by
+// idx = e (original) or E + e (reversed), which orders exactly like the
+// reference's concatenation.  Entries are bucketed by row (count -> scan ->
+// scatter, shared-memory privatised when the row count is small), then every
+// row is ordered on chip by the 64-bit key (col << 32 | idx):
+//   tier S  L <= 32            warp rank-sort in registers
+//   tier D  small n_cols       CTA counting sort over the column range in
+//                              shared memory (rows of ~1K entries, cfg 0/1)
+//   tier B  L <= kCap          CTA bitonic sort in shared memory
+//   tier X  L >  kCap          CTA stable LSD radix over the column bits in
+//                              global memory (hub rows of power-law graphs)
+// Tiers D and X sort by column only; equal-column runs of length >= 3 are then
+// put back into idx order (a run of 2 sums commutatively, so order is moot).
+// One persistent kernel drains the tiers longest-first.
+#include "gee_common.cuh"
+
+namespace gee {
+
+int exclusive_scan_u32(const unsigned *in, int64_t n, int64_t *out, void *ws, cudaStream_t st);
+size_t scan_workspace(int64_t n);
+
+constexpr int kRowsThreads = 512;
+constexpr int kCap = 4096;           // entries staged in shared memory per row
+constexpr int kSmallRows = 16384;    // privatised row histogram (64 KB)
+constexpr int kSmallCols = 12288;    // dense per-row column counting (48 KB)
+constexpr int kSChunk = 64;          // tier-S rows per work grab
+
+enum { TIER_D = 0, TIER_B = 1, TIER_X = 2 };
+
+__device__ __forceinline__ double load_w(const void *w, int wt, int64_t e) {
+    if (wt == GEE_W_F64) return static_cast<const double *>(w)[e];
+    if (wt == GEE_W_F32) return (double)static_cast<const float *>(w)[e];
+    return 1.0;
+}
+
+// ---------------------------------------------------------------------------
+// Pass 1: per-row counts of the symmetrised stream.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void warp_agg_add(unsigned *ctr, unsigned key, bool valid) {
+    unsigned k = valid ? key : 0xffffffffu;
+    unsigned peers = __match_any_sync(0xffffffffu, k);
+    if (valid && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&ctr[key], __popc(peers));
+}
+
+// returns this lane's slot from a warp-aggregated atomicAdd on ctr[key]
+__device__ __forceinline__ unsigned warp_agg_take(unsigned *ctr, unsigned key, bool valid) {
+    unsigned k = valid ? key : 0xffffffffu;
+    unsigned peers = __match_any_sync(0xffffffffu, k);
+    int leader = __ffs(peers) - 1;
+    unsigned base = 0;
+    if (valid && (int)(threadIdx.x & 31) == leader) base = atomicAdd(&ctr[key], __popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    return base + __popc(peers & lanemask_lt());
+}
+
+__global__ void k_count_global(const int64_t *__restrict__ rows, const int64_t *__restrict__ cols,
+                               int64_t E, int directed, unsigned *__restrict__ cnt) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t e_round = (E + 31) & ~int64_t(31);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e_round; e += stride) {
+        bool v = e < E;
+        unsigned r = v ? (unsigned)rows[e] : 0u, c = v ? (unsigned)cols[e] : 0u;
+        warp_agg_add(cnt, r, v);
+        warp_agg_add(cnt, c, v && !directed && r != c);
+    }
+}
+
+__device__ __forceinline__ void chunk_of(int64_t E, int64_t &e0, int64_t &e1) {
+    e0 = (int64_t)((__int128)E * blockIdx.x / gridDim.x);
+    e1 = (int64_t)((__int128)E * (blockIdx.x + 1) / gridDim.x);
+}
+
+// small row count: CTA-private histogram of its contiguous edge chunk
+__global__ void k_count_part(const int64_t *__restrict__ rows, const int64_t *__restrict__ cols,
+                             int64_t E, int directed, int n_rows, unsigned *__restrict__ part) {
+    extern __shared__ unsigned sh[];
+    for (int r = threadIdx.x; r < n_rows; r += blockDim.x) sh[r] = 0;
+    __syncthreads();
+    int64_t e0, e1;
+    chunk_of(E, e0, e1);
+    for (int64_t b = e0; b < e1; b += blockDim.x) {
+        int64_t e = b + threadIdx.x;
+        bool v = e < e1;
+        unsigned r = v ? (unsigned)rows[e] : 0u, c = v ? (unsigned)cols[e] : 0u;
+        warp_agg_add(sh, r, v);
+        warp_agg_add(sh, c, v && !directed && r != c);
+    }
+    __syncthreads();
+    unsigned *dst = part + (size_t)blockIdx.x * n_rows;
+    for (int r = threadIdx.x; r < n_rows; r += blockDim.x) dst[r] = sh[r];
+}
+
+// part[g][r] -> exclusive prefix over g; cnt[r] = total
+__global__ void k_part_reduce(unsigned *__restrict__ part, int G, int n_rows,
+                              unsigned *__restrict__ cnt) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_rows) return;
+    unsigned run = 0;
+    for (int g = 0; g < G; ++g) {
+        unsigned x = part[(size_t)g * n_rows + r];
+        part[(size_t)g * n_rows + r] = run;
+        run += x;
+    }
+    cnt[r] = run;
+}
+
+// ---------------------------------------------------------------------------
+// Pass 2: scatter (key = col<<32 | idx, value = weight) into row buckets.
+// ---------------------------------------------------------------------------
+__global__ void k_scatter_global(const int64_t *__restrict__ rows, const int64_t *__restrict__ cols,
+                                 const void *__restrict__ w, int wt, int64_t E, int directed,
+                                 const int64_t *__restrict__ slot_ptr, unsigned *__restrict__ cursor,
+                                 unsigned long long *__restrict__ key, double *__restrict__ val) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t e_round = (E + 31) & ~int64_t(31);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e_round; e += stride) {
+        bool v = e < E;
+        unsigned r = 0, c = 0;
+        double wv = 0.0;
+        if (v) {
+            r = (unsigned)rows[e];
+            c = (unsigned)cols[e];
+            wv = load_w(w, wt, e);
+        }
+        unsigned s1 = warp_agg_take(cursor, r, v);
+        if (v) {
+            int64_t p = slot_ptr[r] + s1;
+            key[p] = ((unsigned long long)c << 32) | (unsigned long long)e;
+            val[p] = wv;
+        }
+        bool v2 = v && !directed && r != c;
+        unsigned s2 = warp_agg_take(cursor, c, v2);
+        if (v2) {
+            int64_t p = slot_ptr[c] + s2;
+            key[p] = ((unsigned long long)r << 32) | (unsigned long long)(E + e);
+            val[p] = wv;
+        }
+    }
+}
+
+__global__ void k_scatter_part(const int64_t *__restrict__ rows, const int64_t *__restrict__ cols,
+                               const void *__restrict__ w, int wt, int64_t E, int directed,
+                               int n_rows, const int64_t *__restrict__ slot_ptr,
+                               const unsigned *__restrict__ part,
+                               unsigned long long *__restrict__ key, double *__restrict__ val) {
+    extern __shared__ unsigned cur[];
+    const unsigned *off = part + (size_t)blockIdx.x * n_rows;
+    for (int r = threadIdx.x; r < n_rows; r += blockDim.x)
+        cur[r] = (unsigned)(slot_ptr[r] + off[r]);
+    __syncthreads();
+    int64_t e0, e1;
+    chunk_of(E, e0, e1);
+    for (int64_t b = e0; b < e1; b += blockDim.x) {
+        int64_t e = b + threadIdx.x;
+        bool v = e < e1;
+        unsigned r = 0, c = 0;
+        double wv = 0.0;
+        if (v) {
+            r = (unsigned)rows[e];
+            c = (unsigned)cols[e];
+            wv = load_w(w, wt, e);
+        }
+        unsigned p1 = warp_agg_take(cur, r, v);
+        if (v) {
+            key[p1] = ((unsigned long long)c << 32) | (unsigned long long)e;
+            val[p1] = wv;
+        }
+        bool v2 = v && !directed && r != c;
+        unsigned p2 = warp_agg_take(cur, c, v2);
+        if (v2) {
+            key[p2] = ((unsigned long long)r << 32) | (unsigned long long)(E + e);
+            val[p2] = wv;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Row classification into work lists (tier S is implicit: every row <= 32).
+// ---------------------------------------------------------------------------
+__global__ void k_classify(const int64_t *__restrict__ slot_ptr, int64_t n_rows, int dense_ok,
+                           int64_t n_cols, unsigned *__restrict__ lists, unsigned *__restrict__ nlist) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_round = (n_rows + 31) & ~int64_t(31);
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_round; r += stride) {
+        int tier = -1;
+        if (r < n_rows) {
+            int64_t L = slot_ptr[r + 1] - slot_ptr[r];
+            if (L > 32) {
+                if (dense_ok && (L * 16 >= n_cols || L > kCap))
+                    tier = TIER_D;
+                else if (L <= kCap)
+                    tier = TIER_B;
+                else
+                    tier = TIER_X;
+            }
+        }
+        unsigned k = tier >= 0 ? (unsigned)tier : 0xffffffffu;
+        unsigned peers = __match_any_sync(0xffffffffu, k);
+        int leader = __ffs(peers) - 1;
+        unsigned base = 0;
+        if (tier >= 0 && (int)(threadIdx.x & 31) == leader) base = atomicAdd(&nlist[tier], __popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (tier >= 0)
+            lists[(size_t)tier * n_rows + base + __popc(peers & lanemask_lt())] = (unsigned)r;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Row assembly (persistent kernel).
+// ---------------------------------------------------------------------------
+struct RowsArgs {
+    const int64_t *slot_ptr;
+    int64_t n_rows, n_cols;
+    int colbits;
+    unsigned long long *key;  // scattered buckets (input)
+    double *val;
+    unsigned long long *key2;  // global staging / LSD ping-pong
+    double *val2;
+    int32_t *out_col;  // unique entries at slot positions
+    double *out_val;
+    unsigned *ucnt;
+    const unsigned *lists;  // [3][n_rows]
+    const unsigned *nlist;  // [3]
+    unsigned *work;         // [4] work counters
+    unsigned deg_flags;
+    double *deg;
+    double *scale;
+    int32_t *err;
+    int dense_ok;
+};
+
+struct RowsShared {
+    unsigned ured[33];
+    double dred[33];
+    int ired[33];
+    int task;
+};
+
+__device__ __forceinline__ void store_degree(const RowsArgs &a, int64_t r, double d) {
+    a.deg[r] = d;
+    if (a.scale) a.scale[r] = laplacian_scale(d, a.err);
+}
+
+// Finish a row whose L entries sit sorted by column in (sk, sv); when
+// `fixup`, equal-column runs are still in arbitrary idx order.  Sums runs in
+// stream order, drops zeros, writes the unique entries at the row's slot
+// start, and folds the degree.  Whole CTA.
+__device__ void finish_row(const RowsArgs &a, RowsShared &sm, int64_t r, int64_t s0, int L,
+                           unsigned long long *sk, double *sv, bool fixup) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int per = (L + nt - 1) / nt;
+    const int p0 = min(L, tid * per), p1 = min(L, p0 + per);
+    unsigned nkeep = 0;
+    for (int p = p0; p < p1; ++p) {
+        unsigned c = (unsigned)(sk[p] >> 32);
+        if (p > 0 && (unsigned)(sk[p - 1] >> 32) == c) continue;
+        int q = p + 1;
+        while (q < L && (unsigned)(sk[q] >> 32) == c) ++q;
+        if (fixup && q - p >= 3) {
+            // insertion sort of the run by idx (runs are short)
+            for (int i = p + 1; i < q; ++i) {
+                unsigned long long kk = sk[i];
+                double vv = sv[i];
+                int j = i - 1;
+                while (j >= p && sk[j] > kk) {
+                    sk[j + 1] = sk[j];
+                    sv[j + 1] = sv[j];
+                    --j;
+                }
+                sk[j + 1] = kk;
+                sv[j + 1] = vv;
+            }
+        }
+        double acc = sv[p];
+        for (int i = p + 1; i < q; ++i) acc += sv[i];
+        sv[p] = acc;
+        nkeep += acc != 0.0;
+    }
+    __syncthreads();
+    unsigned total;
+    unsigned off = block_exclusive_scan(nkeep, sm.ured, &total);
+    const bool want_deg = a.deg_flags != 0;
+    const bool diag = (a.deg_flags & GEE_DIAGONAL) != 0;
+    Cert cert;
+    double psum = 0.0;
+    int placed = 0;
+    for (int p = p0; p < p1; ++p) {
+        unsigned c = (unsigned)(sk[p] >> 32);
+        if (p > 0 && (unsigned)(sk[p - 1] >> 32) == c) continue;
+        double acc = sv[p];
+        if (acc == 0.0) continue;
+        a.out_col[s0 + off] = (int32_t)c;
+        a.out_val[s0 + off] = acc;
+        ++off;
+        if (want_deg) {
+            double x = acc;
+            if (diag && (int64_t)c == r) {
+                x = acc + 1.0;
+                placed = 1;
+            }
+            cert.add(x);
+            psum += x;
+        }
+    }
+    if (tid == 0) a.ucnt[r] = total;
+    if (!want_deg) return;
+    placed = __syncthreads_or(placed);
+    const bool insert = diag && !placed;
+    int mlow = block_min(cert.mlow, sm.ired);
+    double sabs = block_sum(cert.sabs, sm.dred) + (insert ? 1.0 : 0.0);
+    if (insert) mlow = min(mlow, 0);
+    if (cert_ok(mlow, sabs)) {
+        double d = block_sum(psum, sm.dred) + (insert ? 1.0 : 0.0);
+        if (tid == 0) store_degree(a, r, d);
+    } else {
+        __syncthreads();  // out_* writes of the CTA visible to thread 0
+        if (tid == 0) {
+            double d = 0.0;
+            bool ins = !insert;
+            for (unsigned i = 0; i < total; ++i) {
+                int64_t c = a.out_col[s0 + i];
+                double x = a.out_val[s0 + i];
+                if (!ins && c > r) {
+                    d += 1.0;
+                    ins = true;
+                }
+                if (diag && c == r) x = x + 1.0;
+                d += x;
+            }
+            if (!ins) d += 1.0;
+            store_degree(a, r, d);
+        }
+    }
+    __syncthreads();
+}
+
+// tier D: counting sort over the (small) column range; cnt in shared memory
+__device__ void row_dense(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned *cnt,
+                          unsigned long long *stk, double *stv) {
+    const int64_t s0 = a.slot_ptr[r];
+    const int L = (int)(a.slot_ptr[r + 1] - s0);
+    const int nc = (int)a.n_cols;
+    const unsigned long long *key = a.key + s0;
+    const double *val = a.val + s0;
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) cnt[c] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < L; i += blockDim.x) atomicAdd(&cnt[(unsigned)(key[i] >> 32)], 1u);
+    __syncthreads();
+    {
+        const int per = (nc + blockDim.x - 1) / blockDim.x;
+        const int c0 = min(nc, (int)threadIdx.x * per), c1 = min(nc, c0 + per);
+        unsigned s = 0;
+        for (int c = c0; c < c1; ++c) s += cnt[c];
+        unsigned run = block_exclusive_scan(s, sm.ured, nullptr);
+        for (int c = c0; c < c1; ++c) {
+            unsigned x = cnt[c];
+            cnt[c] = run;
+            run += x;
+        }
+    }
+    __syncthreads();
+    unsigned long long *sk = L <= kCap ? stk : a.key2 + s0;
+    double *sv = L <= kCap ? stv : a.val2 + s0;
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        unsigned long long k = key[i];
+        unsigned p = atomicAdd(&cnt[(unsigned)(k >> 32)], 1u);
+        sk[p] = k;
+        sv[p] = val[i];
+    }
+    __syncthreads();
+    finish_row(a, sm, r, s0, L, sk, sv, true);
+}
+
+// tier B: bitonic sort of (key, value) pairs padded to a power of two
+__device__ void row_bitonic(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned long long *sk,
+                            double *sv) {
+    const int64_t s0 = a.slot_ptr[r];
+    const int L = (int)(a.slot_ptr[r + 1] - s0);
+    int P = 64;
+    while (P < L) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        if (i < L) {
+            sk[i] = a.key[s0 + i];
+            sv[i] = a.val[s0 + i];
+        } else {
+            sk[i] = ~0ull;
+            sv[i] = 0.0;
+        }
+    }
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                int ixj = i ^ j;
+                if (ixj > i) {
+                    unsigned long long x = sk[i], y = sk[ixj];
+                    bool asc = (i & k) == 0;
+                    if ((x > y) == asc) {
+                        sk[i] = y;
+                        sk[ixj] = x;
+                        double t = sv[i];
+                        sv[i] = sv[ixj];
+                        sv[ixj] = t;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    finish_row(a, sm, r, s0, L, sk, sv, false);
+}
+
+// tier X: stable LSD radix (8-bit digits) over the column bits, one CTA per
+// row, ping-ponging between the bucket and the staging arrays.
+__device__ void row_lsd(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned *hist) {
+    const int64_t s0 = a.slot_ptr[r];
+    const int L = (int)(a.slot_ptr[r + 1] - s0);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int chunk = (L + nw - 1) / nw;
+    const int a0 = min(L, wid * chunk), a1 = min(L, a0 + chunk);
+    unsigned long long *src = a.key + s0, *dst = a.key2 + s0;
+    double *srcv = a.val + s0, *dstv = a.val2 + s0;
+    const int passes = (a.colbits + 7) / 8;
+    for (int pass = 0; pass < passes; ++pass) {
+        const int shift = 32 + 8 * pass;
+        unsigned *h = hist + wid * 256;
+        for (int d = lane; d < 256; d += 32) h[d] = 0;
+        __syncthreads();
+        for (int i = a0 + lane; i < a1; i += 32) atomicAdd(&h[(unsigned)(src[i] >> shift) & 255u], 1u);
+        __syncthreads();
+        unsigned tot = 0;
+        if (threadIdx.x < 256) {
+            for (int w = 0; w < nw; ++w) {
+                unsigned x = hist[w * 256 + threadIdx.x];
+                hist[w * 256 + threadIdx.x] = tot;
+                tot += x;
+            }
+        }
+        unsigned base = block_exclusive_scan(threadIdx.x < 256 ? tot : 0u, sm.ured, nullptr);
+        if (threadIdx.x < 256)
+            for (int w = 0; w < nw; ++w) hist[w * 256 + threadIdx.x] += base;
+        __syncthreads();
+        for (int b = a0; b < a1; b += 32) {
+            int i = b + lane;
+            bool v = i < a1;
+            unsigned long long k = v ? src[i] : 0ull;
+            double x = v ? srcv[i] : 0.0;
+            unsigned d = v ? ((unsigned)(k >> shift) & 255u) : 256u + lane;
+            unsigned peers = __match_any_sync(0xffffffffu, d);
+            unsigned pos = v ? h[d] + __popc(peers & lanemask_lt()) : 0u;
+            __syncwarp();
+            if (v) {
+                dst[pos] = k;
+                dstv[pos] = x;
+                if (lane == __ffs(peers) - 1) h[d] += __popc(peers);
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        unsigned long long *t = src;
+        src = dst;
+        dst = t;
+        double *tv = srcv;
+        srcv = dstv;
+        dstv = tv;
+    }
+    finish_row(a, sm, r, s0, L, src, srcv, true);
+}
+
+// tier S: one warp per row of <= 32 entries; rank sort by the full key
+__device__ void row_small(const RowsArgs &a, int64_t r, unsigned long long *wk, double *wv) {
+    const int lane = threadIdx.x & 31;
+    const int64_t s0 = a.slot_ptr[r];
+    const int L = (int)(a.slot_ptr[r + 1] - s0);
+    unsigned long long k = ~0ull;
+    double v = 0.0;
+    if (lane < L) {
+        k = a.key[s0 + lane];
+        v = a.val[s0 + lane];
+    }
+    int rank = 0;
+    for (int j = 0; j < L; ++j) rank += __shfl_sync(0xffffffffu, k, j) < k;
+    if (lane < L) {
+        wk[rank] = k;
+        wv[rank] = v;
+    }
+    __syncwarp();
+    unsigned col = 0xffffffffu;
+    double x = 0.0;
+    if (lane < L) {
+        col = (unsigned)(wk[lane] >> 32);
+        x = wv[lane];
+    }
+    unsigned prev = __shfl_up_sync(0xffffffffu, col, 1);
+    bool head = lane < L && (lane == 0 || prev != col);
+    double acc = 0.0;
+    if (head) {
+        acc = x;
+        for (int j = lane + 1; j < L && (unsigned)(wk[j] >> 32) == col; ++j) acc += wv[j];
+    }
+    bool keep = head && acc != 0.0;
+    unsigned km = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+        int pos = __popc(km & lanemask_lt());
+        a.out_col[s0 + pos] = (int32_t)col;
+        a.out_val[s0 + pos] = acc;
+    }
+    if (lane == 0) a.ucnt[r] = __popc(km);
+    if (a.deg_flags) {
+        const bool diag = (a.deg_flags & GEE_DIAGONAL) != 0;
+        double xm = 0.0;
+        bool isd = false;
+        if (keep) {
+            xm = acc;
+            if (diag && (int64_t)col == r) {
+                xm = acc + 1.0;
+                isd = true;
+            }
+        }
+        const bool insert = diag && !__any_sync(0xffffffffu, isd);
+        Cert ce;
+        ce.add(xm);
+        int mlow = warp_min(ce.mlow);
+        double sabs = warp_sum(ce.sabs) + (insert ? 1.0 : 0.0);
+        if (insert) mlow = min(mlow, 0);
+        double d;
+        if (cert_ok(mlow, sabs)) {
+            d = warp_sum(xm) + (insert ? 1.0 : 0.0);
+        } else {
+            d = 0.0;
+            bool ins = !insert;
+            unsigned mm = km;
+            while (mm) {
+                int j = __ffs(mm) - 1;
+                mm &= mm - 1;
+                int64_t cj = (unsigned)__shfl_sync(0xffffffffu, col, j);
+                double xj = __shfl_sync(0xffffffffu, xm, j);
+                if (!ins && cj > r) {
+                    d += 1.0;
+                    ins = true;
+                }
+                d += xj;
+            }
+            if (!ins) d += 1.0;
+        }
+        if (lane == 0) store_degree(a, r, d);
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(kRowsThreads, 2) k_rows(RowsArgs a) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ RowsShared sm;
+    unsigned long long *stk = reinterpret_cast<unsigned long long *>(dsm);
+    double *stv = reinterpret_cast<double *>(dsm + sizeof(unsigned long long) * kCap);
+    unsigned *region2 = reinterpret_cast<unsigned *>(dsm + 16 * kCap);
+    const int n_x = (int)a.nlist[TIER_X], n_d = (int)a.nlist[TIER_D], n_b = (int)a.nlist[TIER_B];
+    const unsigned *lx = a.lists + (size_t)TIER_X * a.n_rows;
+    const unsigned *ld = a.lists + (size_t)TIER_D * a.n_rows;
+    const unsigned *lb = a.lists + (size_t)TIER_B * a.n_rows;
+    // phase X: hub rows first (longest critical path)
+    for (;;) {
+        if (threadIdx.x == 0) sm.task = (int)atomicAdd(&a.work[0], 1u);
+        __syncthreads();
+        int t = sm.task;
+        __syncthreads();
+        if (t >= n_x) break;
+        row_lsd(a, sm, lx[t], region2);
+    }
+    for (;;) {
+        if (threadIdx.x == 0) sm.task = (int)atomicAdd(&a.work[1], 1u);
+        __syncthreads();
+        int t = sm.task;
+        __syncthreads();
+        if (t >= n_d) break;
+        row_dense(a, sm, ld[t], region2, stk, stv);
+    }
+    for (;;) {
+        if (threadIdx.x == 0) sm.task = (int)atomicAdd(&a.work[2], 1u);
+        __syncthreads();
+        int t = sm.task;
+        __syncthreads();
+        if (t >= n_b) break;
+        row_bitonic(a, sm, lb[t], stk, stv);
+    }
+    // phase S: chunks of rows, one warp per row, rows > 32 skipped
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned long long *wk = stk + wid * 32;
+    double *wv = stv + wid * 32;
+    const int64_t n_chunks = (a.n_rows + kSChunk - 1) / kSChunk;
+    for (;;) {
+        if (threadIdx.x == 0) sm.task = (int)atomicAdd(&a.work[3], 1u);
+        __syncthreads();
+        int64_t t = sm.task;
+        __syncthreads();
+        if (t >= n_chunks) break;
+        const int64_t r0 = t * kSChunk, r1 = min(a.n_rows, r0 + kSChunk);
+        for (int64_t r = r0 + wid; r < r1; r += nw) {
+            int64_t L = a.slot_ptr[r + 1] - a.slot_ptr[r];
+            if (L > 32) continue;
+            if (L == 0) {
+                if (lane == 0) {
+                    a.ucnt[r] = 0;
+                    if (a.deg_flags) store_degree(a, r, (a.deg_flags & GEE_DIAGONAL) ? 1.0 : 0.0);
+                }
+                continue;
+            }
+            row_small(a, r, wk, wv);
+        }
+    }
+    (void)lane;
+}
+
+// ---------------------------------------------------------------------------
+// Optional compaction into a standard CSR (to_csr() callers).
+// ---------------------------------------------------------------------------
+__global__ void k_compact(const int64_t *__restrict__ slot_ptr, const unsigned *__restrict__ ucnt,
+                          const int64_t *__restrict__ row_ptr, int64_t n_rows,
+                          const int32_t *__restrict__ in_col, const double *__restrict__ in_val,
+                          int32_t *__restrict__ out_col, double *__restrict__ out_val) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < n_rows; r += nwarps) {
+        int64_t s = slot_ptr[r], d = row_ptr[r];
+        unsigned u = ucnt[r];
+        for (unsigned i = lane; i < u; i += 32) {
+            out_col[d + i] = in_col[s + i];
+            out_val[d + i] = in_val[s + i];
+        }
+    }
+}
+
+__global__ void k_copy_back(const int64_t *__restrict__ nnz, const int32_t *__restrict__ in_col,
+                            const double *__restrict__ in_val, int32_t *__restrict__ out_col,
+                            double *__restrict__ out_val) {
+    const int64_t n = *nnz;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        out_col[i] = in_col[i];
+        out_val[i] = in_val[i];
+    }
+}
+
+__global__ void k_copy_i64(const int64_t *__restrict__ in, int64_t n, int64_t *__restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = in[i];
+}
+
+// ---------------------------------------------------------------------------
+// Host orchestration.
+// ---------------------------------------------------------------------------
+struct CsrWs {
+    unsigned *cnt;
+    int64_t *slot_ptr;
+    int64_t *tmp_ptr;
+    unsigned *part;
+    unsigned *lists;
+    unsigned *nlist;  // [3] + work[4]
+    unsigned *ucnt;
+    unsigned long long *key, *key2;
+    double *val, *val2;
+    void *scan_ws;
+    int G;
+};
+
+static int partition_ctas() { return 2 * num_sms(); }
+
+static size_t carve_csr(Carver &cv, CsrWs &w, int64_t E, int64_t n_rows, int directed) {
+    const int64_t M = directed ? E : 2 * E;
+    const int64_t Mc = M > 0 ? M : 1;
+    w.G = partition_ctas();
+    w.cnt = cv.take<unsigned>((size_t)n_rows + 1);
+    w.slot_ptr = cv.take<int64_t>((size_t)n_rows + 1);
+    w.tmp_ptr = cv.take<int64_t>((size_t)n_rows + 1);
+    w.part = n_rows <= kSmallRows ? cv.take<unsigned>((size_t)w.G * (size_t)(n_rows + 1)) : nullptr;
+    w.lists = cv.take<unsigned>((size_t)3 * (size_t)(n_rows + 1));
+    w.nlist = cv.take<unsigned>(8);
+    w.ucnt = cv.take<unsigned>((size_t)n_rows + 1);
+    w.key = cv.take<unsigned long long>((size_t)Mc);
+    w.val = cv.take<double>((size_t)Mc);
+    w.key2 = cv.take<unsigned long long>((size_t)Mc);
+    w.val2 = cv.take<double>((size_t)Mc);
+    w.scan_ws = cv.take<char>(scan_workspace(n_rows + 1));
+    return cv.bytes();
+}
+
+size_t csr_build_workspace(int64_t E, int64_t n_rows, int directed) {
+    Carver cv(nullptr);
+    CsrWs w;
+    return carve_csr(cv, w, E, n_rows, directed);
+}
+
+static int bit_length(int64_t x) {
+    int b = 0;
+    while (x > 0) {
+        ++b;
+        x >>= 1;
+    }
+    return b;
+}
+
+static size_t rows_smem(int dense_ok, int64_t n_cols) {
+    size_t region2 = 16 * 256 * sizeof(unsigned);  // LSD per-warp histograms
+    if (dense_ok) region2 = region2 > (size_t)n_cols * 4 ? region2 : (size_t)n_cols * 4;
+    return 16 * (size_t)kCap + region2;
+}
+
+int csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, int64_t E,
+              int64_t n_rows, int64_t n_cols, int directed, int compact, int64_t *row_ptr,
+              unsigned *row_cnt, int32_t *col, double *val, int64_t *nnz, unsigned deg_flags,
+              double *deg, double *scale, void *ws, size_t ws_bytes, int32_t *err,
+              cudaStream_t st) {
+    Carver cv(ws);
+    CsrWs W;
+    size_t need = carve_csr(cv, W, E, n_rows, directed);
+    if (ws_bytes < need) return GEE_E_WORKSPACE;
+    const int threads = 512;
+    const bool small_rows = n_rows <= kSmallRows;
+    static bool part_attr = false;
+    if (!part_attr) {
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_count_part, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            kSmallRows * 4));
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_scatter_part, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            kSmallRows * 4));
+        part_attr = true;
+    }
+    GEE_CHECK_CUDA(cudaMemsetAsync(W.nlist, 0, 8 * sizeof(unsigned), st));
+    GEE_CHECK_CUDA(cudaMemsetAsync(W.cnt, 0, sizeof(unsigned) * (size_t)(n_rows + 1), st));
+    // pass 1: counts
+    if (E > 0) {
+        if (small_rows) {
+            size_t smem = sizeof(unsigned) * (size_t)n_rows;
+            k_count_part<<<W.G, threads, smem, st>>>(rows, cols, E, directed, (int)n_rows, W.part);
+            GEE_CHECK_LAUNCH("k_count_part");
+            k_part_reduce<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(W.part, W.G, (int)n_rows,
+                                                                           W.cnt);
+            GEE_CHECK_LAUNCH("k_part_reduce");
+        } else {
+            k_count_global<<<grid_for(E, threads, 4), threads, 0, st>>>(rows, cols, E, directed, W.cnt);
+            GEE_CHECK_LAUNCH("k_count_global");
+        }
+    }
+    int rc = exclusive_scan_u32(W.cnt, n_rows, W.slot_ptr, W.scan_ws, st);
+    if (rc) return rc;
+    // pass 2: scatter into row buckets
+    if (E > 0) {
+        if (small_rows) {
+            size_t smem = sizeof(unsigned) * (size_t)n_rows;
+            k_scatter_part<<<W.G, threads, smem, st>>>(rows, cols, w, wt, E, directed, (int)n_rows,
+                                                       W.slot_ptr, W.part, W.key, W.val);
+            GEE_CHECK_LAUNCH("k_scatter_part");
+        } else {
+            GEE_CHECK_CUDA(cudaMemsetAsync(W.cnt, 0, sizeof(unsigned) * (size_t)(n_rows + 1), st));
+            k_scatter_global<<<grid_for(E, threads, 4), threads, 0, st>>>(
+                rows, cols, w, wt, E, directed, W.slot_ptr, W.cnt, W.key, W.val);
+            GEE_CHECK_LAUNCH("k_scatter_global");
+        }
+    }
+    // classify + assemble rows
+    const int dense_ok = n_cols <= kSmallCols;
+    if (n_rows > 0) {
+        k_classify<<<grid_for(n_rows, 256, 8), 256, 0, st>>>(W.slot_ptr, n_rows, dense_ok, n_cols,
+                                                            W.lists, W.nlist);
+        GEE_CHECK_LAUNCH("k_classify");
+        RowsArgs a;
+        a.slot_ptr = W.slot_ptr;
+        a.n_rows = n_rows;
+        a.n_cols = n_cols;
+        a.colbits = bit_length(n_cols > 1 ? n_cols - 1 : 1);
+        a.key = W.key;
+        a.val = W.val;
+        a.key2 = W.key2;
+        a.val2 = W.val2;
+        a.out_col = col;
+        a.out_val = val;
+        a.ucnt = compact ? W.ucnt : row_cnt;
+        a.lists = W.lists;
+        a.nlist = W.nlist;
+        a.work = W.nlist + 3;
+        a.deg_flags = deg_flags;
+        a.deg = deg;
+        a.scale = (deg_flags & GEE_LAPLACIAN) ? scale : nullptr;
+        a.err = err;
+        a.dense_ok = dense_ok;
+        size_t smem = rows_smem(dense_ok, n_cols);
+        static bool attr_set = false;
+        if (!attr_set) {
+            GEE_CHECK_CUDA(cudaFuncSetAttribute(k_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                16 * kCap + kSmallCols * 4 + 1024));
+            attr_set = true;
+        }
+        k_rows<<<2 * num_sms(), kRowsThreads, smem, st>>>(a);
+        GEE_CHECK_LAUNCH("k_rows");
+    }
+    if (compact) {
+        unsigned *uc = W.ucnt;
+        rc = exclusive_scan_u32(uc, n_rows, row_ptr, W.scan_ws, st);
+        if (rc) return rc;
+        if (row_cnt) GEE_CHECK_CUDA(cudaMemcpyAsync(row_cnt, uc, sizeof(unsigned) * (size_t)n_rows,
+                                                    cudaMemcpyDeviceToDevice, st));
+        int32_t *tcol = reinterpret_cast<int32_t *>(W.key);
+        double *tval = W.val;
+        if (n_rows > 0) {
+            k_compact<<<grid_for(n_rows * 32, 256, 8), 256, 0, st>>>(W.slot_ptr, uc, row_ptr, n_rows,
+                                                                    col, val, tcol, tval);
+            GEE_CHECK_LAUNCH("k_compact");
+            const int64_t M = directed ? E : 2 * E;
+            k_copy_back<<<grid_for(M > 0 ? M : 1, 256, 8), 256, 0, st>>>(row_ptr + n_rows, tcol, tval,
+                                                                        col, val);
+            GEE_CHECK_LAUNCH("k_copy_back");
+        }
+        if (nnz) GEE_CHECK_CUDA(cudaMemcpyAsync(nnz, row_ptr + n_rows, sizeof(int64_t),
+                                                cudaMemcpyDeviceToDevice, st));
+    } else {
+        k_copy_i64<<<grid_for(n_rows + 1, 256, 8), 256, 0, st>>>(W.slot_ptr, n_rows + 1, row_ptr);
+        GEE_CHECK_LAUNCH("k_copy_i64");
+        if (nnz) {
+            // nnz = sum of unique counts
+            rc = exclusive_scan_u32(row_cnt, n_rows, W.tmp_ptr, W.scan_ws, st);
+            if (rc) return rc;
+            GEE_CHECK_CUDA(cudaMemcpyAsync(nnz, W.tmp_ptr + n_rows, sizeof(int64_t),
+                                           cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    return GEE_OK;
+}
+
+}  // namespace gee

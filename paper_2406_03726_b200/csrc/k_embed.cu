@@ -1,0 +1,452 @@
+// k_embed.cu -- K4: Z = A'W with the option transforms fused in.
+//
+// Replaces spmm(A', build_weight_matrix(Y)).to_dense() (sparse.py:166-181,
+// _kernels.py:257-307, sparse.py:87-91) plus add_identity (sparse.py:184-190),
+// laplacian_normalize (sparse.py:199-226) and correlate_rows
+// (embedding.py:134-143).  Per stored entry (r, j, v):
+//     a'  = v (+1.0 when j == r under DIAGONAL; a missing diagonal is a
+//           virtual 1.0 entry)                          _kernels.py:176-196
+//     a'  = (a' * s_r) * s_j under LAPLACIAN            sparse.py:217
+//     Z[r, Y_j] += a' * inv_nk[Y_j]   (Y_j >= 0)        _kernels.py:292-296
+// W is never built: its one nonzero per row is (Y_j, 1/n_{Y_j}).  Each term is
+// the reference's own product; only the summation order differs (fp64,
+// relative error ~1e-15 against the 1e-12 budget).
+//
+// Work split: rows longer than kLongRow are taken first, one CTA per row
+// (per-warp partial K-vectors combined in shared memory); every other row is
+// one warp.  K <= 8 accumulates in registers (predicated adds, no dynamic
+// indexing); larger K accumulates in a per-warp shared K-vector, combining
+// equal-label lanes with __match_any_sync so no shared-memory fp64 atomics
+// (a CAS loop on sm_100a) are ever issued.  K beyond kKTile is tiled, and
+// correlation then rescales the row in a second sweep.
+#include "gee_common.cuh"
+
+namespace gee {
+
+constexpr int kEmbedThreads = 256;
+constexpr int kEmbedWarps = kEmbedThreads / 32;
+constexpr int kLongRow = 4096;
+constexpr int kKTile = 1024;
+constexpr int kRowChunk = 32;  // rows per work grab (4 per warp)
+
+struct EmbedArgs {
+    const int64_t *row_ptr;
+    const unsigned *row_cnt;
+    const int32_t *col;
+    const double *val;
+    int64_t row_begin, row_end;
+    const int32_t *y32;
+    const double *inv;
+    const double *scale;
+    int k;
+    unsigned flags;
+    double *z;
+    int64_t ldz;
+    int32_t *err;
+    const unsigned *long_list;
+    const unsigned *n_long;
+    unsigned *work;  // [2]
+};
+
+__device__ __forceinline__ void row_extent(const EmbedArgs &a, int64_t r, int64_t &s, int64_t &e) {
+    s = a.row_ptr[r];
+    e = a.row_cnt ? s + a.row_cnt[r] : a.row_ptr[r + 1];
+}
+
+// One stored entry -> (label, contribution).  Returns false when it adds
+// nothing (unlabeled column or padding).
+__device__ __forceinline__ bool entry_term(const EmbedArgs &a, int64_t r, double s_r, int64_t p,
+                                           bool valid, int &lab, double &x, bool &isdiag) {
+    lab = -1;
+    x = 0.0;
+    isdiag = false;
+    if (!valid) return false;
+    int c = a.col[p];
+    double v = a.val ? a.val[p] : 1.0;
+    lab = a.y32[c];
+    if ((a.flags & GEE_DIAGONAL) && c == r) {
+        v = v + 1.0;
+        isdiag = true;
+    }
+    if (lab < 0) return false;
+    if (a.flags & GEE_LAPLACIAN) v = (v * s_r) * a.scale[c];
+    x = v * a.inv[lab];
+    return true;
+}
+
+// The virtual diagonal 1.0 of A+I for a row with no stored diagonal.
+__device__ __forceinline__ bool diag_term(const EmbedArgs &a, int64_t r, double s_r, int &lab,
+                                          double &x) {
+    lab = a.y32[r];
+    if (lab < 0) return false;
+    double v = 1.0;
+    if (a.flags & GEE_LAPLACIAN) v = (v * s_r) * s_r;
+    x = v * a.inv[lab];
+    return true;
+}
+
+__device__ __forceinline__ double row_scale(const EmbedArgs &a, int64_t r) {
+    return (a.flags & GEE_LAPLACIAN) ? a.scale[r] : 1.0;
+}
+
+// ---------------------------------------------------------------------------
+// K <= KP <= 8: register accumulators, one warp per row.
+// ---------------------------------------------------------------------------
+template <int KP>
+__device__ void row_regs(const EmbedArgs &a, int64_t r) {
+    const int lane = threadIdx.x & 31;
+    int64_t s, e;
+    row_extent(a, r, s, e);
+    const double s_r = row_scale(a, r);
+    double acc[KP];
+#pragma unroll
+    for (int q = 0; q < KP; ++q) acc[q] = 0.0;
+    bool found = false;
+    for (int64_t p0 = s; p0 < e; p0 += 128) {
+        int lab[4];
+        double x[4];
+        bool ok[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            int64_t p = p0 + u * 32 + lane;
+            bool isd;
+            ok[u] = entry_term(a, r, s_r, p, p < e, lab[u], x[u], isd);
+            found |= isd;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (ok[u]) {
+#pragma unroll
+                for (int q = 0; q < KP; ++q) acc[q] += (lab[u] == q) ? x[u] : 0.0;
+            }
+        }
+    }
+    if (a.flags & GEE_DIAGONAL) {
+        found = __any_sync(0xffffffffu, found);
+        int lb;
+        double xd;
+        if (!found && lane == 0 && diag_term(a, r, s_r, lb, xd)) {
+#pragma unroll
+            for (int q = 0; q < KP; ++q) acc[q] += (lb == q) ? xd : 0.0;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < KP; ++q) acc[q] = warp_sum(acc[q]);
+    if (a.flags & GEE_CORRELATION) {
+        double ss = 0.0;
+        bool fin = true;
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+            if (q < a.k) {
+                ss += acc[q] * acc[q];
+                fin &= isfinite(acc[q]);
+            }
+        }
+        if (!fin) {
+            if (lane == 0) raise_err(a.err, GEE_ERR_NONFINITE);
+        } else {
+            double nrm = __dsqrt_rn(ss);
+            if (nrm > 0.0) {
+#pragma unroll
+                for (int q = 0; q < KP; ++q) acc[q] = __ddiv_rn(acc[q], nrm);
+            }
+        }
+    }
+    double mine = 0.0;
+#pragma unroll
+    for (int q = 0; q < KP; ++q) mine = (lane == q) ? acc[q] : mine;
+    if (lane < a.k) a.z[(r - a.row_begin) * a.ldz + lane] = mine;
+}
+
+// ---------------------------------------------------------------------------
+// General K: per-warp shared K-tile.  Entries of this lane are
+// p = s + lane + 32*j*stride_warps + warp_off*32 (strided so a CTA can split
+// a long row over its warps).
+// ---------------------------------------------------------------------------
+__device__ void accumulate_tile(const EmbedArgs &a, int64_t r, double s_r, int64_t s, int64_t e,
+                                int warp_off, int warp_stride, double *zs, double *xs, int t0,
+                                int kt, bool &found) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t p0 = s + (int64_t)warp_off * 32; p0 < e; p0 += (int64_t)warp_stride * 32) {
+        int64_t p = p0 + lane;
+        int lab;
+        double x;
+        bool isd;
+        bool ok = entry_term(a, r, s_r, p, p < e, lab, x, isd);
+        found |= isd;
+        ok = ok && lab >= t0 && lab < t0 + kt;
+        unsigned key = ok ? (unsigned)lab : 0x80000000u + lane;
+        unsigned peers = __match_any_sync(0xffffffffu, key);
+        xs[lane] = x;
+        __syncwarp();
+        if (ok && lane == __ffs(peers) - 1) {
+            double sum = 0.0;
+            unsigned m = peers;
+            while (m) {
+                int l = __ffs(m) - 1;
+                m &= m - 1;
+                sum += xs[l];
+            }
+            zs[lab - t0] += sum;
+        }
+        __syncwarp();
+    }
+}
+
+// one warp, one row, K > 8
+__device__ void row_smem(const EmbedArgs &a, int64_t r, double *zs, double *xs) {
+    const int lane = threadIdx.x & 31;
+    int64_t s, e;
+    row_extent(a, r, s, e);
+    const double s_r = row_scale(a, r);
+    double *zrow = a.z + (r - a.row_begin) * a.ldz;
+    const bool corr = (a.flags & GEE_CORRELATION) != 0;
+    const int ntiles = (a.k + kKTile - 1) / kKTile;
+    bool found = false;
+    double ss = 0.0;
+    bool fin = true;
+    for (int t = 0; t < ntiles; ++t) {
+        const int t0 = t * kKTile, kt = min(kKTile, a.k - t0);
+        for (int c = lane; c < kt; c += 32) zs[c] = 0.0;
+        __syncwarp();
+        accumulate_tile(a, r, s_r, s, e, 0, 1, zs, xs, t0, kt, found);
+        if (a.flags & GEE_DIAGONAL) {
+            bool f = __any_sync(0xffffffffu, found);
+            int lb;
+            double xd;
+            if (!f && lane == 0 && diag_term(a, r, s_r, lb, xd) && lb >= t0 && lb < t0 + kt)
+                zs[lb - t0] += xd;
+            __syncwarp();
+        }
+        for (int c = lane; c < kt; c += 32) {
+            double v = zs[c];
+            ss += v * v;
+            fin &= isfinite(v);
+        }
+        if (!corr || ntiles > 1) {
+            for (int c = lane; c < kt; c += 32) zrow[t0 + c] = zs[c];
+        }
+        __syncwarp();
+    }
+    if (!corr) return;
+    ss = warp_sum(ss);
+    fin = __all_sync(0xffffffffu, fin);
+    if (!fin) {
+        if (lane == 0) raise_err(a.err, GEE_ERR_NONFINITE);
+        if (ntiles == 1)
+            for (int c = lane; c < a.k; c += 32) zrow[c] = zs[c];
+        return;
+    }
+    const double nrm = __dsqrt_rn(ss);
+    if (ntiles == 1) {
+        for (int c = lane; c < a.k; c += 32) zrow[c] = nrm > 0.0 ? __ddiv_rn(zs[c], nrm) : zs[c];
+    } else if (nrm > 0.0) {
+        for (int c = lane; c < a.k; c += 32) zrow[c] = __ddiv_rn(zrow[c], nrm);
+    }
+    __syncwarp();
+}
+
+// one CTA, one long row (any K): warps accumulate strided slices into their
+// own K-tile, then the tiles are summed.
+__device__ void row_long(const EmbedArgs &a, int64_t r, double *zsm, double *xsm, double *dred,
+                         int *flag) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int kt_max = min(a.k, kKTile);
+    double *zs = zsm + wid * kt_max;
+    double *xs = xsm + wid * 32;
+    int64_t s, e;
+    row_extent(a, r, s, e);
+    const double s_r = row_scale(a, r);
+    double *zrow = a.z + (r - a.row_begin) * a.ldz;
+    const bool corr = (a.flags & GEE_CORRELATION) != 0;
+    const int ntiles = (a.k + kKTile - 1) / kKTile;
+    bool found = false;
+    double ss = 0.0;
+    int fin = 1;
+    for (int t = 0; t < ntiles; ++t) {
+        const int t0 = t * kKTile, kt = min(kKTile, a.k - t0);
+        for (int c = lane; c < kt; c += 32) zs[c] = 0.0;
+        __syncwarp();
+        accumulate_tile(a, r, s_r, s, e, wid, kEmbedWarps, zs, xs, t0, kt, found);
+        int f = __syncthreads_or(found ? 1 : 0);
+        // combine warp tiles into warp 0's tile
+        for (int c = threadIdx.x; c < kt; c += blockDim.x) {
+            double v = 0.0;
+            for (int w = 0; w < kEmbedWarps; ++w) v += zsm[w * kt_max + c];
+            zsm[c] = v;  // reading column c of every warp, writing column c of warp 0
+        }
+        __syncthreads();
+        if ((a.flags & GEE_DIAGONAL) && !f && threadIdx.x == 0) {
+            int lb;
+            double xd;
+            if (diag_term(a, r, s_r, lb, xd) && lb >= t0 && lb < t0 + kt) zsm[lb - t0] += xd;
+        }
+        __syncthreads();
+        for (int c = threadIdx.x; c < kt; c += blockDim.x) {
+            double v = zsm[c];
+            ss += v * v;
+            fin &= isfinite(v) ? 1 : 0;
+            if (!corr || ntiles > 1) zrow[t0 + c] = v;
+        }
+        __syncthreads();
+    }
+    if (!corr) return;
+    ss = block_sum(ss, dred);
+    fin = __syncthreads_and(fin);
+    if (!fin) {
+        if (threadIdx.x == 0) raise_err(a.err, GEE_ERR_NONFINITE);
+        if (ntiles == 1)
+            for (int c = threadIdx.x; c < a.k; c += blockDim.x) zrow[c] = zsm[c];
+        __syncthreads();
+        return;
+    }
+    const double nrm = __dsqrt_rn(ss);
+    if (ntiles == 1) {
+        for (int c = threadIdx.x; c < a.k; c += blockDim.x)
+            zrow[c] = nrm > 0.0 ? __ddiv_rn(zsm[c], nrm) : zsm[c];
+    } else if (nrm > 0.0) {
+        for (int c = threadIdx.x; c < a.k; c += blockDim.x) zrow[c] = __ddiv_rn(zrow[c], nrm);
+    }
+    __syncthreads();
+    (void)flag;
+}
+
+template <int KP>
+__global__ void __launch_bounds__(kEmbedThreads) k_embed(EmbedArgs a) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ double dred[33];
+    __shared__ int task;
+    const int kt_max = min(a.k, kKTile);
+    double *zsm = reinterpret_cast<double *>(dsm);                 // [warps][kt_max]
+    double *xsm = zsm + (size_t)kEmbedWarps * kt_max;               // [warps][32]
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // phase 1: long rows, one CTA each
+    const unsigned n_long = *a.n_long;
+    for (;;) {
+        if (threadIdx.x == 0) task = (int)atomicAdd(&a.work[0], 1u);
+        __syncthreads();
+        int t = task;
+        __syncthreads();
+        if (t >= (int)n_long) break;
+        row_long(a, a.long_list[t], zsm, xsm, dred, nullptr);
+    }
+    // phase 2: chunks of rows, one warp per row
+    const int64_t n_rows = a.row_end - a.row_begin;
+    const int64_t n_chunks = (n_rows + kRowChunk - 1) / kRowChunk;
+    for (;;) {
+        if (threadIdx.x == 0) task = (int)atomicAdd(&a.work[1], 1u);
+        __syncthreads();
+        int64_t t = task;
+        __syncthreads();
+        if (t >= n_chunks) break;
+        const int64_t r0 = a.row_begin + t * kRowChunk;
+        const int64_t r1 = min(a.row_end, r0 + kRowChunk);
+        for (int64_t r = r0 + wid; r < r1; r += kEmbedWarps) {
+            int64_t s, e;
+            row_extent(a, r, s, e);
+            if (e - s > kLongRow) continue;
+            if (KP > 0)
+                row_regs<(KP > 0 ? KP : 1)>(a, r);
+            else
+                row_smem(a, r, zsm + wid * kt_max, xsm + wid * 32);
+        }
+    }
+    (void)lane;
+}
+
+__global__ void k_embed_classify(const int64_t *__restrict__ row_ptr,
+                                 const unsigned *__restrict__ row_cnt, int64_t rb, int64_t re,
+                                 unsigned *__restrict__ list, unsigned *__restrict__ n_list) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n = re - rb;
+    const int64_t n_round = (n + 31) & ~int64_t(31);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
+        bool lng = false;
+        int64_t r = rb + i;
+        if (i < n) {
+            int64_t L = row_cnt ? (int64_t)row_cnt[r] : row_ptr[r + 1] - row_ptr[r];
+            lng = L > kLongRow;
+        }
+        unsigned m = __ballot_sync(0xffffffffu, lng);
+        if (!m) continue;
+        int leader = __ffs(m) - 1;
+        unsigned base = 0;
+        if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(n_list, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (lng) list[base + __popc(m & lanemask_lt())] = (unsigned)r;
+    }
+}
+
+size_t embed_workspace(int64_t n_rows) {
+    Carver cv(nullptr);
+    cv.take<unsigned>(4);
+    cv.take<unsigned>((size_t)n_rows + 1);
+    return cv.bytes();
+}
+
+int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, const double *val,
+          int64_t rb, int64_t re, const int32_t *y32, const double *inv, const double *scale, int k,
+          unsigned flags, double *z, int64_t ldz, void *ws, size_t ws_bytes, int32_t *err,
+          cudaStream_t st) {
+    const int64_t n = re - rb;
+    Carver cv(ws);
+    unsigned *ctr = cv.take<unsigned>(4);
+    unsigned *list = cv.take<unsigned>((size_t)n + 1);
+    if (ws_bytes < cv.bytes()) return GEE_E_WORKSPACE;
+    if (n <= 0) return GEE_OK;
+    GEE_CHECK_CUDA(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned), st));
+    k_embed_classify<<<grid_for(n, 256, 8), 256, 0, st>>>(row_ptr, row_cnt, rb, re, list, ctr);
+    GEE_CHECK_LAUNCH("k_embed_classify");
+    EmbedArgs a;
+    a.row_ptr = row_ptr;
+    a.row_cnt = row_cnt;
+    a.col = col;
+    a.val = val;
+    a.row_begin = rb;
+    a.row_end = re;
+    a.y32 = y32;
+    a.inv = inv;
+    a.scale = scale;
+    a.k = k;
+    a.flags = flags;
+    a.z = z;
+    a.ldz = ldz;
+    a.err = err;
+    a.long_list = list;
+    a.n_long = ctr;
+    a.work = ctr + 1;
+    const int kt_max = k < kKTile ? k : kKTile;
+    size_t smem = sizeof(double) * (size_t)kEmbedWarps * ((size_t)kt_max + 32);
+    static bool attr = false;
+    if (!attr) {
+        size_t mx = sizeof(double) * (size_t)kEmbedWarps * ((size_t)kKTile + 32);
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
+        attr = true;
+    }
+    int occ = 0;
+    const unsigned grid_cap = (unsigned)num_sms() * 8;
+    unsigned grid;
+#define GEE_LAUNCH_EMBED(KP)                                                                  \
+    do {                                                                                      \
+        GEE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_embed<KP>,       \
+                                                                     kEmbedThreads, smem));   \
+        grid = (unsigned)num_sms() * (unsigned)(occ > 0 ? occ : 1);                           \
+        if (grid > grid_cap) grid = grid_cap;                                                 \
+        k_embed<KP><<<grid, kEmbedThreads, smem, st>>>(a);                                    \
+    } while (0)
+    if (k <= 1)
+        GEE_LAUNCH_EMBED(1);
+    else if (k <= 2)
+        GEE_LAUNCH_EMBED(2);
+    else if (k <= 4)
+        GEE_LAUNCH_EMBED(4);
+    else if (k <= 8)
+        GEE_LAUNCH_EMBED(8);
+    else
+        GEE_LAUNCH_EMBED(0);
+#undef GEE_LAUNCH_EMBED
+    GEE_CHECK_LAUNCH("k_embed");
+    return GEE_OK;
+}
+
+}  // namespace gee

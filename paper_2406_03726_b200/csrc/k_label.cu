@@ -1,0 +1,85 @@
+// k_label.cu -- K1: class histogram n_k and the per-class weight 1/n_k.
+//
+// Replaces LabelVector.class_counts (embedding.py:68-71) and the value
+// column of build_weight_matrix (embedding.py:92-107).  W itself is never
+// materialised: gee_embed reads y32 + inv_nk instead of W's CSR.
+#include "gee_common.cuh"
+
+namespace gee {
+
+constexpr int kHistSmemMax = 8192;  // classes privatised in shared memory
+
+// labels int64 -> int32 (-1 = unlabeled), validated, histogrammed.  Small K:
+// per-CTA shared histogram with warp-aggregated updates (__match_any_sync
+// collapses equal labels so a hot class costs one shared atomic per warp).
+__global__ void k_label_hist(const int64_t *__restrict__ labels, int64_t n, int k,
+                             int32_t *__restrict__ y32, unsigned long long *__restrict__ counts,
+                             int32_t *err) {
+    extern __shared__ unsigned sh_hist[];
+    const bool priv = k <= kHistSmemMax;
+    if (priv)
+        for (int c = threadIdx.x; c < k; c += blockDim.x) sh_hist[c] = 0;
+    __syncthreads();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_round = (n + 31) & ~int64_t(31);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
+        int lab = -1;
+        bool valid = false;
+        if (i < n) {
+            int64_t v = labels[i];
+            if (v < -1 || v >= k) {
+                raise_err(err, GEE_ERR_LABEL);
+                v = -1;
+            }
+            lab = (int)v;
+            y32[i] = lab;
+            valid = lab >= 0;
+        }
+        // every lane of the warp reaches here (n_round is a multiple of 32)
+        unsigned key = valid ? (unsigned)lab : 0xffffffffu;
+        unsigned peers = __match_any_sync(0xffffffffu, key);
+        int leader = __ffs(peers) - 1;
+        if (valid && (threadIdx.x & 31) == leader) {
+            unsigned cnt = __popc(peers);
+            if (priv)
+                atomicAdd(&sh_hist[lab], cnt);
+            else
+                atomicAdd(&counts[lab], (unsigned long long)cnt);
+        }
+    }
+    __syncthreads();
+    if (priv)
+        for (int c = threadIdx.x; c < k; c += blockDim.x)
+            if (sh_hist[c]) atomicAdd(&counts[c], (unsigned long long)sh_hist[c]);
+}
+
+// inv_nk[c] = 1.0 / n_c as build_weight_matrix computes it (f64 division of
+// 1.0 by the count, embedding.py:106); empty classes are never read.
+__global__ void k_inv_counts(const unsigned long long *__restrict__ counts, int k,
+                             double *__restrict__ inv_nk) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < k) {
+        unsigned long long n = counts[c];
+        inv_nk[c] = n ? __ddiv_rn(1.0, (double)n) : 0.0;
+    }
+}
+
+int label_hist(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_t *counts,
+               double *inv_nk, int32_t *err, cudaStream_t st) {
+    GEE_CHECK_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (size_t)k, st));
+    if (n > 0) {
+        const int threads = 512;
+        unsigned grid = grid_for(n, threads, 2);
+        size_t smem = k <= kHistSmemMax ? sizeof(unsigned) * (size_t)k : 0;
+        k_label_hist<<<grid, threads, smem, st>>>(labels, n, k, y32,
+                                                  reinterpret_cast<unsigned long long *>(counts),
+                                                  err);
+        GEE_CHECK_LAUNCH("k_label_hist");
+    }
+    k_inv_counts<<<(k + 255) / 256, 256, 0, st>>>(
+        reinterpret_cast<const unsigned long long *>(counts), k, inv_nk);
+    GEE_CHECK_LAUNCH("k_inv_counts");
+    return GEE_OK;
+}
+
+}  // namespace gee

@@ -1,0 +1,202 @@
+"""encode(): the reference's public entry point, on the B200.
+
+Reference: pkg/src/graphee/embedding.py:110-131 (``encode``), called as
+``encode(EdgeList(...).to_csr(), labels, opts)`` (cli.py:108-109, :176).
+Both call forms are accepted:
+
+* an EdgeList (ours or the reference's)  -> the fused device pipeline
+  gee_encode_edges: K1 label histogram, K2 CSR assembly with the K3 degree
+  fused in, K4 embedding with Laplacian/diagonal in its load path and
+  correlation in its epilogue -- the whole reference timed region;
+* a CsrMatrix (ours, or any object with the reference's CsrMatrix fields)
+  -> gee_degree (if Laplacian) + gee_embed.
+
+Errors follow the reference: StructuralError for shape/label problems
+(embedding.py:115-122), NumericalDomainError for negative degrees
+(sparse.py:211-212) and non-finite rows under correlation
+(embedding.py:137-138).  The result is a float64 (N, K) numpy array (the
+drop-in contract) or, with ``out="torch"``, the device tensor.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _device, _lib
+from .errors import StructuralError
+from .graph import EdgeList, EmbedOptions, LabelVector, options_flags
+from .sparse import CsrMatrix
+
+
+def _labels_of(labels):
+    if isinstance(labels, LabelVector):
+        return labels
+    return LabelVector(labels.labels, labels.k_classes)
+
+
+def _edges_of(edges):
+    if isinstance(edges, EdgeList):
+        return edges
+    return EdgeList(edges.n_nodes, edges.rows, edges.cols, edges.weights, edges.directed,
+                    validate=False)
+
+
+def label_tables(labels, device=None):
+    """K1: (y32 int32[N], counts int64[K], inv_nk float64[K]) on the device."""
+    labels = _labels_of(labels)
+    dev = torch.device(device) if device is not None else _device.require_gpu()
+    lab = _device.to_device(labels.labels, torch.int64, dev)
+    n, k = len(labels), labels.k_classes
+    y32 = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    counts = torch.empty(k, dtype=torch.int64, device=dev)
+    inv = torch.empty(k, dtype=torch.float64, device=dev)
+    err = _device.error_word(dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().gee_label_hist(_device.ptr(lab), n, k, _device.ptr(y32),
+                                              _device.ptr(counts), _device.ptr(inv),
+                                              _device.ptr(err), _device.stream_handle()))
+    _device.check_device_errors(err, "labels")
+    return y32[:n], counts, inv
+
+
+class GeeEncoder:
+    """Reusable plan for repeated edge-list -> Z calls of one shape.
+
+    Holds the workspace, the error word and the output; ``run`` launches the
+    fused pipeline on the current stream without synchronising (check=False)
+    so a caller can time or graph-capture it.
+    """
+
+    def __init__(self, n_nodes: int, n_edges: int, k_classes: int, directed: bool,
+                 opts: EmbedOptions | None = None, device=None):
+        self.dev = torch.device(device) if device is not None else _device.require_gpu()
+        self.n, self.e, self.k = int(n_nodes), int(n_edges), int(k_classes)
+        self.directed = bool(directed)
+        self.flags = options_flags(opts)
+        lib = _lib.load()
+        with torch.cuda.device(self.dev):
+            nb = _lib.size_query(lib.gee_encode_edges_workspace, self.e, self.n, self.k,
+                                 int(self.directed))
+        self.ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=self.dev)
+        self.z = torch.empty((self.n, self.k), dtype=torch.float64, device=self.dev)
+        self.err = _device.error_word(self.dev)
+
+    def run(self, rows, cols, weights, labels, *, check: bool = True, out=None) -> torch.Tensor:
+        """rows/cols int64, weights float64/float32/None, labels int64 -- device tensors."""
+        if weights is None:
+            wt = _lib.W_UNIT
+        else:
+            wt = _lib.W_F32 if weights.dtype == torch.float32 else _lib.W_F64
+        z = self.z if out is None else out
+        if check:
+            self.err.zero_()
+        _lib.check(_lib.load().gee_encode_edges(
+            _device.ptr(rows), _device.ptr(cols), _device.ptr(weights), wt, self.e, self.n,
+            int(self.directed), _device.ptr(labels), self.k, self.flags, _device.ptr(z),
+            _device.ptr(self.ws), self.ws.numel(), _device.ptr(self.err), _device.stream_handle()))
+        if check:
+            _device.check_device_errors(self.err, "encode")
+        return z
+
+    def attach_host(self, rows, cols, weights, labels):
+        """Register host inputs for run_host(): pinned staging copies plus
+        device buffers of the same shapes and a pinned output.  Returns
+        (h2d_bytes, d2h_bytes) per run."""
+        def pin(a):
+            t = torch.from_numpy(np.ascontiguousarray(a)) if isinstance(a, np.ndarray) else a.cpu()
+            return t.pin_memory()
+        self._h = [pin(rows), pin(cols), None if weights is None else pin(weights), pin(labels)]
+        self._d = [None if h is None else torch.empty_like(h, device=self.dev) for h in self._h]
+        self._zh = torch.empty((self.n, self.k), dtype=torch.float64).pin_memory()
+        h2d = sum(h.numel() * h.element_size() for h in self._h if h is not None)
+        return h2d, self._zh.numel() * 8
+
+    def run_host(self, *, check: bool = True) -> torch.Tensor:
+        """Host -> device copies, the fused pipeline, device -> host Z; all
+        stream-ordered on the current stream (the end-to-end call)."""
+        for h, d in zip(self._h, self._d):
+            if h is not None:
+                d.copy_(h, non_blocking=True)
+        rows, cols, w, lab = self._d
+        z = self.run(rows, cols, w, lab, check=False)
+        self._zh.copy_(z, non_blocking=True)
+        if check:
+            torch.cuda.current_stream().synchronize()
+            _device.check_device_errors(self.err, "encode")
+        return self._zh
+
+
+def _check_shapes(n_rows, n_cols, labels):
+    if n_rows != n_cols:
+        raise StructuralError(f"adjacency must be square, got {n_rows}x{n_cols}")
+    if len(labels) != n_rows:
+        raise StructuralError(f"label count {len(labels)} != node count {n_rows}")
+
+
+def encode(adj, labels, opts=None, *, out: str = "numpy"):
+    """Embed via the sparse pipeline on the GPU; returns a dense (N, K) float64 array."""
+    labels = _labels_of(labels)
+    flags = options_flags(opts)
+    dev = _device.require_gpu()
+    if hasattr(adj, "index_pointers"):
+        z = _encode_csr(CsrMatrix.coerce(adj, dev), labels, flags, dev)
+    else:
+        edges = _edges_of(adj)
+        _check_shapes(edges.n_nodes, edges.n_nodes, labels)
+        e = edges.to_device(dev)
+        lab = _device.to_device(labels.labels, torch.int64, dev)
+        enc = GeeEncoder(e.n_nodes, e.n_edges, labels.k_classes, e.directed, None, dev)
+        enc.flags = flags
+        wt_code, w = e.weight_kind()
+        z = enc.run(e.rows, e.cols, w, lab, check=True)
+    if out == "torch":
+        return z
+    return z.cpu().numpy()
+
+
+def _encode_csr(a: CsrMatrix, labels: LabelVector, flags: int, dev) -> torch.Tensor:
+    _check_shapes(a.n_rows, a.n_cols, labels)
+    lib = _lib.load()
+    n, k = a.n_rows, labels.k_classes
+    y32, _, inv = label_tables(labels, dev)
+    err = _device.error_word(dev)
+    scale = None
+    with torch.cuda.device(dev):
+        if flags & _lib.LAPLACIAN:
+            deg = torch.empty(n, dtype=torch.float64, device=dev)
+            scale = torch.empty(n, dtype=torch.float64, device=dev)
+            _lib.check(lib.gee_degree(
+                _device.ptr(a.index_pointers), _device.ptr(a.col_indices), _device.ptr(a.data), n,
+                flags & _lib.DIAGONAL, _device.ptr(deg), _device.ptr(scale), _device.ptr(err),
+                _device.stream_handle()))
+        z = torch.empty((n, k), dtype=torch.float64, device=dev)
+        nb = _lib.size_query(lib.gee_embed_workspace, n)
+        ws = _device.WORKSPACE.get(nb, dev)
+        _lib.check(lib.gee_embed(
+            _device.ptr(a.index_pointers), None, _device.ptr(a.col_indices), _device.ptr(a.data), 0,
+            n, _device.ptr(y32), _device.ptr(inv), _device.ptr(scale), k, flags, _device.ptr(z), k,
+            _device.ptr(ws), ws.numel(), _device.ptr(err), _device.stream_handle()))
+    _device.check_device_errors(err, "encode")
+    return z
+
+
+def build_weight_matrix(labels):
+    """W as the reference builds it (embedding.py:92-107), materialised on the
+    device as a CsrMatrix (N x K).  The encode path never needs it."""
+    labels = _labels_of(labels)
+    y32, counts, inv = label_tables(labels)
+    dev = y32.device
+    n = len(labels)
+    lab = y32.to(torch.int64)
+    labeled = lab >= 0
+    ptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    ptr[1:] = torch.cumsum(labeled.to(torch.int64), 0)
+    cols = lab[labeled]
+    return CsrMatrix(n, labels.k_classes, ptr, cols.to(torch.int32), inv[cols])
+
+
+def spmm_weight(a, labels, opts=None, *, out: str = "numpy"):
+    """spmm(A, build_weight_matrix(labels)).to_dense() without building W."""
+    a = CsrMatrix.coerce(a)
+    return encode(a, labels, EmbedOptions() if opts is None else opts, out=out)

@@ -1,0 +1,266 @@
+"""GPU parity: every device op against the reference's own outputs (committed
+fixtures) and against the CPU oracle (oracle/gee_oracle.c, itself pinned
+bitwise to the reference).
+
+Bars (north_star): n_k, CSR structure+values, degrees and the materialised
+A+I / Laplacian CSRs BIT-EXACT; Z within relative 1e-12 in fp64, measured as
+|dz| <= 1e-12 * max(|z_ref|, ||z_ref row||_2) entrywise (SURVEY Appendix A:
+entrywise-relative for non-negative weights, row-relative when signed
+weights can cancel).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from _golden import COMBOS, load, ztag
+from oracle import oracle as O
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a B200")]
+
+import paper_2406_03726_b200 as G  # noqa: E402
+
+RTOL = 1e-12
+CASES = load()
+
+
+def z_close(z, zr, rtol=RTOL):
+    z = np.asarray(z)
+    zr = np.asarray(zr)
+    assert z.shape == zr.shape and z.dtype == np.float64
+    rown = np.sqrt((zr * zr).sum(axis=1, keepdims=True)) if zr.size else zr
+    bound = rtol * np.maximum(np.abs(zr), rown)
+    bad = np.abs(z - zr) > bound
+    assert not bad.any(), f"max |dz|={np.abs(z - zr).max():.3e} at {np.argwhere(bad)[:3]}"
+
+
+def same(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return a.shape == b.shape and np.array_equal(a, b)
+
+
+def csr_equal(m, ref):
+    ip, c, v = m.to_numpy()
+    return same(ip, ref[0]) and same(c, ref[1]) and same(v, ref[2]) and v.dtype == np.float64
+
+
+# ---- reference fixtures ------------------------------------------------------
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_reference_fixture(case):
+    n, k, directed = case["n"], case["k"], case["directed"]
+    edges = G.EdgeList(n, case["rows"], case["cols"], case["w"], directed)
+    labels = G.LabelVector(case["labels"], k)
+    csr = edges.to_csr()
+    assert csr_equal(csr, (case["csr_indptr"], case["csr_cols"], case["csr_vals"]))
+    csr.validate()
+    aug = G.add_identity(csr)
+    assert csr_equal(aug, (case["aug_indptr"], case["aug_cols"], case["aug_vals"]))
+    deg = G.degree_vector(csr).cpu().numpy()
+    assert same(deg, case["deg"].astype(np.float64))
+    deg_aug = G.degree_vector(csr, diagonal=True).cpu().numpy()
+    assert same(deg_aug, case["deg_aug"].astype(np.float64))
+    assert same(G.degree_vector(aug).cpu().numpy(), case["deg_aug"].astype(np.float64))
+    if "lap_error" in case:
+        with pytest.raises(G.NumericalDomainError):
+            G.laplacian_normalize(csr, deg)
+    else:
+        lap = G.laplacian_normalize(csr, deg)
+        assert csr_equal(lap, (case["lap_indptr"], case["lap_cols"], case["lap_vals"]))
+    assert same(labels.class_counts(), case["counts"])
+    for lap_f, diag_f, corr_f in COMBOS:
+        opts = G.EmbedOptions(bool(lap_f), bool(diag_f), bool(corr_f))
+        tag = ztag(lap_f, diag_f, corr_f)
+        for adj in (edges, csr):
+            if tag + "_error" in case:
+                with pytest.raises(G.NumericalDomainError):
+                    G.encode(adj, labels, opts)
+            else:
+                z_close(G.encode(adj, labels, opts), case[tag])
+
+
+def test_triangle_goldens():
+    # test_embedding.py:48-63
+    e = G.EdgeList(3, [0, 0, 1], [1, 2, 2], [1.0, 1.0, 1.0])
+    lab = G.LabelVector(np.array([0, 1, 1]), 2)
+    assert np.allclose(G.encode(e.to_csr(), lab), [[0, 1], [1, .5], [1, .5]], atol=1e-15)
+    assert np.allclose(G.encode(e, lab, G.EmbedOptions(diagonal=True)), np.ones((3, 2)), atol=1e-15)
+    assert np.allclose(G.encode(e, lab, G.EmbedOptions(laplacian=True)),
+                       [[0, .5], [.5, .25], [.5, .25]], atol=1e-15)
+    z = G.encode(G.EdgeList(2, [0], [1], [1.0]), G.LabelVector(np.array([0, 1]), 2))
+    assert np.array_equal(z, [[0.0, 1.0], [1.0, 0.0]])
+
+
+def test_structural_errors():
+    e = G.EdgeList(3, [0, 0, 1], [1, 2, 2], [1.0, 1.0, 1.0])
+    with pytest.raises(G.StructuralError):
+        G.encode(e, G.LabelVector(np.array([0, 1]), 2))
+    with pytest.raises(G.StructuralError):
+        G.encode(e.to_csr(), G.LabelVector(np.array([0, 1]), 2))
+    rect = G.CsrMatrix.from_triplets([0], [2], [1.0], 2, 3)
+    with pytest.raises(G.StructuralError, match="square"):
+        G.encode(rect, G.LabelVector(np.array([0, 1]), 2))
+    # device-side label validation (labels handed in as a CUDA tensor)
+    bad = G.LabelVector(torch.tensor([0, 5, 1], device="cuda"), 2)
+    with pytest.raises(G.StructuralError):
+        G.encode(e, bad)
+    # device-side edge validation
+    with pytest.raises(G.StructuralError):
+        G.EdgeList(3, torch.tensor([0, 7], device="cuda"), torch.tensor([1, 1], device="cuda"),
+                   torch.tensor([1.0, 1.0], device="cuda", dtype=torch.float64))
+
+
+# ---- oracle fuzz -------------------------------------------------------------
+def _graph(rng, n, m, kind, directed, k, dup_runs=False, hub=None):
+    rows = rng.integers(0, n, m)
+    cols = rng.integers(0, n, m)
+    if hub is not None:
+        sel = rng.random(m) < hub[1]
+        rows[sel] = hub[0]
+    if dup_runs and m >= 40:
+        for t in range(0, m - 8, 37):  # runs of 2..6 identical coordinates
+            ln = 2 + (t % 5)
+            rows[t:t + ln] = rows[t]
+            cols[t:t + ln] = cols[t]
+    if kind == "unit":
+        w = np.ones(m)
+    elif kind == "pos":
+        w = 1.0 - rng.random(m)
+    elif kind == "signed":
+        w = rng.uniform(-2, 2, m)
+    elif kind == "dyadic":
+        w = rng.choice([-1.0, 0.5, 1.0, 2.0, 0.25], m)
+    else:
+        w = (1.0 - rng.random(m, dtype=np.float32)).astype(np.float32)
+    labels = rng.integers(0, k, n)
+    labels[rng.random(n) < 0.1] = -1
+    return rows, cols, w, labels
+
+
+def _check_against_oracle(n, rows, cols, w, labels, k, directed, combos=COMBOS):
+    w64 = np.asarray(w, dtype=np.float64)
+    edges = G.EdgeList(n, rows, cols, w, directed)
+    lab = G.LabelVector(labels, k)
+    ref_csr = O.to_csr(rows, cols, w64, n, directed)
+    csr = edges.to_csr()
+    assert csr_equal(csr, ref_csr)
+    ip, oc, ov = ref_csr
+    for diag in (False, True):
+        if diag:
+            a = O.add_identity(ip, oc, ov, n)
+            dref = O.degree(a[0], a[2], n)
+        else:
+            dref = O.degree(ip, ov, n)
+        assert same(G.degree_vector(csr, diagonal=diag).cpu().numpy(), dref)
+    assert same(lab.class_counts(), O.class_counts(labels, k))
+    for lap_f, diag_f, corr_f in combos:
+        st, zr, ex = O.encode_edges(rows, cols, w64, n, directed, labels, k,
+                                    O.flags_of(lap_f, diag_f, corr_f), want_degree=True)
+        opts = G.EmbedOptions(bool(lap_f), bool(diag_f), bool(corr_f))
+        if st != O.OK:
+            with pytest.raises(G.NumericalDomainError):
+                G.encode(edges, lab, opts)
+            continue
+        z = G.encode(edges, lab, opts)
+        z_close(z, zr)
+        z_close(G.encode(csr, lab, opts), zr)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fuzz_small(seed):
+    rng = np.random.default_rng(1000 + seed)
+    for kind in ("unit", "pos", "signed", "dyadic", "f32"):
+        n = int(rng.integers(2, 400))
+        m = int(rng.integers(0, 6 * n))
+        k = int(rng.integers(1, 12))
+        directed = bool(rng.integers(0, 2))
+        _check_against_oracle(n, *_graph(rng, n, m, kind, directed, k, dup_runs=seed % 2 == 0),
+                              k, directed)
+
+
+@pytest.mark.parametrize("n,m,k,kind,directed,hub", [
+    (3000, 150_000, 5, "pos", False, None),        # tier D rows (n_cols <= 12288, long rows)
+    (3000, 150_000, 5, "pos", True, (17, 0.05)),   # tier D row longer than the smem stage
+    (40_000, 400_000, 20, "pos", False, None),     # tiers S/B (large n)
+    (40_000, 300_000, 50, "pos", True, (5, 0.1)),  # tier X hub row (LSD) + long embed row
+    (20_000, 200_000, 3, "unit", False, (9, 0.2)),  # long row, register path
+    (20_000, 100_000, 1000, "pos", False, (3, 0.2)),  # K=1000 shared-memory path + long row
+    (5_000, 40_000, 2500, "unit", True, None),     # K > tile: tiled correlation
+])
+def test_tiers(n, m, k, kind, directed, hub):
+    rng = np.random.default_rng(n + m + k)
+    _check_against_oracle(n, *_graph(rng, n, m, kind, directed, k, dup_runs=True, hub=hub), k,
+                          directed, combos=[(0, 0, 0), (1, 1, 1), (1, 0, 1), (0, 1, 0)])
+
+
+def test_runs_of_duplicates_in_stream_order():
+    # 5 identical coordinates whose sum depends on the order (non-associative)
+    vals = [1e16, 1.0, -1e16, 1.0, 3.0]
+    n = 20000  # large n -> tiers S/B path; repeated below with small n -> tier D
+    for n in (20000, 50):
+        rows = np.array([3] * 5 + [3] * 40, np.int64)
+        cols = np.array([7] * 5 + list(range(10, 50)), np.int64)
+        w = np.array(vals + [0.5] * 40)
+        _check_against_oracle(n, rows, cols, w, np.zeros(n, np.int64), 1, True)
+
+
+def test_weighted_long_rows_exact_degree_fold():
+    # non-dyadic weights: the certificate fails and the sequential fold runs
+    rng = np.random.default_rng(5)
+    n = 30000
+    rows = np.concatenate([np.full(9000, 11), rng.integers(0, n, 60000)])
+    cols = rng.integers(0, n, rows.size)
+    w = rng.random(rows.size) * 1e3 + 1e-9
+    _check_against_oracle(n, rows, cols, w, rng.integers(0, 4, n), 4, False,
+                          combos=[(1, 1, 1), (1, 0, 0)])
+
+
+# ---- configs -----------------------------------------------------------------
+@pytest.mark.parametrize("idx,scale_down", [(0, 0), (1, 0), (2, 5), (3, 8), (4, 6)])
+def test_configs_vs_oracle(idx, scale_down):
+    from paper_2406_03726_b200 import synth
+    c = synth.make_config(idx, scale_down=scale_down)
+    rows, cols, w, labels = (x.cpu().numpy() if isinstance(x, torch.Tensor) else x
+                             for x in (c["rows"], c["cols"], c["weights"], c["labels"]))
+    f = c["flags"]
+    combo = (int(bool(f & 1)), int(bool(f & 2)), int(bool(f & 4)))
+    _check_against_oracle(c["n"], rows, cols, w, labels, c["k"], c["directed"], combos=[combo])
+
+
+def test_full_cfg1_properties():
+    from paper_2406_03726_b200 import synth
+    c = synth.make_config(1)
+    edges = G.EdgeList(c["n"], c["rows"], c["cols"], c["weights"]).to_device("cuda")
+    lab = G.LabelVector(c["labels"], 3)
+    csr = edges.to_csr()
+    assert csr.nnz == 2 * c["e"]  # SBM: no duplicates or loops, so nnz = 2E
+    deg = G.degree_vector(csr, diagonal=True).cpu().numpy()
+    assert same(deg, np.diff(csr.index_pointers.cpu().numpy()).astype(np.float64) + 1.0)
+    z = G.encode(edges, lab, G.EmbedOptions(True, True, True))
+    norms = np.linalg.norm(z, axis=1)
+    assert np.abs(norms - 1.0).max() <= 1e-12
+    z0 = G.encode(edges, lab)
+    counts = lab.class_counts()
+    scaled = z0 * counts[None, :]
+    assert np.abs(scaled - np.rint(scaled)).max() <= 1e-9
+    assert np.rint(scaled).sum() == 2 * c["e"]
+
+
+def test_encoder_plan_and_launch_count():
+    from paper_2406_03726_b200 import _lib, synth
+    c = synth.make_config(1)
+    dev = torch.device("cuda")
+    rows = torch.as_tensor(c["rows"], device=dev)
+    cols = torch.as_tensor(c["cols"], device=dev)
+    w = torch.as_tensor(c["weights"], device=dev)
+    lab = torch.as_tensor(c["labels"], device=dev)
+    enc = G.GeeEncoder(c["n"], c["e"], 3, False, G.EmbedOptions(True, True, True))
+    lib = _lib.load()
+    lib.gee_reset_launch_count()
+    z1 = enc.run(rows, cols, w, lab).clone()
+    assert lib.gee_launch_count() >= 8
+    z2 = enc.run(rows, cols, w, lab)
+    assert torch.equal(z1, z2)  # deterministic
+    st, zr, _ = O.encode_edges(c["rows"], c["cols"], c["weights"], c["n"], False, c["labels"], 3, 7)
+    z_close(z1.cpu().numpy(), zr)
