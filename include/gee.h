@@ -167,6 +167,12 @@ int gee_profile_start(void *stream);
 int gee_profile_stop(void);
 int gee_profile_read(float *ms, const char **names, int cap);
 
+/* Test hook (thread-local): GEE_DEBUG_FORCE_BUCKETS = 1 makes the CSR
+ * build take the row-bucket path even when (row, col) packs into 32 bits,
+ * so parity tests cover both assembly paths.  Returns the previous value. */
+#define GEE_DEBUG_FORCE_BUCKETS 1
+int gee_debug_set(int key, int value);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,7 +54,9 @@ SIGNATURES = {
     "gee_profile_start": (_int, [_vp]),
     "gee_profile_stop": (_int, []),
     "gee_profile_read": (_int, [ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_char_p), _int]),
+    "gee_debug_set": (_int, [_int, _int]),
 }
+DEBUG_FORCE_BUCKETS = 1
 
 _lib = None
 

@@ -52,7 +52,13 @@ int num_sms() {
 }
 
 int label_hist(const int64_t *, int64_t, int32_t, int32_t *, int64_t *, double *, int32_t *, cudaStream_t);
-size_t csr_build_workspace(int64_t E, int64_t n_rows, int directed);
+size_t csr_build_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
+bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
+int set_force_buckets(int v);
+int sort_csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, int64_t E, int64_t n_rows,
+                   int64_t n_cols, int directed, int force_vals, int64_t *row_ptr, int32_t *col, double *val,
+                   int64_t *nnz, unsigned deg_flags, double *deg, double *scale, void *ws, size_t ws_bytes,
+                   unsigned **val_mode, int32_t *err, cudaStream_t st);
 int csr_build(const int64_t *, const int64_t *, const void *, int, int64_t, int64_t, int64_t, int, int,
               int64_t *, unsigned *, int32_t *, double *, int64_t *, unsigned, double *, double *, void *,
               size_t, int32_t *, cudaStream_t);
@@ -65,14 +71,15 @@ size_t laplacian_workspace(int64_t n);
 int laplacian_normalize(const int64_t *, const int32_t *, const double *, int64_t, const double *, int64_t *,
                         int32_t *, double *, int64_t *, void *, size_t, int32_t *, cudaStream_t);
 size_t embed_workspace(int64_t n_rows);
-int embed(const int64_t *, const unsigned *, const int32_t *, const double *, int64_t, int64_t,
-          const int32_t *, const double *, const double *, int, unsigned, double *, int64_t, void *, size_t,
-          int32_t *, cudaStream_t);
+int embed(const int64_t *, const unsigned *, const int32_t *, const double *, const unsigned *, int64_t,
+          int64_t, const int32_t *, const double *, const double *, int, unsigned, double *, int64_t, void *,
+          size_t, int32_t *, cudaStream_t);
 int validate_edges(const int64_t *, const int64_t *, const void *, int, int64_t, int64_t, int32_t *,
                    cudaStream_t);
 
 static bool index_ok(int64_t x) { return x >= 0 && x < ((int64_t)1 << 31); }
-static bool wt_ok(int wt, const void *w) {
+static bool wt_ok(int wt, const void *w, int64_t n_edges) {
+    if (n_edges == 0) return wt == GEE_W_UNIT || wt == GEE_W_F64 || wt == GEE_W_F32;
     if (wt == GEE_W_UNIT) return true;
     return (wt == GEE_W_F64 || wt == GEE_W_F32) && w != nullptr;
 }
@@ -103,7 +110,7 @@ static size_t carve_encode(Carver &cv, EncodeWs &w, int64_t E, int64_t n, int32_
     w.row_cnt = cv.take<unsigned>((size_t)n + 1);
     w.col = cv.take<int32_t>((size_t)(M > 0 ? M : 1));
     w.val = cv.take<double>((size_t)(M > 0 ? M : 1));
-    w.csr_bytes = csr_build_workspace(E, n, directed);
+    w.csr_bytes = csr_build_workspace(E, n, n, directed);
     w.csr_ws = cv.take<char>(w.csr_bytes);
     w.emb_bytes = embed_workspace(n);
     w.emb_ws = cv.take<char>(w.emb_bytes);
@@ -141,6 +148,11 @@ int gee_profile_start(void *stream) {
     return GEE_OK;
 }
 
+int gee_debug_set(int key, int value) {
+    if (key == GEE_DEBUG_FORCE_BUCKETS) return set_force_buckets(value);
+    return -1;
+}
+
 int gee_profile_stop(void) {
     t_prof.on = false;
     return t_prof.n;
@@ -162,7 +174,7 @@ int gee_profile_read(float *ms, const char **names, int cap) {
 
 int gee_validate_edges(const int64_t *rows, const int64_t *cols, const void *w, int w_type, int64_t n_edges,
                        int64_t n_nodes, int32_t *err, void *stream) {
-    if (n_edges < 0 || n_nodes < 0 || !wt_ok(w_type, w) || !err) return GEE_E_ARG;
+    if (n_edges < 0 || n_nodes < 0 || !wt_ok(w_type, w, n_edges) || !err) return GEE_E_ARG;
     return validate_edges(rows, cols, w, w_type, n_edges, n_nodes, err, (cudaStream_t)stream);
 }
 
@@ -176,7 +188,7 @@ int gee_label_hist(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, in
 int gee_csr_build_workspace(int64_t n_edges, int64_t n_rows, int64_t n_cols, int directed, size_t *ws_bytes) {
     if (!ws_bytes || n_edges < 0 || !index_ok(n_edges) || !index_ok(n_rows) || !index_ok(n_cols))
         return GEE_E_ARG;
-    *ws_bytes = csr_build_workspace(n_edges, n_rows, directed);
+    *ws_bytes = csr_build_workspace(n_edges, n_rows, n_cols, directed);
     return GEE_OK;
 }
 
@@ -184,7 +196,7 @@ int gee_csr_build(const int64_t *rows, const int64_t *cols, const void *w, int w
                   int64_t n_rows, int64_t n_cols, int directed, int compact, int64_t *row_ptr, uint32_t *row_cnt,
                   int32_t *col, double *val, int64_t *nnz, unsigned deg_flags, double *deg, double *scale,
                   void *ws, size_t ws_bytes, int32_t *err, void *stream) {
-    if (!index_ok(n_edges) || !index_ok(n_rows) || !index_ok(n_cols) || !wt_ok(w_type, w)) return GEE_E_ARG;
+    if (!index_ok(n_edges) || !index_ok(n_rows) || !index_ok(n_cols) || !wt_ok(w_type, w, n_edges)) return GEE_E_ARG;
     if (!row_ptr || (!compact && !row_cnt) || (n_edges > 0 && (!rows || !cols || !col || !val)))
         return GEE_E_ARG;
     if (!directed && n_rows != n_cols) return GEE_E_ARG;
@@ -241,7 +253,7 @@ int gee_embed(const int64_t *row_ptr, const uint32_t *row_cnt, const int32_t *co
     if (k < 1 || ldz < k || row_begin < 0 || row_end < row_begin || !index_ok(row_end)) return GEE_E_ARG;
     if (row_end > row_begin && (!row_ptr || !y32 || !inv_nk || !z)) return GEE_E_ARG;
     if ((flags & GEE_LAPLACIAN) && !scale) return GEE_E_ARG;
-    return embed(row_ptr, row_cnt, col, val, row_begin, row_end, y32, inv_nk, scale, k, flags, z, ldz, ws,
+    return embed(row_ptr, row_cnt, col, val, nullptr, row_begin, row_end, y32, inv_nk, scale, k, flags, z, ldz, ws,
                  ws_bytes, err, (cudaStream_t)stream);
 }
 
@@ -256,7 +268,7 @@ int gee_encode_edges_workspace(int64_t n_edges, int64_t n_nodes, int32_t k, int 
 int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, int w_type, int64_t n_edges,
                      int64_t n_nodes, int directed, const int64_t *labels, int32_t k, unsigned flags, double *z,
                      void *ws, size_t ws_bytes, int32_t *err, void *stream) {
-    if (!index_ok(n_edges) || !index_ok(n_nodes) || k < 1 || !wt_ok(w_type, w) || !z) return GEE_E_ARG;
+    if (!index_ok(n_edges) || !index_ok(n_nodes) || k < 1 || !wt_ok(w_type, w, n_edges) || !z) return GEE_E_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     Carver cv(ws);
     EncodeWs W;
@@ -265,11 +277,22 @@ int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, in
     int rc = label_hist(labels, n_nodes, k, W.y32, W.counts, W.inv, err, st);
     if (rc) return rc;
     const unsigned deg_flags = (flags & GEE_LAPLACIAN) ? (GEE_LAPLACIAN | (flags & GEE_DIAGONAL)) : 0u;
+    const double *sc = (flags & GEE_LAPLACIAN) ? W.scale : nullptr;
+    if (sort_path_ok(n_edges, n_nodes, n_nodes, directed)) {
+        // compact CSR from the radix sort; values stay implicit (1.0) when the
+        // graph has unit weights and no duplicate entries
+        unsigned *val_mode = nullptr;
+        rc = sort_csr_build(rows, cols, w, w_type, n_edges, n_nodes, n_nodes, directed, 0, W.row_ptr, W.col, W.val,
+                            nullptr, deg_flags, W.deg, W.scale, W.csr_ws, W.csr_bytes, &val_mode, err, st);
+        if (rc) return rc;
+        return embed(W.row_ptr, nullptr, W.col, W.val, val_mode, 0, n_nodes, W.y32, W.inv, sc, k, flags, z, k,
+                     W.emb_ws, W.emb_bytes, err, st);
+    }
     rc = csr_build(rows, cols, w, w_type, n_edges, n_nodes, n_nodes, directed, 0, W.row_ptr, W.row_cnt, W.col,
                    W.val, nullptr, deg_flags, W.deg, W.scale, W.csr_ws, W.csr_bytes, err, st);
     if (rc) return rc;
-    return embed(W.row_ptr, W.row_cnt, W.col, W.val, 0, n_nodes, W.y32, W.inv,
-                 (flags & GEE_LAPLACIAN) ? W.scale : nullptr, k, flags, z, k, W.emb_ws, W.emb_bytes, err, st);
+    return embed(W.row_ptr, W.row_cnt, W.col, W.val, nullptr, 0, n_nodes, W.y32, W.inv, sc, k, flags, z, k,
+                 W.emb_ws, W.emb_bytes, err, st);
 }
 
 }  // extern "C"

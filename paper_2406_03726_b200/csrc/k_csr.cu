@@ -697,10 +697,24 @@ static size_t carve_csr(Carver &cv, CsrWs &w, int64_t E, int64_t n_rows, int dir
     return cv.bytes();
 }
 
-size_t csr_build_workspace(int64_t E, int64_t n_rows, int directed) {
+bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
+size_t sort_workspace(int64_t E, int64_t n_rows, int directed);
+int sort_csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, int64_t E, int64_t n_rows,
+                   int64_t n_cols, int directed, int force_vals, int64_t *row_ptr, int32_t *col, double *val,
+                   int64_t *nnz, unsigned deg_flags, double *deg, double *scale, void *ws, size_t ws_bytes,
+                   unsigned **val_mode, int32_t *err, cudaStream_t st);
+
+size_t csr_build_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int directed) {
+    if (sort_path_ok(E, n_rows, n_cols, directed)) return sort_workspace(E, n_rows, directed);
     Carver cv(nullptr);
     CsrWs w;
     return carve_csr(cv, w, E, n_rows, directed);
+}
+
+__global__ void k_row_cnt(const int64_t *__restrict__ row_ptr, int64_t n, unsigned *__restrict__ cnt) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride)
+        cnt[r] = (unsigned)(row_ptr[r + 1] - row_ptr[r]);
 }
 
 static int bit_length(int64_t x) {
@@ -723,6 +737,17 @@ int csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, i
               unsigned *row_cnt, int32_t *col, double *val, int64_t *nnz, unsigned deg_flags,
               double *deg, double *scale, void *ws, size_t ws_bytes, int32_t *err,
               cudaStream_t st) {
+    if (sort_path_ok(E, n_rows, n_cols, directed)) {
+        // packed 32-bit (row, col) keys: radix-sort path, always a compact CSR
+        int rc = sort_csr_build(rows, cols, w, wt, E, n_rows, n_cols, directed, 1, row_ptr, col, val, nnz,
+                                deg_flags, deg, scale, ws, ws_bytes, nullptr, err, st);
+        if (rc) return rc;
+        if (row_cnt && n_rows > 0) {
+            k_row_cnt<<<grid_for(n_rows, 256, 8), 256, 0, st>>>(row_ptr, n_rows, row_cnt);
+            GEE_CHECK_LAUNCH("k_row_cnt");
+        }
+        return GEE_OK;
+    }
     Carver cv(ws);
     CsrWs W;
     size_t need = carve_csr(cv, W, E, n_rows, directed);

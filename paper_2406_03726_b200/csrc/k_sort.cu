@@ -1,0 +1,576 @@
+// k_sort.cu -- K2 for graphs whose (row, col) pair packs into 32 bits
+// (n_rows * n_cols <= 2^32, e.g. configs 0/1): a device LSD radix sort of the
+// symmetrised stream, then one pass that sums duplicates, drops zeros and
+// emits the CSR.
+//
+//   k_sort_hist   one read of the edge list: the 8-bit digit histograms of
+//                 every pass, and whether any weight differs from 1.0
+//   k_onesweep    one pass per digit: tile-local stable ranking (warp
+//                 multisplit from 8 ballots, no atomics), decoupled look-back
+//                 for the global digit offsets, then the tile is reordered in
+//                 shared memory so each digit run leaves as one coalesced
+//                 burst.  Pass 0 reads the int64 edge list directly.
+//   k_dedup       runs of equal keys -> one CSR entry (sum in stream order,
+//                 exact zeros dropped), compacted with a second look-back; it
+//                 also writes row_ptr and the pre-dedup stream row pointer.
+//
+// Stream order.  Pass 0 emits edge e's two entries at virtual positions 2e
+// (original) and 2e+1 (reversed; a sentinel key for a self-loop), so equal
+// keys leave the sort in (e, direction) order, not the reference's
+// [originals..., reversed...] order (graph_io.py:82-88).  Every entry
+// carries its true stream index (e or E+e) as payload, and k_dedup restores
+// stream order inside any run of >= 3 duplicates before summing (a run of 2
+// sums commutatively).  With unit weights no payload moves at all: a run's
+// value is its length, and the per-row degree is the row's stream length.
+#include "gee_common.cuh"
+
+namespace gee {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 4096
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr unsigned kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
+
+__device__ __forceinline__ double sort_load_w(const void *w, int wt, int64_t e) {
+    if (wt == GEE_W_F64) return static_cast<const double *>(w)[e];
+    if (wt == GEE_W_F32) return (double)static_cast<const float *>(w)[e];
+    return 1.0;
+}
+
+struct SortGeom {
+    int64_t E;        // input edges
+    int64_t Mv;       // virtual stream length (E directed, 2E undirected)
+    int directed;
+    int colbits;
+    unsigned sentinel;  // all key bits set: sorts last
+    int passes;
+};
+
+// key of virtual position v; false for positions past the stream
+__device__ __forceinline__ unsigned sort_key(const SortGeom &g, const int64_t *rows, const int64_t *cols,
+                                             int64_t v, unsigned &pay) {
+    if (g.directed) {
+        pay = (unsigned)v;
+        return ((unsigned)rows[v] << g.colbits) | (unsigned)cols[v];
+    }
+    int64_t e = v >> 1;
+    unsigned r = (unsigned)rows[e], c = (unsigned)cols[e];
+    if (v & 1) {
+        pay = (unsigned)(g.E + e);
+        return r == c ? g.sentinel : ((c << g.colbits) | r);
+    }
+    pay = (unsigned)e;
+    return (r << g.colbits) | c;
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSortThreads) k_sort_hist(SortGeom g, const int64_t *__restrict__ rows,
+                                                            const int64_t *__restrict__ cols,
+                                                            const void *__restrict__ w, int wt,
+                                                            unsigned *__restrict__ hist,
+                                                            unsigned *__restrict__ nonunit) {
+    __shared__ unsigned sh[4][256];
+    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    bool bad_w = false;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t v_round = (g.Mv + 31) & ~int64_t(31);
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < v_round; v += stride) {
+        const bool valid = v < g.Mv;
+        unsigned pay, key = 0;
+        if (valid) {
+            key = sort_key(g, rows, cols, v, pay);
+            if (wt != GEE_W_UNIT && (g.directed || !(v & 1))) bad_w |= sort_load_w(w, wt, v >> (g.directed ? 0 : 1)) != 1.0;
+        }
+        // valid lanes form a prefix of the warp (v grows with the lane id)
+        const int nv = __popc(__ballot_sync(0xffffffffu, valid));
+        for (int p = 0; p < g.passes; ++p) {
+            const unsigned d = (key >> (8 * p)) & 255u;
+            // run-length aggregation across the warp: rows arrive in runs, so
+            // the high digits repeat and one atomic per run replaces 32
+            const unsigned prev = __shfl_up_sync(0xffffffffu, d, 1);
+            const bool head = valid && (lane == 0 || prev != d);
+            const unsigned heads = __ballot_sync(0xffffffffu, head);
+            if (head) {
+                const unsigned after = heads & ~((2u << lane) - 1u);
+                const int next = after ? __ffs(after) - 1 : nv;
+                atomicAdd(&sh[p][d], (unsigned)(next - lane));
+            }
+        }
+    }
+    if (__any_sync(0xffffffffu, bad_w) && lane == 0) atomicOr(nonunit, 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < g.passes * 256; i += blockDim.x) {
+        unsigned x = (&sh[0][0])[i];
+        if (x) atomicAdd(&hist[i], x);
+    }
+}
+
+// exclusive scan of each pass's 256-bin histogram (one CTA of 256 threads)
+__global__ void k_sort_bases(unsigned *hist, int passes) {
+    __shared__ unsigned red[33];
+    for (int p = 0; p < passes; ++p) {
+        unsigned v = hist[p * 256 + threadIdx.x];
+        unsigned ex = block_exclusive_scan(v, red, nullptr);
+        hist[p * 256 + threadIdx.x] = ex;
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+struct OnesweepArgs {
+    SortGeom g;
+    const int64_t *rows, *cols;         // pass 0 input
+    const unsigned *kin, *pin;          // later passes
+    unsigned *kout, *pout;
+    const unsigned *base;               // [256] exclusive digit bases of this pass
+    unsigned *status;                   // [tiles][256] look-back words (zeroed)
+    unsigned *tile_ctr;
+    const unsigned *nonunit;            // carry payload iff *nonunit
+    int shift;
+    int first;
+};
+
+__global__ void __launch_bounds__(kSortThreads) k_onesweep(OnesweepArgs a) {
+    __shared__ unsigned sk[kSortTile];
+    __shared__ unsigned sp[kSortTile];
+    __shared__ unsigned whist[kSortWarps][256];
+    __shared__ unsigned tstart[256], gbase[256];
+    __shared__ unsigned red[33];
+    __shared__ int s_tile;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const bool carry = *a.nonunit != 0;
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(a.tile_ctr, 1u);
+    for (int i = threadIdx.x; i < kSortWarps * 256; i += kSortThreads) (&whist[0][0])[i] = 0;
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t t0 = tile * kSortTile;
+    const int nvalid = (int)min((int64_t)kSortTile, a.g.Mv - t0);
+    unsigned key[kSortItems], pay[kSortItems], rank[kSortItems];
+    // load: warp w owns items [w*512, w*512+512) in 16 rounds of 32
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const int i = wid * (kSortTile / kSortWarps) + j * 32 + lane;
+        pay[j] = 0;
+        if (i < nvalid) {
+            if (a.first) {
+                key[j] = sort_key(a.g, a.rows, a.cols, t0 + i, pay[j]);
+            } else {
+                key[j] = a.kin[t0 + i];
+                if (carry) pay[j] = a.pin[t0 + i];
+            }
+        } else {
+            key[j] = 0;
+        }
+    }
+    // stable warp multisplit
+    unsigned *wh = whist[wid];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const int i = wid * (kSortTile / kSortWarps) + j * 32 + lane;
+        const bool v = i < nvalid;
+        const unsigned d = (key[j] >> a.shift) & 255u;
+        unsigned peers = __ballot_sync(0xffffffffu, v);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            unsigned m = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+            peers &= ((d >> b) & 1u) ? m : ~m;
+        }
+        unsigned before = v ? wh[d] : 0u;
+        rank[j] = before + __popc(peers & lanemask_lt());
+        __syncwarp();
+        if (v && lane == __ffs(peers) - 1) wh[d] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // per digit: tile total and per-warp exclusive prefix
+    const int d = threadIdx.x;
+    unsigned tot = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) {
+        unsigned x = whist[w][d];
+        whist[w][d] = tot;
+        tot += x;
+    }
+    // decoupled look-back over previous tiles for this digit
+    unsigned *st = a.status + (size_t)tile * 256 + d;
+    unsigned excl = 0;
+    if (tile == 0) {
+        st_release(st, kFlagInc | tot);
+    } else {
+        st_release(st, kFlagAgg | tot);
+        for (int64_t t = tile - 1; t >= 0; --t) {
+            const unsigned *ps = a.status + (size_t)t * 256 + d;
+            unsigned s;
+            do {
+                s = ld_acquire(ps);
+            } while ((s & ~kValMask) == 0);
+            excl += s & kValMask;
+            if (s & kFlagInc) break;
+        }
+        st_release(st, kFlagInc | (excl + tot));
+    }
+    gbase[d] = a.base[d] + excl;
+    tstart[d] = block_exclusive_scan(tot, red, nullptr);
+    __syncthreads();
+    // reorder the tile by digit in shared memory
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const int i = wid * (kSortTile / kSortWarps) + j * 32 + lane;
+        if (i < nvalid) {
+            const unsigned dd = (key[j] >> a.shift) & 255u;
+            const unsigned pos = tstart[dd] + whist[wid][dd] + rank[j];
+            sk[pos] = key[j];
+            sp[pos] = pay[j];
+        }
+    }
+    __syncthreads();
+    // coalesced write-out: consecutive threads write consecutive slots of a digit run
+    for (int i = threadIdx.x; i < nvalid; i += kSortThreads) {
+        const unsigned k = sk[i];
+        const unsigned dd = (k >> a.shift) & 255u;
+        const unsigned o = gbase[dd] + (i - tstart[dd]);
+        a.kout[o] = k;
+        if (carry) a.pout[o] = sp[i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+struct DedupArgs {
+    SortGeom g;
+    const unsigned *key, *pay;  // sorted stream
+    const void *w;
+    int wt;
+    int64_t n_rows;
+    int32_t *out_col;
+    double *out_val;
+    int64_t *row_ptr;   // [n_rows+1] compacted CSR
+    int64_t *sptr;      // [n_rows+1] stream row pointer (pre-dedup), may be null
+    unsigned *status;   // [tiles] look-back words (zeroed)
+    unsigned *tile_ctr;
+    const unsigned *nonunit;
+    unsigned *has_multi;  // set when a unit-weight run has length > 1
+    int force_vals;       // 1: always write out_val; 2: only run if *has_multi
+};
+
+__device__ __forceinline__ void sort_run_by_payload(unsigned *pay, int64_t p, int64_t q) {
+    // in-place insertion sort (runs of duplicates are short); heap sort for long ones
+    const int64_t L = q - p;
+    if (L <= 64) {
+        for (int64_t i = p + 1; i < q; ++i) {
+            unsigned x = pay[i];
+            int64_t j = i - 1;
+            while (j >= p && pay[j] > x) {
+                pay[j + 1] = pay[j];
+                --j;
+            }
+            pay[j + 1] = x;
+        }
+        return;
+    }
+    unsigned *h = pay + p;
+    for (int64_t s = L / 2 - 1; s >= 0; --s) {
+        int64_t i = s;
+        for (;;) {
+            int64_t c = 2 * i + 1;
+            if (c >= L) break;
+            if (c + 1 < L && h[c + 1] > h[c]) ++c;
+            if (h[i] >= h[c]) break;
+            unsigned t = h[i]; h[i] = h[c]; h[c] = t;
+            i = c;
+        }
+    }
+    for (int64_t end = L - 1; end > 0; --end) {
+        unsigned t = h[0]; h[0] = h[end]; h[end] = t;
+        int64_t i = 0;
+        for (;;) {
+            int64_t c = 2 * i + 1;
+            if (c >= end) break;
+            if (c + 1 < end && h[c + 1] > h[c]) ++c;
+            if (h[i] >= h[c]) break;
+            unsigned u = h[i]; h[i] = h[c]; h[c] = u;
+            i = c;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_dedup(DedupArgs a) {
+    __shared__ unsigned red[33];
+    __shared__ unsigned s_excl;
+    __shared__ int s_tile;
+    const bool carry = *a.nonunit != 0;
+    if (a.force_vals == 2 && (carry || *a.has_multi == 0)) return;
+    const bool write_vals = carry || a.force_vals != 0;
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(a.tile_ctr, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t Mv = a.g.Mv;
+    const unsigned cmask = (1u << a.g.colbits) - 1u;
+    const int cb = a.g.colbits;
+    const int64_t p0 = tile * kSortTile + (int64_t)threadIdx.x * kSortItems;
+    const int64_t p1 = min(Mv, p0 + kSortItems);
+    // pass 1: runs headed in my range -> values, keep flags
+    unsigned keepbits = 0;
+    double vals[kSortItems];
+    bool multi = false;
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const int64_t p = p0 + j;
+        vals[j] = 0.0;
+        if (p >= p1) continue;
+        const unsigned k = a.key[p];
+        if (k == a.g.sentinel) continue;
+        if (p > 0 && a.key[p - 1] == k) continue;
+        int64_t q = p + 1;
+        while (q < Mv && a.key[q] == k) ++q;
+        double acc;
+        if (carry) {
+            unsigned *pay = const_cast<unsigned *>(a.pay);
+            if (q - p >= 3) sort_run_by_payload(pay, p, q);
+            const int64_t E = a.g.E;
+            unsigned s = pay[p];
+            acc = sort_load_w(a.w, a.wt, s < E ? s : s - E);
+            for (int64_t i = p + 1; i < q; ++i) {
+                unsigned t = pay[i];
+                acc += sort_load_w(a.w, a.wt, t < E ? t : t - E);
+            }
+        } else {
+            acc = (double)(q - p);
+            multi |= q - p > 1;
+        }
+        vals[j] = acc;
+        if (acc != 0.0) keepbits |= 1u << j;
+    }
+    if (multi) atomicOr(a.has_multi, 1u);
+    unsigned cnt = __popc(keepbits), ttot;
+    unsigned off = block_exclusive_scan(cnt, red, &ttot);
+    // look-back for the tile's output offset
+    if (threadIdx.x == 0) {
+        unsigned *st = a.status + tile;
+        unsigned excl = 0;
+        if (tile == 0) {
+            st_release(st, kFlagInc | ttot);
+        } else {
+            st_release(st, kFlagAgg | ttot);
+            for (int64_t t = tile - 1; t >= 0; --t) {
+                unsigned s;
+                do {
+                    s = ld_acquire(a.status + t);
+                } while ((s & ~kValMask) == 0);
+                excl += s & kValMask;
+                if (s & kFlagInc) break;
+            }
+            st_release(st, kFlagInc | (excl + ttot));
+        }
+        s_excl = excl;
+    }
+    __syncthreads();
+    int64_t o = (int64_t)s_excl + off;
+    // pass 2: emit entries; row starts write row_ptr / sptr for every row they open
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const int64_t p = p0 + j;
+        if (p >= p1) break;
+        const unsigned k = a.key[p];
+        const int64_t row = k == a.g.sentinel ? a.n_rows : (int64_t)(k >> cb);
+        const int64_t prow = p == 0 ? -1 : (a.key[p - 1] == a.g.sentinel ? a.n_rows : (int64_t)(a.key[p - 1] >> cb));
+        if (row != prow) {
+            for (int64_t r = prow + 1; r <= row && r <= a.n_rows; ++r) {
+                a.row_ptr[r] = o;
+                if (a.sptr) a.sptr[r] = p;
+            }
+        }
+        if (keepbits >> j & 1u) {
+            a.out_col[o] = (int32_t)(k & cmask);
+            if (write_vals) a.out_val[o] = vals[j];
+            ++o;
+        }
+        if (p == Mv - 1 && row < a.n_rows) {
+            for (int64_t r = row + 1; r <= a.n_rows; ++r) {
+                a.row_ptr[r] = o;
+                if (a.sptr) a.sptr[r] = Mv;
+            }
+        }
+    }
+}
+
+// unit weights: deg_r = stream length of row r (+1 under A+I), exact
+__global__ void k_degree_stream(const int64_t *__restrict__ sptr, int64_t n, int diag,
+                                const unsigned *__restrict__ nonunit, double *__restrict__ deg,
+                                double *__restrict__ scale, int32_t *err) {
+    if (*nonunit) return;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
+        double d = (double)(sptr[r + 1] - sptr[r]) + (diag ? 1.0 : 0.0);
+        deg[r] = d;
+        if (scale) scale[r] = laplacian_scale(d, err);
+    }
+}
+
+// ---------------------------------------------------------------------------
+int degree_guarded(const int64_t *, const int32_t *, const double *, int64_t, unsigned, double *, double *,
+                   int32_t *, const unsigned *, cudaStream_t);
+
+static int bitlen(int64_t x) {
+    int b = 0;
+    while (x > 0) {
+        ++b;
+        x >>= 1;
+    }
+    return b;
+}
+
+static thread_local int t_force_buckets = 0;
+
+int set_force_buckets(int v) {
+    int old = t_force_buckets;
+    t_force_buckets = v;
+    return old;
+}
+
+bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed) {
+    if (t_force_buckets) return false;
+    const int rb = bitlen(n_rows);  // rows <= n_rows-1 < 2^rb - 1: keys stay below the sentinel
+    const int cb = bitlen(n_cols > 1 ? n_cols - 1 : 1);
+    const int64_t Mv = directed ? E : 2 * E;
+    return rb + cb <= 32 && Mv < ((int64_t)1 << 30) && n_rows > 0;
+}
+
+struct SortWs {
+    unsigned *hist, *flags, *ctr, *status, *keyA, *keyB, *payA, *payB;
+    int64_t *sptr;
+    int64_t tiles;
+};
+
+static void carve_sort(Carver &cv, SortWs &w, int64_t E, int64_t n_rows, int directed) {
+    const int64_t Mv = directed ? E : 2 * E;
+    const int64_t tiles = (Mv + kSortTile - 1) / kSortTile;
+    w.tiles = tiles;
+    w.hist = cv.take<unsigned>(4 * 256);
+    w.flags = cv.take<unsigned>(4);   // [0] nonunit [1] has_multi
+    w.ctr = cv.take<unsigned>(8);     // tile counters: passes 0..3, dedup, dedup-fix
+    w.status = cv.take<unsigned>((size_t)(tiles > 0 ? tiles : 1) * 256 * 4 + (size_t)2 * (tiles + 1));
+    const size_t m = (size_t)(Mv > 0 ? Mv : 1);
+    w.keyA = cv.take<unsigned>(m);
+    w.keyB = cv.take<unsigned>(m);
+    w.payA = cv.take<unsigned>(m);
+    w.payB = cv.take<unsigned>(m);
+    w.sptr = cv.take<int64_t>((size_t)n_rows + 1);
+}
+
+size_t sort_workspace(int64_t E, int64_t n_rows, int directed) {
+    Carver cv(nullptr);
+    SortWs w;
+    carve_sort(cv, w, E, n_rows, directed);
+    return cv.bytes();
+}
+
+// CSR build through the radix sort.  Produces a compacted CSR (row_ptr,
+// col, val) and, under deg_flags, the degrees; *val_mode (device word) is 0
+// when every stored value is exactly 1.0 and out_val was not written.
+int sort_csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, int64_t E, int64_t n_rows,
+                   int64_t n_cols, int directed, int force_vals, int64_t *row_ptr, int32_t *col, double *val,
+                   int64_t *nnz, unsigned deg_flags, double *deg, double *scale, void *ws, size_t ws_bytes,
+                   unsigned **val_mode, int32_t *err, cudaStream_t st) {
+    Carver cv(ws);
+    SortWs W;
+    carve_sort(cv, W, E, n_rows, directed);
+    if (ws_bytes < cv.bytes()) return GEE_E_WORKSPACE;
+    SortGeom g;
+    g.E = E;
+    g.Mv = directed ? E : 2 * E;
+    g.directed = directed;
+    g.colbits = bitlen(n_cols > 1 ? n_cols - 1 : 1);
+    const int keybits = bitlen(n_rows) + g.colbits;
+    g.sentinel = keybits >= 32 ? 0xffffffffu : ((1u << keybits) - 1u);
+    g.passes = (keybits + 7) / 8;
+    const int64_t tiles = W.tiles;
+    // one memset covers hist, flags, counters and every look-back word
+    size_t zero_bytes = (size_t)((char *)(W.status + (size_t)(tiles > 0 ? tiles : 1) * 256 * 4 +
+                                          (size_t)2 * (tiles + 1)) - (char *)W.hist);
+    GEE_CHECK_CUDA(cudaMemsetAsync(W.hist, 0, zero_bytes, st));
+    if (val_mode) *val_mode = W.flags;
+    if (g.Mv > 0) {
+        k_sort_hist<<<grid_for(g.Mv, kSortThreads, 4), kSortThreads, 0, st>>>(g, rows, cols, w, wt, W.hist,
+                                                                             W.flags);
+        GEE_CHECK_LAUNCH("k_sort_hist");
+        k_sort_bases<<<1, 256, 0, st>>>(W.hist, g.passes);
+        GEE_CHECK_LAUNCH("k_sort_bases");
+        unsigned *kin = nullptr, *pin = nullptr, *kout = W.keyA, *pout = W.payA;
+        for (int p = 0; p < g.passes; ++p) {
+            OnesweepArgs a;
+            a.g = g;
+            a.rows = rows;
+            a.cols = cols;
+            a.kin = kin;
+            a.pin = pin;
+            a.kout = kout;
+            a.pout = pout;
+            a.base = W.hist + p * 256;
+            a.status = W.status + (size_t)p * tiles * 256;
+            a.tile_ctr = W.ctr + p;
+            a.nonunit = W.flags;
+            a.shift = 8 * p;
+            a.first = p == 0;
+            k_onesweep<<<(unsigned)tiles, kSortThreads, 0, st>>>(a);
+            GEE_CHECK_LAUNCH("k_onesweep");
+            kin = kout;
+            pin = pout;
+            kout = (kout == W.keyA) ? W.keyB : W.keyA;
+            pout = (pout == W.payA) ? W.payB : W.payA;
+        }
+        DedupArgs d;
+        d.g = g;
+        d.key = kin;
+        d.pay = pin;
+        d.w = w;
+        d.wt = wt;
+        d.n_rows = n_rows;
+        d.out_col = col;
+        d.out_val = val;
+        d.row_ptr = row_ptr;
+        d.sptr = W.sptr;
+        d.status = W.status + (size_t)4 * tiles * 256;
+        d.tile_ctr = W.ctr + 4;
+        d.nonunit = W.flags;
+        d.has_multi = W.flags + 1;
+        d.force_vals = force_vals ? 1 : 0;
+        k_dedup<<<(unsigned)tiles, kSortThreads, 0, st>>>(d);
+        GEE_CHECK_LAUNCH("k_dedup");
+        if (!force_vals) {
+            // rare: unit weights with duplicates -> redo with values materialised
+            d.status = W.status + (size_t)4 * tiles * 256 + (tiles + 1);
+            d.tile_ctr = W.ctr + 5;
+            d.force_vals = 2;
+            k_dedup<<<(unsigned)tiles, kSortThreads, 0, st>>>(d);
+            GEE_CHECK_LAUNCH("k_dedup_fix");
+        }
+    } else {
+        GEE_CHECK_CUDA(cudaMemsetAsync(row_ptr, 0, sizeof(int64_t) * (size_t)(n_rows + 1), st));
+        GEE_CHECK_CUDA(cudaMemsetAsync(W.sptr, 0, sizeof(int64_t) * (size_t)(n_rows + 1), st));
+    }
+    if (nnz) GEE_CHECK_CUDA(cudaMemcpyAsync(nnz, row_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    if (deg_flags) {
+        const int diag = (deg_flags & GEE_DIAGONAL) ? 1 : 0;
+        double *sc = (deg_flags & GEE_LAPLACIAN) ? scale : nullptr;
+        k_degree_stream<<<grid_for(n_rows, 256, 8), 256, 0, st>>>(W.sptr, n_rows, diag, W.flags, deg, sc, err);
+        GEE_CHECK_LAUNCH("k_degree_stream");
+        int rc = degree_guarded(row_ptr, col, val, n_rows, diag ? GEE_DIAGONAL : 0u, deg, sc, err, W.flags, st);
+        if (rc) return rc;
+    }
+    return GEE_OK;
+}
+
+}  // namespace gee

@@ -18,7 +18,9 @@ size_t scan_workspace(int64_t n);
 // replays the exact sequential fold.
 __global__ void k_degree(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                          const double *__restrict__ val, int64_t n, unsigned flags,
-                         double *__restrict__ deg, double *__restrict__ scale, int32_t *err) {
+                         double *__restrict__ deg, double *__restrict__ scale, int32_t *err,
+                         const unsigned *guard) {
+    if (guard && *guard == 0) return;  // device-side skip (unit-weight graphs use k_degree_stream)
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -71,7 +73,19 @@ __global__ void k_degree(const int64_t *__restrict__ row_ptr, const int32_t *__r
 int degree(const int64_t *row_ptr, const int32_t *col, const double *val, int64_t n, unsigned flags,
            double *deg, double *scale, int32_t *err, cudaStream_t st) {
     if (n <= 0) return GEE_OK;
-    k_degree<<<grid_for(n * 32, 256, 8), 256, 0, st>>>(row_ptr, col, val, n, flags, deg, scale, err);
+    k_degree<<<grid_for(n * 32, 256, 8), 256, 0, st>>>(row_ptr, col, val, n, flags, deg, scale, err,
+                                                       nullptr);
+    GEE_CHECK_LAUNCH("k_degree");
+    return GEE_OK;
+}
+
+// degree() that runs only if the device word *guard is nonzero
+int degree_guarded(const int64_t *row_ptr, const int32_t *col, const double *val, int64_t n,
+                   unsigned flags, double *deg, double *scale, int32_t *err, const unsigned *guard,
+                   cudaStream_t st) {
+    if (n <= 0) return GEE_OK;
+    k_degree<<<grid_for(n * 32, 256, 8), 256, 0, st>>>(row_ptr, col, val, n, flags, deg, scale, err,
+                                                       guard);
     GEE_CHECK_LAUNCH("k_degree");
     return GEE_OK;
 }

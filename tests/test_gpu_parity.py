@@ -23,6 +23,23 @@ import paper_2406_03726_b200 as G  # noqa: E402
 
 RTOL = 1e-12
 CASES = load()
+PATHS = ["sort", "buckets"]
+
+
+class assembly_path:
+    """Select the CSR-assembly path: the radix sort (default when (row, col)
+    packs into 32 bits) or the row-bucket path (forced via the test hook)."""
+
+    def __init__(self, path):
+        self.force = 1 if path == "buckets" else 0
+
+    def __enter__(self):
+        from paper_2406_03726_b200 import _lib
+        self.old = _lib.load().gee_debug_set(_lib.DEBUG_FORCE_BUCKETS, self.force)
+
+    def __exit__(self, *exc):
+        from paper_2406_03726_b200 import _lib
+        _lib.load().gee_debug_set(_lib.DEBUG_FORCE_BUCKETS, self.old)
 
 
 def z_close(z, zr, rtol=RTOL):
@@ -30,7 +47,11 @@ def z_close(z, zr, rtol=RTOL):
     zr = np.asarray(zr)
     assert z.shape == zr.shape and z.dtype == np.float64
     rown = np.sqrt((zr * zr).sum(axis=1, keepdims=True)) if zr.size else zr
-    bound = rtol * np.maximum(np.abs(zr), rown)
+    # signed weights can cancel a whole row to ~0 (the reference then holds an
+    # exact 0.0 where any other summation order leaves ~1e-17): a 1e-14
+    # absolute floor, 100x tighter than the reference's own 1e-12 absolute
+    # oracle test (test_embedding.py:130)
+    bound = np.maximum(rtol * np.maximum(np.abs(zr), rown), 1e-14)
     bad = np.abs(z - zr) > bound
     assert not bad.any(), f"max |dz|={np.abs(z - zr).max():.3e} at {np.argwhere(bad)[:3]}"
 
@@ -47,8 +68,14 @@ def csr_equal(m, ref):
 
 
 # ---- reference fixtures ------------------------------------------------------
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
-def test_reference_fixture(case):
+def test_reference_fixture(case, path):
+    with assembly_path(path):
+        _reference_fixture(case)
+
+
+def _reference_fixture(case):
     n, k, directed = case["n"], case["k"], case["directed"]
     edges = G.EdgeList(n, case["rows"], case["cols"], case["w"], directed)
     labels = G.LabelVector(case["labels"], k)
@@ -167,8 +194,14 @@ def _check_against_oracle(n, rows, cols, w, labels, k, directed, combos=COMBOS):
         z_close(G.encode(csr, lab, opts), zr)
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("seed", range(6))
-def test_fuzz_small(seed):
+def test_fuzz_small(seed, path):
+    with assembly_path(path):
+        _fuzz_small(seed)
+
+
+def _fuzz_small(seed):
     rng = np.random.default_rng(1000 + seed)
     for kind in ("unit", "pos", "signed", "dyadic", "f32"):
         n = int(rng.integers(2, 400))
@@ -188,9 +221,11 @@ def test_fuzz_small(seed):
     (20_000, 100_000, 1000, "pos", False, (3, 0.2)),  # K=1000 shared-memory path + long row
     (5_000, 40_000, 2500, "unit", True, None),     # K > tile: tiled correlation
 ])
-def test_tiers(n, m, k, kind, directed, hub):
+@pytest.mark.parametrize("path", PATHS)
+def test_tiers(n, m, k, kind, directed, hub, path):
     rng = np.random.default_rng(n + m + k)
-    _check_against_oracle(n, *_graph(rng, n, m, kind, directed, k, dup_runs=True, hub=hub), k,
+    with assembly_path(path):
+        _check_against_oracle(n, *_graph(rng, n, m, kind, directed, k, dup_runs=True, hub=hub), k,
                           directed, combos=[(0, 0, 0), (1, 1, 1), (1, 0, 1), (0, 1, 0)])
 
 
@@ -198,11 +233,14 @@ def test_runs_of_duplicates_in_stream_order():
     # 5 identical coordinates whose sum depends on the order (non-associative)
     vals = [1e16, 1.0, -1e16, 1.0, 3.0]
     n = 20000  # large n -> tiers S/B path; repeated below with small n -> tier D
-    for n in (20000, 50):
-        rows = np.array([3] * 5 + [3] * 40, np.int64)
-        cols = np.array([7] * 5 + list(range(10, 50)), np.int64)
-        w = np.array(vals + [0.5] * 40)
-        _check_against_oracle(n, rows, cols, w, np.zeros(n, np.int64), 1, True)
+    for path in PATHS:
+        for n in (20000, 50):
+            rows = np.array([3] * 5 + [3] * 40, np.int64)
+            cols = np.array([7] * 5 + list(range(10, 50)), np.int64)
+            w = np.array(vals + [0.5] * 40)
+            with assembly_path(path):
+                _check_against_oracle(n, rows, cols, w, np.zeros(n, np.int64), 1, True)
+                _check_against_oracle(n, cols, rows, w, np.zeros(n, np.int64), 1, False)
 
 
 def test_weighted_long_rows_exact_degree_fold():
@@ -212,8 +250,35 @@ def test_weighted_long_rows_exact_degree_fold():
     rows = np.concatenate([np.full(9000, 11), rng.integers(0, n, 60000)])
     cols = rng.integers(0, n, rows.size)
     w = rng.random(rows.size) * 1e3 + 1e-9
-    _check_against_oracle(n, rows, cols, w, rng.integers(0, 4, n), 4, False,
-                          combos=[(1, 1, 1), (1, 0, 0)])
+    for path in PATHS:
+        with assembly_path(path):
+            _check_against_oracle(n, rows, cols, w, rng.integers(0, 4, n), 4, False,
+                                  combos=[(1, 1, 1), (1, 0, 0)])
+
+
+def test_large_n_multigraph_default_path():
+    # n > 65535: (row, col) no longer packs into 32 bits -> bucket path by default
+    rng = np.random.default_rng(77)
+    n = 100_000
+    rows = np.concatenate([np.full(6000, 4242), rng.integers(0, n, 300_000)])
+    cols = rng.integers(0, n, rows.size)
+    rows[:300] = 17
+    cols[:300] = 23  # a 300-long duplicate run (stream-order sum)
+    w = 1.0 - rng.random(rows.size)
+    _check_against_oracle(n, rows, cols, w, rng.integers(-1, 7, n), 7, False,
+                          combos=[(1, 1, 1), (0, 0, 0)])
+
+
+def test_unit_weights_with_duplicates():
+    # unit weights + duplicate coordinates: the sort path must materialise values
+    rng = np.random.default_rng(3)
+    n = 500
+    rows = rng.integers(0, n, 20_000)
+    cols = rng.integers(0, n, 20_000)
+    for path in PATHS:
+        with assembly_path(path):
+            _check_against_oracle(n, rows, cols, np.ones(rows.size), rng.integers(0, 3, n), 3, False,
+                                  combos=[(1, 1, 1), (0, 0, 0), (1, 0, 0)])
 
 
 # ---- configs -----------------------------------------------------------------
@@ -264,3 +329,6 @@ def test_encoder_plan_and_launch_count():
     assert torch.equal(z1, z2)  # deterministic
     st, zr, _ = O.encode_edges(c["rows"], c["cols"], c["weights"], c["n"], False, c["labels"], 3, 7)
     z_close(z1.cpu().numpy(), zr)
+    # the unit-weight sort path never reads a value array: same Z with weights=None
+    z3 = enc.run(rows, cols, None, lab)
+    z_close(z3.cpu().numpy(), zr)
