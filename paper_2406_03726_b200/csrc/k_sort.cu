@@ -85,28 +85,44 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(SortGeom g, const in
     __syncthreads();
     const int lane = threadIdx.x & 31;
     bool bad_w = false;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t v_round = (g.Mv + 31) & ~int64_t(31);
-    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < v_round; v += stride) {
-        const bool valid = v < g.Mv;
-        unsigned pay, key = 0;
-        if (valid) {
-            key = sort_key(g, rows, cols, v, pay);
-            if (wt != GEE_W_UNIT && (g.directed || !(v & 1))) bad_w |= sort_load_w(w, wt, v >> (g.directed ? 0 : 1)) != 1.0;
+    constexpr int U = 4;  // edges per thread per iteration: all loads issued before use
+    const int64_t E = g.E;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
+    const int64_t e_round = (E + 31) & ~int64_t(31);
+    for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x * U + threadIdx.x; e0 < e_round; e0 += stride) {
+        int64_t r[U], c[U];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t e = e0 + (int64_t)u * blockDim.x;
+            ok[u] = e < E;
+            r[u] = ok[u] ? rows[e] : 0;
+            c[u] = ok[u] ? cols[e] : 0;
+            if (ok[u] && wt != GEE_W_UNIT) bad_w |= sort_load_w(w, wt, e) != 1.0;
         }
-        // valid lanes form a prefix of the warp (v grows with the lane id)
-        const int nv = __popc(__ballot_sync(0xffffffffu, valid));
-        for (int p = 0; p < g.passes; ++p) {
-            const unsigned d = (key >> (8 * p)) & 255u;
-            // run-length aggregation across the warp: rows arrive in runs, so
-            // the high digits repeat and one atomic per run replaces 32
-            const unsigned prev = __shfl_up_sync(0xffffffffu, d, 1);
-            const bool head = valid && (lane == 0 || prev != d);
-            const unsigned heads = __ballot_sync(0xffffffffu, head);
-            if (head) {
-                const unsigned after = heads & ~((2u << lane) - 1u);
-                const int next = after ? __ffs(after) - 1 : nv;
-                atomicAdd(&sh[p][d], (unsigned)(next - lane));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            // valid lanes form a prefix of the warp (e grows with the lane id)
+            const int nv = __popc(__ballot_sync(0xffffffffu, ok[u]));
+            for (int half = 0; half < (g.directed ? 1 : 2); ++half) {
+                unsigned key;
+                if (half == 0)
+                    key = ((unsigned)r[u] << g.colbits) | (unsigned)c[u];
+                else
+                    key = r[u] == c[u] ? g.sentinel : (((unsigned)c[u] << g.colbits) | (unsigned)r[u]);
+                for (int p = 0; p < g.passes; ++p) {
+                    const unsigned d = (key >> (8 * p)) & 255u;
+                    // run-length aggregation across the warp: edges arrive in
+                    // row runs, so high digits repeat; one atomic per run
+                    const unsigned prev = __shfl_up_sync(0xffffffffu, d, 1);
+                    const bool head = ok[u] && (lane == 0 || prev != d);
+                    const unsigned heads = __ballot_sync(0xffffffffu, head);
+                    if (head) {
+                        const unsigned after = heads & ~((2u << lane) - 1u);
+                        const int next = after ? __ffs(after) - 1 : nv;
+                        atomicAdd(&sh[p][d], (unsigned)(next - lane));
+                    }
+                }
             }
         }
     }
@@ -143,7 +159,39 @@ struct OnesweepArgs {
     int first;
 };
 
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(OnesweepArgs a) {
+// Exclusive prefix of digit `d` over tiles [0, tile): each thread walks back
+// through its digit's look-back words kLookback tiles at a time (all loads
+// of a window in flight together), stopping at the nearest inclusive word.
+constexpr int kLookback = 16;
+
+__device__ __forceinline__ unsigned lookback_digit(const unsigned *status, int64_t tile, int d) {
+    unsigned excl = 0;
+    int64_t t = tile - 1;
+    while (t >= 0) {
+        const int nw = (int)min((int64_t)kLookback, t + 1);
+        unsigned s[kLookback];
+#pragma unroll
+        for (int j = 0; j < kLookback; ++j)
+            s[j] = j < nw ? ld_acquire(status + (size_t)(t - j) * 256 + d) : kFlagInc;
+        // words not yet published (flag 0) are re-read until they are
+#pragma unroll
+        for (int j = 0; j < kLookback; ++j)
+            while ((s[j] & ~kValMask) == 0) s[j] = ld_acquire(status + (size_t)(t - j) * 256 + d);
+        bool done = false;
+#pragma unroll
+        for (int j = 0; j < kLookback; ++j) {
+            if (!done && j < nw) {
+                excl += s[j] & kValMask;
+                done = (s[j] & kFlagInc) != 0;
+            }
+        }
+        if (done) break;
+        t -= nw;
+    }
+    return excl;
+}
+
+__global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(OnesweepArgs a) {
     __shared__ unsigned sk[kSortTile];
     __shared__ unsigned sp[kSortTile];
     __shared__ unsigned whist[kSortWarps][256];
@@ -151,30 +199,25 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(OnesweepArgs a) {
     __shared__ unsigned red[33];
     __shared__ int s_tile;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const bool carry = *a.nonunit != 0;
     if (threadIdx.x == 0) s_tile = (int)atomicAdd(a.tile_ctr, 1u);
     for (int i = threadIdx.x; i < kSortWarps * 256; i += kSortThreads) (&whist[0][0])[i] = 0;
     __syncthreads();
     const int64_t tile = s_tile;
     const int64_t t0 = tile * kSortTile;
     const int nvalid = (int)min((int64_t)kSortTile, a.g.Mv - t0);
-    unsigned key[kSortItems], pay[kSortItems], rank[kSortItems];
+    unsigned key[kSortItems], rank[kSortItems];
     // load: warp w owns items [w*512, w*512+512) in 16 rounds of 32
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const int i = wid * (kSortTile / kSortWarps) + j * 32 + lane;
-        pay[j] = 0;
         if (i < nvalid) {
-            if (a.first) {
-                key[j] = sort_key(a.g, a.rows, a.cols, t0 + i, pay[j]);
-            } else {
-                key[j] = a.kin[t0 + i];
-                if (carry) pay[j] = a.pin[t0 + i];
-            }
+            unsigned pay_unused;
+            key[j] = a.first ? sort_key(a.g, a.rows, a.cols, t0 + i, pay_unused) : a.kin[t0 + i];
         } else {
             key[j] = 0;
         }
     }
+    const bool carry = *a.nonunit != 0;  // read after the key loads are in flight
     // stable warp multisplit
     unsigned *wh = whist[wid];
 #pragma unroll
@@ -211,21 +254,14 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(OnesweepArgs a) {
         st_release(st, kFlagInc | tot);
     } else {
         st_release(st, kFlagAgg | tot);
-        for (int64_t t = tile - 1; t >= 0; --t) {
-            const unsigned *ps = a.status + (size_t)t * 256 + d;
-            unsigned s;
-            do {
-                s = ld_acquire(ps);
-            } while ((s & ~kValMask) == 0);
-            excl += s & kValMask;
-            if (s & kFlagInc) break;
-        }
+        excl = lookback_digit(a.status, tile, d);
         st_release(st, kFlagInc | (excl + tot));
     }
     gbase[d] = a.base[d] + excl;
     tstart[d] = block_exclusive_scan(tot, red, nullptr);
     __syncthreads();
-    // reorder the tile by digit in shared memory
+    // reorder the tile by digit in shared memory (payloads are fetched here,
+    // only when they exist, instead of occupying registers through the rank)
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const int i = wid * (kSortTile / kSortWarps) + j * 32 + lane;
@@ -233,7 +269,14 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(OnesweepArgs a) {
             const unsigned dd = (key[j] >> a.shift) & 255u;
             const unsigned pos = tstart[dd] + whist[wid][dd] + rank[j];
             sk[pos] = key[j];
-            sp[pos] = pay[j];
+            if (carry) {
+                unsigned pay = 0;
+                if (a.first)
+                    sort_key(a.g, a.rows, a.cols, t0 + i, pay);
+                else
+                    pay = a.pin[t0 + i];
+                sp[pos] = pay;
+            }
         }
     }
     __syncthreads();
@@ -356,25 +399,36 @@ __global__ void __launch_bounds__(kSortThreads) k_dedup(DedupArgs a) {
     if (multi) atomicOr(a.has_multi, 1u);
     unsigned cnt = __popc(keepbits), ttot;
     unsigned off = block_exclusive_scan(cnt, red, &ttot);
-    // look-back for the tile's output offset
-    if (threadIdx.x == 0) {
+    // look-back for the tile's output offset: warp 0 inspects 32 predecessor
+    // tiles per step (lane l reads tile t-1-l)
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
         unsigned *st = a.status + tile;
         unsigned excl = 0;
         if (tile == 0) {
-            st_release(st, kFlagInc | ttot);
+            if (lane == 0) st_release(st, kFlagInc | ttot);
         } else {
-            st_release(st, kFlagAgg | ttot);
-            for (int64_t t = tile - 1; t >= 0; --t) {
-                unsigned s;
-                do {
-                    s = ld_acquire(a.status + t);
-                } while ((s & ~kValMask) == 0);
-                excl += s & kValMask;
-                if (s & kFlagInc) break;
+            if (lane == 0) st_release(st, kFlagAgg | ttot);
+            int64_t t = tile - 1;
+            while (t >= 0) {
+                const int64_t mine = t - lane;
+                unsigned s = kFlagInc;  // lanes past tile 0 act as an inclusive zero
+                if (mine >= 0) {
+                    do {
+                        s = ld_acquire(a.status + mine);
+                    } while ((s & ~kValMask) == 0);
+                }
+                const unsigned inc = __ballot_sync(0xffffffffu, (s & kFlagInc) != 0);
+                const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive word
+                unsigned v = lane <= stop ? (s & kValMask) : 0u;
+                v = warp_sum_u(v);
+                excl += v;
+                if (inc) break;
+                t -= 32;
             }
-            st_release(st, kFlagInc | (excl + ttot));
+            if (lane == 0) st_release(st, kFlagInc | (excl + ttot));
         }
-        s_excl = excl;
+        if (lane == 0) s_excl = excl;
     }
     __syncthreads();
     int64_t o = (int64_t)s_excl + off;
