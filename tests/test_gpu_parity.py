@@ -44,17 +44,20 @@ class assembly_path:
 
 def z_close(z, zr, rtol=RTOL, zr_pre=None):
     """Compare Z with the reference.  `zr_pre` is the reference's Z before
-    correlation: a row the reference sums to exactly 0.0 through cancelling
-    signed terms is numerically zero -- any summation order other than its
-    left fold leaves ~1e-17 there, which correlate_rows then scales to a unit
-    row (the reference's own encode_reference disagrees with encode the same
-    way, e.g. fixture triple_dup).  Such rows are checked before
-    normalisation (must be ~0, see encode_pre) and skipped after it."""
+    correlation: a row whose terms cancel to within rounding (norm below
+    1e-12 of the matrix scale) is numerically zero -- the reference's left
+    fold leaves exactly 0.0 or some ~1e-17 there, any other order leaves a
+    different ~1e-17, and correlate_rows scales that to a unit row (the
+    reference's own encode_reference disagrees with encode the same way,
+    e.g. fixture triple_dup).  Those rows are compared before normalisation
+    (the same combo without correlation is checked too) and skipped after."""
     z = np.asarray(z)
     zr = np.asarray(zr)
     assert z.shape == zr.shape and z.dtype == np.float64
     if zr_pre is not None and zr.size:
-        live = np.abs(np.asarray(zr_pre)).sum(axis=1) != 0.0
+        zp = np.asarray(zr_pre)
+        scale = max(1.0, float(np.abs(zp).max()))
+        live = np.sqrt((zp * zp).sum(axis=1)) > 1e-12 * scale
         z, zr = z[live], zr[live]
     rown = np.sqrt((zr * zr).sum(axis=1, keepdims=True)) if zr.size else zr
     # signed weights can cancel a whole row to ~0 (the reference then holds an
