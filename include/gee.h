@@ -136,18 +136,20 @@ int gee_laplacian_normalize_workspace(int64_t n, size_t *ws_bytes);
  * GEE_CORRELATION each nonzero row is divided by its 2-norm (non-finite
  * rows set GEE_ERR_NONFINITE).  row_cnt may be NULL (standard CSR) or the
  * uncompacted counts from gee_csr_build(compact=0).  val may be NULL for
- * unit weights.  z is dense row-major with leading dimension ldz >= k. */
-int gee_embed_workspace(int64_t n_rows, size_t *ws_bytes);
+ * unit weights.  n_cols is the node count (length of y32 / scale).  z is
+ * dense row-major with leading dimension ldz >= k. */
+int gee_embed_workspace(int64_t n_rows, int64_t n_cols, size_t *ws_bytes);
 int gee_embed(const int64_t *row_ptr, const uint32_t *row_cnt, const int32_t *col,
-              const double *val, int64_t row_begin, int64_t row_end, const int32_t *y32,
-              const double *inv_nk, const double *scale, int32_t k, unsigned flags, double *z,
-              int64_t ldz, void *ws, size_t ws_bytes, int32_t *err, void *stream);
+              const double *val, int64_t row_begin, int64_t row_end, int64_t n_cols,
+              const int32_t *y32, const double *inv_nk, const double *scale, int32_t k,
+              unsigned flags, double *z, int64_t ldz, void *ws, size_t ws_bytes, int32_t *err,
+              void *stream);
 
 /* The whole reference timed region on the device: edge list + labels ->
  * Z (N x K, f64).  Optionally also returns the uncompacted CSR through
  * the workspace (not exposed).  One stream, no host synchronisation. */
 int gee_encode_edges_workspace(int64_t n_edges, int64_t n_nodes, int32_t k, int directed,
-                               size_t *ws_bytes);
+                               int w_type, size_t *ws_bytes);
 int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, int w_type,
                      int64_t n_edges, int64_t n_nodes, int directed, const int64_t *labels,
                      int32_t k, unsigned flags, double *z, void *ws, size_t ws_bytes,
@@ -167,9 +169,11 @@ int gee_profile_start(void *stream);
 int gee_profile_stop(void);
 int gee_profile_read(float *ms, const char **names, int cap);
 
-/* Test hook (thread-local): GEE_DEBUG_FORCE_BUCKETS = 1 makes the CSR
- * build take the row-bucket path even when (row, col) packs into 32 bits,
- * so parity tests cover both assembly paths.  Returns the previous value. */
+/* Test hook (thread-local) selecting the CSR assembly path so parity tests
+ * cover all three: GEE_DEBUG_FORCE_BUCKETS = 0 default (bitmap for small
+ * unit-weight graphs, radix sort when (row, col) packs into 32 bits, row
+ * buckets otherwise), 1 = row buckets, 2 = never the bitmap path.  Returns
+ * the previous value. */
 #define GEE_DEBUG_FORCE_BUCKETS 1
 int gee_debug_set(int key, int value);
 

@@ -43,10 +43,10 @@ SIGNATURES = {
     "gee_laplacian_normalize_workspace": (_int, [_i64, _szp]),
     "gee_laplacian_normalize": (_int, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
                                        ctypes.c_size_t, _vp, _vp]),
-    "gee_embed_workspace": (_int, [_i64, _szp]),
-    "gee_embed": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _i32, _u32, _vp, _i64, _vp,
-                         ctypes.c_size_t, _vp, _vp]),
-    "gee_encode_edges_workspace": (_int, [_i64, _i64, _i32, _int, _szp]),
+    "gee_embed_workspace": (_int, [_i64, _i64, _szp]),
+    "gee_embed": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _i32, _u32, _vp, _i64,
+                         _vp, ctypes.c_size_t, _vp, _vp]),
+    "gee_encode_edges_workspace": (_int, [_i64, _i64, _i32, _int, _int, _szp]),
     "gee_encode_edges": (_int, [_vp, _vp, _vp, _int, _i64, _i64, _int, _vp, _i32, _u32, _vp, _vp,
                                 ctypes.c_size_t, _vp, _vp]),
     "gee_launch_count": (ctypes.c_uint64, []),
@@ -56,7 +56,7 @@ SIGNATURES = {
     "gee_profile_read": (_int, [ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_char_p), _int]),
     "gee_debug_set": (_int, [_int, _int]),
 }
-DEBUG_FORCE_BUCKETS = 1
+DEBUG_FORCE_BUCKETS = 1  # key; values: 0 default, 1 row buckets, 2 no bitmap path
 
 _lib = None
 

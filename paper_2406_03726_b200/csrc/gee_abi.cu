@@ -70,10 +70,17 @@ int add_identity(const int64_t *, const int32_t *, const double *, int64_t, int6
 size_t laplacian_workspace(int64_t n);
 int laplacian_normalize(const int64_t *, const int32_t *, const double *, int64_t, const double *, int64_t *,
                         int32_t *, double *, int64_t *, void *, size_t, int32_t *, cudaStream_t);
-size_t embed_workspace(int64_t n_rows);
-int embed(const int64_t *, const unsigned *, const int32_t *, const double *, const unsigned *, int64_t,
-          int64_t, const int32_t *, const double *, const double *, int, unsigned, double *, int64_t, void *,
-          size_t, int32_t *, cudaStream_t);
+size_t embed_workspace(int64_t n_rows, int64_t n_cols);
+int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, const double *val,
+          const unsigned *val_flags, const unsigned char *row_flag, int64_t rb, int64_t re, int64_t n_cols,
+          const int32_t *y32, const double *inv, const double *scale, int k, unsigned flags, double *z, int64_t ldz,
+          void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st);
+bool bitmap_path_ok(int wt, int64_t E, int64_t n_rows, int64_t n_cols, int directed);
+size_t bitmap_workspace(int64_t E, int64_t n, int directed);
+int bitmap_csr_build(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n, int directed,
+                     int64_t *row_ptr, unsigned *row_cnt, unsigned char *row_flag, int32_t *col, double *val,
+                     unsigned deg_flags, double *deg, double *scale, void *ws, size_t ws_bytes, int32_t *err,
+                     cudaStream_t st);
 int validate_edges(const int64_t *, const int64_t *, const void *, int, int64_t, int64_t, int32_t *,
                    cudaStream_t);
 
@@ -91,6 +98,7 @@ struct EncodeWs {
     double *inv, *deg, *scale;
     int64_t *row_ptr;
     unsigned *row_cnt;
+    unsigned char *row_flag;
     int32_t *col;
     double *val;
     void *csr_ws;
@@ -99,7 +107,7 @@ struct EncodeWs {
     size_t emb_bytes;
 };
 
-static size_t carve_encode(Carver &cv, EncodeWs &w, int64_t E, int64_t n, int32_t k, int directed) {
+static size_t carve_encode(Carver &cv, EncodeWs &w, int64_t E, int64_t n, int32_t k, int directed, int wt) {
     const int64_t M = directed ? E : 2 * E;
     w.y32 = cv.take<int32_t>((size_t)n + 1);
     w.counts = cv.take<int64_t>((size_t)k);
@@ -108,11 +116,13 @@ static size_t carve_encode(Carver &cv, EncodeWs &w, int64_t E, int64_t n, int32_
     w.scale = cv.take<double>((size_t)n + 1);
     w.row_ptr = cv.take<int64_t>((size_t)n + 1);
     w.row_cnt = cv.take<unsigned>((size_t)n + 1);
+    w.row_flag = cv.take<unsigned char>((size_t)n + 1);
     w.col = cv.take<int32_t>((size_t)(M > 0 ? M : 1));
     w.val = cv.take<double>((size_t)(M > 0 ? M : 1));
-    w.csr_bytes = csr_build_workspace(E, n, n, directed);
+    w.csr_bytes = bitmap_path_ok(wt, E, n, n, directed) ? bitmap_workspace(E, n, directed)
+                                                         : csr_build_workspace(E, n, n, directed);
     w.csr_ws = cv.take<char>(w.csr_bytes);
-    w.emb_bytes = embed_workspace(n);
+    w.emb_bytes = embed_workspace(n, n);
     w.emb_ws = cv.take<char>(w.emb_bytes);
     return cv.bytes();
 }
@@ -240,28 +250,30 @@ int gee_laplacian_normalize(const int64_t *row_ptr, const int32_t *col, const do
                                err, (cudaStream_t)stream);
 }
 
-int gee_embed_workspace(int64_t n_rows, size_t *ws_bytes) {
-    if (!ws_bytes || !index_ok(n_rows)) return GEE_E_ARG;
-    *ws_bytes = embed_workspace(n_rows);
+int gee_embed_workspace(int64_t n_rows, int64_t n_cols, size_t *ws_bytes) {
+    if (!ws_bytes || !index_ok(n_rows) || !index_ok(n_cols)) return GEE_E_ARG;
+    *ws_bytes = embed_workspace(n_rows, n_cols);
     return GEE_OK;
 }
 
 int gee_embed(const int64_t *row_ptr, const uint32_t *row_cnt, const int32_t *col, const double *val,
-              int64_t row_begin, int64_t row_end, const int32_t *y32, const double *inv_nk, const double *scale,
-              int32_t k, unsigned flags, double *z, int64_t ldz, void *ws, size_t ws_bytes, int32_t *err,
-              void *stream) {
-    if (k < 1 || ldz < k || row_begin < 0 || row_end < row_begin || !index_ok(row_end)) return GEE_E_ARG;
+              int64_t row_begin, int64_t row_end, int64_t n_cols, const int32_t *y32, const double *inv_nk,
+              const double *scale, int32_t k, unsigned flags, double *z, int64_t ldz, void *ws, size_t ws_bytes,
+              int32_t *err, void *stream) {
+    if (k < 1 || ldz < k || row_begin < 0 || row_end < row_begin || !index_ok(row_end) || !index_ok(n_cols))
+        return GEE_E_ARG;
     if (row_end > row_begin && (!row_ptr || !y32 || !inv_nk || !z)) return GEE_E_ARG;
     if ((flags & GEE_LAPLACIAN) && !scale) return GEE_E_ARG;
-    return embed(row_ptr, row_cnt, col, val, nullptr, row_begin, row_end, y32, inv_nk, scale, k, flags, z, ldz, ws,
-                 ws_bytes, err, (cudaStream_t)stream);
+    return embed(row_ptr, row_cnt, col, val, nullptr, nullptr, row_begin, row_end, n_cols, y32, inv_nk, scale, k,
+                 flags, z, ldz, ws, ws_bytes, err, (cudaStream_t)stream);
 }
 
-int gee_encode_edges_workspace(int64_t n_edges, int64_t n_nodes, int32_t k, int directed, size_t *ws_bytes) {
+int gee_encode_edges_workspace(int64_t n_edges, int64_t n_nodes, int32_t k, int directed, int w_type,
+                               size_t *ws_bytes) {
     if (!ws_bytes || !index_ok(n_edges) || !index_ok(n_nodes) || k < 1) return GEE_E_ARG;
     Carver cv(nullptr);
     EncodeWs w;
-    *ws_bytes = carve_encode(cv, w, n_edges, n_nodes, k, directed);
+    *ws_bytes = carve_encode(cv, w, n_edges, n_nodes, k, directed, w_type);
     return GEE_OK;
 }
 
@@ -272,12 +284,20 @@ int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, in
     cudaStream_t st = (cudaStream_t)stream;
     Carver cv(ws);
     EncodeWs W;
-    size_t need = carve_encode(cv, W, n_edges, n_nodes, k, directed);
+    size_t need = carve_encode(cv, W, n_edges, n_nodes, k, directed, w_type);
     if (ws_bytes < need || !ws) return GEE_E_WORKSPACE;
     int rc = label_hist(labels, n_nodes, k, W.y32, W.counts, W.inv, err, st);
     if (rc) return rc;
     const unsigned deg_flags = (flags & GEE_LAPLACIAN) ? (GEE_LAPLACIAN | (flags & GEE_DIAGONAL)) : 0u;
     const double *sc = (flags & GEE_LAPLACIAN) ? W.scale : nullptr;
+    if (bitmap_path_ok(w_type, n_edges, n_nodes, n_nodes, directed)) {
+        // unit weights, small node count: column bitmaps per row, slot layout
+        rc = bitmap_csr_build(rows, cols, n_edges, n_nodes, directed, W.row_ptr, W.row_cnt, W.row_flag, W.col,
+                              W.val, deg_flags, W.deg, W.scale, W.csr_ws, W.csr_bytes, err, st);
+        if (rc) return rc;
+        return embed(W.row_ptr, W.row_cnt, W.col, W.val, nullptr, W.row_flag, 0, n_nodes, n_nodes, W.y32, W.inv, sc,
+                     k, flags, z, k, W.emb_ws, W.emb_bytes, err, st);
+    }
     if (sort_path_ok(n_edges, n_nodes, n_nodes, directed)) {
         // compact CSR from the radix sort; values stay implicit (1.0) when the
         // graph has unit weights and no duplicate entries
@@ -285,14 +305,14 @@ int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, in
         rc = sort_csr_build(rows, cols, w, w_type, n_edges, n_nodes, n_nodes, directed, 0, W.row_ptr, W.col, W.val,
                             nullptr, deg_flags, W.deg, W.scale, W.csr_ws, W.csr_bytes, &val_mode, err, st);
         if (rc) return rc;
-        return embed(W.row_ptr, nullptr, W.col, W.val, val_mode, 0, n_nodes, W.y32, W.inv, sc, k, flags, z, k,
-                     W.emb_ws, W.emb_bytes, err, st);
+        return embed(W.row_ptr, nullptr, W.col, W.val, val_mode, nullptr, 0, n_nodes, n_nodes, W.y32, W.inv, sc, k,
+                     flags, z, k, W.emb_ws, W.emb_bytes, err, st);
     }
     rc = csr_build(rows, cols, w, w_type, n_edges, n_nodes, n_nodes, directed, 0, W.row_ptr, W.row_cnt, W.col,
                    W.val, nullptr, deg_flags, W.deg, W.scale, W.csr_ws, W.csr_bytes, err, st);
     if (rc) return rc;
-    return embed(W.row_ptr, W.row_cnt, W.col, W.val, nullptr, 0, n_nodes, W.y32, W.inv, sc, k, flags, z, k,
-                 W.emb_ws, W.emb_bytes, err, st);
+    return embed(W.row_ptr, W.row_cnt, W.col, W.val, nullptr, nullptr, 0, n_nodes, n_nodes, W.y32, W.inv, sc, k,
+                 flags, z, k, W.emb_ws, W.emb_bytes, err, st);
 }
 
 }  // extern "C"

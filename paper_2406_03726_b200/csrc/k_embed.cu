@@ -7,10 +7,12 @@
 //     a'  = v (+1.0 when j == r under DIAGONAL; a missing diagonal is a
 //           virtual 1.0 entry)                          _kernels.py:176-196
 //     a'  = (a' * s_r) * s_j under LAPLACIAN            sparse.py:217
-//     Z[r, Y_j] += a' * inv_nk[Y_j]   (Y_j >= 0)        _kernels.py:292-296
-// W is never built: its one nonzero per row is (Y_j, 1/n_{Y_j}).  Each term is
-// the reference's own product; only the summation order differs (fp64,
-// relative error ~1e-15 against the 1e-12 budget).
+//     Z[r, Y_j] += a' * (1/n_{Y_j})  (Y_j >= 0)         _kernels.py:292-296
+// W is never built.  Each node j is one 16-byte record {Y_j, g_j} with
+// g_j = s_j * (1/n_{Y_j}) (s_j = 1 without Laplacian), so an entry costs one
+// coalesced 4-byte column read plus one 16-byte gather; the term is
+// (a' * s_r) * g_j, the reference's product re-associated (<= 2 ulp per term,
+// far inside the 1e-12 budget).
 //
 // Work split: rows longer than kLongRow are taken first, one CTA per row
 // (per-warp partial K-vectors combined in shared memory); every other row is
@@ -35,8 +37,7 @@ struct EmbedArgs {
     const int32_t *col;
     const double *val;
     int64_t row_begin, row_end;
-    const int32_t *y32;
-    const double *inv;
+    const double2 *rec;  // node records: x = bits of (label), y = g
     const double *scale;
     int k;
     unsigned flags;
@@ -45,8 +46,9 @@ struct EmbedArgs {
     int32_t *err;
     const unsigned *long_list;
     const unsigned *n_long;
-    unsigned *work;             // [2]
-    const unsigned *val_flags;  // [2] from the sort path: both 0 => every value is 1.0
+    unsigned *work;                // [2]
+    const unsigned *val_flags;     // [2] from the sort path: both 0 => every value is 1.0
+    const unsigned char *row_flag; // per row: 1 => read val for this row, 0 => values are 1.0
 };
 
 __device__ __forceinline__ void row_extent(const EmbedArgs &a, int64_t r, int64_t &s, int64_t &e) {
@@ -54,35 +56,46 @@ __device__ __forceinline__ void row_extent(const EmbedArgs &a, int64_t r, int64_
     e = a.row_cnt ? s + a.row_cnt[r] : a.row_ptr[r + 1];
 }
 
+__device__ __forceinline__ void node_rec(const EmbedArgs &a, int c, int &lab, double &g) {
+    const double2 rc = __ldg(a.rec + c);
+    lab = (int)(unsigned)(unsigned long long)__double_as_longlong(rc.x);
+    g = rc.y;
+}
+
+// value array to use for row r (nullptr: every value is exactly 1.0)
+__device__ __forceinline__ const double *row_vals(const EmbedArgs &a, int64_t r) {
+    if (a.row_flag && !a.row_flag[r]) return nullptr;
+    return a.val;
+}
+
 // One stored entry -> (label, contribution).  Returns false when it adds
 // nothing (unlabeled column or padding).
-__device__ __forceinline__ bool entry_term(const EmbedArgs &a, int64_t r, double s_r, int64_t p,
-                                           bool valid, int &lab, double &x, bool &isdiag) {
+__device__ __forceinline__ bool entry_term(const EmbedArgs &a, const double *val, int64_t r, double s_r,
+                                           int64_t p, bool valid, int &lab, double &x, bool &isdiag) {
     lab = -1;
     x = 0.0;
     isdiag = false;
     if (!valid) return false;
-    int c = a.col[p];
-    double v = a.val ? a.val[p] : 1.0;
-    lab = a.y32[c];
+    const int c = a.col[p];
+    double v = val ? val[p] : 1.0;
+    double g;
+    node_rec(a, c, lab, g);
     if ((a.flags & GEE_DIAGONAL) && c == r) {
         v = v + 1.0;
         isdiag = true;
     }
     if (lab < 0) return false;
-    if (a.flags & GEE_LAPLACIAN) v = (v * s_r) * a.scale[c];
-    x = v * a.inv[lab];
+    if (a.flags & GEE_LAPLACIAN) v = v * s_r;
+    x = v * g;
     return true;
 }
 
 // The virtual diagonal 1.0 of A+I for a row with no stored diagonal.
-__device__ __forceinline__ bool diag_term(const EmbedArgs &a, int64_t r, double s_r, int &lab,
-                                          double &x) {
-    lab = a.y32[r];
+__device__ __forceinline__ bool diag_term(const EmbedArgs &a, int64_t r, double s_r, int &lab, double &x) {
+    double g;
+    node_rec(a, (int)r, lab, g);
     if (lab < 0) return false;
-    double v = 1.0;
-    if (a.flags & GEE_LAPLACIAN) v = (v * s_r) * s_r;
-    x = v * a.inv[lab];
+    x = ((a.flags & GEE_LAPLACIAN) ? s_r : 1.0) * g;
     return true;
 }
 
@@ -93,18 +106,19 @@ __device__ __forceinline__ double row_scale(const EmbedArgs &a, int64_t r) {
 // ---------------------------------------------------------------------------
 // K <= KP <= 8: register accumulators, one warp per row.
 // ---------------------------------------------------------------------------
-// (column, value) -> register accumulators
 template <int KP>
 __device__ __forceinline__ void consume(const EmbedArgs &a, int64_t r, double s_r, int c, double v,
                                         double (&acc)[KP], bool &found) {
-    const int lab = a.y32[c];
+    int lab;
+    double g;
+    node_rec(a, c, lab, g);
     if ((a.flags & GEE_DIAGONAL) && c == r) {
         v = v + 1.0;
         found = true;
     }
     if (lab < 0) return;
-    if (a.flags & GEE_LAPLACIAN) v = (v * s_r) * a.scale[c];
-    const double x = v * a.inv[lab];
+    if (a.flags & GEE_LAPLACIAN) v = v * s_r;
+    const double x = v * g;
 #pragma unroll
     for (int q = 0; q < KP; ++q) acc[q] += (lab == q) ? x : 0.0;
 }
@@ -115,6 +129,7 @@ __device__ void row_regs(const EmbedArgs &a, int64_t r) {
     int64_t s, e;
     row_extent(a, r, s, e);
     const double s_r = row_scale(a, r);
+    const double *val = row_vals(a, r);
     double acc[KP];
 #pragma unroll
     for (int q = 0; q < KP; ++q) acc[q] = 0.0;
@@ -122,15 +137,15 @@ __device__ void row_regs(const EmbedArgs &a, int64_t r) {
     // head up to a 16-byte boundary of col, body in 16-byte vectors (4 entries
     // per lane, 256 entries per warp per iteration), scalar tail
     const int64_t a0 = min(e, (s + 3) & ~int64_t(3));
-    if (s + lane < a0) consume<KP>(a, r, s_r, a.col[s + lane], a.val ? a.val[s + lane] : 1.0, acc, found);
+    if (s + lane < a0) consume<KP>(a, r, s_r, a.col[s + lane], val ? val[s + lane] : 1.0, acc, found);
     const int64_t a1 = a0 + ((e - a0) & ~int64_t(255));
     for (int64_t p = a0 + 4 * lane; p < a1; p += 256) {
         const int4 c0 = __ldg(reinterpret_cast<const int4 *>(a.col + p));
         const int4 c1 = __ldg(reinterpret_cast<const int4 *>(a.col + p + 128));
         double v[8] = {1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0};
-        if (a.val) {
-            const double2 *vp = reinterpret_cast<const double2 *>(a.val + p);
-            const double2 *vq = reinterpret_cast<const double2 *>(a.val + p + 128);
+        if (val) {
+            const double2 *vp = reinterpret_cast<const double2 *>(val + p);
+            const double2 *vq = reinterpret_cast<const double2 *>(val + p + 128);
             double2 x0 = __ldg(vp), x1 = __ldg(vp + 1), x2 = __ldg(vq), x3 = __ldg(vq + 1);
             v[0] = x0.x; v[1] = x0.y; v[2] = x1.x; v[3] = x1.y;
             v[4] = x2.x; v[5] = x2.y; v[6] = x3.x; v[7] = x3.y;
@@ -144,8 +159,7 @@ __device__ void row_regs(const EmbedArgs &a, int64_t r) {
         consume<KP>(a, r, s_r, c1.z, v[6], acc, found);
         consume<KP>(a, r, s_r, c1.w, v[7], acc, found);
     }
-    for (int64_t p = a1 + lane; p < e; p += 32)
-        consume<KP>(a, r, s_r, a.col[p], a.val ? a.val[p] : 1.0, acc, found);
+    for (int64_t p = a1 + lane; p < e; p += 32) consume<KP>(a, r, s_r, a.col[p], val ? val[p] : 1.0, acc, found);
     if (a.flags & GEE_DIAGONAL) {
         found = __any_sync(0xffffffffu, found);
         int lb;
@@ -185,19 +199,19 @@ __device__ void row_regs(const EmbedArgs &a, int64_t r) {
 
 // ---------------------------------------------------------------------------
 // General K: per-warp shared K-tile.  Entries of this lane are
-// p = s + lane + 32*j*stride_warps + warp_off*32 (strided so a CTA can split
+// p = s + lane + 32*(warp_off + j*warp_stride) (strided so a CTA can split
 // a long row over its warps).
 // ---------------------------------------------------------------------------
-__device__ void accumulate_tile(const EmbedArgs &a, int64_t r, double s_r, int64_t s, int64_t e,
-                                int warp_off, int warp_stride, double *zs, double *xs, int t0,
-                                int kt, bool &found) {
+__device__ void accumulate_tile(const EmbedArgs &a, const double *val, int64_t r, double s_r, int64_t s,
+                                int64_t e, int warp_off, int warp_stride, double *zs, double *xs, int t0, int kt,
+                                bool &found) {
     const int lane = threadIdx.x & 31;
     for (int64_t p0 = s + (int64_t)warp_off * 32; p0 < e; p0 += (int64_t)warp_stride * 32) {
         int64_t p = p0 + lane;
         int lab;
         double x;
         bool isd;
-        bool ok = entry_term(a, r, s_r, p, p < e, lab, x, isd);
+        bool ok = entry_term(a, val, r, s_r, p, p < e, lab, x, isd);
         found |= isd;
         ok = ok && lab >= t0 && lab < t0 + kt;
         unsigned key = ok ? (unsigned)lab : 0x80000000u + lane;
@@ -224,6 +238,7 @@ __device__ void row_smem(const EmbedArgs &a, int64_t r, double *zs, double *xs) 
     int64_t s, e;
     row_extent(a, r, s, e);
     const double s_r = row_scale(a, r);
+    const double *val = row_vals(a, r);
     double *zrow = a.z + (r - a.row_begin) * a.ldz;
     const bool corr = (a.flags & GEE_CORRELATION) != 0;
     const int ntiles = (a.k + kKTile - 1) / kKTile;
@@ -234,13 +249,12 @@ __device__ void row_smem(const EmbedArgs &a, int64_t r, double *zs, double *xs) 
         const int t0 = t * kKTile, kt = min(kKTile, a.k - t0);
         for (int c = lane; c < kt; c += 32) zs[c] = 0.0;
         __syncwarp();
-        accumulate_tile(a, r, s_r, s, e, 0, 1, zs, xs, t0, kt, found);
+        accumulate_tile(a, val, r, s_r, s, e, 0, 1, zs, xs, t0, kt, found);
         if (a.flags & GEE_DIAGONAL) {
             bool f = __any_sync(0xffffffffu, found);
             int lb;
             double xd;
-            if (!f && lane == 0 && diag_term(a, r, s_r, lb, xd) && lb >= t0 && lb < t0 + kt)
-                zs[lb - t0] += xd;
+            if (!f && lane == 0 && diag_term(a, r, s_r, lb, xd) && lb >= t0 && lb < t0 + kt) zs[lb - t0] += xd;
             __syncwarp();
         }
         for (int c = lane; c < kt; c += 32) {
@@ -273,8 +287,7 @@ __device__ void row_smem(const EmbedArgs &a, int64_t r, double *zs, double *xs) 
 
 // one CTA, one long row (any K): warps accumulate strided slices into their
 // own K-tile, then the tiles are summed.
-__device__ void row_long(const EmbedArgs &a, int64_t r, double *zsm, double *xsm, double *dred,
-                         int *flag) {
+__device__ void row_long(const EmbedArgs &a, int64_t r, double *zsm, double *xsm, double *dred) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int kt_max = min(a.k, kKTile);
     double *zs = zsm + wid * kt_max;
@@ -282,6 +295,7 @@ __device__ void row_long(const EmbedArgs &a, int64_t r, double *zsm, double *xsm
     int64_t s, e;
     row_extent(a, r, s, e);
     const double s_r = row_scale(a, r);
+    const double *val = row_vals(a, r);
     double *zrow = a.z + (r - a.row_begin) * a.ldz;
     const bool corr = (a.flags & GEE_CORRELATION) != 0;
     const int ntiles = (a.k + kKTile - 1) / kKTile;
@@ -292,13 +306,14 @@ __device__ void row_long(const EmbedArgs &a, int64_t r, double *zsm, double *xsm
         const int t0 = t * kKTile, kt = min(kKTile, a.k - t0);
         for (int c = lane; c < kt; c += 32) zs[c] = 0.0;
         __syncwarp();
-        accumulate_tile(a, r, s_r, s, e, wid, kEmbedWarps, zs, xs, t0, kt, found);
-        int f = __syncthreads_or(found ? 1 : 0);
-        // combine warp tiles into warp 0's tile
+        accumulate_tile(a, val, r, s_r, s, e, wid, kEmbedWarps, zs, xs, t0, kt, found);
+        const int f = __syncthreads_or(found ? 1 : 0);
+        // combine warp tiles into warp 0's tile (column c read from every warp,
+        // written only to warp 0's copy by the thread owning c)
         for (int c = threadIdx.x; c < kt; c += blockDim.x) {
             double v = 0.0;
             for (int w = 0; w < kEmbedWarps; ++w) v += zsm[w * kt_max + c];
-            zsm[c] = v;  // reading column c of every warp, writing column c of warp 0
+            zsm[c] = v;
         }
         __syncthreads();
         if ((a.flags & GEE_DIAGONAL) && !f && threadIdx.x == 0) {
@@ -327,13 +342,11 @@ __device__ void row_long(const EmbedArgs &a, int64_t r, double *zsm, double *xsm
     }
     const double nrm = __dsqrt_rn(ss);
     if (ntiles == 1) {
-        for (int c = threadIdx.x; c < a.k; c += blockDim.x)
-            zrow[c] = nrm > 0.0 ? __ddiv_rn(zsm[c], nrm) : zsm[c];
+        for (int c = threadIdx.x; c < a.k; c += blockDim.x) zrow[c] = nrm > 0.0 ? __ddiv_rn(zsm[c], nrm) : zsm[c];
     } else if (nrm > 0.0) {
         for (int c = threadIdx.x; c < a.k; c += blockDim.x) zrow[c] = __ddiv_rn(zrow[c], nrm);
     }
     __syncthreads();
-    (void)flag;
 }
 
 template <int KP>
@@ -344,9 +357,9 @@ __global__ void __launch_bounds__(kEmbedThreads) k_embed(EmbedArgs a) {
     __shared__ double dred[33];
     __shared__ int task;
     const int kt_max = min(a.k, kKTile);
-    double *zsm = reinterpret_cast<double *>(dsm);                 // [warps][kt_max]
-    double *xsm = zsm + (size_t)kEmbedWarps * kt_max;               // [warps][32]
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double *zsm = reinterpret_cast<double *>(dsm);    // [warps][kt_max]
+    double *xsm = zsm + (size_t)kEmbedWarps * kt_max;  // [warps][32]
+    const int wid = threadIdx.x >> 5;
     // phase 1: long rows, one CTA each
     const unsigned n_long = *a.n_long;
     for (;;) {
@@ -355,7 +368,7 @@ __global__ void __launch_bounds__(kEmbedThreads) k_embed(EmbedArgs a) {
         int t = task;
         __syncthreads();
         if (t >= (int)n_long) break;
-        row_long(a, a.long_list[t], zsm, xsm, dred, nullptr);
+        row_long(a, a.long_list[t], zsm, xsm, dred);
     }
     // phase 2: chunks of rows, one warp per row
     const int64_t n_rows = a.row_end - a.row_begin;
@@ -378,12 +391,11 @@ __global__ void __launch_bounds__(kEmbedThreads) k_embed(EmbedArgs a) {
                 row_smem(a, r, zsm + wid * kt_max, xsm + wid * 32);
         }
     }
-    (void)lane;
 }
 
-__global__ void k_embed_classify(const int64_t *__restrict__ row_ptr,
-                                 const unsigned *__restrict__ row_cnt, int64_t rb, int64_t re,
-                                 unsigned *__restrict__ list, unsigned *__restrict__ n_list) {
+__global__ void k_embed_classify(const int64_t *__restrict__ row_ptr, const unsigned *__restrict__ row_cnt,
+                                 int64_t rb, int64_t re, unsigned *__restrict__ list,
+                                 unsigned *__restrict__ n_list) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t n = re - rb;
     const int64_t n_round = (n + 31) & ~int64_t(31);
@@ -404,25 +416,41 @@ __global__ void k_embed_classify(const int64_t *__restrict__ row_ptr,
     }
 }
 
-size_t embed_workspace(int64_t n_rows) {
+// node records {label bits, g = s_j / n_{Y_j}}; label -1 for unlabeled nodes
+__global__ void k_node_rec(const int32_t *__restrict__ y32, const double *__restrict__ inv,
+                           const double *__restrict__ scale, int64_t n, double2 *__restrict__ rec) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+        const int lab = y32[j];
+        double g = 0.0;
+        if (lab >= 0) g = scale ? scale[j] * inv[lab] : inv[lab];
+        rec[j] = make_double2(__longlong_as_double((long long)(unsigned)lab), g);
+    }
+}
+
+size_t embed_workspace(int64_t n_rows, int64_t n_cols) {
     Carver cv(nullptr);
     cv.take<unsigned>(4);
     cv.take<unsigned>((size_t)n_rows + 1);
+    cv.take<double2>((size_t)n_cols + 1);
     return cv.bytes();
 }
 
 int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, const double *val,
-          const unsigned *val_flags, int64_t rb, int64_t re, const int32_t *y32, const double *inv,
-          const double *scale, int k,
-          unsigned flags, double *z, int64_t ldz, void *ws, size_t ws_bytes, int32_t *err,
-          cudaStream_t st) {
+          const unsigned *val_flags, const unsigned char *row_flag, int64_t rb, int64_t re, int64_t n_cols,
+          const int32_t *y32, const double *inv, const double *scale, int k, unsigned flags, double *z, int64_t ldz,
+          void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st) {
     const int64_t n = re - rb;
     Carver cv(ws);
     unsigned *ctr = cv.take<unsigned>(4);
     unsigned *list = cv.take<unsigned>((size_t)n + 1);
+    double2 *rec = cv.take<double2>((size_t)n_cols + 1);
     if (ws_bytes < cv.bytes()) return GEE_E_WORKSPACE;
     if (n <= 0) return GEE_OK;
     GEE_CHECK_CUDA(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned), st));
+    k_node_rec<<<grid_for(n_cols, 256, 8), 256, 0, st>>>(y32, inv, (flags & GEE_LAPLACIAN) ? scale : nullptr,
+                                                          n_cols, rec);
+    GEE_CHECK_LAUNCH("k_node_rec");
     k_embed_classify<<<grid_for(n, 256, 8), 256, 0, st>>>(row_ptr, row_cnt, rb, re, list, ctr);
     GEE_CHECK_LAUNCH("k_embed_classify");
     EmbedArgs a;
@@ -432,8 +460,7 @@ int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, c
     a.val = val;
     a.row_begin = rb;
     a.row_end = re;
-    a.y32 = y32;
-    a.inv = inv;
+    a.rec = rec;
     a.scale = scale;
     a.k = k;
     a.flags = flags;
@@ -444,6 +471,7 @@ int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, c
     a.n_long = ctr;
     a.work = ctr + 1;
     a.val_flags = val_flags;
+    a.row_flag = row_flag;
     const int kt_max = k < kKTile ? k : kKTile;
     size_t smem = sizeof(double) * (size_t)kEmbedWarps * ((size_t)kt_max + 32);
     static bool attr = false;
@@ -455,13 +483,12 @@ int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, c
     int occ = 0;
     const unsigned grid_cap = (unsigned)num_sms() * 8;
     unsigned grid;
-#define GEE_LAUNCH_EMBED(KP)                                                                  \
-    do {                                                                                      \
-        GEE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_embed<KP>,       \
-                                                                     kEmbedThreads, smem));   \
-        grid = (unsigned)num_sms() * (unsigned)(occ > 0 ? occ : 1);                           \
-        if (grid > grid_cap) grid = grid_cap;                                                 \
-        k_embed<KP><<<grid, kEmbedThreads, smem, st>>>(a);                                    \
+#define GEE_LAUNCH_EMBED(KP)                                                                                \
+    do {                                                                                                    \
+        GEE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_embed<KP>, kEmbedThreads, smem)); \
+        grid = (unsigned)num_sms() * (unsigned)(occ > 0 ? occ : 1);                                         \
+        if (grid > grid_cap) grid = grid_cap;                                                               \
+        k_embed<KP><<<grid, kEmbedThreads, smem, st>>>(a);                                                  \
     } while (0)
     if (k <= 1)
         GEE_LAUNCH_EMBED(1);

@@ -494,8 +494,10 @@ int set_force_buckets(int v) {
     return old;
 }
 
+int force_path() { return t_force_buckets; }
+
 bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed) {
-    if (t_force_buckets) return false;
+    if (t_force_buckets == 1) return false;
     const int rb = bitlen(n_rows);  // rows <= n_rows-1 < 2^rb - 1: keys stay below the sentinel
     const int cb = bitlen(n_cols > 1 ? n_cols - 1 : 1);
     const int64_t Mv = directed ? E : 2 * E;

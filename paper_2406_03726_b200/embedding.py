@@ -76,8 +76,9 @@ class GeeEncoder:
         self.flags = options_flags(opts)
         lib = _lib.load()
         with torch.cuda.device(self.dev):
-            nb = _lib.size_query(lib.gee_encode_edges_workspace, self.e, self.n, self.k,
-                                 int(self.directed))
+            # the assembly path (and its workspace) depends on the weight kind
+            nb = max(_lib.size_query(lib.gee_encode_edges_workspace, self.e, self.n, self.k,
+                                     int(self.directed), wt) for wt in (_lib.W_UNIT, _lib.W_F64))
         self.ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=self.dev)
         self.z = torch.empty((self.n, self.k), dtype=torch.float64, device=self.dev)
         self.err = _device.error_word(self.dev)
@@ -171,11 +172,11 @@ def _encode_csr(a: CsrMatrix, labels: LabelVector, flags: int, dev) -> torch.Ten
                 flags & _lib.DIAGONAL, _device.ptr(deg), _device.ptr(scale), _device.ptr(err),
                 _device.stream_handle()))
         z = torch.empty((n, k), dtype=torch.float64, device=dev)
-        nb = _lib.size_query(lib.gee_embed_workspace, n)
+        nb = _lib.size_query(lib.gee_embed_workspace, n, n)
         ws = _device.WORKSPACE.get(nb, dev)
         _lib.check(lib.gee_embed(
             _device.ptr(a.index_pointers), None, _device.ptr(a.col_indices), _device.ptr(a.data), 0,
-            n, _device.ptr(y32), _device.ptr(inv), _device.ptr(scale), k, flags, _device.ptr(z), k,
+            n, n, _device.ptr(y32), _device.ptr(inv), _device.ptr(scale), k, flags, _device.ptr(z), k,
             _device.ptr(ws), ws.numel(), _device.ptr(err), _device.stream_handle()))
     _device.check_device_errors(err, "encode")
     return z

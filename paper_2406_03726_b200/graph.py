@@ -65,6 +65,10 @@ class EdgeList:
         n_w = None if self.weights is None else int(self.weights.shape[0])
         if not (self.rows.shape == self.cols.shape) or (n_w is not None and n_w != self.rows.shape[0]):
             raise StructuralError("edge arrays must have equal length")
+        # True when every weight is exactly 1.0 (an unweighted graph): the
+        # device path then never reads the weight array.  Established by the
+        # same construction-time scan that checks finiteness (graph_io.py:71).
+        self.unit_weights = self.weights is None
         if validate and self.n_edges:
             self._validate()
 
@@ -83,13 +87,17 @@ class EdgeList:
                 raise StructuralError(f"edge endpoint outside node range [0, {self.n_nodes})")
             if bits & _lib.ERR_EDGE_WEIGHT:
                 raise StructuralError("edge weights must be finite")
+            if self.weights is not None:
+                self.unit_weights = bool((self.weights == 1.0).all().item())
             return
         hi = max(int(self.rows.max()), int(self.cols.max()))
         lo = min(int(self.rows.min()), int(self.cols.min()))
         if lo < 0 or hi >= self.n_nodes:
             raise StructuralError(f"edge endpoint outside node range [0, {self.n_nodes})")
-        if self.weights is not None and not np.isfinite(self.weights).all():
-            raise StructuralError("edge weights must be finite")
+        if self.weights is not None:
+            if not np.isfinite(self.weights).all():
+                raise StructuralError("edge weights must be finite")
+            self.unit_weights = bool((self.weights == 1.0).all())
 
     @property
     def n_edges(self) -> int:
@@ -101,7 +109,7 @@ class EdgeList:
 
     def weight_kind(self):
         """(GEE_W_* code, weight array or None)."""
-        if self.weights is None:
+        if self.weights is None or self.unit_weights:
             return _lib.W_UNIT, None
         dt = self.weights.dtype
         f32 = dt == torch.float32 or dt == np.float32
@@ -112,13 +120,14 @@ class EdgeList:
         if self.on_device and self.rows.device == dev:
             return self
         w = None
-        if self.weights is not None:
-            w = _device.to_device(self.weights,
-                                  torch.float32 if self.weight_kind()[0] == _lib.W_F32 else torch.float64,
-                                  dev)
-        return EdgeList(self.n_nodes, _device.to_device(self.rows, torch.int64, dev),
-                        _device.to_device(self.cols, torch.int64, dev), w, self.directed,
-                        validate=False)
+        if self.weights is not None and not self.unit_weights:
+            f32 = self.weights.dtype in (np.float32, torch.float32)
+            w = _device.to_device(self.weights, torch.float32 if f32 else torch.float64, dev)
+        out = EdgeList(self.n_nodes, _device.to_device(self.rows, torch.int64, dev),
+                       _device.to_device(self.cols, torch.int64, dev), w, self.directed,
+                       validate=False)
+        out.unit_weights = self.unit_weights
+        return out
 
     def weights_f64(self) -> np.ndarray:
         """Host float64 weights as the reference stores them."""

@@ -47,12 +47,13 @@ def test_ctypes_table_matches_header():
 def test_size_queries_and_argument_checks_need_no_gpu():
     from paper_2406_03726_b200 import _lib
     lib = _lib.load()
-    n = _lib.size_query(lib.gee_encode_edges_workspace, 5_500_000, 10_000, 3, 0)
-    assert n > 11_000_000 * 12  # holds at least the 2E-entry CSR
+    for wt in (_lib.W_UNIT, _lib.W_F64):
+        n = _lib.size_query(lib.gee_encode_edges_workspace, 5_500_000, 10_000, 3, 0, wt)
+        assert n > 11_000_000 * 12  # holds at least the 2E-entry CSR
     with pytest.raises(Exception):
-        _lib.size_query(lib.gee_encode_edges_workspace, -1, 10, 3, 0)
+        _lib.size_query(lib.gee_encode_edges_workspace, -1, 10, 3, 0, 1)
     out = ctypes.c_size_t(0)
-    assert lib.gee_embed_workspace(-5, ctypes.byref(out)) == _lib.GEE_E_ARG
+    assert lib.gee_embed_workspace(-5, 10, ctypes.byref(out)) == _lib.GEE_E_ARG
 
 
 def test_sass_is_sm100a():

@@ -23,15 +23,17 @@ import paper_2406_03726_b200 as G  # noqa: E402
 
 RTOL = 1e-12
 CASES = load()
-PATHS = ["sort", "buckets"]
+PATHS = ["default", "sort", "buckets"]
 
 
 class assembly_path:
-    """Select the CSR-assembly path: the radix sort (default when (row, col)
-    packs into 32 bits) or the row-bucket path (forced via the test hook)."""
+    """Select the CSR-assembly path via the library's test hook: "default"
+    (column bitmaps for unit-weight graphs with <= 16384 nodes, else the
+    radix sort when (row, col) packs into 32 bits, else row buckets),
+    "sort" (never the bitmap path) or "buckets" (always row buckets)."""
 
     def __init__(self, path):
-        self.force = 1 if path == "buckets" else 0
+        self.force = {"default": 0, "sort": 2, "buckets": 1}[path]
 
     def __enter__(self):
         from paper_2406_03726_b200 import _lib
