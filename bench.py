@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--eager", action="store_true", help="launch kernels one by one instead of a CUDA graph")
     p.add_argument("--flush-mib", type=int, default=512)
     p.add_argument("--cpu-budget-s", type=float, default=12.0)
     return p.parse_args()
@@ -267,9 +268,21 @@ def run_b200(args):
     wbytes = 0 if w is None else w.element_size()
 
     enc.run(rows, cols, w, lab, check=True)  # surfaces any data error once
+    lib.gee_reset_launch_count()
+    enc.run(rows, cols, w, lab, check=False)
+    launches_per_step = int(lib.gee_launch_count())
+    if not args.eager:
+        # the whole step as one CUDA graph, with per-kernel event-record nodes
+        enc.capture(rows, cols, w, lab, profile=True)
+        step_fn = enc.replay
+    else:
+        def step_fn():
+            lib.gee_profile_start(torch.cuda.current_stream().cuda_stream)
+            enc.run(rows, cols, w, lab, check=False)
+            lib.gee_profile_stop()
     for _ in range(args.warmup):
         flush.zero_()
-        enc.run(rows, cols, w, lab, check=False)
+        step_fn()
     torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
@@ -280,22 +293,19 @@ def run_b200(args):
     cap = 256
     ms_buf = (ctypes.c_float * cap)()
     nm_buf = (ctypes.c_char_p * cap)()
-    lib.gee_reset_launch_count()
     sampler = ClockSampler(local)
     torch.cuda.synchronize()
     with sampler:
         for i in range(args.steps):
             flush.zero_()
             starts[i].record(stream)
-            lib.gee_profile_start(stream.cuda_stream)
-            enc.run(rows, cols, w, lab, check=False)
-            lib.gee_profile_stop()
+            step_fn()
             ends[i].record(stream)
             got = lib.gee_profile_read(ms_buf, nm_buf, cap)
             for j in range(got):
                 per_kernel.setdefault(nm_buf[j].decode(), []).append(ms_buf[j])
         torch.cuda.synchronize()
-    launches = int(lib.gee_launch_count())
+    launches = launches_per_step * args.steps
     step_ms = [s.elapsed_time(t) for s, t in zip(starts, ends)]
     _device_err = int(enc.err.item())
     ms = statistics.mean(step_ms)
@@ -373,6 +383,7 @@ def run_b200(args):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
+        "launch_mode": "eager" if args.eager else "cuda_graph (one graph replay per step)",
         "clocks": sampler.summary(),
         "device_error_bits": _device_err,
     }

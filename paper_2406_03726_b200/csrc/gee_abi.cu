@@ -28,7 +28,12 @@ void profile_mark(const char *name, cudaStream_t st) {
     Profile &p = t_prof;
     if (!p.on || p.n >= kMaxMarks) return;
     if (!p.ev[p.n]) cudaEventCreate(&p.ev[p.n]);
-    cudaEventRecord(p.ev[p.n], st);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusActive)
+        cudaEventRecordWithFlags(p.ev[p.n], st, cudaEventRecordExternal);  // a record node in the graph
+    else
+        cudaEventRecord(p.ev[p.n], st);
     p.name[p.n] = name;
     ++p.n;
 }

@@ -56,6 +56,8 @@ __device__ __forceinline__ void chunk_range(int64_t E, int64_t &e0, int64_t &e1)
     e1 = (int64_t)((__int128)E * (blockIdx.x + 1) / gridDim.x);
 }
 
+constexpr int kBmUnroll = 4;  // edges per thread per iteration (loads issued together)
+
 __global__ void __launch_bounds__(kBmThreads) k_bm_count(const int64_t *__restrict__ rows,
                                                           const int64_t *__restrict__ cols, int64_t E,
                                                           int directed, int n, unsigned *__restrict__ part) {
@@ -64,17 +66,22 @@ __global__ void __launch_bounds__(kBmThreads) k_bm_count(const int64_t *__restri
     __syncthreads();
     int64_t e0, e1;
     chunk_range(E, e0, e1);
-    for (int64_t b = e0; b < e1; b += blockDim.x) {
-        const int64_t e = b + threadIdx.x;
-        const bool v = e < e1;
-        const unsigned r = v ? (unsigned)rows[e] : 0u, c = v ? (unsigned)cols[e] : 0u;
-        const int nv = __popc(__ballot_sync(0xffffffffu, v));
-        rle_take(h, r, v, nv, false);
-        if (!directed) {
-            const bool v2 = v && r != c;
-            // reversed entries: their rows are the (random) columns; lanes
-            // with a self loop drop out, so aggregate without the prefix rule
-            if (v2) atomicAdd(&h[c], 1u);
+    for (int64_t b = e0; b < e1; b += (int64_t)blockDim.x * kBmUnroll) {
+        unsigned r[kBmUnroll], c[kBmUnroll];
+#pragma unroll
+        for (int u = 0; u < kBmUnroll; ++u) {
+            const int64_t e = b + (int64_t)u * blockDim.x + threadIdx.x;
+            r[u] = e < e1 ? (unsigned)__ldcs(rows + e) : 0u;
+            c[u] = e < e1 ? (unsigned)__ldcs(cols + e) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kBmUnroll; ++u) {
+            const int64_t e = b + (int64_t)u * blockDim.x + threadIdx.x;
+            const bool v = e < e1;
+            const int nv = __popc(__ballot_sync(0xffffffffu, v));
+            rle_take(h, r[u], v, nv, false);
+            // reversed entries: their rows are the (random) columns
+            if (!directed && v && r[u] != c[u]) atomicAdd(&h[c[u]], 1u);
         }
     }
     __syncthreads();
@@ -82,28 +89,28 @@ __global__ void __launch_bounds__(kBmThreads) k_bm_count(const int64_t *__restri
     for (int r = threadIdx.x; r < n; r += blockDim.x) dst[r] = h[r];
 }
 
-// part[g][r] -> exclusive prefix over g (each chunk's offset inside row r); cnt[r] = total
+// part[g][r] -> exclusive prefix over g (each chunk's offset inside row r);
+// cnt[r] = total.  One warp per row, 32 chunks per step.
 __global__ void k_bm_reduce(unsigned *__restrict__ part, int G, int n, unsigned *__restrict__ cnt) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    unsigned run = 0;
-    int g = 0;
-    for (; g + 8 <= G; g += 8) {
-        unsigned x[8];
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < n; r += nwarps) {
+        unsigned run = 0;
+        for (int g0 = 0; g0 < G; g0 += 32) {
+            const int g = g0 + lane;
+            const unsigned x = g < G ? part[(size_t)g * n + r] : 0u;
+            unsigned incl = x;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = part[(size_t)(g + u) * n + r];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            part[(size_t)(g + u) * n + r] = run;
-            run += x[u];
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (g < G) part[(size_t)g * n + r] = run + incl - x;
+            run += __shfl_sync(0xffffffffu, incl, 31);
         }
+        if (lane == 0) cnt[r] = run;
     }
-    for (; g < G; ++g) {
-        unsigned x = part[(size_t)g * n + r];
-        part[(size_t)g * n + r] = run;
-        run += x;
-    }
-    cnt[r] = run;
 }
 
 __global__ void __launch_bounds__(kBmThreads) k_bm_scatter(const int64_t *__restrict__ rows,
@@ -118,14 +125,23 @@ __global__ void __launch_bounds__(kBmThreads) k_bm_scatter(const int64_t *__rest
     __syncthreads();
     int64_t e0, e1;
     chunk_range(E, e0, e1);
-    for (int64_t b = e0; b < e1; b += blockDim.x) {
-        const int64_t e = b + threadIdx.x;
-        const bool v = e < e1;
-        const unsigned r = v ? (unsigned)rows[e] : 0u, c = v ? (unsigned)cols[e] : 0u;
-        const int nv = __popc(__ballot_sync(0xffffffffu, v));
-        const unsigned p = rle_take(cur, r, v, nv, true);
-        if (v) colbuf[p] = (unsigned short)c;
-        if (!directed && v && r != c) colbuf[atomicAdd(&cur[c], 1u)] = (unsigned short)r;
+    for (int64_t b = e0; b < e1; b += (int64_t)blockDim.x * kBmUnroll) {
+        unsigned r[kBmUnroll], c[kBmUnroll];
+#pragma unroll
+        for (int u = 0; u < kBmUnroll; ++u) {
+            const int64_t e = b + (int64_t)u * blockDim.x + threadIdx.x;
+            r[u] = e < e1 ? (unsigned)__ldcs(rows + e) : 0u;
+            c[u] = e < e1 ? (unsigned)__ldcs(cols + e) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kBmUnroll; ++u) {
+            const int64_t e = b + (int64_t)u * blockDim.x + threadIdx.x;
+            const bool v = e < e1;
+            const int nv = __popc(__ballot_sync(0xffffffffu, v));
+            const unsigned p = rle_take(cur, r[u], v, nv, true);
+            if (v) colbuf[p] = (unsigned short)c[u];
+            if (!directed && v && r[u] != c[u]) colbuf[atomicAdd(&cur[c[u]], 1u)] = (unsigned short)r[u];
+        }
     }
 }
 
@@ -144,13 +160,16 @@ struct BmRowsArgs {
     int32_t *err;
 };
 
+constexpr int kBmStage = 1536;  // per-warp staging of a row's sorted columns
+
 __global__ void __launch_bounds__(kBmRowsThreads) k_bm_rows(BmRowsArgs a) {
     extern __shared__ unsigned bsm[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int W = a.words;
-    unsigned *bm = bsm + (size_t)wid * 2 * W;  // bitmap
-    unsigned *pre = bm + W;                    // exclusive popc prefix per word
-    const int wpl = (W + 31) / 32;             // words per lane in the emission
+    unsigned *bm = bsm + (size_t)wid * (2 * W + kBmStage);  // bitmap
+    unsigned *pre = bm + W;                                 // exclusive popc prefix per word
+    unsigned *stage = pre + W;                              // sorted columns of the row
+    const int wpl = (W + 31) / 32;                          // words per lane in the emission
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t r = warp; r < a.n; r += nwarps) {
@@ -165,7 +184,8 @@ __global__ void __launch_bounds__(kBmRowsThreads) k_bm_rows(BmRowsArgs a) {
             dup |= atomicOr(&bm[c >> 5], bit) & bit;
         }
         __syncwarp();
-        // emission: lane l owns words [l*wpl, (l+1)*wpl)
+        // emission: lane l owns words [l*wpl, (l+1)*wpl); set bits leave in
+        // column order, staged in shared memory so the global write coalesces
         const int w0 = min(W, lane * wpl), w1 = min(W, w0 + wpl);
         unsigned cnt = 0;
         for (int w = w0; w < w1; ++w) cnt += __popc(bm[w]);
@@ -177,16 +197,23 @@ __global__ void __launch_bounds__(kBmRowsThreads) k_bm_rows(BmRowsArgs a) {
         }
         unsigned off = incl - cnt;
         const unsigned u = __shfl_sync(0xffffffffu, incl, 31);
+        const bool staged = u <= (unsigned)kBmStage;
         for (int w = w0; w < w1; ++w) {
             unsigned word = bm[w];
             pre[w] = off;
             while (word) {
                 const int b = __ffs(word) - 1;
                 word &= word - 1;
-                a.out_col[s + off] = w * 32 + b;
+                if (staged)
+                    stage[off] = w * 32 + b;
+                else
+                    a.out_col[s + off] = w * 32 + b;
                 ++off;
             }
         }
+        __syncwarp();
+        if (staged)
+            for (unsigned i = lane; i < u; i += 32) a.out_col[s + i] = (int32_t)stage[i];
         const bool multi = __any_sync(0xffffffffu, dup != 0);
         if (lane == 0) {
             a.row_cnt[r] = u;
@@ -263,7 +290,7 @@ int bitmap_csr_build(const int64_t *rows, const int64_t *cols, int64_t E, int64_
         GEE_CHECK_CUDA(cudaFuncSetAttribute(k_bm_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kBmMax * 4));
         GEE_CHECK_CUDA(cudaFuncSetAttribute(k_bm_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kBmMax * 4));
         GEE_CHECK_CUDA(cudaFuncSetAttribute(k_bm_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (kBmRowsThreads / 32) * 2 * (kBmMax / 32) * 4));
+                                            (kBmRowsThreads / 32) * (2 * (kBmMax / 32) + kBmStage) * 4));
         attr = true;
     }
     GEE_CHECK_CUDA(cudaMemsetAsync(W.flags, 0, 4 * sizeof(unsigned), st));
@@ -271,7 +298,7 @@ int bitmap_csr_build(const int64_t *rows, const int64_t *cols, int64_t E, int64_
     if (E > 0) {
         k_bm_count<<<W.G, kBmThreads, hsm, st>>>(rows, cols, E, directed, (int)n, W.part);
         GEE_CHECK_LAUNCH("k_bm_count");
-        k_bm_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(W.part, W.G, (int)n, W.cnt);
+        k_bm_reduce<<<grid_for(n * 32, 256, 8), 256, 0, st>>>(W.part, W.G, (int)n, W.cnt);
         GEE_CHECK_LAUNCH("k_bm_reduce");
     } else {
         GEE_CHECK_CUDA(cudaMemsetAsync(W.cnt, 0, sizeof(unsigned) * (size_t)(n + 1), st));
@@ -296,7 +323,7 @@ int bitmap_csr_build(const int64_t *rows, const int64_t *cols, int64_t E, int64_
     a.deg = deg;
     a.scale = (deg_flags & GEE_LAPLACIAN) ? scale : nullptr;
     a.err = err;
-    const size_t rsm = (size_t)(kBmRowsThreads / 32) * 2 * (size_t)a.words * 4;
+    const size_t rsm = (size_t)(kBmRowsThreads / 32) * (2 * (size_t)a.words + kBmStage) * 4;
     k_bm_rows<<<grid_for(n * 32, kBmRowsThreads, 8), kBmRowsThreads, rsm, st>>>(a);
     GEE_CHECK_LAUNCH("k_bm_rows");
     return GEE_OK;

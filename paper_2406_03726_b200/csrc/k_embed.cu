@@ -103,6 +103,16 @@ __device__ __forceinline__ double row_scale(const EmbedArgs &a, int64_t r) {
     return (a.flags & GEE_LAPLACIAN) ? a.scale[r] : 1.0;
 }
 
+// streaming 16-byte load of column indices: read once, so keep them out of
+// L1 (which holds the node-record table the gathers hit)
+__device__ __forceinline__ int4 ld_stream_i4(const int32_t *p) {
+    int4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
 // ---------------------------------------------------------------------------
 // K <= KP <= 8: register accumulators, one warp per row.
 // ---------------------------------------------------------------------------
@@ -138,28 +148,42 @@ __device__ void row_regs(const EmbedArgs &a, int64_t r) {
     // per lane, 256 entries per warp per iteration), scalar tail
     const int64_t a0 = min(e, (s + 3) & ~int64_t(3));
     if (s + lane < a0) consume<KP>(a, r, s_r, a.col[s + lane], val ? val[s + lane] : 1.0, acc, found);
-    const int64_t a1 = a0 + ((e - a0) & ~int64_t(255));
-    for (int64_t p = a0 + 4 * lane; p < a1; p += 256) {
-        const int4 c0 = __ldg(reinterpret_cast<const int4 *>(a.col + p));
-        const int4 c1 = __ldg(reinterpret_cast<const int4 *>(a.col + p + 128));
-        double v[8] = {1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0};
+    // body: 4 x 16-byte column loads per lane in flight (512 entries per warp)
+    const int64_t a1 = a0 + ((e - a0) & ~int64_t(511));
+    for (int64_t p = a0 + 4 * lane; p < a1; p += 512) {
+        int4 cc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cc[u] = ld_stream_i4(a.col + p + 128 * u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            double v[4] = {1.0, 1.0, 1.0, 1.0};
+            if (val) {
+                const double2 *vp = reinterpret_cast<const double2 *>(val + p + 128 * u);
+                const double2 x0 = __ldg(vp), x1 = __ldg(vp + 1);
+                v[0] = x0.x; v[1] = x0.y; v[2] = x1.x; v[3] = x1.y;
+            }
+            consume<KP>(a, r, s_r, cc[u].x, v[0], acc, found);
+            consume<KP>(a, r, s_r, cc[u].y, v[1], acc, found);
+            consume<KP>(a, r, s_r, cc[u].z, v[2], acc, found);
+            consume<KP>(a, r, s_r, cc[u].w, v[3], acc, found);
+        }
+    }
+    // remaining whole vectors, then the scalar tail
+    const int64_t a2 = a1 + ((e - a1) & ~int64_t(3));
+    for (int64_t p = a1 + 4 * lane; p < a2; p += 128) {
+        const int4 c4 = ld_stream_i4(a.col + p);
+        double v[4] = {1.0, 1.0, 1.0, 1.0};
         if (val) {
             const double2 *vp = reinterpret_cast<const double2 *>(val + p);
-            const double2 *vq = reinterpret_cast<const double2 *>(val + p + 128);
-            double2 x0 = __ldg(vp), x1 = __ldg(vp + 1), x2 = __ldg(vq), x3 = __ldg(vq + 1);
+            const double2 x0 = __ldg(vp), x1 = __ldg(vp + 1);
             v[0] = x0.x; v[1] = x0.y; v[2] = x1.x; v[3] = x1.y;
-            v[4] = x2.x; v[5] = x2.y; v[6] = x3.x; v[7] = x3.y;
         }
-        consume<KP>(a, r, s_r, c0.x, v[0], acc, found);
-        consume<KP>(a, r, s_r, c0.y, v[1], acc, found);
-        consume<KP>(a, r, s_r, c0.z, v[2], acc, found);
-        consume<KP>(a, r, s_r, c0.w, v[3], acc, found);
-        consume<KP>(a, r, s_r, c1.x, v[4], acc, found);
-        consume<KP>(a, r, s_r, c1.y, v[5], acc, found);
-        consume<KP>(a, r, s_r, c1.z, v[6], acc, found);
-        consume<KP>(a, r, s_r, c1.w, v[7], acc, found);
+        consume<KP>(a, r, s_r, c4.x, v[0], acc, found);
+        consume<KP>(a, r, s_r, c4.y, v[1], acc, found);
+        consume<KP>(a, r, s_r, c4.z, v[2], acc, found);
+        consume<KP>(a, r, s_r, c4.w, v[3], acc, found);
     }
-    for (int64_t p = a1 + lane; p < e; p += 32) consume<KP>(a, r, s_r, a.col[p], val ? val[p] : 1.0, acc, found);
+    for (int64_t p = a2 + lane; p < e; p += 32) consume<KP>(a, r, s_r, a.col[p], val ? val[p] : 1.0, acc, found);
     if (a.flags & GEE_DIAGONAL) {
         found = __any_sync(0xffffffffu, found);
         int lb;

@@ -100,6 +100,28 @@ class GeeEncoder:
             _device.check_device_errors(self.err, "encode")
         return z
 
+    def capture(self, rows, cols, weights, labels, *, profile: bool = False):
+        """Capture the pipeline for these device inputs into a CUDA graph
+        (removes host launch gaps between the ~12 kernels).  With `profile`,
+        per-kernel event-record nodes are captured too (gee_profile_read
+        reports per-kernel times after each replay)."""
+        lib = _lib.load()
+        self.run(rows, cols, weights, labels, check=True)  # warm-up: attributes, errors
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            if profile:
+                lib.gee_profile_start(torch.cuda.current_stream().cuda_stream)
+            self.run(rows, cols, weights, labels, check=False)
+            if profile:
+                lib.gee_profile_stop()
+        torch.cuda.synchronize()
+        return self.graph
+
+    def replay(self) -> torch.Tensor:
+        self.graph.replay()
+        return self.z
+
     def attach_host(self, rows, cols, weights, labels):
         """Register host inputs for run_host(): pinned staging copies plus
         device buffers of the same shapes and a pinned output.  Returns
