@@ -272,17 +272,25 @@ def run_b200(args):
     enc.run(rows, cols, w, lab, check=False)
     launches_per_step = int(lib.gee_launch_count())
     if not args.eager:
-        # the whole step as one CUDA graph, with per-kernel event-record nodes
-        enc.capture(rows, cols, w, lab, profile=True)
-        step_fn = enc.replay
+        # the whole step as one CUDA graph (no host launch gaps); a second
+        # capture carries an event-record node after every kernel for the
+        # per-kernel breakdown
+        g_plain = enc.capture(rows, cols, w, lab, profile=False)
+        g_prof = enc.capture(rows, cols, w, lab, profile=True)
+        step_fn, prof_fn = g_plain.replay, g_prof.replay
     else:
         def step_fn():
+            enc.run(rows, cols, w, lab, check=False)
+
+        def prof_fn():
             lib.gee_profile_start(torch.cuda.current_stream().cuda_stream)
             enc.run(rows, cols, w, lab, check=False)
             lib.gee_profile_stop()
     for _ in range(args.warmup):
         flush.zero_()
         step_fn()
+        flush.zero_()
+        prof_fn()
     torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
@@ -296,12 +304,22 @@ def run_b200(args):
     sampler = ClockSampler(local)
     torch.cuda.synchronize()
     with sampler:
+        # timed region: K steps, L2 flushed before each, CUDA events around each
         for i in range(args.steps):
             flush.zero_()
             starts[i].record(stream)
             step_fn()
             ends[i].record(stream)
+        torch.cuda.synchronize()
+        # per-kernel breakdown: the same step with event records between kernels
+        prof_steps = []
+        for i in range(args.steps):
+            flush.zero_()
+            prof_fn()
             got = lib.gee_profile_read(ms_buf, nm_buf, cap)
+            if got < 0:
+                raise RuntimeError("gee_profile_read: " + lib.gee_last_error_string().decode())
+            prof_steps.append(sum(ms_buf[j] for j in range(got)))
             for j in range(got):
                 per_kernel.setdefault(nm_buf[j].decode(), []).append(ms_buf[j])
         torch.cuda.synchronize()
@@ -320,7 +338,7 @@ def run_b200(args):
         t_launch = statistics.mean(ts)
         b = models.get(name)
         ktab.append({"kernel": name, "ms_per_launch": t_launch, "launches_per_step": launches_per_step,
-                     "share": sum(ts) / sum(step_ms),
+                     "share": sum(ts) / sum(prof_steps),
                      "alg_bytes": b, "gbs": (b / (t_launch * 1e-3) / 1e9) if b else None})
     ktab.sort(key=lambda r: -r["share"])
     dom = next(r for r in ktab if r["alg_bytes"])

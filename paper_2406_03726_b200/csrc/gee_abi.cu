@@ -79,13 +79,16 @@ size_t embed_workspace(int64_t n_rows, int64_t n_cols);
 int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, const double *val,
           const unsigned *val_flags, const unsigned char *row_flag, int64_t rb, int64_t re, int64_t n_cols,
           const int32_t *y32, const double *inv, const double *scale, int k, unsigned flags, double *z, int64_t ldz,
-          void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st);
+          void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st, int prepared = 0);
+int embed_long_row();
+void embed_scratch(void *ws, int64_t n_rows, int64_t n_cols, unsigned **ctr, unsigned **list, double2 **rec);
 bool bitmap_path_ok(int wt, int64_t E, int64_t n_rows, int64_t n_cols, int directed);
 size_t bitmap_workspace(int64_t E, int64_t n, int directed);
 int bitmap_csr_build(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n, int directed,
                      int64_t *row_ptr, unsigned *row_cnt, unsigned char *row_flag, int32_t *col, double *val,
-                     unsigned deg_flags, double *deg, double *scale, void *ws, size_t ws_bytes, int32_t *err,
-                     cudaStream_t st);
+                     unsigned deg_flags, double *deg, double *scale, const int32_t *y32, const double *inv,
+                     unsigned laplacian, double2 *rec, unsigned *long_list, unsigned *n_long, int long_row,
+                     void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st);
 int validate_edges(const int64_t *, const int64_t *, const void *, int, int64_t, int64_t, int32_t *,
                    cudaStream_t);
 
@@ -176,11 +179,13 @@ int gee_profile_stop(void) {
 int gee_profile_read(float *ms, const char **names, int cap) {
     Profile &p = t_prof;
     if (p.n < 1) return 0;
-    GEE_CHECK_CUDA(cudaEventSynchronize(p.ev[p.n - 1]));
+    cudaError_t e = cudaEventSynchronize(p.ev[p.n - 1]);
+    if (e != cudaSuccess) return -cuda_status(e);
     int m = 0;
     for (int i = 1; i < p.n && m < cap; ++i, ++m) {
         float t = 0.f;
-        GEE_CHECK_CUDA(cudaEventElapsedTime(&t, p.ev[i - 1], p.ev[i]));
+        e = cudaEventElapsedTime(&t, p.ev[i - 1], p.ev[i]);
+        if (e != cudaSuccess) return -cuda_status(e);
         ms[m] = t;
         names[m] = p.name[i];
     }
@@ -296,12 +301,18 @@ int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, in
     const unsigned deg_flags = (flags & GEE_LAPLACIAN) ? (GEE_LAPLACIAN | (flags & GEE_DIAGONAL)) : 0u;
     const double *sc = (flags & GEE_LAPLACIAN) ? W.scale : nullptr;
     if (bitmap_path_ok(w_type, n_edges, n_nodes, n_nodes, directed)) {
-        // unit weights, small node count: column bitmaps per row, slot layout
+        // unit weights, small node count: column bitmaps per row (slot layout);
+        // the row pass also writes the embed's node records and long-row list
+        unsigned *ectr, *elist;
+        double2 *erec;
+        embed_scratch(W.emb_ws, n_nodes, n_nodes, &ectr, &elist, &erec);
+        GEE_CHECK_CUDA(cudaMemsetAsync(ectr, 0, 4 * sizeof(unsigned), st));
         rc = bitmap_csr_build(rows, cols, n_edges, n_nodes, directed, W.row_ptr, W.row_cnt, W.row_flag, W.col,
-                              W.val, deg_flags, W.deg, W.scale, W.csr_ws, W.csr_bytes, err, st);
+                              W.val, deg_flags, W.deg, W.scale, W.y32, W.inv, flags & GEE_LAPLACIAN, erec, elist,
+                              ectr, embed_long_row(), W.csr_ws, W.csr_bytes, err, st);
         if (rc) return rc;
         return embed(W.row_ptr, W.row_cnt, W.col, W.val, nullptr, W.row_flag, 0, n_nodes, n_nodes, W.y32, W.inv, sc,
-                     k, flags, z, k, W.emb_ws, W.emb_bytes, err, st);
+                     k, flags, z, k, W.emb_ws, W.emb_bytes, err, st, 1);
     }
     if (sort_path_ok(n_edges, n_nodes, n_nodes, directed)) {
         // compact CSR from the radix sort; values stay implicit (1.0) when the

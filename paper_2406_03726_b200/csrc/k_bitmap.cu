@@ -90,8 +90,14 @@ __global__ void __launch_bounds__(kBmThreads) k_bm_count(const int64_t *__restri
 }
 
 // part[g][r] -> exclusive prefix over g (each chunk's offset inside row r);
-// cnt[r] = total.  One warp per row, 32 chunks per step.
-__global__ void k_bm_reduce(unsigned *__restrict__ part, int G, int n, unsigned *__restrict__ cnt) {
+// cnt[r] = total.  One warp per row, 32 chunks per step.  The last CTA to
+// finish also turns cnt into the slot pointers (exclusive scan, n <= 16384),
+// so no separate scan launches are needed.
+__global__ void __launch_bounds__(1024) k_bm_reduce(unsigned *__restrict__ part, int G, int n,
+                                                    unsigned *__restrict__ cnt, int64_t *__restrict__ slot_ptr,
+                                                    unsigned *__restrict__ done) {
+    __shared__ unsigned red[33];
+    __shared__ bool last;
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -110,6 +116,27 @@ __global__ void k_bm_reduce(unsigned *__restrict__ part, int G, int n, unsigned 
             run += __shfl_sync(0xffffffffu, incl, 31);
         }
         if (lane == 0) cnt[r] = run;
+    }
+    // last-CTA-done: the final CTA sees every cnt[] and scans them
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int r0 = min(n, (int)threadIdx.x * per), r1 = min(n, r0 + per);
+    unsigned s = 0;
+    for (int r = r0; r < r1; ++r) s += __ldcg(cnt + r);
+    unsigned tot;
+    unsigned run = block_exclusive_scan(s, red, &tot);
+    for (int r = r0; r < r1; ++r) {
+        slot_ptr[r] = run;
+        run += __ldcg(cnt + r);
+    }
+    if (threadIdx.x == 0) {
+        slot_ptr[n] = tot;
+        *done = 0;  // reusable by the next launch / graph replay
     }
 }
 
@@ -158,6 +185,14 @@ struct BmRowsArgs {
     unsigned deg_flags;
     double *deg, *scale;
     int32_t *err;
+    // embed inputs produced here (one pass over rows): node records and the
+    // list of long rows gee_embed hands to whole CTAs
+    const int32_t *y32;
+    const double *inv;
+    unsigned laplacian;
+    double2 *rec;
+    unsigned *long_list, *n_long;
+    int long_row;
 };
 
 constexpr int kBmStage = 1536;  // per-warp staging of a row's sorted columns
@@ -231,10 +266,22 @@ __global__ void __launch_bounds__(kBmRowsThreads) k_bm_rows(BmRowsArgs a) {
             }
             if (lane == 0) atomicOr(a.has_multi, 1u);
         }
-        if (a.deg_flags && lane == 0) {
-            const double d = (double)L + ((a.deg_flags & GEE_DIAGONAL) ? 1.0 : 0.0);
-            a.deg[r] = d;
-            if (a.scale) a.scale[r] = laplacian_scale(d, a.err);
+        if (lane == 0) {
+            double sr = 1.0;
+            if (a.deg_flags) {
+                const double d = (double)L + ((a.deg_flags & GEE_DIAGONAL) ? 1.0 : 0.0);
+                a.deg[r] = d;
+                if (a.scale) {
+                    sr = laplacian_scale(d, a.err);
+                    a.scale[r] = sr;
+                }
+            }
+            if (a.rec) {
+                const int lab = a.y32[r];
+                const double g = lab < 0 ? 0.0 : (a.laplacian ? sr * a.inv[lab] : a.inv[lab]);
+                a.rec[r] = make_double2(__longlong_as_double((long long)(unsigned)lab), g);
+            }
+            if (a.long_list && (int)u > a.long_row) a.long_list[atomicAdd(a.n_long, 1u)] = (unsigned)r;
         }
         __syncwarp();
     }
@@ -252,19 +299,17 @@ struct BmWs {
     unsigned *part, *cnt, *flags;
     int64_t *slot_ptr;
     unsigned short *colbuf;
-    void *scan_ws;
     int G;
 };
 
 static void carve_bm(Carver &cv, BmWs &w, int64_t E, int64_t n, int directed) {
     const int64_t M = directed ? E : 2 * E;
-    w.G = num_sms();
+    w.G = 2 * num_sms();  // two 512-thread CTAs per SM for count/scatter
     w.part = cv.take<unsigned>((size_t)w.G * (size_t)n);
     w.cnt = cv.take<unsigned>((size_t)n + 1);
     w.flags = cv.take<unsigned>(4);
     w.slot_ptr = cv.take<int64_t>((size_t)n + 1);
     w.colbuf = cv.take<unsigned short>((size_t)(M > 0 ? M : 1));
-    w.scan_ws = cv.take<char>(scan_workspace(n));
 }
 
 size_t bitmap_workspace(int64_t E, int64_t n, int directed) {
@@ -276,11 +321,14 @@ size_t bitmap_workspace(int64_t E, int64_t n, int directed) {
 
 // Unit-weight CSR in the slot layout: row r's distinct columns at
 // [slot_ptr[r], slot_ptr[r] + row_cnt[r]); multiplicities in val only for
-// rows with row_flag[r] != 0.  row_ptr receives the slot pointers.
+// rows with row_flag[r] != 0.  row_ptr receives the slot pointers.  Also
+// emits the embed's node records and long-row list (rec/long_list/n_long,
+// n_long zeroed by the caller) so gee_embed needs no preparation launches.
 int bitmap_csr_build(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n, int directed,
                      int64_t *row_ptr, unsigned *row_cnt, unsigned char *row_flag, int32_t *col, double *val,
-                     unsigned deg_flags, double *deg, double *scale, void *ws, size_t ws_bytes, int32_t *err,
-                     cudaStream_t st) {
+                     unsigned deg_flags, double *deg, double *scale, const int32_t *y32, const double *inv,
+                     unsigned laplacian, double2 *rec, unsigned *long_list, unsigned *n_long, int long_row,
+                     void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st) {
     Carver cv(ws);
     BmWs W;
     carve_bm(cv, W, E, n, directed);
@@ -298,16 +346,12 @@ int bitmap_csr_build(const int64_t *rows, const int64_t *cols, int64_t E, int64_
     if (E > 0) {
         k_bm_count<<<W.G, kBmThreads, hsm, st>>>(rows, cols, E, directed, (int)n, W.part);
         GEE_CHECK_LAUNCH("k_bm_count");
-        k_bm_reduce<<<grid_for(n * 32, 256, 8), 256, 0, st>>>(W.part, W.G, (int)n, W.cnt);
-        GEE_CHECK_LAUNCH("k_bm_reduce");
-    } else {
-        GEE_CHECK_CUDA(cudaMemsetAsync(W.cnt, 0, sizeof(unsigned) * (size_t)(n + 1), st));
-    }
-    int rc = exclusive_scan_u32(W.cnt, n, row_ptr, W.scan_ws, st);
-    if (rc) return rc;
-    if (E > 0) {
+        k_bm_reduce<<<grid_for(n * 32, 1024, 2), 1024, 0, st>>>(W.part, W.G, (int)n, W.cnt, row_ptr, W.flags + 2);
+        GEE_CHECK_LAUNCH("k_bm_reduce_scan");
         k_bm_scatter<<<W.G, kBmThreads, hsm, st>>>(rows, cols, E, directed, (int)n, row_ptr, W.part, W.colbuf);
         GEE_CHECK_LAUNCH("k_bm_scatter");
+    } else {
+        GEE_CHECK_CUDA(cudaMemsetAsync(row_ptr, 0, sizeof(int64_t) * (size_t)(n + 1), st));
     }
     BmRowsArgs a;
     a.slot_ptr = row_ptr;
@@ -323,6 +367,13 @@ int bitmap_csr_build(const int64_t *rows, const int64_t *cols, int64_t E, int64_
     a.deg = deg;
     a.scale = (deg_flags & GEE_LAPLACIAN) ? scale : nullptr;
     a.err = err;
+    a.y32 = y32;
+    a.inv = inv;
+    a.laplacian = laplacian;
+    a.rec = rec;
+    a.long_list = long_list;
+    a.n_long = n_long;
+    a.long_row = long_row;
     const size_t rsm = (size_t)(kBmRowsThreads / 32) * (2 * (size_t)a.words + kBmStage) * 4;
     k_bm_rows<<<grid_for(n * 32, kBmRowsThreads, 8), kBmRowsThreads, rsm, st>>>(a);
     GEE_CHECK_LAUNCH("k_bm_rows");

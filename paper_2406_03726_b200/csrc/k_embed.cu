@@ -452,31 +452,57 @@ __global__ void k_node_rec(const int32_t *__restrict__ y32, const double *__rest
     }
 }
 
+// Embed workspace: [4] counters (n_long, work0, work1), the long-row list and
+// the node-record table.  A CSR builder that already knows row lengths and
+// degrees (the bitmap path) fills them itself and calls embed(prepared=1).
+struct EmbedScratch {
+    unsigned *ctr, *list;
+    double2 *rec;
+};
+
+static EmbedScratch carve_embed(Carver &cv, int64_t n_rows, int64_t n_cols) {
+    EmbedScratch s;
+    s.ctr = cv.take<unsigned>(4);
+    s.list = cv.take<unsigned>((size_t)n_rows + 1);
+    s.rec = cv.take<double2>((size_t)n_cols + 1);
+    return s;
+}
+
 size_t embed_workspace(int64_t n_rows, int64_t n_cols) {
     Carver cv(nullptr);
-    cv.take<unsigned>(4);
-    cv.take<unsigned>((size_t)n_rows + 1);
-    cv.take<double2>((size_t)n_cols + 1);
+    carve_embed(cv, n_rows, n_cols);
     return cv.bytes();
+}
+
+int embed_long_row() { return kLongRow; }
+
+void embed_scratch(void *ws, int64_t n_rows, int64_t n_cols, unsigned **ctr, unsigned **list, double2 **rec) {
+    Carver cv(ws);
+    EmbedScratch s = carve_embed(cv, n_rows, n_cols);
+    *ctr = s.ctr;
+    *list = s.list;
+    *rec = s.rec;
 }
 
 int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, const double *val,
           const unsigned *val_flags, const unsigned char *row_flag, int64_t rb, int64_t re, int64_t n_cols,
           const int32_t *y32, const double *inv, const double *scale, int k, unsigned flags, double *z, int64_t ldz,
-          void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st) {
+          void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st, int prepared) {
     const int64_t n = re - rb;
     Carver cv(ws);
-    unsigned *ctr = cv.take<unsigned>(4);
-    unsigned *list = cv.take<unsigned>((size_t)n + 1);
-    double2 *rec = cv.take<double2>((size_t)n_cols + 1);
+    EmbedScratch sc = carve_embed(cv, n, n_cols);
+    unsigned *ctr = sc.ctr, *list = sc.list;
+    double2 *rec = sc.rec;
     if (ws_bytes < cv.bytes()) return GEE_E_WORKSPACE;
     if (n <= 0) return GEE_OK;
-    GEE_CHECK_CUDA(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned), st));
-    k_node_rec<<<grid_for(n_cols, 256, 8), 256, 0, st>>>(y32, inv, (flags & GEE_LAPLACIAN) ? scale : nullptr,
-                                                          n_cols, rec);
-    GEE_CHECK_LAUNCH("k_node_rec");
-    k_embed_classify<<<grid_for(n, 256, 8), 256, 0, st>>>(row_ptr, row_cnt, rb, re, list, ctr);
-    GEE_CHECK_LAUNCH("k_embed_classify");
+    if (!prepared) {
+        GEE_CHECK_CUDA(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned), st));
+        k_node_rec<<<grid_for(n_cols, 256, 8), 256, 0, st>>>(y32, inv, (flags & GEE_LAPLACIAN) ? scale : nullptr,
+                                                              n_cols, rec);
+        GEE_CHECK_LAUNCH("k_node_rec");
+        k_embed_classify<<<grid_for(n, 256, 8), 256, 0, st>>>(row_ptr, row_cnt, rb, re, list, ctr);
+        GEE_CHECK_LAUNCH("k_embed_classify");
+    }
     EmbedArgs a;
     a.row_ptr = row_ptr;
     a.row_cnt = row_cnt;

@@ -64,8 +64,51 @@ __global__ void k_inv_counts(const unsigned long long *__restrict__ counts, int 
     }
 }
 
+// Small label vectors: one CTA does histogram, counts and 1/n_k in one launch
+// (no memset, no second kernel).
+__global__ void __launch_bounds__(1024) k_label_small(const int64_t *__restrict__ labels, int64_t n, int k,
+                                                      int32_t *__restrict__ y32, long long *__restrict__ counts,
+                                                      double *__restrict__ inv_nk, int32_t *err) {
+    extern __shared__ unsigned sh_hist[];
+    for (int c = threadIdx.x; c < k; c += blockDim.x) sh_hist[c] = 0;
+    __syncthreads();
+    const int64_t n_round = (n + 31) & ~int64_t(31);
+    for (int64_t i = threadIdx.x; i < n_round; i += blockDim.x) {
+        int lab = -1;
+        bool valid = false;
+        if (i < n) {
+            int64_t v = labels[i];
+            if (v < -1 || v >= k) {
+                raise_err(err, GEE_ERR_LABEL);
+                v = -1;
+            }
+            lab = (int)v;
+            y32[i] = lab;
+            valid = lab >= 0;
+        }
+        unsigned key = valid ? (unsigned)lab : 0xffffffffu;
+        unsigned peers = __match_any_sync(0xffffffffu, key);
+        if (valid && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh_hist[lab], __popc(peers));
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+        const unsigned m = sh_hist[c];
+        counts[c] = (long long)m;
+        inv_nk[c] = m ? __ddiv_rn(1.0, (double)m) : 0.0;
+    }
+}
+
+constexpr int64_t kLabelSmall = 1 << 18;
+
 int label_hist(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_t *counts,
                double *inv_nk, int32_t *err, cudaStream_t st) {
+    if (n <= kLabelSmall && k <= kHistSmemMax) {
+        k_label_small<<<1, 1024, sizeof(unsigned) * (size_t)k, st>>>(labels, n, k, y32,
+                                                                    reinterpret_cast<long long *>(counts),
+                                                                    inv_nk, err);
+        GEE_CHECK_LAUNCH("k_label_hist");
+        return GEE_OK;
+    }
     GEE_CHECK_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (size_t)k, st));
     if (n > 0) {
         const int threads = 512;
