@@ -57,6 +57,9 @@ int num_sms() {
 }
 
 int label_hist(const int64_t *, int64_t, int32_t, int32_t *, int64_t *, double *, int32_t *, cudaStream_t);
+size_t label_partial_words(int64_t n, int k);
+int label_hist_pipeline(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_t *counts, double *inv_nk,
+                        unsigned *partial, unsigned *done, int32_t *err, cudaStream_t st);
 size_t csr_build_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
 bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
 int set_force_buckets(int v);
@@ -109,6 +112,7 @@ struct EncodeWs {
     unsigned char *row_flag;
     int32_t *col;
     double *val;
+    unsigned *label_partial;
     void *csr_ws;
     size_t csr_bytes;
     void *emb_ws;
@@ -127,6 +131,7 @@ static size_t carve_encode(Carver &cv, EncodeWs &w, int64_t E, int64_t n, int32_
     w.row_flag = cv.take<unsigned char>((size_t)n + 1);
     w.col = cv.take<int32_t>((size_t)(M > 0 ? M : 1));
     w.val = cv.take<double>((size_t)(M > 0 ? M : 1));
+    w.label_partial = cv.take<unsigned>(label_partial_words(n, k));
     w.csr_bytes = bitmap_path_ok(wt, E, n, n, directed) ? bitmap_workspace(E, n, directed)
                                                          : csr_build_workspace(E, n, n, directed);
     w.csr_ws = cv.take<char>(w.csr_bytes);
@@ -296,17 +301,18 @@ int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, in
     EncodeWs W;
     size_t need = carve_encode(cv, W, n_edges, n_nodes, k, directed, w_type);
     if (ws_bytes < need || !ws) return GEE_E_WORKSPACE;
-    int rc = label_hist(labels, n_nodes, k, W.y32, W.counts, W.inv, err, st);
+    // control words: embed counters [0..2] and the label kernel's done word [3]
+    unsigned *ectr, *elist;
+    double2 *erec;
+    embed_scratch(W.emb_ws, n_nodes, n_nodes, &ectr, &elist, &erec);
+    GEE_CHECK_CUDA(cudaMemsetAsync(ectr, 0, 4 * sizeof(unsigned), st));
+    int rc = label_hist_pipeline(labels, n_nodes, k, W.y32, W.counts, W.inv, W.label_partial, ectr + 3, err, st);
     if (rc) return rc;
     const unsigned deg_flags = (flags & GEE_LAPLACIAN) ? (GEE_LAPLACIAN | (flags & GEE_DIAGONAL)) : 0u;
     const double *sc = (flags & GEE_LAPLACIAN) ? W.scale : nullptr;
     if (bitmap_path_ok(w_type, n_edges, n_nodes, n_nodes, directed)) {
         // unit weights, small node count: column bitmaps per row (slot layout);
         // the row pass also writes the embed's node records and long-row list
-        unsigned *ectr, *elist;
-        double2 *erec;
-        embed_scratch(W.emb_ws, n_nodes, n_nodes, &ectr, &elist, &erec);
-        GEE_CHECK_CUDA(cudaMemsetAsync(ectr, 0, 4 * sizeof(unsigned), st));
         rc = bitmap_csr_build(rows, cols, n_edges, n_nodes, directed, W.row_ptr, W.row_cnt, W.row_flag, W.col,
                               W.val, deg_flags, W.deg, W.scale, W.y32, W.inv, flags & GEE_LAPLACIAN, erec, elist,
                               ectr, embed_long_row(), W.csr_ws, W.csr_bytes, err, st);

@@ -90,32 +90,46 @@ __global__ void __launch_bounds__(kBmThreads) k_bm_count(const int64_t *__restri
 }
 
 // part[g][r] -> exclusive prefix over g (each chunk's offset inside row r);
-// cnt[r] = total.  One warp per row, 32 chunks per step.  The last CTA to
-// finish also turns cnt into the slot pointers (exclusive scan, n <= 16384),
-// so no separate scan launches are needed.
+// cnt[r] = total.  A CTA takes 32 consecutive rows: the [G x 32] tile is
+// staged in shared memory with coalesced loads (consecutive threads read
+// consecutive rows of one chunk), warp w scans row w across the chunks, and
+// the tile is written back coalesced.  The last CTA to finish also turns cnt
+// into the slot pointers (exclusive scan, n <= 16384), so no separate scan
+// launches are needed.
 __global__ void __launch_bounds__(1024) k_bm_reduce(unsigned *__restrict__ part, int G, int n,
                                                     unsigned *__restrict__ cnt, int64_t *__restrict__ slot_ptr,
                                                     unsigned *__restrict__ done) {
+    extern __shared__ unsigned tile[];  // [G][33]
     __shared__ unsigned red[33];
     __shared__ bool last;
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = warp; r < n; r += nwarps) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int r0 = blockIdx.x * 32;
+    const int nr = min(32, n - r0);
+    for (int i = threadIdx.x; i < G * 32; i += blockDim.x) {
+        const int g = i >> 5, c = i & 31;
+        tile[g * 33 + c] = c < nr ? part[(size_t)g * n + r0 + c] : 0u;
+    }
+    __syncthreads();
+    {
         unsigned run = 0;
         for (int g0 = 0; g0 < G; g0 += 32) {
             const int g = g0 + lane;
-            const unsigned x = g < G ? part[(size_t)g * n + r] : 0u;
+            const unsigned x = g < G ? tile[g * 33 + wid] : 0u;
             unsigned incl = x;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
-            if (g < G) part[(size_t)g * n + r] = run + incl - x;
+            if (g < G) tile[g * 33 + wid] = run + incl - x;
             run += __shfl_sync(0xffffffffu, incl, 31);
         }
-        if (lane == 0) cnt[r] = run;
+        if (lane == 0 && wid < nr) cnt[r0 + wid] = run;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < G * 32; i += blockDim.x) {
+        const int g = i >> 5, c = i & 31;
+        if (c < nr) part[(size_t)g * n + r0 + c] = tile[g * 33 + c];
     }
     // last-CTA-done: the final CTA sees every cnt[] and scans them
     __threadfence();
@@ -125,12 +139,12 @@ __global__ void __launch_bounds__(1024) k_bm_reduce(unsigned *__restrict__ part,
     if (!last) return;
     __threadfence();
     const int per = (n + blockDim.x - 1) / blockDim.x;
-    const int r0 = min(n, (int)threadIdx.x * per), r1 = min(n, r0 + per);
+    const int q0 = min(n, (int)threadIdx.x * per), q1 = min(n, q0 + per);
     unsigned s = 0;
-    for (int r = r0; r < r1; ++r) s += __ldcg(cnt + r);
+    for (int r = q0; r < q1; ++r) s += __ldcg(cnt + r);
     unsigned tot;
     unsigned run = block_exclusive_scan(s, red, &tot);
-    for (int r = r0; r < r1; ++r) {
+    for (int r = q0; r < q1; ++r) {
         slot_ptr[r] = run;
         run += __ldcg(cnt + r);
     }
@@ -346,7 +360,8 @@ int bitmap_csr_build(const int64_t *rows, const int64_t *cols, int64_t E, int64_
     if (E > 0) {
         k_bm_count<<<W.G, kBmThreads, hsm, st>>>(rows, cols, E, directed, (int)n, W.part);
         GEE_CHECK_LAUNCH("k_bm_count");
-        k_bm_reduce<<<grid_for(n * 32, 1024, 2), 1024, 0, st>>>(W.part, W.G, (int)n, W.cnt, row_ptr, W.flags + 2);
+        k_bm_reduce<<<(unsigned)((n + 31) / 32), 1024, sizeof(unsigned) * 33 * (size_t)W.G, st>>>(
+            W.part, W.G, (int)n, W.cnt, row_ptr, W.flags + 2);
         GEE_CHECK_LAUNCH("k_bm_reduce_scan");
         k_bm_scatter<<<W.G, kBmThreads, hsm, st>>>(rows, cols, E, directed, (int)n, row_ptr, W.part, W.colbuf);
         GEE_CHECK_LAUNCH("k_bm_scatter");

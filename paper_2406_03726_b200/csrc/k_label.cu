@@ -99,6 +99,77 @@ __global__ void __launch_bounds__(1024) k_label_small(const int64_t *__restrict_
 }
 
 constexpr int64_t kLabelSmall = 1 << 18;
+constexpr int kLabelMaxBlocks = 1024;
+
+// Pipeline variant: each CTA histograms a contiguous slice into its own row
+// of `partial` (no atomics on the result, no memset); the last CTA to finish
+// sums the rows into counts, computes 1/n_k and re-arms `done` for the next
+// launch or graph replay.
+__global__ void __launch_bounds__(1024) k_label_multi(const int64_t *__restrict__ labels, int64_t n, int k,
+                                                      int64_t per_block, int32_t *__restrict__ y32,
+                                                      unsigned *__restrict__ partial, long long *__restrict__ counts,
+                                                      double *__restrict__ inv_nk, unsigned *__restrict__ done,
+                                                      int32_t *err) {
+    extern __shared__ unsigned sh_hist[];
+    __shared__ bool last;
+    for (int c = threadIdx.x; c < k; c += blockDim.x) sh_hist[c] = 0;
+    __syncthreads();
+    const int64_t i0 = (int64_t)blockIdx.x * per_block;
+    const int64_t i1 = min(n, i0 + per_block);
+    for (int64_t b = i0; b < i1; b += 4 * (int64_t)blockDim.x) {
+        int64_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = b + u * (int64_t)blockDim.x + threadIdx.x;
+            v[u] = i < i1 ? labels[i] : -2;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = b + u * (int64_t)blockDim.x + threadIdx.x;
+            int lab = -1;
+            if (i < i1) {
+                int64_t x = v[u];
+                if (x < -1 || x >= k) {
+                    raise_err(err, GEE_ERR_LABEL);
+                    x = -1;
+                }
+                lab = (int)x;
+                y32[i] = lab;
+            }
+            const unsigned key = lab >= 0 ? (unsigned)lab : 0xffffffffu;
+            const unsigned peers = __match_any_sync(0xffffffffu, key);
+            if (lab >= 0 && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh_hist[lab], __popc(peers));
+        }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < k; c += blockDim.x) partial[(size_t)blockIdx.x * k + c] = sh_hist[c];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+        unsigned long long m = 0;
+        for (unsigned b = 0; b < gridDim.x; ++b) m += __ldcg(partial + (size_t)b * k + c);
+        counts[c] = (long long)m;
+        inv_nk[c] = m ? __ddiv_rn(1.0, (double)m) : 0.0;
+    }
+    if (threadIdx.x == 0) *done = 0;
+}
+
+size_t label_partial_words(int64_t n, int k) {
+    int64_t per = n > 2048 * (int64_t)kLabelMaxBlocks ? (n + kLabelMaxBlocks - 1) / kLabelMaxBlocks : 2048;
+    int64_t nb = (n + per - 1) / per;
+    if (nb < 1) nb = 1;
+    return (size_t)nb * (size_t)k;
+}
+
+// labels -> y32, counts, 1/n_k in one launch; `done` must be zero on the
+// first call (the kernel leaves it zero).  Falls back to label_hist for K
+// beyond the shared-memory histogram.
+int label_hist_pipeline(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_t *counts, double *inv_nk,
+                        unsigned *partial, unsigned *done, int32_t *err, cudaStream_t st);
 
 int label_hist(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_t *counts,
                double *inv_nk, int32_t *err, cudaStream_t st) {
@@ -122,6 +193,18 @@ int label_hist(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_
     k_inv_counts<<<(k + 255) / 256, 256, 0, st>>>(
         reinterpret_cast<const unsigned long long *>(counts), k, inv_nk);
     GEE_CHECK_LAUNCH("k_inv_counts");
+    return GEE_OK;
+}
+
+int label_hist_pipeline(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_t *counts, double *inv_nk,
+                        unsigned *partial, unsigned *done, int32_t *err, cudaStream_t st) {
+    if (k > kHistSmemMax || n <= 0) return label_hist(labels, n, k, y32, counts, inv_nk, err, st);
+    const int64_t per = n > 2048 * (int64_t)kLabelMaxBlocks ? (n + kLabelMaxBlocks - 1) / kLabelMaxBlocks : 2048;
+    const unsigned nb = (unsigned)((n + per - 1) / per);
+    k_label_multi<<<nb, 1024, sizeof(unsigned) * (size_t)k, st>>>(labels, n, k, per, y32, partial,
+                                                                 reinterpret_cast<long long *>(counts), inv_nk,
+                                                                 done, err);
+    GEE_CHECK_LAUNCH("k_label_hist");
     return GEE_OK;
 }
 
