@@ -30,6 +30,7 @@ constexpr int kEmbedWarps = kEmbedThreads / 32;
 constexpr int kLongRow = 4096;
 constexpr int kKTile = 1024;
 constexpr int kRowChunk = 32;  // rows per work grab (4 per warp)
+constexpr int kTabMax = 12288; // nodes whose table (9 B each) is staged in shared memory
 
 struct EmbedArgs {
     const int64_t *row_ptr;
@@ -116,12 +117,23 @@ __device__ __forceinline__ int4 ld_stream_i4(const int32_t *p) {
 // ---------------------------------------------------------------------------
 // K <= KP <= 8: register accumulators, one warp per row.
 // ---------------------------------------------------------------------------
-template <int KP>
-__device__ __forceinline__ void consume(const EmbedArgs &a, int64_t r, double s_r, int c, double v,
-                                        double (&acc)[KP], bool &found) {
+// Node table staged in shared memory (small graphs): 9 bytes per node.
+struct NodeTab {
+    const double *g;
+    const signed char *lab;
+};
+
+template <int KP, bool TAB>
+__device__ __forceinline__ void consume(const EmbedArgs &a, const NodeTab &tab, int64_t r, double s_r, int c,
+                                        double v, double (&acc)[KP], bool &found) {
     int lab;
     double g;
-    node_rec(a, c, lab, g);
+    if (TAB) {
+        lab = tab.lab[c];
+        g = tab.g[c];
+    } else {
+        node_rec(a, c, lab, g);
+    }
     if ((a.flags & GEE_DIAGONAL) && c == r) {
         v = v + 1.0;
         found = true;
@@ -133,8 +145,8 @@ __device__ __forceinline__ void consume(const EmbedArgs &a, int64_t r, double s_
     for (int q = 0; q < KP; ++q) acc[q] += (lab == q) ? x : 0.0;
 }
 
-template <int KP>
-__device__ void row_regs(const EmbedArgs &a, int64_t r) {
+template <int KP, bool TAB>
+__device__ void row_regs(const EmbedArgs &a, const NodeTab &tab, int64_t r) {
     const int lane = threadIdx.x & 31;
     int64_t s, e;
     row_extent(a, r, s, e);
@@ -147,7 +159,7 @@ __device__ void row_regs(const EmbedArgs &a, int64_t r) {
     // head up to a 16-byte boundary of col, body in 16-byte vectors (4 entries
     // per lane, 256 entries per warp per iteration), scalar tail
     const int64_t a0 = min(e, (s + 3) & ~int64_t(3));
-    if (s + lane < a0) consume<KP>(a, r, s_r, a.col[s + lane], val ? val[s + lane] : 1.0, acc, found);
+    if (s + lane < a0) consume<KP, TAB>(a, tab, r, s_r, a.col[s + lane], val ? val[s + lane] : 1.0, acc, found);
     // body: 4 x 16-byte column loads per lane in flight (512 entries per warp)
     const int64_t a1 = a0 + ((e - a0) & ~int64_t(511));
     for (int64_t p = a0 + 4 * lane; p < a1; p += 512) {
@@ -162,10 +174,10 @@ __device__ void row_regs(const EmbedArgs &a, int64_t r) {
                 const double2 x0 = __ldg(vp), x1 = __ldg(vp + 1);
                 v[0] = x0.x; v[1] = x0.y; v[2] = x1.x; v[3] = x1.y;
             }
-            consume<KP>(a, r, s_r, cc[u].x, v[0], acc, found);
-            consume<KP>(a, r, s_r, cc[u].y, v[1], acc, found);
-            consume<KP>(a, r, s_r, cc[u].z, v[2], acc, found);
-            consume<KP>(a, r, s_r, cc[u].w, v[3], acc, found);
+            consume<KP, TAB>(a, tab, r, s_r, cc[u].x, v[0], acc, found);
+            consume<KP, TAB>(a, tab, r, s_r, cc[u].y, v[1], acc, found);
+            consume<KP, TAB>(a, tab, r, s_r, cc[u].z, v[2], acc, found);
+            consume<KP, TAB>(a, tab, r, s_r, cc[u].w, v[3], acc, found);
         }
     }
     // remaining whole vectors, then the scalar tail
@@ -178,12 +190,12 @@ __device__ void row_regs(const EmbedArgs &a, int64_t r) {
             const double2 x0 = __ldg(vp), x1 = __ldg(vp + 1);
             v[0] = x0.x; v[1] = x0.y; v[2] = x1.x; v[3] = x1.y;
         }
-        consume<KP>(a, r, s_r, c4.x, v[0], acc, found);
-        consume<KP>(a, r, s_r, c4.y, v[1], acc, found);
-        consume<KP>(a, r, s_r, c4.z, v[2], acc, found);
-        consume<KP>(a, r, s_r, c4.w, v[3], acc, found);
+        consume<KP, TAB>(a, tab, r, s_r, c4.x, v[0], acc, found);
+        consume<KP, TAB>(a, tab, r, s_r, c4.y, v[1], acc, found);
+        consume<KP, TAB>(a, tab, r, s_r, c4.z, v[2], acc, found);
+        consume<KP, TAB>(a, tab, r, s_r, c4.w, v[3], acc, found);
     }
-    for (int64_t p = a2 + lane; p < e; p += 32) consume<KP>(a, r, s_r, a.col[p], val ? val[p] : 1.0, acc, found);
+    for (int64_t p = a2 + lane; p < e; p += 32) consume<KP, TAB>(a, tab, r, s_r, a.col[p], val ? val[p] : 1.0, acc, found);
     if (a.flags & GEE_DIAGONAL) {
         found = __any_sync(0xffffffffu, found);
         int lb;
@@ -373,8 +385,8 @@ __device__ void row_long(const EmbedArgs &a, int64_t r, double *zsm, double *xsm
     __syncthreads();
 }
 
-template <int KP>
-__global__ void __launch_bounds__(kEmbedThreads) k_embed(EmbedArgs a) {
+template <int KP, bool TAB>
+__global__ void __launch_bounds__(kEmbedThreads) k_embed(EmbedArgs a, int n_tab) {
     // values implicit (all exactly 1.0) when the sort path says so: skip the val stream
     if (a.val_flags && a.val_flags[0] == 0 && a.val_flags[1] == 0) a.val = nullptr;
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -384,6 +396,20 @@ __global__ void __launch_bounds__(kEmbedThreads) k_embed(EmbedArgs a) {
     double *zsm = reinterpret_cast<double *>(dsm);    // [warps][kt_max]
     double *xsm = zsm + (size_t)kEmbedWarps * kt_max;  // [warps][32]
     const int wid = threadIdx.x >> 5;
+    NodeTab tab{nullptr, nullptr};
+    if (TAB) {
+        // stage the node table on chip: g (8 B) and the label (1 B) per node
+        double *tg = xsm + (size_t)kEmbedWarps * 32;
+        signed char *tl = reinterpret_cast<signed char *>(tg + n_tab);
+        for (int j = threadIdx.x; j < n_tab; j += blockDim.x) {
+            const double2 rc = __ldg(a.rec + j);
+            tg[j] = rc.y;
+            tl[j] = (signed char)(int)(unsigned)(unsigned long long)__double_as_longlong(rc.x);
+        }
+        tab.g = tg;
+        tab.lab = tl;
+        __syncthreads();
+    }
     // phase 1: long rows, one CTA each
     const unsigned n_long = *a.n_long;
     for (;;) {
@@ -410,7 +436,7 @@ __global__ void __launch_bounds__(kEmbedThreads) k_embed(EmbedArgs a) {
             row_extent(a, r, s, e);
             if (e - s > kLongRow) continue;
             if (KP > 0)
-                row_regs<(KP > 0 ? KP : 1)>(a, r);
+                row_regs<(KP > 0 ? KP : 1), TAB>(a, tab, r);
             else
                 row_smem(a, r, zsm + wid * kt_max, xsm + wid * 32);
         }
@@ -523,33 +549,43 @@ int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, c
     a.val_flags = val_flags;
     a.row_flag = row_flag;
     const int kt_max = k < kKTile ? k : kKTile;
-    size_t smem = sizeof(double) * (size_t)kEmbedWarps * ((size_t)kt_max + 32);
+    const size_t base_smem = sizeof(double) * (size_t)kEmbedWarps * ((size_t)kt_max + 32);
+    // small graphs with K <= 8: node table (9 B/node) staged in shared memory
+    const bool tab = k <= 8 && n_cols <= kTabMax;
+    const size_t smem = base_smem + (tab ? 9 * (size_t)n_cols + 16 : 0);
     static bool attr = false;
     if (!attr) {
         size_t mx = sizeof(double) * (size_t)kEmbedWarps * ((size_t)kKTile + 32);
-        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
+        const int tmx = (int)(sizeof(double) * kEmbedWarps * (8 + 32) + 9 * kTabMax + 16);
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
         attr = true;
     }
     int occ = 0;
     const unsigned grid_cap = (unsigned)num_sms() * 8;
     unsigned grid;
-#define GEE_LAUNCH_EMBED(KP)                                                                                \
-    do {                                                                                                    \
-        GEE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_embed<KP>, kEmbedThreads, smem)); \
-        grid = (unsigned)num_sms() * (unsigned)(occ > 0 ? occ : 1);                                         \
-        if (grid > grid_cap) grid = grid_cap;                                                               \
-        k_embed<KP><<<grid, kEmbedThreads, smem, st>>>(a);                                                  \
+    const int n_tab = tab ? (int)n_cols : 0;
+#define GEE_LAUNCH_EMBED(KP, TB)                                                                              \
+    do {                                                                                                      \
+        GEE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_embed<KP, TB>, kEmbedThreads, smem)); \
+        grid = (unsigned)num_sms() * (unsigned)(occ > 0 ? occ : 1);                                           \
+        if (grid > grid_cap) grid = grid_cap;                                                                 \
+        k_embed<KP, TB><<<grid, kEmbedThreads, smem, st>>>(a, n_tab);                                         \
     } while (0)
-    if (k <= 1)
-        GEE_LAUNCH_EMBED(1);
-    else if (k <= 2)
-        GEE_LAUNCH_EMBED(2);
-    else if (k <= 4)
-        GEE_LAUNCH_EMBED(4);
-    else if (k <= 8)
-        GEE_LAUNCH_EMBED(8);
-    else
-        GEE_LAUNCH_EMBED(0);
+    if (k <= 1) {
+        if (tab) GEE_LAUNCH_EMBED(1, true); else GEE_LAUNCH_EMBED(1, false);
+    } else if (k <= 2) {
+        if (tab) GEE_LAUNCH_EMBED(2, true); else GEE_LAUNCH_EMBED(2, false);
+    } else if (k <= 4) {
+        if (tab) GEE_LAUNCH_EMBED(4, true); else GEE_LAUNCH_EMBED(4, false);
+    } else if (k <= 8) {
+        if (tab) GEE_LAUNCH_EMBED(8, true); else GEE_LAUNCH_EMBED(8, false);
+    } else {
+        GEE_LAUNCH_EMBED(0, false);
+    }
 #undef GEE_LAUNCH_EMBED
     GEE_CHECK_LAUNCH("k_embed");
     return GEE_OK;
