@@ -84,13 +84,15 @@ int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, c
           const int32_t *y32, const double *inv, const double *scale, int k, unsigned flags, double *z, int64_t ldz,
           void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st, int prepared = 0);
 int embed_long_row();
-void embed_scratch(void *ws, int64_t n_rows, int64_t n_cols, unsigned **ctr, unsigned **list, double2 **rec);
+void embed_scratch(void *ws, int64_t n_rows, int64_t n_cols, unsigned **ctr, unsigned **list, double2 **rec,
+                   double **tab_g, signed char **tab_lab);
 bool bitmap_path_ok(int wt, int64_t E, int64_t n_rows, int64_t n_cols, int directed);
 size_t bitmap_workspace(int64_t E, int64_t n, int directed);
 int bitmap_csr_build(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n, int directed,
                      int64_t *row_ptr, unsigned *row_cnt, unsigned char *row_flag, int32_t *col, double *val,
                      unsigned deg_flags, double *deg, double *scale, const int32_t *y32, const double *inv,
-                     unsigned laplacian, double2 *rec, unsigned *long_list, unsigned *n_long, int long_row,
+                     unsigned laplacian, double2 *rec, double *tab_g, signed char *tab_lab,
+                     unsigned *long_list, unsigned *n_long, int long_row,
                      void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st);
 int validate_edges(const int64_t *, const int64_t *, const void *, int, int64_t, int64_t, int32_t *,
                    cudaStream_t);
@@ -304,7 +306,9 @@ int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, in
     // control words: embed counters [0..2] and the label kernel's done word [3]
     unsigned *ectr, *elist;
     double2 *erec;
-    embed_scratch(W.emb_ws, n_nodes, n_nodes, &ectr, &elist, &erec);
+    double *etg;
+    signed char *etl;
+    embed_scratch(W.emb_ws, n_nodes, n_nodes, &ectr, &elist, &erec, &etg, &etl);
     GEE_CHECK_CUDA(cudaMemsetAsync(ectr, 0, 4 * sizeof(unsigned), st));
     int rc = label_hist_pipeline(labels, n_nodes, k, W.y32, W.counts, W.inv, W.label_partial, ectr + 3, err, st);
     if (rc) return rc;
@@ -314,7 +318,7 @@ int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, in
         // unit weights, small node count: column bitmaps per row (slot layout);
         // the row pass also writes the embed's node records and long-row list
         rc = bitmap_csr_build(rows, cols, n_edges, n_nodes, directed, W.row_ptr, W.row_cnt, W.row_flag, W.col,
-                              W.val, deg_flags, W.deg, W.scale, W.y32, W.inv, flags & GEE_LAPLACIAN, erec, elist,
+                              W.val, deg_flags, W.deg, W.scale, W.y32, W.inv, flags & GEE_LAPLACIAN, erec, etg, etl, elist,
                               ectr, embed_long_row(), W.csr_ws, W.csr_bytes, err, st);
         if (rc) return rc;
         return embed(W.row_ptr, W.row_cnt, W.col, W.val, nullptr, W.row_flag, 0, n_nodes, n_nodes, W.y32, W.inv, sc,

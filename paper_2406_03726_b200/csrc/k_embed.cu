@@ -50,6 +50,8 @@ struct EmbedArgs {
     unsigned *work;                // [2]
     const unsigned *val_flags;     // [2] from the sort path: both 0 => every value is 1.0
     const unsigned char *row_flag; // per row: 1 => read val for this row, 0 => values are 1.0
+    const double *tab_g;           // optional compact node table (g, label) to stage on chip
+    const signed char *tab_lab;
 };
 
 __device__ __forceinline__ void row_extent(const EmbedArgs &a, int64_t r, int64_t &s, int64_t &e) {
@@ -401,10 +403,18 @@ __global__ void __launch_bounds__(kEmbedThreads) k_embed(EmbedArgs a, int n_tab)
         // stage the node table on chip: g (8 B) and the label (1 B) per node
         double *tg = xsm + (size_t)kEmbedWarps * 32;
         signed char *tl = reinterpret_cast<signed char *>(tg + n_tab);
-        for (int j = threadIdx.x; j < n_tab; j += blockDim.x) {
-            const double2 rc = __ldg(a.rec + j);
-            tg[j] = rc.y;
-            tl[j] = (signed char)(int)(unsigned)(unsigned long long)__double_as_longlong(rc.x);
+        if (a.tab_g) {
+            // compact 9-byte/node source (written by the bitmap row pass)
+            for (int j = threadIdx.x; j < n_tab; j += blockDim.x) {
+                tg[j] = __ldcg(a.tab_g + j);
+                tl[j] = a.tab_lab[j];
+            }
+        } else {
+            for (int j = threadIdx.x; j < n_tab; j += blockDim.x) {
+                const double2 rc = __ldg(a.rec + j);
+                tg[j] = rc.y;
+                tl[j] = (signed char)(int)(unsigned)(unsigned long long)__double_as_longlong(rc.x);
+            }
         }
         tab.g = tg;
         tab.lab = tl;
@@ -484,6 +494,8 @@ __global__ void k_node_rec(const int32_t *__restrict__ y32, const double *__rest
 struct EmbedScratch {
     unsigned *ctr, *list;
     double2 *rec;
+    double *tab_g;
+    signed char *tab_lab;
 };
 
 static EmbedScratch carve_embed(Carver &cv, int64_t n_rows, int64_t n_cols) {
@@ -491,6 +503,9 @@ static EmbedScratch carve_embed(Carver &cv, int64_t n_rows, int64_t n_cols) {
     s.ctr = cv.take<unsigned>(4);
     s.list = cv.take<unsigned>((size_t)n_rows + 1);
     s.rec = cv.take<double2>((size_t)n_cols + 1);
+    const bool small = n_cols <= kTabMax;
+    s.tab_g = cv.take<double>(small ? (size_t)n_cols + 1 : 0);
+    s.tab_lab = cv.take<signed char>(small ? (size_t)n_cols + 1 : 0);
     return s;
 }
 
@@ -502,12 +517,15 @@ size_t embed_workspace(int64_t n_rows, int64_t n_cols) {
 
 int embed_long_row() { return kLongRow; }
 
-void embed_scratch(void *ws, int64_t n_rows, int64_t n_cols, unsigned **ctr, unsigned **list, double2 **rec) {
+void embed_scratch(void *ws, int64_t n_rows, int64_t n_cols, unsigned **ctr, unsigned **list, double2 **rec,
+                   double **tab_g, signed char **tab_lab) {
     Carver cv(ws);
     EmbedScratch s = carve_embed(cv, n_rows, n_cols);
     *ctr = s.ctr;
     *list = s.list;
     *rec = s.rec;
+    *tab_g = n_cols <= kTabMax ? s.tab_g : nullptr;
+    *tab_lab = n_cols <= kTabMax ? s.tab_lab : nullptr;
 }
 
 int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, const double *val,
@@ -548,6 +566,9 @@ int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, c
     a.work = ctr + 1;
     a.val_flags = val_flags;
     a.row_flag = row_flag;
+    // prepared by the bitmap row pass: the compact table is valid
+    a.tab_g = (prepared && n_cols <= kTabMax) ? sc.tab_g : nullptr;
+    a.tab_lab = (prepared && n_cols <= kTabMax) ? sc.tab_lab : nullptr;
     const int kt_max = k < kKTile ? k : kKTile;
     const size_t base_smem = sizeof(double) * (size_t)kEmbedWarps * ((size_t)kt_max + 32);
     // small graphs with K <= 8: node table (9 B/node) staged in shared memory
