@@ -402,13 +402,33 @@ __global__ void __launch_bounds__(kEmbedThreads) k_embed(EmbedArgs a, int n_tab)
     if (TAB) {
         // stage the node table on chip: g (8 B) and the label (1 B) per node
         double *tg = xsm + (size_t)kEmbedWarps * 32;
-        signed char *tl = reinterpret_cast<signed char *>(tg + n_tab);
+        signed char *tl = reinterpret_cast<signed char *>(tg + ((n_tab + 1) & ~1));  // 16-B aligned
         if (a.tab_g) {
-            // compact 9-byte/node source (written by the bitmap row pass)
-            for (int j = threadIdx.x; j < n_tab; j += blockDim.x) {
-                tg[j] = __ldcg(a.tab_g + j);
-                tl[j] = a.tab_lab[j];
+            // compact 9-byte/node source (written by the bitmap row pass):
+            // 16-byte loads, 4 in flight per thread, so staging is not a
+            // chain of dependent L2 round trips
+            const int n2 = n_tab / 2;
+            const double2 *src = reinterpret_cast<const double2 *>(a.tab_g);
+            double2 *dst = reinterpret_cast<double2 *>(tg);
+            for (int j0 = threadIdx.x; j0 < n2; j0 += 4 * blockDim.x) {
+                double2 v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j0 + u * blockDim.x;
+                    if (j < n2) v[u] = __ldcg(src + j);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j0 + u * blockDim.x;
+                    if (j < n2) dst[j] = v[u];
+                }
             }
+            if ((n_tab & 1) && threadIdx.x == 0) tg[n_tab - 1] = __ldcg(a.tab_g + n_tab - 1);
+            const int n16 = n_tab / 16;
+            const int4 *lsrc = reinterpret_cast<const int4 *>(a.tab_lab);
+            int4 *ldst = reinterpret_cast<int4 *>(tl);
+            for (int j = threadIdx.x; j < n16; j += blockDim.x) ldst[j] = __ldcg(lsrc + j);
+            for (int j = n16 * 16 + threadIdx.x; j < n_tab; j += blockDim.x) tl[j] = a.tab_lab[j];
         } else {
             for (int j = threadIdx.x; j < n_tab; j += blockDim.x) {
                 const double2 rc = __ldg(a.rec + j);
