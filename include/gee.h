@@ -87,6 +87,10 @@ int gee_validate_edges(const int64_t *rows, const int64_t *cols, const void *w, 
 int gee_label_hist(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_t *counts,
                    double *inv_nk, int32_t *err, void *stream);
 
+/* inv_nk[c] = 1.0 / counts[c] (0 for empty classes): used after the class
+ * histograms of row shards are all-reduced (multi-GPU, dist.py). */
+int gee_inv_counts(const int64_t *counts, int32_t k, double *inv_nk, void *stream);
+
 /* K2: edge list -> CSR with the reference's exact structure and values:
  * undirected lists are symmetrised in the order [originals, reversed
  * off-diagonals]; entries are ordered by (row, col); duplicates are summed

@@ -58,6 +58,7 @@ int num_sms() {
 
 int label_hist(const int64_t *, int64_t, int32_t, int32_t *, int64_t *, double *, int32_t *, cudaStream_t);
 size_t label_partial_words(int64_t n, int k);
+int inv_counts(const int64_t *counts, int32_t k, double *inv_nk, cudaStream_t st);
 int label_hist_pipeline(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_t *counts, double *inv_nk,
                         unsigned *partial, unsigned *done, int32_t *err, cudaStream_t st);
 size_t csr_build_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
@@ -210,6 +211,11 @@ int gee_label_hist(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, in
     if (n < 0 || k < 1 || !index_ok(n) || !y32 || !counts || !inv_nk) return GEE_E_ARG;
     if (n > 0 && !labels) return GEE_E_ARG;
     return label_hist(labels, n, k, y32, counts, inv_nk, err, (cudaStream_t)stream);
+}
+
+int gee_inv_counts(const int64_t *counts, int32_t k, double *inv_nk, void *stream) {
+    if (k < 1 || !counts || !inv_nk) return GEE_E_ARG;
+    return inv_counts(counts, k, inv_nk, (cudaStream_t)stream);
 }
 
 int gee_csr_build_workspace(int64_t n_edges, int64_t n_rows, int64_t n_cols, int directed, size_t *ws_bytes) {

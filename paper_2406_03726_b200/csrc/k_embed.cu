@@ -30,7 +30,10 @@ constexpr int kEmbedWarps = kEmbedThreads / 32;
 constexpr int kLongRow = 4096;
 constexpr int kKTile = 1024;
 constexpr int kRowChunk = 32;  // rows per work grab (4 per warp)
-constexpr int kTabMax = 12288; // nodes whose table (9 B each) is staged in shared memory
+// nodes whose table (9 B each) is staged in shared memory: only while it keeps
+// >= 4 CTAs per SM (measured: at N = 10^4 the 90 KB table halves occupancy
+// and loses to L1-resident 16-B record gathers, 68 us vs 50 us at cfg 1)
+constexpr int kTabMax = 4096;
 
 struct EmbedArgs {
     const int64_t *row_ptr;

@@ -196,6 +196,12 @@ int label_hist(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_
     return GEE_OK;
 }
 
+int inv_counts(const int64_t *counts, int32_t k, double *inv_nk, cudaStream_t st) {
+    k_inv_counts<<<(k + 255) / 256, 256, 0, st>>>(reinterpret_cast<const unsigned long long *>(counts), k, inv_nk);
+    GEE_CHECK_LAUNCH("k_inv_counts");
+    return GEE_OK;
+}
+
 int label_hist_pipeline(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_t *counts, double *inv_nk,
                         unsigned *partial, unsigned *done, int32_t *err, cudaStream_t st) {
     if (k > kHistSmemMax || n <= 0) return label_hist(labels, n, k, y32, counts, inv_nk, err, st);

@@ -1,0 +1,277 @@
+"""Row-sharded multi-GPU encode: one process per GPU, torch.distributed.
+
+Rows of Z are independent once every rank knows the per-node tables, so the
+graph is split into P contiguous row ranges holding equal numbers of stream
+entries.  Rank p owns rows [rb, re):
+
+  1. its slice of the symmetrised stream -- the entries whose row falls in
+     [rb, re), kept in stream order ([originals..., reversed...],
+     graph_io.py:82-88), so duplicate sums and hence the CSR are bitwise
+     identical to the unsharded build (shard-count invariance);
+  2. K1 on its label slice, then ALL-REDUCE(sum) of the class histogram
+     (int64, K) and ALL-GATHER of the int32 labels (every column's class is
+     needed by the embed);
+  3. K2+K3 on its stream slice: CSR rows and their degrees (a row's degree
+     depends only on its own entries);
+  4. under Laplacian, ALL-GATHER of the scale vector s = d^-1/2 (f64, N) --
+     the one real exchange of the algorithm: row r needs s_j of every
+     neighbour j, owned by other ranks;
+  5. K4 over rows [rb, re); Z stays row-sharded (gather_z collects it).
+
+The collectives are torch.distributed calls (NCCL over NVLink on the GPU
+box; gloo in the CPU tests).  The per-rank compute is an object with four
+methods; the product uses GpuShardOps (libgee).  tests/test_dist_gloo.py
+drives the same orchestration with an oracle-backed stand-in to prove
+shard-count invariance on CPU -- the product never constructs one.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _device, _lib
+
+
+# ---------------------------------------------------------------------------
+# host-side partitioning (data distribution, outside the timed region)
+# ---------------------------------------------------------------------------
+def stream_row_counts(rows, cols, n: int, directed: bool) -> np.ndarray:
+    """Entries per row of the symmetrised stream (numpy, int64[n])."""
+    rows = _np(rows)
+    cols = _np(cols)
+    cnt = np.bincount(rows, minlength=n)
+    if not directed:
+        off = rows != cols
+        cnt = cnt + np.bincount(cols[off], minlength=n)
+    return cnt.astype(np.int64)
+
+
+def row_ranges(row_counts, world: int) -> list[tuple[int, int]]:
+    """`world` contiguous row ranges with (nearly) equal stream entries."""
+    c = np.concatenate([[0], np.cumsum(np.asarray(row_counts, dtype=np.int64))])
+    n = len(c) - 1
+    total = int(c[-1])
+    bounds = [0]
+    for p in range(1, world):
+        target = total * p // world
+        b = int(np.searchsorted(c, target, side="left"))
+        bounds.append(min(max(b, bounds[-1]), n))
+    bounds.append(n)
+    return [(bounds[p], bounds[p + 1]) for p in range(world)]
+
+
+def local_stream(rows, cols, weights, directed: bool, rb: int, re: int):
+    """Stream entries whose row is in [rb, re), in stream order, as a
+    directed edge list (global node ids)."""
+    is_t = isinstance(rows, torch.Tensor)
+    cat = torch.cat if is_t else np.concatenate
+    in1 = (rows >= rb) & (rows < re)
+    r_parts, c_parts, w_parts = [rows[in1]], [cols[in1]], []
+    if weights is not None:
+        w_parts.append(weights[in1])
+    if not directed:
+        in2 = (cols >= rb) & (cols < re) & (rows != cols)
+        r_parts.append(cols[in2])
+        c_parts.append(rows[in2])
+        if weights is not None:
+            w_parts.append(weights[in2])
+    r = cat(r_parts)
+    c = cat(c_parts)
+    w = cat(w_parts) if weights is not None else None
+    return r, c, w
+
+
+def _np(x):
+    return x.cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
+
+
+# ---------------------------------------------------------------------------
+# collectives (equal-size padded all-gather works for gloo and NCCL alike)
+# ---------------------------------------------------------------------------
+def all_gather_ranges(local: torch.Tensor, ranges, group=None) -> torch.Tensor:
+    """Concatenate every rank's slice (lengths re-rb) into one full vector."""
+    world = len(ranges)
+    width = max(re - rb for rb, re in ranges)
+    buf = torch.zeros(width, dtype=local.dtype, device=local.device)
+    buf[: local.numel()] = local
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    return torch.cat([parts[p][: re - rb] for p, (rb, re) in enumerate(ranges)])
+
+
+# ---------------------------------------------------------------------------
+# per-rank compute on the GPU (libgee)
+# ---------------------------------------------------------------------------
+class GpuShardOps:
+    """K1..K4 for one row shard through the C ABI."""
+
+    def __init__(self, device):
+        self.dev = torch.device(device)
+        self.lib = _lib.load()
+
+    def label_hist(self, labels_slice, k):
+        lab = _device.to_device(labels_slice, torch.int64, self.dev)
+        n = lab.numel()
+        y32 = torch.empty(max(n, 1), dtype=torch.int32, device=self.dev)
+        counts = torch.empty(k, dtype=torch.int64, device=self.dev)
+        inv = torch.empty(k, dtype=torch.float64, device=self.dev)
+        err = _device.error_word(self.dev)
+        _lib.check(self.lib.gee_label_hist(_device.ptr(lab), n, k, _device.ptr(y32), _device.ptr(counts),
+                                           _device.ptr(inv), _device.ptr(err), _device.stream_handle()))
+        self._err = err
+        return y32[:n], counts
+
+    def inv_counts(self, counts):
+        inv = torch.empty(counts.numel(), dtype=torch.float64, device=self.dev)
+        _lib.check(self.lib.gee_inv_counts(_device.ptr(counts), counts.numel(), _device.ptr(inv),
+                                           _device.stream_handle()))
+        return inv
+
+    def csr_degree(self, r, c, w, n, flags):
+        """CSR of the shard's rows (global ids, other rows empty) + degrees/scale."""
+        e = int(r.numel())
+        if w is None:
+            wt = _lib.W_UNIT
+        else:
+            wt = _lib.W_F32 if w.dtype == torch.float32 else _lib.W_F64
+        cap = max(e, 1)
+        row_ptr = torch.empty(n + 1, dtype=torch.int64, device=self.dev)
+        col = torch.empty(cap, dtype=torch.int32, device=self.dev)
+        val = torch.empty(cap, dtype=torch.float64, device=self.dev)
+        deg = torch.empty(n, dtype=torch.float64, device=self.dev)
+        scale = torch.empty(n, dtype=torch.float64, device=self.dev)
+        err = _device.error_word(self.dev)
+        dflags = (_lib.LAPLACIAN | (flags & _lib.DIAGONAL)) if flags & _lib.LAPLACIAN else 0
+        nb = _lib.size_query(self.lib.gee_csr_build_workspace, e, n, n, 1)
+        ws = _device.WORKSPACE.get(nb, self.dev)
+        _lib.check(self.lib.gee_csr_build(
+            _device.ptr(r), _device.ptr(c), _device.ptr(w), wt, e, n, n, 1, 1, _device.ptr(row_ptr), None,
+            _device.ptr(col), _device.ptr(val), None, dflags, _device.ptr(deg), _device.ptr(scale),
+            _device.ptr(ws), ws.numel(), _device.ptr(err), _device.stream_handle()))
+        self._err2 = err
+        return (row_ptr, col, val), scale
+
+    def embed(self, csr, rb, re, n, y32, inv, scale, k, flags):
+        row_ptr, col, val = csr
+        z = torch.empty((re - rb, k), dtype=torch.float64, device=self.dev)
+        err = _device.error_word(self.dev)
+        nb = _lib.size_query(self.lib.gee_embed_workspace, re - rb, n)
+        ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=self.dev)
+        _lib.check(self.lib.gee_embed(
+            _device.ptr(row_ptr), None, _device.ptr(col), _device.ptr(val), rb, re, n, _device.ptr(y32),
+            _device.ptr(inv), _device.ptr(scale) if flags & _lib.LAPLACIAN else None, k, flags, _device.ptr(z), k,
+            _device.ptr(ws), ws.numel(), _device.ptr(err), _device.stream_handle()))
+        bits = int(self._err.item()) | int(self._err2.item()) | int(err.item())
+        _lib.raise_device_errors(bits, "sharded encode")
+        return z
+
+
+# ---------------------------------------------------------------------------
+# orchestration
+# ---------------------------------------------------------------------------
+def shard_plan(rows, cols, n, directed, world):
+    return row_ranges(stream_row_counts(rows, cols, n, directed), world)
+
+
+def encode_rows(ops, stream, labels, n, k, flags, ranges, rank, group=None):
+    """Steps 2-5 for rank `rank` given its stream slice; returns Z[rb:re]."""
+    rb, re = ranges[rank]
+    r, c, w = stream
+    y32_local, counts = ops.label_hist(labels[rb:re], k)
+    dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)        # class histogram
+    y32 = all_gather_ranges(y32_local, ranges, group)                   # labels of every column
+    inv = ops.inv_counts(counts)
+    csr, scale = ops.csr_degree(r, c, w, n, flags)
+    if flags & _lib.LAPLACIAN:
+        scale = all_gather_ranges(scale[rb:re].contiguous(), ranges, group)  # degree scale vector
+    return ops.embed(csr, rb, re, n, y32, inv, scale, k, flags)
+
+
+def encode_sharded(edges, labels, opts=None, group=None, ops=None):
+    """Row-sharded encode of an EdgeList replicated on every rank.  Returns
+    (z_local, (rb, re)): this rank's rows of Z."""
+    from .graph import options_flags
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    ops = ops or GpuShardOps(_device.require_gpu())
+    n, k = edges.n_nodes, labels.k_classes
+    flags = options_flags(opts)
+    ranges = shard_plan(edges.rows, edges.cols, n, edges.directed, world)
+    rb, re = ranges[rank]
+    dev = ops.dev
+    e = edges.to_device(dev)
+    _, w = e.weight_kind()
+    stream = local_stream(e.rows, e.cols, w, edges.directed, rb, re)
+    lab = _device.to_device(labels.labels, torch.int64, dev)
+    z = encode_rows(ops, stream, lab, n, k, flags, ranges, rank, group)
+    return z, (rb, re)
+
+
+def gather_z(z_local, ranges, group=None):
+    """Row-sharded Z -> full Z on every rank (optional gather)."""
+    k = z_local.shape[1]
+    width = max(re - rb for rb, re in ranges)
+    buf = torch.zeros((width, k), dtype=z_local.dtype, device=z_local.device)
+    buf[: z_local.shape[0]] = z_local
+    parts = [torch.empty_like(buf) for _ in ranges]
+    dist.all_gather(parts, buf, group=group)
+    return torch.cat([parts[p][: re - rb] for p, (rb, re) in enumerate(ranges)])
+
+
+# ---------------------------------------------------------------------------
+# bench.py under torchrun
+# ---------------------------------------------------------------------------
+def bench_sharded(args, rank, world, dev):
+    """Strong scaling of one config's step over `world` GPUs: every rank
+    builds the same seeded input, keeps its stream slice (outside the timed
+    region), then times label hist + collectives + CSR/degree + embed.
+    value = input edges / max-over-ranks step time."""
+    import json
+    import statistics
+    import sys
+
+    sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    from . import synth
+    cfg = synth.make_config(args.config, device=dev if args.config in (3, 4) else "cpu")
+    n, k, directed, flags = cfg["n"], cfg["k"], cfg["directed"], cfg["flags"]
+    rows = torch.as_tensor(cfg["rows"], device=dev)
+    cols = torch.as_tensor(cfg["cols"], device=dev)
+    w = torch.as_tensor(cfg["weights"], device=dev)
+    if bool((w == 1.0).all()):
+        w = None
+    lab = torch.as_tensor(cfg["labels"], device=dev)
+    ranges = shard_plan(rows, cols, n, directed, world)
+    rb, re = ranges[rank]
+    stream = local_stream(rows, cols, w, directed, rb, re)
+    ops = GpuShardOps(dev)
+    for _ in range(args.warmup):
+        encode_rows(ops, stream, lab, n, k, flags, ranges, rank)
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(args.steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        s, t = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        encode_rows(ops, stream, lab, n, k, flags, ranges, rank)
+        t.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        times.append(s.elapsed_time(t))
+    ms = torch.tensor([statistics.mean(times)], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        e = int(cfg["e"])
+        line = {"metric": "GEE edges/sec", "value": e / (float(ms) * 1e-3), "unit": "edges/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(ms),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded, BASELINE.json shapes)",
+                "config": {"workload": f"configs[{args.config}] {cfg['name']}", "n_nodes": n, "n_edges": e,
+                           "k_classes": k, "parallelism": f"row-sharded x{world} (NCCL all-reduce n_k, "
+                           "all-gather labels + Laplacian scale)"}}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0

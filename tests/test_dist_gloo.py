@@ -1,0 +1,136 @@
+"""Multi-GPU row sharding, exercised on CPU with the gloo backend (world 2).
+
+dist.encode_rows runs the real orchestration (all-reduce of the class
+histogram, all-gather of labels and of the Laplacian scale, row-range
+embed); the per-rank compute is an oracle-backed stand-in defined here (the
+product uses GpuShardOps).  Shard-count invariance: the assembled Z must be
+BITWISE equal to the unsharded reference pipeline, because every row is
+computed from exactly the same entries, degrees and scales.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+from paper_2406_03726_b200 import dist as gdist
+
+LAP, DIAG, CORR = 1, 2, 4
+
+
+class OracleShardOps:
+    """CPU stand-in for GpuShardOps built from the oracle (test only)."""
+
+    dev = torch.device("cpu")
+
+    def label_hist(self, labels_slice, k):
+        lab = labels_slice.numpy()
+        return torch.as_tensor(lab.astype(np.int32)), torch.as_tensor(O.class_counts(lab, k))
+
+    def inv_counts(self, counts):
+        c = counts.to(torch.float64)
+        return torch.where(c > 0, 1.0 / c, torch.zeros_like(c))
+
+    def csr_degree(self, r, c, w, n, flags):
+        w64 = np.ones(r.numel()) if w is None else w.numpy().astype(np.float64)
+        ip, cc, cv = O.coo_to_csr(r.numpy(), c.numpy(), w64, n, n)
+        if flags & DIAG:
+            dip, _, dcv = O.add_identity(ip, cc, cv, n)
+            deg = O.degree(dip, dcv, n)
+        else:
+            deg = O.degree(ip, cv, n)
+        scale = np.where(deg > 0, 1.0 / np.sqrt(np.where(deg > 0, deg, 1.0)), 0.0)
+        return (ip, cc, cv), torch.as_tensor(scale)
+
+    def embed(self, csr, rb, re, n, y32, inv, scale, k, flags):
+        ip, cc, cv = csr
+        if flags & DIAG:
+            ip, cc, cv = O.add_identity(ip, cc, cv, n)
+        if flags & LAP:
+            s = scale.numpy()
+            rid = np.repeat(np.arange(n), np.diff(ip))
+            v = cv * s[rid] * s[cc]
+            keep = v != 0.0
+            ptr = np.zeros(n + 1, np.int64)
+            np.cumsum(np.bincount(rid[keep], minlength=n), out=ptr[1:])
+            ip, cc, cv = ptr, cc[keep], v[keep]
+        z = O.spmm_onehot_dense(ip, cc, cv, y32.numpy().astype(np.int64), k)[rb:re]
+        if flags & CORR:
+            z = O.correlate_rows(z)
+        return torch.as_tensor(z)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _graph(seed, n=300, m=2000, k=4, directed=False, weighted=True):
+    rng = np.random.default_rng(seed)
+    rows = rng.integers(0, n, m)
+    cols = rng.integers(0, n, m)
+    rows[:40] = 7  # a hub row and duplicate coordinates
+    cols[:10] = 11
+    w = (1.0 - rng.random(m)) if weighted else np.ones(m)
+    labels = rng.integers(-1, k, n)
+    return n, rows, cols, w, labels, k, directed
+
+
+def _worker(rank, world, port, case, flags, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, rows, cols, w, labels, k, directed = case
+        ranges = gdist.shard_plan(rows, cols, n, directed, world)
+        rb, re = ranges[rank]
+        r, c, ww = gdist.local_stream(torch.as_tensor(rows), torch.as_tensor(cols), torch.as_tensor(w),
+                                      directed, rb, re)
+        z = gdist.encode_rows(OracleShardOps(), (r, c, ww), torch.as_tensor(labels), n, k, flags, ranges,
+                              rank)
+        full = gdist.gather_z(z, ranges)
+        if rank == 0:
+            out.put(full.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("flags", [0, LAP | DIAG | CORR, LAP, DIAG | CORR])
+@pytest.mark.parametrize("directed", [False, True])
+def test_two_rank_sharding_is_bitwise_shard_invariant(flags, directed):
+    case = _graph(3 + flags + directed, directed=directed)
+    n, rows, cols, w, labels, k, _ = case
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_worker, args=(2, _free_port(), case, flags, q), nprocs=2, join=True)
+    z = q.get(timeout=60)
+    st, zr, _ = O.encode_edges(rows, cols, w, n, directed, labels, k, flags)
+    assert st == O.OK
+    assert z.shape == zr.shape and np.array_equal(z, zr)
+
+
+def test_row_ranges_balance_stream_entries():
+    counts = np.array([5, 0, 0, 100, 1, 1, 1, 1, 50, 2])
+    rr = gdist.row_ranges(counts, 3)
+    assert rr[0][0] == 0 and rr[-1][1] == len(counts)
+    assert all(a[1] == b[0] for a, b in zip(rr, rr[1:]))
+    rr1 = gdist.row_ranges(counts, 1)
+    assert rr1 == [(0, len(counts))]
+
+
+def test_local_stream_keeps_stream_order():
+    rows = np.array([0, 2, 1, 2, 0])
+    cols = np.array([2, 1, 1, 0, 2])
+    w = np.array([1.0, 2.0, 3.0, 4.0, 5.0])
+    r, c, ww = gdist.local_stream(rows, cols, w, False, 2, 3)
+    # originals with row 2 (e=1, e=3) first, then reversed off-diagonals with col 2 (e=0, e=4)
+    assert r.tolist() == [2, 2, 2, 2] and c.tolist() == [1, 0, 0, 0]
+    assert ww.tolist() == [2.0, 4.0, 1.0, 5.0]
+    counts = gdist.stream_row_counts(rows, cols, 3, False)
+    # 5 originals + 4 reversed off-diagonals (e=2 is a self loop, counted once)
+    assert counts.tolist() == [3, 2, 4] and counts.sum() == 9
