@@ -27,7 +27,7 @@ int exclusive_scan_u32(const unsigned *in, int64_t n, int64_t *out, void *ws, cu
 size_t scan_workspace(int64_t n);
 
 constexpr int kBmMax = 16384;       // nodes (bitmap 2 KB + prefix 2 KB per warp)
-constexpr int kBmThreads = 512;
+constexpr int kBmThreads = 1024;
 constexpr int kBmRowsThreads = 256;
 
 // warp run-length aggregation of ctr[key] += 1 for lanes in `valid`
@@ -229,11 +229,19 @@ __global__ void __launch_bounds__(kBmRowsThreads) k_bm_rows(BmRowsArgs a) {
         const int L = (int)(a.slot_ptr[r + 1] - s);
         for (int i = lane; i < W; i += 32) bm[i] = 0u;
         __syncwarp();
-        unsigned dup = 0;
-        for (int i = lane; i < L; i += 32) {
-            const unsigned c = a.colbuf[s + i];
-            const unsigned bit = 1u << (c & 31);
-            dup |= atomicOr(&bm[c >> 5], bit) & bit;
+        // set bits with non-returning shared atomics (RED); duplicates show up
+        // as fewer distinct columns than stream entries (u < L), so no
+        // per-entry old-value check is needed
+        for (int i0 = lane; i0 < L; i0 += 128) {
+            unsigned c[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + 32 * u;
+                c[u] = i < L ? (unsigned)a.colbuf[s + i] : 0xffffffffu;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (c[u] != 0xffffffffu) atomicOr(&bm[c[u] >> 5], 1u << (c[u] & 31));
         }
         __syncwarp();
         // emission: lane l owns words [l*wpl, (l+1)*wpl); set bits leave in
@@ -266,7 +274,7 @@ __global__ void __launch_bounds__(kBmRowsThreads) k_bm_rows(BmRowsArgs a) {
         __syncwarp();
         if (staged)
             for (unsigned i = lane; i < u; i += 32) a.out_col[s + i] = (int32_t)stage[i];
-        const bool multi = __any_sync(0xffffffffu, dup != 0);
+        const bool multi = u < (unsigned)L;
         if (lane == 0) {
             a.row_cnt[r] = u;
             a.row_flag[r] = multi ? 1 : 0;
@@ -325,7 +333,7 @@ struct BmWs {
 
 static void carve_bm(Carver &cv, BmWs &w, int64_t E, int64_t n, int directed) {
     const int64_t M = directed ? E : 2 * E;
-    w.G = 2 * num_sms();  // two 512-thread CTAs per SM for count/scatter
+    w.G = num_sms();  // one 1024-thread CTA per SM for count/scatter
     w.part = cv.take<unsigned>((size_t)w.G * (size_t)n);
     w.cnt = cv.take<unsigned>((size_t)n + 1);
     w.flags = cv.take<unsigned>(4);
