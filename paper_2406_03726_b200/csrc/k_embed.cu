@@ -30,10 +30,11 @@ constexpr int kEmbedWarps = kEmbedThreads / 32;
 constexpr int kLongRow = 4096;
 constexpr int kKTile = 1024;
 constexpr int kRowChunk = 32;  // rows per work grab (4 per warp)
-// nodes whose table (9 B each) is staged in shared memory: only while it keeps
-// >= 4 CTAs per SM (measured: at N = 10^4 the 90 KB table halves occupancy
-// and loses to L1-resident 16-B record gathers, 68 us vs 50 us at cfg 1)
-constexpr int kTabMax = 4096;
+// nodes whose table (9 B each) is staged in shared memory, by one 1024-thread
+// CTA per SM so a single table copy serves 32 warps (with 256-thread CTAs the
+// 90 KB table at N = 10^4 halved occupancy and lost to L1 record gathers)
+constexpr int kTabMax = 12288;
+constexpr int kTabThreads = 1024;
 
 struct EmbedArgs {
     const int64_t *row_ptr;
@@ -161,6 +162,24 @@ __device__ void row_regs(const EmbedArgs &a, const NodeTab &tab, int64_t r) {
 #pragma unroll
     for (int q = 0; q < KP; ++q) acc[q] = 0.0;
     bool found = false;
+    if (TAB) {
+        // node table in shared memory: lane-consecutive entries (a row's
+        // columns are sorted, so one 32-lane gather spans ~32 nearby nodes and
+        // hits distinct banks), 8 coalesced 128-byte loads in flight per warp
+        for (int64_t p0 = s; p0 < e; p0 += 256) {
+            int cc[8];
+            double vv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t p = p0 + 32 * u + lane;
+                cc[u] = p < e ? __ldcs(a.col + p) : -1;
+                vv[u] = (val && p < e) ? val[p] : 1.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (cc[u] >= 0) consume<KP, TAB>(a, tab, r, s_r, cc[u], vv[u], acc, found);
+        }
+    } else {
     // head up to a 16-byte boundary of col, body in 16-byte vectors (4 entries
     // per lane, 256 entries per warp per iteration), scalar tail
     const int64_t a0 = min(e, (s + 3) & ~int64_t(3));
@@ -201,6 +220,7 @@ __device__ void row_regs(const EmbedArgs &a, const NodeTab &tab, int64_t r) {
         consume<KP, TAB>(a, tab, r, s_r, c4.w, v[3], acc, found);
     }
     for (int64_t p = a2 + lane; p < e; p += 32) consume<KP, TAB>(a, tab, r, s_r, a.col[p], val ? val[p] : 1.0, acc, found);
+    }
     if (a.flags & GEE_DIAGONAL) {
         found = __any_sync(0xffffffffu, found);
         int lb;
@@ -347,13 +367,13 @@ __device__ void row_long(const EmbedArgs &a, int64_t r, double *zsm, double *xsm
         const int t0 = t * kKTile, kt = min(kKTile, a.k - t0);
         for (int c = lane; c < kt; c += 32) zs[c] = 0.0;
         __syncwarp();
-        accumulate_tile(a, val, r, s_r, s, e, wid, kEmbedWarps, zs, xs, t0, kt, found);
+        accumulate_tile(a, val, r, s_r, s, e, wid, (int)(blockDim.x >> 5), zs, xs, t0, kt, found);
         const int f = __syncthreads_or(found ? 1 : 0);
         // combine warp tiles into warp 0's tile (column c read from every warp,
         // written only to warp 0's copy by the thread owning c)
         for (int c = threadIdx.x; c < kt; c += blockDim.x) {
             double v = 0.0;
-            for (int w = 0; w < kEmbedWarps; ++w) v += zsm[w * kt_max + c];
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += zsm[w * kt_max + c];
             zsm[c] = v;
         }
         __syncthreads();
@@ -390,8 +410,9 @@ __device__ void row_long(const EmbedArgs &a, int64_t r, double *zsm, double *xsm
     __syncthreads();
 }
 
-template <int KP, bool TAB>
-__global__ void __launch_bounds__(kEmbedThreads) k_embed(EmbedArgs a, int n_tab) {
+template <int KP, bool TAB, int NT>
+__global__ void __launch_bounds__(NT) k_embed(EmbedArgs a, int n_tab) {
+    constexpr int kWarps = NT / 32;
     // values implicit (all exactly 1.0) when the sort path says so: skip the val stream
     if (a.val_flags && a.val_flags[0] == 0 && a.val_flags[1] == 0) a.val = nullptr;
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -399,12 +420,12 @@ __global__ void __launch_bounds__(kEmbedThreads) k_embed(EmbedArgs a, int n_tab)
     __shared__ int task;
     const int kt_max = min(a.k, kKTile);
     double *zsm = reinterpret_cast<double *>(dsm);    // [warps][kt_max]
-    double *xsm = zsm + (size_t)kEmbedWarps * kt_max;  // [warps][32]
+    double *xsm = zsm + (size_t)kWarps * kt_max;  // [warps][32]
     const int wid = threadIdx.x >> 5;
     NodeTab tab{nullptr, nullptr};
     if (TAB) {
         // stage the node table on chip: g (8 B) and the label (1 B) per node
-        double *tg = xsm + (size_t)kEmbedWarps * 32;
+        double *tg = xsm + (size_t)kWarps * 32;
         signed char *tl = reinterpret_cast<signed char *>(tg + ((n_tab + 1) & ~1));  // 16-B aligned
         if (a.tab_g) {
             // compact 9-byte/node source (written by the bitmap row pass):
@@ -464,7 +485,7 @@ __global__ void __launch_bounds__(kEmbedThreads) k_embed(EmbedArgs a, int n_tab)
         if (t >= n_chunks) break;
         const int64_t r0 = a.row_begin + t * kRowChunk;
         const int64_t r1 = min(a.row_end, r0 + kRowChunk);
-        for (int64_t r = r0 + wid; r < r1; r += kEmbedWarps) {
+        for (int64_t r = r0 + wid; r < r1; r += kWarps) {
             int64_t s, e;
             row_extent(a, r, s, e);
             if (e - s > kLongRow) continue;
@@ -593,44 +614,48 @@ int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, c
     a.tab_g = (prepared && n_cols <= kTabMax) ? sc.tab_g : nullptr;
     a.tab_lab = (prepared && n_cols <= kTabMax) ? sc.tab_lab : nullptr;
     const int kt_max = k < kKTile ? k : kKTile;
-    const size_t base_smem = sizeof(double) * (size_t)kEmbedWarps * ((size_t)kt_max + 32);
     // small graphs with K <= 8: node table (9 B/node) staged in shared memory
+    // by one 1024-thread CTA per SM (one table copy serves 32 warps)
     const bool tab = k <= 8 && n_cols <= kTabMax;
-    const size_t smem = base_smem + (tab ? 9 * (size_t)n_cols + 16 : 0);
+    const int nt = tab ? kTabThreads : kEmbedThreads;
+    const size_t base_smem = sizeof(double) * (size_t)(nt / 32) * ((size_t)kt_max + 32);
+    const size_t smem = base_smem + (tab ? 9 * (size_t)n_cols + 32 : 0);
     static bool attr = false;
     if (!attr) {
         size_t mx = sizeof(double) * (size_t)kEmbedWarps * ((size_t)kKTile + 32);
-        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
-        const int tmx = (int)(sizeof(double) * kEmbedWarps * (8 + 32) + 9 * kTabMax + 16);
-        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
-        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
-        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
-        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<0, false, kEmbedThreads>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
+        const int tmx = (int)(sizeof(double) * (kTabThreads / 32) * (8 + 32) + 9 * kTabMax + 32);
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<1, true, kTabThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<2, true, kTabThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<4, true, kTabThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<8, true, kTabThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
         attr = true;
     }
     int occ = 0;
     const unsigned grid_cap = (unsigned)num_sms() * 8;
     unsigned grid;
     const int n_tab = tab ? (int)n_cols : 0;
-#define GEE_LAUNCH_EMBED(KP, TB)                                                                              \
-    do {                                                                                                      \
-        GEE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_embed<KP, TB>, kEmbedThreads, smem)); \
-        grid = (unsigned)num_sms() * (unsigned)(occ > 0 ? occ : 1);                                           \
-        if (grid > grid_cap) grid = grid_cap;                                                                 \
-        k_embed<KP, TB><<<grid, kEmbedThreads, smem, st>>>(a, n_tab);                                         \
+#define GEE_LAUNCH_EMBED(KP, TB, NT)                                                                         \
+    do {                                                                                                     \
+        GEE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_embed<KP, TB, NT>, NT, smem));  \
+        grid = (unsigned)num_sms() * (unsigned)(occ > 0 ? occ : 1);                                          \
+        if (grid > grid_cap) grid = grid_cap;                                                                \
+        k_embed<KP, TB, NT><<<grid, NT, smem, st>>>(a, n_tab);                                               \
     } while (0)
     if (k <= 1) {
-        if (tab) GEE_LAUNCH_EMBED(1, true); else GEE_LAUNCH_EMBED(1, false);
+        if (tab) GEE_LAUNCH_EMBED(1, true, kTabThreads); else GEE_LAUNCH_EMBED(1, false, kEmbedThreads);
     } else if (k <= 2) {
-        if (tab) GEE_LAUNCH_EMBED(2, true); else GEE_LAUNCH_EMBED(2, false);
+        if (tab) GEE_LAUNCH_EMBED(2, true, kTabThreads); else GEE_LAUNCH_EMBED(2, false, kEmbedThreads);
     } else if (k <= 4) {
-        if (tab) GEE_LAUNCH_EMBED(4, true); else GEE_LAUNCH_EMBED(4, false);
+        if (tab) GEE_LAUNCH_EMBED(4, true, kTabThreads); else GEE_LAUNCH_EMBED(4, false, kEmbedThreads);
     } else if (k <= 8) {
-        if (tab) GEE_LAUNCH_EMBED(8, true); else GEE_LAUNCH_EMBED(8, false);
+        if (tab) GEE_LAUNCH_EMBED(8, true, kTabThreads); else GEE_LAUNCH_EMBED(8, false, kEmbedThreads);
     } else {
-        GEE_LAUNCH_EMBED(0, false);
+        GEE_LAUNCH_EMBED(0, false, kEmbedThreads);
     }
 #undef GEE_LAUNCH_EMBED
+    (void)nt;
     GEE_CHECK_LAUNCH("k_embed");
     return GEE_OK;
 }
