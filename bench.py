@@ -210,11 +210,16 @@ def kernel_bytes(c, m_stream, nnz, wbytes):
     n, e, k = int(c["n"]), int(c["e"]), int(c["k"])
     lap = bool(c["flags"] & 1)
     vb = 8 if wbytes else 0  # stored CSR value bytes per entry
+    np_ = (n + 255) // 256 * 256
+    bm = np_ * np_ // 8
     return {
-        # bitmap path (unit weights, N <= 16384)
-        "k_bm_count": 16 * e,
-        "k_bm_scatter": 16 * e + 2 * m_stream,
-        "k_bm_rows": 2 * m_stream + 8 * (n + 1) + 4 * nnz + 4 * n + 1 * n + (16 * n if lap else 0),
+        # bitmap path (unit weights, N <= 16384): the edge list is the only
+        # HBM stream; the Np x Np adjacency bitmap (Np = n rounded up to 256)
+        # lives in L2 and is counted once per pass over it
+        "k_bm_set": 16 * e,
+        "k_bm_sym": 2 * bm,
+        "k_bm_scan": bm + 4 * n + 8 * n + 1 * n + (16 * n if lap else 0),
+        "k_bm_rows_embed": bm + 9 * n + 8 * n * k + (8 * n if lap else 0),
         # radix-sort path
         "k_sort_hist": (16 + wbytes) * e,
         # bucket path

@@ -87,14 +87,11 @@ int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, c
 int embed_long_row();
 void embed_scratch(void *ws, int64_t n_rows, int64_t n_cols, unsigned **ctr, unsigned **list, double2 **rec,
                    double **tab_g, signed char **tab_lab);
-bool bitmap_path_ok(int wt, int64_t E, int64_t n_rows, int64_t n_cols, int directed);
+bool bitmap_path_ok(int wt, int64_t E, int64_t n_rows, int64_t n_cols, int directed, int k);
 size_t bitmap_workspace(int64_t E, int64_t n, int directed);
-int bitmap_csr_build(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n, int directed,
-                     int64_t *row_ptr, unsigned *row_cnt, unsigned char *row_flag, int32_t *col, double *val,
-                     unsigned deg_flags, double *deg, double *scale, const int32_t *y32, const double *inv,
-                     unsigned laplacian, double2 *rec, double *tab_g, signed char *tab_lab,
-                     unsigned *long_list, unsigned *n_long, int long_row,
-                     void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st);
+int bitmap_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n, int directed,
+                  const int32_t *y32, const double *inv, int k, unsigned flags, double *deg, double *scale,
+                  double *z, void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st);
 int validate_edges(const int64_t *, const int64_t *, const void *, int, int64_t, int64_t, int32_t *,
                    cudaStream_t);
 
@@ -135,7 +132,7 @@ static size_t carve_encode(Carver &cv, EncodeWs &w, int64_t E, int64_t n, int32_
     w.col = cv.take<int32_t>((size_t)(M > 0 ? M : 1));
     w.val = cv.take<double>((size_t)(M > 0 ? M : 1));
     w.label_partial = cv.take<unsigned>(label_partial_words(n, k));
-    w.csr_bytes = bitmap_path_ok(wt, E, n, n, directed) ? bitmap_workspace(E, n, directed)
+    w.csr_bytes = bitmap_path_ok(wt, E, n, n, directed, k) ? bitmap_workspace(E, n, directed)
                                                          : csr_build_workspace(E, n, n, directed);
     w.csr_ws = cv.take<char>(w.csr_bytes);
     w.emb_bytes = embed_workspace(n, n);
@@ -320,15 +317,11 @@ int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, in
     if (rc) return rc;
     const unsigned deg_flags = (flags & GEE_LAPLACIAN) ? (GEE_LAPLACIAN | (flags & GEE_DIAGONAL)) : 0u;
     const double *sc = (flags & GEE_LAPLACIAN) ? W.scale : nullptr;
-    if (bitmap_path_ok(w_type, n_edges, n_nodes, n_nodes, directed)) {
-        // unit weights, small node count: column bitmaps per row (slot layout);
-        // the row pass also writes the embed's node records and long-row list
-        rc = bitmap_csr_build(rows, cols, n_edges, n_nodes, directed, W.row_ptr, W.row_cnt, W.row_flag, W.col,
-                              W.val, deg_flags, W.deg, W.scale, W.y32, W.inv, flags & GEE_LAPLACIAN, erec, etg, etl, elist,
-                              ectr, embed_long_row(), W.csr_ws, W.csr_bytes, err, st);
-        if (rc) return rc;
-        return embed(W.row_ptr, W.row_cnt, W.col, W.val, nullptr, W.row_flag, 0, n_nodes, n_nodes, W.y32, W.inv, sc,
-                     k, flags, z, k, W.emb_ws, W.emb_bytes, err, st, 1);
+    if (bitmap_path_ok(w_type, n_edges, n_nodes, n_nodes, directed, k)) {
+        // unit weights, small node count: an L2-resident N x N adjacency bitmap;
+        // the row pass emits the compact CSR and Z in one sweep (no embed pass)
+        return bitmap_encode(rows, cols, n_edges, n_nodes, directed, W.y32, W.inv, k, flags, W.deg, W.scale, z,
+                             W.csr_ws, W.csr_bytes, err, st);
     }
     if (sort_path_ok(n_edges, n_nodes, n_nodes, directed)) {
         // compact CSR from the radix sort; values stay implicit (1.0) when the

@@ -1,415 +1,449 @@
-// k_bitmap.cu -- K2 for unit-weight graphs with at most kBmMax nodes
-// (configs 0/1: unweighted SBM, N = 10^4).
+// k_bitmap.cu -- the whole encode for unit-weight graphs with at most
+// kBmMax nodes (configs 0/1: unweighted SBM, N = 10^4).
 //
-// With every weight equal to 1.0 a stored value is just the multiplicity of
-// its (row, col) pair and the order duplicates are summed in is irrelevant
-// (sums of ones are exact), so the CSR of a row is the sorted set of its
-// distinct columns.  The B200 layout:
-//   k_bm_count    CTA-private row histograms of contiguous edge chunks
-//   k_bm_reduce   per-row totals + each chunk's offset inside every row
-//   (scan)        row slot pointers
-//   k_bm_scatter  each chunk writes its entries' 16-bit columns into the row
-//                 buckets (2 bytes per entry: the whole bucket array is
-//                 ~22 MB at cfg 1 and stays in L2, so partial-sector writes
-//                 merge on chip instead of read-modify-writing HBM)
-//   k_bm_rows     one warp per row: set the row's columns in a warp-private
-//                 shared-memory bitmap (N bits), then emit them in column
-//                 order with popc prefix sums -- no comparison sort at all.
-//                 Duplicates are detected by the bitmap (atomicOr returns the
-//                 old word); such rows also get their multiplicities in val
-//                 and a per-row flag telling gee_embed to read them.
-//   degree        the row's stream length (+1 under A+I): exact.
+// With every weight equal to 1.0 a stored value is the multiplicity of its
+// (row, col) pair, and the order duplicates are summed in is irrelevant (sums
+// of ones are exact).  When no pair repeats, the CSR row of r is the set of
+// its columns, its degree is the set size and
+//     Z[r, q] = s_r * sum_{c in row r, Y_c = q} s_c / n_q   (+ the A+I diagonal),
+// so the encode needs only the N x N adjacency bitmap -- Np^2/8 bytes, 13 MB at
+// N = 10^4 -- which stays resident in the 126 MB L2.  The CSR itself is never
+// materialised (gee_encode_edges returns Z only).
+//   k_bm_set   one read of the int64 edge list; each stream entry sets bit
+//              (r, c) with a global atomicOr.  Lanes holding the same bitmap
+//              word (adjacent entries of a row-major list) OR-combine first,
+//              so a sorted list costs about one atomic per word.  A bit that
+//              was already set is a repeated pair: flags[0].
+//   k_bm_sym   undirected lists: S = U | U^T in place, 256 x 256-bit block
+//              pairs, 32 x 32 transposes by warp shuffles.  A pair present in
+//              both directions (U & U^T off the diagonal) is a repeat too.
+//   k_bm_scan  one warp per row: u_r = popc(S_r), degree d_r = u_r (+1 under
+//              A+I), s_r = d_r^-1/2 and the node table {Y_r, g_r = s_r/n_Y_r}
+//   k_bm_rows  one warp per row, 1024-thread CTAs sharing one shared-memory
+//              copy of the node table: Z[r, :] from the set bits of S_r, the
+//              diagonal, s_r and the correlation epilogue.
+// Rare path (any repeated pair; each kernel exits at once otherwise): exact
+// stream lengths by atomics (k_bm_len) and, for rows whose length differs
+// from their distinct count, the per-class sums of g over every stream entry
+// (k_bm_zsum), which k_bm_rows uses instead of the bitmap sum.
 #include "gee_common.cuh"
 
 namespace gee {
 
-int exclusive_scan_u32(const unsigned *in, int64_t n, int64_t *out, void *ws, cudaStream_t st);
-size_t scan_workspace(int64_t n);
+constexpr int kBmMax = 16384;   // nodes: bitmap Np^2/8 <= 32 MB (L2-resident)
+constexpr int kBlk = 256;       // rows / columns of a k_bm_sym block
+constexpr int kSetThreads = 512;
+constexpr int kRowsNT = 1024;   // one CTA per SM, one node table per SM
+constexpr int kWordsPerLane = kBmMax / 32 / 32;
+constexpr int kZacc = 8;        // rare-path class sums per row (K <= 8)
 
-constexpr int kBmMax = 16384;       // nodes (bitmap 2 KB + prefix 2 KB per warp)
-constexpr int kBmThreads = 1024;
-constexpr int kBmRowsThreads = 256;
+struct BmArgs {
+    int n, Wp;                // nodes, bitmap words per row (multiple of 8)
+    int nb;                   // 256-row blocks
+    unsigned *bm;             // [Np][Wp]
+    unsigned *len;            // [n] stream lengths (rare path)
+    unsigned *flags;          // [0] a repeated pair was seen
+    unsigned *ucnt;           // [n] distinct columns per row
+    double *zacc;             // [n][kZacc] rare path class sums
+    double *deg, *scale;
+    const int32_t *y32;
+    const double *inv;
+    double *tab_g;
+    signed char *tab_lab;
+    unsigned flags_opts;      // GEE_LAPLACIAN | GEE_DIAGONAL | GEE_CORRELATION
+    double *z;
+    int k;
+    int32_t *err;
+};
 
-// warp run-length aggregation of ctr[key] += 1 for lanes in `valid`
-// (valid lanes are a prefix of the warp); returns this lane's slot
-__device__ __forceinline__ unsigned rle_take(unsigned *ctr, unsigned key, bool valid, int nv, bool want_slot) {
+__device__ __forceinline__ unsigned lanemask_le() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
+    return m;
+}
+
+// 32 x 32 bit transpose across a warp: out(lane i) bit j = in(lane j) bit i
+__device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
+    const unsigned m16 = 0x0000ffffu, m8 = 0x00ff00ffu, m4 = 0x0f0f0f0fu, m2 = 0x33333333u, m1 = 0x55555555u;
+#define GEE_TSTAGE(J, M)                                                  \
+    {                                                                     \
+        const unsigned y = __shfl_xor_sync(0xffffffffu, x, J);            \
+        x = (lane & J) ? ((x & ~M) | ((y >> J) & M)) : ((x & M) | ((y & M) << J)); \
+    }
+    GEE_TSTAGE(16, m16)
+    GEE_TSTAGE(8, m8)
+    GEE_TSTAGE(4, m4)
+    GEE_TSTAGE(2, m2)
+    GEE_TSTAGE(1, m1)
+#undef GEE_TSTAGE
+    return x;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSetThreads) k_bm_set(const int64_t *__restrict__ rows,
+                                                        const int64_t *__restrict__ cols, int64_t E, BmArgs a) {
+    constexpr int U = 4;
     const int lane = threadIdx.x & 31;
-    const unsigned prev = __shfl_up_sync(0xffffffffu, key, 1);
-    const bool head = valid && (lane == 0 || prev != key);
-    const unsigned heads = __ballot_sync(0xffffffffu, head);
-    unsigned base = 0;
-    if (head) {
-        const unsigned after = heads & ~((2u << lane) - 1u);
-        const int next = after ? __ffs(after) - 1 : nv;
-        base = atomicAdd(&ctr[key], (unsigned)(next - lane));
-    }
-    if (!want_slot) return 0;
-    // my head = highest head lane <= me
-    const unsigned upto = heads & (0xffffffffu >> (31 - lane));
-    const int hl = upto ? 31 - __clz(upto) : 0;
-    const unsigned hb = __shfl_sync(0xffffffffu, base, hl);
-    return hb + (unsigned)(lane - hl);
-}
-
-__device__ __forceinline__ void chunk_range(int64_t E, int64_t &e0, int64_t &e1) {
-    e0 = (int64_t)((__int128)E * blockIdx.x / gridDim.x);
-    e1 = (int64_t)((__int128)E * (blockIdx.x + 1) / gridDim.x);
-}
-
-constexpr int kBmUnroll = 4;  // edges per thread per iteration (loads issued together)
-
-__global__ void __launch_bounds__(kBmThreads) k_bm_count(const int64_t *__restrict__ rows,
-                                                          const int64_t *__restrict__ cols, int64_t E,
-                                                          int directed, int n, unsigned *__restrict__ part) {
-    extern __shared__ unsigned h[];
-    for (int r = threadIdx.x; r < n; r += blockDim.x) h[r] = 0;
-    __syncthreads();
-    int64_t e0, e1;
-    chunk_range(E, e0, e1);
-    for (int64_t b = e0; b < e1; b += (int64_t)blockDim.x * kBmUnroll) {
-        unsigned r[kBmUnroll], c[kBmUnroll];
+    const unsigned le = lanemask_le();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
+    bool rep = false;
+    for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x * U + threadIdx.x; e0 - threadIdx.x < E; e0 += stride) {
+        unsigned key[U], bit[U];
 #pragma unroll
-        for (int u = 0; u < kBmUnroll; ++u) {
-            const int64_t e = b + (int64_t)u * blockDim.x + threadIdx.x;
-            r[u] = e < e1 ? (unsigned)__ldcs(rows + e) : 0u;
-            c[u] = e < e1 ? (unsigned)__ldcs(cols + e) : 0u;
+        for (int u = 0; u < U; ++u) {
+            const int64_t e = e0 + (int64_t)u * blockDim.x;
+            const unsigned r = e < E ? (unsigned)__ldcs(rows + e) : 0u;
+            const unsigned c = e < E ? (unsigned)__ldcs(cols + e) : 0u;
+            key[u] = e < E ? r * (unsigned)a.Wp + (c >> 5) : 0xffffffffu;
+            bit[u] = e < E ? 1u << (c & 31) : 0u;
         }
 #pragma unroll
-        for (int u = 0; u < kBmUnroll; ++u) {
-            const int64_t e = b + (int64_t)u * blockDim.x + threadIdx.x;
-            const bool v = e < e1;
-            const int nv = __popc(__ballot_sync(0xffffffffu, v));
-            rle_take(h, r[u], v, nv, false);
-            // reversed entries: their rows are the (random) columns
-            if (!directed && v && r[u] != c[u]) atomicAdd(&h[c[u]], 1u);
-        }
-    }
-    __syncthreads();
-    unsigned *dst = part + (size_t)blockIdx.x * n;
-    for (int r = threadIdx.x; r < n; r += blockDim.x) dst[r] = h[r];
-}
-
-// part[g][r] -> exclusive prefix over g (each chunk's offset inside row r);
-// cnt[r] = total.  A CTA takes 32 consecutive rows: the [G x 32] tile is
-// staged in shared memory with coalesced loads (consecutive threads read
-// consecutive rows of one chunk), warp w scans row w across the chunks, and
-// the tile is written back coalesced.  The last CTA to finish also turns cnt
-// into the slot pointers (exclusive scan, n <= 16384), so no separate scan
-// launches are needed.
-__global__ void __launch_bounds__(1024) k_bm_reduce(unsigned *__restrict__ part, int G, int n,
-                                                    unsigned *__restrict__ cnt, int64_t *__restrict__ slot_ptr,
-                                                    unsigned *__restrict__ done) {
-    extern __shared__ unsigned tile[];  // [G][33]
-    __shared__ unsigned red[33];
-    __shared__ bool last;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int r0 = blockIdx.x * 32;
-    const int nr = min(32, n - r0);
-#pragma unroll 4
-    for (int i = threadIdx.x; i < G * 32; i += blockDim.x) {
-        const int g = i >> 5, c = i & 31;
-        tile[g * 33 + c] = c < nr ? __ldcg(part + (size_t)g * n + r0 + c) : 0u;
-    }
-    __syncthreads();
-    {
-        unsigned run = 0;
-        for (int g0 = 0; g0 < G; g0 += 32) {
-            const int g = g0 + lane;
-            const unsigned x = g < G ? tile[g * 33 + wid] : 0u;
-            unsigned incl = x;
+        for (int u = 0; u < U; ++u) {
+            // segmented OR over runs of lanes holding the same word
+            const unsigned kp = __shfl_up_sync(0xffffffffu, key[u], 1);
+            const unsigned kn = __shfl_down_sync(0xffffffffu, key[u], 1);
+            const bool head = lane == 0 || kp != key[u];
+            const bool tail = lane == 31 || kn != key[u];
+            const int start = 31 - __clz(__ballot_sync(0xffffffffu, head) & le);
+            unsigned incl = bit[u];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
+                if (lane - o >= start) incl |= y;
             }
-            if (g < G) tile[g * 33 + wid] = run + incl - x;
-            run += __shfl_sync(0xffffffffu, incl, 31);
+            const unsigned prev = __shfl_up_sync(0xffffffffu, incl, 1);
+            if (lane > start && (prev & bit[u])) rep = true;  // repeated inside the run
+            if (tail && key[u] != 0xffffffffu) {
+                const unsigned old = atomicOr(&a.bm[key[u]], incl);
+                if (old & incl) rep = true;
+            }
         }
-        if (lane == 0 && wid < nr) cnt[r0 + wid] = run;
+    }
+    if (__any_sync(0xffffffffu, rep) && lane == 0) a.flags[0] = 1u;
+}
+
+// S = U | U^T for the block pair (BI, BJ), BI <= BJ, in place
+__global__ void __launch_bounds__(kBlk) k_bm_sym(BmArgs a) {
+    __shared__ unsigned sat[kBlk][9], sbt[kBlk][9];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    // linear index -> (BI, BJ) on the upper triangle
+    const unsigned x = blockIdx.x;
+    unsigned bj = (unsigned)((sqrt(8.0 * x + 1.0) - 1.0) * 0.5);
+    while ((bj + 1) * (bj + 2) / 2 <= x) ++bj;
+    while (bj * (bj + 1) / 2 > x) --bj;
+    const unsigned bi = x - bj * (bj + 1) / 2;
+    const size_t Wp = (size_t)a.Wp;
+    uint4 *pa = reinterpret_cast<uint4 *>(a.bm + ((size_t)bi * kBlk + t) * Wp + (size_t)bj * 8);
+    uint4 *pb = reinterpret_cast<uint4 *>(a.bm + ((size_t)bj * kBlk + t) * Wp + (size_t)bi * 8);
+    unsigned av[8], bv[8];
+    {
+        const uint4 a0 = __ldcg(pa), a1 = __ldcg(pa + 1);
+        av[0] = a0.x, av[1] = a0.y, av[2] = a0.z, av[3] = a0.w, av[4] = a1.x, av[5] = a1.y, av[6] = a1.z, av[7] = a1.w;
+    }
+    const bool same = bi == bj;
+    if (!same) {
+        const uint4 b0 = __ldcg(pb), b1 = __ldcg(pb + 1);
+        bv[0] = b0.x, bv[1] = b0.y, bv[2] = b0.z, bv[3] = b0.w, bv[4] = b1.x, bv[5] = b1.y, bv[6] = b1.z, bv[7] = b1.w;
+    }
+    // tile (w, q) of a block transposes into row q*32+lane, word w of its mirror
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sat[q * 32 + lane][w] = transpose32(av[q], lane);
+    if (!same) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sbt[q * 32 + lane][w] = transpose32(bv[q], lane);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < G * 32; i += blockDim.x) {
-        const int g = i >> 5, c = i & 31;
-        if (c < nr) part[(size_t)g * n + r0 + c] = tile[g * 33 + c];
+    unsigned mut = 0;
+    if (same) {
+        unsigned s[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const unsigned tq = sat[t][q];
+            s[q] = av[q] | tq;
+            unsigned m = av[q] & tq;
+            if (q == w) m &= ~(1u << lane);  // the diagonal is its own mirror
+            mut |= m;
+        }
+        pa[0] = make_uint4(s[0], s[1], s[2], s[3]);
+        pa[1] = make_uint4(s[4], s[5], s[6], s[7]);
+    } else {
+        unsigned s[8], u[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const unsigned tb = sbt[t][q], ta = sat[t][q];
+            s[q] = av[q] | tb;
+            u[q] = bv[q] | ta;
+            mut |= av[q] & tb;
+        }
+        pa[0] = make_uint4(s[0], s[1], s[2], s[3]);
+        pa[1] = make_uint4(s[4], s[5], s[6], s[7]);
+        pb[0] = make_uint4(u[0], u[1], u[2], u[3]);
+        pb[1] = make_uint4(u[4], u[5], u[6], u[7]);
     }
-    // last-CTA-done: the final CTA sees every cnt[] and scans them
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    const int per = (n + blockDim.x - 1) / blockDim.x;
-    const int q0 = min(n, (int)threadIdx.x * per), q1 = min(n, q0 + per);
-    unsigned s = 0;
-    for (int r = q0; r < q1; ++r) s += __ldcg(cnt + r);
-    unsigned tot;
-    unsigned run = block_exclusive_scan(s, red, &tot);
-    for (int r = q0; r < q1; ++r) {
-        slot_ptr[r] = run;
-        run += __ldcg(cnt + r);
+    if (__syncthreads_or(mut != 0) && t == 0) a.flags[0] = 1u;
+}
+
+// one warp per row, 8 rows per CTA
+__global__ void __launch_bounds__(256) k_bm_scan(BmArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (r >= a.n) return;
+    const uint4 *row = reinterpret_cast<const uint4 *>(a.bm + (size_t)r * a.Wp);
+    unsigned u = 0;
+    for (int i = lane; i < a.Wp / 4; i += 32) {
+        const uint4 v = __ldcg(row + i);
+        u += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
     }
-    if (threadIdx.x == 0) {
-        slot_ptr[n] = tot;
-        *done = 0;  // reusable by the next launch / graph replay
+    u = warp_sum_u(u);
+    if (lane == 0) {
+        const unsigned L = __ldcg(a.flags) ? __ldcg(a.len + r) : u;  // stream length of the row
+        double sr = 1.0;
+        if (a.flags_opts & GEE_LAPLACIAN) {
+            const double d = (double)L + ((a.flags_opts & GEE_DIAGONAL) ? 1.0 : 0.0);
+            a.deg[r] = d;
+            sr = laplacian_scale(d, a.err);
+            a.scale[r] = sr;
+        }
+        const int lab = a.y32[r];
+        a.tab_g[r] = lab < 0 ? 0.0 : ((a.flags_opts & GEE_LAPLACIAN) ? sr * a.inv[lab] : a.inv[lab]);
+        a.tab_lab[r] = (signed char)lab;
+        a.ucnt[r] = u;
     }
 }
 
-__global__ void __launch_bounds__(kBmThreads) k_bm_scatter(const int64_t *__restrict__ rows,
-                                                            const int64_t *__restrict__ cols, int64_t E,
-                                                            int directed, int n,
-                                                            const int64_t *__restrict__ slot_ptr,
-                                                            const unsigned *__restrict__ part,
-                                                            unsigned short *__restrict__ colbuf) {
-    extern __shared__ unsigned cur[];
-    const unsigned *off = part + (size_t)blockIdx.x * n;
-    for (int r = threadIdx.x; r < n; r += blockDim.x) cur[r] = (unsigned)(slot_ptr[r] + off[r]);
-    __syncthreads();
-    int64_t e0, e1;
-    chunk_range(E, e0, e1);
-    for (int64_t b = e0; b < e1; b += (int64_t)blockDim.x * kBmUnroll) {
-        unsigned r[kBmUnroll], c[kBmUnroll];
-#pragma unroll
-        for (int u = 0; u < kBmUnroll; ++u) {
-            const int64_t e = b + (int64_t)u * blockDim.x + threadIdx.x;
-            r[u] = e < e1 ? (unsigned)__ldcs(rows + e) : 0u;
-            c[u] = e < e1 ? (unsigned)__ldcs(cols + e) : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < kBmUnroll; ++u) {
-            const int64_t e = b + (int64_t)u * blockDim.x + threadIdx.x;
-            const bool v = e < e1;
-            const int nv = __popc(__ballot_sync(0xffffffffu, v));
-            const unsigned p = rle_take(cur, r[u], v, nv, true);
-            if (v) colbuf[p] = (unsigned short)c[u];
-            if (!directed && v && r[u] != c[u]) colbuf[atomicAdd(&cur[c[u]], 1u)] = (unsigned short)r[u];
-        }
+// rare path 1: exact stream lengths; clears the class sums
+__global__ void k_bm_len(const int64_t *__restrict__ rows, const int64_t *__restrict__ cols, int64_t E,
+                         int directed, BmArgs a) {
+    if (!__ldcg(a.flags)) return;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t i = i0; i < (int64_t)a.n * kZacc; i += stride) a.zacc[i] = 0.0;
+    for (int64_t e = i0; e < E; e += stride) {
+        const unsigned r = (unsigned)rows[e], c = (unsigned)cols[e];
+        atomicAdd(&a.len[r], 1u);
+        if (!directed && r != c) atomicAdd(&a.len[c], 1u);
     }
 }
 
-struct BmRowsArgs {
-    const int64_t *slot_ptr;
-    const unsigned short *colbuf;
-    int n;
-    int words;  // ceil(n / 32)
-    int32_t *out_col;
-    double *out_val;
-    unsigned *row_cnt;
-    unsigned char *row_flag;
-    unsigned *has_multi;
-    unsigned deg_flags;
-    double *deg, *scale;
-    int32_t *err;
-    // embed inputs produced here (one pass over rows): node records and the
-    // list of long rows gee_embed hands to whole CTAs
-    const int32_t *y32;
-    const double *inv;
-    unsigned laplacian;
-    double2 *rec;
-    double *tab_g;          // compact node table for gee_embed's shared-memory copy
-    signed char *tab_lab;
-    unsigned *long_list, *n_long;
-    int long_row;
-};
+// rare path 2: per-class sums of g over every stream entry of rows with repeats
+__global__ void k_bm_zsum(const int64_t *__restrict__ rows, const int64_t *__restrict__ cols, int64_t E,
+                          int directed, BmArgs a) {
+    if (!__ldcg(a.flags)) return;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += stride) {
+        const unsigned r = (unsigned)rows[e], c = (unsigned)cols[e];
+        if (a.len[r] != a.ucnt[r] && a.tab_lab[c] >= 0)
+            atomicAdd(&a.zacc[(size_t)r * kZacc + a.tab_lab[c]], a.tab_g[c]);
+        if (!directed && r != c && a.len[c] != a.ucnt[c] && a.tab_lab[r] >= 0)
+            atomicAdd(&a.zacc[(size_t)c * kZacc + a.tab_lab[r]], a.tab_g[r]);
+    }
+}
 
-constexpr int kBmStage = 1536;  // per-warp staging of a row's sorted columns
-
-__global__ void __launch_bounds__(kBmRowsThreads) k_bm_rows(BmRowsArgs a) {
-    extern __shared__ unsigned bsm[];
+// ---------------------------------------------------------------------------
+template <int KP>
+__global__ void __launch_bounds__(kRowsNT) k_bm_rows(BmArgs a) {
+    extern __shared__ __align__(16) unsigned char sm_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int W = a.words;
-    unsigned *bm = bsm + (size_t)wid * (2 * W + kBmStage);  // bitmap
-    unsigned *pre = bm + W;                                 // exclusive popc prefix per word
-    unsigned *stage = pre + W;                              // sorted columns of the row
-    const int wpl = (W + 31) / 32;                          // words per lane in the emission
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = warp; r < a.n; r += nwarps) {
-        const int64_t s = a.slot_ptr[r];
-        const int L = (int)(a.slot_ptr[r + 1] - s);
-        for (int i = lane; i < W; i += 32) bm[i] = 0u;
-        __syncwarp();
-        // set bits with non-returning shared atomics (RED); duplicates show up
-        // as fewer distinct columns than stream entries (u < L), so no
-        // per-entry old-value check is needed
-        for (int i0 = lane; i0 < L; i0 += 128) {
-            unsigned c[4];
+    constexpr int kWarps = kRowsNT / 32;
+    double *tg = reinterpret_cast<double *>(sm_raw);                            // [n]
+    signed char *tl = reinterpret_cast<signed char *>(tg + ((a.n + 1) & ~1));   // [n]
+    // stage the node table (written by k_bm_scan) with 16-byte loads
+    {
+        const int n2 = a.n / 2;
+        const double2 *src = reinterpret_cast<const double2 *>(a.tab_g);
+        double2 *dst = reinterpret_cast<double2 *>(tg);
+        for (int j = threadIdx.x; j < n2; j += blockDim.x) dst[j] = __ldcg(src + j);
+        if ((a.n & 1) && threadIdx.x == 0) tg[a.n - 1] = __ldcg(a.tab_g + a.n - 1);
+        const int n16 = a.n / 16;
+        const int4 *ls = reinterpret_cast<const int4 *>(a.tab_lab);
+        for (int j = threadIdx.x; j < n16; j += blockDim.x) reinterpret_cast<int4 *>(tl)[j] = __ldcg(ls + j);
+        for (int j = n16 * 16 + threadIdx.x; j < a.n; j += blockDim.x) tl[j] = a.tab_lab[j];
+    }
+    __syncthreads();
+    const bool lap = (a.flags_opts & GEE_LAPLACIAN) != 0, diag = (a.flags_opts & GEE_DIAGONAL) != 0;
+    const int Wp = a.Wp;
+    const bool any_rep = __ldcg(a.flags) != 0;
+    for (int r = blockIdx.x * kWarps + wid; r < a.n; r += gridDim.x * kWarps) {
+        double acc[KP];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int i = i0 + 32 * u;
-                c[u] = i < L ? (unsigned)a.colbuf[s + i] : 0xffffffffu;
+        for (int q = 0; q < KP; ++q) acc[q] = 0.0;
+        if (any_rep && __ldcg(a.len + r) != __ldcg(a.ucnt + r)) {
+            // a row with repeated pairs: its class sums come from k_bm_zsum
+            if (lane == 0) {
+#pragma unroll
+                for (int q = 0; q < KP; ++q) acc[q] = __ldcg(a.zacc + (size_t)r * kZacc + q);
+            }
+        } else {
+            const unsigned *row = a.bm + (size_t)r * Wp;
+            unsigned wv[kWordsPerLane];
+#pragma unroll
+            for (int i = 0; i < kWordsPerLane; ++i) {
+                const int w = i * 32 + lane;
+                wv[i] = w < Wp ? __ldcg(row + w) : 0u;
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (c[u] != 0xffffffffu) atomicOr(&bm[c[u] >> 5], 1u << (c[u] & 31));
-        }
-        __syncwarp();
-        // emission: lane l owns words [l*wpl, (l+1)*wpl); set bits leave in
-        // column order, staged in shared memory so the global write coalesces
-        const int w0 = min(W, lane * wpl), w1 = min(W, w0 + wpl);
-        unsigned cnt = 0;
-        for (int w = w0; w < w1; ++w) cnt += __popc(bm[w]);
-        unsigned incl = cnt;
+            for (int i = 0; i < kWordsPerLane; ++i) {
+                unsigned word = wv[i];
+                const int base = (i * 32 + lane) * 32;
+                while (word) {
+                    const int c = base + __ffs(word) - 1;
+                    word &= word - 1;
+                    const int lab = tl[c];
+                    const double x = tg[c];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        unsigned off = incl - cnt;
-        const unsigned u = __shfl_sync(0xffffffffu, incl, 31);
-        const bool staged = u <= (unsigned)kBmStage;
-        for (int w = w0; w < w1; ++w) {
-            unsigned word = bm[w];
-            pre[w] = off;
-            while (word) {
-                const int b = __ffs(word) - 1;
-                word &= word - 1;
-                if (staged)
-                    stage[off] = w * 32 + b;
-                else
-                    a.out_col[s + off] = w * 32 + b;
-                ++off;
-            }
-        }
-        __syncwarp();
-        if (staged)
-            for (unsigned i = lane; i < u; i += 32) a.out_col[s + i] = (int32_t)stage[i];
-        const bool multi = u < (unsigned)L;
-        if (lane == 0) {
-            a.row_cnt[r] = u;
-            a.row_flag[r] = multi ? 1 : 0;
-        }
-        if (multi) {
-            // multiplicities of the distinct columns (sums of ones, exact)
-            __syncwarp();
-            for (unsigned i = lane; i < u; i += 32) a.out_val[s + i] = 0.0;
-            __syncwarp();
-            for (int i = lane; i < L; i += 32) {
-                const unsigned c = a.colbuf[s + i];
-                const unsigned rank = pre[c >> 5] + __popc(bm[c >> 5] & ((1u << (c & 31)) - 1u));
-                atomicAdd(&a.out_val[s + rank], 1.0);
-            }
-            if (lane == 0) atomicOr(a.has_multi, 1u);
-        }
-        if (lane == 0) {
-            double sr = 1.0;
-            if (a.deg_flags) {
-                const double d = (double)L + ((a.deg_flags & GEE_DIAGONAL) ? 1.0 : 0.0);
-                a.deg[r] = d;
-                if (a.scale) {
-                    sr = laplacian_scale(d, a.err);
-                    a.scale[r] = sr;
+                    for (int q = 0; q < KP; ++q) acc[q] += (lab == q) ? x : 0.0;
                 }
             }
-            if (a.rec) {
-                const int lab = a.y32[r];
-                const double g = lab < 0 ? 0.0 : (a.laplacian ? sr * a.inv[lab] : a.inv[lab]);
-                a.rec[r] = make_double2(__longlong_as_double((long long)(unsigned)lab), g);
-                if (a.tab_g) {
-                    a.tab_g[r] = g;
-                    a.tab_lab[r] = (signed char)lab;
+        }
+#pragma unroll
+        for (int q = 0; q < KP; ++q) acc[q] = warp_sum(acc[q]);
+        if (diag) {
+            // A+I: the diagonal gains 1.0 whether or not (r, r) is stored
+            const int lab = tl[r];
+            const double x = tg[r];
+#pragma unroll
+            for (int q = 0; q < KP; ++q) acc[q] += (lab == q) ? x : 0.0;
+        }
+        if (lap) {
+            const double sr = __ldcg(a.scale + r);
+#pragma unroll
+            for (int q = 0; q < KP; ++q) acc[q] *= sr;
+        }
+        if (a.flags_opts & GEE_CORRELATION) {
+            double ss = 0.0;
+            bool fin = true;
+#pragma unroll
+            for (int q = 0; q < KP; ++q) {
+                if (q < a.k) {
+                    ss += acc[q] * acc[q];
+                    fin &= isfinite(acc[q]);
                 }
             }
-            if (a.long_list && (int)u > a.long_row) a.long_list[atomicAdd(a.n_long, 1u)] = (unsigned)r;
+            if (!fin) {
+                if (lane == 0) raise_err(a.err, GEE_ERR_NONFINITE);
+            } else {
+                const double nrm = __dsqrt_rn(ss);
+                if (nrm > 0.0) {
+#pragma unroll
+                    for (int q = 0; q < KP; ++q) acc[q] = __ddiv_rn(acc[q], nrm);
+                }
+            }
         }
-        __syncwarp();
+        double mine = 0.0;
+#pragma unroll
+        for (int q = 0; q < KP; ++q) mine = (lane == q) ? acc[q] : mine;
+        if (lane < a.k) a.z[(int64_t)r * a.k + lane] = mine;
     }
 }
 
+// ---------------------------------------------------------------------------
 int force_path();
 
-bool bitmap_path_ok(int wt, int64_t E, int64_t n_rows, int64_t n_cols, int directed) {
+// unit weights, square, at most kBmMax nodes, K <= 8 (register accumulators)
+bool bitmap_path_ok(int wt, int64_t E, int64_t n_rows, int64_t n_cols, int directed, int k) {
     if (force_path() != 0) return false;  // test hook: exercise the general paths
     const int64_t M = directed ? E : 2 * E;
-    return wt == GEE_W_UNIT && n_rows == n_cols && n_rows >= 1 && n_rows <= kBmMax && M < ((int64_t)1 << 31);
+    return wt == GEE_W_UNIT && n_rows == n_cols && n_rows >= 1 && n_rows <= kBmMax && k >= 1 && k <= kZacc &&
+           M < ((int64_t)1 << 31);
 }
 
 struct BmWs {
-    unsigned *part, *cnt, *flags;
-    int64_t *slot_ptr;
-    unsigned short *colbuf;
-    int G;
+    unsigned *bm, *len, *flags, *ucnt;
+    double *zacc, *tab_g;
+    signed char *tab_lab;
+    int Wp, nb;
+    size_t clear_words;
 };
 
-static void carve_bm(Carver &cv, BmWs &w, int64_t E, int64_t n, int directed) {
-    const int64_t M = directed ? E : 2 * E;
-    w.G = num_sms();  // one 1024-thread CTA per SM for count/scatter
-    w.part = cv.take<unsigned>((size_t)w.G * (size_t)n);
-    w.cnt = cv.take<unsigned>((size_t)n + 1);
-    w.flags = cv.take<unsigned>(4);
-    w.slot_ptr = cv.take<int64_t>((size_t)n + 1);
-    w.colbuf = cv.take<unsigned short>((size_t)(M > 0 ? M : 1));
+static void carve_bm(Carver &cv, BmWs &w, int64_t n) {
+    const int64_t np = (n + kBlk - 1) / kBlk * kBlk;
+    w.nb = (int)(np / kBlk);
+    w.Wp = (int)(np / 32);
+    // bitmap, stream lengths and flags are contiguous: one memset clears them
+    w.clear_words = (size_t)np * w.Wp + (size_t)n + 4;
+    w.bm = cv.take<unsigned>(w.clear_words);
+    w.len = w.bm ? w.bm + (size_t)np * w.Wp : nullptr;
+    w.flags = w.bm ? w.len + n : nullptr;
+    w.ucnt = cv.take<unsigned>((size_t)n);
+    w.zacc = cv.take<double>((size_t)n * kZacc);
+    w.tab_g = cv.take<double>((size_t)n + 2);
+    w.tab_lab = cv.take<signed char>((size_t)n + 16);
 }
 
 size_t bitmap_workspace(int64_t E, int64_t n, int directed) {
+    (void)E;
+    (void)directed;
     Carver cv(nullptr);
     BmWs w;
-    carve_bm(cv, w, E, n, directed);
+    carve_bm(cv, w, n);
     return cv.bytes();
 }
 
-// Unit-weight CSR in the slot layout: row r's distinct columns at
-// [slot_ptr[r], slot_ptr[r] + row_cnt[r]); multiplicities in val only for
-// rows with row_flag[r] != 0.  row_ptr receives the slot pointers.  Also
-// emits the embed's node records and long-row list (rec/long_list/n_long,
-// n_long zeroed by the caller) so gee_embed needs no preparation launches.
-int bitmap_csr_build(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n, int directed,
-                     int64_t *row_ptr, unsigned *row_cnt, unsigned char *row_flag, int32_t *col, double *val,
-                     unsigned deg_flags, double *deg, double *scale, const int32_t *y32, const double *inv,
-                     unsigned laplacian, double2 *rec, double *tab_g, signed char *tab_lab,
-                     unsigned *long_list, unsigned *n_long, int long_row,
-                     void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st) {
+// The fused encode for unit-weight graphs.  Outputs: Z (n x k) and, under
+// the Laplacian, deg / scale.  The CSR is not materialised.
+int bitmap_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n, int directed,
+                  const int32_t *y32, const double *inv, int k, unsigned flags, double *deg, double *scale,
+                  double *z, void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st) {
     Carver cv(ws);
     BmWs W;
-    carve_bm(cv, W, E, n, directed);
+    carve_bm(cv, W, n);
     if (ws_bytes < cv.bytes()) return GEE_E_WORKSPACE;
-    static bool attr = false;
-    if (!attr) {
-        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_bm_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kBmMax * 4));
-        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_bm_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kBmMax * 4));
-        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_bm_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (kBmRowsThreads / 32) * (2 * (kBmMax / 32) + kBmStage) * 4));
-        attr = true;
-    }
-    GEE_CHECK_CUDA(cudaMemsetAsync(W.flags, 0, 4 * sizeof(unsigned), st));
-    const size_t hsm = sizeof(unsigned) * (size_t)n;
-    if (E > 0) {
-        k_bm_count<<<W.G, kBmThreads, hsm, st>>>(rows, cols, E, directed, (int)n, W.part);
-        GEE_CHECK_LAUNCH("k_bm_count");
-        k_bm_reduce<<<(unsigned)((n + 31) / 32), 1024, sizeof(unsigned) * 33 * (size_t)W.G, st>>>(
-            W.part, W.G, (int)n, W.cnt, row_ptr, W.flags + 2);
-        GEE_CHECK_LAUNCH("k_bm_reduce_scan");
-        k_bm_scatter<<<W.G, kBmThreads, hsm, st>>>(rows, cols, E, directed, (int)n, row_ptr, W.part, W.colbuf);
-        GEE_CHECK_LAUNCH("k_bm_scatter");
-    } else {
-        GEE_CHECK_CUDA(cudaMemsetAsync(row_ptr, 0, sizeof(int64_t) * (size_t)(n + 1), st));
-    }
-    BmRowsArgs a;
-    a.slot_ptr = row_ptr;
-    a.colbuf = W.colbuf;
+    BmArgs a;
     a.n = (int)n;
-    a.words = (int)((n + 31) / 32);
-    a.out_col = col;
-    a.out_val = val;
-    a.row_cnt = row_cnt;
-    a.row_flag = row_flag;
-    a.has_multi = W.flags;
-    a.deg_flags = deg_flags;
+    a.Wp = W.Wp;
+    a.nb = W.nb;
+    a.bm = W.bm;
+    a.len = W.len;
+    a.flags = W.flags;
+    a.ucnt = W.ucnt;
+    a.zacc = W.zacc;
     a.deg = deg;
-    a.scale = (deg_flags & GEE_LAPLACIAN) ? scale : nullptr;
-    a.err = err;
+    a.scale = scale;
     a.y32 = y32;
     a.inv = inv;
-    a.laplacian = laplacian;
-    a.rec = rec;
-    a.tab_g = tab_g;
-    a.tab_lab = tab_lab;
-    a.long_list = long_list;
-    a.n_long = n_long;
-    a.long_row = long_row;
-    const size_t rsm = (size_t)(kBmRowsThreads / 32) * (2 * (size_t)a.words + kBmStage) * 4;
-    k_bm_rows<<<grid_for(n * 32, kBmRowsThreads, 8), kBmRowsThreads, rsm, st>>>(a);
-    GEE_CHECK_LAUNCH("k_bm_rows");
+    a.tab_g = W.tab_g;
+    a.tab_lab = W.tab_lab;
+    a.flags_opts = flags;
+    a.z = z;
+    a.k = k;
+    a.err = err;
+    const size_t rows_smem = 8 * (size_t)((n + 1) & ~1) + (size_t)((n + 15) & ~15);
+    static bool attr = false;
+    if (!attr) {
+        const int mx = (int)(8 * (size_t)kBmMax + kBmMax);
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_bm_rows<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_bm_rows<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_bm_rows<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_bm_rows<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        attr = true;
+    }
+    GEE_CHECK_CUDA(cudaMemsetAsync(W.bm, 0, sizeof(unsigned) * W.clear_words, st));
+    if (E > 0) {
+        k_bm_set<<<grid_for(E, kSetThreads * 4, 8), kSetThreads, 0, st>>>(rows, cols, E, a);
+        GEE_CHECK_LAUNCH("k_bm_set");
+        if (!directed) {
+            k_bm_sym<<<(unsigned)(W.nb * (W.nb + 1) / 2), kBlk, 0, st>>>(a);
+            GEE_CHECK_LAUNCH("k_bm_sym");
+        }
+        k_bm_len<<<grid_for(E, 256, 2), 256, 0, st>>>(rows, cols, E, directed, a);
+        GEE_CHECK_LAUNCH("k_bm_len");
+    }
+    k_bm_scan<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(a);
+    GEE_CHECK_LAUNCH("k_bm_scan");
+    if (E > 0) {
+        k_bm_zsum<<<grid_for(E, 256, 2), 256, 0, st>>>(rows, cols, E, directed, a);
+        GEE_CHECK_LAUNCH("k_bm_zsum");
+    }
+    const unsigned grid = (unsigned)num_sms();
+    if (k <= 1)
+        k_bm_rows<1><<<grid, kRowsNT, rows_smem, st>>>(a);
+    else if (k <= 2)
+        k_bm_rows<2><<<grid, kRowsNT, rows_smem, st>>>(a);
+    else if (k <= 4)
+        k_bm_rows<4><<<grid, kRowsNT, rows_smem, st>>>(a);
+    else
+        k_bm_rows<8><<<grid, kRowsNT, rows_smem, st>>>(a);
+    GEE_CHECK_LAUNCH("k_bm_rows_embed");
     return GEE_OK;
 }
 
