@@ -212,14 +212,15 @@ def kernel_bytes(c, m_stream, nnz, wbytes):
     vb = 8 if wbytes else 0  # stored CSR value bytes per entry
     np_ = (n + 255) // 256 * 256
     bm = np_ * np_ // 8
+    nbx = 16 if 7 * k <= 16 else 32 if 7 * k <= 32 else 64  # X digit columns (k_bitmap.cu)
     return {
         # bitmap path (unit weights, N <= 16384): the edge list is the only
         # HBM stream; the Np x Np adjacency bitmap (Np = n rounded up to 256)
         # lives in L2 and is counted once per pass over it
-        "k_bm_set": 16 * e,
-        "k_bm_sym": 2 * bm,
-        "k_bm_scan": bm + 4 * n + 8 * n + 1 * n + (16 * n if lap else 0),
-        "k_bm_rows_embed": bm + 9 * n + 8 * n * k + (8 * n if lap else 0),
+        "k_bm_set": 16 * e + 8 * n,
+        "k_bm_sym": 2 * bm + 4 * n + 9 * n + (16 * n if lap else 0),
+        "k_bm_scan": bm + 4 * n + 9 * n + (16 * n if lap else 0),
+        "k_bm_gemm": bm + nbx * np_ + 8 * n * k + 4 * n + (8 * n if lap else 0),
         # radix-sort path
         "k_sort_hist": (16 + wbytes) * e,
         # bucket path

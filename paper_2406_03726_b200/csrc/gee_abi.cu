@@ -88,10 +88,11 @@ int embed_long_row();
 void embed_scratch(void *ws, int64_t n_rows, int64_t n_cols, unsigned **ctr, unsigned **list, double2 **rec,
                    double **tab_g, signed char **tab_lab);
 bool bitmap_path_ok(int wt, int64_t E, int64_t n_rows, int64_t n_cols, int directed, int k);
-size_t bitmap_workspace(int64_t E, int64_t n, int directed);
+size_t bitmap_workspace(int64_t E, int64_t n, int directed, int k);
 int bitmap_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n, int directed,
-                  const int32_t *y32, const double *inv, int k, unsigned flags, double *deg, double *scale,
-                  double *z, void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st);
+                  const int64_t *labels, int k, unsigned flags, int32_t *y32, int64_t *counts, double *inv,
+                  double *deg, double *scale, double *z, void *ws, size_t ws_bytes, int32_t *err,
+                  cudaStream_t st);
 int validate_edges(const int64_t *, const int64_t *, const void *, int, int64_t, int64_t, int32_t *,
                    cudaStream_t);
 
@@ -132,7 +133,7 @@ static size_t carve_encode(Carver &cv, EncodeWs &w, int64_t E, int64_t n, int32_
     w.col = cv.take<int32_t>((size_t)(M > 0 ? M : 1));
     w.val = cv.take<double>((size_t)(M > 0 ? M : 1));
     w.label_partial = cv.take<unsigned>(label_partial_words(n, k));
-    w.csr_bytes = bitmap_path_ok(wt, E, n, n, directed, k) ? bitmap_workspace(E, n, directed)
+    w.csr_bytes = bitmap_path_ok(wt, E, n, n, directed, k) ? bitmap_workspace(E, n, directed, k)
                                                          : csr_build_workspace(E, n, n, directed);
     w.csr_ws = cv.take<char>(w.csr_bytes);
     w.emb_bytes = embed_workspace(n, n);
@@ -306,6 +307,12 @@ int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, in
     EncodeWs W;
     size_t need = carve_encode(cv, W, n_edges, n_nodes, k, directed, w_type);
     if (ws_bytes < need || !ws) return GEE_E_WORKSPACE;
+    if (bitmap_path_ok(w_type, n_edges, n_nodes, n_nodes, directed, k)) {
+        // unit weights, small node count, K <= 8: labels, an L2-resident N x N
+        // adjacency bitmap and Z in three launches (no CSR, no embed pass)
+        return bitmap_encode(rows, cols, n_edges, n_nodes, directed, labels, k, flags, W.y32, W.counts, W.inv,
+                             W.deg, W.scale, z, W.csr_ws, W.csr_bytes, err, st);
+    }
     // control words: embed counters [0..2] and the label kernel's done word [3]
     unsigned *ectr, *elist;
     double2 *erec;
@@ -317,12 +324,6 @@ int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, in
     if (rc) return rc;
     const unsigned deg_flags = (flags & GEE_LAPLACIAN) ? (GEE_LAPLACIAN | (flags & GEE_DIAGONAL)) : 0u;
     const double *sc = (flags & GEE_LAPLACIAN) ? W.scale : nullptr;
-    if (bitmap_path_ok(w_type, n_edges, n_nodes, n_nodes, directed, k)) {
-        // unit weights, small node count: an L2-resident N x N adjacency bitmap;
-        // the row pass emits the compact CSR and Z in one sweep (no embed pass)
-        return bitmap_encode(rows, cols, n_edges, n_nodes, directed, W.y32, W.inv, k, flags, W.deg, W.scale, z,
-                             W.csr_ws, W.csr_bytes, err, st);
-    }
     if (sort_path_ok(n_edges, n_nodes, n_nodes, directed)) {
         // compact CSR from the radix sort; values stay implicit (1.0) when the
         // graph has unit weights and no duplicate entries

@@ -1,31 +1,42 @@
 // k_bitmap.cu -- the whole encode for unit-weight graphs with at most
-// kBmMax nodes (configs 0/1: unweighted SBM, N = 10^4).
+// kBmMax nodes and K <= 8 classes (configs 0/1: unweighted SBM, N = 10^4).
 //
 // With every weight equal to 1.0 a stored value is the multiplicity of its
 // (row, col) pair, and the order duplicates are summed in is irrelevant (sums
 // of ones are exact).  When no pair repeats, the CSR row of r is the set of
 // its columns, its degree is the set size and
-//     Z[r, q] = s_r * sum_{c in row r, Y_c = q} s_c / n_q   (+ the A+I diagonal),
-// so the encode needs only the N x N adjacency bitmap -- Np^2/8 bytes, 13 MB at
-// N = 10^4 -- which stays resident in the 126 MB L2.  The CSR itself is never
-// materialised (gee_encode_edges returns Z only).
-//   k_bm_set   one read of the int64 edge list; each stream entry sets bit
-//              (r, c) with a global atomicOr.  Lanes holding the same bitmap
-//              word (adjacent entries of a row-major list) OR-combine first,
-//              so a sorted list costs about one atomic per word.  A bit that
-//              was already set is a repeated pair: flags[0].
+//     Z[r, q] = s_r * (1/n_q) * sum_{c in row r, Y_c = q} s_c   (+ the A+I diagonal),
+// a product of the 0/1 adjacency matrix S with the N x K matrix X[c, q] =
+// s_c [Y_c = q].  The encode needs only the N x N adjacency bitmap -- Np^2/8
+// bytes, 13 MB at N = 10^4 -- which stays resident in the 126 MB L2; the CSR
+// itself is never materialised (gee_encode_edges returns Z only).
+//   k_bm_set   the labels (validated, y32, class histogram) and one read of the
+//              int64 edge list: each stream entry sets bit (r, c) of U with a
+//              global reduction (RED.OR, no return).  Lanes holding the same
+//              bitmap word (adjacent entries of a row-major list) OR-combine
+//              first, so a sorted list costs about one reduction per word.
 //   k_bm_sym   undirected lists: S = U | U^T in place, 256 x 256-bit block
-//              pairs, 32 x 32 transposes by warp shuffles.  A pair present in
-//              both directions (U & U^T off the diagonal) is a repeat too.
-//   k_bm_scan  one warp per row: u_r = popc(S_r), degree d_r = u_r (+1 under
-//              A+I), s_r = d_r^-1/2 and the node table {Y_r, g_r = s_r/n_Y_r}
-//   k_bm_rows  one warp per row, 1024-thread CTAs sharing one shared-memory
-//              copy of the node table: Z[r, :] from the set bits of S_r, the
-//              diagonal, s_r and the correlation epilogue.
-// Rare path (any repeated pair; each kernel exits at once otherwise): exact
-// stream lengths by atomics (k_bm_len) and, for rows whose length differs
-// from their distinct count, the per-class sums of g over every stream entry
-// (k_bm_zsum), which k_bm_rows uses instead of the bitmap sum.
+//              pairs, 32 x 32 transposes by warp shuffles.  It also counts
+//              popc(U) (= E exactly when no pair repeats in the list) and
+//              flags pairs present in both directions (U & U^T off the
+//              diagonal), the other way a pair repeats in the stream.  Each
+//              block pair adds its rows' popcounts to u_r; the CTA that
+//              completes a 256-row block writes that block's node table:
+//              d_r = u_r (+1 under A+I), s_r = d_r^-1/2, and X's row as
+//              7 base-256 digits of s_r * 2^55 in the columns of class Y_r.
+//              (Directed lists: k_bm_scan, one warp per row, instead.)
+//   k_bm_gemm  S x X on the 5th-generation tensor cores (tcgen05.mma
+//              kind::i8, u8 x u8 -> s32 in TMEM): 128-row tiles, 128-column
+//              K steps; the A tile is S's bits expanded to bytes in shared
+//              memory (128B-swizzled K-major), the B tile X's digit columns.
+//              Integer accumulation is exact, so sum_c S_rc s_c is known to
+//              2^-55 per term, whatever the order; split-K partials are
+//              integer too.  The epilogue recombines the digits in f64 and
+//              applies 1/n_q, the diagonal, s_r and the correlation.
+// Rare path (some pair repeats): k_bm_gemm first recomputes the stream
+// lengths by atomics, the node table and, for rows with repeats, per-class
+// sums of g = s_c/n_q over every stream entry, in grid-wide phases (all CTAs
+// are co-resident); those rows take their sums from there.
 #include "gee_common.cuh"
 
 namespace gee {
@@ -33,21 +44,33 @@ namespace gee {
 constexpr int kBmMax = 16384;   // nodes: bitmap Np^2/8 <= 32 MB (L2-resident)
 constexpr int kBlk = 256;       // rows / columns of a k_bm_sym block
 constexpr int kSetThreads = 512;
-constexpr int kRowsNT = 1024;   // one CTA per SM, one node table per SM
-constexpr int kWordsPerLane = kBmMax / 32 / 32;
-constexpr int kZacc = 8;        // rare-path class sums per row (K <= 8)
+constexpr int kKMax = 8;        // classes
+constexpr int kDig = 7;         // base-256 digits of s * 2^55
+constexpr int kTM = 128;        // GEMM rows per tile (TMEM lanes)
+constexpr int kTK = 128;        // GEMM columns per K step (bytes of a swizzle row)
+constexpr int kStages = 4;
+constexpr int kGemmNT = 256;
 
 struct BmArgs {
-    int n, Wp;                // nodes, bitmap words per row (multiple of 8)
-    int nb;                   // 256-row blocks
+    int n, Wp, nb, Np;        // nodes, bitmap words per row (multiple of 8), 256-row blocks, Wp*32
+    int64_t E;
+    int directed;
     unsigned *bm;             // [Np][Wp]
-    unsigned *len;            // [n] stream lengths (rare path)
-    unsigned *flags;          // [0] a repeated pair was seen
     unsigned *ucnt;           // [n] distinct columns per row
-    double *zacc;             // [n][kZacc] rare path class sums
+    unsigned *len;            // [n] stream lengths (rare path)
+    unsigned *cnt;            // [kKMax] class histogram
+    unsigned *blkdone;        // [nb] finished block pairs per 256-row block
+    unsigned *mdone;          // [Np/128] split-K arrivals per GEMM row tile
+    unsigned *flags;          // [0] pair in both directions, [1] grid barrier, [2] popc(U)
+    unsigned char *xt;        // [NB][Np] X^T digits (K-major B operand)
+    int nbx;                  // NB: X columns (kDig * K padded to 16/32/64)
+    int32_t *cpart;           // [splits][Np][NB] split-K partial sums
+    double *zacc;             // [n][kKMax] rare path class sums
+    const int64_t *labels;
+    int32_t *y32;
+    int64_t *counts;
+    double *inv;
     double *deg, *scale;
-    const int32_t *y32;
-    const double *inv;
     double *tab_g;
     signed char *tab_lab;
     unsigned flags_opts;      // GEE_LAPLACIAN | GEE_DIAGONAL | GEE_CORRELATION
@@ -62,12 +85,18 @@ __device__ __forceinline__ unsigned lanemask_le() {
     return m;
 }
 
+__device__ __forceinline__ unsigned ld_gpu(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // 32 x 32 bit transpose across a warp: out(lane i) bit j = in(lane j) bit i
 __device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
     const unsigned m16 = 0x0000ffffu, m8 = 0x00ff00ffu, m4 = 0x0f0f0f0fu, m2 = 0x33333333u, m1 = 0x55555555u;
-#define GEE_TSTAGE(J, M)                                                  \
-    {                                                                     \
-        const unsigned y = __shfl_xor_sync(0xffffffffu, x, J);            \
+#define GEE_TSTAGE(J, M)                                                           \
+    {                                                                              \
+        const unsigned y = __shfl_xor_sync(0xffffffffu, x, J);                     \
         x = (lane & J) ? ((x & ~M) | ((y >> J) & M)) : ((x & M) | ((y & M) << J)); \
     }
     GEE_TSTAGE(16, m16)
@@ -79,14 +108,72 @@ __device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
     return x;
 }
 
+// node-table entry of row r from its stream length L (k_bm_sym / k_bm_scan /
+// the rare path); y32 and the histogram are complete when this runs
+__device__ __forceinline__ void node_entry(const BmArgs &a, int r, unsigned L) {
+    double sr = 1.0;
+    if (a.flags_opts & GEE_LAPLACIAN) {
+        const double d = (double)L + ((a.flags_opts & GEE_DIAGONAL) ? 1.0 : 0.0);
+        a.deg[r] = d;
+        sr = laplacian_scale(d, a.err);
+        a.scale[r] = sr;
+    }
+    const int lab = a.y32[r];
+    double g = 0.0;
+    if (lab >= 0) {
+        const double inv = __ddiv_rn(1.0, (double)__ldcg(a.cnt + lab));  // 1/n_k (embedding.py:106)
+        g = (a.flags_opts & GEE_LAPLACIAN) ? sr * inv : inv;
+        // X[r, lab] = s_r as 7 base-256 digits of floor(s_r * 2^55) (s_r <= 1)
+        const unsigned long long T = __double2ull_rz(sr * 0x1p55);
+        unsigned char *x = a.xt + (size_t)lab * kDig * a.Np + r;
+#pragma unroll
+        for (int d = 0; d < kDig; ++d) x[(size_t)d * a.Np] = (unsigned char)(T >> (8 * d));
+    }
+    a.tab_g[r] = g;
+    a.tab_lab[r] = (signed char)lab;
+}
+
+// class counts and 1/n_k as the reference's LabelVector / W (run once)
+__device__ __forceinline__ void write_counts(const BmArgs &a, int t) {
+    if (t < a.k) {
+        const unsigned m = __ldcg(a.cnt + t);
+        a.counts[t] = (int64_t)m;
+        a.inv[t] = m ? __ddiv_rn(1.0, (double)m) : 0.0;
+    }
+}
+
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kSetThreads) k_bm_set(const int64_t *__restrict__ rows,
-                                                        const int64_t *__restrict__ cols, int64_t E, BmArgs a) {
-    constexpr int U = 4;
+                                                        const int64_t *__restrict__ cols, BmArgs a) {
+    __shared__ unsigned sh_hist[kKMax];
     const int lane = threadIdx.x & 31;
+    // labels: int64 -> int32 (-1 = unlabeled), validated, histogrammed
+    if (threadIdx.x < kKMax) sh_hist[threadIdx.x] = 0;
+    __syncthreads();
+    for (int base = blockIdx.x * blockDim.x; base < a.n; base += gridDim.x * blockDim.x) {
+        const int i = base + threadIdx.x;
+        int lab = -1;
+        if (i < a.n) {
+            int64_t v = a.labels[i];
+            if (v < -1 || v >= a.k) {
+                raise_err(a.err, GEE_ERR_LABEL);
+                v = -1;
+            }
+            lab = (int)v;
+            a.y32[i] = lab;
+        }
+        for (int q = 0; q < a.k; ++q) {
+            const unsigned c = __popc(__ballot_sync(0xffffffffu, lab == q));
+            if (lane == 0 && c) atomicAdd(&sh_hist[q], c);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < a.k && sh_hist[threadIdx.x]) atomicAdd(&a.cnt[threadIdx.x], sh_hist[threadIdx.x]);
+
+    constexpr int U = 4;
+    const int64_t E = a.E;
     const unsigned le = lanemask_le();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
-    bool rep = false;
     for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x * U + threadIdx.x; e0 - threadIdx.x < E; e0 += stride) {
         unsigned key[U], bit[U];
 #pragma unroll
@@ -99,7 +186,8 @@ __global__ void __launch_bounds__(kSetThreads) k_bm_set(const int64_t *__restric
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            // segmented OR over runs of lanes holding the same word
+            // segmented OR over runs of lanes holding the same word; the run's
+            // last lane issues one reduction (no return value: RED, not ATOM)
             const unsigned kp = __shfl_up_sync(0xffffffffu, key[u], 1);
             const unsigned kn = __shfl_down_sync(0xffffffffu, key[u], 1);
             const bool head = lane == 0 || kp != key[u];
@@ -111,20 +199,16 @@ __global__ void __launch_bounds__(kSetThreads) k_bm_set(const int64_t *__restric
                 const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane - o >= start) incl |= y;
             }
-            const unsigned prev = __shfl_up_sync(0xffffffffu, incl, 1);
-            if (lane > start && (prev & bit[u])) rep = true;  // repeated inside the run
-            if (tail && key[u] != 0xffffffffu) {
-                const unsigned old = atomicOr(&a.bm[key[u]], incl);
-                if (old & incl) rep = true;
-            }
+            if (tail && key[u] != 0xffffffffu) atomicOr(&a.bm[key[u]], incl);
         }
     }
-    if (__any_sync(0xffffffffu, rep) && lane == 0) a.flags[0] = 1u;
 }
 
 // S = U | U^T for the block pair (BI, BJ), BI <= BJ, in place
 __global__ void __launch_bounds__(kBlk) k_bm_sym(BmArgs a) {
     __shared__ unsigned sat[kBlk][9], sbt[kBlk][9];
+    __shared__ unsigned red[kBlk / 32];
+    __shared__ bool fin[2];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     // linear index -> (BI, BJ) on the upper triangle
     const unsigned x = blockIdx.x;
@@ -133,8 +217,9 @@ __global__ void __launch_bounds__(kBlk) k_bm_sym(BmArgs a) {
     while (bj * (bj + 1) / 2 > x) --bj;
     const unsigned bi = x - bj * (bj + 1) / 2;
     const size_t Wp = (size_t)a.Wp;
-    uint4 *pa = reinterpret_cast<uint4 *>(a.bm + ((size_t)bi * kBlk + t) * Wp + (size_t)bj * 8);
-    uint4 *pb = reinterpret_cast<uint4 *>(a.bm + ((size_t)bj * kBlk + t) * Wp + (size_t)bi * 8);
+    const int ra = bi * kBlk + t, rb = bj * kBlk + t;
+    uint4 *pa = reinterpret_cast<uint4 *>(a.bm + (size_t)ra * Wp + (size_t)bj * 8);
+    uint4 *pb = reinterpret_cast<uint4 *>(a.bm + (size_t)rb * Wp + (size_t)bi * 8);
     unsigned av[8], bv[8];
     {
         const uint4 a0 = __ldcg(pa), a1 = __ldcg(pa + 1);
@@ -146,14 +231,23 @@ __global__ void __launch_bounds__(kBlk) k_bm_sym(BmArgs a) {
         bv[0] = b0.x, bv[1] = b0.y, bv[2] = b0.z, bv[3] = b0.w, bv[4] = b1.x, bv[5] = b1.y, bv[6] = b1.z, bv[7] = b1.w;
     }
     // tile (w, q) of a block transposes into row q*32+lane, word w of its mirror
+    unsigned pu = 0;  // popc of the U words read here (each U word is read once)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) sat[q * 32 + lane][w] = transpose32(av[q], lane);
+    for (int q = 0; q < 8; ++q) {
+        pu += __popc(av[q]);
+        sat[q * 32 + lane][w] = transpose32(av[q], lane);
+    }
     if (!same) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) sbt[q * 32 + lane][w] = transpose32(bv[q], lane);
+        for (int q = 0; q < 8; ++q) {
+            pu += __popc(bv[q]);
+            sbt[q * 32 + lane][w] = transpose32(bv[q], lane);
+        }
     }
+    pu = warp_sum_u(pu);
+    if (lane == 0) red[w] = pu;
     __syncthreads();
-    unsigned mut = 0;
+    unsigned mut = 0, ca = 0, cb = 0;
     if (same) {
         unsigned s[8];
 #pragma unroll
@@ -163,6 +257,7 @@ __global__ void __launch_bounds__(kBlk) k_bm_sym(BmArgs a) {
             unsigned m = av[q] & tq;
             if (q == w) m &= ~(1u << lane);  // the diagonal is its own mirror
             mut |= m;
+            ca += __popc(s[q]);
         }
         pa[0] = make_uint4(s[0], s[1], s[2], s[3]);
         pa[1] = make_uint4(s[4], s[5], s[6], s[7]);
@@ -174,19 +269,43 @@ __global__ void __launch_bounds__(kBlk) k_bm_sym(BmArgs a) {
             s[q] = av[q] | tb;
             u[q] = bv[q] | ta;
             mut |= av[q] & tb;
+            ca += __popc(s[q]);
+            cb += __popc(u[q]);
         }
         pa[0] = make_uint4(s[0], s[1], s[2], s[3]);
         pa[1] = make_uint4(s[4], s[5], s[6], s[7]);
         pb[0] = make_uint4(u[0], u[1], u[2], u[3]);
         pb[1] = make_uint4(u[4], u[5], u[6], u[7]);
     }
+    if (t == 0) {
+        unsigned tot = 0;
+#pragma unroll
+        for (int i = 0; i < kBlk / 32; ++i) tot += red[i];
+        if (tot) atomicAdd(a.flags + 2, tot);
+    }
+    // rows >= n are padding and stay empty
+    if (ca) atomicAdd(&a.ucnt[ra], ca);
+    if (cb) atomicAdd(&a.ucnt[rb], cb);
+    __threadfence();
     if (__syncthreads_or(mut != 0) && t == 0) a.flags[0] = 1u;
+    if (t == 0) {
+        fin[0] = atomicAdd(&a.blkdone[bi], 1u) == (unsigned)a.nb - 1;
+        fin[1] = !same && atomicAdd(&a.blkdone[bj], 1u) == (unsigned)a.nb - 1;
+    }
+    __syncthreads();
+    if (!fin[0] && !fin[1]) return;
+    __threadfence();
+    // this CTA completed a 256-row block: its node table entries
+    if (fin[0] && ra < a.n) node_entry(a, ra, __ldcg(a.ucnt + ra));
+    if (fin[1] && rb < a.n) node_entry(a, rb, __ldcg(a.ucnt + rb));
+    if (fin[0] && bi == 0) write_counts(a, t);
 }
 
-// one warp per row, 8 rows per CTA
+// directed lists: one warp per row, 8 rows per CTA
 __global__ void __launch_bounds__(256) k_bm_scan(BmArgs a) {
     const int lane = threadIdx.x & 31;
     const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (blockIdx.x == 0) write_counts(a, threadIdx.x);
     if (r >= a.n) return;
     const uint4 *row = reinterpret_cast<const uint4 *>(a.bm + (size_t)r * a.Wp);
     unsigned u = 0;
@@ -196,255 +315,487 @@ __global__ void __launch_bounds__(256) k_bm_scan(BmArgs a) {
     }
     u = warp_sum_u(u);
     if (lane == 0) {
-        const unsigned L = __ldcg(a.flags) ? __ldcg(a.len + r) : u;  // stream length of the row
-        double sr = 1.0;
-        if (a.flags_opts & GEE_LAPLACIAN) {
-            const double d = (double)L + ((a.flags_opts & GEE_DIAGONAL) ? 1.0 : 0.0);
-            a.deg[r] = d;
-            sr = laplacian_scale(d, a.err);
-            a.scale[r] = sr;
-        }
-        const int lab = a.y32[r];
-        a.tab_g[r] = lab < 0 ? 0.0 : ((a.flags_opts & GEE_LAPLACIAN) ? sr * a.inv[lab] : a.inv[lab]);
-        a.tab_lab[r] = (signed char)lab;
         a.ucnt[r] = u;
-    }
-}
-
-// rare path 1: exact stream lengths; clears the class sums
-__global__ void k_bm_len(const int64_t *__restrict__ rows, const int64_t *__restrict__ cols, int64_t E,
-                         int directed, BmArgs a) {
-    if (!__ldcg(a.flags)) return;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int64_t i = i0; i < (int64_t)a.n * kZacc; i += stride) a.zacc[i] = 0.0;
-    for (int64_t e = i0; e < E; e += stride) {
-        const unsigned r = (unsigned)rows[e], c = (unsigned)cols[e];
-        atomicAdd(&a.len[r], 1u);
-        if (!directed && r != c) atomicAdd(&a.len[c], 1u);
-    }
-}
-
-// rare path 2: per-class sums of g over every stream entry of rows with repeats
-__global__ void k_bm_zsum(const int64_t *__restrict__ rows, const int64_t *__restrict__ cols, int64_t E,
-                          int directed, BmArgs a) {
-    if (!__ldcg(a.flags)) return;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += stride) {
-        const unsigned r = (unsigned)rows[e], c = (unsigned)cols[e];
-        if (a.len[r] != a.ucnt[r] && a.tab_lab[c] >= 0)
-            atomicAdd(&a.zacc[(size_t)r * kZacc + a.tab_lab[c]], a.tab_g[c]);
-        if (!directed && r != c && a.len[c] != a.ucnt[c] && a.tab_lab[r] >= 0)
-            atomicAdd(&a.zacc[(size_t)c * kZacc + a.tab_lab[r]], a.tab_g[r]);
+        if (u) atomicAdd(a.flags + 2, u);  // popc(U): S = U for directed lists
+        node_entry(a, r, u);
     }
 }
 
 // ---------------------------------------------------------------------------
-template <int KP>
-__global__ void __launch_bounds__(kRowsNT) k_bm_rows(BmArgs a) {
-    extern __shared__ __align__(16) unsigned char sm_raw[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    constexpr int kWarps = kRowsNT / 32;
-    double *tg = reinterpret_cast<double *>(sm_raw);                            // [n]
-    signed char *tl = reinterpret_cast<signed char *>(tg + ((a.n + 1) & ~1));   // [n]
-    // stage the node table (written by k_bm_scan) with 16-byte loads
-    {
-        const int n2 = a.n / 2;
-        const double2 *src = reinterpret_cast<const double2 *>(a.tab_g);
-        double2 *dst = reinterpret_cast<double2 *>(tg);
-        for (int j = threadIdx.x; j < n2; j += blockDim.x) dst[j] = __ldcg(src + j);
-        if ((a.n & 1) && threadIdx.x == 0) tg[a.n - 1] = __ldcg(a.tab_g + a.n - 1);
-        const int n16 = a.n / 16;
-        const int4 *ls = reinterpret_cast<const int4 *>(a.tab_lab);
-        for (int j = threadIdx.x; j < n16; j += blockDim.x) reinterpret_cast<int4 *>(tl)[j] = __ldcg(ls + j);
-        for (int j = n16 * 16 + threadIdx.x; j < a.n; j += blockDim.x) tl[j] = a.tab_lab[j];
+// rare path
+__device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        while (ld_gpu(ctr) < target) __nanosleep(32);
+        __threadfence();
     }
     __syncthreads();
-    const bool lap = (a.flags_opts & GEE_LAPLACIAN) != 0, diag = (a.flags_opts & GEE_DIAGONAL) != 0;
-    const int Wp = a.Wp;
-    const bool any_rep = __ldcg(a.flags) != 0;
-    for (int r = blockIdx.x * kWarps + wid; r < a.n; r += gridDim.x * kWarps) {
-        double acc[KP];
+}
+
+// rare path phases 1-3 (all CTAs of k_bm_gemm; co-resident)
+__device__ void repeat_phases(const int64_t *__restrict__ rows, const int64_t *__restrict__ cols, const BmArgs &a) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const bool und = !a.directed;
+    // 1: exact stream lengths
+    for (int64_t i = tid; i < (int64_t)a.n * kKMax; i += nth) a.zacc[i] = 0.0;
+    for (int64_t e = tid; e < a.E; e += nth) {
+        const unsigned r = (unsigned)rows[e], c = (unsigned)cols[e];
+        atomicAdd(&a.len[r], 1u);
+        if (und && r != c) atomicAdd(&a.len[c], 1u);
+    }
+    grid_barrier(a.flags + 1, gridDim.x);
+    // 2: node table from the stream lengths
+    for (int64_t r = tid; r < a.n; r += nth) node_entry(a, (int)r, __ldcg(a.len + r));
+    grid_barrier(a.flags + 1, 2 * gridDim.x);
+    // 3: per-class sums of g over every stream entry of rows with repeats
+    for (int64_t e = tid; e < a.E; e += nth) {
+        const unsigned r = (unsigned)rows[e], c = (unsigned)cols[e];
+        if (__ldcg(a.len + r) != __ldcg(a.ucnt + r)) {
+            const int lab = __ldcg(a.tab_lab + c);
+            if (lab >= 0) atomicAdd(&a.zacc[(size_t)r * kKMax + lab], __ldcg(a.tab_g + c));
+        }
+        if (und && r != c && __ldcg(a.len + c) != __ldcg(a.ucnt + c)) {
+            const int lab = __ldcg(a.tab_lab + r);
+            if (lab >= 0) atomicAdd(&a.zacc[(size_t)c * kKMax + lab], __ldcg(a.tab_g + r));
+        }
+    }
+    grid_barrier(a.flags + 1, 3 * gridDim.x);
+}
+
+// ---------------------------------------------------------------------------
+// k_bm_gemm: tcgen05 helpers (inline PTX, sm_100a)
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "GEE_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra GEE_DONE;\n\t"
+        "bra GEE_WAIT;\n"
+        "GEE_DONE:\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+// K-major operand, 128-byte swizzle: 8-row core groups 1024 B apart
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+    uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+    d |= (uint64_t)1 << 16;             // leading byte offset (unused: K fits one swizzle row)
+    d |= (uint64_t)(1024 >> 4) << 32;   // stride byte offset
+    d |= (uint64_t)1 << 46;             // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;             // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+
+// 8 bits of a word -> 8 bytes of 0/1 (two u32): nibble * 0x00204081 puts
+// bit i of the nibble at bit 8i, no carries
+__device__ __forceinline__ uint4 expand16(unsigned w) {
+    uint4 o;
+    o.x = ((w & 0xFu) * 0x00204081u) & 0x01010101u;
+    o.y = (((w >> 4) & 0xFu) * 0x00204081u) & 0x01010101u;
+    o.z = (((w >> 8) & 0xFu) * 0x00204081u) & 0x01010101u;
+    o.w = (((w >> 12) & 0xFu) * 0x00204081u) & 0x01010101u;
+    return o;
+}
+
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// 2^e for a normal exponent, exactly
+__device__ __forceinline__ double pow2i(int e) {
+    return __longlong_as_double((long long)(1023 + e) << 52);
+}
+
+// Z row epilogue (one thread per row): per-class sums v_q of s_c (digits
+// recombined, or the rare path's f64 sums of g), then 1/n_q, diagonal, s_r,
+// correlation
+template <int NB>
+__device__ __forceinline__ void gemm_epilogue(const BmArgs &a, int r, const int32_t (&C)[NB], bool rep) {
+    double acc[kKMax];
+    const bool lap = (a.flags_opts & GEE_LAPLACIAN) != 0;
+    if (rep) {
 #pragma unroll
-        for (int q = 0; q < KP; ++q) acc[q] = 0.0;
-        if (any_rep && __ldcg(a.len + r) != __ldcg(a.ucnt + r)) {
-            // a row with repeated pairs: its class sums come from k_bm_zsum
-            if (lane == 0) {
+        for (int q = 0; q < kKMax; ++q) acc[q] = q < a.k ? __ldcg(a.zacc + (size_t)r * kKMax + q) : 0.0;
+    } else {
 #pragma unroll
-                for (int q = 0; q < KP; ++q) acc[q] = __ldcg(a.zacc + (size_t)r * kZacc + q);
+        for (int q = 0; q < kKMax; ++q) {
+            double v = 0.0;
+            if (q * kDig + kDig <= NB && q < a.k) {
+#pragma unroll
+                for (int d = 0; d < kDig; ++d) v += (double)C[q * kDig + d] * pow2i(8 * d - 55);
+                v *= __ldcg(a.inv + q);
+            }
+            acc[q] = v;
+        }
+    }
+    const double sr = lap ? __ldcg(a.scale + r) : 1.0;
+    if (a.flags_opts & GEE_DIAGONAL) {
+        // A+I: the diagonal gains 1.0 whether or not (r, r) is stored
+        const int lab = a.y32[r];
+#pragma unroll
+        for (int q = 0; q < kKMax; ++q)
+            if (q == lab) acc[q] += sr * __ldcg(a.inv + q);
+    }
+    if (lap) {
+#pragma unroll
+        for (int q = 0; q < kKMax; ++q) acc[q] *= sr;
+    }
+    if (a.flags_opts & GEE_CORRELATION) {
+        double ss = 0.0;
+        bool fin = true;
+#pragma unroll
+        for (int q = 0; q < kKMax; ++q) {
+            if (q < a.k) {
+                ss += acc[q] * acc[q];
+                fin &= isfinite(acc[q]);
+            }
+        }
+        if (!fin) {
+            raise_err(a.err, GEE_ERR_NONFINITE);
+        } else {
+            const double nrm = __dsqrt_rn(ss);
+            if (nrm > 0.0) {
+#pragma unroll
+                for (int q = 0; q < kKMax; ++q) acc[q] = __ddiv_rn(acc[q], nrm);
+            }
+        }
+    }
+    double *zr = a.z + (int64_t)r * a.k;
+#pragma unroll
+    for (int q = 0; q < kKMax; ++q)
+        if (q < a.k) zr[q] = acc[q];
+}
+
+// smem: A stages [kStages][128 x 128 B], B stages [kStages][NB x 128 B],
+// mbarriers, the TMEM address slot (1024-B aligned base)
+template <int NB>
+__global__ void __launch_bounds__(kGemmNT) k_bm_gemm(const int64_t *__restrict__ rows,
+                                                     const int64_t *__restrict__ cols, BmArgs a, int splits,
+                                                     int kps) {
+    extern __shared__ unsigned char sm_raw[];
+    constexpr int kAB = kTM * kTK;   // 16 KB
+    constexpr int kBB = NB * kTK;
+    constexpr int kTmemCols = NB < 32 ? 32 : NB;
+    unsigned char *sm = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *sA = sm;
+    unsigned char *sB = sm + kStages * kAB;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + kStages * kBB);
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + kStages);
+    __shared__ bool last_split;
+
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const bool rep = __ldcg(a.flags) != 0 || (int64_t)__ldcg(a.flags + 2) != a.E;
+    if (rep) repeat_phases(rows, cols, a);
+
+    const int mtile = blockIdx.x / splits, split = blockIdx.x % splits;
+    if (w == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (t == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(smem_u32(bars + s), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tslot;
+
+    const int KT = a.Np / kTK;
+    const int kb = split * kps, ke = min(KT, kb + kps), nit = max(0, ke - kb);
+    const uint32_t idesc = (2u << 4) | ((uint32_t)(NB >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+    const int rl = t >> 1, h = t & 1;  // A producer: row of the tile, which half of its 4 words
+    const unsigned *arow = a.bm + (size_t)(mtile * kTM + rl) * a.Wp + 2 * h;
+    for (int it = 0; it < nit; ++it) {
+        const int st = it % kStages;
+        if (it >= kStages) mbar_wait(smem_u32(bars + st), ((it / kStages) - 1) & 1);
+        const int ks = kb + it;
+        // A: 2 bitmap words -> 64 bytes (chunks 4h..4h+3 of the row, swizzled)
+        {
+            const uint2 wd = __ldcg(reinterpret_cast<const uint2 *>(arow + ks * 4));
+            const uint32_t base = smem_u32(sA + st * kAB) + (rl >> 3) * 1024 + (rl & 7) * 128;
+            const int sw = rl & 7;
+            sts128(base + (((4 * h + 0) ^ sw) << 4), expand16(wd.x));
+            sts128(base + (((4 * h + 1) ^ sw) << 4), expand16(wd.x >> 16));
+            sts128(base + (((4 * h + 2) ^ sw) << 4), expand16(wd.y));
+            sts128(base + (((4 * h + 3) ^ sw) << 4), expand16(wd.y >> 16));
+        }
+        // B: NB rows x 128 B of X^T
+        for (int i = t; i < NB * 8; i += kGemmNT) {
+            const int j = i >> 3, c = i & 7;
+            const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(a.xt + (size_t)j * a.Np + (size_t)ks * kTK + c * 16));
+            sts128(smem_u32(sB + st * kBB) + (j >> 3) * 1024 + (j & 7) * 128 + ((c ^ (j & 7)) << 4), v);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (t == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint64_t ad = sdesc_sw128(smem_u32(sA + st * kAB));
+            const uint64_t bd = sdesc_sw128(smem_u32(sB + st * kBB));
+#pragma unroll
+            for (int k = 0; k < kTK / 32; ++k)
+                mma_i8(tmem, ad + 2 * k, bd + 2 * k, idesc, (it | k) != 0);
+            mma_commit(smem_u32(bars + st));
+        }
+    }
+    if (nit > 0) mbar_wait(smem_u32(bars + (nit - 1) % kStages), ((nit - 1) / kStages) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+    // accumulators: warp w < 4 owns TMEM lanes 32w..32w+31 = tile rows
+    int32_t C[NB];
+    const int r = mtile * kTM + w * 32 + lane;
+    if (w < 4) {
+        if (nit > 0) {
+#pragma unroll
+            for (int c0 = 0; c0 < NB; c0 += 16) {
+                uint32_t v[16];
+                tmem_ld16(tmem + ((uint32_t)(w * 32) << 16) + c0, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 16; ++j) C[c0 + j] = (int32_t)v[j];
             }
         } else {
-            const unsigned *row = a.bm + (size_t)r * Wp;
-            unsigned wv[kWordsPerLane];
 #pragma unroll
-            for (int i = 0; i < kWordsPerLane; ++i) {
-                const int w = i * 32 + lane;
-                wv[i] = w < Wp ? __ldcg(row + w) : 0u;
-            }
-#pragma unroll
-            for (int i = 0; i < kWordsPerLane; ++i) {
-                unsigned word = wv[i];
-                const int base = (i * 32 + lane) * 32;
-                while (word) {
-                    const int c = base + __ffs(word) - 1;
-                    word &= word - 1;
-                    const int lab = tl[c];
-                    const double x = tg[c];
-#pragma unroll
-                    for (int q = 0; q < KP; ++q) acc[q] += (lab == q) ? x : 0.0;
-                }
-            }
+            for (int j = 0; j < NB; ++j) C[j] = 0;
         }
-#pragma unroll
-        for (int q = 0; q < KP; ++q) acc[q] = warp_sum(acc[q]);
-        if (diag) {
-            // A+I: the diagonal gains 1.0 whether or not (r, r) is stored
-            const int lab = tl[r];
-            const double x = tg[r];
-#pragma unroll
-            for (int q = 0; q < KP; ++q) acc[q] += (lab == q) ? x : 0.0;
-        }
-        if (lap) {
-            const double sr = __ldcg(a.scale + r);
-#pragma unroll
-            for (int q = 0; q < KP; ++q) acc[q] *= sr;
-        }
-        if (a.flags_opts & GEE_CORRELATION) {
-            double ss = 0.0;
-            bool fin = true;
-#pragma unroll
-            for (int q = 0; q < KP; ++q) {
-                if (q < a.k) {
-                    ss += acc[q] * acc[q];
-                    fin &= isfinite(acc[q]);
-                }
-            }
-            if (!fin) {
-                if (lane == 0) raise_err(a.err, GEE_ERR_NONFINITE);
-            } else {
-                const double nrm = __dsqrt_rn(ss);
-                if (nrm > 0.0) {
-#pragma unroll
-                    for (int q = 0; q < KP; ++q) acc[q] = __ddiv_rn(acc[q], nrm);
-                }
-            }
-        }
-        double mine = 0.0;
-#pragma unroll
-        for (int q = 0; q < KP; ++q) mine = (lane == q) ? acc[q] : mine;
-        if (lane < a.k) a.z[(int64_t)r * a.k + lane] = mine;
     }
+    bool finish = true;
+    if (splits > 1) {
+        if (w < 4) {
+            int4 *dst = reinterpret_cast<int4 *>(a.cpart + ((size_t)split * a.Np + r) * NB);
+#pragma unroll
+            for (int j = 0; j < NB / 4; ++j) dst[j] = make_int4(C[4 * j], C[4 * j + 1], C[4 * j + 2], C[4 * j + 3]);
+        }
+        __threadfence();
+        __syncthreads();
+        if (t == 0) last_split = atomicAdd(&a.mdone[mtile], 1u) == (unsigned)splits - 1;
+        __syncthreads();
+        finish = last_split;
+        if (finish && w < 4) {
+            __threadfence();
+            for (int s = 0; s < splits; ++s) {
+                if (s == split) continue;
+                const int4 *src = reinterpret_cast<const int4 *>(a.cpart + ((size_t)s * a.Np + r) * NB);
+#pragma unroll
+                for (int j = 0; j < NB / 4; ++j) {
+                    const int4 v = __ldcg(src + j);
+                    C[4 * j] += v.x, C[4 * j + 1] += v.y, C[4 * j + 2] += v.z, C[4 * j + 3] += v.w;
+                }
+            }
+        }
+    }
+    if (finish && w < 4 && r < a.n) {
+        const bool rrep = rep && __ldcg(a.len + r) != __ldcg(a.ucnt + r);
+        gemm_epilogue<NB>(a, r, C, rrep);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
 
 // ---------------------------------------------------------------------------
 int force_path();
 
-// unit weights, square, at most kBmMax nodes, K <= 8 (register accumulators)
+// unit weights, square, at most kBmMax nodes, K <= 8
 bool bitmap_path_ok(int wt, int64_t E, int64_t n_rows, int64_t n_cols, int directed, int k) {
     if (force_path() != 0) return false;  // test hook: exercise the general paths
     const int64_t M = directed ? E : 2 * E;
-    return wt == GEE_W_UNIT && n_rows == n_cols && n_rows >= 1 && n_rows <= kBmMax && k >= 1 && k <= kZacc &&
+    return wt == GEE_W_UNIT && n_rows == n_cols && n_rows >= 1 && n_rows <= kBmMax && k >= 1 && k <= kKMax &&
            M < ((int64_t)1 << 31);
 }
 
+static int nb_cols(int k) {
+    const int need = k * kDig;
+    return need <= 16 ? 16 : need <= 32 ? 32 : 64;
+}
+
+template <int NB>
+constexpr size_t gemm_smem() {
+    return 1024 + kStages * (size_t)(kTM * kTK + NB * kTK) + 8 * kStages + 16;
+}
+
+// co-resident CTAs per SM of k_bm_gemm<NB> (the rare path's grid barrier and
+// the cooperative launch need every CTA resident)
+template <int NB>
+static int gemm_occupancy() {
+    static int occ = 0;
+    if (!occ) {
+        if (cudaFuncSetAttribute(k_bm_gemm<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem<NB>()) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(k_bm_gemm<NB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bm_gemm<NB>, kGemmNT, gemm_smem<NB>()) !=
+                cudaSuccess ||
+            occ < 1)
+            occ = 1;
+    }
+    return occ;
+}
+
+static int gemm_splits(int64_t np, int nbx) {
+    const int occ = nbx == 16 ? gemm_occupancy<16>() : nbx == 32 ? gemm_occupancy<32>() : gemm_occupancy<64>();
+    const int mt = (int)(np / kTM), kt = (int)(np / kTK);
+    int s = (occ * num_sms()) / mt;
+    if (s < 1) s = 1;
+    if (s > kt) s = kt;
+    return s;
+}
+
 struct BmWs {
-    unsigned *bm, *len, *flags, *ucnt;
+    unsigned *bm, *ucnt, *len, *cnt, *blkdone, *mdone, *flags;
+    unsigned char *xt;
+    int32_t *cpart;
     double *zacc, *tab_g;
     signed char *tab_lab;
-    int Wp, nb;
-    size_t clear_words;
+    int Wp, nb, Np, nbx, splits;
+    size_t clear_bytes;
 };
 
-static void carve_bm(Carver &cv, BmWs &w, int64_t n) {
+static void carve_bm(Carver &cv, BmWs &w, int64_t n, int k) {
     const int64_t np = (n + kBlk - 1) / kBlk * kBlk;
     w.nb = (int)(np / kBlk);
     w.Wp = (int)(np / 32);
-    // bitmap, stream lengths and flags are contiguous: one memset clears them
-    w.clear_words = (size_t)np * w.Wp + (size_t)n + 4;
-    w.bm = cv.take<unsigned>(w.clear_words);
-    w.len = w.bm ? w.bm + (size_t)np * w.Wp : nullptr;
-    w.flags = w.bm ? w.len + n : nullptr;
-    w.ucnt = cv.take<unsigned>((size_t)n);
-    w.zacc = cv.take<double>((size_t)n * kZacc);
+    w.Np = (int)np;
+    w.nbx = nb_cols(k);
+    w.splits = gemm_splits(np, w.nbx);
+    // bitmap, counters, flags and X^T are contiguous: one memset clears them
+    const size_t bmw = (size_t)np * w.Wp;
+    const size_t words = (bmw + 2 * (size_t)n + kKMax + (size_t)w.nb + (size_t)(np / kTM) + 4 + 3) & ~size_t(3);
+    const size_t xbytes = (size_t)w.nbx * (size_t)np;
+    w.clear_bytes = 4 * words + xbytes;
+    unsigned char *base = cv.take<unsigned char>(w.clear_bytes);
+    w.bm = reinterpret_cast<unsigned *>(base);
+    w.ucnt = w.bm ? w.bm + bmw : nullptr;
+    w.len = w.bm ? w.ucnt + n : nullptr;
+    w.cnt = w.bm ? w.len + n : nullptr;
+    w.blkdone = w.bm ? w.cnt + kKMax : nullptr;
+    w.mdone = w.bm ? w.blkdone + w.nb : nullptr;
+    w.flags = w.bm ? w.mdone + np / kTM : nullptr;
+    w.xt = base ? base + 4 * words : nullptr;
+    w.cpart = cv.take<int32_t>(w.splits > 1 ? (size_t)w.splits * np * w.nbx : 1);
+    w.zacc = cv.take<double>((size_t)n * kKMax);
     w.tab_g = cv.take<double>((size_t)n + 2);
     w.tab_lab = cv.take<signed char>((size_t)n + 16);
 }
 
-size_t bitmap_workspace(int64_t E, int64_t n, int directed) {
+size_t bitmap_workspace(int64_t E, int64_t n, int directed, int k) {
     (void)E;
     (void)directed;
     Carver cv(nullptr);
     BmWs w;
-    carve_bm(cv, w, n);
+    carve_bm(cv, w, n, k);
     return cv.bytes();
 }
 
-// The fused encode for unit-weight graphs.  Outputs: Z (n x k) and, under
-// the Laplacian, deg / scale.  The CSR is not materialised.
+template <int NB>
+static int launch_gemm(const BmArgs &a, const int64_t *rows, const int64_t *cols, int splits, cudaStream_t st) {
+    gemm_occupancy<NB>();  // function attributes
+    const int mt = a.Np / kTM, kt = a.Np / kTK;
+    const int kps = (kt + splits - 1) / splits;
+    // cooperative: every CTA co-resident (or a launch error, never a hang)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(mt * splits));
+    cfg.blockDim = dim3(kGemmNT);
+    cfg.dynamicSmemBytes = gemm_smem<NB>();
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    GEE_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_bm_gemm<NB>, rows, cols, a, splits, kps));
+    GEE_CHECK_LAUNCH("k_bm_gemm");
+    return GEE_OK;
+}
+
+// The fused encode for unit-weight graphs, labels included.  Outputs: y32,
+// counts, 1/n_k, Z (n x k) and, under the Laplacian, deg / scale.  The CSR
+// is not materialised.
 int bitmap_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n, int directed,
-                  const int32_t *y32, const double *inv, int k, unsigned flags, double *deg, double *scale,
-                  double *z, void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st) {
+                  const int64_t *labels, int k, unsigned flags, int32_t *y32, int64_t *counts, double *inv,
+                  double *deg, double *scale, double *z, void *ws, size_t ws_bytes, int32_t *err,
+                  cudaStream_t st) {
     Carver cv(ws);
     BmWs W;
-    carve_bm(cv, W, n);
+    carve_bm(cv, W, n, k);
     if (ws_bytes < cv.bytes()) return GEE_E_WORKSPACE;
     BmArgs a;
     a.n = (int)n;
     a.Wp = W.Wp;
     a.nb = W.nb;
+    a.Np = W.Np;
+    a.E = E;
+    a.directed = directed;
     a.bm = W.bm;
-    a.len = W.len;
-    a.flags = W.flags;
     a.ucnt = W.ucnt;
+    a.len = W.len;
+    a.cnt = W.cnt;
+    a.blkdone = W.blkdone;
+    a.mdone = W.mdone;
+    a.flags = W.flags;
+    a.xt = W.xt;
+    a.nbx = W.nbx;
+    a.cpart = W.cpart;
     a.zacc = W.zacc;
+    a.labels = labels;
+    a.y32 = y32;
+    a.counts = counts;
+    a.inv = inv;
     a.deg = deg;
     a.scale = scale;
-    a.y32 = y32;
-    a.inv = inv;
     a.tab_g = W.tab_g;
     a.tab_lab = W.tab_lab;
     a.flags_opts = flags;
     a.z = z;
     a.k = k;
     a.err = err;
-    const size_t rows_smem = 8 * (size_t)((n + 1) & ~1) + (size_t)((n + 15) & ~15);
-    static bool attr = false;
-    if (!attr) {
-        const int mx = (int)(8 * (size_t)kBmMax + kBmMax);
-        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_bm_rows<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_bm_rows<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_bm_rows<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_bm_rows<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-        attr = true;
+    GEE_CHECK_CUDA(cudaMemsetAsync(W.bm, 0, W.clear_bytes, st));
+    k_bm_set<<<(unsigned)num_sms() * 4, kSetThreads, 0, st>>>(rows, cols, a);
+    GEE_CHECK_LAUNCH("k_bm_set");
+    if (!directed) {
+        k_bm_sym<<<(unsigned)(W.nb * (W.nb + 1) / 2), kBlk, 0, st>>>(a);
+        GEE_CHECK_LAUNCH("k_bm_sym");
+    } else {
+        k_bm_scan<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(a);
+        GEE_CHECK_LAUNCH("k_bm_scan");
     }
-    GEE_CHECK_CUDA(cudaMemsetAsync(W.bm, 0, sizeof(unsigned) * W.clear_words, st));
-    if (E > 0) {
-        k_bm_set<<<grid_for(E, kSetThreads * 4, 8), kSetThreads, 0, st>>>(rows, cols, E, a);
-        GEE_CHECK_LAUNCH("k_bm_set");
-        if (!directed) {
-            k_bm_sym<<<(unsigned)(W.nb * (W.nb + 1) / 2), kBlk, 0, st>>>(a);
-            GEE_CHECK_LAUNCH("k_bm_sym");
-        }
-        k_bm_len<<<grid_for(E, 256, 2), 256, 0, st>>>(rows, cols, E, directed, a);
-        GEE_CHECK_LAUNCH("k_bm_len");
-    }
-    k_bm_scan<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(a);
-    GEE_CHECK_LAUNCH("k_bm_scan");
-    if (E > 0) {
-        k_bm_zsum<<<grid_for(E, 256, 2), 256, 0, st>>>(rows, cols, E, directed, a);
-        GEE_CHECK_LAUNCH("k_bm_zsum");
-    }
-    const unsigned grid = (unsigned)num_sms();
-    if (k <= 1)
-        k_bm_rows<1><<<grid, kRowsNT, rows_smem, st>>>(a);
-    else if (k <= 2)
-        k_bm_rows<2><<<grid, kRowsNT, rows_smem, st>>>(a);
-    else if (k <= 4)
-        k_bm_rows<4><<<grid, kRowsNT, rows_smem, st>>>(a);
-    else
-        k_bm_rows<8><<<grid, kRowsNT, rows_smem, st>>>(a);
-    GEE_CHECK_LAUNCH("k_bm_rows_embed");
-    return GEE_OK;
+    if (W.nbx == 16) return launch_gemm<16>(a, rows, cols, W.splits, st);
+    if (W.nbx == 32) return launch_gemm<32>(a, rows, cols, W.splits, st);
+    return launch_gemm<64>(a, rows, cols, W.splits, st);
 }
 
 }  // namespace gee
