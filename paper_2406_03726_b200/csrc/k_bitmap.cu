@@ -39,6 +39,9 @@
 // are co-resident); those rows take their sums from there.
 #include "gee_common.cuh"
 
+#include <stdio.h>
+#include <stdlib.h>
+
 namespace gee {
 
 constexpr int kBmMax = 16384;   // nodes: bitmap Np^2/8 <= 32 MB (L2-resident)
@@ -48,8 +51,6 @@ constexpr int kKMax = 8;        // classes
 constexpr int kDig = 7;         // base-256 digits of s * 2^55
 constexpr int kTM = 128;        // GEMM rows per tile (TMEM lanes)
 constexpr int kTK = 128;        // GEMM columns per K step (bytes of a swizzle row)
-constexpr int kStages = 4;
-constexpr int kGemmNT = 256;
 
 struct BmArgs {
     int n, Wp, nb, Np;        // nodes, bitmap words per row (multiple of 8), 256-row blocks, Wp*32
@@ -60,11 +61,11 @@ struct BmArgs {
     unsigned *len;            // [n] stream lengths (rare path)
     unsigned *cnt;            // [kKMax] class histogram
     unsigned *blkdone;        // [nb] finished block pairs per 256-row block
-    unsigned *mdone;          // [Np/128] split-K arrivals per GEMM row tile
+    unsigned *mdone;          // [Np/128] K steps accumulated per GEMM row tile
     unsigned *flags;          // [0] pair in both directions, [1] grid barrier, [2] popc(U)
     unsigned char *xt;        // [NB][Np] X^T digits (K-major B operand)
     int nbx;                  // NB: X columns (kDig * K padded to 16/32/64)
-    int32_t *cpart;           // [splits][Np][NB] split-K partial sums
+    int32_t *cpart;           // [Np][NB] integer GEMM accumulators (stream-K partials added)
     double *zacc;             // [n][kKMax] rare path class sums
     const int64_t *labels;
     int32_t *y32;
@@ -500,35 +501,88 @@ __device__ __forceinline__ void gemm_epilogue(const BmArgs &a, int r, const int3
         if (q < a.k) zr[q] = acc[q];
 }
 
-// smem: A stages [kStages][128 x 128 B], B stages [kStages][NB x 128 B],
-// mbarriers, the TMEM address slot (1024-B aligned base)
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// k_bm_gemm geometry
+constexpr int kAS = 4;          // expanded A stages (16 KB each)
+constexpr int kRR = 12;         // raw stages: 128 x 16 B of bitmap words + the B tile
+constexpr int kPF = 10;         // cp.async prefetch distance (< kRR)
+constexpr int kGemmNT = 288;    // warps 0-3 producers, 4-7 epilogue, 8 MMA
+
 template <int NB>
-__global__ void __launch_bounds__(kGemmNT) k_bm_gemm(const int64_t *__restrict__ rows,
-                                                     const int64_t *__restrict__ cols, BmArgs a, int splits,
-                                                     int kps) {
+constexpr size_t gemm_smem() {
+    return 1024 + (size_t)kAS * kTM * kTK + (size_t)kRR * (kTM * 16 + NB * kTK) +
+           8 * (2 * kAS + kRR + 4) + 16;
+}
+
+// Stream-K over the flattened (row tile, K step) space: CTA b takes steps
+// [b*T/G, (b+1)*T/G), T = tiles * KT, so every CTA does the same number of K
+// steps; the steps of one row tile form a segment whose integer partial sums
+// are added to Cacc, and the CTA completing a tile's KT steps runs its
+// epilogue.  Warps 0-3 produce (thread = tile row): cp.async of the row's 16
+// bitmap bytes and of the B tile kPF steps ahead, then the bit -> byte
+// expansion into the swizzled A stage; warp 8 issues the MMAs into one of two
+// TMEM accumulators (segment parity); warps 4-7 drain the accumulators.
+template <int NB>
+__global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restrict__ rows,
+                                                        const int64_t *__restrict__ cols, BmArgs a) {
     extern __shared__ unsigned char sm_raw[];
     constexpr int kAB = kTM * kTK;   // 16 KB
+    constexpr int kRB = kTM * 16;    // 2 KB raw bitmap bytes
     constexpr int kBB = NB * kTK;
-    constexpr int kTmemCols = NB < 32 ? 32 : NB;
+    constexpr int kTmemCols = 2 * NB < 32 ? 32 : 2 * NB;
     unsigned char *sm = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
     unsigned char *sA = sm;
-    unsigned char *sB = sm + kStages * kAB;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + kStages * kBB);
-    uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + kStages);
-    __shared__ bool last_split;
+    unsigned char *sB = sA + kAS * kAB;
+    unsigned char *sR = sB + kRR * kBB;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sR + kRR * kRB);
+    uint64_t *aempty = full + kAS;
+    uint64_t *rempty = aempty + kAS;
+    uint64_t *accfull = rempty + kRR;
+    uint64_t *accempty = accfull + 2;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(accempty + 2);
+    __shared__ bool s_last;
 
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const bool rep = __ldcg(a.flags) != 0 || (int64_t)__ldcg(a.flags + 2) != a.E;
     if (rep) repeat_phases(rows, cols, a);
 
-    const int mtile = blockIdx.x / splits, split = blockIdx.x % splits;
-    if (w == 0) {
+    if (w == 8) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
                      "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (t == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(smem_u32(bars + s), 1);
+        for (int s = 0; s < kAS; ++s) {
+            mbar_init(smem_u32(full + s), kTM);
+            mbar_init(smem_u32(aempty + s), 1);
+        }
+        for (int s = 0; s < kRR; ++s) mbar_init(smem_u32(rempty + s), 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(smem_u32(accfull + s), 1);
+            mbar_init(smem_u32(accempty + s), kTM);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -537,95 +591,132 @@ __global__ void __launch_bounds__(kGemmNT) k_bm_gemm(const int64_t *__restrict__
     const uint32_t tmem = *tslot;
 
     const int KT = a.Np / kTK;
-    const int kb = split * kps, ke = min(KT, kb + kps), nit = max(0, ke - kb);
-    const uint32_t idesc = (2u << 4) | ((uint32_t)(NB >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
-    const int rl = t >> 1, h = t & 1;  // A producer: row of the tile, which half of its 4 words
-    const unsigned *arow = a.bm + (size_t)(mtile * kTM + rl) * a.Wp + 2 * h;
-    for (int it = 0; it < nit; ++it) {
-        const int st = it % kStages;
-        if (it >= kStages) mbar_wait(smem_u32(bars + st), ((it / kStages) - 1) & 1);
-        const int ks = kb + it;
-        // A: 2 bitmap words -> 64 bytes (chunks 4h..4h+3 of the row, swizzled)
-        {
-            const uint2 wd = __ldcg(reinterpret_cast<const uint2 *>(arow + ks * 4));
-            const uint32_t base = smem_u32(sA + st * kAB) + (rl >> 3) * 1024 + (rl & 7) * 128;
-            const int sw = rl & 7;
-            sts128(base + (((4 * h + 0) ^ sw) << 4), expand16(wd.x));
-            sts128(base + (((4 * h + 1) ^ sw) << 4), expand16(wd.x >> 16));
-            sts128(base + (((4 * h + 2) ^ sw) << 4), expand16(wd.y));
-            sts128(base + (((4 * h + 3) ^ sw) << 4), expand16(wd.y >> 16));
-        }
-        // B: NB rows x 128 B of X^T
-        for (int i = t; i < NB * 8; i += kGemmNT) {
-            const int j = i >> 3, c = i & 7;
-            const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(a.xt + (size_t)j * a.Np + (size_t)ks * kTK + c * 16));
-            sts128(smem_u32(sB + st * kBB) + (j >> 3) * 1024 + (j & 7) * 128 + ((c ^ (j & 7)) << 4), v);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        if (t == 0) {
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint64_t ad = sdesc_sw128(smem_u32(sA + st * kAB));
-            const uint64_t bd = sdesc_sw128(smem_u32(sB + st * kBB));
-#pragma unroll
-            for (int k = 0; k < kTK / 32; ++k)
-                mma_i8(tmem, ad + 2 * k, bd + 2 * k, idesc, (it | k) != 0);
-            mma_commit(smem_u32(bars + st));
-        }
-    }
-    if (nit > 0) mbar_wait(smem_u32(bars + (nit - 1) % kStages), ((nit - 1) / kStages) & 1);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int64_t total = (int64_t)(a.Np / kTM) * KT;
+    const int s0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
+    const int s1 = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
+    const int nsteps = s1 - s0;
 
-    // accumulators: warp w < 4 owns TMEM lanes 32w..32w+31 = tile rows
-    int32_t C[NB];
-    const int r = mtile * kTM + w * 32 + lane;
     if (w < 4) {
-        if (nit > 0) {
+        // ---- producers
+        const int rl = t;
+        auto issue = [&](int i) {
+            const int g = s0 + i, m = g / KT, ks = g % KT, rs = i % kRR;
+            cp_async16(smem_u32(sR + rs * kRB + rl * 16), a.bm + (size_t)(m * kTM + rl) * a.Wp + ks * 4);
+#pragma unroll
+            for (int q = 0; q < NB / 16; ++q) {
+                const int ch = rl + q * kTM;
+                const int j = ch >> 3, c = ch & 7;
+                cp_async16(smem_u32(sB + rs * kBB) + (j >> 3) * 1024 + (j & 7) * 128 + ((c ^ (j & 7)) << 4),
+                           a.xt + (size_t)j * a.Np + (size_t)ks * kTK + c * 16);
+            }
+        };
+#pragma unroll 1
+        for (int i = 0; i < kPF; ++i) {
+            if (i < nsteps) issue(i);
+            cp_async_commit();
+        }
+#pragma unroll 1
+        for (int i = 0; i < nsteps; ++i) {
+            const int ip = i + kPF;
+            if (ip < nsteps) {
+                if (ip >= kRR) mbar_wait(smem_u32(rempty + ip % kRR), ((ip / kRR) - 1) & 1);
+                issue(ip);
+            }
+            cp_async_commit();
+            cp_async_wait<kPF>();
+            const int as = i % kAS;
+            if (i >= kAS) mbar_wait(smem_u32(aempty + as), ((i / kAS) - 1) & 1);
+            const uint4 wd = lds128(smem_u32(sR + (i % kRR) * kRB + rl * 16));
+            const uint32_t base = smem_u32(sA + as * kAB) + (rl >> 3) * 1024 + (rl & 7) * 128;
+            const int sw = rl & 7;
+            sts128(base + ((0 ^ sw) << 4), expand16(wd.x));
+            sts128(base + ((1 ^ sw) << 4), expand16(wd.x >> 16));
+            sts128(base + ((2 ^ sw) << 4), expand16(wd.y));
+            sts128(base + ((3 ^ sw) << 4), expand16(wd.y >> 16));
+            sts128(base + ((4 ^ sw) << 4), expand16(wd.z));
+            sts128(base + ((5 ^ sw) << 4), expand16(wd.z >> 16));
+            sts128(base + ((6 ^ sw) << 4), expand16(wd.w));
+            sts128(base + ((7 ^ sw) << 4), expand16(wd.w >> 16));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(smem_u32(full + as));
+        }
+        cp_async_wait<0>();
+    } else if (w == 8) {
+        // ---- MMA issue
+        if (lane == 0) {
+            const uint32_t idesc = (2u << 4) | ((uint32_t)(NB >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+            int seg = 0;
+#pragma unroll 1
+            for (int i = 0; i < nsteps; ++i) {
+                const int ks = (s0 + i) % KT;
+                const bool first = i == 0 || ks == 0, last = i == nsteps - 1 || ks == KT - 1;
+                const int buf = seg & 1;
+                if (first && seg >= 2) mbar_wait(smem_u32(accempty + buf), ((seg >> 1) - 1) & 1);
+                const int as = i % kAS, rs = i % kRR;
+                mbar_wait(smem_u32(full + as), (i / kAS) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint64_t ad = sdesc_sw128(smem_u32(sA + as * kAB));
+                const uint64_t bd = sdesc_sw128(smem_u32(sB + rs * kBB));
+#pragma unroll
+                for (int k = 0; k < kTK / 32; ++k)
+                    mma_i8(tmem + buf * NB, ad + 2 * k, bd + 2 * k, idesc, !(first && k == 0));
+                mma_commit(smem_u32(aempty + as));
+                mma_commit(smem_u32(rempty + rs));
+                if (last) {
+                    mma_commit(smem_u32(accfull + buf));
+                    ++seg;
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---- epilogue: warp 4 + e reads TMEM lanes 32e..32e+31 (= tile rows)
+        const int e = w - 4;
+        int seg = 0;
+#pragma unroll 1
+        for (int i = 0; i < nsteps; ++seg) {
+            const int g = s0 + i, m = g / KT;
+            const int seglen = min(nsteps - i, KT - g % KT);
+            const int buf = seg & 1;
+            mbar_wait(smem_u32(accfull + buf), (seg >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            int32_t C[NB];
 #pragma unroll
             for (int c0 = 0; c0 < NB; c0 += 16) {
                 uint32_t v[16];
-                tmem_ld16(tmem + ((uint32_t)(w * 32) << 16) + c0, v);
+                tmem_ld16(tmem + ((uint32_t)(e * 32) << 16) + buf * NB + c0, v);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
                 for (int j = 0; j < 16; ++j) C[c0 + j] = (int32_t)v[j];
             }
-        } else {
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(smem_u32(accempty + buf));
+            const int r = m * kTM + e * 32 + lane;
+            int32_t *acc = a.cpart + (size_t)r * NB;
 #pragma unroll
-            for (int j = 0; j < NB; ++j) C[j] = 0;
-        }
-    }
-    bool finish = true;
-    if (splits > 1) {
-        if (w < 4) {
-            int4 *dst = reinterpret_cast<int4 *>(a.cpart + ((size_t)split * a.Np + r) * NB);
-#pragma unroll
-            for (int j = 0; j < NB / 4; ++j) dst[j] = make_int4(C[4 * j], C[4 * j + 1], C[4 * j + 2], C[4 * j + 3]);
-        }
-        __threadfence();
-        __syncthreads();
-        if (t == 0) last_split = atomicAdd(&a.mdone[mtile], 1u) == (unsigned)splits - 1;
-        __syncthreads();
-        finish = last_split;
-        if (finish && w < 4) {
+            for (int j = 0; j < NB; ++j)
+                if (C[j]) atomicAdd(acc + j, C[j]);
             __threadfence();
-            for (int s = 0; s < splits; ++s) {
-                if (s == split) continue;
-                const int4 *src = reinterpret_cast<const int4 *>(a.cpart + ((size_t)s * a.Np + r) * NB);
+            epi_bar();
+            if (e == 0 && lane == 0) s_last = atomicAdd(&a.mdone[m], (unsigned)seglen) + seglen == (unsigned)KT;
+            epi_bar();
+            if (s_last && r < a.n) {
+                __threadfence();
+                const int4 *src = reinterpret_cast<const int4 *>(acc);
 #pragma unroll
                 for (int j = 0; j < NB / 4; ++j) {
                     const int4 v = __ldcg(src + j);
-                    C[4 * j] += v.x, C[4 * j + 1] += v.y, C[4 * j + 2] += v.z, C[4 * j + 3] += v.w;
+                    C[4 * j] = v.x, C[4 * j + 1] = v.y, C[4 * j + 2] = v.z, C[4 * j + 3] = v.w;
                 }
+                const bool rrep = rep && __ldcg(a.len + r) != __ldcg(a.ucnt + r);
+                gemm_epilogue<NB>(a, r, C, rrep);
             }
+            i += seglen;
         }
-    }
-    if (finish && w < 4 && r < a.n) {
-        const bool rrep = rep && __ldcg(a.len + r) != __ldcg(a.ucnt + r);
-        gemm_epilogue<NB>(a, r, C, rrep);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    if (w == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
 
 // ---------------------------------------------------------------------------
@@ -644,44 +735,13 @@ static int nb_cols(int k) {
     return need <= 16 ? 16 : need <= 32 ? 32 : 64;
 }
 
-template <int NB>
-constexpr size_t gemm_smem() {
-    return 1024 + kStages * (size_t)(kTM * kTK + NB * kTK) + 8 * kStages + 16;
-}
-
-// co-resident CTAs per SM of k_bm_gemm<NB> (the rare path's grid barrier and
-// the cooperative launch need every CTA resident)
-template <int NB>
-static int gemm_occupancy() {
-    static int occ = 0;
-    if (!occ) {
-        if (cudaFuncSetAttribute(k_bm_gemm<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem<NB>()) !=
-                cudaSuccess ||
-            cudaFuncSetAttribute(k_bm_gemm<NB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess ||
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bm_gemm<NB>, kGemmNT, gemm_smem<NB>()) !=
-                cudaSuccess ||
-            occ < 1)
-            occ = 1;
-    }
-    return occ;
-}
-
-static int gemm_splits(int64_t np, int nbx) {
-    const int occ = nbx == 16 ? gemm_occupancy<16>() : nbx == 32 ? gemm_occupancy<32>() : gemm_occupancy<64>();
-    const int mt = (int)(np / kTM), kt = (int)(np / kTK);
-    int s = (occ * num_sms()) / mt;
-    if (s < 1) s = 1;
-    if (s > kt) s = kt;
-    return s;
-}
-
 struct BmWs {
     unsigned *bm, *ucnt, *len, *cnt, *blkdone, *mdone, *flags;
     unsigned char *xt;
-    int32_t *cpart;
+    int32_t *cacc;
     double *zacc, *tab_g;
     signed char *tab_lab;
-    int Wp, nb, Np, nbx, splits;
+    int Wp, nb, Np, nbx;
     size_t clear_bytes;
 };
 
@@ -691,12 +751,13 @@ static void carve_bm(Carver &cv, BmWs &w, int64_t n, int k) {
     w.Wp = (int)(np / 32);
     w.Np = (int)np;
     w.nbx = nb_cols(k);
-    w.splits = gemm_splits(np, w.nbx);
-    // bitmap, counters, flags and X^T are contiguous: one memset clears them
+    // bitmap, counters, flags, X^T and the GEMM accumulators are contiguous:
+    // one memset clears them
     const size_t bmw = (size_t)np * w.Wp;
     const size_t words = (bmw + 2 * (size_t)n + kKMax + (size_t)w.nb + (size_t)(np / kTM) + 4 + 3) & ~size_t(3);
     const size_t xbytes = (size_t)w.nbx * (size_t)np;
-    w.clear_bytes = 4 * words + xbytes;
+    const size_t cbytes = 4 * (size_t)np * w.nbx;
+    w.clear_bytes = 4 * words + xbytes + cbytes;
     unsigned char *base = cv.take<unsigned char>(w.clear_bytes);
     w.bm = reinterpret_cast<unsigned *>(base);
     w.ucnt = w.bm ? w.bm + bmw : nullptr;
@@ -706,7 +767,7 @@ static void carve_bm(Carver &cv, BmWs &w, int64_t n, int k) {
     w.mdone = w.bm ? w.blkdone + w.nb : nullptr;
     w.flags = w.bm ? w.mdone + np / kTM : nullptr;
     w.xt = base ? base + 4 * words : nullptr;
-    w.cpart = cv.take<int32_t>(w.splits > 1 ? (size_t)w.splits * np * w.nbx : 1);
+    w.cacc = base ? reinterpret_cast<int32_t *>(base + 4 * words + xbytes) : nullptr;
     w.zacc = cv.take<double>((size_t)n * kKMax);
     w.tab_g = cv.take<double>((size_t)n + 2);
     w.tab_lab = cv.take<signed char>((size_t)n + 16);
@@ -722,13 +783,17 @@ size_t bitmap_workspace(int64_t E, int64_t n, int directed, int k) {
 }
 
 template <int NB>
-static int launch_gemm(const BmArgs &a, const int64_t *rows, const int64_t *cols, int splits, cudaStream_t st) {
-    gemm_occupancy<NB>();  // function attributes
-    const int mt = a.Np / kTM, kt = a.Np / kTK;
-    const int kps = (kt + splits - 1) / splits;
-    // cooperative: every CTA co-resident (or a launch error, never a hang)
+static int launch_gemm(const BmArgs &a, const int64_t *rows, const int64_t *cols, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_bm_gemm<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)gemm_smem<NB>()));
+        attr = true;
+    }
+    // persistent stream-K grid, one CTA per SM; cooperative so the rare
+    // path's grid barrier is safe (a launch error, never a hang)
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(mt * splits));
+    cfg.gridDim = dim3((unsigned)num_sms());
     cfg.blockDim = dim3(kGemmNT);
     cfg.dynamicSmemBytes = gemm_smem<NB>();
     cfg.stream = st;
@@ -737,7 +802,7 @@ static int launch_gemm(const BmArgs &a, const int64_t *rows, const int64_t *cols
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    GEE_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_bm_gemm<NB>, rows, cols, a, splits, kps));
+    GEE_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_bm_gemm<NB>, rows, cols, a));
     GEE_CHECK_LAUNCH("k_bm_gemm");
     return GEE_OK;
 }
@@ -769,7 +834,7 @@ int bitmap_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n
     a.flags = W.flags;
     a.xt = W.xt;
     a.nbx = W.nbx;
-    a.cpart = W.cpart;
+    a.cpart = W.cacc;
     a.zacc = W.zacc;
     a.labels = labels;
     a.y32 = y32;
@@ -793,9 +858,9 @@ int bitmap_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n
         k_bm_scan<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(a);
         GEE_CHECK_LAUNCH("k_bm_scan");
     }
-    if (W.nbx == 16) return launch_gemm<16>(a, rows, cols, W.splits, st);
-    if (W.nbx == 32) return launch_gemm<32>(a, rows, cols, W.splits, st);
-    return launch_gemm<64>(a, rows, cols, W.splits, st);
+    if (W.nbx == 16) return launch_gemm<16>(a, rows, cols, st);
+    if (W.nbx == 32) return launch_gemm<32>(a, rows, cols, st);
+    return launch_gemm<64>(a, rows, cols, st);
 }
 
 }  // namespace gee
