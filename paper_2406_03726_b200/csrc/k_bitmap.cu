@@ -50,7 +50,7 @@ constexpr int kSetThreads = 512;
 constexpr int kKMax = 8;        // classes
 constexpr int kDig = 7;         // base-256 digits of s * 2^55
 constexpr int kTM = 128;        // GEMM rows per tile (TMEM lanes)
-constexpr int kTK = 128;        // GEMM columns per K step (bytes of a swizzle row)
+constexpr int kTK = 256;        // GEMM columns per K step (two 128-byte swizzle atoms)
 
 struct BmArgs {
     int n, Wp, nb, Np;        // nodes, bitmap words per row (multiple of 8), 256-row blocks, Wp*32
@@ -65,7 +65,7 @@ struct BmArgs {
     unsigned *flags;          // [0] pair in both directions, [1] grid barrier, [2] popc(U)
     unsigned char *xt;        // [NB][Np] X^T digits (K-major B operand)
     int nbx;                  // NB: X columns (kDig * K padded to 16/32/64)
-    int32_t *cpart;           // [Np][NB] integer GEMM accumulators (stream-K partials added)
+    int32_t *cpart;           // [grid][2][128][NB] stream-K partial sums (slab per CTA segment)
     double *zacc;             // [n][kKMax] rare path class sums
     const int64_t *labels;
     int32_t *y32;
@@ -90,6 +90,21 @@ __device__ __forceinline__ unsigned ld_gpu(const unsigned *p) {
     unsigned v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+
+// The bitmap is stored in 128 x 128-bit tiles (2 KB, row-major inside: a
+// row's 4 words are 16 contiguous bytes), tile (R, K) at (R * Wp/4 + K) * 2 KB,
+// so one GEMM K step of a 128-row tile is one contiguous bulk copy.
+__device__ __forceinline__ unsigned bm_index(const BmArgs &a, unsigned r, unsigned w) {
+    return (((r >> 7) * (unsigned)(a.Wp >> 2) + (w >> 2)) << 9) + ((r & 127u) << 2) + (w & 3u);
+}
+
+// X^T is stored as the K-step tiles of the GEMM's B operand, each exactly its
+// shared-memory image (NB rows x 128 B, 128-byte swizzle: 16-byte chunk c of
+// row j at chunk c ^ (j & 7), 8-row groups 1 KB apart)
+__device__ __forceinline__ size_t xt_index(const BmArgs &a, int j, int c) {
+    const int ks = c >> 7, cin = c & 127;
+    return (size_t)ks * a.nbx * 128 + (j >> 3) * 1024 + (j & 7) * 128 + ((((cin >> 4) ^ (j & 7))) << 4) + (cin & 15);
 }
 
 // 32 x 32 bit transpose across a warp: out(lane i) bit j = in(lane j) bit i
@@ -126,9 +141,8 @@ __device__ __forceinline__ void node_entry(const BmArgs &a, int r, unsigned L) {
         g = (a.flags_opts & GEE_LAPLACIAN) ? sr * inv : inv;
         // X[r, lab] = s_r as 7 base-256 digits of floor(s_r * 2^55) (s_r <= 1)
         const unsigned long long T = __double2ull_rz(sr * 0x1p55);
-        unsigned char *x = a.xt + (size_t)lab * kDig * a.Np + r;
 #pragma unroll
-        for (int d = 0; d < kDig; ++d) x[(size_t)d * a.Np] = (unsigned char)(T >> (8 * d));
+        for (int d = 0; d < kDig; ++d) a.xt[xt_index(a, lab * kDig + d, r)] = (unsigned char)(T >> (8 * d));
     }
     a.tab_g[r] = g;
     a.tab_lab[r] = (signed char)lab;
@@ -182,7 +196,7 @@ __global__ void __launch_bounds__(kSetThreads) k_bm_set(const int64_t *__restric
             const int64_t e = e0 + (int64_t)u * blockDim.x;
             const unsigned r = e < E ? (unsigned)__ldcs(rows + e) : 0u;
             const unsigned c = e < E ? (unsigned)__ldcs(cols + e) : 0u;
-            key[u] = e < E ? r * (unsigned)a.Wp + (c >> 5) : 0xffffffffu;
+            key[u] = e < E ? bm_index(a, r, c >> 5) : 0xffffffffu;
             bit[u] = e < E ? 1u << (c & 31) : 0u;
         }
 #pragma unroll
@@ -217,18 +231,19 @@ __global__ void __launch_bounds__(kBlk) k_bm_sym(BmArgs a) {
     while ((bj + 1) * (bj + 2) / 2 <= x) ++bj;
     while (bj * (bj + 1) / 2 > x) --bj;
     const unsigned bi = x - bj * (bj + 1) / 2;
-    const size_t Wp = (size_t)a.Wp;
     const int ra = bi * kBlk + t, rb = bj * kBlk + t;
-    uint4 *pa = reinterpret_cast<uint4 *>(a.bm + (size_t)ra * Wp + (size_t)bj * 8);
-    uint4 *pb = reinterpret_cast<uint4 *>(a.bm + (size_t)rb * Wp + (size_t)bi * 8);
+    uint4 *pa0 = reinterpret_cast<uint4 *>(a.bm + bm_index(a, ra, bj * 8));
+    uint4 *pa1 = reinterpret_cast<uint4 *>(a.bm + bm_index(a, ra, bj * 8 + 4));
+    uint4 *pb0 = reinterpret_cast<uint4 *>(a.bm + bm_index(a, rb, bi * 8));
+    uint4 *pb1 = reinterpret_cast<uint4 *>(a.bm + bm_index(a, rb, bi * 8 + 4));
     unsigned av[8], bv[8];
     {
-        const uint4 a0 = __ldcg(pa), a1 = __ldcg(pa + 1);
+        const uint4 a0 = __ldcg(pa0), a1 = __ldcg(pa1);
         av[0] = a0.x, av[1] = a0.y, av[2] = a0.z, av[3] = a0.w, av[4] = a1.x, av[5] = a1.y, av[6] = a1.z, av[7] = a1.w;
     }
     const bool same = bi == bj;
     if (!same) {
-        const uint4 b0 = __ldcg(pb), b1 = __ldcg(pb + 1);
+        const uint4 b0 = __ldcg(pb0), b1 = __ldcg(pb1);
         bv[0] = b0.x, bv[1] = b0.y, bv[2] = b0.z, bv[3] = b0.w, bv[4] = b1.x, bv[5] = b1.y, bv[6] = b1.z, bv[7] = b1.w;
     }
     // tile (w, q) of a block transposes into row q*32+lane, word w of its mirror
@@ -260,8 +275,8 @@ __global__ void __launch_bounds__(kBlk) k_bm_sym(BmArgs a) {
             mut |= m;
             ca += __popc(s[q]);
         }
-        pa[0] = make_uint4(s[0], s[1], s[2], s[3]);
-        pa[1] = make_uint4(s[4], s[5], s[6], s[7]);
+        *pa0 = make_uint4(s[0], s[1], s[2], s[3]);
+        *pa1 = make_uint4(s[4], s[5], s[6], s[7]);
     } else {
         unsigned s[8], u[8];
 #pragma unroll
@@ -273,10 +288,10 @@ __global__ void __launch_bounds__(kBlk) k_bm_sym(BmArgs a) {
             ca += __popc(s[q]);
             cb += __popc(u[q]);
         }
-        pa[0] = make_uint4(s[0], s[1], s[2], s[3]);
-        pa[1] = make_uint4(s[4], s[5], s[6], s[7]);
-        pb[0] = make_uint4(u[0], u[1], u[2], u[3]);
-        pb[1] = make_uint4(u[4], u[5], u[6], u[7]);
+        *pa0 = make_uint4(s[0], s[1], s[2], s[3]);
+        *pa1 = make_uint4(s[4], s[5], s[6], s[7]);
+        *pb0 = make_uint4(u[0], u[1], u[2], u[3]);
+        *pb1 = make_uint4(u[4], u[5], u[6], u[7]);
     }
     if (t == 0) {
         unsigned tot = 0;
@@ -308,10 +323,9 @@ __global__ void __launch_bounds__(256) k_bm_scan(BmArgs a) {
     const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (blockIdx.x == 0) write_counts(a, threadIdx.x);
     if (r >= a.n) return;
-    const uint4 *row = reinterpret_cast<const uint4 *>(a.bm + (size_t)r * a.Wp);
     unsigned u = 0;
     for (int i = lane; i < a.Wp / 4; i += 32) {
-        const uint4 v = __ldcg(row + i);
+        const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(a.bm + bm_index(a, r, 4 * i)));
         u += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
     }
     u = warp_sum_u(u);
@@ -388,6 +402,23 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
+// a waiter off the critical path: back off between polls so the spinning
+// warp does not take issue slots from the producers
+__device__ __forceinline__ void mbar_wait_idle(uint32_t bar, uint32_t parity, unsigned ns) {
+    uint32_t ok = 0;
+    for (;;) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P1;\n\t}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(ns);
+    }
+}
+
 // K-major operand, 128-byte swizzle: 8-row core groups 1024 B apart
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
     uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
@@ -404,6 +435,32 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t adesc, uint64_t b
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+
+// A from TMEM (K-major, row = lane), B from shared memory
+__device__ __forceinline__ void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+
+// two bitmap words (64 columns of a row) -> 16 TMEM columns of bytes 0/1
+__device__ __forceinline__ void tmem_st_word2(uint32_t taddr, unsigned x, unsigned y) {
+    uint32_t v[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        v[i] = ((x >> (4 * i)) & 0xFu) * 0x00204081u & 0x01010101u;
+        v[8 + i] = ((y >> (4 * i)) & 0xFu) * 0x00204081u & 0x01010101u;
+    }
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
 }
 
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
@@ -505,15 +562,15 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+// 1-D bulk copy global -> shared (async proxy), completion on an mbarrier
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
 }
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
@@ -524,49 +581,73 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+#ifdef GEE_TRACE
+__device__ unsigned long long g_trace[10][64];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    return v;
+}
+#define TRACE(slot, i) \
+    do {               \
+        if (blockIdx.x == 0 && (i) < 64) g_trace[slot][i] = gtime(); \
+    } while (0)
+#else
+#define TRACE(slot, i) \
+    do {               \
+    } while (0)
+#endif
+
 // k_bm_gemm geometry
-constexpr int kAS = 4;          // expanded A stages (16 KB each)
-constexpr int kRR = 12;         // raw stages: 128 x 16 B of bitmap words + the B tile
-constexpr int kPF = 10;         // cp.async prefetch distance (< kRR)
-constexpr int kGemmNT = 288;    // warps 0-3 producers, 4-7 epilogue, 8 MMA
+constexpr int kAS = 4;          // expanded A stages in TMEM (64 columns = 128 rows x 256 bytes each)
+constexpr int kACols = kTK / 4;  // TMEM columns per A stage (4 bytes per column)
+template <int NB>
+constexpr int rr_stages() { return NB == 64 ? 6 : 8; }  // bulk-copied stages: 4 KB bitmap + the B tile
+template <int NB>
+constexpr int chains() { return NB == 64 ? 2 : 4; }     // independent accumulators per buffer
+constexpr int kGemmNT = 320;    // warps 0-3 expand, 4-7 epilogue, 8 MMA, 9 bulk copies
 
 template <int NB>
 constexpr size_t gemm_smem() {
-    return 1024 + (size_t)kAS * kTM * kTK + (size_t)kRR * (kTM * 16 + NB * kTK) +
-           8 * (2 * kAS + kRR + 4) + 16;
+    return 1024 + (size_t)rr_stages<NB>() * (kTM * 32 + NB * kTK) + 8 * (2 * kAS + 2 * rr_stages<NB>() + 4) + 16;
 }
 
 // Stream-K over the flattened (row tile, K step) space: CTA b takes steps
 // [b*T/G, (b+1)*T/G), T = tiles * KT, so every CTA does the same number of K
 // steps; the steps of one row tile form a segment whose integer partial sums
 // are added to Cacc, and the CTA completing a tile's KT steps runs its
-// epilogue.  Warps 0-3 produce (thread = tile row): cp.async of the row's 16
-// bitmap bytes and of the B tile kPF steps ahead, then the bit -> byte
-// expansion into the swizzled A stage; warp 8 issues the MMAs into one of two
-// TMEM accumulators (segment parity); warps 4-7 drain the accumulators.
+// epilogue.  Warp 9 bulk-copies each step's 2 KB bitmap tile and B tile
+// (kRR stages ahead); warps 0-3 (thread = tile row) expand the row's 256
+// bits to bytes in the swizzled A stage; warp 8 issues the MMAs into one of
+// two TMEM accumulators (segment parity); warps 4-7 drain the accumulators.
 template <int NB>
 __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restrict__ rows,
                                                         const int64_t *__restrict__ cols, BmArgs a) {
     extern __shared__ unsigned char sm_raw[];
-    constexpr int kAB = kTM * kTK;   // 16 KB
-    constexpr int kRB = kTM * 16;    // 2 KB raw bitmap bytes
-    constexpr int kBB = NB * kTK;
-    constexpr int kTmemCols = 2 * NB < 32 ? 32 : 2 * NB;
+    constexpr int kRR = rr_stages<NB>();
+    constexpr int kRB = kTM * 32;    // 4 KB: two consecutive 2 KB bitmap tiles
+    constexpr int kBB = NB * kTK;    // two consecutive X^T tiles
+    constexpr int kChains = chains<NB>();
+    constexpr int kAccCols = 2 * kChains * NB;  // two accumulator buffers, then the A stages
+    constexpr int kTmemCols = 512;
+    static_assert(kAccCols + kAS * kACols <= kTmemCols, "TMEM budget");
     unsigned char *sm = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
-    unsigned char *sA = sm;
-    unsigned char *sB = sA + kAS * kAB;
+    unsigned char *sB = sm;
     unsigned char *sR = sB + kRR * kBB;
     uint64_t *full = reinterpret_cast<uint64_t *>(sR + kRR * kRB);
     uint64_t *aempty = full + kAS;
-    uint64_t *rempty = aempty + kAS;
+    uint64_t *rfull = aempty + kAS;
+    uint64_t *rempty = rfull + kRR;
     uint64_t *accfull = rempty + kRR;
     uint64_t *accempty = accfull + 2;
     uint32_t *tslot = reinterpret_cast<uint32_t *>(accempty + 2);
     __shared__ bool s_last;
 
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (t == 0) TRACE(7, 0);
     const bool rep = __ldcg(a.flags) != 0 || (int64_t)__ldcg(a.flags + 2) != a.E;
     if (rep) repeat_phases(rows, cols, a);
+    if (t == 0) TRACE(7, 1);
 
     if (w == 8) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
@@ -578,7 +659,10 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
             mbar_init(smem_u32(full + s), kTM);
             mbar_init(smem_u32(aempty + s), 1);
         }
-        for (int s = 0; s < kRR; ++s) mbar_init(smem_u32(rempty + s), 1);
+        for (int s = 0; s < kRR; ++s) {
+            mbar_init(smem_u32(rfull + s), 1);
+            mbar_init(smem_u32(rempty + s), kTM + 1);  // expanders read the bitmap tile, the MMA the B tile
+        }
         for (int s = 0; s < 2; ++s) {
             mbar_init(smem_u32(accfull + s), 1);
             mbar_init(smem_u32(accempty + s), kTM);
@@ -589,6 +673,7 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tslot;
+    if (t == 0) TRACE(7, 2);
 
     const int KT = a.Np / kTK;
     const int64_t total = (int64_t)(a.Np / kTM) * KT;
@@ -596,51 +681,44 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
     const int s1 = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
     const int nsteps = s1 - s0;
 
-    if (w < 4) {
-        // ---- producers
-        const int rl = t;
-        auto issue = [&](int i) {
-            const int g = s0 + i, m = g / KT, ks = g % KT, rs = i % kRR;
-            cp_async16(smem_u32(sR + rs * kRB + rl * 16), a.bm + (size_t)(m * kTM + rl) * a.Wp + ks * 4);
-#pragma unroll
-            for (int q = 0; q < NB / 16; ++q) {
-                const int ch = rl + q * kTM;
-                const int j = ch >> 3, c = ch & 7;
-                cp_async16(smem_u32(sB + rs * kBB) + (j >> 3) * 1024 + (j & 7) * 128 + ((c ^ (j & 7)) << 4),
-                           a.xt + (size_t)j * a.Np + (size_t)ks * kTK + c * 16);
-            }
-        };
+    if (w == 9) {
+        // ---- bulk copies
+        if (lane == 0) {
 #pragma unroll 1
-        for (int i = 0; i < kPF; ++i) {
-            if (i < nsteps) issue(i);
-            cp_async_commit();
+            for (int i = 0; i < nsteps; ++i) {
+                const int rs = i % kRR, g = s0 + i, m = g / KT, ks = g % KT;
+                if (i >= kRR) mbar_wait_idle(smem_u32(rempty + rs), ((i / kRR) - 1) & 1, 32);
+                const uint32_t bar = smem_u32(rfull + rs);
+                TRACE(0, i);
+                mbar_expect_tx(bar, kRB + kBB);
+                bulk_g2s(smem_u32(sR + rs * kRB), a.bm + ((size_t)(m * KT + ks) << 10), kRB, bar);
+                bulk_g2s(smem_u32(sB + rs * kBB), a.xt + (size_t)ks * kBB, kBB, bar);
+            }
         }
+        __syncwarp();
+    } else if (w < 4) {
+        // ---- bit -> byte expansion (thread = tile row)
+        const int rl = t;
 #pragma unroll 1
         for (int i = 0; i < nsteps; ++i) {
-            const int ip = i + kPF;
-            if (ip < nsteps) {
-                if (ip >= kRR) mbar_wait(smem_u32(rempty + ip % kRR), ((ip / kRR) - 1) & 1);
-                issue(ip);
-            }
-            cp_async_commit();
-            cp_async_wait<kPF>();
-            const int as = i % kAS;
+            const int rs = i % kRR, as = i % kAS;
+            mbar_wait(smem_u32(rfull + rs), (i / kRR) & 1);
+            const uint4 w0 = lds128(smem_u32(sR + rs * kRB + rl * 16));
+            const uint4 w1 = lds128(smem_u32(sR + rs * kRB + kTM * 16 + rl * 16));
+            mbar_arrive(smem_u32(rempty + rs));
             if (i >= kAS) mbar_wait(smem_u32(aempty + as), ((i / kAS) - 1) & 1);
-            const uint4 wd = lds128(smem_u32(sR + (i % kRR) * kRB + rl * 16));
-            const uint32_t base = smem_u32(sA + as * kAB) + (rl >> 3) * 1024 + (rl & 7) * 128;
-            const int sw = rl & 7;
-            sts128(base + ((0 ^ sw) << 4), expand16(wd.x));
-            sts128(base + ((1 ^ sw) << 4), expand16(wd.x >> 16));
-            sts128(base + ((2 ^ sw) << 4), expand16(wd.y));
-            sts128(base + ((3 ^ sw) << 4), expand16(wd.y >> 16));
-            sts128(base + ((4 ^ sw) << 4), expand16(wd.z));
-            sts128(base + ((5 ^ sw) << 4), expand16(wd.z >> 16));
-            sts128(base + ((6 ^ sw) << 4), expand16(wd.w));
-            sts128(base + ((7 ^ sw) << 4), expand16(wd.w >> 16));
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            // row rl of the A stage = TMEM lane rl: column 8m + i holds the
+            // bytes of bits 4i..4i+3 of word m (K-major, 4 bytes per column)
+            const uint32_t ta = tmem + ((uint32_t)(w * 32) << 16) + kAccCols + as * kACols;
+            tmem_st_word2(ta + 0, w0.x, w0.y);
+            tmem_st_word2(ta + 16, w0.z, w0.w);
+            tmem_st_word2(ta + 32, w1.x, w1.y);
+            tmem_st_word2(ta + 48, w1.z, w1.w);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             mbar_arrive(smem_u32(full + as));
+            if ((rl & 31) == 0) TRACE(1 + (rl >> 5), i);
         }
-        cp_async_wait<0>();
     } else if (w == 8) {
         // ---- MMA issue
         if (lane == 0) {
@@ -653,13 +731,15 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
                 const int buf = seg & 1;
                 if (first && seg >= 2) mbar_wait(smem_u32(accempty + buf), ((seg >> 1) - 1) & 1);
                 const int as = i % kAS, rs = i % kRR;
-                mbar_wait(smem_u32(full + as), (i / kAS) & 1);
+                mbar_wait(smem_u32(full + as), (i / kAS) & 1);  // expanders passed rfull[rs] first
+                TRACE(8, i);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint64_t ad = sdesc_sw128(smem_u32(sA + as * kAB));
+                const uint32_t ta = tmem + kAccCols + as * kACols;
                 const uint64_t bd = sdesc_sw128(smem_u32(sB + rs * kBB));
 #pragma unroll
                 for (int k = 0; k < kTK / 32; ++k)
-                    mma_i8(tmem + buf * NB, ad + 2 * k, bd + 2 * k, idesc, !(first && k == 0));
+                    mma_i8_ts(tmem + (buf * kChains + (k % kChains)) * NB, ta + 8 * k,
+                              bd + (k >> 2) * (NB * 128 >> 4) + 2 * (k & 3), idesc, !first || k >= kChains);
                 mma_commit(smem_u32(aempty + as));
                 mma_commit(smem_u32(rempty + rs));
                 if (last) {
@@ -678,42 +758,69 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
             const int g = s0 + i, m = g / KT;
             const int seglen = min(nsteps - i, KT - g % KT);
             const int buf = seg & 1;
-            mbar_wait(smem_u32(accfull + buf), (seg >> 1) & 1);
+            mbar_wait_idle(smem_u32(accfull + buf), (seg >> 1) & 1, 256);
+            if (e == 0 && lane == 0) TRACE(9, seg);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             int32_t C[NB];
 #pragma unroll
-            for (int c0 = 0; c0 < NB; c0 += 16) {
-                uint32_t v[16];
-                tmem_ld16(tmem + ((uint32_t)(e * 32) << 16) + buf * NB + c0, v);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            for (int j = 0; j < NB; ++j) C[j] = 0;
 #pragma unroll
-                for (int j = 0; j < 16; ++j) C[c0 + j] = (int32_t)v[j];
+            for (int ch = 0; ch < kChains; ++ch) {
+#pragma unroll
+                for (int c0 = 0; c0 < NB; c0 += 16) {
+                    uint32_t v[16];
+                    tmem_ld16(tmem + ((uint32_t)(e * 32) << 16) + (buf * kChains + ch) * NB + c0, v);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) C[c0 + j] += (int32_t)v[j];
+                }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             mbar_arrive(smem_u32(accempty + buf));
             const int r = m * kTM + e * 32 + lane;
-            int32_t *acc = a.cpart + (size_t)r * NB;
+            const int sidx = m - s0 / KT;  // this CTA's segment index (0 or 1)
+            const bool whole = seglen == KT;  // this CTA did the whole tile: no partial sums to merge
+            if (!whole) {
+                // partial sums to this CTA's slab, plain stores; the CTA that
+                // completes the tile's KT steps merges the slabs
+                int4 *dst = reinterpret_cast<int4 *>(a.cpart + (((size_t)blockIdx.x * 2 + sidx) * kTM + e * 32 + lane) * NB);
 #pragma unroll
-            for (int j = 0; j < NB; ++j)
-                if (C[j]) atomicAdd(acc + j, C[j]);
-            __threadfence();
-            epi_bar();
-            if (e == 0 && lane == 0) s_last = atomicAdd(&a.mdone[m], (unsigned)seglen) + seglen == (unsigned)KT;
-            epi_bar();
-            if (s_last && r < a.n) {
+                for (int j = 0; j < NB / 4; ++j) dst[j] = make_int4(C[4 * j], C[4 * j + 1], C[4 * j + 2], C[4 * j + 3]);
                 __threadfence();
-                const int4 *src = reinterpret_cast<const int4 *>(acc);
+                epi_bar();
+                if (e == 0 && lane == 0) s_last = atomicAdd(&a.mdone[m], (unsigned)seglen) + seglen == (unsigned)KT;
+                epi_bar();
+            }
+            if ((whole || s_last) && r < a.n) {
+                if (!whole) {
+                    __threadfence();
+                    // the CTAs whose step ranges meet tile m
+                    const int64_t lo = (int64_t)m * KT, hi = lo + KT;
+                    int b = (int)(lo * gridDim.x / total);
+                    while (b > 0 && (int64_t)b * total / gridDim.x > lo) --b;
+                    while ((int64_t)(b + 1) * total / gridDim.x <= lo) ++b;
+                    for (; b < (int)gridDim.x && (int64_t)b * total / gridDim.x < hi; ++b) {
+                        const int bs0 = (int)((int64_t)b * total / gridDim.x);
+                        const int bs1 = (int)((int64_t)(b + 1) * total / gridDim.x);
+                        if (b == (int)blockIdx.x || bs1 == bs0 || bs1 <= lo) continue;  // self, idle CTAs
+                        const int bsi = m - bs0 / KT;
+                        const int4 *src = reinterpret_cast<const int4 *>(
+                            a.cpart + (((size_t)b * 2 + bsi) * kTM + e * 32 + lane) * NB);
 #pragma unroll
-                for (int j = 0; j < NB / 4; ++j) {
-                    const int4 v = __ldcg(src + j);
-                    C[4 * j] = v.x, C[4 * j + 1] = v.y, C[4 * j + 2] = v.z, C[4 * j + 3] = v.w;
+                        for (int j = 0; j < NB / 4; ++j) {
+                            const int4 v = __ldcg(src + j);
+                            C[4 * j] += v.x, C[4 * j + 1] += v.y, C[4 * j + 2] += v.z, C[4 * j + 3] += v.w;
+                        }
+                    }
                 }
                 const bool rrep = rep && __ldcg(a.len + r) != __ldcg(a.ucnt + r);
                 gemm_epilogue<NB>(a, r, C, rrep);
             }
+            if (e == 0 && lane == 0) TRACE(9, 8 + seg);
             i += seglen;
         }
     }
+    if (t == 0) TRACE(5, 0);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (w == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
@@ -751,13 +858,11 @@ static void carve_bm(Carver &cv, BmWs &w, int64_t n, int k) {
     w.Wp = (int)(np / 32);
     w.Np = (int)np;
     w.nbx = nb_cols(k);
-    // bitmap, counters, flags, X^T and the GEMM accumulators are contiguous:
-    // one memset clears them
+    // bitmap, counters, flags and X^T are contiguous: one memset clears them
     const size_t bmw = (size_t)np * w.Wp;
     const size_t words = (bmw + 2 * (size_t)n + kKMax + (size_t)w.nb + (size_t)(np / kTM) + 4 + 3) & ~size_t(3);
     const size_t xbytes = (size_t)w.nbx * (size_t)np;
-    const size_t cbytes = 4 * (size_t)np * w.nbx;
-    w.clear_bytes = 4 * words + xbytes + cbytes;
+    w.clear_bytes = 4 * words + xbytes;
     unsigned char *base = cv.take<unsigned char>(w.clear_bytes);
     w.bm = reinterpret_cast<unsigned *>(base);
     w.ucnt = w.bm ? w.bm + bmw : nullptr;
@@ -767,7 +872,7 @@ static void carve_bm(Carver &cv, BmWs &w, int64_t n, int k) {
     w.mdone = w.bm ? w.blkdone + w.nb : nullptr;
     w.flags = w.bm ? w.mdone + np / kTM : nullptr;
     w.xt = base ? base + 4 * words : nullptr;
-    w.cacc = base ? reinterpret_cast<int32_t *>(base + 4 * words + xbytes) : nullptr;
+    w.cacc = cv.take<int32_t>((size_t)num_sms() * 2 * kTM * w.nbx);
     w.zacc = cv.take<double>((size_t)n * kKMax);
     w.tab_g = cv.take<double>((size_t)n + 2);
     w.tab_lab = cv.take<signed char>((size_t)n + 16);
@@ -863,4 +968,9 @@ int bitmap_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n
     return launch_gemm<64>(a, rows, cols, st);
 }
 
+#ifdef GEE_TRACE
+extern "C" int gee_trace_dump(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif
 }  // namespace gee

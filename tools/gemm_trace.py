@@ -1,0 +1,26 @@
+"""Per-step timeline of k_bm_gemm CTA 0 (build with -DGEE_TRACE; debug only)."""
+import ctypes
+import numpy as np
+import torch
+import paper_2406_03726_b200 as G
+from paper_2406_03726_b200 import synth, _lib
+
+c = synth.make_config(1)
+dev = torch.device("cuda")
+rows = torch.as_tensor(c["rows"], device=dev)
+cols = torch.as_tensor(c["cols"], device=dev)
+lab = torch.as_tensor(c["labels"], device=dev)
+enc = G.GeeEncoder(c["n"], c["e"], 3, False, G.EmbedOptions(True, True, True))
+for _ in range(5):
+    enc.run(rows, cols, None, lab)
+torch.cuda.synchronize()
+lib = _lib.load()
+buf = (ctypes.c_ulonglong * (10 * 64))()
+assert lib.gee_trace_dump(buf) == 0
+t = np.array(buf, dtype=np.int64).reshape(10, 64)
+t0 = t[7, 0]
+print("start->rep", t[7, 1] - t0, "->setup", t[7, 2] - t0)
+print("step tma  exp0  exp1  exp2  exp3  mma")
+for i in range(48):
+    print(i, *[f"{(t[s, i] - t0) if t[s, i] else -1:>7}" for s in (0, 1, 2, 3, 4, 8)])
+print("epi acc ready", t[9, 0] - t0, t[9, 1] - t0, "epi done", t[9, 8] - t0, t[9, 9] - t0)
