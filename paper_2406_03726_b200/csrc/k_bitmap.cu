@@ -463,6 +463,17 @@ __device__ __forceinline__ void tmem_st_word2(uint32_t taddr, unsigned x, unsign
         : "memory");
 }
 
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+        "elect.sync rx|px, %1;\n\t"
+        "@px mov.s32 %0, 1;\n\t}"
+        : "+r"(pred)
+        : "r"(0xffffffffu));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                  : "memory");
@@ -720,35 +731,35 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
             if ((rl & 31) == 0) TRACE(1 + (rl >> 5), i);
         }
     } else if (w == 8) {
-        // ---- MMA issue
-        if (lane == 0) {
-            const uint32_t idesc = (2u << 4) | ((uint32_t)(NB >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
-            int seg = 0;
+        // ---- MMA issue: the whole warp runs the loop (warp-uniform operands
+        // stay in uniform registers); one elected lane issues
+        const bool leader = elect_one();
+        const uint32_t idesc = (2u << 4) | ((uint32_t)(NB >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+        int seg = 0;
 #pragma unroll 1
-            for (int i = 0; i < nsteps; ++i) {
-                const int ks = (s0 + i) % KT;
-                const bool first = i == 0 || ks == 0, last = i == nsteps - 1 || ks == KT - 1;
-                const int buf = seg & 1;
-                if (first && seg >= 2) mbar_wait(smem_u32(accempty + buf), ((seg >> 1) - 1) & 1);
-                const int as = i % kAS, rs = i % kRR;
-                mbar_wait(smem_u32(full + as), (i / kAS) & 1);  // expanders passed rfull[rs] first
-                TRACE(8, i);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t ta = tmem + kAccCols + as * kACols;
-                const uint64_t bd = sdesc_sw128(smem_u32(sB + rs * kBB));
+        for (int i = 0; i < nsteps; ++i) {
+            const int ks = (s0 + i) % KT;
+            const bool first = i == 0 || ks == 0, last = i == nsteps - 1 || ks == KT - 1;
+            const int buf = seg & 1;
+            if (first && seg >= 2) mbar_wait(smem_u32(accempty + buf), ((seg >> 1) - 1) & 1);
+            const int as = i % kAS, rs = i % kRR;
+            mbar_wait(smem_u32(full + as), (i / kAS) & 1);  // expanders passed rfull[rs] first
+            if (leader) TRACE(8, i);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t ta = tmem + kAccCols + as * kACols;
+            const uint64_t bd = sdesc_sw128(smem_u32(sB + rs * kBB));
+            if (leader) {
 #pragma unroll
                 for (int k = 0; k < kTK / 32; ++k)
                     mma_i8_ts(tmem + (buf * kChains + (k % kChains)) * NB, ta + 8 * k,
                               bd + (k >> 2) * (NB * 128 >> 4) + 2 * (k & 3), idesc, !first || k >= kChains);
                 mma_commit(smem_u32(aempty + as));
                 mma_commit(smem_u32(rempty + rs));
-                if (last) {
-                    mma_commit(smem_u32(accfull + buf));
-                    ++seg;
-                }
+                if (last) mma_commit(smem_u32(accfull + buf));
             }
+            __syncwarp();
+            if (last) ++seg;
         }
-        __syncwarp();
     } else {
         // ---- epilogue: warp 4 + e reads TMEM lanes 32e..32e+31 (= tile rows)
         const int e = w - 4;
@@ -764,16 +775,19 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
             int32_t C[NB];
 #pragma unroll
             for (int j = 0; j < NB; ++j) C[j] = 0;
+            {
+                uint32_t v[kChains][NB];
 #pragma unroll
-            for (int ch = 0; ch < kChains; ++ch) {
+                for (int ch = 0; ch < kChains; ++ch)
 #pragma unroll
-                for (int c0 = 0; c0 < NB; c0 += 16) {
-                    uint32_t v[16];
-                    tmem_ld16(tmem + ((uint32_t)(e * 32) << 16) + (buf * kChains + ch) * NB + c0, v);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    for (int c0 = 0; c0 < NB; c0 += 16)
+                        tmem_ld16(tmem + ((uint32_t)(e * 32) << 16) + (buf * kChains + ch) * NB + c0,
+                                  *reinterpret_cast<uint32_t(*)[16]>(&v[ch][c0]));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) C[c0 + j] += (int32_t)v[j];
-                }
+                for (int ch = 0; ch < kChains; ++ch)
+#pragma unroll
+                    for (int j = 0; j < NB; ++j) C[j] += (int32_t)v[ch][j];
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             mbar_arrive(smem_u32(accempty + buf));
