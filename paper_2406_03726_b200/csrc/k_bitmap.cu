@@ -513,7 +513,8 @@ __device__ __forceinline__ double pow2i(int e) {
 // recombined, or the rare path's f64 sums of g), then 1/n_q, diagonal, s_r,
 // correlation
 template <int NB>
-__device__ __forceinline__ void gemm_epilogue(const BmArgs &a, int r, const int32_t (&C)[NB], bool rep) {
+__device__ __forceinline__ void gemm_epilogue(const BmArgs &a, int r, const int32_t (&C)[NB], bool rep,
+                                              const double (&inv)[kKMax], double sr, int lab) {
     double acc[kKMax];
     const bool lap = (a.flags_opts & GEE_LAPLACIAN) != 0;
     if (rep) {
@@ -526,18 +527,16 @@ __device__ __forceinline__ void gemm_epilogue(const BmArgs &a, int r, const int3
             if (q * kDig + kDig <= NB && q < a.k) {
 #pragma unroll
                 for (int d = 0; d < kDig; ++d) v += (double)C[q * kDig + d] * pow2i(8 * d - 55);
-                v *= __ldcg(a.inv + q);
+                v *= inv[q];
             }
             acc[q] = v;
         }
     }
-    const double sr = lap ? __ldcg(a.scale + r) : 1.0;
     if (a.flags_opts & GEE_DIAGONAL) {
         // A+I: the diagonal gains 1.0 whether or not (r, r) is stored
-        const int lab = a.y32[r];
 #pragma unroll
         for (int q = 0; q < kKMax; ++q)
-            if (q == lab) acc[q] += sr * __ldcg(a.inv + q);
+            if (q == lab) acc[q] += sr * inv[q];
     }
     if (lap) {
 #pragma unroll
@@ -594,6 +593,7 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: 
 
 #ifdef GEE_TRACE
 __device__ unsigned long long g_trace[10][64];
+__device__ unsigned long long g_trace_end[160];
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long v;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
@@ -610,17 +610,19 @@ __device__ __forceinline__ unsigned long long gtime() {
 #endif
 
 // k_bm_gemm geometry
-constexpr int kAS = 4;          // expanded A stages in TMEM (64 columns = 128 rows x 256 bytes each)
-constexpr int kACols = kTK / 4;  // TMEM columns per A stage (4 bytes per column)
+constexpr int kACols = kTK / 4;  // TMEM columns per A stage (128 rows x 256 bytes, 4 bytes per column)
 template <int NB>
-constexpr int rr_stages() { return NB == 64 ? 6 : 8; }  // bulk-copied stages: 4 KB bitmap + the B tile
+constexpr int rr_stages() { return NB == 64 ? 9 : 16; }  // bulk-copied stages: 4 KB bitmap + the B tile
 template <int NB>
-constexpr int chains() { return NB == 64 ? 2 : 4; }     // independent accumulators per buffer
+constexpr int chains() { return 2; }                    // independent accumulators per buffer
+template <int NB>
+constexpr int a_stages() { return (512 - 4 * NB) / kACols; }  // TMEM A stages after 2 x 2 accumulators
 constexpr int kGemmNT = 320;    // warps 0-3 expand, 4-7 epilogue, 8 MMA, 9 bulk copies
 
 template <int NB>
 constexpr size_t gemm_smem() {
-    return 1024 + (size_t)rr_stages<NB>() * (kTM * 32 + NB * kTK) + 8 * (2 * kAS + 2 * rr_stages<NB>() + 4) + 16;
+    return 1024 + (size_t)rr_stages<NB>() * (kTM * 32 + NB * kTK) + 8 * (2 * a_stages<NB>() + 2 * rr_stages<NB>() + 4) +
+           16;
 }
 
 // Stream-K over the flattened (row tile, K step) space: CTA b takes steps
@@ -639,6 +641,7 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
     constexpr int kRB = kTM * 32;    // 4 KB: two consecutive 2 KB bitmap tiles
     constexpr int kBB = NB * kTK;    // two consecutive X^T tiles
     constexpr int kChains = chains<NB>();
+    constexpr int kAS = a_stages<NB>();
     constexpr int kAccCols = 2 * kChains * NB;  // two accumulator buffers, then the A stages
     constexpr int kTmemCols = 512;
     static_assert(kAccCols + kAS * kACols <= kTmemCols, "TMEM budget");
@@ -763,12 +766,20 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
     } else {
         // ---- epilogue: warp 4 + e reads TMEM lanes 32e..32e+31 (= tile rows)
         const int e = w - 4;
+        double inv[kKMax];
+#pragma unroll
+        for (int q = 0; q < kKMax; ++q) inv[q] = q < a.k ? __ldcg(a.inv + q) : 0.0;
+        const bool lap = (a.flags_opts & GEE_LAPLACIAN) != 0;
         int seg = 0;
 #pragma unroll 1
         for (int i = 0; i < nsteps; ++seg) {
             const int g = s0 + i, m = g / KT;
             const int seglen = min(nsteps - i, KT - g % KT);
             const int buf = seg & 1;
+            const int r = m * kTM + e * 32 + lane;
+            // the row's epilogue inputs, loaded while the MMAs run
+            const int rlab = r < a.n ? __ldcg(a.y32 + r) : -1;
+            const double rsc = (lap && r < a.n) ? __ldcg(a.scale + r) : 1.0;
             mbar_wait_idle(smem_u32(accfull + buf), (seg >> 1) & 1, 256);
             if (e == 0 && lane == 0) TRACE(9, seg);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -789,9 +800,9 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
 #pragma unroll
                     for (int j = 0; j < NB; ++j) C[j] += (int32_t)v[ch][j];
             }
+            if (e == 0 && lane == 0) TRACE(9, 16 + 8 * seg);
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             mbar_arrive(smem_u32(accempty + buf));
-            const int r = m * kTM + e * 32 + lane;
             const int sidx = m - s0 / KT;  // this CTA's segment index (0 or 1)
             const bool whole = seglen == KT;  // this CTA did the whole tile: no partial sums to merge
             if (!whole) {
@@ -801,23 +812,25 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
 #pragma unroll
                 for (int j = 0; j < NB / 4; ++j) dst[j] = make_int4(C[4 * j], C[4 * j + 1], C[4 * j + 2], C[4 * j + 3]);
                 __threadfence();
+                if (e == 0 && lane == 0) TRACE(9, 17 + 8 * seg);
                 epi_bar();
                 if (e == 0 && lane == 0) s_last = atomicAdd(&a.mdone[m], (unsigned)seglen) + seglen == (unsigned)KT;
                 epi_bar();
+                if (e == 0 && lane == 0) TRACE(9, 18 + 8 * seg);
             }
             if ((whole || s_last) && r < a.n) {
                 if (!whole) {
                     __threadfence();
-                    // the CTAs whose step ranges meet tile m
-                    const int64_t lo = (int64_t)m * KT, hi = lo + KT;
-                    int b = (int)(lo * gridDim.x / total);
-                    while (b > 0 && (int64_t)b * total / gridDim.x > lo) --b;
-                    while ((int64_t)(b + 1) * total / gridDim.x <= lo) ++b;
-                    for (; b < (int)gridDim.x && (int64_t)b * total / gridDim.x < hi; ++b) {
-                        const int bs0 = (int)((int64_t)b * total / gridDim.x);
-                        const int bs1 = (int)((int64_t)(b + 1) * total / gridDim.x);
-                        if (b == (int)blockIdx.x || bs1 == bs0 || bs1 <= lo) continue;  // self, idle CTAs
-                        const int bsi = m - bs0 / KT;
+                    // the CTAs whose step ranges meet tile m (32-bit: T <= 128 * 64)
+                    const unsigned G = gridDim.x, T = (unsigned)total;
+                    const unsigned lo = (unsigned)m * KT, hi = lo + KT;
+                    unsigned b = lo * G / T;
+                    while (b > 0 && b * T / G > lo) --b;
+                    while ((b + 1) * T / G <= lo) ++b;
+                    for (; b < G && b * T / G < hi; ++b) {
+                        const unsigned bs0 = b * T / G, bs1 = (b + 1) * T / G;
+                        if (b == blockIdx.x || bs1 == bs0 || bs1 <= lo) continue;  // self, idle CTAs
+                        const int bsi = m - (int)(bs0 / KT);
                         const int4 *src = reinterpret_cast<const int4 *>(
                             a.cpart + (((size_t)b * 2 + bsi) * kTM + e * 32 + lane) * NB);
 #pragma unroll
@@ -827,14 +840,19 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
                         }
                     }
                 }
+                if (e == 0 && lane == 0) TRACE(9, 19 + 8 * seg);
                 const bool rrep = rep && __ldcg(a.len + r) != __ldcg(a.ucnt + r);
-                gemm_epilogue<NB>(a, r, C, rrep);
+                gemm_epilogue<NB>(a, r, C, rrep, inv, rsc, rlab);
+                if (e == 0 && lane == 0) TRACE(9, 20 + 8 * seg);
             }
             if (e == 0 && lane == 0) TRACE(9, 8 + seg);
             i += seglen;
         }
     }
     if (t == 0) TRACE(5, 0);
+#ifdef GEE_TRACE
+    if (t == 128) g_trace_end[blockIdx.x] = gtime();
+#endif
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (w == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
@@ -984,7 +1002,10 @@ int bitmap_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n
 
 #ifdef GEE_TRACE
 extern "C" int gee_trace_dump(unsigned long long *out) {
-    return cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)) == cudaSuccess ? 0 : -1;
+    return cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)) == cudaSuccess &&
+                   cudaMemcpyFromSymbol(out + 640, g_trace_end, sizeof(g_trace_end)) == cudaSuccess
+               ? 0
+               : -1;
 }
 #endif
 }  // namespace gee

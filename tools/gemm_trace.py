@@ -15,12 +15,17 @@ for _ in range(5):
     enc.run(rows, cols, None, lab)
 torch.cuda.synchronize()
 lib = _lib.load()
-buf = (ctypes.c_ulonglong * (10 * 64))()
+buf = (ctypes.c_ulonglong * (10 * 64 + 160))()
 assert lib.gee_trace_dump(buf) == 0
-t = np.array(buf, dtype=np.int64).reshape(10, 64)
+arr = np.array(buf, dtype=np.int64); t = arr[:640].reshape(10, 64); ends = arr[640:640 + 148]
 t0 = t[7, 0]
 print("start->rep", t[7, 1] - t0, "->setup", t[7, 2] - t0)
 print("step tma  exp0  exp1  exp2  exp3  mma")
 for i in range(48):
     print(i, *[f"{(t[s, i] - t0) if t[s, i] else -1:>7}" for s in (0, 1, 2, 3, 4, 8)])
 print("epi acc ready", t[9, 0] - t0, t[9, 1] - t0, "epi done", t[9, 8] - t0, t[9, 9] - t0)
+for seg in range(3):
+    print("seg", seg, "tmem", t[9, 16 + 8 * seg] - t0, "store+fence", t[9, 17 + 8 * seg] - t0, "atomic", t[9, 18 + 8 * seg] - t0,
+          "merged", t[9, 19 + 8 * seg] - t0, "z", t[9, 20 + 8 * seg] - t0)
+# a finishing CTA: look at CTA traces only for CTA 0
+print("cta end: min", (ends.min() - t0), "max", (ends.max() - t0), "argmax", ends.argmax())
