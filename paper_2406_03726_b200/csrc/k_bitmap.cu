@@ -124,6 +124,21 @@ __device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
     return x;
 }
 
+// NQ independent 32 x 32 transposes, stage-major
+template <int NQ>
+__device__ __forceinline__ void transpose32_n(unsigned (&x)[NQ], int lane) {
+#pragma unroll
+    for (int J = 16; J >= 1; J >>= 1) {
+        const unsigned M = J == 16 ? 0x0000ffffu : J == 8 ? 0x00ff00ffu : J == 4 ? 0x0f0f0f0fu : J == 2 ? 0x33333333u : 0x55555555u;
+        unsigned y[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) y[q] = __shfl_xor_sync(0xffffffffu, x[q], J);
+        const bool hi = (lane & J) != 0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) x[q] = hi ? ((x[q] & ~M) | ((y[q] >> J) & M)) : ((x[q] & M) | ((y[q] & M) << J));
+    }
+}
+
 // node-table entry of row r from its stream length L (k_bm_sym / k_bm_scan /
 // the rare path); y32 and the histogram are complete when this runs
 __device__ __forceinline__ void node_entry(const BmArgs &a, int r, unsigned L) {
@@ -248,16 +263,30 @@ __global__ void __launch_bounds__(kBlk) k_bm_sym(BmArgs a) {
     }
     // tile (w, q) of a block transposes into row q*32+lane, word w of its mirror
     unsigned pu = 0;  // popc of the U words read here (each U word is read once)
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        pu += __popc(av[q]);
-        sat[q * 32 + lane][w] = transpose32(av[q], lane);
-    }
-    if (!same) {
+    // 8 (or 16) independent transposes, stage-major so the shuffles overlap
+    if (same) {
+        unsigned x[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            pu += __popc(bv[q]);
-            sbt[q * 32 + lane][w] = transpose32(bv[q], lane);
+            pu += __popc(av[q]);
+            x[q] = av[q];
+        }
+        transpose32_n<8>(x, lane);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sat[q * 32 + lane][w] = x[q];
+    } else {
+        unsigned x[16];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            pu += __popc(av[q]) + __popc(bv[q]);
+            x[q] = av[q];
+            x[8 + q] = bv[q];
+        }
+        transpose32_n<16>(x, lane);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            sat[q * 32 + lane][w] = x[q];
+            sbt[q * 32 + lane][w] = x[8 + q];
         }
     }
     pu = warp_sum_u(pu);
