@@ -62,7 +62,7 @@ struct BmArgs {
     unsigned *cnt;            // [kKMax] class histogram
     unsigned *blkdone;        // [nb] finished block pairs per 256-row block
     unsigned *mdone;          // [Np/128] K steps accumulated per GEMM row tile
-    unsigned *flags;          // [0] pair in both directions, [1] grid barrier, [2] popc(U)
+    unsigned *flags;          // [0] pair in both directions, [1] rare-path barrier, [2] popc(U), [3] table barrier
     unsigned char *xt;        // [NB][Np] X^T digits (K-major B operand)
     int nbx;                  // NB: X columns (kDig * K padded to 16/32/64)
     int32_t *cpart;           // [grid][2][128][NB] stream-K partial sums (slab per CTA segment)
@@ -238,7 +238,6 @@ __global__ void __launch_bounds__(kSetThreads) k_bm_set(const int64_t *__restric
 __global__ void __launch_bounds__(kBlk) k_bm_sym(BmArgs a) {
     __shared__ unsigned sat[kBlk][9], sbt[kBlk][9];
     __shared__ unsigned red[kBlk / 32];
-    __shared__ bool fin[2];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     // linear index -> (BI, BJ) on the upper triangle
     const unsigned x = blockIdx.x;
@@ -331,26 +330,13 @@ __global__ void __launch_bounds__(kBlk) k_bm_sym(BmArgs a) {
     // rows >= n are padding and stay empty
     if (ca) atomicAdd(&a.ucnt[ra], ca);
     if (cb) atomicAdd(&a.ucnt[rb], cb);
-    __threadfence();
     if (__syncthreads_or(mut != 0) && t == 0) a.flags[0] = 1u;
-    if (t == 0) {
-        fin[0] = atomicAdd(&a.blkdone[bi], 1u) == (unsigned)a.nb - 1;
-        fin[1] = !same && atomicAdd(&a.blkdone[bj], 1u) == (unsigned)a.nb - 1;
-    }
-    __syncthreads();
-    if (!fin[0] && !fin[1]) return;
-    __threadfence();
-    // this CTA completed a 256-row block: its node table entries
-    if (fin[0] && ra < a.n) node_entry(a, ra, __ldcg(a.ucnt + ra));
-    if (fin[1] && rb < a.n) node_entry(a, rb, __ldcg(a.ucnt + rb));
-    if (fin[0] && bi == 0) write_counts(a, t);
 }
 
 // directed lists: one warp per row, 8 rows per CTA
 __global__ void __launch_bounds__(256) k_bm_scan(BmArgs a) {
     const int lane = threadIdx.x & 31;
     const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (blockIdx.x == 0) write_counts(a, threadIdx.x);
     if (r >= a.n) return;
     unsigned u = 0;
     for (int i = lane; i < a.Wp / 4; i += 32) {
@@ -361,7 +347,6 @@ __global__ void __launch_bounds__(256) k_bm_scan(BmArgs a) {
     if (lane == 0) {
         a.ucnt[r] = u;
         if (u) atomicAdd(a.flags + 2, u);  // popc(U): S = U for directed lists
-        node_entry(a, r, u);
     }
 }
 
@@ -393,6 +378,7 @@ __device__ void repeat_phases(const int64_t *__restrict__ rows, const int64_t *_
     grid_barrier(a.flags + 1, gridDim.x);
     // 2: node table from the stream lengths
     for (int64_t r = tid; r < a.n; r += nth) node_entry(a, (int)r, __ldcg(a.len + r));
+    asm volatile("fence.proxy.async.global;" ::: "memory");
     grid_barrier(a.flags + 1, 2 * gridDim.x);
     // 3: per-class sums of g over every stream entry of rows with repeats
     for (int64_t e = tid; e < a.E; e += nth) {
@@ -689,6 +675,14 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     if (t == 0) TRACE(7, 0);
     const bool rep = __ldcg(a.flags) != 0 || (int64_t)__ldcg(a.flags + 2) != a.E;
+    {
+        // node table from the distinct counts: d_r, s_r, X^T digits, g_r
+        const int64_t tid = (int64_t)blockIdx.x * blockDim.x + t, nth = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t r = tid; r < a.n; r += nth) node_entry(a, (int)r, __ldcg(a.ucnt + r));
+        if (blockIdx.x == 0) write_counts(a, t);
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // X^T is read by bulk copies
+        grid_barrier(a.flags + 3, gridDim.x);
+    }
     if (rep) repeat_phases(rows, cols, a);
     if (t == 0) TRACE(7, 1);
 
