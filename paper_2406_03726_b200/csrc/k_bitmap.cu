@@ -48,6 +48,7 @@ constexpr int kBmMax = 16384;   // nodes: bitmap Np^2/8 <= 32 MB (L2-resident)
 constexpr int kBlk = 256;       // rows / columns of a k_bm_sym block
 constexpr int kSetThreads = 512;
 constexpr int kKMax = 8;        // classes
+constexpr int kPopParts = 64;   // spread counters for popc(U)
 constexpr int kDig = 7;         // base-256 digits of s * 2^55
 constexpr int kTM = 128;        // GEMM rows per tile (TMEM lanes)
 constexpr int kTK = 256;        // GEMM columns per K step (two 128-byte swizzle atoms)
@@ -62,7 +63,8 @@ struct BmArgs {
     unsigned *cnt;            // [kKMax] class histogram
     unsigned *blkdone;        // [nb] finished block pairs per 256-row block
     unsigned *mdone;          // [Np/128] K steps accumulated per GEMM row tile
-    unsigned *flags;          // [0] pair in both directions, [1] rare-path barrier, [2] popc(U), [3] table barrier
+    unsigned *flags;          // [0] pair in both directions, [1] rare-path barrier, [3] table barrier
+    unsigned *upop;           // [kPopParts * 32] popc(U) partial sums, 128 B apart
     unsigned char *xt;        // [NB][Np] X^T digits (K-major B operand)
     int nbx;                  // NB: X columns (kDig * K padded to 16/32/64)
     int32_t *cpart;           // [grid][2][128][NB] stream-K partial sums (slab per CTA segment)
@@ -234,102 +236,73 @@ __global__ void __launch_bounds__(kSetThreads) k_bm_set(const int64_t *__restric
     }
 }
 
-// S = U | U^T for the block pair (BI, BJ), BI <= BJ, in place
-__global__ void __launch_bounds__(kBlk) k_bm_sym(BmArgs a) {
-    __shared__ unsigned sat[kBlk][9], sbt[kBlk][9];
-    __shared__ unsigned red[kBlk / 32];
+// S = U | U^T for the block pair (BI, BJ), BI <= BJ, in place.  Blocks are
+// the bitmap's 128 x 128-bit tiles, so each side is one contiguous 2 KB tile
+// (thread t = tile row t, one 16-byte load and store per side).
+constexpr int kSB = 128;
+__global__ void __launch_bounds__(kSB) k_bm_sym(BmArgs a) {
+    constexpr int kW = kSB / 32;  // words per tile row
+    __shared__ unsigned sat[kSB][kW + 1], sbt[kSB][kW + 1];
+    __shared__ unsigned red[kSB / 32];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     // linear index -> (BI, BJ) on the upper triangle
     const unsigned x = blockIdx.x;
-    unsigned bj = (unsigned)((sqrt(8.0 * x + 1.0) - 1.0) * 0.5);
+    unsigned bj = (unsigned)((sqrtf(8.0f * x + 1.0f) - 1.0f) * 0.5f);
     while ((bj + 1) * (bj + 2) / 2 <= x) ++bj;
     while (bj * (bj + 1) / 2 > x) --bj;
     const unsigned bi = x - bj * (bj + 1) / 2;
-    const int ra = bi * kBlk + t, rb = bj * kBlk + t;
-    uint4 *pa0 = reinterpret_cast<uint4 *>(a.bm + bm_index(a, ra, bj * 8));
-    uint4 *pa1 = reinterpret_cast<uint4 *>(a.bm + bm_index(a, ra, bj * 8 + 4));
-    uint4 *pb0 = reinterpret_cast<uint4 *>(a.bm + bm_index(a, rb, bi * 8));
-    uint4 *pb1 = reinterpret_cast<uint4 *>(a.bm + bm_index(a, rb, bi * 8 + 4));
-    unsigned av[8], bv[8];
-    {
-        const uint4 a0 = __ldcg(pa0), a1 = __ldcg(pa1);
-        av[0] = a0.x, av[1] = a0.y, av[2] = a0.z, av[3] = a0.w, av[4] = a1.x, av[5] = a1.y, av[6] = a1.z, av[7] = a1.w;
-    }
+    const int ra = bi * kSB + t, rb = bj * kSB + t;
+    uint4 *pa = reinterpret_cast<uint4 *>(a.bm + bm_index(a, ra, bj * kW));
+    uint4 *pb = reinterpret_cast<uint4 *>(a.bm + bm_index(a, rb, bi * kW));
     const bool same = bi == bj;
-    if (!same) {
-        const uint4 b0 = __ldcg(pb0), b1 = __ldcg(pb1);
-        bv[0] = b0.x, bv[1] = b0.y, bv[2] = b0.z, bv[3] = b0.w, bv[4] = b1.x, bv[5] = b1.y, bv[6] = b1.z, bv[7] = b1.w;
-    }
-    // tile (w, q) of a block transposes into row q*32+lane, word w of its mirror
+    const uint4 av4 = __ldcg(pa);
+    const uint4 bv4 = same ? av4 : __ldcg(pb);
+    unsigned av[kW] = {av4.x, av4.y, av4.z, av4.w}, bv[kW] = {bv4.x, bv4.y, bv4.z, bv4.w};
+    // sub-tile (w, q) transposes into row q*32+lane, word w of its mirror;
+    // 8 independent transposes, stage-major so the shuffles overlap
     unsigned pu = 0;  // popc of the U words read here (each U word is read once)
-    // 8 (or 16) independent transposes, stage-major so the shuffles overlap
-    if (same) {
-        unsigned x[8];
+    {
+        unsigned xx[2 * kW];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            pu += __popc(av[q]);
-            x[q] = av[q];
+        for (int q = 0; q < kW; ++q) {
+            pu += __popc(av[q]) + (same ? 0u : __popc(bv[q]));
+            xx[q] = av[q];
+            xx[kW + q] = bv[q];
         }
-        transpose32_n<8>(x, lane);
+        transpose32_n<2 * kW>(xx, lane);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) sat[q * 32 + lane][w] = x[q];
-    } else {
-        unsigned x[16];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            pu += __popc(av[q]) + __popc(bv[q]);
-            x[q] = av[q];
-            x[8 + q] = bv[q];
-        }
-        transpose32_n<16>(x, lane);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            sat[q * 32 + lane][w] = x[q];
-            sbt[q * 32 + lane][w] = x[8 + q];
+        for (int q = 0; q < kW; ++q) {
+            sat[q * 32 + lane][w] = xx[q];
+            sbt[q * 32 + lane][w] = xx[kW + q];
         }
     }
     pu = warp_sum_u(pu);
     if (lane == 0) red[w] = pu;
     __syncthreads();
     unsigned mut = 0, ca = 0, cb = 0;
-    if (same) {
-        unsigned s[8];
+    unsigned sv[kW], uv[kW];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const unsigned tq = sat[t][q];
-            s[q] = av[q] | tq;
-            unsigned m = av[q] & tq;
-            if (q == w) m &= ~(1u << lane);  // the diagonal is its own mirror
-            mut |= m;
-            ca += __popc(s[q]);
-        }
-        *pa0 = make_uint4(s[0], s[1], s[2], s[3]);
-        *pa1 = make_uint4(s[4], s[5], s[6], s[7]);
-    } else {
-        unsigned s[8], u[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const unsigned tb = sbt[t][q], ta = sat[t][q];
-            s[q] = av[q] | tb;
-            u[q] = bv[q] | ta;
-            mut |= av[q] & tb;
-            ca += __popc(s[q]);
-            cb += __popc(u[q]);
-        }
-        *pa0 = make_uint4(s[0], s[1], s[2], s[3]);
-        *pa1 = make_uint4(s[4], s[5], s[6], s[7]);
-        *pb0 = make_uint4(u[0], u[1], u[2], u[3]);
-        *pb1 = make_uint4(u[4], u[5], u[6], u[7]);
+    for (int q = 0; q < kW; ++q) {
+        const unsigned tb = sbt[t][q], ta = sat[t][q];
+        sv[q] = av[q] | tb;
+        uv[q] = bv[q] | ta;
+        unsigned m = av[q] & tb;
+        if (same && q == w) m &= ~(1u << lane);  // the diagonal is its own mirror
+        mut |= m;
+        ca += __popc(sv[q]);
+        cb += __popc(uv[q]);
     }
+    *pa = make_uint4(sv[0], sv[1], sv[2], sv[3]);
+    if (!same) *pb = make_uint4(uv[0], uv[1], uv[2], uv[3]);
     if (t == 0) {
         unsigned tot = 0;
 #pragma unroll
-        for (int i = 0; i < kBlk / 32; ++i) tot += red[i];
-        if (tot) atomicAdd(a.flags + 2, tot);
+        for (int i = 0; i < kSB / 32; ++i) tot += red[i];
+        if (tot) atomicAdd(a.upop + (blockIdx.x % kPopParts) * 32, tot);  // spread: one address serialises
     }
     // rows >= n are padding and stay empty
     if (ca) atomicAdd(&a.ucnt[ra], ca);
-    if (cb) atomicAdd(&a.ucnt[rb], cb);
+    if (cb && !same) atomicAdd(&a.ucnt[rb], cb);
     if (__syncthreads_or(mut != 0) && t == 0) a.flags[0] = 1u;
 }
 
@@ -346,7 +319,7 @@ __global__ void __launch_bounds__(256) k_bm_scan(BmArgs a) {
     u = warp_sum_u(u);
     if (lane == 0) {
         a.ucnt[r] = u;
-        if (u) atomicAdd(a.flags + 2, u);  // popc(U): S = U for directed lists
+        if (u) atomicAdd(a.upop + (blockIdx.x % kPopParts) * 32, u);  // popc(U): S = U for directed lists
     }
 }
 
@@ -674,7 +647,20 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
 
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     if (t == 0) TRACE(7, 0);
-    const bool rep = __ldcg(a.flags) != 0 || (int64_t)__ldcg(a.flags + 2) != a.E;
+    bool rep;
+    {
+        // popc(U) = E exactly when no pair repeats in the list
+        __shared__ unsigned s_rep;
+        if (t < 32) {
+            unsigned long long tot = 0;
+            for (int i = t; i < kPopParts; i += 32) tot += __ldcg(a.upop + i * 32);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+            if (t == 0) s_rep = __ldcg(a.flags) != 0 || (int64_t)tot != a.E;
+        }
+        __syncthreads();
+        rep = s_rep != 0;
+    }
     {
         // node table from the distinct counts: d_r, s_r, X^T digits, g_r
         const int64_t tid = (int64_t)blockIdx.x * blockDim.x + t, nth = (int64_t)gridDim.x * blockDim.x;
@@ -898,7 +884,7 @@ static int nb_cols(int k) {
 }
 
 struct BmWs {
-    unsigned *bm, *ucnt, *len, *cnt, *blkdone, *mdone, *flags;
+    unsigned *bm, *ucnt, *len, *cnt, *blkdone, *mdone, *flags, *upop;
     unsigned char *xt;
     int32_t *cacc;
     double *zacc, *tab_g;
@@ -915,7 +901,8 @@ static void carve_bm(Carver &cv, BmWs &w, int64_t n, int k) {
     w.nbx = nb_cols(k);
     // bitmap, counters, flags and X^T are contiguous: one memset clears them
     const size_t bmw = (size_t)np * w.Wp;
-    const size_t words = (bmw + 2 * (size_t)n + kKMax + (size_t)w.nb + (size_t)(np / kTM) + 4 + 3) & ~size_t(3);
+    const size_t words =
+        (bmw + 2 * (size_t)n + kKMax + (size_t)w.nb + (size_t)(np / kTM) + 4 + 32 * kPopParts + 3) & ~size_t(3);
     const size_t xbytes = (size_t)w.nbx * (size_t)np;
     w.clear_bytes = 4 * words + xbytes;
     unsigned char *base = cv.take<unsigned char>(w.clear_bytes);
@@ -926,6 +913,7 @@ static void carve_bm(Carver &cv, BmWs &w, int64_t n, int k) {
     w.blkdone = w.bm ? w.cnt + kKMax : nullptr;
     w.mdone = w.bm ? w.blkdone + w.nb : nullptr;
     w.flags = w.bm ? w.mdone + np / kTM : nullptr;
+    w.upop = w.bm ? w.flags + 4 : nullptr;
     w.xt = base ? base + 4 * words : nullptr;
     w.cacc = cv.take<int32_t>((size_t)num_sms() * 2 * kTM * w.nbx);
     w.zacc = cv.take<double>((size_t)n * kKMax);
@@ -992,6 +980,7 @@ int bitmap_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n
     a.blkdone = W.blkdone;
     a.mdone = W.mdone;
     a.flags = W.flags;
+    a.upop = W.upop;
     a.xt = W.xt;
     a.nbx = W.nbx;
     a.cpart = W.cacc;
@@ -1012,7 +1001,8 @@ int bitmap_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n
     k_bm_set<<<(unsigned)num_sms() * 4, kSetThreads, 0, st>>>(rows, cols, a);
     GEE_CHECK_LAUNCH("k_bm_set");
     if (!directed) {
-        k_bm_sym<<<(unsigned)(W.nb * (W.nb + 1) / 2), kBlk, 0, st>>>(a);
+        const unsigned nt = (unsigned)(W.Np / kSB);
+        k_bm_sym<<<nt * (nt + 1) / 2, kSB, 0, st>>>(a);
         GEE_CHECK_LAUNCH("k_bm_sym");
     } else {
         k_bm_scan<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(a);
