@@ -218,7 +218,8 @@ def kernel_bytes(c, m_stream, nnz, wbytes):
         # HBM stream; the Np x Np adjacency bitmap (Np = n rounded up to 256)
         # lives in L2 and is counted once per pass over it
         "k_bm_set": 16 * e + 8 * n,
-        "k_bm_sym": 2 * bm + 4 * n + 9 * n + (16 * n if lap else 0),
+        "k_bm_sym": 2 * bm + 4 * n,
+        "k_bm_table": 4 * n + 4 * n + 9 * n + 7 * n + (16 * n if lap else 0),
         "k_bm_scan": bm + 4 * n + 9 * n + (16 * n if lap else 0),
         "k_bm_gemm": bm + nbx * np_ + 8 * n * k + 4 * n + (8 * n if lap else 0),
         # radix-sort path

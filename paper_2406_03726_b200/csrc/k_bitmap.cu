@@ -82,6 +82,13 @@ struct BmArgs {
     int32_t *err;
 };
 
+// programmatic dependent launch: a kernel launched with the PDL attribute
+// may start while its predecessor drains; it waits here before touching the
+// predecessor's outputs, and the predecessor lets it launch once its CTAs
+// have written everything
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned lanemask_le() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
@@ -234,6 +241,7 @@ __global__ void __launch_bounds__(kSetThreads) k_bm_set(const int64_t *__restric
             if (tail && key[u] != 0xffffffffu) atomicOr(&a.bm[key[u]], incl);
         }
     }
+    pdl_trigger();
 }
 
 // S = U | U^T for the block pair (BI, BJ), BI <= BJ, in place.  Blocks are
@@ -248,6 +256,7 @@ __global__ void __launch_bounds__(kSB) k_bm_sym(BmArgs a) {
     // linear index -> (BI, BJ) on the upper triangle
     const unsigned x = blockIdx.x;
     unsigned bj = (unsigned)((sqrtf(8.0f * x + 1.0f) - 1.0f) * 0.5f);
+    pdl_wait();
     while ((bj + 1) * (bj + 2) / 2 <= x) ++bj;
     while (bj * (bj + 1) / 2 > x) --bj;
     const unsigned bi = x - bj * (bj + 1) / 2;
@@ -304,12 +313,24 @@ __global__ void __launch_bounds__(kSB) k_bm_sym(BmArgs a) {
     if (ca) atomicAdd(&a.ucnt[ra], ca);
     if (cb && !same) atomicAdd(&a.ucnt[rb], cb);
     if (__syncthreads_or(mut != 0) && t == 0) a.flags[0] = 1u;
+    pdl_trigger();
+}
+
+// node table from the distinct counts: d_r, s_r, X^T digits, g_r (thread per row)
+__global__ void __launch_bounds__(256) k_bm_table(BmArgs a) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    pdl_wait();
+    if (blockIdx.x == 0) write_counts(a, threadIdx.x);
+    if (r < a.n) node_entry(a, r, __ldcg(a.ucnt + r));
+    __syncthreads();
+    pdl_trigger();
 }
 
 // directed lists: one warp per row, 8 rows per CTA
 __global__ void __launch_bounds__(256) k_bm_scan(BmArgs a) {
     const int lane = threadIdx.x & 31;
     const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+    pdl_wait();
     if (r >= a.n) return;
     unsigned u = 0;
     for (int i = lane; i < a.Wp / 4; i += 32) {
@@ -647,6 +668,7 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
 
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     if (t == 0) TRACE(7, 0);
+    pdl_wait();
     bool rep;
     {
         // popc(U) = E exactly when no pair repeats in the list
@@ -660,14 +682,6 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
         }
         __syncthreads();
         rep = s_rep != 0;
-    }
-    {
-        // node table from the distinct counts: d_r, s_r, X^T digits, g_r
-        const int64_t tid = (int64_t)blockIdx.x * blockDim.x + t, nth = (int64_t)gridDim.x * blockDim.x;
-        for (int64_t r = tid; r < a.n; r += nth) node_entry(a, (int)r, __ldcg(a.ucnt + r));
-        if (blockIdx.x == 0) write_counts(a, t);
-        asm volatile("fence.proxy.async.global;" ::: "memory");  // X^T is read by bulk copies
-        grid_barrier(a.flags + 3, gridDim.x);
     }
     if (rep) repeat_phases(rows, cols, a);
     if (t == 0) TRACE(7, 1);
@@ -930,6 +944,31 @@ size_t bitmap_workspace(int64_t E, int64_t n, int directed, int k) {
     return cv.bytes();
 }
 
+// launch with the programmatic-dependent-launch attribute (and optionally
+// cooperative); its kernel calls pdl_wait() before reading its inputs
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              bool coop, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+    if (coop) {
+        at[na].id = cudaLaunchAttributeCooperative;
+        at[na].val.cooperative = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int NB>
 static int launch_gemm(const BmArgs &a, const int64_t *rows, const int64_t *cols, cudaStream_t st) {
     static bool attr = false;
@@ -940,17 +979,8 @@ static int launch_gemm(const BmArgs &a, const int64_t *rows, const int64_t *cols
     }
     // persistent stream-K grid, one CTA per SM; cooperative so the rare
     // path's grid barrier is safe (a launch error, never a hang)
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)num_sms());
-    cfg.blockDim = dim3(kGemmNT);
-    cfg.dynamicSmemBytes = gemm_smem<NB>();
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    GEE_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_bm_gemm<NB>, rows, cols, a));
+    GEE_CHECK_CUDA(launch_pdl(k_bm_gemm<NB>, dim3((unsigned)num_sms()), dim3(kGemmNT), gemm_smem<NB>(), st, true, rows,
+                              cols, a));
     GEE_CHECK_LAUNCH("k_bm_gemm");
     return GEE_OK;
 }
@@ -1002,12 +1032,14 @@ int bitmap_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n
     GEE_CHECK_LAUNCH("k_bm_set");
     if (!directed) {
         const unsigned nt = (unsigned)(W.Np / kSB);
-        k_bm_sym<<<nt * (nt + 1) / 2, kSB, 0, st>>>(a);
+        GEE_CHECK_CUDA(launch_pdl(k_bm_sym, dim3(nt * (nt + 1) / 2), dim3(kSB), 0, st, false, a));
         GEE_CHECK_LAUNCH("k_bm_sym");
     } else {
-        k_bm_scan<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(a);
+        GEE_CHECK_CUDA(launch_pdl(k_bm_scan, dim3((unsigned)((n + 7) / 8)), dim3(256), 0, st, false, a));
         GEE_CHECK_LAUNCH("k_bm_scan");
     }
+    GEE_CHECK_CUDA(launch_pdl(k_bm_table, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, false, a));
+    GEE_CHECK_LAUNCH("k_bm_table");
     if (W.nbx == 16) return launch_gemm<16>(a, rows, cols, st);
     if (W.nbx == 32) return launch_gemm<32>(a, rows, cols, st);
     return launch_gemm<64>(a, rows, cols, st);
