@@ -320,10 +320,9 @@ __global__ void __launch_bounds__(kSB) k_bm_sym(BmArgs a) {
 __global__ void __launch_bounds__(256) k_bm_table(BmArgs a) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     pdl_wait();
+    pdl_trigger();  // k_bm_gemm may start now: it waits for this grid before reading the table
     if (blockIdx.x == 0) write_counts(a, threadIdx.x);
     if (r < a.n) node_entry(a, r, __ldcg(a.ucnt + r));
-    __syncthreads();
-    pdl_trigger();
 }
 
 // directed lists: one warp per row, 8 rows per CTA
@@ -668,7 +667,8 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
 
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     if (t == 0) TRACE(7, 0);
-    pdl_wait();
+    // Launched while k_bm_table runs (PDL): k_bm_sym's outputs (bitmap, counts,
+    // flags) are complete, the node table is not until pdl_wait().
     bool rep;
     {
         // popc(U) = E exactly when no pair repeats in the list
@@ -683,7 +683,10 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
         __syncthreads();
         rep = s_rep != 0;
     }
-    if (rep) repeat_phases(rows, cols, a);
+    if (rep) {
+        pdl_wait();
+        repeat_phases(rows, cols, a);
+    }
     if (t == 0) TRACE(7, 1);
 
     if (w == 8) {
@@ -721,10 +724,25 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
     if (w == 9) {
         // ---- bulk copies
         if (lane == 0) {
+            // the first kRR bitmap tiles go out before the node table (X^T)
+            // is known to be complete
+            const int pre = min(nsteps, kRR);
+            for (int i = 0; i < pre; ++i) {
+                const int g = s0 + i, m = g / KT, ks = g % KT;
+                const uint32_t bar = smem_u32(rfull + i);
+                mbar_expect_tx(bar, kRB + kBB);
+                bulk_g2s(smem_u32(sR + i * kRB), a.bm + ((size_t)(m * KT + ks) << 10), kRB, bar);
+            }
+            pdl_wait();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            for (int i = 0; i < pre; ++i) {
+                const int ks = (s0 + i) % KT;
+                bulk_g2s(smem_u32(sB + i * kBB), a.xt + (size_t)ks * kBB, kBB, smem_u32(rfull + i));
+            }
 #pragma unroll 1
-            for (int i = 0; i < nsteps; ++i) {
+            for (int i = pre; i < nsteps; ++i) {
                 const int rs = i % kRR, g = s0 + i, m = g / KT, ks = g % KT;
-                if (i >= kRR) mbar_wait_idle(smem_u32(rempty + rs), ((i / kRR) - 1) & 1, 32);
+                mbar_wait_idle(smem_u32(rempty + rs), ((i / kRR) - 1) & 1, 32);
                 const uint32_t bar = smem_u32(rfull + rs);
                 TRACE(0, i);
                 mbar_expect_tx(bar, kRB + kBB);
@@ -789,6 +807,7 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
     } else {
         // ---- epilogue: warp 4 + e reads TMEM lanes 32e..32e+31 (= tile rows)
         const int e = w - 4;
+        pdl_wait();  // inv, scale come from k_bm_table
         double inv[kKMax];
 #pragma unroll
         for (int q = 0; q < kKMax; ++q) inv[q] = q < a.k ? __ldcg(a.inv + q) : 0.0;
