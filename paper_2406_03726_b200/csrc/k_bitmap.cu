@@ -209,36 +209,59 @@ __global__ void __launch_bounds__(kSetThreads) k_bm_set(const int64_t *__restric
     __syncthreads();
     if (threadIdx.x < a.k && sh_hist[threadIdx.x]) atomicAdd(&a.cnt[threadIdx.x], sh_hist[threadIdx.x]);
 
-    constexpr int U = 4;
+    // Each lane takes a pair of consecutive stream entries (16-byte loads of
+    // rows and cols), so a warp covers 64 consecutive entries.  Runs of
+    // entries on the same bitmap word OR-combine: inside the pair, then across
+    // lanes with one segmented scan over the lanes' last runs; each run issues
+    // one reduction (RED.OR, no return value).  A sorted list costs about one
+    // reduction per touched word.
+    constexpr int U = 2;  // pairs per lane per iteration
+    constexpr unsigned INV = 0xffffffffu;
     const int64_t E = a.E;
     const unsigned le = lanemask_le();
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
-    for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x * U + threadIdx.x; e0 - threadIdx.x < E; e0 += stride) {
-        unsigned key[U], bit[U];
+    const bool vec = (((uintptr_t)rows | (uintptr_t)cols) & 15) == 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 2 * U;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * 2 * U; base < E; base += stride) {
+        unsigned k0[U], k1[U], b0[U], b1[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t e = e0 + (int64_t)u * blockDim.x;
-            const unsigned r = e < E ? (unsigned)__ldcs(rows + e) : 0u;
-            const unsigned c = e < E ? (unsigned)__ldcs(cols + e) : 0u;
-            key[u] = e < E ? bm_index(a, r, c >> 5) : 0xffffffffu;
-            bit[u] = e < E ? 1u << (c & 31) : 0u;
+            const int64_t e = base + ((int64_t)u * blockDim.x + threadIdx.x) * 2;
+            int64_t r0 = -1, r1 = -1, c0 = 0, c1 = 0;
+            if (vec && e + 1 < E) {
+                const longlong2 rv = __ldcs(reinterpret_cast<const longlong2 *>(rows + e));
+                const longlong2 cv = __ldcs(reinterpret_cast<const longlong2 *>(cols + e));
+                r0 = rv.x, r1 = rv.y, c0 = cv.x, c1 = cv.y;
+            } else {
+                if (e < E) r0 = rows[e], c0 = cols[e];
+                if (e + 1 < E) r1 = rows[e + 1], c1 = cols[e + 1];
+            }
+            k0[u] = r0 >= 0 ? bm_index(a, (unsigned)r0, (unsigned)c0 >> 5) : INV;
+            k1[u] = r1 >= 0 ? bm_index(a, (unsigned)r1, (unsigned)c1 >> 5) : INV;
+            b0[u] = r0 >= 0 ? 1u << (c0 & 31) : 0u;
+            b1[u] = r1 >= 0 ? 1u << (c1 & 31) : 0u;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            // segmented OR over runs of lanes holding the same word; the run's
-            // last lane issues one reduction (no return value: RED, not ATOM)
-            const unsigned kp = __shfl_up_sync(0xffffffffu, key[u], 1);
-            const unsigned kn = __shfl_down_sync(0xffffffffu, key[u], 1);
-            const bool head = lane == 0 || kp != key[u];
-            const bool tail = lane == 31 || kn != key[u];
+            const bool two = k1[u] != INV && k1[u] != k0[u];  // two distinct runs in this pair
+            const unsigned kf = k0[u], kl = k1[u] == INV ? k0[u] : k1[u];
+            const unsigned bf = two ? b0[u] : (b0[u] | b1[u]);
+            const unsigned bl = two ? b1[u] : (b0[u] | b1[u]);
+            const unsigned kl_prev = __shfl_up_sync(0xffffffffu, kl, 1);
+            const unsigned kf_next = __shfl_down_sync(0xffffffffu, kf, 1);
+            // the first run continues the previous lane's last run
+            const bool cont = lane > 0 && kf != INV && kl_prev == kf;
+            const bool head = !(cont && !two);
             const int start = 31 - __clz(__ballot_sync(0xffffffffu, head) & le);
-            unsigned incl = bit[u];
+            unsigned incl = bl;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane - o >= start) incl |= y;
             }
-            if (tail && key[u] != 0xffffffffu) atomicOr(&a.bm[key[u]], incl);
+            const unsigned prev = __shfl_up_sync(0xffffffffu, incl, 1);
+            if (two) atomicOr(&a.bm[kf], bf | (cont ? prev : 0u));
+            const bool tail = lane == 31 || kf_next != kl;
+            if (tail && kl != INV) atomicOr(&a.bm[kl], incl);
         }
     }
     pdl_trigger();
