@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kSetThreads) k_bm_set(const int64_t *__restric
     // lanes with one segmented scan over the lanes' last runs; each run issues
     // one reduction (RED.OR, no return value).  A sorted list costs about one
     // reduction per touched word.
-    constexpr int U = 2;  // pairs per lane per iteration
+    constexpr int U = 1;  // pairs per lane per iteration
     constexpr unsigned INV = 0xffffffffu;
     const int64_t E = a.E;
     const unsigned le = lanemask_le();
