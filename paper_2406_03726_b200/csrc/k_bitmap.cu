@@ -95,6 +95,12 @@ __device__ __forceinline__ unsigned lanemask_le() {
     return m;
 }
 
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ unsigned ld_gpu(const unsigned *p) {
     unsigned v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -686,7 +692,6 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
     uint64_t *accfull = rempty + kRR;
     uint64_t *accempty = accfull + 2;
     uint32_t *tslot = reinterpret_cast<uint32_t *>(accempty + 2);
-    __shared__ bool s_last;
 
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     if (t == 0) TRACE(7, 0);
@@ -869,42 +874,47 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             mbar_arrive(smem_u32(accempty + buf));
             const int sidx = m - s0 / KT;  // this CTA's segment index (0 or 1)
-            const bool whole = seglen == KT;  // this CTA did the whole tile: no partial sums to merge
-            if (!whole) {
-                // partial sums to this CTA's slab, plain stores; the CTA that
-                // completes the tile's KT steps merges the slabs
+            // Tile m's finisher is the CTA holding its first K step (its segment
+            // of m ends last in time: it is that CTA's final segment, while the
+            // partners' segments of m are mostly their first).  Partners store
+            // their partial sums and bump ready[m]; the finisher never waits on
+            // its own store, it only polls ready[m] and reads the partners' slabs.
+            const bool fin = g % KT == 0;
+            // the CTAs whose step ranges meet tile m (32-bit: T <= 128 * 64)
+            const unsigned G = gridDim.x, T = (unsigned)total;
+            const unsigned lo = (unsigned)m * KT, hi = lo + KT;
+            if (!fin) {
                 int4 *dst = reinterpret_cast<int4 *>(a.cpart + (((size_t)blockIdx.x * 2 + sidx) * kTM + e * 32 + lane) * NB);
 #pragma unroll
                 for (int j = 0; j < NB / 4; ++j) dst[j] = make_int4(C[4 * j], C[4 * j + 1], C[4 * j + 2], C[4 * j + 3]);
                 __threadfence();
-                if (e == 0 && lane == 0) TRACE(9, 17 + 8 * seg);
                 epi_bar();
-                if (e == 0 && lane == 0) s_last = atomicAdd(&a.mdone[m], (unsigned)seglen) + seglen == (unsigned)KT;
-                epi_bar();
-                if (e == 0 && lane == 0) TRACE(9, 18 + 8 * seg);
-            }
-            if ((whole || s_last) && r < a.n) {
-                if (!whole) {
-                    __threadfence();
-                    // the CTAs whose step ranges meet tile m (32-bit: T <= 128 * 64)
-                    const unsigned G = gridDim.x, T = (unsigned)total;
-                    const unsigned lo = (unsigned)m * KT, hi = lo + KT;
-                    unsigned b = lo * G / T;
-                    while (b > 0 && b * T / G > lo) --b;
-                    while ((b + 1) * T / G <= lo) ++b;
-                    for (; b < G && b * T / G < hi; ++b) {
-                        const unsigned bs0 = b * T / G, bs1 = (b + 1) * T / G;
-                        if (b == blockIdx.x || bs1 == bs0 || bs1 <= lo) continue;  // self, idle CTAs
-                        const int bsi = m - (int)(bs0 / KT);
-                        const int4 *src = reinterpret_cast<const int4 *>(
-                            a.cpart + (((size_t)b * 2 + bsi) * kTM + e * 32 + lane) * NB);
+                if (e == 0 && lane == 0) atomicAdd(&a.mdone[m], 1u);
+            } else if (seglen < KT && r < a.n) {
+                // partners: participating CTAs other than this one
+                unsigned b = lo * G / T;
+                while (b > 0 && b * T / G > lo) --b;
+                while ((b + 1) * T / G <= lo) ++b;
+                unsigned npart = 0;
+                for (unsigned bb = b; bb < G && bb * T / G < hi; ++bb) {
+                    const unsigned bs0 = bb * T / G, bs1 = (bb + 1) * T / G;
+                    if (bb != blockIdx.x && bs1 != bs0 && bs1 > lo) ++npart;
+                }
+                while (ld_acquire_gpu(a.mdone + m) < npart) __nanosleep(64);
+                for (; b < G && b * T / G < hi; ++b) {
+                    const unsigned bs0 = b * T / G, bs1 = (b + 1) * T / G;
+                    if (b == blockIdx.x || bs1 == bs0 || bs1 <= lo) continue;  // self, idle CTAs
+                    const int bsi = m - (int)(bs0 / KT);
+                    const int4 *src = reinterpret_cast<const int4 *>(
+                        a.cpart + (((size_t)b * 2 + bsi) * kTM + e * 32 + lane) * NB);
 #pragma unroll
-                        for (int j = 0; j < NB / 4; ++j) {
-                            const int4 v = __ldcg(src + j);
-                            C[4 * j] += v.x, C[4 * j + 1] += v.y, C[4 * j + 2] += v.z, C[4 * j + 3] += v.w;
-                        }
+                    for (int j = 0; j < NB / 4; ++j) {
+                        const int4 v = __ldcg(src + j);
+                        C[4 * j] += v.x, C[4 * j + 1] += v.y, C[4 * j + 2] += v.z, C[4 * j + 3] += v.w;
                     }
                 }
+            }
+            if (fin && r < a.n) {
                 if (e == 0 && lane == 0) TRACE(9, 19 + 8 * seg);
                 const bool rrep = rep && __ldcg(a.len + r) != __ldcg(a.ucnt + r);
                 gemm_epilogue<NB>(a, r, C, rrep, inv, rsc, rlab);
