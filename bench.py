@@ -360,6 +360,7 @@ def run_b200(args):
                 "peak_source": peak_src, "unit": "GB/s", "frac": dom["gbs"] / hbm,
                 "traffic": traffic, "alg_bytes_per_launch": dom["alg_bytes"]}
     emb = next((r for r in ktab if r["kernel"] == "k_embed"), None)
+    prod = next((r for r in ktab if r["kernel"] in ("k_bm_gemm", "k_embed")), None)
 
     # end to end: pinned host in -> Z on host, through the public plan API
     e2e = None
@@ -396,7 +397,8 @@ def run_b200(args):
         "vs_baseline_basis": "PAPER.md:93 sparse GEE 0.6 s for SBM 10k/5.6M edges lap+diag+corr "
                              "(laptop i5) = 9.33e6 edges/s" if args.config in PUBLISHED else None,
         "dtype": "f64", "data": "synthetic (seeded, BASELINE.json shapes)",
-        "config": dict(workload_desc(c), l2="flushed: 512 MiB write before every timed step",
+        "config": dict(workload_desc(c), l2=(f"flushed: {args.flush_mib} MiB write before every timed step"
+                                             if args.flush_mib > 0 else "not flushed"),
                        stream_entries=m_stream, nnz=nnz,
                        unit_weights=bool(w is None),
                        weights_read_per_step="none: EdgeList found every weight == 1.0 at "
@@ -404,6 +406,11 @@ def run_b200(args):
         "roofline": roofline,
         "embed_kernel": ({"ms_per_launch": emb["ms_per_launch"], "gbs": emb["gbs"],
                           "frac": emb["gbs"] / hbm} if emb else None),
+        # SURVEY 8(d) scope T1: the product kernel alone (inputs resident); the
+        # line's value is T2 (device pipeline) and e2e is T3 (host to host)
+        "t1": ({"kernel": prod["kernel"], "ms": prod["ms_per_launch"],
+                "edges_per_s": e / (prod["ms_per_launch"] * 1e-3),
+                "nnz_per_s": nnz / (prod["ms_per_launch"] * 1e-3)} if prod else None),
         "kernels": ktab,
         "cpu_baseline": cpu,
         "e2e": e2e,
