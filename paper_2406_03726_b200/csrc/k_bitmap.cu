@@ -221,54 +221,57 @@ __global__ void __launch_bounds__(kSetThreads) k_bm_set(const int64_t *__restric
     // lanes with one segmented scan over the lanes' last runs; each run issues
     // one reduction (RED.OR, no return value).  A sorted list costs about one
     // reduction per touched word.
-    constexpr int U = 1;  // pairs per lane per iteration
     constexpr unsigned INV = 0xffffffffu;
     const int64_t E = a.E;
     const unsigned le = lanemask_le();
     const bool vec = (((uintptr_t)rows | (uintptr_t)cols) & 15) == 0;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 2 * U;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * 2 * U; base < E; base += stride) {
-        unsigned k0[U], k1[U], b0[U], b1[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t e = base + ((int64_t)u * blockDim.x + threadIdx.x) * 2;
-            int64_t r0 = -1, r1 = -1, c0 = 0, c1 = 0;
-            if (vec && e + 1 < E) {
-                const longlong2 rv = __ldcs(reinterpret_cast<const longlong2 *>(rows + e));
-                const longlong2 cv = __ldcs(reinterpret_cast<const longlong2 *>(cols + e));
-                r0 = rv.x, r1 = rv.y, c0 = cv.x, c1 = cv.y;
-            } else {
-                if (e < E) r0 = rows[e], c0 = cols[e];
-                if (e + 1 < E) r1 = rows[e + 1], c1 = cols[e + 1];
-            }
-            k0[u] = r0 >= 0 ? bm_index(a, (unsigned)r0, (unsigned)c0 >> 5) : INV;
-            k1[u] = r1 >= 0 ? bm_index(a, (unsigned)r1, (unsigned)c1 >> 5) : INV;
-            b0[u] = r0 >= 0 ? 1u << (c0 & 31) : 0u;
-            b1[u] = r1 >= 0 ? 1u << (c1 & 31) : 0u;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 2;
+    // this lane's pair at e (row INV = past the end); only the low 32 bits of
+    // the int64 indices are used (n <= kBmMax)
+    auto fetch = [&](int64_t e, unsigned &r0, unsigned &r1, unsigned &c0, unsigned &c1) {
+        r0 = r1 = INV;
+        c0 = c1 = 0;
+        if (vec && e + 1 < E) {
+            const longlong2 rv = __ldcs(reinterpret_cast<const longlong2 *>(rows + e));
+            const longlong2 cv = __ldcs(reinterpret_cast<const longlong2 *>(cols + e));
+            r0 = (unsigned)rv.x, r1 = (unsigned)rv.y, c0 = (unsigned)cv.x, c1 = (unsigned)cv.y;
+        } else {
+            if (e < E) r0 = (unsigned)rows[e], c0 = (unsigned)cols[e];
+            if (e + 1 < E) r1 = (unsigned)rows[e + 1], c1 = (unsigned)cols[e + 1];
         }
+    };
+    int64_t base = (int64_t)blockIdx.x * blockDim.x * 2;
+    unsigned r0, r1, c0, c1;
+    fetch(base + threadIdx.x * 2, r0, r1, c0, c1);
+    // software-pipelined: the next pair is in flight while this one is scanned
+    for (; base < E; base += stride) {
+        unsigned nr0, nr1, nc0, nc1;
+        fetch(base + stride + threadIdx.x * 2, nr0, nr1, nc0, nc1);
+        const unsigned k0 = r0 != INV ? bm_index(a, r0, c0 >> 5) : INV;
+        const unsigned k1 = r1 != INV ? bm_index(a, r1, c1 >> 5) : INV;
+        const unsigned b0 = r0 != INV ? 1u << (c0 & 31) : 0u;
+        const unsigned b1 = r1 != INV ? 1u << (c1 & 31) : 0u;
+        const bool two = k1 != INV && k1 != k0;  // two distinct runs in this pair
+        const unsigned kf = k0, kl = k1 == INV ? k0 : k1;
+        const unsigned bf = two ? b0 : (b0 | b1);
+        const unsigned bl = two ? b1 : (b0 | b1);
+        const unsigned kl_prev = __shfl_up_sync(0xffffffffu, kl, 1);
+        const unsigned kf_next = __shfl_down_sync(0xffffffffu, kf, 1);
+        // the first run continues the previous lane's last run
+        const bool cont = lane > 0 && kf != INV && kl_prev == kf;
+        const bool head = !(cont && !two);
+        const int start = 31 - __clz(__ballot_sync(0xffffffffu, head) & le);
+        unsigned incl = bl;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const bool two = k1[u] != INV && k1[u] != k0[u];  // two distinct runs in this pair
-            const unsigned kf = k0[u], kl = k1[u] == INV ? k0[u] : k1[u];
-            const unsigned bf = two ? b0[u] : (b0[u] | b1[u]);
-            const unsigned bl = two ? b1[u] : (b0[u] | b1[u]);
-            const unsigned kl_prev = __shfl_up_sync(0xffffffffu, kl, 1);
-            const unsigned kf_next = __shfl_down_sync(0xffffffffu, kf, 1);
-            // the first run continues the previous lane's last run
-            const bool cont = lane > 0 && kf != INV && kl_prev == kf;
-            const bool head = !(cont && !two);
-            const int start = 31 - __clz(__ballot_sync(0xffffffffu, head) & le);
-            unsigned incl = bl;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane - o >= start) incl |= y;
-            }
-            const unsigned prev = __shfl_up_sync(0xffffffffu, incl, 1);
-            if (two) atomicOr(&a.bm[kf], bf | (cont ? prev : 0u));
-            const bool tail = lane == 31 || kf_next != kl;
-            if (tail && kl != INV) atomicOr(&a.bm[kl], incl);
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane - o >= start) incl |= y;
         }
+        const unsigned prev = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (two) atomicOr(&a.bm[kf], bf | (cont ? prev : 0u));
+        const bool tail = lane == 31 || kf_next != kl;
+        if (tail && kl != INV) atomicOr(&a.bm[kl], incl);
+        r0 = nr0, r1 = nr1, c0 = nc0, c1 = nc1;
     }
     pdl_trigger();
 }
