@@ -16,6 +16,7 @@
 // scatter, shared-memory privatised when the row count is small), then every
 // row is ordered on chip by the 64-bit key (col << 32 | idx):
 //   tier S  L <= 32            warp rank-sort in registers
+//   tier M  L <= kMCap         warp bitonic sort in a per-warp shared slice
 //   tier D  small n_cols       CTA counting sort over the column range in
 //                              shared memory (rows of ~1K entries, cfg 0/1)
 //   tier B  L <= kCap          CTA bitonic sort in shared memory
@@ -36,8 +37,9 @@ constexpr int kCap = 4096;           // entries staged in shared memory per row
 constexpr int kSmallRows = 16384;    // privatised row histogram (64 KB)
 constexpr int kSmallCols = 12288;    // dense per-row column counting (48 KB)
 constexpr int kSChunk = 64;          // tier-S rows per work grab
+constexpr int kMCap = 256;           // tier-M rows: one warp, 256 x 16 B of shared memory
 
-enum { TIER_D = 0, TIER_B = 1, TIER_X = 2 };
+enum { TIER_D = 0, TIER_B = 1, TIER_X = 2, TIER_M = 3, kTiers = 4 };
 
 __device__ __forceinline__ double load_w(const void *w, int wt, int64_t e) {
     if (wt == GEE_W_F64) return static_cast<const double *>(w)[e];
@@ -200,6 +202,8 @@ __global__ void k_classify(const int64_t *__restrict__ slot_ptr, int64_t n_rows,
             if (L > 32) {
                 if (dense_ok && (L * 16 >= n_cols || L > kCap))
                     tier = TIER_D;
+                else if (L <= kMCap)
+                    tier = TIER_M;
                 else if (L <= kCap)
                     tier = TIER_B;
                 else
@@ -231,9 +235,9 @@ struct RowsArgs {
     int32_t *out_col;  // unique entries at slot positions
     double *out_val;
     unsigned *ucnt;
-    const unsigned *lists;  // [3][n_rows]
-    const unsigned *nlist;  // [3]
-    unsigned *work;         // [4] work counters
+    const unsigned *lists;  // [kTiers][n_rows]
+    const unsigned *nlist;  // [kTiers]
+    unsigned *work;         // [5] work counters
     unsigned deg_flags;
     double *deg;
     double *scale;
@@ -560,6 +564,104 @@ __device__ void row_small(const RowsArgs &a, int64_t r, unsigned long long *wk, 
     __syncwarp();
 }
 
+// tier M: one warp per row of kMCap or fewer entries: bitonic sort of the
+// full key (col << 32 | idx, so equal-column runs come out in stream order)
+// in a per-warp shared slice, then the warp sums runs, drops zeros, writes the
+// unique entries at the row's slot start and folds the degree.
+__device__ void row_medium(const RowsArgs &a, int64_t r, unsigned long long *wk, double *wv) {
+    const int lane = threadIdx.x & 31;
+    const int64_t s0 = a.slot_ptr[r];
+    const int L = (int)(a.slot_ptr[r + 1] - s0);
+    int P = 64;
+    while (P < L) P <<= 1;
+    for (int i = lane; i < P; i += 32) {
+        wk[i] = i < L ? a.key[s0 + i] : ~0ull;
+        wv[i] = i < L ? a.val[s0 + i] : 0.0;
+    }
+    __syncwarp();
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < P; i += 32) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const unsigned long long x = wk[i], y = wk[ixj];
+                    if ((x > y) == ((i & k) == 0)) {
+                        wk[i] = y;
+                        wk[ixj] = x;
+                        const double t = wv[i];
+                        wv[i] = wv[ixj];
+                        wv[ixj] = t;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+    const bool want_deg = a.deg_flags != 0;
+    const bool diag = (a.deg_flags & GEE_DIAGONAL) != 0;
+    unsigned base = 0;
+    Cert cert;
+    double psum = 0.0;
+    bool placed = false;
+    for (int c0 = 0; c0 < L; c0 += 32) {
+        const int i = c0 + lane;
+        const bool v = i < L;
+        const unsigned col = v ? (unsigned)(wk[i] >> 32) : 0xffffffffu;
+        const bool head = v && (i == 0 || (unsigned)(wk[i - 1] >> 32) != col);
+        double acc = 0.0;
+        if (head) {
+            acc = wv[i];
+            for (int j = i + 1; j < L && (unsigned)(wk[j] >> 32) == col; ++j) acc += wv[j];  // stream order
+        }
+        const bool keep = head && acc != 0.0;
+        const unsigned km = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const unsigned pos = base + __popc(km & lanemask_lt());
+            a.out_col[s0 + pos] = (int32_t)col;
+            a.out_val[s0 + pos] = acc;
+            if (want_deg) {
+                double x = acc;
+                if (diag && (int64_t)col == r) {
+                    x = acc + 1.0;
+                    placed = true;
+                }
+                cert.add(x);
+                psum += x;
+            }
+        }
+        base += __popc(km);
+    }
+    if (lane == 0) a.ucnt[r] = base;
+    if (!want_deg) return;
+    const bool insert = diag && !__any_sync(0xffffffffu, placed);
+    int mlow = warp_min(cert.mlow);
+    double sabs = warp_sum(cert.sabs) + (insert ? 1.0 : 0.0);
+    if (insert) mlow = min(mlow, 0);
+    if (cert_ok(mlow, sabs)) {
+        const double d = warp_sum(psum) + (insert ? 1.0 : 0.0);
+        if (lane == 0) store_degree(a, r, d);
+    } else {
+        __syncwarp();  // the warp's out_* writes visible to lane 0
+        if (lane == 0) {
+            double d = 0.0;
+            bool ins = !insert;
+            for (unsigned i = 0; i < base; ++i) {
+                const int64_t c = a.out_col[s0 + i];
+                double x = a.out_val[s0 + i];
+                if (!ins && c > r) {
+                    d += 1.0;
+                    ins = true;
+                }
+                if (diag && c == r) x = x + 1.0;
+                d += x;
+            }
+            if (!ins) d += 1.0;
+            store_degree(a, r, d);
+        }
+    }
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(kRowsThreads, 2) k_rows(RowsArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ RowsShared sm;
@@ -567,6 +669,7 @@ __global__ void __launch_bounds__(kRowsThreads, 2) k_rows(RowsArgs a) {
     double *stv = reinterpret_cast<double *>(dsm + sizeof(unsigned long long) * kCap);
     unsigned *region2 = reinterpret_cast<unsigned *>(dsm + 16 * kCap);
     const int n_x = (int)a.nlist[TIER_X], n_d = (int)a.nlist[TIER_D], n_b = (int)a.nlist[TIER_B];
+    const int n_m = (int)a.nlist[TIER_M];
     const unsigned *lx = a.lists + (size_t)TIER_X * a.n_rows;
     const unsigned *ld = a.lists + (size_t)TIER_D * a.n_rows;
     const unsigned *lb = a.lists + (size_t)TIER_B * a.n_rows;
@@ -595,8 +698,21 @@ __global__ void __launch_bounds__(kRowsThreads, 2) k_rows(RowsArgs a) {
         if (t >= n_b) break;
         row_bitonic(a, sm, lb[t], stk, stv);
     }
-    // phase S: chunks of rows, one warp per row, rows > 32 skipped
+    // phase M: one warp per row, warps grab rows independently
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    {
+        const unsigned *lm = a.lists + (size_t)TIER_M * a.n_rows;
+        unsigned long long *mk = stk + wid * kMCap;
+        double *mv = stv + wid * kMCap;
+        for (;;) {
+            int t = 0;
+            if (lane == 0) t = (int)atomicAdd(&a.work[4], 1u);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= n_m) break;
+            row_medium(a, lm[t], mk, mv);
+        }
+    }
+    // phase S: chunks of rows, one warp per row, rows > 32 skipped
     unsigned long long *wk = stk + wid * 32;
     double *wv = stv + wid * 32;
     const int64_t n_chunks = (a.n_rows + kSChunk - 1) / kSChunk;
@@ -668,7 +784,7 @@ struct CsrWs {
     int64_t *tmp_ptr;
     unsigned *part;
     unsigned *lists;
-    unsigned *nlist;  // [3] + work[4]
+    unsigned *nlist;  // [kTiers] tier counts, then the work counters
     unsigned *ucnt;
     unsigned long long *key, *key2;
     double *val, *val2;
@@ -686,8 +802,8 @@ static size_t carve_csr(Carver &cv, CsrWs &w, int64_t E, int64_t n_rows, int dir
     w.slot_ptr = cv.take<int64_t>((size_t)n_rows + 1);
     w.tmp_ptr = cv.take<int64_t>((size_t)n_rows + 1);
     w.part = n_rows <= kSmallRows ? cv.take<unsigned>((size_t)w.G * (size_t)(n_rows + 1)) : nullptr;
-    w.lists = cv.take<unsigned>((size_t)3 * (size_t)(n_rows + 1));
-    w.nlist = cv.take<unsigned>(8);
+    w.lists = cv.take<unsigned>((size_t)kTiers * (size_t)(n_rows + 1));
+    w.nlist = cv.take<unsigned>(16);
     w.ucnt = cv.take<unsigned>((size_t)n_rows + 1);
     w.key = cv.take<unsigned long long>((size_t)Mc);
     w.val = cv.take<double>((size_t)Mc);
@@ -762,7 +878,7 @@ int csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, i
                                             kSmallRows * 4));
         part_attr = true;
     }
-    GEE_CHECK_CUDA(cudaMemsetAsync(W.nlist, 0, 8 * sizeof(unsigned), st));
+    GEE_CHECK_CUDA(cudaMemsetAsync(W.nlist, 0, 16 * sizeof(unsigned), st));
     GEE_CHECK_CUDA(cudaMemsetAsync(W.cnt, 0, sizeof(unsigned) * (size_t)(n_rows + 1), st));
     // pass 1: counts
     if (E > 0) {
@@ -814,7 +930,7 @@ int csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, i
         a.ucnt = compact ? W.ucnt : row_cnt;
         a.lists = W.lists;
         a.nlist = W.nlist;
-        a.work = W.nlist + 3;
+        a.work = W.nlist + kTiers;
         a.deg_flags = deg_flags;
         a.deg = deg;
         a.scale = (deg_flags & GEE_LAPLACIAN) ? scale : nullptr;
