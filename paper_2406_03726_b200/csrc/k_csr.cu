@@ -70,12 +70,10 @@ __device__ __forceinline__ unsigned warp_agg_take(unsigned *ctr, unsigned key, b
 __global__ void k_count_global(const int64_t *__restrict__ rows, const int64_t *__restrict__ cols,
                                int64_t E, int directed, unsigned *__restrict__ cnt) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t e_round = (E + 31) & ~int64_t(31);
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e_round; e += stride) {
-        bool v = e < E;
-        unsigned r = v ? (unsigned)rows[e] : 0u, c = v ? (unsigned)cols[e] : 0u;
-        warp_agg_add(cnt, r, v);
-        warp_agg_add(cnt, c, v && !directed && r != c);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += stride) {
+        const unsigned r = (unsigned)rows[e], c = (unsigned)cols[e];
+        atomicAdd(&cnt[r], 1u);  // RED: no return, nothing waits on it
+        if (!directed && r != c) atomicAdd(&cnt[c], 1u);
     }
 }
 
@@ -125,29 +123,42 @@ __global__ void k_scatter_global(const int64_t *__restrict__ rows, const int64_t
                                  const void *__restrict__ w, int wt, int64_t E, int directed,
                                  const int64_t *__restrict__ slot_ptr, unsigned *__restrict__ cursor,
                                  unsigned long long *__restrict__ key, double *__restrict__ val) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t e_round = (E + 31) & ~int64_t(31);
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e_round; e += stride) {
-        bool v = e < E;
-        unsigned r = 0, c = 0;
-        double wv = 0.0;
-        if (v) {
-            r = (unsigned)rows[e];
-            c = (unsigned)cols[e];
-            wv = load_w(w, wt, e);
+    // kU entries per thread with every slot reservation (a returning atomic)
+    // and bucket-start load in flight together: one round trip per kU entries
+    constexpr int kU = 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * kU;
+    for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x * kU + threadIdx.x; e0 < E; e0 += stride) {
+        unsigned r[kU], c[kU], s1[kU], s2[kU];
+        double wv[kU];
+        int64_t p1[kU], p2[kU];
+        bool v[kU], v2[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t e = e0 + (int64_t)u * blockDim.x;
+            v[u] = e < E;
+            r[u] = v[u] ? (unsigned)rows[e] : 0u;
+            c[u] = v[u] ? (unsigned)cols[e] : 0u;
+            wv[u] = v[u] ? load_w(w, wt, e) : 0.0;
         }
-        unsigned s1 = warp_agg_take(cursor, r, v);
-        if (v) {
-            int64_t p = slot_ptr[r] + s1;
-            key[p] = ((unsigned long long)c << 32) | (unsigned long long)e;
-            val[p] = wv;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            v2[u] = v[u] && !directed && r[u] != c[u];
+            s1[u] = v[u] ? atomicAdd(&cursor[r[u]], 1u) : 0u;
+            s2[u] = v2[u] ? atomicAdd(&cursor[c[u]], 1u) : 0u;
+            p1[u] = v[u] ? slot_ptr[r[u]] : 0;
+            p2[u] = v2[u] ? slot_ptr[c[u]] : 0;
         }
-        bool v2 = v && !directed && r != c;
-        unsigned s2 = warp_agg_take(cursor, c, v2);
-        if (v2) {
-            int64_t p = slot_ptr[c] + s2;
-            key[p] = ((unsigned long long)r << 32) | (unsigned long long)(E + e);
-            val[p] = wv;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t e = e0 + (int64_t)u * blockDim.x;
+            if (v[u]) {
+                key[p1[u] + s1[u]] = ((unsigned long long)c[u] << 32) | (unsigned long long)e;
+                if (wt != GEE_W_UNIT) val[p1[u] + s1[u]] = wv[u];
+            }
+            if (v2[u]) {
+                key[p2[u] + s2[u]] = ((unsigned long long)r[u] << 32) | (unsigned long long)(E + e);
+                if (wt != GEE_W_UNIT) val[p2[u] + s2[u]] = wv[u];
+            }
         }
     }
 }
@@ -177,13 +188,13 @@ __global__ void k_scatter_part(const int64_t *__restrict__ rows, const int64_t *
         unsigned p1 = warp_agg_take(cur, r, v);
         if (v) {
             key[p1] = ((unsigned long long)c << 32) | (unsigned long long)e;
-            val[p1] = wv;
+            if (wt != GEE_W_UNIT) val[p1] = wv;
         }
         bool v2 = v && !directed && r != c;
         unsigned p2 = warp_agg_take(cur, c, v2);
         if (v2) {
             key[p2] = ((unsigned long long)r << 32) | (unsigned long long)(E + e);
-            val[p2] = wv;
+            if (wt != GEE_W_UNIT) val[p2] = wv;
         }
     }
 }
@@ -232,6 +243,7 @@ struct RowsArgs {
     double *val;
     unsigned long long *key2;  // global staging / LSD ping-pong
     double *val2;
+    int unit;  // unit weights: bucket values are implicit 1.0 and never stored
     int32_t *out_col;  // unique entries at slot positions
     double *out_val;
     unsigned *ucnt;
@@ -244,6 +256,9 @@ struct RowsArgs {
     int32_t *err;
     int dense_ok;
 };
+
+// a bucket entry's value
+__device__ __forceinline__ double bval(const RowsArgs &a, int64_t p) { return a.unit ? 1.0 : a.val[p]; }
 
 struct RowsShared {
     unsigned ured[33];
@@ -357,7 +372,6 @@ __device__ void row_dense(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned
     const int L = (int)(a.slot_ptr[r + 1] - s0);
     const int nc = (int)a.n_cols;
     const unsigned long long *key = a.key + s0;
-    const double *val = a.val + s0;
     for (int c = threadIdx.x; c < nc; c += blockDim.x) cnt[c] = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < L; i += blockDim.x) atomicAdd(&cnt[(unsigned)(key[i] >> 32)], 1u);
@@ -381,7 +395,7 @@ __device__ void row_dense(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned
         unsigned long long k = key[i];
         unsigned p = atomicAdd(&cnt[(unsigned)(k >> 32)], 1u);
         sk[p] = k;
-        sv[p] = val[i];
+        sv[p] = bval(a, s0 + i);
     }
     __syncthreads();
     finish_row(a, sm, r, s0, L, sk, sv, true);
@@ -397,7 +411,7 @@ __device__ void row_bitonic(const RowsArgs &a, RowsShared &sm, int64_t r, unsign
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
         if (i < L) {
             sk[i] = a.key[s0 + i];
-            sv[i] = a.val[s0 + i];
+            sv[i] = bval(a, s0 + i);
         } else {
             sk[i] = ~0ull;
             sv[i] = 0.0;
@@ -436,6 +450,10 @@ __device__ void row_lsd(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned *
     const int a0 = min(L, wid * chunk), a1 = min(L, a0 + chunk);
     unsigned long long *src = a.key + s0, *dst = a.key2 + s0;
     double *srcv = a.val + s0, *dstv = a.val2 + s0;
+    if (a.unit) {
+        for (int i = threadIdx.x; i < L; i += blockDim.x) srcv[i] = 1.0;
+        __syncthreads();
+    }
     const int passes = (a.colbits + 7) / 8;
     for (int pass = 0; pass < passes; ++pass) {
         const int shift = 32 + 8 * pass;
@@ -492,7 +510,7 @@ __device__ void row_small(const RowsArgs &a, int64_t r, unsigned long long *wk, 
     double v = 0.0;
     if (lane < L) {
         k = a.key[s0 + lane];
-        v = a.val[s0 + lane];
+        v = bval(a, s0 + lane);
     }
     int rank = 0;
     for (int j = 0; j < L; ++j) rank += __shfl_sync(0xffffffffu, k, j) < k;
@@ -576,7 +594,7 @@ __device__ void row_medium(const RowsArgs &a, int64_t r, unsigned long long *wk,
     while (P < L) P <<= 1;
     for (int i = lane; i < P; i += 32) {
         wk[i] = i < L ? a.key[s0 + i] : ~0ull;
-        wv[i] = i < L ? a.val[s0 + i] : 0.0;
+        wv[i] = i < L ? bval(a, s0 + i) : 0.0;
     }
     __syncwarp();
     for (int k = 2; k <= P; k <<= 1) {
@@ -925,6 +943,7 @@ int csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, i
         a.val = W.val;
         a.key2 = W.key2;
         a.val2 = W.val2;
+        a.unit = wt == GEE_W_UNIT;
         a.out_col = col;
         a.out_val = val;
         a.ucnt = compact ? W.ucnt : row_cnt;
