@@ -308,7 +308,7 @@ def _sorted_unit(rng, n, p):
 
 
 @pytest.mark.parametrize("variant", ["plain", "adjacent_dup", "both_directions", "loops", "directed",
-                                     "max_n"])
+                                     "max_n", "no_edges", "unlabeled", "tiny", "k1"])
 def test_bitmap_encode_variants(variant):
     # the fused bitmap encode (unit weights, n <= 16384, K <= 8): warp-combined
     # atomics on sorted lists, the in-place symmetrisation, and the rare path
@@ -334,8 +334,17 @@ def test_bitmap_encode_variants(variant):
     elif variant == "directed":
         directed = True
         rows, cols = np.concatenate([rows, cols[::3]]), np.concatenate([cols, rows[::3]])
+    elif variant == "no_edges":
+        rows, cols = rows[:0], cols[:0]
+    elif variant == "tiny":
+        n = 5
+        rows, cols = np.array([0, 0, 1, 3], np.int64), np.array([1, 4, 2, 3], np.int64)
+    elif variant == "k1":
+        k = 1
     labels = rng.integers(0, k, n)
     labels[::11] = -1
+    if variant == "unlabeled":
+        labels[:] = -1
     _check_against_oracle(n, rows, cols, np.ones(rows.size), labels, k, directed,
                           combos=[(0, 0, 0), (1, 1, 1), (1, 0, 1), (0, 1, 0)])
 
