@@ -9,43 +9,44 @@
 // a product of the 0/1 adjacency matrix S with the N x K matrix X[c, q] =
 // s_c [Y_c = q].  The encode needs only the N x N adjacency bitmap -- Np^2/8
 // bytes, 13 MB at N = 10^4 -- which stays resident in the 126 MB L2; the CSR
-// itself is never materialised (gee_encode_edges returns Z only).
+// itself is never materialised (gee_encode_edges returns Z only).  The
+// bitmap is stored as 128 x 128-bit tiles (see bm_index).  Four kernels, each
+// launched with programmatic dependent launch behind the previous one:
 //   k_bm_set   the labels (validated, y32, class histogram) and one read of the
-//              int64 edge list: each stream entry sets bit (r, c) of U with a
-//              global reduction (RED.OR, no return).  Lanes holding the same
-//              bitmap word (adjacent entries of a row-major list) OR-combine
-//              first, so a sorted list costs about one reduction per word.
-//   k_bm_sym   undirected lists: S = U | U^T in place, 256 x 256-bit block
-//              pairs, 32 x 32 transposes by warp shuffles.  It also counts
-//              popc(U) (= E exactly when no pair repeats in the list) and
-//              flags pairs present in both directions (U & U^T off the
-//              diagonal), the other way a pair repeats in the stream.  Each
-//              block pair adds its rows' popcounts to u_r; the CTA that
-//              completes a 256-row block writes that block's node table:
-//              d_r = u_r (+1 under A+I), s_r = d_r^-1/2, and X's row as
-//              7 base-256 digits of s_r * 2^55 in the columns of class Y_r.
+//              int64 edge list, a pair of entries per lane (16-byte loads):
+//              each entry sets bit (r, c) of U with a global reduction
+//              (RED.OR, no return).  Runs of entries on the same bitmap word
+//              (a row-major list) OR-combine first, in the lane and then by a
+//              segmented warp scan, so a sorted list costs about one
+//              reduction per touched word.
+//   k_bm_sym   undirected lists: S = U | U^T in place, one CTA per pair of
+//              128 x 128 tiles, 32 x 32 transposes by warp shuffles; row
+//              popcounts u_r, popc(U) (= E exactly when no pair repeats in the
+//              list) and pairs present in both directions (U & U^T off the
+//              diagonal, the other way a pair repeats in the stream).
 //              (Directed lists: k_bm_scan, one warp per row, instead.)
+//   k_bm_table thread per node: d_r = u_r (+1 under A+I), s_r = d_r^-1/2, and
+//              X^T's column r as 7 base-256 digits of s_r * 2^55 in the rows
+//              of class Y_r, stored as the GEMM's shared-memory B tiles.
 //   k_bm_gemm  S x X on the 5th-generation tensor cores (tcgen05.mma
-//              kind::i8, u8 x u8 -> s32 in TMEM): 128-row tiles, 128-column
-//              K steps; the A tile is S's bits expanded to bytes in shared
-//              memory (128B-swizzled K-major), the B tile X's digit columns.
-//              Integer accumulation is exact, so sum_c S_rc s_c is known to
-//              2^-55 per term, whatever the order; split-K partials are
-//              integer too.  The epilogue recombines the digits in f64 and
-//              applies 1/n_q, the diagonal, s_r and the correlation.
+//              kind::i8, u8 x u8 -> s32): A = S's bits expanded to bytes and
+//              written straight into TMEM (tcgen05.st), B = the X^T tile
+//              bulk-copied into shared memory; persistent stream-K over
+//              (128-row tile, 256-column K step).  Integer accumulation is
+//              exact, so sum_c S_rc s_c is known to 2^-55 per term whatever
+//              the order; stream-K partials are integer too.  The epilogue
+//              recombines the digits in f64 and applies 1/n_q, the diagonal,
+//              s_r and the correlation.
 // Rare path (some pair repeats): k_bm_gemm first recomputes the stream
 // lengths by atomics, the node table and, for rows with repeats, per-class
 // sums of g = s_c/n_q over every stream entry, in grid-wide phases (all CTAs
-// are co-resident); those rows take their sums from there.
+// are co-resident: cooperative launch); those rows take their sums from there.
 #include "gee_common.cuh"
-
-#include <stdio.h>
-#include <stdlib.h>
 
 namespace gee {
 
 constexpr int kBmMax = 16384;   // nodes: bitmap Np^2/8 <= 32 MB (L2-resident)
-constexpr int kBlk = 256;       // rows / columns of a k_bm_sym block
+constexpr int kBlk = 256;       // the bitmap's side is padded to a multiple of 256
 constexpr int kSetThreads = 512;
 constexpr int kKMax = 8;        // classes
 constexpr int kPopParts = 64;   // spread counters for popc(U)
@@ -54,14 +55,13 @@ constexpr int kTM = 128;        // GEMM rows per tile (TMEM lanes)
 constexpr int kTK = 256;        // GEMM columns per K step (two 128-byte swizzle atoms)
 
 struct BmArgs {
-    int n, Wp, nb, Np;        // nodes, bitmap words per row (multiple of 8), 256-row blocks, Wp*32
+    int n, Wp, Np;            // nodes, bitmap words per row (multiple of 8), Wp*32
     int64_t E;
     int directed;
     unsigned *bm;             // [Np][Wp]
     unsigned *ucnt;           // [n] distinct columns per row
     unsigned *len;            // [n] stream lengths (rare path)
     unsigned *cnt;            // [kKMax] class histogram
-    unsigned *blkdone;        // [nb] finished block pairs per 256-row block
     unsigned *mdone;          // [Np/128] K steps accumulated per GEMM row tile
     unsigned *flags;          // [0] pair in both directions, [1] rare-path barrier, [3] table barrier
     unsigned *upop;           // [kPopParts * 32] popc(U) partial sums, 128 B apart
@@ -953,25 +953,24 @@ static int nb_cols(int k) {
 }
 
 struct BmWs {
-    unsigned *bm, *ucnt, *len, *cnt, *blkdone, *mdone, *flags, *upop;
+    unsigned *bm, *ucnt, *len, *cnt, *mdone, *flags, *upop;
     unsigned char *xt;
     int32_t *cacc;
     double *zacc, *tab_g;
     signed char *tab_lab;
-    int Wp, nb, Np, nbx;
+    int Wp, Np, nbx;
     size_t clear_bytes;
 };
 
 static void carve_bm(Carver &cv, BmWs &w, int64_t n, int k) {
     const int64_t np = (n + kBlk - 1) / kBlk * kBlk;
-    w.nb = (int)(np / kBlk);
     w.Wp = (int)(np / 32);
     w.Np = (int)np;
     w.nbx = nb_cols(k);
     // bitmap, counters, flags and X^T are contiguous: one memset clears them
     const size_t bmw = (size_t)np * w.Wp;
     const size_t words =
-        (bmw + 2 * (size_t)n + kKMax + (size_t)w.nb + (size_t)(np / kTM) + 4 + 32 * kPopParts + 3) & ~size_t(3);
+        (bmw + 2 * (size_t)n + kKMax + (size_t)(np / kTM) + 4 + 32 * kPopParts + 3) & ~size_t(3);
     const size_t xbytes = (size_t)w.nbx * (size_t)np;
     w.clear_bytes = 4 * words + xbytes;
     unsigned char *base = cv.take<unsigned char>(w.clear_bytes);
@@ -979,8 +978,7 @@ static void carve_bm(Carver &cv, BmWs &w, int64_t n, int k) {
     w.ucnt = w.bm ? w.bm + bmw : nullptr;
     w.len = w.bm ? w.ucnt + n : nullptr;
     w.cnt = w.bm ? w.len + n : nullptr;
-    w.blkdone = w.bm ? w.cnt + kKMax : nullptr;
-    w.mdone = w.bm ? w.blkdone + w.nb : nullptr;
+    w.mdone = w.bm ? w.cnt + kKMax : nullptr;
     w.flags = w.bm ? w.mdone + np / kTM : nullptr;
     w.upop = w.bm ? w.flags + 4 : nullptr;
     w.xt = base ? base + 4 * words : nullptr;
@@ -1054,7 +1052,6 @@ int bitmap_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n
     BmArgs a;
     a.n = (int)n;
     a.Wp = W.Wp;
-    a.nb = W.nb;
     a.Np = W.Np;
     a.E = E;
     a.directed = directed;
@@ -1062,7 +1059,6 @@ int bitmap_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n
     a.ucnt = W.ucnt;
     a.len = W.len;
     a.cnt = W.cnt;
-    a.blkdone = W.blkdone;
     a.mdone = W.mdone;
     a.flags = W.flags;
     a.upop = W.upop;
