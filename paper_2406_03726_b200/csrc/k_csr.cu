@@ -238,7 +238,7 @@ __global__ void k_classify(const int64_t *__restrict__ slot_ptr, int64_t n_rows,
 struct RowsArgs {
     const int64_t *slot_ptr;
     int64_t n_rows, n_cols;
-    int colbits;
+    int colbits, idxbits;     // bits of a column index, of a stream index
     unsigned long long *key;  // scattered buckets (input)
     double *val;
     unsigned long long *key2;  // global staging / LSD ping-pong
@@ -288,18 +288,25 @@ __device__ void finish_row(const RowsArgs &a, RowsShared &sm, int64_t r, int64_t
         int q = p + 1;
         while (q < L && (unsigned)(sk[q] >> 32) == c) ++q;
         if (fixup && q - p >= 3) {
-            // insertion sort of the run by idx (runs are short)
-            for (int i = p + 1; i < q; ++i) {
-                unsigned long long kk = sk[i];
-                double vv = sv[i];
-                int j = i - 1;
-                while (j >= p && sk[j] > kk) {
-                    sk[j + 1] = sk[j];
-                    sv[j + 1] = sv[j];
-                    --j;
+            // the run back into idx (stream) order: Shell sort with Ciura's
+            // gaps, so the long duplicate runs of power-law hubs (thousands of
+            // repeats of one pair) stay O(n^1.3) for the one thread that owns them
+            const int gaps[9] = {1750, 701, 301, 132, 57, 23, 10, 4, 1};
+            for (int gi = 0; gi < 9; ++gi) {
+                const int gap = gaps[gi];
+                if (gap >= q - p) continue;
+                for (int i = p + gap; i < q; ++i) {
+                    const unsigned long long kk = sk[i];
+                    const double vv = sv[i];
+                    int j = i;
+                    while (j - gap >= p && sk[j - gap] > kk) {
+                        sk[j] = sk[j - gap];
+                        sv[j] = sv[j - gap];
+                        j -= gap;
+                    }
+                    sk[j] = kk;
+                    sv[j] = vv;
                 }
-                sk[j + 1] = kk;
-                sv[j + 1] = vv;
             }
         }
         double acc = sv[p];
@@ -454,13 +461,25 @@ __device__ void row_lsd(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned *
         for (int i = threadIdx.x; i < L; i += blockDim.x) srcv[i] = 1.0;
         __syncthreads();
     }
-    const int passes = (a.colbits + 7) / 8;
+    // the full key (col << 32 | idx): idx digits first, then column digits,
+    // so equal-column runs leave in stream order (hub rows of power-law
+    // graphs carry runs of thousands of repeats; no per-run fix-up)
+    const int ipasses = (a.idxbits + 7) / 8;
+    const int passes = ipasses + (a.colbits + 7) / 8;
     for (int pass = 0; pass < passes; ++pass) {
-        const int shift = 32 + 8 * pass;
+        const int shift = pass < ipasses ? 8 * pass : 32 + 8 * (pass - ipasses);
         unsigned *h = hist + wid * 256;
         for (int d = lane; d < 256; d += 32) h[d] = 0;
         __syncthreads();
-        for (int i = a0 + lane; i < a1; i += 32) atomicAdd(&h[(unsigned)(src[i] >> shift) & 255u], 1u);
+        // warp-aggregated: a hub row's columns crowd a few digits, and one
+        // shared atomic per distinct digit per 32 entries avoids serialising
+        for (int b = a0; b < a1; b += 32) {
+            const int i = b + lane;
+            const bool v = i < a1;
+            const unsigned d = v ? ((unsigned)(src[i] >> shift) & 255u) : 256u + lane;
+            const unsigned peers = __match_any_sync(0xffffffffu, d);
+            if (v && lane == __ffs(peers) - 1) atomicAdd(&h[d], (unsigned)__popc(peers));
+        }
         __syncthreads();
         unsigned tot = 0;
         if (threadIdx.x < 256) {
@@ -498,7 +517,7 @@ __device__ void row_lsd(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned *
         srcv = dstv;
         dstv = tv;
     }
-    finish_row(a, sm, r, s0, L, src, srcv, true);
+    finish_row(a, sm, r, s0, L, src, srcv, false);
 }
 
 // tier S: one warp per row of <= 32 entries; rank sort by the full key
@@ -680,6 +699,16 @@ __device__ void row_medium(const RowsArgs &a, int64_t r, unsigned long long *wk,
     __syncwarp();
 }
 
+#ifdef GEE_TRACE
+__device__ unsigned long long g_rows_t[4096][3];
+__device__ unsigned g_rows_n;
+#define ROWS_TRACE_BEGIN() long long _t0 = clock64();
+#define ROWS_TRACE_END(tier, row) \
+    if (threadIdx.x == 0) { unsigned _i = atomicAdd(&g_rows_n, 1u); if (_i < 4096) { g_rows_t[_i][0] = tier; g_rows_t[_i][1] = row; g_rows_t[_i][2] = clock64() - _t0; } }
+#else
+#define ROWS_TRACE_BEGIN()
+#define ROWS_TRACE_END(tier, row)
+#endif
 __global__ void __launch_bounds__(kRowsThreads, 2) k_rows(RowsArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ RowsShared sm;
@@ -698,7 +727,9 @@ __global__ void __launch_bounds__(kRowsThreads, 2) k_rows(RowsArgs a) {
         int t = sm.task;
         __syncthreads();
         if (t >= n_x) break;
+        ROWS_TRACE_BEGIN();
         row_lsd(a, sm, lx[t], region2);
+        ROWS_TRACE_END(2, lx[t]);
     }
     for (;;) {
         if (threadIdx.x == 0) sm.task = (int)atomicAdd(&a.work[1], 1u);
@@ -714,7 +745,9 @@ __global__ void __launch_bounds__(kRowsThreads, 2) k_rows(RowsArgs a) {
         int t = sm.task;
         __syncthreads();
         if (t >= n_b) break;
+        ROWS_TRACE_BEGIN();
         row_bitonic(a, sm, lb[t], stk, stv);
+        ROWS_TRACE_END(1, lb[t]);
     }
     // phase M: one warp per row, warps grab rows independently
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -722,12 +755,15 @@ __global__ void __launch_bounds__(kRowsThreads, 2) k_rows(RowsArgs a) {
         const unsigned *lm = a.lists + (size_t)TIER_M * a.n_rows;
         unsigned long long *mk = stk + wid * kMCap;
         double *mv = stv + wid * kMCap;
+        // rows are grabbed kMChunk at a time: one counter shared by every
+        // warp of the grid would otherwise serialise 10^5 atomics
+        constexpr int kMChunk = 16;
         for (;;) {
             int t = 0;
-            if (lane == 0) t = (int)atomicAdd(&a.work[4], 1u);
+            if (lane == 0) t = (int)atomicAdd(&a.work[4], (unsigned)kMChunk);
             t = __shfl_sync(0xffffffffu, t, 0);
             if (t >= n_m) break;
-            row_medium(a, lm[t], mk, mv);
+            for (int u = t; u < min(n_m, t + kMChunk); ++u) row_medium(a, lm[u], mk, mv);
         }
     }
     // phase S: chunks of rows, one warp per row, rows > 32 skipped
@@ -939,6 +975,7 @@ int csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, i
         a.n_rows = n_rows;
         a.n_cols = n_cols;
         a.colbits = bit_length(n_cols > 1 ? n_cols - 1 : 1);
+        a.idxbits = bit_length(2 * E > 1 ? 2 * E - 1 : 1);
         a.key = W.key;
         a.val = W.val;
         a.key2 = W.key2;
@@ -998,4 +1035,12 @@ int csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, i
     return GEE_OK;
 }
 
+#ifdef GEE_TRACE
+extern "C" int gee_rows_dump(unsigned long long *out, unsigned *n) {
+    cudaMemcpyFromSymbol(n, g_rows_n, sizeof(unsigned));
+    unsigned z = 0;
+    cudaMemcpyToSymbol(g_rows_n, &z, sizeof(unsigned));
+    return cudaMemcpyFromSymbol(out, g_rows_t, sizeof(g_rows_t)) == cudaSuccess ? 0 : -1;
+}
+#endif
 }  // namespace gee
