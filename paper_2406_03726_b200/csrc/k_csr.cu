@@ -605,33 +605,107 @@ __device__ void row_small(const RowsArgs &a, int64_t r, unsigned long long *wk, 
 // full key (col << 32 | idx, so equal-column runs come out in stream order)
 // in a per-warp shared slice, then the warp sums runs, drops zeros, writes the
 // unique entries at the row's slot start and folds the degree.
+// ascending bitonic sort of 32*E keys held striped in registers (element
+// e*32 + lane in x[e]): partners across lanes by shuffles, within a lane by
+// register swaps; no shared memory, no barriers
+template <int E>
+__device__ __forceinline__ void warp_sort_u32(unsigned (&x)[E], int lane) {
+    constexpr int P = E * 32;
+#pragma unroll
+    for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int f = e ^ (j >> 5);
+                    if (f > e) {
+                        const bool asc = ((e * 32 + lane) & k) == 0;
+                        const unsigned lo = min(x[e], x[f]), hi = max(x[e], x[f]);
+                        x[e] = asc ? lo : hi;
+                        x[f] = asc ? hi : lo;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const unsigned y = __shfl_xor_sync(0xffffffffu, x[e], j);
+                    const bool asc = ((e * 32 + lane) & k) == 0;
+                    const bool lower = (lane & j) == 0;
+                    x[e] = (lower == asc) ? min(x[e], y) : max(x[e], y);
+                }
+            }
+        }
+    }
+}
+
+// sort the row by (col, bucket position) in registers, then gather the full
+// entries into the warp's shared slice in that order
+template <int E>
+__device__ __forceinline__ void row_medium_sort(const RowsArgs &a, int64_t s0, int L, unsigned long long *wk,
+                                                double *wv, int lane) {
+    unsigned x[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = e * 32 + lane;
+        x[e] = i < L ? ((unsigned)(a.key[s0 + i] >> 32) << 8) | (unsigned)i : 0xffffffffu;
+    }
+    warp_sort_u32<E>(x, lane);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = e * 32 + lane;
+        if (i < L) {
+            const int pos = (int)(x[e] & 255u);
+            wk[i] = a.key[s0 + pos];
+            wv[i] = bval(a, s0 + pos);
+        }
+    }
+}
+
+// tier M: one warp per row of kMCap or fewer entries.  Columns < 2^24: a
+// register bitonic sort of (col << 8 | position); equal-column runs of >= 3
+// are then put back into stream order (runs of 2 sum commutatively).
+// Otherwise a shared-memory bitonic sort of the full key (col << 32 | idx).
+// The warp then sums runs, drops zeros, writes the unique entries at the
+// row's slot start and folds the degree.
 __device__ void row_medium(const RowsArgs &a, int64_t r, unsigned long long *wk, double *wv) {
     const int lane = threadIdx.x & 31;
     const int64_t s0 = a.slot_ptr[r];
     const int L = (int)(a.slot_ptr[r + 1] - s0);
-    int P = 64;
-    while (P < L) P <<= 1;
-    for (int i = lane; i < P; i += 32) {
-        wk[i] = i < L ? a.key[s0 + i] : ~0ull;
-        wv[i] = i < L ? bval(a, s0 + i) : 0.0;
-    }
-    __syncwarp();
-    for (int k = 2; k <= P; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = lane; i < P; i += 32) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const unsigned long long x = wk[i], y = wk[ixj];
-                    if ((x > y) == ((i & k) == 0)) {
-                        wk[i] = y;
-                        wk[ixj] = x;
-                        const double t = wv[i];
-                        wv[i] = wv[ixj];
-                        wv[ixj] = t;
+    const bool regsort = a.colbits <= 24;
+    if (regsort) {
+        if (L <= 64)
+            row_medium_sort<2>(a, s0, L, wk, wv, lane);
+        else if (L <= 128)
+            row_medium_sort<4>(a, s0, L, wk, wv, lane);
+        else
+            row_medium_sort<8>(a, s0, L, wk, wv, lane);
+        __syncwarp();
+    } else {
+        int P = 64;
+        while (P < L) P <<= 1;
+        for (int i = lane; i < P; i += 32) {
+            wk[i] = i < L ? a.key[s0 + i] : ~0ull;
+            wv[i] = i < L ? bval(a, s0 + i) : 0.0;
+        }
+        __syncwarp();
+        for (int k = 2; k <= P; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = lane; i < P; i += 32) {
+                    const int ixj = i ^ j;
+                    if (ixj > i) {
+                        const unsigned long long x = wk[i], y = wk[ixj];
+                        if ((x > y) == ((i & k) == 0)) {
+                            wk[i] = y;
+                            wk[ixj] = x;
+                            const double t = wv[i];
+                            wv[i] = wv[ixj];
+                            wv[ixj] = t;
+                        }
                     }
                 }
+                __syncwarp();
             }
-            __syncwarp();
         }
     }
     const bool want_deg = a.deg_flags != 0;
@@ -647,8 +721,25 @@ __device__ void row_medium(const RowsArgs &a, int64_t r, unsigned long long *wk,
         const bool head = v && (i == 0 || (unsigned)(wk[i - 1] >> 32) != col);
         double acc = 0.0;
         if (head) {
+            int q = i + 1;
+            while (q < L && (unsigned)(wk[q] >> 32) == col) ++q;
+            if (regsort && q - i >= 3) {
+                // a run of repeats: back into stream (idx) order
+                for (int m = i + 1; m < q; ++m) {
+                    const unsigned long long kk = wk[m];
+                    const double vv = wv[m];
+                    int j = m - 1;
+                    while (j >= i && wk[j] > kk) {
+                        wk[j + 1] = wk[j];
+                        wv[j + 1] = wv[j];
+                        --j;
+                    }
+                    wk[j + 1] = kk;
+                    wv[j + 1] = vv;
+                }
+            }
             acc = wv[i];
-            for (int j = i + 1; j < L && (unsigned)(wk[j] >> 32) == col; ++j) acc += wv[j];  // stream order
+            for (int j = i + 1; j < q; ++j) acc += wv[j];  // stream order
         }
         const bool keep = head && acc != 0.0;
         const unsigned km = __ballot_sync(0xffffffffu, keep);
