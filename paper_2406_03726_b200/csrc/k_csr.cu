@@ -28,6 +28,9 @@
 #include "gee_common.cuh"
 
 namespace gee {
+#ifdef GEE_TRACE
+__device__ unsigned long long g_lsd_t[512][4];
+#endif
 
 int exclusive_scan_u32(const unsigned *in, int64_t n, int64_t *out, void *ws, cudaStream_t st);
 size_t scan_workspace(int64_t n);
@@ -277,7 +280,7 @@ __device__ __forceinline__ void store_degree(const RowsArgs &a, int64_t r, doubl
 // stream order, drops zeros, writes the unique entries at the row's slot
 // start, and folds the degree.  Whole CTA.
 __device__ void finish_row(const RowsArgs &a, RowsShared &sm, int64_t r, int64_t s0, int L,
-                           unsigned long long *sk, double *sv, bool fixup) {
+                           unsigned long long *sk, double *sv, bool fixup, int32_t *scol, double *sval) {
     const int tid = threadIdx.x, nt = blockDim.x;
     const int per = (L + nt - 1) / nt;
     const int p0 = min(L, tid * per), p1 = min(L, p0 + per);
@@ -285,8 +288,22 @@ __device__ void finish_row(const RowsArgs &a, RowsShared &sm, int64_t r, int64_t
     for (int p = p0; p < p1; ++p) {
         unsigned c = (unsigned)(sk[p] >> 32);
         if (p > 0 && (unsigned)(sk[p - 1] >> 32) == c) continue;
+        // run end: a short linear probe, then binary search (the keys are
+        // sorted by column), so a hub's run of thousands of repeats costs
+        // log2(L) dependent loads instead of one per repeat
         int q = p + 1;
-        while (q < L && (unsigned)(sk[q] >> 32) == c) ++q;
+        while (q < L && q < p + 8 && (unsigned)(sk[q] >> 32) == c) ++q;
+        if (q == p + 8 && q < L && (unsigned)(sk[q] >> 32) == c) {
+            int lo = q, hi = L;  // sk[lo] has column c; find the first index with a larger column
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if ((unsigned)(sk[mid] >> 32) == c)
+                    lo = mid;
+                else
+                    hi = mid;
+            }
+            q = hi;
+        }
         if (fixup && q - p >= 3) {
             // the run back into idx (stream) order: Shell sort with Ciura's
             // gaps, so the long duplicate runs of power-law hubs (thousands of
@@ -310,7 +327,8 @@ __device__ void finish_row(const RowsArgs &a, RowsShared &sm, int64_t r, int64_t
             }
         }
         double acc = sv[p];
-        for (int i = p + 1; i < q; ++i) acc += sv[i];
+#pragma unroll 8
+        for (int i = p + 1; i < q; ++i) acc += sv[i];  // stream order; loads run ahead of the adds
         sv[p] = acc;
         nkeep += acc != 0.0;
     }
@@ -351,20 +369,34 @@ __device__ void finish_row(const RowsArgs &a, RowsShared &sm, int64_t r, int64_t
         double d = block_sum(psum, sm.dred) + (insert ? 1.0 : 0.0);
         if (tid == 0) store_degree(a, r, d);
     } else {
-        __syncthreads();  // out_* writes of the CTA visible to thread 0
-        if (tid == 0) {
-            double d = 0.0;
-            bool ins = !insert;
-            for (unsigned i = 0; i < total; ++i) {
-                int64_t c = a.out_col[s0 + i];
-                double x = a.out_val[s0 + i];
-                if (!ins && c > r) {
-                    d += 1.0;
-                    ins = true;
-                }
-                if (diag && c == r) x = x + 1.0;
-                d += x;
+        // the sequential fold in column order (sparse.py:196): the CTA stages
+        // the row's output kCap entries at a time in shared memory (scol/sval,
+        // free once the outputs are written) so thread 0 folds from shared
+        // memory instead of one dependent global load per entry
+        double d = 0.0;
+        bool ins = !insert;
+        for (unsigned b = 0; b < total; b += kCap) {
+            const unsigned nb = min((unsigned)kCap, total - b);
+            __syncthreads();  // out_* writes visible; the previous chunk consumed
+            for (unsigned i = tid; i < nb; i += nt) {
+                scol[i] = a.out_col[s0 + b + i];
+                sval[i] = a.out_val[s0 + b + i];
             }
+            __syncthreads();
+            if (tid == 0) {
+                for (unsigned i = 0; i < nb; ++i) {
+                    const int64_t c = scol[i];
+                    double x = sval[i];
+                    if (!ins && c > r) {
+                        d += 1.0;
+                        ins = true;
+                    }
+                    if (diag && c == r) x = x + 1.0;
+                    d += x;
+                }
+            }
+        }
+        if (tid == 0) {
             if (!ins) d += 1.0;
             store_degree(a, r, d);
         }
@@ -405,7 +437,7 @@ __device__ void row_dense(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned
         sv[p] = bval(a, s0 + i);
     }
     __syncthreads();
-    finish_row(a, sm, r, s0, L, sk, sv, true);
+    finish_row(a, sm, r, s0, L, sk, sv, true, reinterpret_cast<int32_t *>(stk), stv);
 }
 
 // tier B: bitonic sort of (key, value) pairs padded to a power of two
@@ -444,12 +476,13 @@ __device__ void row_bitonic(const RowsArgs &a, RowsShared &sm, int64_t r, unsign
             __syncthreads();
         }
     }
-    finish_row(a, sm, r, s0, L, sk, sv, false);
+    finish_row(a, sm, r, s0, L, sk, sv, false, reinterpret_cast<int32_t *>(sk), sv);
 }
 
 // tier X: stable LSD radix (8-bit digits) over the column bits, one CTA per
 // row, ping-ponging between the bucket and the staging arrays.
-__device__ void row_lsd(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned *hist) {
+__device__ void row_lsd(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned *hist, unsigned long long *stk,
+                        double *stv) {
     const int64_t s0 = a.slot_ptr[r];
     const int L = (int)(a.slot_ptr[r + 1] - s0);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -466,6 +499,9 @@ __device__ void row_lsd(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned *
     // graphs carry runs of thousands of repeats; no per-run fix-up)
     const int ipasses = (a.idxbits + 7) / 8;
     const int passes = ipasses + (a.colbits + 7) / 8;
+#ifdef GEE_TRACE
+    const long long tl0 = clock64();
+#endif
     for (int pass = 0; pass < passes; ++pass) {
         const int shift = pass < ipasses ? 8 * pass : 32 + 8 * (pass - ipasses);
         unsigned *h = hist + wid * 256;
@@ -517,7 +553,18 @@ __device__ void row_lsd(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned *
         srcv = dstv;
         dstv = tv;
     }
-    finish_row(a, sm, r, s0, L, src, srcv, false);
+#ifdef GEE_TRACE
+    const long long tf0 = clock64();
+#endif
+    finish_row(a, sm, r, s0, L, src, srcv, false, reinterpret_cast<int32_t *>(stk), stv);
+#ifdef GEE_TRACE
+    if (threadIdx.x == 0 && blockIdx.x < 512 && L > (int)g_lsd_t[blockIdx.x][0]) {
+        g_lsd_t[blockIdx.x][0] = L;
+        g_lsd_t[blockIdx.x][1] = tf0 - tl0;
+        g_lsd_t[blockIdx.x][2] = clock64() - tf0;
+        g_lsd_t[blockIdx.x][3] = r;
+    }
+#endif
 }
 
 // tier S: one warp per row of <= 32 entries; rank sort by the full key
@@ -791,6 +838,7 @@ __device__ void row_medium(const RowsArgs &a, int64_t r, unsigned long long *wk,
 }
 
 #ifdef GEE_TRACE
+__device__ unsigned long long g_phase_t[512][6];
 __device__ unsigned long long g_rows_t[4096][3];
 __device__ unsigned g_rows_n;
 #define ROWS_TRACE_BEGIN() long long _t0 = clock64();
@@ -811,6 +859,12 @@ __global__ void __launch_bounds__(kRowsThreads, 2) k_rows(RowsArgs a) {
     const unsigned *lx = a.lists + (size_t)TIER_X * a.n_rows;
     const unsigned *ld = a.lists + (size_t)TIER_D * a.n_rows;
     const unsigned *lb = a.lists + (size_t)TIER_B * a.n_rows;
+#ifdef GEE_TRACE
+    if (threadIdx.x == 0 && blockIdx.x < 512) g_phase_t[blockIdx.x][0] = clock64();
+#define PHASE_MARK(k) if (threadIdx.x == 0 && blockIdx.x < 512) g_phase_t[blockIdx.x][k] = clock64();
+#else
+#define PHASE_MARK(k)
+#endif
     // phase X: hub rows first (longest critical path)
     for (;;) {
         if (threadIdx.x == 0) sm.task = (int)atomicAdd(&a.work[0], 1u);
@@ -819,9 +873,10 @@ __global__ void __launch_bounds__(kRowsThreads, 2) k_rows(RowsArgs a) {
         __syncthreads();
         if (t >= n_x) break;
         ROWS_TRACE_BEGIN();
-        row_lsd(a, sm, lx[t], region2);
+        row_lsd(a, sm, lx[t], region2, stk, stv);
         ROWS_TRACE_END(2, lx[t]);
     }
+    PHASE_MARK(1);
     for (;;) {
         if (threadIdx.x == 0) sm.task = (int)atomicAdd(&a.work[1], 1u);
         __syncthreads();
@@ -840,6 +895,7 @@ __global__ void __launch_bounds__(kRowsThreads, 2) k_rows(RowsArgs a) {
         row_bitonic(a, sm, lb[t], stk, stv);
         ROWS_TRACE_END(1, lb[t]);
     }
+    PHASE_MARK(2);
     // phase M: one warp per row, warps grab rows independently
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     {
@@ -857,6 +913,8 @@ __global__ void __launch_bounds__(kRowsThreads, 2) k_rows(RowsArgs a) {
             for (int u = t; u < min(n_m, t + kMChunk); ++u) row_medium(a, lm[u], mk, mv);
         }
     }
+    __syncthreads();
+    PHASE_MARK(3);
     // phase S: chunks of rows, one warp per row, rows > 32 skipped
     unsigned long long *wk = stk + wid * 32;
     double *wv = stv + wid * 32;
@@ -881,6 +939,7 @@ __global__ void __launch_bounds__(kRowsThreads, 2) k_rows(RowsArgs a) {
             row_small(a, r, wk, wv);
         }
     }
+    PHASE_MARK(4);
     (void)lane;
 }
 
@@ -1127,6 +1186,12 @@ int csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, i
 }
 
 #ifdef GEE_TRACE
+extern "C" int gee_lsd_dump(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_lsd_t, sizeof(g_lsd_t)) == cudaSuccess ? 0 : -1;
+}
+extern "C" int gee_phase_dump(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_phase_t, sizeof(g_phase_t)) == cudaSuccess ? 0 : -1;
+}
 extern "C" int gee_rows_dump(unsigned long long *out, unsigned *n) {
     cudaMemcpyFromSymbol(n, g_rows_n, sizeof(unsigned));
     unsigned z = 0;

@@ -25,3 +25,15 @@ print("tasks", n.value)
 o = np.argsort(-t[:, 2].astype(np.int64))
 for i in o[:12]:
     print("tier", t[i, 0], "row", t[i, 1], "cycles", t[i, 2])
+buf2 = (ctypes.c_ulonglong * (512 * 6))()
+lib.gee_phase_dump(buf2)
+ph = np.array(buf2, dtype=np.int64).reshape(512, 6)[:296]
+d = np.diff(ph[:, :5], axis=1)
+print("per-CTA phase cycles (X, D+B, M, S): mean", d.mean(axis=0).astype(int), "max", d.max(axis=0))
+print("CTA total max", (ph[:, 4] - ph[:, 0]).max(), "argmax", (ph[:, 4] - ph[:, 0]).argmax())
+buf3 = (ctypes.c_ulonglong * (512 * 4))()
+lib.gee_lsd_dump(buf3)
+ls = np.array(buf3, dtype=np.int64).reshape(512, 4)[:296]
+o = np.argsort(-(ls[:, 1] + ls[:, 2]))
+for i in o[:6]:
+    print("CTA", i, "row", ls[i, 3], "L", ls[i, 0], "lsd cycles", ls[i, 1], "finish cycles", ls[i, 2])
