@@ -508,13 +508,21 @@ __device__ void row_lsd(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned *
         for (int d = lane; d < 256; d += 32) h[d] = 0;
         __syncthreads();
         // warp-aggregated: a hub row's columns crowd a few digits, and one
-        // shared atomic per distinct digit per 32 entries avoids serialising
-        for (int b = a0; b < a1; b += 32) {
-            const int i = b + lane;
-            const bool v = i < a1;
-            const unsigned d = v ? ((unsigned)(src[i] >> shift) & 255u) : 256u + lane;
-            const unsigned peers = __match_any_sync(0xffffffffu, d);
-            if (v && lane == __ffs(peers) - 1) atomicAdd(&h[d], (unsigned)__popc(peers));
+        // shared atomic per distinct digit per 32 entries avoids serialising;
+        // kLU chunks of keys are loaded before any is used (latency overlap)
+        constexpr int kLU = 4;
+        for (int b = a0; b < a1; b += 32 * kLU) {
+            unsigned dd[kLU];
+#pragma unroll
+            for (int u = 0; u < kLU; ++u) {
+                const int i = b + u * 32 + lane;
+                dd[u] = i < a1 ? ((unsigned)(src[i] >> shift) & 255u) : 256u + lane;
+            }
+#pragma unroll
+            for (int u = 0; u < kLU; ++u) {
+                const unsigned peers = __match_any_sync(0xffffffffu, dd[u]);
+                if (dd[u] < 256u && lane == __ffs(peers) - 1) atomicAdd(&h[dd[u]], (unsigned)__popc(peers));
+            }
         }
         __syncthreads();
         unsigned tot = 0;
@@ -529,21 +537,29 @@ __device__ void row_lsd(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned *
         if (threadIdx.x < 256)
             for (int w = 0; w < nw; ++w) hist[w * 256 + threadIdx.x] += base;
         __syncthreads();
-        for (int b = a0; b < a1; b += 32) {
-            int i = b + lane;
-            bool v = i < a1;
-            unsigned long long k = v ? src[i] : 0ull;
-            double x = v ? srcv[i] : 0.0;
-            unsigned d = v ? ((unsigned)(k >> shift) & 255u) : 256u + lane;
-            unsigned peers = __match_any_sync(0xffffffffu, d);
-            unsigned pos = v ? h[d] + __popc(peers & lanemask_lt()) : 0u;
-            __syncwarp();
-            if (v) {
-                dst[pos] = k;
-                dstv[pos] = x;
-                if (lane == __ffs(peers) - 1) h[d] += __popc(peers);
+        for (int b = a0; b < a1; b += 32 * kLU) {
+            unsigned long long kk[kLU];
+            double xx[kLU];
+#pragma unroll
+            for (int u = 0; u < kLU; ++u) {
+                const int i = b + u * 32 + lane;
+                kk[u] = i < a1 ? src[i] : 0ull;
+                xx[u] = i < a1 ? srcv[i] : 0.0;
             }
-            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < kLU; ++u) {
+                const bool v = b + u * 32 + lane < a1;
+                const unsigned d = v ? ((unsigned)(kk[u] >> shift) & 255u) : 256u + lane;
+                const unsigned peers = __match_any_sync(0xffffffffu, d);
+                const unsigned pos = v ? h[d] + __popc(peers & lanemask_lt()) : 0u;
+                __syncwarp();
+                if (v) {
+                    dst[pos] = kk[u];
+                    dstv[pos] = xx[u];
+                    if (lane == __ffs(peers) - 1) h[d] += __popc(peers);
+                }
+                __syncwarp();
+            }
         }
         __syncthreads();
         unsigned long long *t = src;
