@@ -247,6 +247,9 @@ struct RowsArgs {
     unsigned long long *key2;  // global staging / LSD ping-pong
     double *val2;
     int unit;  // unit weights: bucket values are implicit 1.0 and never stored
+    const void *w;  // the input weights (tier B gathers values by stream index)
+    int wt;
+    int64_t E;
     int32_t *out_col;  // unique entries at slot positions
     double *out_val;
     unsigned *ucnt;
@@ -441,41 +444,98 @@ __device__ void row_dense(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned
 }
 
 // tier B: bitonic sort of (key, value) pairs padded to a power of two
+// weight of stream entry idx (idx < E: original edge idx, else its reverse)
+__device__ __forceinline__ double stream_w(const RowsArgs &a, unsigned long long idx) {
+    if (a.wt == GEE_W_UNIT) return 1.0;
+    const int64_t e = (int64_t)idx < a.E ? (int64_t)idx : (int64_t)idx - a.E;
+    return load_w(a.w, a.wt, e);
+}
+
+// tier B: bitonic sort of the full keys (col << 32 | idx) of a row of
+// 257..kCap entries, E = P/512 keys per thread in registers: partners within
+// a thread are register swaps, within a warp shuffles, across warps one
+// shared-memory exchange per stage.  Values are gathered after the sort from
+// the weight array by stream index.
+template <int E>
+__device__ __forceinline__ void block_bitonic_keys(unsigned long long (&x)[E], unsigned long long *sk, int tid,
+                                                   int lane) {
+    constexpr int P = E * kRowsThreads;
+#pragma unroll 1
+    for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll 1
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= kRowsThreads) {
+                // partner in the same thread: element e ^ (j / 512), static indices
+#pragma unroll
+                for (int jj = 1; jj < E; jj <<= 1) {
+                    if (j != jj * kRowsThreads) continue;
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const int f = e ^ jj;
+                        if (f > e) {
+                            const bool asc = ((e * kRowsThreads + tid) & k) == 0;
+                            const unsigned long long lo = min(x[e], x[f]), hi = max(x[e], x[f]);
+                            x[e] = asc ? lo : hi;
+                            x[f] = asc ? hi : lo;
+                        }
+                    }
+                }
+            } else if (j >= 32) {
+                __syncthreads();  // previous readers of sk are done
+#pragma unroll
+                for (int e = 0; e < E; ++e) sk[e * kRowsThreads + tid] = x[e];
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int i = e * kRowsThreads + tid;
+                    const unsigned long long y = sk[i ^ j];
+                    const bool asc = (i & k) == 0, lower = (i & j) == 0;
+                    x[e] = (lower == asc) ? min(x[e], y) : max(x[e], y);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int i = e * kRowsThreads + tid;
+                    const unsigned long long y = __shfl_xor_sync(0xffffffffu, x[e], j);
+                    const bool asc = (i & k) == 0, lower = (i & j) == 0;
+                    x[e] = (lower == asc) ? min(x[e], y) : max(x[e], y);
+                }
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) sk[e * kRowsThreads + threadIdx.x] = x[e];
+    __syncthreads();
+}
+
+template <int E>
+__device__ __forceinline__ void row_bitonic_e(const RowsArgs &a, int64_t s0, int L, unsigned long long *sk,
+                                              double *sv) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    unsigned long long x[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = e * kRowsThreads + tid;
+        x[e] = i < L ? a.key[s0 + i] : ~0ull;
+    }
+    block_bitonic_keys<E>(x, sk, tid, lane);
+    for (int i = tid; i < L; i += kRowsThreads) sv[i] = stream_w(a, sk[i] & 0xffffffffull);
+    __syncthreads();
+}
+
 __device__ void row_bitonic(const RowsArgs &a, RowsShared &sm, int64_t r, unsigned long long *sk,
                             double *sv) {
     const int64_t s0 = a.slot_ptr[r];
     const int L = (int)(a.slot_ptr[r + 1] - s0);
-    int P = 64;
-    while (P < L) P <<= 1;
-    for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        if (i < L) {
-            sk[i] = a.key[s0 + i];
-            sv[i] = bval(a, s0 + i);
-        } else {
-            sk[i] = ~0ull;
-            sv[i] = 0.0;
-        }
-    }
-    __syncthreads();
-    for (int k = 2; k <= P; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < P; i += blockDim.x) {
-                int ixj = i ^ j;
-                if (ixj > i) {
-                    unsigned long long x = sk[i], y = sk[ixj];
-                    bool asc = (i & k) == 0;
-                    if ((x > y) == asc) {
-                        sk[i] = y;
-                        sk[ixj] = x;
-                        double t = sv[i];
-                        sv[i] = sv[ixj];
-                        sv[ixj] = t;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
+    if (L <= kRowsThreads)
+        row_bitonic_e<1>(a, s0, L, sk, sv);
+    else if (L <= 2 * kRowsThreads)
+        row_bitonic_e<2>(a, s0, L, sk, sv);
+    else if (L <= 4 * kRowsThreads)
+        row_bitonic_e<4>(a, s0, L, sk, sv);
+    else
+        row_bitonic_e<8>(a, s0, L, sk, sv);
     finish_row(a, sm, r, s0, L, sk, sv, false, reinterpret_cast<int32_t *>(sk), sv);
 }
 
@@ -1147,6 +1207,9 @@ int csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, i
         a.key2 = W.key2;
         a.val2 = W.val2;
         a.unit = wt == GEE_W_UNIT;
+        a.w = w;
+        a.wt = wt;
+        a.E = E;
         a.out_col = col;
         a.out_val = val;
         a.ucnt = compact ? W.ucnt : row_cnt;
