@@ -159,6 +159,31 @@ int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, in
                      int32_t k, unsigned flags, double *z, void *ws, size_t ws_bytes,
                      int32_t *err, void *stream);
 
+/* Row shard of a unit-weight graph (multi-GPU, dist.py; replaces the
+ * per-shard share of encode() embedding.py:110-131 for graphs of at most
+ * 16384 nodes and k <= 8).  The shard owns rows [row_begin, row_end); rows /
+ * cols hold its e_local entries of the SYMMETRISED stream (both directions
+ * of every off-diagonal undirected edge, global node ids), labels all
+ * n_nodes labels (replicated).  Two phases on the same workspace:
+ *   gee_bitmap_shard_degrees -> deg_local uint32[row_end - row_begin], the
+ *     stream length (unit-weight degree, without the A+I 1) of each local row;
+ *   the caller all-gathers them into deg_all uint32[n_nodes] (only needed
+ *     under GEE_LAPLACIAN; may be NULL otherwise);
+ *   gee_bitmap_shard_encode -> z_local f64[(row_end - row_begin) x k].
+ * Every encode must follow its own degrees call (the first clears the
+ * workspace's counters).  Entries whose row is outside the shard set
+ * GEE_ERR_EDGE_RANGE and are dropped. */
+int gee_bitmap_shard_workspace(int64_t e_local, int64_t n_nodes, int64_t row_begin, int64_t row_end,
+                               int32_t k, size_t *ws_bytes);
+int gee_bitmap_shard_degrees(const int64_t *rows, const int64_t *cols, int64_t e_local,
+                             int64_t n_nodes, int64_t row_begin, int64_t row_end,
+                             const int64_t *labels, int32_t k, unsigned flags, uint32_t *deg_local,
+                             void *ws, size_t ws_bytes, int32_t *err, void *stream);
+int gee_bitmap_shard_encode(const int64_t *rows, const int64_t *cols, int64_t e_local,
+                            int64_t n_nodes, int64_t row_begin, int64_t row_end, int32_t k,
+                            unsigned flags, const uint32_t *deg_all, double *z_local, void *ws,
+                            size_t ws_bytes, int32_t *err, void *stream);
+
 /* Launch statistics: number of kernels this thread launched through the
  * library since the last reset (for bench.py's gpu_launches). */
 uint64_t gee_launch_count(void);

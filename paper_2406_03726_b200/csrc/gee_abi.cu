@@ -95,6 +95,14 @@ int bitmap_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n
                   cudaStream_t st);
 int validate_edges(const int64_t *, const int64_t *, const void *, int, int64_t, int64_t, int32_t *,
                    cudaStream_t);
+size_t bitmap_shard_workspace(int64_t n, int64_t nloc, int k);
+int bitmap_shard_degrees(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n, int64_t row0, int64_t nloc,
+                         const int64_t *labels, int k, unsigned flags, unsigned *deg_local, void *ws,
+                         size_t ws_bytes, int32_t *err, cudaStream_t st);
+int bitmap_shard_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n, int64_t row0, int64_t nloc,
+                        int k, unsigned flags, const unsigned *deg_all, double *z_local, void *ws, size_t ws_bytes,
+                        int32_t *err, cudaStream_t st);
+int bitmap_max_nodes();
 
 static bool index_ok(int64_t x) { return x >= 0 && x < ((int64_t)1 << 31); }
 static bool wt_ok(int wt, const void *w, int64_t n_edges) {
@@ -287,6 +295,40 @@ int gee_embed(const int64_t *row_ptr, const uint32_t *row_cnt, const int32_t *co
     if ((flags & GEE_LAPLACIAN) && !scale) return GEE_E_ARG;
     return embed(row_ptr, row_cnt, col, val, nullptr, nullptr, row_begin, row_end, n_cols, y32, inv_nk, scale, k,
                  flags, z, ldz, ws, ws_bytes, err, (cudaStream_t)stream);
+}
+
+// row shard of a unit-weight graph on the bitmap path
+static bool bm_shard_ok(int64_t e_local, int64_t n, int64_t rb, int64_t re, int32_t k) {
+    return index_ok(e_local) && n >= 1 && n <= bitmap_max_nodes() && rb >= 0 && rb <= re && re <= n && k >= 1 &&
+           k <= 8;
+}
+
+int gee_bitmap_shard_workspace(int64_t e_local, int64_t n_nodes, int64_t row_begin, int64_t row_end, int32_t k,
+                               size_t *ws_bytes) {
+    if (!ws_bytes || !bm_shard_ok(e_local, n_nodes, row_begin, row_end, k)) return GEE_E_ARG;
+    *ws_bytes = bitmap_shard_workspace(n_nodes, row_end - row_begin, k);
+    return GEE_OK;
+}
+
+int gee_bitmap_shard_degrees(const int64_t *rows, const int64_t *cols, int64_t e_local, int64_t n_nodes,
+                             int64_t row_begin, int64_t row_end, const int64_t *labels, int32_t k, unsigned flags,
+                             uint32_t *deg_local, void *ws, size_t ws_bytes, int32_t *err, void *stream) {
+    if (!bm_shard_ok(e_local, n_nodes, row_begin, row_end, k) || !labels || !err) return GEE_E_ARG;
+    if ((e_local && (!rows || !cols)) || (row_end > row_begin && !deg_local)) return GEE_E_ARG;
+    if (!ws) return GEE_E_WORKSPACE;
+    return bitmap_shard_degrees(rows, cols, e_local, n_nodes, row_begin, row_end - row_begin, labels, k, flags,
+                                deg_local, ws, ws_bytes, err, (cudaStream_t)stream);
+}
+
+int gee_bitmap_shard_encode(const int64_t *rows, const int64_t *cols, int64_t e_local, int64_t n_nodes,
+                            int64_t row_begin, int64_t row_end, int32_t k, unsigned flags, const uint32_t *deg_all,
+                            double *z_local, void *ws, size_t ws_bytes, int32_t *err, void *stream) {
+    if (!bm_shard_ok(e_local, n_nodes, row_begin, row_end, k) || !err) return GEE_E_ARG;
+    if ((e_local && (!rows || !cols)) || (row_end > row_begin && !z_local)) return GEE_E_ARG;
+    if ((flags & GEE_LAPLACIAN) && !deg_all) return GEE_E_ARG;
+    if (!ws) return GEE_E_WORKSPACE;
+    return bitmap_shard_encode(rows, cols, e_local, n_nodes, row_begin, row_end - row_begin, k, flags, deg_all,
+                               z_local, ws, ws_bytes, err, (cudaStream_t)stream);
 }
 
 int gee_encode_edges_workspace(int64_t n_edges, int64_t n_nodes, int32_t k, int directed, int w_type,

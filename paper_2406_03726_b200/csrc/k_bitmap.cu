@@ -41,6 +41,8 @@
 // lengths by atomics, the node table and, for rows with repeats, per-class
 // sums of g = s_c/n_q over every stream entry, in grid-wide phases (all CTAs
 // are co-resident: cooperative launch); those rows take their sums from there.
+#include <algorithm>
+
 #include "gee_common.cuh"
 
 namespace gee {
@@ -56,19 +58,28 @@ constexpr int kTK = 256;        // GEMM columns per K step (two 128-byte swizzle
 
 struct BmArgs {
     int n, Wp, Np;            // nodes, bitmap words per row (multiple of 8), Wp*32
+    // Rows held here: [row0, row0 + nloc), bitmap rows Nlp (a multiple of
+    // 128).  The single-GPU encode holds every row (row0 = 0, nloc = n,
+    // Nlp = Np); a row shard (multi-GPU, bitmap_shard_*) holds its range
+    // and reads the degrees of every node from deg_all.  ucnt, len, zacc, z
+    // and the bitmap are indexed by local row r - row0; labels, the node
+    // table and X^T by global node.
+    int row0, nloc, Nlp;
+    int shard;
+    const unsigned *deg_all;  // [n] shard encode: stream lengths of every row (NULL without Laplacian)
     int64_t E;
     int directed;
     unsigned *bm;             // [Np][Wp]
-    unsigned *ucnt;           // [n] distinct columns per row
-    unsigned *len;            // [n] stream lengths (rare path)
+    unsigned *ucnt;           // [nloc] distinct columns per row
+    unsigned *len;            // [nloc] stream lengths (rare path)
     unsigned *cnt;            // [kKMax] class histogram
-    unsigned *mdone;          // [Np/128] K steps accumulated per GEMM row tile
+    unsigned *mdone;          // [Nlp/128] K steps accumulated per GEMM row tile
     unsigned *flags;          // [0] pair in both directions, [1] rare-path barrier, [3] table barrier
     unsigned *upop;           // [kPopParts * 32] popc(U) partial sums, 128 B apart
     unsigned char *xt;        // [NB][Np] X^T digits (K-major B operand)
     int nbx;                  // NB: X columns (kDig * K padded to 16/32/64)
     int32_t *cpart;           // [grid][2][128][NB] stream-K partial sums (slab per CTA segment)
-    double *zacc;             // [n][kKMax] rare path class sums
+    double *zacc;             // [nloc][kKMax] rare path class sums
     const int64_t *labels;
     int32_t *y32;
     int64_t *counts;
@@ -240,6 +251,26 @@ __global__ void __launch_bounds__(kSetThreads) k_bm_set(const int64_t *__restric
             if (e + 1 < E) r1 = (unsigned)rows[e + 1], c1 = (unsigned)cols[e + 1];
         }
     };
+    // global row -> local bitmap row; an entry outside this bitmap's rows or
+    // columns is an edge-range error, dropped (EdgeList validates first)
+    auto localise = [&](unsigned &r0, unsigned &r1, unsigned &c0, unsigned &c1) {
+        const unsigned nl = (unsigned)a.nloc, nc = (unsigned)a.n;
+        if (r0 != INV) {
+            r0 -= (unsigned)a.row0;
+            if (r0 >= nl || c0 >= nc) {
+                raise_err(a.err, GEE_ERR_EDGE_RANGE);
+                r0 = INV;
+            }
+        }
+        if (r1 != INV) {
+            r1 -= (unsigned)a.row0;
+            if (r1 >= nl || c1 >= nc) {
+                raise_err(a.err, GEE_ERR_EDGE_RANGE);
+                r1 = INV;
+            }
+        }
+        if (r0 == INV) r0 = r1, c0 = c1, r1 = INV;  // an empty first slot only ends the list
+    };
     int64_t base = (int64_t)blockIdx.x * blockDim.x * 2;
     unsigned r0, r1, c0, c1;
     fetch(base + threadIdx.x * 2, r0, r1, c0, c1);
@@ -247,6 +278,7 @@ __global__ void __launch_bounds__(kSetThreads) k_bm_set(const int64_t *__restric
     for (; base < E; base += stride) {
         unsigned nr0, nr1, nc0, nc1;
         fetch(base + stride + threadIdx.x * 2, nr0, nr1, nc0, nc1);
+        localise(r0, r1, c0, c1);
         const unsigned k0 = r0 != INV ? bm_index(a, r0, c0 >> 5) : INV;
         const unsigned k1 = r1 != INV ? bm_index(a, r1, c1 >> 5) : INV;
         const unsigned b0 = r0 != INV ? 1u << (c0 & 31) : 0u;
@@ -354,7 +386,11 @@ __global__ void __launch_bounds__(256) k_bm_table(BmArgs a) {
     pdl_wait();
     pdl_trigger();  // k_bm_gemm may start now: it waits for this grid before reading the table
     if (blockIdx.x == 0) write_counts(a, threadIdx.x);
-    if (r < a.n) node_entry(a, r, __ldcg(a.ucnt + r));
+    if (r < a.n) {
+        // a shard without the Laplacian needs no degrees (s_r = 1)
+        const unsigned L = !a.shard ? __ldcg(a.ucnt + r) : a.deg_all ? __ldcg(a.deg_all + r) : 0u;
+        node_entry(a, r, L);
+    }
 }
 
 // directed lists: one warp per row, 8 rows per CTA
@@ -362,7 +398,7 @@ __global__ void __launch_bounds__(256) k_bm_scan(BmArgs a) {
     const int lane = threadIdx.x & 31;
     const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
     pdl_wait();
-    if (r >= a.n) return;
+    if (r >= a.nloc) return;
     unsigned u = 0;
     for (int i = lane; i < a.Wp / 4; i += 32) {
         const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(a.bm + bm_index(a, r, 4 * i)));
@@ -373,6 +409,44 @@ __global__ void __launch_bounds__(256) k_bm_scan(BmArgs a) {
         a.ucnt[r] = u;
         if (u) atomicAdd(a.upop + (blockIdx.x % kPopParts) * 32, u);  // popc(U): S = U for directed lists
     }
+}
+
+// Does some pair repeat in the stream?  popc(U) = E exactly when none does
+// (undirected lists: and no pair is present in both directions).  Every
+// thread of the CTA gets the answer.
+__device__ __forceinline__ bool block_repeats(const BmArgs &a) {
+    __shared__ unsigned s_rep;
+    if (threadIdx.x < 32) {
+        unsigned long long tot = 0;
+        for (int i = threadIdx.x; i < kPopParts; i += 32) tot += __ldcg(a.upop + i * 32);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (threadIdx.x == 0) s_rep = __ldcg(a.flags) != 0 || (int64_t)tot != a.E;
+    }
+    __syncthreads();
+    return s_rep != 0;
+}
+
+// Row shard, after k_bm_scan: when some pair repeats, the exact stream
+// lengths of the local rows (their degrees) and zeroed class sums.
+__global__ void __launch_bounds__(256) k_bm_len(const int64_t *__restrict__ rows, BmArgs a) {
+    pdl_wait();
+    if (!block_repeats(a)) return;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = tid; i < (int64_t)a.nloc * kKMax; i += nth) a.zacc[i] = 0.0;
+    for (int64_t e = tid; e < a.E; e += nth) {
+        const unsigned r = (unsigned)rows[e] - (unsigned)a.row0;
+        if (r < (unsigned)a.nloc) atomicAdd(&a.len[r], 1u);
+    }
+}
+
+// Row shard: the local rows' degrees (stream lengths) for the all-gather
+__global__ void __launch_bounds__(256) k_bm_deg(BmArgs a, unsigned *__restrict__ deg_local) {
+    pdl_wait();
+    const bool rep = block_repeats(a);
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < a.nloc) deg_local[r] = rep ? __ldcg(a.len + r) : __ldcg(a.ucnt + r);
 }
 
 // ---------------------------------------------------------------------------
@@ -392,6 +466,20 @@ __device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned target) {
 __device__ void repeat_phases(const int64_t *__restrict__ rows, const int64_t *__restrict__ cols, const BmArgs &a) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    if (a.shard) {
+        // a row shard's lengths, zeroed sums (k_bm_len) and node table (from
+        // the all-gathered degrees) are ready: only the class sums of the
+        // local rows with repeats, over the local (directed) stream
+        for (int64_t e = tid; e < a.E; e += nth) {
+            const unsigned r = (unsigned)rows[e] - (unsigned)a.row0, c = (unsigned)cols[e];
+            if (r < (unsigned)a.nloc && __ldcg(a.len + r) != __ldcg(a.ucnt + r)) {
+                const int lab = __ldcg(a.tab_lab + c);
+                if (lab >= 0) atomicAdd(&a.zacc[(size_t)r * kKMax + lab], __ldcg(a.tab_g + c));
+            }
+        }
+        grid_barrier(a.flags + 1, gridDim.x);
+        return;
+    }
     const bool und = !a.directed;
     // 1: exact stream lengths
     for (int64_t i = tid; i < (int64_t)a.n * kKMax; i += nth) a.zacc[i] = 0.0;
@@ -700,20 +788,7 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
     if (t == 0) TRACE(7, 0);
     // Launched while k_bm_table runs (PDL): k_bm_sym's outputs (bitmap, counts,
     // flags) are complete, the node table is not until pdl_wait().
-    bool rep;
-    {
-        // popc(U) = E exactly when no pair repeats in the list
-        __shared__ unsigned s_rep;
-        if (t < 32) {
-            unsigned long long tot = 0;
-            for (int i = t; i < kPopParts; i += 32) tot += __ldcg(a.upop + i * 32);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-            if (t == 0) s_rep = __ldcg(a.flags) != 0 || (int64_t)tot != a.E;
-        }
-        __syncthreads();
-        rep = s_rep != 0;
-    }
+    const bool rep = block_repeats(a);
     if (rep) {
         pdl_wait();
         repeat_phases(rows, cols, a);
@@ -747,7 +822,7 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
     if (t == 0) TRACE(7, 2);
 
     const int KT = a.Np / kTK;
-    const int64_t total = (int64_t)(a.Np / kTM) * KT;
+    const int64_t total = (int64_t)(a.Nlp / kTM) * KT;
     const int s0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
     const int s1 = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
     const int nsteps = s1 - s0;
@@ -849,10 +924,11 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
             const int g = s0 + i, m = g / KT;
             const int seglen = min(nsteps - i, KT - g % KT);
             const int buf = seg & 1;
-            const int r = m * kTM + e * 32 + lane;
+            const int r = m * kTM + e * 32 + lane;  // local row
+            const bool live = r < a.nloc;
             // the row's epilogue inputs, loaded while the MMAs run
-            const int rlab = r < a.n ? __ldcg(a.y32 + r) : -1;
-            const double rsc = (lap && r < a.n) ? __ldcg(a.scale + r) : 1.0;
+            const int rlab = live ? __ldcg(a.y32 + a.row0 + r) : -1;
+            const double rsc = (lap && live) ? __ldcg(a.scale + a.row0 + r) : 1.0;
             mbar_wait_idle(smem_u32(accfull + buf), (seg >> 1) & 1, 256);
             if (e == 0 && lane == 0) TRACE(9, seg);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -893,7 +969,7 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
                 __threadfence();
                 epi_bar();
                 if (e == 0 && lane == 0) atomicAdd(&a.mdone[m], 1u);
-            } else if (seglen < KT && r < a.n) {
+            } else if (seglen < KT && live) {
                 // partners: participating CTAs other than this one
                 unsigned b = lo * G / T;
                 while (b > 0 && b * T / G > lo) --b;
@@ -917,7 +993,7 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
                     }
                 }
             }
-            if (fin && r < a.n) {
+            if (fin && live) {
                 if (e == 0 && lane == 0) TRACE(9, 19 + 8 * seg);
                 const bool rrep = rep && __ldcg(a.len + r) != __ldcg(a.ucnt + r);
                 gemm_epilogue<NB>(a, r, C, rrep, inv, rsc, rlab);
@@ -939,6 +1015,8 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
 // ---------------------------------------------------------------------------
 int force_path();
 
+int bitmap_max_nodes() { return kBmMax; }
+
 // unit weights, square, at most kBmMax nodes, K <= 8
 bool bitmap_path_ok(int wt, int64_t E, int64_t n_rows, int64_t n_cols, int directed, int k) {
     if (force_path() != 0) return false;  // test hook: exercise the general paths
@@ -958,34 +1036,51 @@ struct BmWs {
     int32_t *cacc;
     double *zacc, *tab_g;
     signed char *tab_lab;
-    int Wp, Np, nbx;
+    int Wp, Np, Nlp, nbx;
     size_t clear_bytes;
+    // row shards only: the label outputs and node tables of every node
+    int32_t *y32;
+    int64_t *counts;
+    double *inv, *deg, *scale;
 };
 
-static void carve_bm(Carver &cv, BmWs &w, int64_t n, int k) {
+// nloc rows of an n-node graph (the single-GPU encode: nloc = n)
+static void carve_bm(Carver &cv, BmWs &w, int64_t n, int64_t nloc, int k, bool shard) {
     const int64_t np = (n + kBlk - 1) / kBlk * kBlk;
+    const int64_t nlp = shard ? std::max<int64_t>(kTM, (nloc + kTM - 1) / kTM * kTM) : np;
     w.Wp = (int)(np / 32);
     w.Np = (int)np;
+    w.Nlp = (int)nlp;
     w.nbx = nb_cols(k);
     // bitmap, counters, flags and X^T are contiguous: one memset clears them
-    const size_t bmw = (size_t)np * w.Wp;
+    const size_t bmw = (size_t)nlp * w.Wp;
     const size_t words =
-        (bmw + 2 * (size_t)n + kKMax + (size_t)(np / kTM) + 4 + 32 * kPopParts + 3) & ~size_t(3);
+        (bmw + 2 * (size_t)nloc + kKMax + (size_t)(nlp / kTM) + 4 + 32 * kPopParts + 3) & ~size_t(3);
     const size_t xbytes = (size_t)w.nbx * (size_t)np;
     w.clear_bytes = 4 * words + xbytes;
     unsigned char *base = cv.take<unsigned char>(w.clear_bytes);
     w.bm = reinterpret_cast<unsigned *>(base);
     w.ucnt = w.bm ? w.bm + bmw : nullptr;
-    w.len = w.bm ? w.ucnt + n : nullptr;
-    w.cnt = w.bm ? w.len + n : nullptr;
+    w.len = w.bm ? w.ucnt + nloc : nullptr;
+    w.cnt = w.bm ? w.len + nloc : nullptr;
     w.mdone = w.bm ? w.cnt + kKMax : nullptr;
-    w.flags = w.bm ? w.mdone + np / kTM : nullptr;
+    w.flags = w.bm ? w.mdone + nlp / kTM : nullptr;
     w.upop = w.bm ? w.flags + 4 : nullptr;
     w.xt = base ? base + 4 * words : nullptr;
     w.cacc = cv.take<int32_t>((size_t)num_sms() * 2 * kTM * w.nbx);
-    w.zacc = cv.take<double>((size_t)n * kKMax);
+    w.zacc = cv.take<double>((size_t)std::max<int64_t>(nloc, 1) * kKMax);
     w.tab_g = cv.take<double>((size_t)n + 2);
     w.tab_lab = cv.take<signed char>((size_t)n + 16);
+    w.y32 = nullptr;
+    w.counts = nullptr;
+    w.inv = w.deg = w.scale = nullptr;
+    if (shard) {
+        w.y32 = cv.take<int32_t>((size_t)n);
+        w.counts = cv.take<int64_t>(kKMax);
+        w.inv = cv.take<double>(kKMax);
+        w.deg = cv.take<double>((size_t)n);
+        w.scale = cv.take<double>((size_t)n);
+    }
 }
 
 size_t bitmap_workspace(int64_t E, int64_t n, int directed, int k) {
@@ -993,7 +1088,7 @@ size_t bitmap_workspace(int64_t E, int64_t n, int directed, int k) {
     (void)directed;
     Carver cv(nullptr);
     BmWs w;
-    carve_bm(cv, w, n, k);
+    carve_bm(cv, w, n, n, k, false);
     return cv.bytes();
 }
 
@@ -1047,12 +1142,17 @@ int bitmap_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n
                   cudaStream_t st) {
     Carver cv(ws);
     BmWs W;
-    carve_bm(cv, W, n, k);
+    carve_bm(cv, W, n, n, k, false);
     if (ws_bytes < cv.bytes()) return GEE_E_WORKSPACE;
     BmArgs a;
     a.n = (int)n;
     a.Wp = W.Wp;
     a.Np = W.Np;
+    a.row0 = 0;
+    a.nloc = (int)n;
+    a.Nlp = W.Nlp;
+    a.shard = 0;
+    a.deg_all = nullptr;
     a.E = E;
     a.directed = directed;
     a.bm = W.bm;
@@ -1090,6 +1190,102 @@ int bitmap_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n
         GEE_CHECK_LAUNCH("k_bm_scan");
     }
     GEE_CHECK_CUDA(launch_pdl(k_bm_table, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, false, a));
+    GEE_CHECK_LAUNCH("k_bm_table");
+    if (W.nbx == 16) return launch_gemm<16>(a, rows, cols, st);
+    if (W.nbx == 32) return launch_gemm<32>(a, rows, cols, st);
+    return launch_gemm<64>(a, rows, cols, st);
+}
+
+// ---------------------------------------------------------------------------
+// Row shards (multi-GPU, dist.py): rank p holds rows [row0, row0 + nloc) and
+// their entries of the symmetrised stream (a directed list, global ids).
+// Phase 1 (bitmap_shard_degrees): labels of every node, the local bitmap
+// rows, their popcounts and -- when a pair repeats -- exact stream lengths;
+// returns the local rows' degrees.  The caller all-gathers them (NCCL).
+// Phase 2 (bitmap_shard_encode): the node table of every node from the
+// gathered degrees, then the GEMM over the local row tiles -> Z's local rows.
+// Both phases take the same workspace, untouched in between.
+static BmArgs shard_args(const BmWs &W, int64_t E, int64_t n, int64_t row0, int64_t nloc, int k, unsigned flags,
+                         int32_t *err) {
+    BmArgs a = {};
+    a.n = (int)n;
+    a.Wp = W.Wp;
+    a.Np = W.Np;
+    a.row0 = (int)row0;
+    a.nloc = (int)nloc;
+    a.Nlp = W.Nlp;
+    a.shard = 1;
+    a.deg_all = nullptr;
+    a.E = E;
+    a.directed = 1;  // the local stream holds both directions explicitly
+    a.bm = W.bm;
+    a.ucnt = W.ucnt;
+    a.len = W.len;
+    a.cnt = W.cnt;
+    a.mdone = W.mdone;
+    a.flags = W.flags;
+    a.upop = W.upop;
+    a.xt = W.xt;
+    a.nbx = W.nbx;
+    a.cpart = W.cacc;
+    a.zacc = W.zacc;
+    a.labels = nullptr;
+    a.y32 = W.y32;
+    a.counts = W.counts;
+    a.inv = W.inv;
+    a.deg = W.deg;
+    a.scale = W.scale;
+    a.tab_g = W.tab_g;
+    a.tab_lab = W.tab_lab;
+    a.flags_opts = flags;
+    a.z = nullptr;
+    a.k = k;
+    a.err = err;
+    return a;
+}
+
+size_t bitmap_shard_workspace(int64_t n, int64_t nloc, int k) {
+    Carver cv(nullptr);
+    BmWs w;
+    carve_bm(cv, w, n, nloc, k, true);
+    return cv.bytes();
+}
+
+int bitmap_shard_degrees(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n, int64_t row0, int64_t nloc,
+                         const int64_t *labels, int k, unsigned flags, unsigned *deg_local, void *ws,
+                         size_t ws_bytes, int32_t *err, cudaStream_t st) {
+    Carver cv(ws);
+    BmWs W;
+    carve_bm(cv, W, n, nloc, k, true);
+    if (ws_bytes < cv.bytes()) return GEE_E_WORKSPACE;
+    BmArgs a = shard_args(W, E, n, row0, nloc, k, flags, err);
+    a.labels = labels;
+    GEE_CHECK_CUDA(cudaMemsetAsync(W.bm, 0, W.clear_bytes, st));
+    k_bm_set<<<(unsigned)num_sms() * 4, kSetThreads, 0, st>>>(rows, cols, a);
+    GEE_CHECK_LAUNCH("k_bm_set");
+    const unsigned nb = (unsigned)std::max<int64_t>(1, (nloc + 7) / 8);
+    GEE_CHECK_CUDA(launch_pdl(k_bm_scan, dim3(nb), dim3(256), 0, st, false, a));
+    GEE_CHECK_LAUNCH("k_bm_scan");
+    GEE_CHECK_CUDA(launch_pdl(k_bm_len, dim3((unsigned)num_sms() * 2), dim3(256), 0, st, false, rows, a));
+    GEE_CHECK_LAUNCH("k_bm_len");
+    GEE_CHECK_CUDA(launch_pdl(k_bm_deg, dim3((unsigned)std::max<int64_t>(1, (nloc + 255) / 256)), dim3(256), 0, st,
+                              false, a, deg_local));
+    GEE_CHECK_LAUNCH("k_bm_deg");
+    return GEE_OK;
+}
+
+int bitmap_shard_encode(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n, int64_t row0, int64_t nloc,
+                        int k, unsigned flags, const unsigned *deg_all, double *z_local, void *ws, size_t ws_bytes,
+                        int32_t *err, cudaStream_t st) {
+    Carver cv(ws);
+    BmWs W;
+    carve_bm(cv, W, n, nloc, k, true);
+    if (ws_bytes < cv.bytes()) return GEE_E_WORKSPACE;
+    BmArgs a = shard_args(W, E, n, row0, nloc, k, flags, err);
+    a.deg_all = (flags & GEE_LAPLACIAN) ? deg_all : nullptr;
+    a.z = z_local;
+    // plain launch: the predecessor is the degree all-gather
+    k_bm_table<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a);
     GEE_CHECK_LAUNCH("k_bm_table");
     if (W.nbx == 16) return launch_gemm<16>(a, rows, cols, st);
     if (W.nbx == 32) return launch_gemm<32>(a, rows, cols, st);

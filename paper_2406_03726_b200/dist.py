@@ -18,6 +18,14 @@ entries.  Rank p owns rows [rb, re):
      neighbour j, owned by other ranks;
   5. K4 over rows [rb, re); Z stays row-sharded (gather_z collects it).
 
+Unit-weight graphs of at most 16384 nodes and K <= 8 (configs 0/1) take the
+bitmap path instead (encode_rows_bitmap): each rank sets the adjacency bits of
+its own rows only (no transpose pass: its slice already holds both
+directions), reports its rows' degrees, and after ONE all-gather of those
+degrees (uint32, N; only under the Laplacian) runs the node table and the
+tensor-core product over its row tiles.  Labels are replicated, so the class
+histogram needs no all-reduce there.
+
 The collectives are torch.distributed calls (NCCL over NVLink on the GPU
 box; gloo in the CPU tests).  The per-rank compute is an object with four
 methods; the product uses GpuShardOps (libgee).  tests/test_dist_gloo.py
@@ -167,6 +175,41 @@ class GpuShardOps:
         _lib.raise_device_errors(bits, "sharded encode")
         return z
 
+    # -- bitmap path (unit weights, n <= 16384, k <= 8) ----------------------
+    BITMAP_MAX_NODES = 16384
+
+    @classmethod
+    def bitmap_ok(cls, n, k, weighted):
+        return not weighted and 1 <= n <= cls.BITMAP_MAX_NODES and 1 <= k <= 8
+
+    def bm_degrees(self, r, c, n, rb, re, labels, k, flags):
+        """Phase 1: local bitmap rows -> int32[re-rb] stream lengths (the
+        rows' unit-weight degrees).  labels: all n (replicated)."""
+        e = int(r.numel())
+        nb = _lib.size_query(self.lib.gee_bitmap_shard_workspace, e, n, rb, re, k)
+        ws = getattr(self, "_bm_ws", None)
+        if ws is None or ws.numel() < nb:
+            ws = self._bm_ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=self.dev)
+        self._bm_err = _device.error_word(self.dev)
+        deg = torch.empty(max(re - rb, 1), dtype=torch.int32, device=self.dev)
+        _lib.check(self.lib.gee_bitmap_shard_degrees(
+            _device.ptr(r), _device.ptr(c), e, n, rb, re, _device.ptr(labels), k, flags, _device.ptr(deg),
+            _device.ptr(ws), ws.numel(), _device.ptr(self._bm_err), _device.stream_handle()))
+        return deg[: re - rb]
+
+    def bm_encode(self, r, c, n, rb, re, k, flags, deg_all, check=True):
+        """Phase 2 (after bm_degrees on this object): Z[rb:re]."""
+        e = int(r.numel())
+        z = torch.empty((re - rb, k), dtype=torch.float64, device=self.dev)
+        ws = self._bm_ws
+        _lib.check(self.lib.gee_bitmap_shard_encode(
+            _device.ptr(r), _device.ptr(c), e, n, rb, re, k, flags,
+            _device.ptr(deg_all) if deg_all is not None else None, _device.ptr(z), _device.ptr(ws), ws.numel(),
+            _device.ptr(self._bm_err), _device.stream_handle()))
+        if check:
+            _lib.raise_device_errors(int(self._bm_err.item()), "sharded bitmap encode")
+        return z
+
 
 # ---------------------------------------------------------------------------
 # orchestration
@@ -189,6 +232,16 @@ def encode_rows(ops, stream, labels, n, k, flags, ranges, rank, group=None):
     return ops.embed(csr, rb, re, n, y32, inv, scale, k, flags)
 
 
+def encode_rows_bitmap(ops, stream, labels, n, k, flags, ranges, rank, group=None, check=True):
+    """Bitmap path for rank `rank` (unit weights): degrees of the local rows,
+    ALL-GATHER of the degree vector (Laplacian only), then Z[rb:re]."""
+    rb, re = ranges[rank]
+    r, c, _ = stream
+    deg_local = ops.bm_degrees(r, c, n, rb, re, labels, k, flags)
+    deg_all = all_gather_ranges(deg_local, ranges, group) if flags & _lib.LAPLACIAN else None
+    return ops.bm_encode(r, c, n, rb, re, k, flags, deg_all, check=check)
+
+
 def encode_sharded(edges, labels, opts=None, group=None, ops=None):
     """Row-sharded encode of an EdgeList replicated on every rank.  Returns
     (z_local, (rb, re)): this rank's rows of Z."""
@@ -205,7 +258,10 @@ def encode_sharded(edges, labels, opts=None, group=None, ops=None):
     _, w = e.weight_kind()
     stream = local_stream(e.rows, e.cols, w, edges.directed, rb, re)
     lab = _device.to_device(labels.labels, torch.int64, dev)
-    z = encode_rows(ops, stream, lab, n, k, flags, ranges, rank, group)
+    if ops.bitmap_ok(n, k, w is not None):
+        z = encode_rows_bitmap(ops, stream, lab, n, k, flags, ranges, rank, group)
+    else:
+        z = encode_rows(ops, stream, lab, n, k, flags, ranges, rank, group)
     return z, (rb, re)
 
 
@@ -246,16 +302,40 @@ def bench_sharded(args, rank, world, dev):
     rb, re = ranges[rank]
     stream = local_stream(rows, cols, w, directed, rb, re)
     ops = GpuShardOps(dev)
+    use_bm = ops.bitmap_ok(n, k, w is not None)
+    if use_bm:
+        def step():
+            return encode_rows_bitmap(ops, stream, lab, n, k, flags, ranges, rank, check=False)
+    else:
+        def step():
+            return encode_rows(ops, stream, lab, n, k, flags, ranges, rank)
     for _ in range(args.warmup):
-        encode_rows(ops, stream, lab, n, k, flags, ranges, rank)
+        step()
     torch.cuda.synchronize()
+    run = step
+    graphed = False
+    if use_bm and not args.eager:
+        # the whole step (kernels + the NCCL all-gather) as one CUDA graph
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step()
+            run = g.replay
+            graphed = True
+            run()
+            torch.cuda.synchronize()
+        except Exception as ex:  # capture unsupported here: time eager launches
+            print(f"[rank {rank}] CUDA graph capture failed ({ex}); timing eager launches", file=sys.stderr)
+            run = step
+    if use_bm:
+        _lib.raise_device_errors(int(ops._bm_err.item()), "sharded bitmap encode")
     times = []
     for _ in range(args.steps):
         dist.barrier()
         torch.cuda.synchronize()
         s, t = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        encode_rows(ops, stream, lab, n, k, flags, ranges, rank)
+        run()
         t.record()
         torch.cuda.synchronize()
         dist.barrier()
@@ -269,8 +349,11 @@ def bench_sharded(args, rank, world, dev):
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded, BASELINE.json shapes)",
                 "config": {"workload": f"configs[{args.config}] {cfg['name']}", "n_nodes": n, "n_edges": e,
-                           "k_classes": k, "parallelism": f"row-sharded x{world} (NCCL all-reduce n_k, "
-                           "all-gather labels + Laplacian scale)"}}
+                           "k_classes": k,
+                           "parallelism": (f"row-sharded x{world}, bitmap path (NCCL all-gather of degrees)"
+                                           if use_bm else f"row-sharded x{world} (NCCL all-reduce n_k, "
+                                           "all-gather labels + Laplacian scale)"),
+                           "cuda_graph": graphed}}
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()

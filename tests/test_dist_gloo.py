@@ -64,6 +64,24 @@ class OracleShardOps:
             z = O.correlate_rows(z)
         return torch.as_tensor(z)
 
+    # bitmap path: phase 1 = stream lengths of the local rows, phase 2 = Z
+    # rows from the local stream and the gathered degree vector
+    def bm_degrees(self, r, c, n, rb, re, labels, k, flags):
+        self._labels = labels.numpy().astype(np.int64)
+        return torch.as_tensor(np.bincount(r.numpy() - rb, minlength=re - rb).astype(np.int32))
+
+    def bm_encode(self, r, c, n, rb, re, k, flags, deg_all, check=True):
+        rr = r.numpy()
+        assert ((rr >= rb) & (rr < re)).all()
+        ip, cc, cv = O.coo_to_csr(rr, c.numpy(), np.ones(rr.size), n, n)
+        scale = None
+        if flags & LAP:
+            deg = deg_all.numpy().astype(np.float64) + (1.0 if flags & DIAG else 0.0)
+            scale = torch.as_tensor(np.where(deg > 0, 1.0 / np.sqrt(np.where(deg > 0, deg, 1.0)), 0.0))
+        y32 = torch.as_tensor(self._labels.astype(np.int32))
+        inv = self.inv_counts(torch.as_tensor(O.class_counts(self._labels, k)))
+        return self.embed((ip, cc, cv), rb, re, n, y32, inv, scale, k, flags)
+
 
 def _free_port():
     with socket.socket() as s:
@@ -108,6 +126,38 @@ def test_two_rank_sharding_is_bitwise_shard_invariant(flags, directed):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     mp.spawn(_worker, args=(2, _free_port(), case, flags, q), nprocs=2, join=True)
+    z = q.get(timeout=60)
+    st, zr, _ = O.encode_edges(rows, cols, w, n, directed, labels, k, flags)
+    assert st == O.OK
+    assert z.shape == zr.shape and np.array_equal(z, zr)
+
+
+def _bm_worker(rank, world, port, case, flags, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, rows, cols, _, labels, k, directed = case
+        ranges = gdist.shard_plan(rows, cols, n, directed, world)
+        stream = gdist.local_stream(torch.as_tensor(rows), torch.as_tensor(cols), None, directed, *ranges[rank])
+        z = gdist.encode_rows_bitmap(OracleShardOps(), stream, torch.as_tensor(labels), n, k, flags, ranges,
+                                     rank)
+        full = gdist.gather_z(z, ranges)
+        if rank == 0:
+            out.put(full.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("flags", [0, LAP | DIAG | CORR, LAP])
+@pytest.mark.parametrize("directed", [False, True])
+def test_two_rank_bitmap_path_degree_allgather(flags, directed):
+    """Unit-weight path: only the degree vector is exchanged; Z assembled
+    from the two shards equals the unsharded oracle bitwise."""
+    case = _graph(11 + flags + directed, directed=directed, weighted=False, k=3)
+    n, rows, cols, w, labels, k, _ = case
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_bm_worker, args=(2, _free_port(), case, flags, q), nprocs=2, join=True)
     z = q.get(timeout=60)
     st, zr, _ = O.encode_edges(rows, cols, w, n, directed, labels, k, flags)
     assert st == O.OK

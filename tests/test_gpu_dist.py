@@ -78,3 +78,91 @@ def test_single_rank_nccl_group():
         z_close(z.cpu().numpy(), zr)
     finally:
         dist.destroy_process_group()
+
+
+def _unit_graph(seed, n, m, k, directed, repeats):
+    rng = np.random.default_rng(seed)
+    rows = rng.integers(0, n, m)
+    cols = rng.integers(0, n, m)
+    if not directed and not repeats:
+        # a simple undirected graph: i < j pairs, each once
+        lo, hi = np.minimum(rows, cols), np.maximum(rows, cols)
+        key = np.unique(lo[lo != hi] * n + hi[lo != hi])
+        rows, cols = key // n, key % n
+    if repeats:
+        rows[:50] = rows[50:100]       # repeated pairs
+        cols[:50] = cols[50:100]
+        rows[100:120] = cols[130:150]  # pairs in both directions
+        cols[100:120] = rows[130:150]
+        rows[200:210] = cols[200:210]  # self loops
+    labels = rng.integers(-1, k, n)
+    return rows, cols, labels
+
+
+@pytest.mark.parametrize("shards", [1, 2, 3, 5])
+@pytest.mark.parametrize("flags", [7, 1, 0, 6])
+@pytest.mark.parametrize("kind", ["simple", "repeats", "directed"])
+def test_bitmap_shards_match_oracle(shards, flags, kind):
+    """Unit-weight row shards on the bitmap path (gee_bitmap_shard_*), run one
+    after another in this process with the degree all-gather done by hand."""
+    directed = kind == "directed"
+    n, m, k = 2500, 60_000, 3
+    rows, cols, labels = _unit_graph(shards * 31 + flags, n, m, k, directed, kind == "repeats")
+    dev = torch.device("cuda")
+    ranges = gdist.shard_plan(rows, cols, n, directed, shards)
+    tr, tc = (torch.as_tensor(x, device=dev) for x in (rows, cols))
+    lab = torch.as_tensor(labels, device=dev)
+    ops = [gdist.GpuShardOps(dev) for _ in ranges]
+    streams = [gdist.local_stream(tr, tc, None, directed, rb, re) for rb, re in ranges]
+    degs = [o.bm_degrees(s[0], s[1], n, rb, re, lab, k, flags) for o, s, (rb, re) in zip(ops, streams, ranges)]
+    deg_all = torch.cat(degs)                                 # all-gather
+    ref_len = gdist.stream_row_counts(rows, cols, n, directed)
+    assert np.array_equal(deg_all.cpu().numpy(), ref_len)    # exact degrees of A
+    z = torch.cat([o.bm_encode(s[0], s[1], n, rb, re, k, flags, deg_all)
+                   for o, s, (rb, re) in zip(ops, streams, ranges)])
+    w = np.ones(len(rows))
+    st, zr, _ = O.encode_edges(rows, cols, w, n, directed, labels, k, flags)
+    pre = None
+    if flags & 4:
+        _, pre, _ = O.encode_edges(rows, cols, w, n, directed, labels, k, flags & 3)
+    z_close(z.cpu().numpy(), zr, zr_pre=pre)
+
+
+def test_bitmap_shard_empty_and_out_of_range():
+    dev = torch.device("cuda")
+    n, k = 600, 2
+    rows, cols, labels = _unit_graph(5, n, 5000, k, False, False)
+    tr, tc = (torch.as_tensor(x, device=dev) for x in (rows, cols))
+    lab = torch.as_tensor(labels, device=dev)
+    # an empty row range
+    o = gdist.GpuShardOps(dev)
+    r, c, _ = gdist.local_stream(tr, tc, None, False, 300, 300)
+    d = o.bm_degrees(r, c, n, 300, 300, lab, k, 7)
+    assert d.numel() == 0
+    z = o.bm_encode(r, c, n, 300, 300, k, 7, torch.zeros(n, dtype=torch.int32, device=dev))
+    assert z.shape == (0, k)
+    # entries outside the shard's rows are an edge-range error
+    o = gdist.GpuShardOps(dev)
+    r, c, _ = gdist.local_stream(tr, tc, None, False, 0, 300)
+    o.bm_degrees(r, c, n, 0, 200, lab, k, 0)
+    with pytest.raises(G.StructuralError):
+        o.bm_encode(r, c, n, 0, 200, k, 0, None)
+
+
+def test_single_rank_nccl_group_bitmap_path():
+    import torch.distributed as dist
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rows, cols, labels = _unit_graph(9, 3000, 80_000, 3, False, False)
+        e = G.EdgeList(3000, rows, cols, None)
+        z, (rb, re) = gdist.encode_sharded(e, G.LabelVector(labels, 3), G.EmbedOptions(True, True, True))
+        assert (rb, re) == (0, 3000)
+        st, zr, _ = O.encode_edges(rows, cols, np.ones(len(rows)), 3000, False, labels, 3, 7)
+        _, pre, _ = O.encode_edges(rows, cols, np.ones(len(rows)), 3000, False, labels, 3, 3)
+        z_close(z.cpu().numpy(), zr, zr_pre=pre)
+    finally:
+        dist.destroy_process_group()
