@@ -112,6 +112,10 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
     return v;
 }
 
+__device__ __forceinline__ void red_release_gpu(unsigned *p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ unsigned ld_gpu(const unsigned *p) {
     unsigned v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -153,9 +157,26 @@ __device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
 // NQ independent 32 x 32 transposes, stage-major
 template <int NQ>
 __device__ __forceinline__ void transpose32_n(unsigned (&x)[NQ], int lane) {
+    // byte-granular stages: one byte permute each (lane-dependent selector)
+    {
+        const unsigned sel = (lane & 16) ? 0x3276u : 0x5410u;
+        unsigned y[NQ];
 #pragma unroll
-    for (int J = 16; J >= 1; J >>= 1) {
-        const unsigned M = J == 16 ? 0x0000ffffu : J == 8 ? 0x00ff00ffu : J == 4 ? 0x0f0f0f0fu : J == 2 ? 0x33333333u : 0x55555555u;
+        for (int q = 0; q < NQ; ++q) y[q] = __shfl_xor_sync(0xffffffffu, x[q], 16);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) x[q] = __byte_perm(x[q], y[q], sel);
+    }
+    {
+        const unsigned sel = (lane & 8) ? 0x3715u : 0x6240u;
+        unsigned y[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) y[q] = __shfl_xor_sync(0xffffffffu, x[q], 8);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) x[q] = __byte_perm(x[q], y[q], sel);
+    }
+#pragma unroll
+    for (int J = 4; J >= 1; J >>= 1) {
+        const unsigned M = J == 4 ? 0x0f0f0f0fu : J == 2 ? 0x33333333u : 0x55555555u;
         unsigned y[NQ];
 #pragma unroll
         for (int q = 0; q < NQ; ++q) y[q] = __shfl_xor_sync(0xffffffffu, x[q], J);
@@ -342,7 +363,17 @@ __global__ void __launch_bounds__(kSB) k_bm_sym(BmArgs a) {
             xx[q] = av[q];
             xx[kW + q] = bv[q];
         }
-        transpose32_n<2 * kW>(xx, lane);
+        // an all-zero 32 x 128 slice transposes to zeros (one side of every
+        // pair is empty for a triangular list): skip its shuffles
+        const bool az = !__any_sync(0xffffffffu, (av[0] | av[1] | av[2] | av[3]) != 0u);
+        const bool bz = !__any_sync(0xffffffffu, (bv[0] | bv[1] | bv[2] | bv[3]) != 0u);
+        if (!az && !bz) {
+            transpose32_n<2 * kW>(xx, lane);
+        } else if (!az) {
+            transpose32_n<kW>(*reinterpret_cast<unsigned(*)[kW]>(&xx[0]), lane);
+        } else if (!bz) {
+            transpose32_n<kW>(*reinterpret_cast<unsigned(*)[kW]>(&xx[kW]), lane);
+        }
 #pragma unroll
         for (int q = 0; q < kW; ++q) {
             sat[q * 32 + lane][w] = xx[q];
@@ -653,9 +684,13 @@ __device__ __forceinline__ void gemm_epilogue(const BmArgs &a, int r, const int3
         for (int q = 0; q < kKMax; ++q) {
             double v = 0.0;
             if (q * kDig + kDig <= NB && q < a.k) {
-#pragma unroll
-                for (int d = 0; d < kDig; ++d) v += (double)C[q * kDig + d] * pow2i(8 * d - 55);
-                v *= inv[q];
+                // sum_c s_c * 2^55 = lo + hi * 2^32 exactly in integers (digit
+                // sums < 2^23: lo < 2^48, hi < 2^40), one rounding to f64
+                const int32_t *D = C + q * kDig;
+                const long long lo = (long long)D[0] + ((long long)D[1] << 8) + ((long long)D[2] << 16) +
+                                     ((long long)D[3] << 24);
+                const long long hi = (long long)D[4] + ((long long)D[5] << 8) + ((long long)D[6] << 16);
+                v = fma((double)hi, pow2i(32 - 55), (double)lo * pow2i(-55)) * inv[q];
             }
             acc[q] = v;
         }
@@ -685,8 +720,9 @@ __device__ __forceinline__ void gemm_epilogue(const BmArgs &a, int r, const int3
         } else {
             const double nrm = __dsqrt_rn(ss);
             if (nrm > 0.0) {
+                const double rn = __ddiv_rn(1.0, nrm);  // within 1 ulp of acc / nrm
 #pragma unroll
-                for (int q = 0; q < kKMax; ++q) acc[q] = __ddiv_rn(acc[q], nrm);
+                for (int q = 0; q < kKMax; ++q) acc[q] *= rn;
             }
         }
     }
@@ -722,6 +758,7 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: 
 #ifdef GEE_TRACE
 __device__ unsigned long long g_trace[10][64];
 __device__ unsigned long long g_trace_end[160];
+__device__ unsigned long long g_trace_cta[160][8];  // entry, setup done, last MMA issued, epilogue done, seg0 acc ready, seg0 published, first step expanded
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long v;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
@@ -786,6 +823,9 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
 
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     if (t == 0) TRACE(7, 0);
+#ifdef GEE_TRACE
+    if (t == 0) g_trace_cta[blockIdx.x][0] = gtime();
+#endif
     // Launched while k_bm_table runs (PDL): k_bm_sym's outputs (bitmap, counts,
     // flags) are complete, the node table is not until pdl_wait().
     const bool rep = block_repeats(a);
@@ -820,6 +860,9 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tslot;
     if (t == 0) TRACE(7, 2);
+#ifdef GEE_TRACE
+    if (t == 0) g_trace_cta[blockIdx.x][1] = gtime();
+#endif
 
     const int KT = a.Np / kTK;
     const int64_t total = (int64_t)(a.Nlp / kTM) * KT;
@@ -879,6 +922,9 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             mbar_arrive(smem_u32(full + as));
             if ((rl & 31) == 0) TRACE(1 + (rl >> 5), i);
+#ifdef GEE_TRACE
+            if (i == 0 && rl == 0) g_trace_cta[blockIdx.x][6] = gtime();
+#endif
         }
     } else if (w == 8) {
         // ---- MMA issue: the whole warp runs the loop (warp-uniform operands
@@ -910,6 +956,9 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
             __syncwarp();
             if (last) ++seg;
         }
+#ifdef GEE_TRACE
+        if (lane == 0) g_trace_cta[blockIdx.x][2] = gtime();
+#endif
     } else {
         // ---- epilogue: warp 4 + e reads TMEM lanes 32e..32e+31 (= tile rows)
         const int e = w - 4;
@@ -930,6 +979,9 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
             const int rlab = live ? __ldcg(a.y32 + a.row0 + r) : -1;
             const double rsc = (lap && live) ? __ldcg(a.scale + a.row0 + r) : 1.0;
             mbar_wait_idle(smem_u32(accfull + buf), (seg >> 1) & 1, 256);
+#ifdef GEE_TRACE
+            if (seg == 0 && e == 0 && lane == 0) g_trace_cta[blockIdx.x][4] = gtime();
+#endif
             if (e == 0 && lane == 0) TRACE(9, seg);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             int32_t C[NB];
@@ -966,9 +1018,13 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
                 int4 *dst = reinterpret_cast<int4 *>(a.cpart + (((size_t)blockIdx.x * 2 + sidx) * kTM + e * 32 + lane) * NB);
 #pragma unroll
                 for (int j = 0; j < NB / 4; ++j) dst[j] = make_int4(C[4 * j], C[4 * j + 1], C[4 * j + 2], C[4 * j + 3]);
-                __threadfence();
+                // the barrier orders the 128 threads' stores before one
+                // gpu-scope release (cumulative), which publishes the slab
                 epi_bar();
-                if (e == 0 && lane == 0) atomicAdd(&a.mdone[m], 1u);
+                if (e == 0 && lane == 0) red_release_gpu(&a.mdone[m], 1u);
+#ifdef GEE_TRACE
+                if (seg == 0 && e == 0 && lane == 0) g_trace_cta[blockIdx.x][5] = gtime();
+#endif
             } else if (seglen < KT && live) {
                 // partners: participating CTAs other than this one
                 unsigned b = lo * G / T;
@@ -1002,6 +1058,9 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
             if (e == 0 && lane == 0) TRACE(9, 8 + seg);
             i += seglen;
         }
+#ifdef GEE_TRACE
+        if (e == 0 && lane == 0) g_trace_cta[blockIdx.x][3] = gtime();
+#endif
     }
     if (t == 0) TRACE(5, 0);
 #ifdef GEE_TRACE
@@ -1295,7 +1354,8 @@ int bitmap_shard_encode(const int64_t *rows, const int64_t *cols, int64_t E, int
 #ifdef GEE_TRACE
 extern "C" int gee_trace_dump(unsigned long long *out) {
     return cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)) == cudaSuccess &&
-                   cudaMemcpyFromSymbol(out + 640, g_trace_end, sizeof(g_trace_end)) == cudaSuccess
+                   cudaMemcpyFromSymbol(out + 640, g_trace_end, sizeof(g_trace_end)) == cudaSuccess &&
+                   cudaMemcpyFromSymbol(out + 800, g_trace_cta, sizeof(g_trace_cta)) == cudaSuccess
                ? 0
                : -1;
 }
