@@ -188,7 +188,7 @@ __device__ __forceinline__ void transpose32_n(unsigned (&x)[NQ], int lane) {
 
 // node-table entry of row r from its stream length L (k_bm_sym / k_bm_scan /
 // the rare path); y32 and the histogram are complete when this runs
-__device__ __forceinline__ void node_entry(const BmArgs &a, int r, unsigned L) {
+__device__ __forceinline__ void node_entry(const BmArgs &a, int r, unsigned L, int lab, unsigned nk) {
     double sr = 1.0;
     if (a.flags_opts & GEE_LAPLACIAN) {
         const double d = (double)L + ((a.flags_opts & GEE_DIAGONAL) ? 1.0 : 0.0);
@@ -196,10 +196,9 @@ __device__ __forceinline__ void node_entry(const BmArgs &a, int r, unsigned L) {
         sr = laplacian_scale(d, a.err);
         a.scale[r] = sr;
     }
-    const int lab = a.y32[r];
     double g = 0.0;
     if (lab >= 0) {
-        const double inv = __ddiv_rn(1.0, (double)__ldcg(a.cnt + lab));  // 1/n_k (embedding.py:106)
+        const double inv = __ddiv_rn(1.0, (double)nk);  // 1/n_k (embedding.py:106)
         g = (a.flags_opts & GEE_LAPLACIAN) ? sr * inv : inv;
         // X[r, lab] = s_r as 7 base-256 digits of floor(s_r * 2^55) (s_r <= 1)
         const unsigned long long T = __double2ull_rz(sr * 0x1p55);
@@ -208,6 +207,11 @@ __device__ __forceinline__ void node_entry(const BmArgs &a, int r, unsigned L) {
     }
     a.tab_g[r] = g;
     a.tab_lab[r] = (signed char)lab;
+}
+
+__device__ __forceinline__ void node_entry(const BmArgs &a, int r, unsigned L) {
+    const int lab = __ldcg(a.y32 + r);
+    node_entry(a, r, L, lab, lab >= 0 ? __ldcg(a.cnt + lab) : 0u);
 }
 
 // class counts and 1/n_k as the reference's LabelVector / W (run once)
@@ -414,13 +418,21 @@ __global__ void __launch_bounds__(kSB) k_bm_sym(BmArgs a) {
 // node table from the distinct counts: d_r, s_r, X^T digits, g_r (thread per row)
 __global__ void __launch_bounds__(256) k_bm_table(BmArgs a) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    // labels and class sizes are k_bm_set's (complete when this grid is
+    // launched): loaded while the distinct counts are still being finished
+    int lab = -1;
+    unsigned nk = 0;
+    if (r < a.n) {
+        lab = __ldcg(a.y32 + r);
+        if (lab >= 0) nk = __ldcg(a.cnt + lab);
+    }
+    if (blockIdx.x == 0) write_counts(a, threadIdx.x);
     pdl_wait();
     pdl_trigger();  // k_bm_gemm may start now: it waits for this grid before reading the table
-    if (blockIdx.x == 0) write_counts(a, threadIdx.x);
     if (r < a.n) {
         // a shard without the Laplacian needs no degrees (s_r = 1)
         const unsigned L = !a.shard ? __ldcg(a.ucnt + r) : a.deg_all ? __ldcg(a.deg_all + r) : 0u;
-        node_entry(a, r, L);
+        node_entry(a, r, L, lab, nk);
     }
 }
 
@@ -758,7 +770,7 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: 
 #ifdef GEE_TRACE
 __device__ unsigned long long g_trace[10][64];
 __device__ unsigned long long g_trace_end[160];
-__device__ unsigned long long g_trace_cta[160][8];  // entry, setup done, last MMA issued, epilogue done, seg0 acc ready, seg0 published, first step expanded
+__device__ unsigned long long g_trace_cta[160][12];  // entry, setup done, last MMA issued, epilogue done, seg0 acc ready, seg0 published, first step expanded
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long v;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
@@ -962,6 +974,21 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
     } else {
         // ---- epilogue: warp 4 + e reads TMEM lanes 32e..32e+31 (= tile rows)
         const int e = w - 4;
+        {
+            // Touch the pages the tail will use (partial slabs of this CTA and
+            // its neighbours, the stream-K counters, this CTA's Z rows) while
+            // waiting for the first accumulator: their address translations
+            // are then cached when the epilogue is on the critical path.
+            const int tt = t - 128;
+            const int nb = (int)gridDim.x;
+            const int bb = min(max((int)blockIdx.x + (tt % 5) - 2, 0), nb - 1);
+            const char *p0 = reinterpret_cast<const char *>(a.cpart + (size_t)bb * 2 * kTM * NB) + (tt / 5) * 4096;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p0));
+            const int m0 = s0 / KT, m1 = (s1 - 1) / KT;
+            const int rr = min((tt & 1 ? m1 : m0) * kTM + (tt >> 1), a.n - 1);
+            if (nsteps > 0 && rr >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.z + (size_t)rr * a.k));
+            if (tt == 0 && nsteps > 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.mdone + m0));
+        }
         pdl_wait();  // inv, scale come from k_bm_table
         double inv[kKMax];
 #pragma unroll
@@ -978,9 +1005,10 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
             // the row's epilogue inputs, loaded while the MMAs run
             const int rlab = live ? __ldcg(a.y32 + a.row0 + r) : -1;
             const double rsc = (lap && live) ? __ldcg(a.scale + a.row0 + r) : 1.0;
-            mbar_wait_idle(smem_u32(accfull + buf), (seg >> 1) & 1, 256);
+            mbar_wait_idle(smem_u32(accfull + buf), (seg >> 1) & 1, 32);
 #ifdef GEE_TRACE
             if (seg == 0 && e == 0 && lane == 0) g_trace_cta[blockIdx.x][4] = gtime();
+            if (e == 0 && lane == 0) g_trace_cta[blockIdx.x][11] = gtime();
 #endif
             if (e == 0 && lane == 0) TRACE(9, seg);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1035,7 +1063,11 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
                     const unsigned bs0 = bb * T / G, bs1 = (bb + 1) * T / G;
                     if (bb != blockIdx.x && bs1 != bs0 && bs1 > lo) ++npart;
                 }
-                while (ld_acquire_gpu(a.mdone + m) < npart) __nanosleep(64);
+                while (ld_acquire_gpu(a.mdone + m) < npart) {
+                }
+#ifdef GEE_TRACE
+                if (e == 0 && lane == 0) g_trace_cta[blockIdx.x][8] = gtime();
+#endif
                 for (; b < G && b * T / G < hi; ++b) {
                     const unsigned bs0 = b * T / G, bs1 = (b + 1) * T / G;
                     if (b == blockIdx.x || bs1 == bs0 || bs1 <= lo) continue;  // self, idle CTAs
@@ -1044,16 +1076,22 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
                         a.cpart + (((size_t)b * 2 + bsi) * kTM + e * 32 + lane) * NB);
 #pragma unroll
                     for (int j = 0; j < NB / 4; ++j) {
-                        const int4 v = __ldcg(src + j);
+                        const int4 v = src[j];  // after the acquire: L1 holds no stale copy
                         C[4 * j] += v.x, C[4 * j + 1] += v.y, C[4 * j + 2] += v.z, C[4 * j + 3] += v.w;
                     }
                 }
             }
             if (fin && live) {
                 if (e == 0 && lane == 0) TRACE(9, 19 + 8 * seg);
+#ifdef GEE_TRACE
+                if (e == 0 && lane == 0) g_trace_cta[blockIdx.x][9] = gtime();
+#endif
                 const bool rrep = rep && __ldcg(a.len + r) != __ldcg(a.ucnt + r);
                 gemm_epilogue<NB>(a, r, C, rrep, inv, rsc, rlab);
                 if (e == 0 && lane == 0) TRACE(9, 20 + 8 * seg);
+#ifdef GEE_TRACE
+                if (e == 0 && lane == 0) g_trace_cta[blockIdx.x][10] = gtime();
+#endif
             }
             if (e == 0 && lane == 0) TRACE(9, 8 + seg);
             i += seglen;

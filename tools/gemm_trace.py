@@ -17,7 +17,7 @@ for _ in range(5):
     enc.run(rows, cols, None, lab)
 torch.cuda.synchronize()
 lib = _lib.load()
-buf = (ctypes.c_ulonglong * (10 * 64 + 160 + 1280))()
+buf = (ctypes.c_ulonglong * (10 * 64 + 160 + 1920))()
 assert lib.gee_trace_dump(buf) == 0
 arr = np.array(buf, dtype=np.int64); t = arr[:640].reshape(10, 64); ends = arr[640:640 + 148]
 t0 = t[7, 0]
@@ -31,12 +31,12 @@ for seg in range(3):
           "merged", t[9, 19 + 8 * seg] - t0, "z", t[9, 20 + 8 * seg] - t0)
 # a finishing CTA: look at CTA traces only for CTA 0
 print("cta end: min", (ends.min() - t0), "max", (ends.max() - t0), "argmax", ends.argmax())
-cta = arr[800:800 + 1280].reshape(160, 8)[:148]
+cta = arr[800:800 + 1920].reshape(160, 12)[:148]
 b0 = cta[:, 0].min()
-for j, nm in enumerate(["entry", "setup", "last_mma", "epi_done", "seg0_acc", "seg0_pub", "step0_exp"]):
+for j, nm in enumerate(["entry", "setup", "last_mma", "epi_done", "seg0_acc", "seg0_pub", "step0_exp", "-", "polled", "merged", "z_done", "last_acc"]):
     v = (cta[:, j] - b0) / 1e3
     print(f"{nm:>9} us: min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f}")
 v = (ends - b0) / 1e3
 print(f"{'end':>9} us: min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f}")
 for b in range(6):
-    print("cta", b, " ".join(f"{(cta[b, j] - b0) / 1e3:7.2f}" if cta[b, j] else "   -   " for j in range(7)))
+    print("cta", b, " ".join(f"{(cta[b, j] - b0) / 1e3:7.2f}" if cta[b, j] else "   -   " for j in range(12)))
