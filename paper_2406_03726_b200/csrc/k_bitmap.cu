@@ -789,11 +789,11 @@ __device__ __forceinline__ unsigned long long gtime() {
 // k_bm_gemm geometry
 constexpr int kACols = kTK / 4;  // TMEM columns per A stage (128 rows x 256 bytes, 4 bytes per column)
 template <int NB>
-constexpr int rr_stages() { return NB == 64 ? 9 : 16; }  // bulk-copied stages: 4 KB bitmap + the B tile
-template <int NB>
 constexpr int chains() { return 2; }                    // independent accumulators per buffer
 template <int NB>
 constexpr int a_stages() { return (512 - 4 * NB) / kACols; }  // TMEM A stages after 2 x 2 accumulators
+template <int NB>
+constexpr int rr_stages() { return a_stages<NB>(); }  // ring stage s = A stage s: one release per K step
 constexpr int kGemmNT = 448;    // warps 0-7 expand, 8-11 epilogue, 12 MMA, 13 bulk copies
 constexpr int kExp = 128;       // expander threads per K step (thread = tile row)
 constexpr int kWMma = 12, kWTma = 13;
@@ -928,7 +928,8 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
             const uint4 w0 = lds128(smem_u32(sR + rs * kRB + rl * 16));
             const uint4 w1 = lds128(smem_u32(sR + rs * kRB + kTM * 16 + rl * 16));
             mbar_arrive(smem_u32(rempty + rs));
-            if (i >= kAS) mbar_wait(smem_u32(aempty + as), ((i / kAS) - 1) & 1);
+            // A stage as is free: the ring refilled stage rs (= as) only after
+            // the MMAs of step i - kAS, which read it, had completed
             // row rl of the A stage = TMEM lane rl: column 8m + i holds the
             // bytes of bits 4i..4i+3 of word m (K-major, 4 bytes per column)
             const uint32_t ta = tmem + ((uint32_t)((w & 3) * 32) << 16) + kAccCols + as * kACols;
@@ -967,8 +968,7 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
                 for (int k = 0; k < kTK / 32; ++k)
                     mma_i8_ts(tmem + (buf * kChains + (k % kChains)) * NB, ta + 8 * k,
                               bd + (k >> 2) * (NB * 128 >> 4) + 2 * (k & 3), idesc, !first || k >= kChains);
-                mma_commit(smem_u32(aempty + as));
-                mma_commit(smem_u32(rempty + rs));
+                mma_commit(smem_u32(rempty + rs));  // bitmap, B and A stage all free
                 if (last) mma_commit(smem_u32(accfull + buf));
             }
             __syncwarp();
