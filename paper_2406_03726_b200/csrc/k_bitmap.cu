@@ -47,6 +47,37 @@
 
 namespace gee {
 
+#ifdef GEE_TRACE
+__device__ unsigned long long g_trace[10][64];
+__device__ unsigned long long g_trace_end[160];
+__device__ unsigned long long g_trace_cta[160][12];  // entry, setup done, last MMA issued, epilogue done, seg0 acc ready, seg0 published, first step expanded
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    return v;
+}
+#define TRACE(slot, i) \
+    do {               \
+        if (blockIdx.x == 0 && (i) < 64) g_trace[slot][i] = gtime(); \
+    } while (0)
+// kernel spans: [k][0] first CTA start, [k][1] first dependency wait passed, [k][2] last CTA end
+__device__ unsigned long long g_kspan[8][3];
+#define KSPAN(k, j)                                                              \
+    do {                                                                         \
+        if (threadIdx.x == 0) {                                                  \
+            if ((j) < 2) atomicMin(&g_kspan[k][j], gtime());                     \
+            else atomicMax(&g_kspan[k][j], gtime());                             \
+        }                                                                        \
+    } while (0)
+#else
+#define KSPAN(k, j) \
+    do {            \
+    } while (0)
+#define TRACE(slot, i) \
+    do {               \
+    } while (0)
+#endif
+
 constexpr int kBmMax = 16384;   // nodes: bitmap Np^2/8 <= 32 MB (L2-resident)
 constexpr int kBlk = 256;       // the bitmap's side is padded to a multiple of 256
 constexpr int kSetThreads = 512;
@@ -228,6 +259,9 @@ __global__ void __launch_bounds__(kSetThreads) k_bm_set(const int64_t *__restric
                                                         const int64_t *__restrict__ cols, BmArgs a) {
     __shared__ unsigned sh_hist[kKMax];
     const int lane = threadIdx.x & 31;
+    KSPAN(0, 0);
+    // k_bm_sym may be scheduled as this grid drains; it waits for its completion
+    pdl_trigger();
     // labels: int64 -> int32 (-1 = unlabeled), validated, histogrammed
     if (threadIdx.x < kKMax) sh_hist[threadIdx.x] = 0;
     __syncthreads();
@@ -325,12 +359,16 @@ __global__ void __launch_bounds__(kSetThreads) k_bm_set(const int64_t *__restric
             if (lane - o >= start) incl |= y;
         }
         const unsigned prev = __shfl_up_sync(0xffffffffu, incl, 1);
+#ifndef GEE_NORED  // timing experiment only: no bitmap reductions
         if (two) atomicOr(&a.bm[kf], bf | (cont ? prev : 0u));
         const bool tail = lane == 31 || kf_next != kl;
         if (tail && kl != INV) atomicOr(&a.bm[kl], incl);
+#else
+        if (two && kf == 0x7fffffffu) a.bm[0] = bf | prev | incl;
+#endif
         r0 = nr0, r1 = nr1, c0 = nc0, c1 = nc1;
     }
-    pdl_trigger();
+    KSPAN(0, 2);
 }
 
 // S = U | U^T for the block pair (BI, BJ), BI <= BJ, in place.  Blocks are
@@ -345,7 +383,12 @@ __global__ void __launch_bounds__(kSB) k_bm_sym(BmArgs a) {
     // linear index -> (BI, BJ) on the upper triangle
     const unsigned x = blockIdx.x;
     unsigned bj = (unsigned)((sqrtf(8.0f * x + 1.0f) - 1.0f) * 0.5f);
+    KSPAN(1, 0);
     pdl_wait();
+    KSPAN(1, 1);
+    // k_bm_table may be scheduled as this grid drains (it reads only k_bm_set's
+    // outputs before waiting for this grid)
+    pdl_trigger();
     while ((bj + 1) * (bj + 2) / 2 <= x) ++bj;
     while (bj * (bj + 1) / 2 > x) --bj;
     const unsigned bi = x - bj * (bj + 1) / 2;
@@ -412,7 +455,7 @@ __global__ void __launch_bounds__(kSB) k_bm_sym(BmArgs a) {
     if (ca) atomicAdd(&a.ucnt[ra], ca);
     if (cb && !same) atomicAdd(&a.ucnt[rb], cb);
     if (__syncthreads_or(mut != 0) && t == 0) a.flags[0] = 1u;
-    pdl_trigger();
+    KSPAN(1, 2);
 }
 
 // node table from the distinct counts: d_r, s_r, X^T digits, g_r (thread per row)
@@ -427,13 +470,18 @@ __global__ void __launch_bounds__(256) k_bm_table(BmArgs a) {
         if (lab >= 0) nk = __ldcg(a.cnt + lab);
     }
     if (blockIdx.x == 0) write_counts(a, threadIdx.x);
+    KSPAN(2, 0);
+    // k_bm_gemm may be scheduled now: it sets up TMEM and its barriers, then
+    // waits for this grid (and so for k_bm_sym) before reading anything
+    pdl_trigger();
     pdl_wait();
-    pdl_trigger();  // k_bm_gemm may start now: it waits for this grid before reading the table
+    KSPAN(2, 1);
     if (r < a.n) {
         // a shard without the Laplacian needs no degrees (s_r = 1)
         const unsigned L = !a.shard ? __ldcg(a.ucnt + r) : a.deg_all ? __ldcg(a.deg_all + r) : 0u;
         node_entry(a, r, L, lab, nk);
     }
+    KSPAN(2, 2);
 }
 
 // directed lists: one warp per row, 8 rows per CTA
@@ -460,11 +508,16 @@ __global__ void __launch_bounds__(256) k_bm_scan(BmArgs a) {
 __device__ __forceinline__ bool block_repeats(const BmArgs &a) {
     __shared__ unsigned s_rep;
     if (threadIdx.x < 32) {
+        if (threadIdx.x == 0) TRACE(7, 3);
+        // every load issued before any is used: one round trip
+        const unsigned mut = threadIdx.x == 0 ? __ldcg(a.flags) : 0u;
         unsigned long long tot = 0;
         for (int i = threadIdx.x; i < kPopParts; i += 32) tot += __ldcg(a.upop + i * 32);
+        if (threadIdx.x == 0) TRACE(7, 4);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-        if (threadIdx.x == 0) s_rep = __ldcg(a.flags) != 0 || (int64_t)tot != a.E;
+        if (threadIdx.x == 0) s_rep = mut != 0 || (int64_t)tot != a.E;
+        if (threadIdx.x == 0) TRACE(7, 5);
     }
     __syncthreads();
     return s_rep != 0;
@@ -767,24 +820,7 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-#ifdef GEE_TRACE
-__device__ unsigned long long g_trace[10][64];
-__device__ unsigned long long g_trace_end[160];
-__device__ unsigned long long g_trace_cta[160][12];  // entry, setup done, last MMA issued, epilogue done, seg0 acc ready, seg0 published, first step expanded
-__device__ __forceinline__ unsigned long long gtime() {
-    unsigned long long v;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
-    return v;
-}
-#define TRACE(slot, i) \
-    do {               \
-        if (blockIdx.x == 0 && (i) < 64) g_trace[slot][i] = gtime(); \
-    } while (0)
-#else
-#define TRACE(slot, i) \
-    do {               \
-    } while (0)
-#endif
+
 
 // k_bm_gemm geometry
 constexpr int kACols = kTK / 4;  // TMEM columns per A stage (128 rows x 256 bytes, 4 bytes per column)
@@ -841,15 +877,9 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
 #ifdef GEE_TRACE
     if (t == 0) g_trace_cta[blockIdx.x][0] = gtime();
 #endif
+    KSPAN(3, 0);
     // Launched while k_bm_table runs (PDL): k_bm_sym's outputs (bitmap, counts,
     // flags) are complete, the node table is not until pdl_wait().
-    const bool rep = block_repeats(a);
-    if (rep) {
-        pdl_wait();
-        repeat_phases(rows, cols, a);
-    }
-    if (t == 0) TRACE(7, 1);
-
     if (w == kWMma) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
                      "r"(kTmemCols));
@@ -884,20 +914,32 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
     const int s0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
     const int s1 = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
     const int nsteps = s1 - s0;
+    const int pre = min(nsteps, kRR);
+
+    // Launched (PDL) while k_bm_table runs, possibly before k_bm_sym is
+    // done: TMEM and the barriers are set up by now; after pdl_wait() the
+    // bitmap, counts and node table are complete.  The first kRR bitmap tiles
+    // go out at once; the repeat check (one round trip) overlaps them, and
+    // the X^T tiles follow it (the rare path rewrites X^T).
+    pdl_wait();
+#ifdef GEE_TRACE
+    if (t == 0) atomicMin(&g_kspan[3][1], gtime());
+#endif
+    if (w == kWTma && lane == 0) {
+        for (int i = 0; i < pre; ++i) {
+            const int g = s0 + i, m = g / KT, ks = g % KT;
+            const uint32_t bar = smem_u32(rfull + i);
+            mbar_expect_tx(bar, kRB + kBB);
+            bulk_g2s(smem_u32(sR + i * kRB), a.bm + ((size_t)(m * KT + ks) << 10), kRB, bar);
+        }
+    }
+    const bool rep = block_repeats(a);
+    if (rep) repeat_phases(rows, cols, a);
+    if (t == 0) TRACE(7, 1);
 
     if (w == kWTma) {
         // ---- bulk copies
         if (lane == 0) {
-            // the first kRR bitmap tiles go out before the node table (X^T)
-            // is known to be complete
-            const int pre = min(nsteps, kRR);
-            for (int i = 0; i < pre; ++i) {
-                const int g = s0 + i, m = g / KT, ks = g % KT;
-                const uint32_t bar = smem_u32(rfull + i);
-                mbar_expect_tx(bar, kRB + kBB);
-                bulk_g2s(smem_u32(sR + i * kRB), a.bm + ((size_t)(m * KT + ks) << 10), kRB, bar);
-            }
-            pdl_wait();
             asm volatile("fence.proxy.async.global;" ::: "memory");
             for (int i = 0; i < pre; ++i) {
                 const int ks = (s0 + i) % KT;
@@ -995,7 +1037,6 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
             if (nsteps > 0 && rr >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.z + (size_t)rr * a.k));
             if (tt == 0 && nsteps > 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.mdone + m0));
         }
-        pdl_wait();  // inv, scale come from k_bm_table
         double inv[kKMax];
 #pragma unroll
         for (int q = 0; q < kKMax; ++q) inv[q] = q < a.k ? __ldcg(a.inv + q) : 0.0;
@@ -1112,6 +1153,7 @@ __global__ void __launch_bounds__(kGemmNT, 1) k_bm_gemm(const int64_t *__restric
 #endif
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    KSPAN(3, 2);
     if (w == kWMma) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
 
@@ -1398,6 +1440,15 @@ int bitmap_shard_encode(const int64_t *rows, const int64_t *cols, int64_t E, int
 }
 
 #ifdef GEE_TRACE
+extern "C" int gee_kspan(unsigned long long *out, int reset) {
+    if (reset) {
+        unsigned long long init[8][3];
+        for (int k = 0; k < 8; ++k) init[k][0] = init[k][1] = ~0ull, init[k][2] = 0;
+        return cudaMemcpyToSymbol(g_kspan, init, sizeof(init)) == cudaSuccess ? 0 : -1;
+    }
+    return cudaMemcpyFromSymbol(out, g_kspan, sizeof(g_kspan)) == cudaSuccess ? 0 : -1;
+}
+
 extern "C" int gee_trace_dump(unsigned long long *out) {
     return cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)) == cudaSuccess &&
                    cudaMemcpyFromSymbol(out + 640, g_trace_end, sizeof(g_trace_end)) == cudaSuccess &&

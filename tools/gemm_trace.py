@@ -21,7 +21,7 @@ buf = (ctypes.c_ulonglong * (10 * 64 + 160 + 1920))()
 assert lib.gee_trace_dump(buf) == 0
 arr = np.array(buf, dtype=np.int64); t = arr[:640].reshape(10, 64); ends = arr[640:640 + 148]
 t0 = t[7, 0]
-print("start->rep", t[7, 1] - t0, "->setup", t[7, 2] - t0)
+print("start->rep", t[7, 1] - t0, "->setup", t[7, 2] - t0, "rep: pre", t[7, 3] - t0, "loaded", t[7, 4] - t0, "flag", t[7, 5] - t0)
 print("step tma  exp0  exp1  exp2  exp3  mma")
 for i in range(48):
     print(i, *[f"{(t[s, i] - t0) if t[s, i] else -1:>7}" for s in (0, 1, 2, 3, 4, 8)])
