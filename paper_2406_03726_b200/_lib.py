@@ -62,7 +62,7 @@ SIGNATURES = {
     "gee_profile_read": (_int, [ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_char_p), _int]),
     "gee_debug_set": (_int, [_int, _int]),
 }
-DEBUG_FORCE_BUCKETS = 1  # key; values: 0 default, 1 row buckets, 2 no bitmap path
+DEBUG_FORCE_BUCKETS = 1  # key; values: 0 default, 1 row buckets, 2 no bitmap path, 3 = 2 + 64-bit sort keys
 
 _lib = None
 

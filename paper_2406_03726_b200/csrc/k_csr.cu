@@ -1094,14 +1094,14 @@ static size_t carve_csr(Carver &cv, CsrWs &w, int64_t E, int64_t n_rows, int dir
 }
 
 bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
-size_t sort_workspace(int64_t E, int64_t n_rows, int directed);
+size_t sort_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
 int sort_csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, int64_t E, int64_t n_rows,
                    int64_t n_cols, int directed, int force_vals, int64_t *row_ptr, int32_t *col, double *val,
                    int64_t *nnz, unsigned deg_flags, double *deg, double *scale, void *ws, size_t ws_bytes,
                    unsigned **val_mode, int32_t *err, cudaStream_t st);
 
 size_t csr_build_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int directed) {
-    if (sort_path_ok(E, n_rows, n_cols, directed)) return sort_workspace(E, n_rows, directed);
+    if (sort_path_ok(E, n_rows, n_cols, directed)) return sort_workspace(E, n_rows, n_cols, directed);
     Carver cv(nullptr);
     CsrWs w;
     return carve_csr(cv, w, E, n_rows, directed);
@@ -1134,7 +1134,7 @@ int csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, i
               double *deg, double *scale, void *ws, size_t ws_bytes, int32_t *err,
               cudaStream_t st) {
     if (sort_path_ok(E, n_rows, n_cols, directed)) {
-        // packed 32-bit (row, col) keys: radix-sort path, always a compact CSR
+        // packed (row, col) keys: radix-sort path, always a compact CSR
         int rc = sort_csr_build(rows, cols, w, wt, E, n_rows, n_cols, directed, 1, row_ptr, col, val, nnz,
                                 deg_flags, deg, scale, ws, ws_bytes, nullptr, err, st);
         if (rc) return rc;

@@ -23,17 +23,18 @@ import paper_2406_03726_b200 as G  # noqa: E402
 
 RTOL = 1e-12
 CASES = load()
-PATHS = ["default", "sort", "buckets"]
+PATHS = ["default", "sort", "buckets", "sort64"]
 
 
 class assembly_path:
     """Select the CSR-assembly path via the library's test hook: "default"
     (column bitmaps for unit-weight graphs with <= 16384 nodes, else the
     radix sort when (row, col) packs into 32 bits, else row buckets),
-    "sort" (never the bitmap path) or "buckets" (always row buckets)."""
+    "sort" (never the bitmap path), "buckets" (always row buckets) or
+    "sort64" (the radix sort also on 64-bit (row, col) keys)."""
 
     def __init__(self, path):
-        self.force = {"default": 0, "sort": 2, "buckets": 1}[path]
+        self.force = {"default": 0, "sort": 2, "buckets": 1, "sort64": 3}[path]
 
     def __enter__(self):
         from paper_2406_03726_b200 import _lib
