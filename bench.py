@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--eager", action="store_true", help="launch kernels one by one instead of a CUDA graph")
     p.add_argument("--flush-mib", type=int, default=512)
     p.add_argument("--cpu-budget-s", type=float, default=12.0)
+    p.add_argument("--sharded", action="store_true",
+                   help="run the row-sharded multi-GPU step even with one rank (exercises dist.py under NCCL)")
     return p.parse_args()
 
 
@@ -247,8 +249,11 @@ def run_b200(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if world > 1 or args.sharded:
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
         from paper_2406_03726_b200 import dist as gdist
         return gdist.bench_sharded(args, rank, world, dev)
 
