@@ -339,9 +339,13 @@ __device__ void row_smem(const EmbedArgs &a, int64_t r, double *zs, double *xs) 
     }
     const double nrm = __dsqrt_rn(ss);
     if (ntiles == 1) {
-        for (int c = lane; c < a.k; c += 32) zrow[c] = nrm > 0.0 ? __ddiv_rn(zs[c], nrm) : zs[c];
+        // one division per row; z * (1/nrm) is within 1 ulp of z / nrm
+        // (embedding.py:140 divides; Z's bar is 1e-12 relative)
+        const double rn = nrm > 0.0 ? __ddiv_rn(1.0, nrm) : 1.0;
+        for (int c = lane; c < a.k; c += 32) zrow[c] = zs[c] * rn;
     } else if (nrm > 0.0) {
-        for (int c = lane; c < a.k; c += 32) zrow[c] = __ddiv_rn(zrow[c], nrm);
+        const double rn = __ddiv_rn(1.0, nrm);
+        for (int c = lane; c < a.k; c += 32) zrow[c] = zrow[c] * rn;
     }
     __syncwarp();
 }
@@ -403,9 +407,11 @@ __device__ void row_long(const EmbedArgs &a, int64_t r, double *zsm, double *xsm
     }
     const double nrm = __dsqrt_rn(ss);
     if (ntiles == 1) {
-        for (int c = threadIdx.x; c < a.k; c += blockDim.x) zrow[c] = nrm > 0.0 ? __ddiv_rn(zsm[c], nrm) : zsm[c];
+        const double rn = nrm > 0.0 ? __ddiv_rn(1.0, nrm) : 1.0;
+        for (int c = threadIdx.x; c < a.k; c += blockDim.x) zrow[c] = zsm[c] * rn;
     } else if (nrm > 0.0) {
-        for (int c = threadIdx.x; c < a.k; c += blockDim.x) zrow[c] = __ddiv_rn(zrow[c], nrm);
+        const double rn = __ddiv_rn(1.0, nrm);
+        for (int c = threadIdx.x; c < a.k; c += blockDim.x) zrow[c] = zrow[c] * rn;
     }
     __syncthreads();
 }
