@@ -29,7 +29,7 @@ constexpr int kEmbedThreads = 256;
 constexpr int kEmbedWarps = kEmbedThreads / 32;
 constexpr int kLongRow = 4096;
 constexpr int kKTile = 1024;
-constexpr int kRowChunk = 32;  // rows per work grab (4 per warp)
+constexpr int kRowChunk = 32;  // rows per work grab (one warp)
 // nodes whose table (9 B each) is staged in shared memory, by one 1024-thread
 // CTA per SM so a single table copy serves 32 warps (with 256-thread CTAs the
 // 90 KB table at N = 10^4 halved occupancy and lost to L1 record gathers)
@@ -480,18 +480,20 @@ __global__ void __launch_bounds__(NT) k_embed(EmbedArgs a, int n_tab) {
         if (t >= (int)n_long) break;
         row_long(a, a.long_list[t], zsm, xsm, dred);
     }
-    // phase 2: chunks of rows, one warp per row
+    // phase 2: every warp grabs its own chunks of rows, one warp per row (no
+    // CTA-wide barrier: row lengths vary, so a barrier per chunk would idle
+    // the warps that drew short rows)
     const int64_t n_rows = a.row_end - a.row_begin;
     const int64_t n_chunks = (n_rows + kRowChunk - 1) / kRowChunk;
+    const int lane = threadIdx.x & 31;
     for (;;) {
-        if (threadIdx.x == 0) task = (int)atomicAdd(&a.work[1], 1u);
-        __syncthreads();
-        int64_t t = task;
-        __syncthreads();
+        unsigned tw = 0;
+        if (lane == 0) tw = atomicAdd(&a.work[1], 1u);
+        const int64_t t = __shfl_sync(0xffffffffu, tw, 0);
         if (t >= n_chunks) break;
         const int64_t r0 = a.row_begin + t * kRowChunk;
         const int64_t r1 = min(a.row_end, r0 + kRowChunk);
-        for (int64_t r = r0 + wid; r < r1; r += kWarps) {
+        for (int64_t r = r0; r < r1; ++r) {
             int64_t s, e;
             row_extent(a, r, s, e);
             if (e - s > kLongRow) continue;
