@@ -991,18 +991,18 @@ __global__ void __launch_bounds__(kRowsThreads, 2) k_rows(RowsArgs a) {
     }
     __syncthreads();
     PHASE_MARK(3);
-    // phase S: chunks of rows, one warp per row, rows > 32 skipped
+    // phase S: every warp grabs its own chunks of rows (no CTA barrier per
+    // chunk: row lengths vary), one warp per row, rows > 32 skipped
     unsigned long long *wk = stk + wid * 32;
     double *wv = stv + wid * 32;
     const int64_t n_chunks = (a.n_rows + kSChunk - 1) / kSChunk;
     for (;;) {
-        if (threadIdx.x == 0) sm.task = (int)atomicAdd(&a.work[3], 1u);
-        __syncthreads();
-        int64_t t = sm.task;
-        __syncthreads();
+        unsigned tw = 0;
+        if (lane == 0) tw = atomicAdd(&a.work[3], 1u);
+        const int64_t t = __shfl_sync(0xffffffffu, tw, 0);
         if (t >= n_chunks) break;
         const int64_t r0 = t * kSChunk, r1 = min(a.n_rows, r0 + kSChunk);
-        for (int64_t r = r0 + wid; r < r1; r += nw) {
+        for (int64_t r = r0; r < r1; ++r) {
             int64_t L = a.slot_ptr[r + 1] - a.slot_ptr[r];
             if (L > 32) continue;
             if (L == 0) {
@@ -1016,7 +1016,7 @@ __global__ void __launch_bounds__(kRowsThreads, 2) k_rows(RowsArgs a) {
         }
     }
     PHASE_MARK(4);
-    (void)lane;
+    (void)nw;
 }
 
 // ---------------------------------------------------------------------------
