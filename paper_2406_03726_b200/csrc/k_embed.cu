@@ -491,9 +491,10 @@ __global__ void __launch_bounds__(NT) k_embed(EmbedArgs a, int n_tab) {
         if (lane == 0) tw = atomicAdd(&a.work[1], 1u);
         const int64_t t = __shfl_sync(0xffffffffu, tw, 0);
         if (t >= n_chunks) break;
-        const int64_t r0 = a.row_begin + t * kRowChunk;
-        const int64_t r1 = min(a.row_end, r0 + kRowChunk);
-        for (int64_t r = r0; r < r1; ++r) {
+        // chunk t = rows t, t + n_chunks, t + 2 n_chunks, ...: long rows
+        // cluster in id ranges of power-law graphs, a strided chunk spreads
+        // them over many warps
+        for (int64_t r = a.row_begin + t; r < a.row_end; r += n_chunks) {
             int64_t s, e;
             row_extent(a, r, s, e);
             if (e - s > kLongRow) continue;
