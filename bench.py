@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--eager", action="store_true", help="launch kernels one by one instead of a CUDA graph")
     p.add_argument("--flush-mib", type=int, default=512)
     p.add_argument("--cpu-budget-s", type=float, default=12.0)
+    p.add_argument("--force-path", type=int, default=0,
+                   help="debug: CSR assembly path hook (gee_debug_set GEE_DEBUG_FORCE_BUCKETS)")
     p.add_argument("--sharded", action="store_true",
                    help="run the row-sharded multi-GPU step even with one rank (exercises dist.py under NCCL)")
     return p.parse_args()
@@ -261,6 +263,8 @@ def run_b200(args):
     from paper_2406_03726_b200 import _lib
 
     lib = _lib.load()
+    if args.force_path:
+        lib.gee_debug_set(_lib.DEBUG_FORCE_BUCKETS, args.force_path)
     c = load_config(args.config, dev)
     n, e, k, directed, flags = c["n"], c["e"], c["k"], c["directed"], c["flags"]
     rows = torch.as_tensor(c["rows"], device=dev)

@@ -14,14 +14,14 @@
 //                 exact zeros dropped), compacted with a second look-back; it
 //                 also writes row_ptr and the pre-dedup stream row pointer.
 //
-// Stream order.  Pass 0 emits edge e's two entries at virtual positions 2e
-// (original) and 2e+1 (reversed; a sentinel key for a self-loop), so equal
-// keys leave the sort in (e, direction) order, not the reference's
-// [originals..., reversed...] order (graph_io.py:82-88).  Every entry
-// carries its true stream index (e or E+e) as payload, and k_dedup restores
-// stream order inside any run of >= 3 duplicates before summing (a run of 2
-// sums commutatively).  With unit weights no payload moves at all: a run's
-// value is its length, and the per-row degree is the row's stream length.
+// Stream order.  Pass 0 reads stream position v as the reference orders the
+// symmetrised stream, [originals..., reversed off-diagonals...]
+// (graph_io.py:82-88; a self-loop's mirror is a sentinel key that sorts last
+// and is dropped), and every pass is stable, so each run of equal keys leaves
+// the sort in stream order.  The payload is the entry's weight in its own
+// width (f32 or f64 bits), so k_dedup sums a run left to right as it reads it
+// -- no stream index, no gather.  With unit weights no payload moves at all: a
+// run's value is its length, and the per-row degree is the row's stream length.
 #include "gee_common.cuh"
 
 namespace gee {
@@ -49,22 +49,34 @@ struct SortGeom {
     int passes;
 };
 
-// key of virtual position v (K = unsigned or unsigned long long)
+// Key of stream position v (K = unsigned or unsigned long long).  Positions
+// follow the reference's stream exactly -- [originals..., reversed...]
+// (graph_io.py:82-88) -- so the stable LSD sort leaves every run of equal keys
+// in stream order and duplicates can be summed as they come.
 template <typename K>
-__device__ __forceinline__ K sort_key(const SortGeom &g, const int64_t *rows, const int64_t *cols, int64_t v,
-                                      unsigned &pay) {
-    if (g.directed) {
-        pay = (unsigned)v;
-        return ((K)rows[v] << g.colbits) | (K)cols[v];
-    }
-    int64_t e = v >> 1;
+__device__ __forceinline__ K sort_key(const SortGeom &g, const int64_t *rows, const int64_t *cols, int64_t v) {
+    if (v < g.E) return ((K)rows[v] << g.colbits) | (K)cols[v];
+    const int64_t e = v - g.E;
     const K r = (K)rows[e], c = (K)cols[e];
-    if (v & 1) {
-        pay = (unsigned)(g.E + e);
-        return r == c ? (K)g.sentinel : ((c << g.colbits) | r);
-    }
-    pay = (unsigned)e;
-    return (r << g.colbits) | c;
+    return r == c ? (K)g.sentinel : ((c << g.colbits) | r);
+}
+
+// Payload = the entry's weight, carried through the sort in its own width:
+// P = unsigned (f32 bits) or unsigned long long (f64 bits).
+template <typename P>
+__device__ __forceinline__ P weight_bits(const void *w, int64_t e) {
+    if constexpr (sizeof(P) == 8)
+        return (P)__double_as_longlong(static_cast<const double *>(w)[e]);
+    else
+        return (P)__float_as_uint(static_cast<const float *>(w)[e]);
+}
+
+template <typename P>
+__device__ __forceinline__ double pay_value(P p) {
+    if constexpr (sizeof(P) == 8)
+        return __longlong_as_double((long long)p);
+    else
+        return (double)__uint_as_float((unsigned)p);  // f32 -> f64 is exact (graph_io.py:61)
 }
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
@@ -150,14 +162,15 @@ __global__ void k_sort_bases(unsigned *hist, int passes) {
 }
 
 // ---------------------------------------------------------------------------
-template <typename K>
+template <typename K, typename P>
 struct OnesweepArgs {
     SortGeom g;
     const int64_t *rows, *cols;         // pass 0 input
+    const void *w;                      // pass 0 payload source (weights)
     const K *kin;                       // later passes
-    const unsigned *pin;
+    const P *pin;
     K *kout;
-    unsigned *pout;
+    P *pout;
     const unsigned *base;               // [256] exclusive digit bases of this pass
     unsigned *status;                   // [tiles][256] look-back words (zeroed)
     unsigned *tile_ctr;
@@ -199,14 +212,14 @@ __device__ __forceinline__ unsigned lookback_digit(const unsigned *status, int64
 }
 
 // dynamic shared memory: the tile's keys (K[kSortTile]) then payloads
-template <typename K>
-constexpr size_t onesweep_smem() { return (size_t)kSortTile * (sizeof(K) + sizeof(unsigned)); }
+template <typename K, typename P>
+constexpr size_t onesweep_smem() { return (size_t)kSortTile * (sizeof(K) + sizeof(P)); }
 
-template <typename K>
-__global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(OnesweepArgs<K> a) {
+template <typename K, typename P>
+__global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(OnesweepArgs<K, P> a) {
     extern __shared__ __align__(16) unsigned char os_dyn[];
     K *sk = reinterpret_cast<K *>(os_dyn);
-    unsigned *sp = reinterpret_cast<unsigned *>(os_dyn + (size_t)kSortTile * sizeof(K));
+    P *sp = reinterpret_cast<P *>(os_dyn + (size_t)kSortTile * sizeof(K));
     __shared__ unsigned whist[kSortWarps][256];
     __shared__ unsigned tstart[256], gbase[256];
     __shared__ unsigned red[33];
@@ -225,8 +238,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(OnesweepArgs<K> a)
     for (int j = 0; j < kSortItems; ++j) {
         const int i = wid * (kSortTile / kSortWarps) + j * 32 + lane;
         if (i < nvalid) {
-            unsigned pay_unused;
-            key[j] = a.first ? sort_key<K>(a.g, a.rows, a.cols, t0 + i, pay_unused) : a.kin[t0 + i];
+            key[j] = a.first ? sort_key<K>(a.g, a.rows, a.cols, t0 + i) : a.kin[t0 + i];
         } else {
             key[j] = 0;
         }
@@ -284,12 +296,8 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(OnesweepArgs<K> a)
             const unsigned pos = tstart[dd] + whist[wid][dd] + rank[j];
             sk[pos] = key[j];
             if (carry) {
-                unsigned pay = 0;
-                if (a.first)
-                    sort_key<K>(a.g, a.rows, a.cols, t0 + i, pay);
-                else
-                    pay = a.pin[t0 + i];
-                sp[pos] = pay;
+                const int64_t v = t0 + i;
+                sp[pos] = a.first ? weight_bits<P>(a.w, v < a.g.E ? v : v - a.g.E) : a.pin[v];
             }
         }
     }
@@ -305,11 +313,11 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(OnesweepArgs<K> a)
 }
 
 // ---------------------------------------------------------------------------
-template <typename K>
+template <typename K, typename P>
 struct DedupArgs {
     SortGeom g;
     const K *key;               // sorted stream
-    const unsigned *pay;
+    const P *pay;               // weights, in stream order inside every run
     const void *w;
     int wt;
     int64_t n_rows;
@@ -324,49 +332,8 @@ struct DedupArgs {
     int force_vals;       // 1: always write out_val; 2: only run if *has_multi
 };
 
-__device__ __forceinline__ void sort_run_by_payload(unsigned *pay, int64_t p, int64_t q) {
-    // in-place insertion sort (runs of duplicates are short); heap sort for long ones
-    const int64_t L = q - p;
-    if (L <= 64) {
-        for (int64_t i = p + 1; i < q; ++i) {
-            unsigned x = pay[i];
-            int64_t j = i - 1;
-            while (j >= p && pay[j] > x) {
-                pay[j + 1] = pay[j];
-                --j;
-            }
-            pay[j + 1] = x;
-        }
-        return;
-    }
-    unsigned *h = pay + p;
-    for (int64_t s = L / 2 - 1; s >= 0; --s) {
-        int64_t i = s;
-        for (;;) {
-            int64_t c = 2 * i + 1;
-            if (c >= L) break;
-            if (c + 1 < L && h[c + 1] > h[c]) ++c;
-            if (h[i] >= h[c]) break;
-            unsigned t = h[i]; h[i] = h[c]; h[c] = t;
-            i = c;
-        }
-    }
-    for (int64_t end = L - 1; end > 0; --end) {
-        unsigned t = h[0]; h[0] = h[end]; h[end] = t;
-        int64_t i = 0;
-        for (;;) {
-            int64_t c = 2 * i + 1;
-            if (c >= end) break;
-            if (c + 1 < end && h[c + 1] > h[c]) ++c;
-            if (h[i] >= h[c]) break;
-            unsigned u = h[i]; h[i] = h[c]; h[c] = u;
-            i = c;
-        }
-    }
-}
-
-template <typename K>
-__global__ void __launch_bounds__(kSortThreads) k_dedup(DedupArgs<K> a) {
+template <typename K, typename P>
+__global__ void __launch_bounds__(kSortThreads) k_dedup(DedupArgs<K, P> a) {
     __shared__ unsigned red[33];
     __shared__ unsigned s_excl;
     __shared__ int s_tile;
@@ -398,15 +365,9 @@ __global__ void __launch_bounds__(kSortThreads) k_dedup(DedupArgs<K> a) {
         while (q < Mv && a.key[q] == k) ++q;
         double acc;
         if (carry) {
-            unsigned *pay = const_cast<unsigned *>(a.pay);
-            if (q - p >= 3) sort_run_by_payload(pay, p, q);
-            const int64_t E = a.g.E;
-            unsigned s = pay[p];
-            acc = sort_load_w(a.w, a.wt, s < E ? s : s - E);
-            for (int64_t i = p + 1; i < q; ++i) {
-                unsigned t = pay[i];
-                acc += sort_load_w(a.w, a.wt, t < E ? t : t - E);
-            }
+            // the run is in stream order (stable sort of the stream): sum left to right
+            acc = pay_value<P>(a.pay[p]);
+            for (int64_t i = p + 1; i < q; ++i) acc += pay_value<P>(a.pay[i]);
         } else {
             acc = (double)(q - p);
             multi |= q - p > 1;
@@ -494,7 +455,8 @@ __global__ void k_degree_stream(const int64_t *__restrict__ sptr, int64_t n, int
 
 // ---------------------------------------------------------------------------
 int degree_guarded(const int64_t *, const int32_t *, const double *, int64_t, unsigned, double *, double *,
-                   int32_t *, const unsigned *, cudaStream_t);
+                   int32_t *, const unsigned *, unsigned *, cudaStream_t);
+size_t degree_hub_words(int64_t nnz);
 
 static int bitlen(int64_t x) {
     int b = 0;
@@ -533,9 +495,11 @@ static int sort_keybits(int64_t n_rows, int64_t n_cols) {
 }
 
 struct SortWs {
-    unsigned *hist, *flags, *ctr, *status, *payA, *payB;
+    unsigned *hist, *flags, *ctr, *status;
+    void *payA, *payB;  // 8 bytes per entry (f64 weights; f32 use half)
     void *keyA, *keyB;
     int64_t *sptr;
+    unsigned *hubs;  // k_degree's hub-row list
     int64_t tiles;
     int passes;
     size_t zero_bytes;
@@ -558,9 +522,10 @@ static void carve_sort(Carver &cv, SortWs &w, int64_t E, int64_t n_rows, int64_t
     const size_t m = (size_t)(Mv > 0 ? Mv : 1);
     w.keyA = cv.take<unsigned char>(m * kbytes);
     w.keyB = cv.take<unsigned char>(m * kbytes);
-    w.payA = cv.take<unsigned>(m);
-    w.payB = cv.take<unsigned>(m);
+    w.payA = cv.take<unsigned long long>(m);
+    w.payB = cv.take<unsigned long long>(m);
     w.sptr = cv.take<int64_t>((size_t)n_rows + 1);
+    w.hubs = cv.take<unsigned>(degree_hub_words(Mv));
 }
 
 size_t sort_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int directed) {
@@ -570,14 +535,14 @@ size_t sort_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int directed) {
     return cv.bytes();
 }
 
-template <typename K>
+template <typename K, typename P>
 static int sort_passes(const SortGeom &g, const int64_t *rows, const int64_t *cols, const void *w, int wt,
                        int64_t n_rows, int force_vals, int64_t *row_ptr, int32_t *col, double *val, SortWs &W,
                        cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_onesweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)onesweep_smem<K>()));
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_onesweep<K, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)onesweep_smem<K, P>()));
         attr = true;
     }
     const int64_t tiles = W.tiles;
@@ -586,14 +551,15 @@ static int sort_passes(const SortGeom &g, const int64_t *rows, const int64_t *co
     k_sort_bases<<<1, 256, 0, st>>>(W.hist, g.passes);
     GEE_CHECK_LAUNCH("k_sort_bases");
     const K *kin = nullptr;
-    const unsigned *pin = nullptr;
+    const P *pin = nullptr;
     K *kout = static_cast<K *>(W.keyA);
-    unsigned *pout = W.payA;
+    P *pout = static_cast<P *>(W.payA);
     for (int p = 0; p < g.passes; ++p) {
-        OnesweepArgs<K> a;
+        OnesweepArgs<K, P> a;
         a.g = g;
         a.rows = rows;
         a.cols = cols;
+        a.w = w;
         a.kin = kin;
         a.pin = pin;
         a.kout = kout;
@@ -604,14 +570,14 @@ static int sort_passes(const SortGeom &g, const int64_t *rows, const int64_t *co
         a.nonunit = W.flags;
         a.shift = 8 * p;
         a.first = p == 0;
-        k_onesweep<K><<<(unsigned)tiles, kSortThreads, onesweep_smem<K>(), st>>>(a);
+        k_onesweep<K, P><<<(unsigned)tiles, kSortThreads, onesweep_smem<K, P>(), st>>>(a);
         GEE_CHECK_LAUNCH("k_onesweep");
         kin = kout;
         pin = pout;
         kout = (kout == static_cast<K *>(W.keyA)) ? static_cast<K *>(W.keyB) : static_cast<K *>(W.keyA);
-        pout = (pout == W.payA) ? W.payB : W.payA;
+        pout = (pout == static_cast<P *>(W.payA)) ? static_cast<P *>(W.payB) : static_cast<P *>(W.payA);
     }
-    DedupArgs<K> d;
+    DedupArgs<K, P> d;
     d.g = g;
     d.key = kin;
     d.pay = pin;
@@ -627,14 +593,14 @@ static int sort_passes(const SortGeom &g, const int64_t *rows, const int64_t *co
     d.nonunit = W.flags;
     d.has_multi = W.flags + 1;
     d.force_vals = force_vals ? 1 : 0;
-    k_dedup<K><<<(unsigned)tiles, kSortThreads, 0, st>>>(d);
+    k_dedup<K, P><<<(unsigned)tiles, kSortThreads, 0, st>>>(d);
     GEE_CHECK_LAUNCH("k_dedup");
     if (!force_vals) {
         // rare: unit weights with duplicates -> redo with values materialised
         d.status = W.status + (size_t)g.passes * tiles * 256 + (tiles + 1);
         d.tile_ctr = W.ctr + kMaxPasses + 1;
         d.force_vals = 2;
-        k_dedup<K><<<(unsigned)tiles, kSortThreads, 0, st>>>(d);
+        k_dedup<K, P><<<(unsigned)tiles, kSortThreads, 0, st>>>(d);
         GEE_CHECK_LAUNCH("k_dedup_fix");
     }
     return GEE_OK;
@@ -662,11 +628,16 @@ int sort_csr_build(const int64_t *rows, const int64_t *cols, const void *w, int 
     GEE_CHECK_CUDA(cudaMemsetAsync(W.hist, 0, W.zero_bytes, st));
     if (val_mode) *val_mode = W.flags;
     if (g.Mv > 0) {
-        const int rc = keybits > 32
-                           ? sort_passes<unsigned long long>(g, rows, cols, w, wt, n_rows, force_vals, row_ptr, col,
-                                                             val, W, st)
-                           : sort_passes<unsigned>(g, rows, cols, w, wt, n_rows, force_vals, row_ptr, col, val, W,
-                                                   st);
+        using u64 = unsigned long long;
+        const bool wide_key = keybits > 32, f64 = wt == GEE_W_F64;
+        const int rc =
+            wide_key ? (f64 ? sort_passes<u64, u64>(g, rows, cols, w, wt, n_rows, force_vals, row_ptr, col, val, W, st)
+                            : sort_passes<u64, unsigned>(g, rows, cols, w, wt, n_rows, force_vals, row_ptr, col, val,
+                                                         W, st))
+                     : (f64 ? sort_passes<unsigned, u64>(g, rows, cols, w, wt, n_rows, force_vals, row_ptr, col, val,
+                                                         W, st)
+                            : sort_passes<unsigned, unsigned>(g, rows, cols, w, wt, n_rows, force_vals, row_ptr, col,
+                                                              val, W, st));
         if (rc) return rc;
     } else {
         GEE_CHECK_CUDA(cudaMemsetAsync(row_ptr, 0, sizeof(int64_t) * (size_t)(n_rows + 1), st));
@@ -678,7 +649,8 @@ int sort_csr_build(const int64_t *rows, const int64_t *cols, const void *w, int 
         double *sc = (deg_flags & GEE_LAPLACIAN) ? scale : nullptr;
         k_degree_stream<<<grid_for(n_rows, 256, 8), 256, 0, st>>>(W.sptr, n_rows, diag, W.flags, deg, sc, err);
         GEE_CHECK_LAUNCH("k_degree_stream");
-        int rc = degree_guarded(row_ptr, col, val, n_rows, diag ? GEE_DIAGONAL : 0u, deg, sc, err, W.flags, st);
+        int rc = degree_guarded(row_ptr, col, val, n_rows, diag ? GEE_DIAGONAL : 0u, deg, sc, err, W.flags, W.hubs,
+                                st);
         if (rc) return rc;
     }
     return GEE_OK;

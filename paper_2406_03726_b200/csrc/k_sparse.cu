@@ -13,81 +13,271 @@ int exclusive_scan_u32(const unsigned *in, int64_t n, int64_t *out, void *ws, cu
 size_t scan_workspace(int64_t n);
 
 // Degree of row r of A (or A+I): the reference folds the row's stored values
-// left to right (np.bincount).  When the exactness certificate holds any
-// order is bitwise equal, so the warp reduces in parallel; otherwise lane 0
-// replays the exact sequential fold.
+// left to right (np.bincount, sparse.py:196).  Three tiers, each exact:
+//  * a thread per row of <= kDegShort entries folds it itself, in order;
+//  * a warp per longer row: when the exactness certificate holds (every
+//    addend a multiple of 2^m, sum|x| < 2^(m+52)) any order is bitwise equal,
+//    so the warp reduces in parallel; otherwise lane 0 replays the fold;
+//  * rows over kDegHub entries are listed and taken by a whole CTA each
+//    (k_degree_hub) -- a hub row would otherwise hold one warp for the kernel.
+constexpr int kDegShort = 16;
+constexpr int64_t kDegHub = 4096;
+constexpr int kDegU = 4;  // entries per lane loaded before any is used
+
+__device__ __forceinline__ void degree_store(double *deg, double *scale, int64_t r, double d, int32_t *err) {
+    deg[r] = d;
+    if (scale) scale[r] = laplacian_scale(d, err);
+}
+
+// the exact sequential fold of row r, entries [s, e), the A+I diagonal
+// merged into a stored (r, r) or inserted at its sorted position
+__device__ __forceinline__ double fold_row(const int32_t *col, const double *val, int64_t r, int64_t s, int64_t e,
+                                           bool diag) {
+    double d = 0.0;
+    bool ins = !diag;
+    int64_t p = s;
+    for (; p + 4 <= e; p += 4) {
+        int32_t c4[4];
+        double x4[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            c4[j] = col[p + j];
+            x4[j] = val[p + j];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            double x = x4[j];
+            if (diag && (int64_t)c4[j] == r) {
+                x = x + 1.0;
+                ins = true;
+            } else if (!ins && (int64_t)c4[j] > r) {
+                d += 1.0;
+                ins = true;
+            }
+            d += x;
+        }
+    }
+    for (; p < e; ++p) {
+        const int64_t c = col[p];
+        double x = val[p];
+        if (diag && c == r) {
+            x = x + 1.0;
+            ins = true;
+        } else if (!ins && c > r) {
+            d += 1.0;
+            ins = true;
+        }
+        d += x;
+    }
+    if (!ins) d += 1.0;
+    return d;
+}
+
 __global__ void k_degree(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                          const double *__restrict__ val, int64_t n, unsigned flags,
                          double *__restrict__ deg, double *__restrict__ scale, int32_t *err,
-                         const unsigned *guard) {
+                         const unsigned *guard, unsigned *__restrict__ hubs, unsigned *__restrict__ n_hubs,
+                         unsigned *__restrict__ work) {
     if (guard && *guard == 0) return;  // device-side skip (unit-weight graphs use k_degree_stream)
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const bool diag = (flags & GEE_DIAGONAL) != 0;
-    for (int64_t r = warp; r < n; r += nwarps) {
+    // A warp takes 32 rows at a time, rows c, c + nc, c + 2 nc, ... of chunk c
+    // (long rows cluster by id in power-law graphs); lanes fold the short
+    // ones.  Chunks are grabbed from a counter when there is one, else dealt
+    // round robin.
+    const int64_t nc = (n + 31) / 32;
+    int64_t c = warp;
+    for (;;) {
+        if (work) {
+            unsigned t = 0;
+            if (lane == 0) t = atomicAdd(work, 1u);
+            c = __shfl_sync(0xffffffffu, t, 0);
+        }
+        if (c >= nc) break;
+        const int64_t r = c + (int64_t)lane * nc;
+        const int64_t r0 = c;
+        int64_t s = 0, e = 0;
+        if (r < n) {
+            s = row_ptr[r];
+            e = row_ptr[r + 1];
+        }
+        const int64_t L = e - s;
+        if (r < n && L <= kDegShort) degree_store(deg, scale, r, fold_row(col, val, r, s, e, diag), err);
+        // with a hub list, rows over kDegHub go to k_degree_hub; without one
+        // (gee_degree has no workspace) the warp takes them too
+        const bool hub = hubs && L > kDegHub;
+        unsigned longer = __ballot_sync(0xffffffffu, r < n && L > kDegShort && !hub);
+        if (r < n && hub) hubs[atomicAdd(n_hubs, 1u)] = (unsigned)r;
+        while (longer) {
+            const int src = __ffs(longer) - 1;
+            longer &= longer - 1;
+            const int64_t rr = r0 + (int64_t)src * nc;
+            const int64_t ss = __shfl_sync(0xffffffffu, s, src), ee = __shfl_sync(0xffffffffu, e, src);
+            Cert ce;
+            double psum = 0.0;
+            bool placed = false;
+            for (int64_t p0 = ss + lane; p0 < ee; p0 += 32 * kDegU) {
+                double xs[kDegU];
+                int32_t cs[kDegU];
+#pragma unroll
+                for (int j = 0; j < kDegU; ++j) {
+                    const int64_t p = p0 + 32 * j;
+                    xs[j] = p < ee ? val[p] : 0.0;
+                    cs[j] = (diag && p < ee) ? col[p] : -1;
+                }
+#pragma unroll
+                for (int j = 0; j < kDegU; ++j) {
+                    double x = xs[j];
+                    if (diag && (int64_t)cs[j] == rr) {
+                        x = x + 1.0;
+                        placed = true;
+                    }
+                    ce.add(x);  // zeros (padding included) change nothing
+                    psum += x;
+                }
+            }
+            const bool insert = diag && !__any_sync(0xffffffffu, placed);
+            int mlow = warp_min(ce.mlow);
+            const double sabs = warp_sum(ce.sabs) + (insert ? 1.0 : 0.0);
+            if (insert) mlow = min(mlow, 0);
+            const bool ok = cert_ok(mlow, sabs);
+            const double tot = warp_sum(psum);
+            if (lane == 0) degree_store(deg, scale, rr, ok ? tot + (insert ? 1.0 : 0.0) : fold_row(col, val, rr, ss, ee, diag), err);
+        }
+        if (!work) c += nwarps;
+    }
+}
+
+// one CTA per hub row: certificate by block reductions, else thread 0 folds
+// while the other warps stage the next 2048 entries in shared memory
+constexpr int kHubThreads = 512, kHubStage = 1536;
+__global__ void __launch_bounds__(kHubThreads) k_degree_hub(const int64_t *__restrict__ row_ptr,
+                                                            const int32_t *__restrict__ col,
+                                                            const double *__restrict__ val, unsigned flags,
+                                                            double *__restrict__ deg, double *__restrict__ scale,
+                                                            int32_t *err, const unsigned *guard,
+                                                            const unsigned *__restrict__ hubs,
+                                                            const unsigned *__restrict__ n_hubs) {
+    if (guard && *guard == 0) return;
+    __shared__ int32_t sc[2][kHubStage];
+    __shared__ double sv[2][kHubStage];
+    __shared__ double dred[33];
+    __shared__ int ired[33];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const bool diag = (flags & GEE_DIAGONAL) != 0;
+    for (unsigned h = blockIdx.x; h < *n_hubs; h += gridDim.x) {
+        const int64_t r = hubs[h];
         const int64_t s = row_ptr[r], e = row_ptr[r + 1];
         Cert ce;
         double psum = 0.0;
-        bool placed = false;
-        for (int64_t p = s + lane; p < e; p += 32) {
-            double x = val[p];
-            if (diag && col[p] == r) {
-                x = x + 1.0;
-                placed = true;
+        int placed = 0;
+        for (int64_t p0 = s + tid; p0 < e; p0 += (int64_t)nt * kDegU) {
+            double xs[kDegU];
+            int32_t cs[kDegU];
+#pragma unroll
+            for (int j = 0; j < kDegU; ++j) {
+                const int64_t p = p0 + (int64_t)nt * j;
+                xs[j] = p < e ? val[p] : 0.0;
+                cs[j] = (diag && p < e) ? col[p] : -1;
             }
-            ce.add(x);
-            psum += x;
+#pragma unroll
+            for (int j = 0; j < kDegU; ++j) {
+                double x = xs[j];
+                if (diag && (int64_t)cs[j] == r) {
+                    x = x + 1.0;
+                    placed = 1;
+                }
+                ce.add(x);
+                psum += x;
+            }
         }
-        const bool insert = diag && !__any_sync(0xffffffffu, placed);
-        int mlow = warp_min(ce.mlow);
-        double sabs = warp_sum(ce.sabs) + (insert ? 1.0 : 0.0);
+        placed = __syncthreads_or(placed);
+        const bool insert = diag && !placed;
+        int mlow = block_min(ce.mlow, ired);
+        const double sabs = block_sum(ce.sabs, dred) + (insert ? 1.0 : 0.0);
         if (insert) mlow = min(mlow, 0);
-        double d;
         if (cert_ok(mlow, sabs)) {
-            d = warp_sum(psum) + (insert ? 1.0 : 0.0);
-        } else {
-            d = 0.0;
-            if (lane == 0) {
-                bool ins = !insert;
-                for (int64_t p = s; p < e; ++p) {
-                    int64_t c = col[p];
-                    double x = val[p];
-                    if (!ins && c > r) {
+            const double d = block_sum(psum, dred) + (insert ? 1.0 : 0.0);
+            if (tid == 0) degree_store(deg, scale, r, d, err);
+            continue;
+        }
+        double d = 0.0;
+        bool ins = !diag;
+        const int64_t L = e - s;
+        for (int64_t i = tid; i < (L < (int64_t)kHubStage ? L : (int64_t)kHubStage); i += nt) {
+            sc[0][i] = col[s + i];
+            sv[0][i] = val[s + i];
+        }
+        __syncthreads();
+        for (int64_t b = 0; b < L; b += kHubStage) {
+            const int half = (int)((b / kHubStage) & 1);
+            const int nb = (int)(L - b < (int64_t)kHubStage ? L - b : (int64_t)kHubStage);
+            const int64_t bn = b + kHubStage;
+            const int nn = bn < L ? (int)(L - bn < (int64_t)kHubStage ? L - bn : (int64_t)kHubStage) : 0;
+            if (tid >= 32) {
+                for (int i = tid - 32; i < nn; i += nt - 32) {
+                    sc[half ^ 1][i] = col[s + bn + i];
+                    sv[half ^ 1][i] = val[s + bn + i];
+                }
+            } else if (tid == 0) {
+                for (int i = 0; i < nb; ++i) {
+                    double x = sv[half][i];
+                    const int64_t c = sc[half][i];
+                    if (diag && c == r) {
+                        x = x + 1.0;
+                        ins = true;
+                    } else if (!ins && c > r) {
                         d += 1.0;
                         ins = true;
                     }
-                    if (diag && c == r) x = x + 1.0;
                     d += x;
                 }
-                if (!ins) d += 1.0;
             }
+            __syncthreads();
         }
-        if (lane == 0) {
-            deg[r] = d;
-            if (scale) scale[r] = laplacian_scale(d, err);
+        if (tid == 0) {
+            if (!ins) d += 1.0;
+            degree_store(deg, scale, r, d, err);
         }
+        __syncthreads();
     }
 }
+
+// hub_buf: [1 + nnz / kDegHub] words (count, then row ids) or null
+static int launch_degree(const int64_t *row_ptr, const int32_t *col, const double *val, int64_t n, unsigned flags,
+                         double *deg, double *scale, int32_t *err, const unsigned *guard, unsigned *hub_buf,
+                         cudaStream_t st) {
+    // hub_buf: [0] hub count, [1] chunk counter, [2..] hub rows
+    if (hub_buf) GEE_CHECK_CUDA(cudaMemsetAsync(hub_buf, 0, 2 * sizeof(unsigned), st));
+    k_degree<<<grid_for((n + 31) / 32 * 32, 256, 8), 256, 0, st>>>(row_ptr, col, val, n, flags, deg, scale, err,
+                                                                   guard, hub_buf ? hub_buf + 2 : nullptr, hub_buf,
+                                                                   hub_buf ? hub_buf + 1 : nullptr);
+    GEE_CHECK_LAUNCH("k_degree");
+    if (hub_buf) {
+        k_degree_hub<<<(unsigned)num_sms(), kHubThreads, 0, st>>>(row_ptr, col, val, flags, deg, scale, err, guard,
+                                                                  hub_buf + 2, hub_buf);
+        GEE_CHECK_LAUNCH("k_degree_hub");
+    }
+    return GEE_OK;
+}
+
+size_t degree_hub_words(int64_t nnz) { return 3 + (size_t)(nnz / kDegHub); }
 
 int degree(const int64_t *row_ptr, const int32_t *col, const double *val, int64_t n, unsigned flags,
            double *deg, double *scale, int32_t *err, cudaStream_t st) {
     if (n <= 0) return GEE_OK;
-    k_degree<<<grid_for(n * 32, 256, 8), 256, 0, st>>>(row_ptr, col, val, n, flags, deg, scale, err,
-                                                       nullptr);
-    GEE_CHECK_LAUNCH("k_degree");
-    return GEE_OK;
+    return launch_degree(row_ptr, col, val, n, flags, deg, scale, err, nullptr, nullptr, st);
 }
 
-// degree() that runs only if the device word *guard is nonzero
+// degree() that runs only if the device word *guard is nonzero; hub_buf
+// (degree_hub_words(nnz) words of workspace) lets a CTA take each hub row
 int degree_guarded(const int64_t *row_ptr, const int32_t *col, const double *val, int64_t n,
                    unsigned flags, double *deg, double *scale, int32_t *err, const unsigned *guard,
-                   cudaStream_t st) {
+                   unsigned *hub_buf, cudaStream_t st) {
     if (n <= 0) return GEE_OK;
-    k_degree<<<grid_for(n * 32, 256, 8), 256, 0, st>>>(row_ptr, col, val, n, flags, deg, scale, err,
-                                                       guard);
-    GEE_CHECK_LAUNCH("k_degree");
-    return GEE_OK;
+    return launch_degree(row_ptr, col, val, n, flags, deg, scale, err, guard, hub_buf, st);
 }
 
 // ---- A + I ------------------------------------------------------------------

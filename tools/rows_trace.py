@@ -37,3 +37,9 @@ ls = np.array(buf3, dtype=np.int64).reshape(512, 4)[:296]
 o = np.argsort(-(ls[:, 1] + ls[:, 2]))
 for i in o[:6]:
     print("CTA", i, "row", ls[i, 3], "L", ls[i, 0], "lsd cycles", ls[i, 1], "finish cycles", ls[i, 2])
+buf4 = (ctypes.c_ulonglong * (512 * 8))()
+lib.gee_fin_dump(buf4)
+fn = np.array(buf4, dtype=np.int64).reshape(512, 8)[:296]
+o = np.argsort(-fn[:, 0])
+for i in o[:6]:
+    print("CTA", i, "row", fn[i, 6], "L", fn[i, 0], "runs", fn[i, 1], "scan+out", fn[i, 2], "cert", fn[i, 3], "degree", fn[i, 4], "certified", fn[i, 5])
