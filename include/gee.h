@@ -200,10 +200,10 @@ int gee_profile_read(float *ms, const char **names, int cap);
 
 /* Test hook (thread-local) selecting the CSR assembly path so parity tests
  * cover all three: GEE_DEBUG_FORCE_BUCKETS = 0 default (bitmap for small
- * unit-weight graphs, radix sort when (row, col) packs into 32 bits, row
- * buckets otherwise), 1 = row buckets, 2 = never the bitmap path, 3 = as 2
- * with the radix sort also on 64-bit (row, col) keys.  Returns the previous
- * value. */
+ * unit-weight graphs, radix sort when (row, col) packs into 32 bits or the
+ * graph is weighted, row buckets otherwise), 1 = row buckets, 2 = never the
+ * bitmap path, 3 = as 2 with the radix sort on every 64-bit (row, col) key.
+ * Returns the previous value. */
 #define GEE_DEBUG_FORCE_BUCKETS 1
 int gee_debug_set(int key, int value);
 

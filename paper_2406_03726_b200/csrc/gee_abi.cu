@@ -62,7 +62,7 @@ int inv_counts(const int64_t *counts, int32_t k, double *inv_nk, cudaStream_t st
 int label_hist_pipeline(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_t *counts, double *inv_nk,
                         unsigned *partial, unsigned *done, int32_t *err, cudaStream_t st);
 size_t csr_build_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
-bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
+bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed, int wt);
 int set_force_buckets(int v);
 int sort_csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, int64_t E, int64_t n_rows,
                    int64_t n_cols, int directed, int force_vals, int64_t *row_ptr, int32_t *col, double *val,
@@ -366,7 +366,7 @@ int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, in
     if (rc) return rc;
     const unsigned deg_flags = (flags & GEE_LAPLACIAN) ? (GEE_LAPLACIAN | (flags & GEE_DIAGONAL)) : 0u;
     const double *sc = (flags & GEE_LAPLACIAN) ? W.scale : nullptr;
-    if (sort_path_ok(n_edges, n_nodes, n_nodes, directed)) {
+    if (sort_path_ok(n_edges, n_nodes, n_nodes, directed, w_type)) {
         // compact CSR from the radix sort; values stay implicit (1.0) when the
         // graph has unit weights and no duplicate entries
         unsigned *val_mode = nullptr;

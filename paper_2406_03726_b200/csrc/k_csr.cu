@@ -1093,18 +1093,24 @@ static size_t carve_csr(Carver &cv, CsrWs &w, int64_t E, int64_t n_rows, int dir
     return cv.bytes();
 }
 
-bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
+bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed, int wt);
 size_t sort_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
 int sort_csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, int64_t E, int64_t n_rows,
                    int64_t n_cols, int directed, int force_vals, int64_t *row_ptr, int32_t *col, double *val,
                    int64_t *nnz, unsigned deg_flags, double *deg, double *scale, void *ws, size_t ws_bytes,
                    unsigned **val_mode, int32_t *err, cudaStream_t st);
 
+// the weight type is not known here: room for whichever path csr_build picks
 size_t csr_build_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int directed) {
-    if (sort_path_ok(E, n_rows, n_cols, directed)) return sort_workspace(E, n_rows, n_cols, directed);
-    Carver cv(nullptr);
-    CsrWs w;
-    return carve_csr(cv, w, E, n_rows, directed);
+    size_t need = 0;
+    if (sort_path_ok(E, n_rows, n_cols, directed, -1)) need = sort_workspace(E, n_rows, n_cols, directed);
+    if (!sort_path_ok(E, n_rows, n_cols, directed, GEE_W_UNIT)) {
+        Carver cv(nullptr);
+        CsrWs w;
+        const size_t b = carve_csr(cv, w, E, n_rows, directed);
+        need = need > b ? need : b;
+    }
+    return need;
 }
 
 __global__ void k_row_cnt(const int64_t *__restrict__ row_ptr, int64_t n, unsigned *__restrict__ cnt) {
@@ -1133,7 +1139,7 @@ int csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, i
               unsigned *row_cnt, int32_t *col, double *val, int64_t *nnz, unsigned deg_flags,
               double *deg, double *scale, void *ws, size_t ws_bytes, int32_t *err,
               cudaStream_t st) {
-    if (sort_path_ok(E, n_rows, n_cols, directed)) {
+    if (sort_path_ok(E, n_rows, n_cols, directed, wt)) {
         // packed (row, col) keys: radix-sort path, always a compact CSR
         int rc = sort_csr_build(rows, cols, w, wt, E, n_rows, n_cols, directed, 1, row_ptr, col, val, nnz,
                                 deg_flags, deg, scale, ws, ws_bytes, nullptr, err, st);

@@ -477,17 +477,21 @@ int set_force_buckets(int v) {
 
 int force_path() { return t_force_buckets; }
 
-bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed) {
+// wt: the graph's weight type, or -1 when unknown (workspace sizing)
+bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed, int wt) {
     if (t_force_buckets == 1) return false;
     const int rb = bitlen(n_rows);  // rows <= n_rows-1 < 2^rb - 1: keys stay below the sentinel
     const int cb = bitlen(n_cols > 1 ? n_cols - 1 : 1);
     const int64_t Mv = directed ? E : 2 * E;
-    // 30-bit look-back counts; int32 columns.  By default only 32-bit keys:
-    // with 64-bit keys the row-bucket path measures faster on configs 2-4
-    // (weighted hub rows: its fused degree fold; unit weights: fewer passes);
-    // test hook 3 selects the 64-bit sort to keep it covered.
-    const int maxbits = t_force_buckets == 3 ? 64 : 32;
-    return rb + cb <= maxbits && Mv < ((int64_t)1 << 30) && n_rows > 0 && n_cols <= ((int64_t)1 << 31);
+    // 30-bit look-back counts; int32 columns
+    if (!(Mv < ((int64_t)1 << 30) && n_rows > 0 && n_cols <= ((int64_t)1 << 31))) return false;
+    if (rb + cb <= 32) return true;
+    if (rb + cb > 64) return false;
+    // 64-bit keys: the sort carries weights in stream order and the degree
+    // kernel is tiered, which beats the row buckets on weighted graphs
+    // (configs 2, 3); unit-weight graphs keep the buckets (config 4), whose
+    // fused degree is the stream length.  Test hook 3 forces the sort.
+    return t_force_buckets == 3 || wt == GEE_W_F64 || wt == GEE_W_F32 || wt < 0;
 }
 
 static int sort_keybits(int64_t n_rows, int64_t n_cols) {

@@ -152,7 +152,20 @@ __global__ void k_degree(const int64_t *__restrict__ row_ptr, const int32_t *__r
 
 // one CTA per hub row: certificate by block reductions, else thread 0 folds
 // while the other warps stage the next 2048 entries in shared memory
-constexpr int kHubThreads = 512, kHubStage = 1536;
+constexpr int kHubThreads = 512, kHubStage = 2048;
+__device__ __forceinline__ double fold_plain(const double *x, int lo, int hi, double d) {
+    int i = lo;
+    for (; i + 8 <= hi; i += 8) {
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = x[i + j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d += v[j];
+    }
+    for (; i < hi; ++i) d += x[i];
+    return d;
+}
+
 __global__ void __launch_bounds__(kHubThreads) k_degree_hub(const int64_t *__restrict__ row_ptr,
                                                             const int32_t *__restrict__ col,
                                                             const double *__restrict__ val, unsigned flags,
@@ -161,7 +174,6 @@ __global__ void __launch_bounds__(kHubThreads) k_degree_hub(const int64_t *__res
                                                             const unsigned *__restrict__ hubs,
                                                             const unsigned *__restrict__ n_hubs) {
     if (guard && *guard == 0) return;
-    __shared__ int32_t sc[2][kHubStage];
     __shared__ double sv[2][kHubStage];
     __shared__ double dred[33];
     __shared__ int ired[33];
@@ -170,9 +182,11 @@ __global__ void __launch_bounds__(kHubThreads) k_degree_hub(const int64_t *__res
     for (unsigned h = blockIdx.x; h < *n_hubs; h += gridDim.x) {
         const int64_t r = hubs[h];
         const int64_t s = row_ptr[r], e = row_ptr[r + 1];
+        const int64_t L = e - s;
         Cert ce;
         double psum = 0.0;
         int placed = 0;
+        int kfirst = INT_MAX;  // first position whose column is >= r (where A+I's diagonal goes)
         for (int64_t p0 = s + tid; p0 < e; p0 += (int64_t)nt * kDegU) {
             double xs[kDegU];
             int32_t cs[kDegU];
@@ -185,6 +199,7 @@ __global__ void __launch_bounds__(kHubThreads) k_degree_hub(const int64_t *__res
 #pragma unroll
             for (int j = 0; j < kDegU; ++j) {
                 double x = xs[j];
+                if (diag && (int64_t)cs[j] >= r) kfirst = min(kfirst, (int)(p0 + (int64_t)nt * j - s));
                 if (diag && (int64_t)cs[j] == r) {
                     x = x + 1.0;
                     placed = 1;
@@ -203,42 +218,40 @@ __global__ void __launch_bounds__(kHubThreads) k_degree_hub(const int64_t *__res
             if (tid == 0) degree_store(deg, scale, r, d, err);
             continue;
         }
+        // The exact fold: plain left-to-right adds with the diagonal applied at
+        // position kfirst (merged into the stored value, or a 1.0 inserted
+        // before it), so thread 0's loop is a pure add chain over shared
+        // memory while warps 1.. stage the next kHubStage values.
+        const int64_t kd = diag ? min((int64_t)block_min(kfirst, ired), L) : L + 1;
+        auto stage = [&](int64_t b, int buf, int t0, int tstep) {
+            const int nb = (int)(L - b < (int64_t)kHubStage ? L - b : (int64_t)kHubStage);
+            for (int i = t0; i < nb; i += tstep) {
+                double x = val[s + b + i];
+                if (placed && b + i == kd) x = x + 1.0;
+                sv[buf][i] = x;
+            }
+        };
         double d = 0.0;
-        bool ins = !diag;
-        const int64_t L = e - s;
-        for (int64_t i = tid; i < (L < (int64_t)kHubStage ? L : (int64_t)kHubStage); i += nt) {
-            sc[0][i] = col[s + i];
-            sv[0][i] = val[s + i];
-        }
+        stage(0, 0, tid, nt);
         __syncthreads();
         for (int64_t b = 0; b < L; b += kHubStage) {
             const int half = (int)((b / kHubStage) & 1);
             const int nb = (int)(L - b < (int64_t)kHubStage ? L - b : (int64_t)kHubStage);
-            const int64_t bn = b + kHubStage;
-            const int nn = bn < L ? (int)(L - bn < (int64_t)kHubStage ? L - bn : (int64_t)kHubStage) : 0;
             if (tid >= 32) {
-                for (int i = tid - 32; i < nn; i += nt - 32) {
-                    sc[half ^ 1][i] = col[s + bn + i];
-                    sv[half ^ 1][i] = val[s + bn + i];
-                }
+                if (b + kHubStage < L) stage(b + kHubStage, half ^ 1, tid - 32, nt - 32);
             } else if (tid == 0) {
-                for (int i = 0; i < nb; ++i) {
-                    double x = sv[half][i];
-                    const int64_t c = sc[half][i];
-                    if (diag && c == r) {
-                        x = x + 1.0;
-                        ins = true;
-                    } else if (!ins && c > r) {
-                        d += 1.0;
-                        ins = true;
-                    }
-                    d += x;
+                if (insert && kd >= b && kd < b + nb) {
+                    d = fold_plain(sv[half], 0, (int)(kd - b), d);
+                    d += 1.0;
+                    d = fold_plain(sv[half], (int)(kd - b), nb, d);
+                } else {
+                    d = fold_plain(sv[half], 0, nb, d);
                 }
             }
             __syncthreads();
         }
         if (tid == 0) {
-            if (!ins) d += 1.0;
+            if (insert && kd >= L) d += 1.0;
             degree_store(deg, scale, r, d, err);
         }
         __syncthreads();

@@ -29,7 +29,8 @@ PATHS = ["default", "sort", "buckets", "sort64"]
 class assembly_path:
     """Select the CSR-assembly path via the library's test hook: "default"
     (column bitmaps for unit-weight graphs with <= 16384 nodes, else the
-    radix sort when (row, col) packs into 32 bits, else row buckets),
+    radix sort when (row, col) packs into 32 bits or the graph is weighted,
+    else row buckets),
     "sort" (never the bitmap path), "buckets" (always row buckets) or
     "sort64" (the radix sort also on 64-bit (row, col) keys)."""
 
@@ -278,7 +279,7 @@ def test_weighted_long_rows_exact_degree_fold():
 
 
 def test_large_n_multigraph_default_path():
-    # n > 65535: (row, col) no longer packs into 32 bits -> bucket path by default
+    # n > 65535: (row, col) no longer packs into 32 bits -> 64-bit radix sort by default (weighted)
     rng = np.random.default_rng(77)
     n = 100_000
     rows = np.concatenate([np.full(6000, 4242), rng.integers(0, n, 300_000)])
