@@ -211,15 +211,24 @@ __device__ __forceinline__ unsigned lookback_digit(const unsigned *status, int64
     return excl;
 }
 
-// dynamic shared memory: the tile's keys (K[kSortTile]) then payloads
+// dynamic shared memory: the tile's keys (K[kSortTile]), the reordered
+// payloads, then the payloads in input order (prefetched with cp.async)
 template <typename K, typename P>
-constexpr size_t onesweep_smem() { return (size_t)kSortTile * (sizeof(K) + sizeof(P)); }
+constexpr size_t onesweep_smem() { return (size_t)kSortTile * (sizeof(K) + 2 * sizeof(P)); }
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void *smem, const void *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem), "n"(BYTES)
+                 : "memory");
+}
 
 template <typename K, typename P>
 __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(OnesweepArgs<K, P> a) {
     extern __shared__ __align__(16) unsigned char os_dyn[];
     K *sk = reinterpret_cast<K *>(os_dyn);
     P *sp = reinterpret_cast<P *>(os_dyn + (size_t)kSortTile * sizeof(K));
+    P *spin = sp + kSortTile;
     __shared__ unsigned whist[kSortWarps][256];
     __shared__ unsigned tstart[256], gbase[256];
     __shared__ unsigned red[33];
@@ -244,6 +253,20 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(OnesweepArgs<K, P>
         }
     }
     const bool carry = *a.nonunit != 0;  // read after the key loads are in flight
+    if (carry) {
+        // the payloads land in shared memory in the background while the
+        // tile is ranked and its digit offsets are looked back
+#pragma unroll
+        for (int j = 0; j < kSortItems; ++j) {
+            const int i = wid * (kSortTile / kSortWarps) + j * 32 + lane;
+            if (i < nvalid) {
+                const int64_t v = t0 + i;
+                const P *src = a.first ? static_cast<const P *>(a.w) + (v < a.g.E ? v : v - a.g.E) : a.pin + v;
+                cp_async<sizeof(P)>(spin + i, src);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     // stable warp multisplit
     unsigned *wh = whist[wid];
 #pragma unroll
@@ -296,8 +319,8 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(OnesweepArgs<K, P>
             const unsigned pos = tstart[dd] + whist[wid][dd] + rank[j];
             sk[pos] = key[j];
             if (carry) {
-                const int64_t v = t0 + i;
-                sp[pos] = a.first ? weight_bits<P>(a.w, v < a.g.E ? v : v - a.g.E) : a.pin[v];
+                if (j == 0) asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's own copies
+                sp[pos] = spin[i];
             }
         }
     }
