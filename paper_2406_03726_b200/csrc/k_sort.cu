@@ -355,8 +355,27 @@ struct DedupArgs {
     int force_vals;       // 1: always write out_val; 2: only run if *has_multi
 };
 
+// k_dedup stages its tile in shared memory: keys and payloads (read once,
+// coalesced; index i stored at i + i/16 so a thread's 16 consecutive entries
+// hit distinct banks), then the compacted outputs, written back coalesced.
+template <typename K, typename P>
+constexpr size_t dedup_smem() {
+    constexpr size_t kpad = (size_t)(kSortTile + kSortTile / 16) * sizeof(K);
+    constexpr size_t ppad = (size_t)(kSortTile + kSortTile / 16) * sizeof(P);
+    constexpr size_t outb = (size_t)kSortTile * (sizeof(int32_t) + sizeof(double));
+    return kpad + (ppad > outb ? ppad : outb);
+}
+
+__device__ __forceinline__ int dpad(int i) { return i + (i >> 4); }
+
 template <typename K, typename P>
 __global__ void __launch_bounds__(kSortThreads) k_dedup(DedupArgs<K, P> a) {
+    extern __shared__ __align__(16) unsigned char dd_dyn[];
+    K *sk = reinterpret_cast<K *>(dd_dyn);
+    unsigned char *area = dd_dyn + (size_t)(kSortTile + kSortTile / 16) * sizeof(K);
+    P *sp = reinterpret_cast<P *>(area);                     // pass 1
+    double *oval = reinterpret_cast<double *>(area);         // pass 2 (after sp is consumed)
+    int32_t *ocol = reinterpret_cast<int32_t *>(area + (size_t)kSortTile * sizeof(double));
     __shared__ unsigned red[33];
     __shared__ unsigned s_excl;
     __shared__ int s_tile;
@@ -370,37 +389,45 @@ __global__ void __launch_bounds__(kSortThreads) k_dedup(DedupArgs<K, P> a) {
     const K cmask = ((K)1 << a.g.colbits) - (K)1;
     const K sentinel = (K)a.g.sentinel;
     const int cb = a.g.colbits;
-    const int64_t p0 = tile * kSortTile + (int64_t)threadIdx.x * kSortItems;
-    const int64_t p1 = min(Mv, p0 + kSortItems);
+    const int64_t tb = tile * kSortTile;
+    const int n = (int)min((int64_t)kSortTile, Mv - tb);
+    for (int i = threadIdx.x; i < n; i += kSortThreads) {
+        sk[dpad(i)] = a.key[tb + i];
+        if (carry) sp[dpad(i)] = a.pay[tb + i];
+    }
+    const K kprev = tb > 0 ? a.key[tb - 1] : (K)0;
+    __syncthreads();
+    const int i0 = threadIdx.x * kSortItems;
     // pass 1: runs headed in my range -> values, keep flags
     unsigned keepbits = 0;
     double vals[kSortItems];
     bool multi = false;
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
-        const int64_t p = p0 + j;
+        const int i = i0 + j;
         vals[j] = 0.0;
-        if (p >= p1) continue;
-        const K k = a.key[p];
+        if (i >= n) continue;
+        const K k = sk[dpad(i)];
         if (k == sentinel) continue;
-        if (p > 0 && a.key[p - 1] == k) continue;
-        int64_t q = p + 1;
-        while (q < Mv && a.key[q] == k) ++q;
+        const K kb = i > 0 ? sk[dpad(i - 1)] : kprev;
+        if ((tb + i > 0) && kb == k) continue;
+        int64_t q = i + 1;  // run end, possibly past the tile (then read from global memory)
+        while (tb + q < Mv && (q < n ? sk[dpad((int)q)] : a.key[tb + q]) == k) ++q;
         double acc;
         if (carry) {
             // the run is in stream order (stable sort of the stream): sum left to right
-            acc = pay_value<P>(a.pay[p]);
-            for (int64_t i = p + 1; i < q; ++i) acc += pay_value<P>(a.pay[i]);
+            acc = pay_value<P>(sp[dpad(i)]);
+            for (int64_t t = i + 1; t < q; ++t) acc += pay_value<P>(t < n ? sp[dpad((int)t)] : a.pay[tb + t]);
         } else {
-            acc = (double)(q - p);
-            multi |= q - p > 1;
+            acc = (double)(q - i);
+            multi |= q - i > 1;
         }
         vals[j] = acc;
         if (acc != 0.0) keepbits |= 1u << j;
     }
     if (multi) atomicOr(a.has_multi, 1u);
     unsigned cnt = __popc(keepbits), ttot;
-    unsigned off = block_exclusive_scan(cnt, red, &ttot);
+    unsigned off = block_exclusive_scan(cnt, red, &ttot);  // its barriers also retire sp
     // look-back for the tile's output offset: warp 0 inspects 32 predecessor
     // tiles per step (lane l reads tile t-1-l)
     if (threadIdx.x < 32) {
@@ -414,15 +441,15 @@ __global__ void __launch_bounds__(kSortThreads) k_dedup(DedupArgs<K, P> a) {
             int64_t t = tile - 1;
             while (t >= 0) {
                 const int64_t mine = t - lane;
-                unsigned s = kFlagInc;  // lanes past tile 0 act as an inclusive zero
+                unsigned sw = kFlagInc;  // lanes past tile 0 act as an inclusive zero
                 if (mine >= 0) {
                     do {
-                        s = ld_acquire(a.status + mine);
-                    } while ((s & ~kValMask) == 0);
+                        sw = ld_acquire(a.status + mine);
+                    } while ((sw & ~kValMask) == 0);
                 }
-                const unsigned inc = __ballot_sync(0xffffffffu, (s & kFlagInc) != 0);
+                const unsigned inc = __ballot_sync(0xffffffffu, (sw & kFlagInc) != 0);
                 const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive word
-                unsigned v = lane <= stop ? (s & kValMask) : 0u;
+                unsigned v = lane <= stop ? (sw & kValMask) : 0u;
                 v = warp_sum_u(v);
                 excl += v;
                 if (inc) break;
@@ -433,33 +460,40 @@ __global__ void __launch_bounds__(kSortThreads) k_dedup(DedupArgs<K, P> a) {
         if (lane == 0) s_excl = excl;
     }
     __syncthreads();
-    int64_t o = (int64_t)s_excl + off;
-    // pass 2: emit entries; row starts write row_ptr / sptr for every row they open
+    const int64_t obase = (int64_t)s_excl;
+    unsigned lo = off;  // this thread's next slot in the tile's output
+    // pass 2: outputs into shared memory; row starts write row_ptr / sptr
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
-        const int64_t p = p0 + j;
-        if (p >= p1) break;
-        const K k = a.key[p];
+        const int i = i0 + j;
+        if (i >= n) break;
+        const int64_t p = tb + i;
+        const K k = sk[dpad(i)];
         const int64_t row = k == sentinel ? a.n_rows : (int64_t)(k >> cb);
-        const K kp = p == 0 ? (K)0 : a.key[p - 1];
+        const K kp = i > 0 ? sk[dpad(i - 1)] : kprev;
         const int64_t prow = p == 0 ? -1 : (kp == sentinel ? a.n_rows : (int64_t)(kp >> cb));
         if (row != prow) {
             for (int64_t r = prow + 1; r <= row && r <= a.n_rows; ++r) {
-                a.row_ptr[r] = o;
+                a.row_ptr[r] = obase + lo;
                 if (a.sptr) a.sptr[r] = p;
             }
         }
         if (keepbits >> j & 1u) {
-            a.out_col[o] = (int32_t)(k & cmask);
-            if (write_vals) a.out_val[o] = vals[j];
-            ++o;
+            ocol[lo] = (int32_t)(k & cmask);
+            oval[lo] = vals[j];
+            ++lo;
         }
         if (p == Mv - 1 && row < a.n_rows) {
             for (int64_t r = row + 1; r <= a.n_rows; ++r) {
-                a.row_ptr[r] = o;
+                a.row_ptr[r] = obase + lo;
                 if (a.sptr) a.sptr[r] = Mv;
             }
         }
+    }
+    __syncthreads();
+    for (unsigned t = threadIdx.x; t < ttot; t += kSortThreads) {
+        a.out_col[obase + t] = ocol[t];
+        if (write_vals) a.out_val[obase + t] = oval[t];
     }
 }
 
@@ -570,6 +604,8 @@ static int sort_passes(const SortGeom &g, const int64_t *rows, const int64_t *co
     if (!attr) {
         GEE_CHECK_CUDA(cudaFuncSetAttribute(k_onesweep<K, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)onesweep_smem<K, P>()));
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_dedup<K, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)dedup_smem<K, P>()));
         attr = true;
     }
     const int64_t tiles = W.tiles;
@@ -620,14 +656,14 @@ static int sort_passes(const SortGeom &g, const int64_t *rows, const int64_t *co
     d.nonunit = W.flags;
     d.has_multi = W.flags + 1;
     d.force_vals = force_vals ? 1 : 0;
-    k_dedup<K, P><<<(unsigned)tiles, kSortThreads, 0, st>>>(d);
+    k_dedup<K, P><<<(unsigned)tiles, kSortThreads, dedup_smem<K, P>(), st>>>(d);
     GEE_CHECK_LAUNCH("k_dedup");
     if (!force_vals) {
         // rare: unit weights with duplicates -> redo with values materialised
         d.status = W.status + (size_t)g.passes * tiles * 256 + (tiles + 1);
         d.tile_ctr = W.ctr + kMaxPasses + 1;
         d.force_vals = 2;
-        k_dedup<K, P><<<(unsigned)tiles, kSortThreads, 0, st>>>(d);
+        k_dedup<K, P><<<(unsigned)tiles, kSortThreads, dedup_smem<K, P>(), st>>>(d);
         GEE_CHECK_LAUNCH("k_dedup_fix");
     }
     return GEE_OK;
