@@ -551,8 +551,17 @@ bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed, int w
     return t_force_buckets == 3 || wt == GEE_W_F64 || wt == GEE_W_F32 || wt < 0;
 }
 
-static int sort_keybits(int64_t n_rows, int64_t n_cols) {
-    return bitlen(n_rows) + bitlen(n_cols > 1 ? n_cols - 1 : 1);
+// Key width.  Undirected streams need a sentinel above every real key (the
+// mirror of a self-loop): rows take bitlen(n_rows) bits so the all-ones key is
+// never a real one.  Directed streams have no mirrors: rows take
+// bitlen(n_rows - 1) bits (configs 3: 24 + 24 = 48 bits, six 8-bit passes).
+// 64-bit key words when the key needs them; a directed key keeps one spare
+// bit so the all-ones word stays unreachable
+static bool sort_wide_key(int keybits, int directed) { return keybits > (directed ? 31 : 32); }
+
+static int sort_keybits(int64_t n_rows, int64_t n_cols, int directed) {
+    const int rb = directed ? bitlen(n_rows > 1 ? n_rows - 1 : 1) : bitlen(n_rows);
+    return rb + bitlen(n_cols > 1 ? n_cols - 1 : 1);
 }
 
 struct SortWs {
@@ -569,8 +578,8 @@ struct SortWs {
 static void carve_sort(Carver &cv, SortWs &w, int64_t E, int64_t n_rows, int64_t n_cols, int directed) {
     const int64_t Mv = directed ? E : 2 * E;
     const int64_t tiles = (Mv + kSortTile - 1) / kSortTile;
-    const int keybits = sort_keybits(n_rows, n_cols);
-    const size_t kbytes = keybits > 32 ? 8 : 4;
+    const int keybits = sort_keybits(n_rows, n_cols, directed);
+    const size_t kbytes = sort_wide_key(keybits, directed) ? 8 : 4;
     w.tiles = tiles;
     w.passes = (keybits + 7) / 8;
     // hist, flags, counters and every look-back word are contiguous: one memset
@@ -685,14 +694,16 @@ int sort_csr_build(const int64_t *rows, const int64_t *cols, const void *w, int 
     g.Mv = directed ? E : 2 * E;
     g.directed = directed;
     g.colbits = bitlen(n_cols > 1 ? n_cols - 1 : 1);
-    const int keybits = sort_keybits(n_rows, n_cols);
-    g.sentinel = keybits >= 64 ? ~0ull : ((1ull << keybits) - 1ull);
+    const int keybits = sort_keybits(n_rows, n_cols, directed);
+    // directed: no sentinel key is ever produced; all-ones above the key width
+    // (or of the whole word) cannot match a real key
+    g.sentinel = directed ? ~0ull : (keybits >= 64 ? ~0ull : ((1ull << keybits) - 1ull));
     g.passes = W.passes;
     GEE_CHECK_CUDA(cudaMemsetAsync(W.hist, 0, W.zero_bytes, st));
     if (val_mode) *val_mode = W.flags;
     if (g.Mv > 0) {
         using u64 = unsigned long long;
-        const bool wide_key = keybits > 32, f64 = wt == GEE_W_F64;
+        const bool wide_key = sort_wide_key(keybits, directed), f64 = wt == GEE_W_F64;
         const int rc =
             wide_key ? (f64 ? sort_passes<u64, u64>(g, rows, cols, w, wt, n_rows, force_vals, row_ptr, col, val, W, st)
                             : sort_passes<u64, unsigned>(g, rows, cols, w, wt, n_rows, force_vals, row_ptr, col, val,
