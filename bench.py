@@ -213,6 +213,10 @@ def kernel_bytes(c, m_stream, nnz, wbytes):
     values are implicit 1.0 and never stored or read)."""
     n, e, k = int(c["n"]), int(c["e"]), int(c["k"])
     lap = bool(c["flags"] & 1)
+    directed = bool(c["directed"])
+    rb = (max(n - 1, 1)).bit_length() if directed else n.bit_length()
+    keybits = rb + (max(n - 1, 1)).bit_length()
+    kb = 8 if keybits > (31 if directed else 32) else 4  # sort key bytes
     vb = 8 if wbytes else 0  # stored CSR value bytes per entry
     np_ = (n + 255) // 256 * 256
     bm = np_ * np_ // 8
@@ -226,8 +230,12 @@ def kernel_bytes(c, m_stream, nnz, wbytes):
         "k_bm_table": 4 * n + 4 * n + 9 * n + 7 * n + (16 * n if lap else 0),
         "k_bm_scan": bm + 4 * n + 9 * n + (16 * n if lap else 0),
         "k_bm_gemm": bm + nbx * np_ + 8 * n * k + 4 * n + (8 * n if lap else 0),
-        # radix-sort path
+        # radix-sort path (k_sort.cu): key width as sort_keybits / sort_wide_key,
+        # payload = the weight in its own width (none for unit weights)
         "k_sort_hist": (16 + wbytes) * e,
+        "k_onesweep": 2 * m_stream * (kb + wbytes),
+        "k_dedup": m_stream * (kb + wbytes) + (4 + vb) * nnz + 16 * (n + 1),
+        "k_degree": (4 + vb) * nnz + 8 * (n + 1) + (16 * n if lap else 8 * n),
         # bucket path
         "k_count_part": 16 * e,
         "k_count_global": 16 * e,
