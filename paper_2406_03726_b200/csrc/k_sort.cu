@@ -27,9 +27,11 @@
 namespace gee {
 
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 4096
+constexpr int kSortItems = 12;  // one-sweep tile: 3,072 entries (measured best of 8/12/16)
+constexpr int kSortTile = kSortThreads * kSortItems;
 constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kDedupItems = 8;  // k_dedup tile: 2,048 entries (its look-back prefers more, smaller tiles)
+constexpr int kDedupTile = kSortThreads * kDedupItems;
 constexpr unsigned kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
 
 __device__ __forceinline__ double sort_load_w(const void *w, int wt, int64_t e) {
@@ -360,9 +362,9 @@ struct DedupArgs {
 // hit distinct banks), then the compacted outputs, written back coalesced.
 template <typename K, typename P>
 constexpr size_t dedup_smem() {
-    constexpr size_t kpad = (size_t)(kSortTile + kSortTile / 16) * sizeof(K);
-    constexpr size_t ppad = (size_t)(kSortTile + kSortTile / 16) * sizeof(P);
-    constexpr size_t outb = (size_t)kSortTile * (sizeof(int32_t) + sizeof(double));
+    constexpr size_t kpad = (size_t)(kDedupTile + kDedupTile / 16) * sizeof(K);
+    constexpr size_t ppad = (size_t)(kDedupTile + kDedupTile / 16) * sizeof(P);
+    constexpr size_t outb = (size_t)kDedupTile * (sizeof(int32_t) + sizeof(double));
     return kpad + (ppad > outb ? ppad : outb);
 }
 
@@ -372,10 +374,10 @@ template <typename K, typename P>
 __global__ void __launch_bounds__(kSortThreads) k_dedup(DedupArgs<K, P> a) {
     extern __shared__ __align__(16) unsigned char dd_dyn[];
     K *sk = reinterpret_cast<K *>(dd_dyn);
-    unsigned char *area = dd_dyn + (size_t)(kSortTile + kSortTile / 16) * sizeof(K);
+    unsigned char *area = dd_dyn + (size_t)(kDedupTile + kDedupTile / 16) * sizeof(K);
     P *sp = reinterpret_cast<P *>(area);                     // pass 1
     double *oval = reinterpret_cast<double *>(area);         // pass 2 (after sp is consumed)
-    int32_t *ocol = reinterpret_cast<int32_t *>(area + (size_t)kSortTile * sizeof(double));
+    int32_t *ocol = reinterpret_cast<int32_t *>(area + (size_t)kDedupTile * sizeof(double));
     __shared__ unsigned red[33];
     __shared__ unsigned s_excl;
     __shared__ int s_tile;
@@ -389,21 +391,21 @@ __global__ void __launch_bounds__(kSortThreads) k_dedup(DedupArgs<K, P> a) {
     const K cmask = ((K)1 << a.g.colbits) - (K)1;
     const K sentinel = (K)a.g.sentinel;
     const int cb = a.g.colbits;
-    const int64_t tb = tile * kSortTile;
-    const int n = (int)min((int64_t)kSortTile, Mv - tb);
+    const int64_t tb = tile * kDedupTile;
+    const int n = (int)min((int64_t)kDedupTile, Mv - tb);
     for (int i = threadIdx.x; i < n; i += kSortThreads) {
         sk[dpad(i)] = a.key[tb + i];
         if (carry) sp[dpad(i)] = a.pay[tb + i];
     }
     const K kprev = tb > 0 ? a.key[tb - 1] : (K)0;
     __syncthreads();
-    const int i0 = threadIdx.x * kSortItems;
+    const int i0 = threadIdx.x * kDedupItems;
     // pass 1: runs headed in my range -> values, keep flags
     unsigned keepbits = 0;
-    double vals[kSortItems];
+    double vals[kDedupItems];
     bool multi = false;
 #pragma unroll
-    for (int j = 0; j < kSortItems; ++j) {
+    for (int j = 0; j < kDedupItems; ++j) {
         const int i = i0 + j;
         vals[j] = 0.0;
         if (i >= n) continue;
@@ -464,7 +466,7 @@ __global__ void __launch_bounds__(kSortThreads) k_dedup(DedupArgs<K, P> a) {
     unsigned lo = off;  // this thread's next slot in the tile's output
     // pass 2: outputs into shared memory; row starts write row_ptr / sptr
 #pragma unroll
-    for (int j = 0; j < kSortItems; ++j) {
+    for (int j = 0; j < kDedupItems; ++j) {
         const int i = i0 + j;
         if (i >= n) break;
         const int64_t p = tb + i;
@@ -570,7 +572,7 @@ struct SortWs {
     void *keyA, *keyB;
     int64_t *sptr;
     unsigned *hubs;  // k_degree's hub-row list
-    int64_t tiles;
+    int64_t tiles, dtiles;  // one-sweep tiles, k_dedup tiles
     int passes;
     size_t zero_bytes;
 };
@@ -578,15 +580,17 @@ struct SortWs {
 static void carve_sort(Carver &cv, SortWs &w, int64_t E, int64_t n_rows, int64_t n_cols, int directed) {
     const int64_t Mv = directed ? E : 2 * E;
     const int64_t tiles = (Mv + kSortTile - 1) / kSortTile;
+    const int64_t dtiles = (Mv + kDedupTile - 1) / kDedupTile;
     const int keybits = sort_keybits(n_rows, n_cols, directed);
     const size_t kbytes = sort_wide_key(keybits, directed) ? 8 : 4;
     w.tiles = tiles;
+    w.dtiles = dtiles;
     w.passes = (keybits + 7) / 8;
     // hist, flags, counters and every look-back word are contiguous: one memset
     w.hist = cv.take<unsigned>(kMaxPasses * 256);
     w.flags = cv.take<unsigned>(4);   // [0] nonunit [1] has_multi
     w.ctr = cv.take<unsigned>(16);    // tile counters: passes 0..7, dedup, dedup-fix
-    const size_t status_words = (size_t)(tiles > 0 ? tiles : 1) * 256 * w.passes + (size_t)2 * (tiles + 1);
+    const size_t status_words = (size_t)(tiles > 0 ? tiles : 1) * 256 * w.passes + (size_t)2 * (dtiles + 1);
     w.status = cv.take<unsigned>(status_words);
     w.zero_bytes = (size_t)((char *)(w.status + status_words) - (char *)w.hist);
     const size_t m = (size_t)(Mv > 0 ? Mv : 1);
@@ -665,14 +669,14 @@ static int sort_passes(const SortGeom &g, const int64_t *rows, const int64_t *co
     d.nonunit = W.flags;
     d.has_multi = W.flags + 1;
     d.force_vals = force_vals ? 1 : 0;
-    k_dedup<K, P><<<(unsigned)tiles, kSortThreads, dedup_smem<K, P>(), st>>>(d);
+    k_dedup<K, P><<<(unsigned)W.dtiles, kSortThreads, dedup_smem<K, P>(), st>>>(d);
     GEE_CHECK_LAUNCH("k_dedup");
     if (!force_vals) {
         // rare: unit weights with duplicates -> redo with values materialised
-        d.status = W.status + (size_t)g.passes * tiles * 256 + (tiles + 1);
+        d.status = W.status + (size_t)g.passes * tiles * 256 + (W.dtiles + 1);
         d.tile_ctr = W.ctr + kMaxPasses + 1;
         d.force_vals = 2;
-        k_dedup<K, P><<<(unsigned)tiles, kSortThreads, dedup_smem<K, P>(), st>>>(d);
+        k_dedup<K, P><<<(unsigned)W.dtiles, kSortThreads, dedup_smem<K, P>(), st>>>(d);
         GEE_CHECK_LAUNCH("k_dedup_fix");
     }
     return GEE_OK;
