@@ -302,6 +302,25 @@ __device__ void row_smem(const EmbedArgs &a, int64_t r, double *zs, double *xs) 
     const double *val = row_vals(a, r);
     double *zrow = a.z + (r - a.row_begin) * a.ldz;
     const bool corr = (a.flags & GEE_CORRELATION) != 0;
+    if (e == s) {
+        // empty row (common in power-law graphs): zeros, plus A+I's diagonal
+        // term x = s_r * g_r at the row's own label (x / |x| under correlation)
+        int lb = -1;
+        double xd = 0.0;
+        if (a.flags & GEE_DIAGONAL) {
+            if (!diag_term(a, r, s_r, lb, xd)) lb = -1;
+        }
+        if (lb >= 0 && corr) {
+            if (!isfinite(xd)) {
+                if (lane == 0) raise_err(a.err, GEE_ERR_NONFINITE);
+            } else {
+                const double nrm = __dsqrt_rn(xd * xd);
+                if (nrm > 0.0) xd = xd * __ddiv_rn(1.0, nrm);
+            }
+        }
+        for (int c = lane; c < a.k; c += 32) zrow[c] = c == lb ? xd : 0.0;
+        return;
+    }
     const int ntiles = (a.k + kKTile - 1) / kKTile;
     bool found = false;
     double ss = 0.0;
