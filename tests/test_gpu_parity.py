@@ -402,3 +402,32 @@ def test_encoder_plan_and_launch_count():
     # the unit-weight sort path never reads a value array: same Z with weights=None
     z3 = enc.run(rows, cols, None, lab)
     z_close(z3.cpu().numpy(), zr)
+
+
+@pytest.mark.parametrize("directed", [True, False])
+@pytest.mark.parametrize("offset", [0, 1000, 2040, 3070])
+def test_long_duplicate_runs_cross_sort_tiles(directed, offset):
+    """64-bit-key radix path: a 5,000-entry run of one (row, col) pair with
+    non-associative weights (its sum depends on the order) placed so it
+    crosses one-sweep (3,072) and dedup (2,048) tile boundaries, mixed with
+    original and reversed directions: the CSR value must be the stream-order
+    sum, bit for bit."""
+    rng = np.random.default_rng(offset + 7 * directed)
+    n = 100_000
+    m = 20_000
+    rows = rng.integers(0, n, m)
+    cols = rng.integers(0, n, m)
+    w = 1.0 - rng.random(m)
+    run = slice(3000, 8000)
+    rows[run], cols[run] = 5, 9                     # row 5's entries sort first in row 5
+    rows[offset:offset + 30] = 5
+    cols[offset:offset + 30] = rng.integers(0, 9, 30)  # shift where the run starts in the sorted stream
+    rng2 = np.random.default_rng(3)
+    w[run] = rng2.choice([1e16, 1.0, -1e16, 3.0, 0.25], 5000)
+    if not directed:
+        rows[8000:8100], cols[8000:8100] = 9, 5     # mirrors join the (5, 9) run after the originals
+        w[8000:8100] = rng2.choice([1e16, -1e16, 1.5], 100)
+    for path in ("default", "sort64"):
+        with assembly_path(path):
+            _check_against_oracle(n, rows, cols, w, rng.integers(0, 3, n), 3, directed,
+                                  combos=[(1, 1, 1), (0, 0, 0)])
