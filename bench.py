@@ -53,6 +53,11 @@ def parse():
     p.add_argument("--eager", action="store_true", help="launch kernels one by one instead of a CUDA graph")
     p.add_argument("--flush-mib", type=int, default=512)
     p.add_argument("--cpu-budget-s", type=float, default=12.0)
+    p.add_argument("--embed-flat-bytes", type=int, default=None,
+                   help="debug: per-warp shared budget of the K > 8 embed's flat row blocks "
+                        "(gee_debug_set GEE_DEBUG_EMBED_FLAT_BYTES; 0 = one warp per row)")
+    p.add_argument("--embed-flat-rowmax", type=int, default=None,
+                   help="debug: longest row a flat embed block takes (GEE_DEBUG_EMBED_FLAT_ROWMAX)")
     p.add_argument("--force-path", type=int, default=0,
                    help="debug: CSR assembly path hook (gee_debug_set GEE_DEBUG_FORCE_BUCKETS)")
     p.add_argument("--sharded", action="store_true",
@@ -273,6 +278,10 @@ def run_b200(args):
     lib = _lib.load()
     if args.force_path:
         lib.gee_debug_set(_lib.DEBUG_FORCE_BUCKETS, args.force_path)
+    if args.embed_flat_bytes is not None:
+        lib.gee_debug_set(_lib.DEBUG_EMBED_FLAT_BYTES, args.embed_flat_bytes)
+    if args.embed_flat_rowmax is not None:
+        lib.gee_debug_set(_lib.DEBUG_EMBED_FLAT_ROWMAX, args.embed_flat_rowmax)
     c = load_config(args.config, dev)
     n, e, k, directed, flags = c["n"], c["e"], c["k"], c["directed"], c["flags"]
     rows = torch.as_tensor(c["rows"], device=dev)

@@ -205,6 +205,12 @@ int gee_profile_read(float *ms, const char **names, int cap);
  * bitmap path, 3 = as 2 with the radix sort on every 64-bit (row, col) key.
  * Returns the previous value. */
 #define GEE_DEBUG_FORCE_BUCKETS 1
+/* Second hook: the shared-memory budget (bytes per warp) of the embed's flat
+ * row blocks for K > 8; 0 = one warp per row instead.  Default 8192. */
+#define GEE_DEBUG_EMBED_FLAT_BYTES 2
+/* Third hook: the longest row a flat block takes (default 256); longer rows
+ * get a warp each, rows over 4096 entries a CTA each. */
+#define GEE_DEBUG_EMBED_FLAT_ROWMAX 3
 int gee_debug_set(int key, int value);
 
 #ifdef __cplusplus

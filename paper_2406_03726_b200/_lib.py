@@ -63,6 +63,8 @@ SIGNATURES = {
     "gee_debug_set": (_int, [_int, _int]),
 }
 DEBUG_FORCE_BUCKETS = 1  # key; values: 0 default, 1 row buckets, 2 no bitmap path, 3 = 2 + 64-bit sort keys
+DEBUG_EMBED_FLAT_BYTES = 2  # key; per-warp shared bytes of the K > 8 flat embed blocks (0 = warp per row)
+DEBUG_EMBED_FLAT_ROWMAX = 3  # key; longest row a flat embed block takes (longer: a warp each)
 
 _lib = None
 

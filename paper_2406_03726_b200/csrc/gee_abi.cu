@@ -64,6 +64,8 @@ int label_hist_pipeline(const int64_t *labels, int64_t n, int32_t k, int32_t *y3
 size_t csr_build_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
 bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed, int wt);
 int set_force_buckets(int v);
+int set_embed_flat_bytes(int v);
+int set_embed_flat_rowmax(int v);
 int sort_csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, int64_t E, int64_t n_rows,
                    int64_t n_cols, int directed, int force_vals, int64_t *row_ptr, int32_t *col, double *val,
                    int64_t *nnz, unsigned deg_flags, double *deg, double *scale, void *ws, size_t ws_bytes,
@@ -182,6 +184,8 @@ int gee_profile_start(void *stream) {
 
 int gee_debug_set(int key, int value) {
     if (key == GEE_DEBUG_FORCE_BUCKETS) return set_force_buckets(value);
+    if (key == GEE_DEBUG_EMBED_FLAT_BYTES) return set_embed_flat_bytes(value);
+    if (key == GEE_DEBUG_EMBED_FLAT_ROWMAX) return set_embed_flat_rowmax(value);
     return -1;
 }
 
@@ -361,7 +365,7 @@ int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, in
     double *etg;
     signed char *etl;
     embed_scratch(W.emb_ws, n_nodes, n_nodes, &ectr, &elist, &erec, &etg, &etl);
-    GEE_CHECK_CUDA(cudaMemsetAsync(ectr, 0, 4 * sizeof(unsigned), st));
+    GEE_CHECK_CUDA(cudaMemsetAsync(ectr, 0, 8 * sizeof(unsigned), st));
     int rc = label_hist_pipeline(labels, n_nodes, k, W.y32, W.counts, W.inv, W.label_partial, ectr + 3, err, st);
     if (rc) return rc;
     const unsigned deg_flags = (flags & GEE_LAPLACIAN) ? (GEE_LAPLACIAN | (flags & GEE_DIAGONAL)) : 0u;

@@ -56,6 +56,9 @@ struct EmbedArgs {
     const unsigned char *row_flag; // per row: 1 => read val for this row, 0 => values are 1.0
     const double *tab_g;           // optional compact node table (g, label) to stage on chip
     const signed char *tab_lab;
+    int flat_rows;                 // > 0: phase 2 streams blocks of this many rows (K > 8)
+    int flat_max;                  // longest row a block takes (longer: phase 1.5 / phase 1)
+    int kp;                        // row stride of a flat block's shared tile
 };
 
 __device__ __forceinline__ void row_extent(const EmbedArgs &a, int64_t r, int64_t &s, int64_t &e) {
@@ -117,6 +120,12 @@ __device__ __forceinline__ int4 ld_stream_i4(const int32_t *p) {
     asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ int ld_stream_i1(const int32_t *p) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
 
@@ -435,8 +444,214 @@ __device__ void row_long(const EmbedArgs &a, int64_t r, double *zsm, double *xsm
     __syncthreads();
 }
 
-template <int KP, bool TAB, int NT>
-__global__ void __launch_bounds__(NT) k_embed(EmbedArgs a, int n_tab) {
+
+// ---------------------------------------------------------------------------
+// K > 8, rows up to kLongRow: a warp takes R = a.flat_rows consecutive rows
+// and streams their entries as ONE lane-consecutive sequence (entry f of the
+// block belongs to the row whose prefix brackets f), accumulating into an
+// R x K shared tile.  The per-row fixed costs of a warp-per-row walk (extent
+// loads, a K-vector clear and sweep, a partial-sector Z row) are shared by R
+// rows: extents, scales and flags of the block arrive in one round trip,
+// every iteration has 32*U column loads and then 32*U node-record gathers in
+// flight, and the block's R x K slice of Z is written as one contiguous run.
+// Rows longer than kLongRow are left to phase 1 (their Z rows are skipped).
+// ---------------------------------------------------------------------------
+constexpr int kFlatU = 4;
+
+// One flat block: rows r0 .. r0+nr-1 (a lone listed row when nr == 1 and
+// rmax == kLongRow); rows longer than rmax are left to their own phase and
+// their Z rows are not written.
+__device__ void flat_block(const EmbedArgs &a, int64_t r0, int nr, int rmax, double *zs, double *xs) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int K = a.k, Kp = a.kp;
+    const bool lap = (a.flags & GEE_LAPLACIAN) != 0, dia = (a.flags & GEE_DIAGONAL) != 0;
+    const bool corr = (a.flags & GEE_CORRELATION) != 0;
+    int64_t st = 0;
+    int cnt = 0, uv = 0, dlab = -1;
+    bool excl = false;
+    double sr = 1.0, dg = 0.0;
+    if (lane < nr) {
+        const int64_t r = r0 + lane;
+        int64_t s, e;
+        row_extent(a, r, s, e);
+        st = s;
+        excl = e - s > rmax;
+        cnt = excl ? 0 : (int)(e - s);
+        if (lap) sr = a.scale[r];
+        uv = (a.val != nullptr && !(a.row_flag && !a.row_flag[r])) ? 1 : 0;
+        if (dia) node_rec(a, (int)r, dlab, dg);
+    }
+    const unsigned exmask = __ballot_sync(full, excl);
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(full, inc, o);
+        if (lane >= o) inc += y;
+    }
+    const int pre = lane < nr ? inc - cnt : INT_MAX;
+    const int T = __shfl_sync(full, inc, 31);
+    for (int q = lane; q < nr * Kp; q += 32) zs[q] = 0.0;
+    __syncwarp();
+    unsigned dmask = 0;
+    for (int f0 = 0; f0 < T; f0 += 32 * kFlatU) {
+        int ri[kFlatU], cc[kFlatU];
+        double vv[kFlatU];
+#pragma unroll
+        for (int u = 0; u < kFlatU; ++u) {
+            const int f = f0 + 32 * u + lane;
+            int lo = 0;
+            if (nr > 1) {
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    const int pm = __shfl_sync(full, pre, lo + step);
+                    if (pm <= f) lo += step;
+                }
+            }
+            ri[u] = lo;
+            const int64_t p = __shfl_sync(full, st, lo) + (f - __shfl_sync(full, pre, lo));
+            const int use_v = __shfl_sync(full, uv, lo);
+            const bool ok = f < T;
+            cc[u] = ok ? ld_stream_i1(a.col + p) : -1;
+            vv[u] = (ok && use_v) ? a.val[p] : 1.0;
+        }
+        int lab[kFlatU];
+        double g[kFlatU];
+#pragma unroll
+        for (int u = 0; u < kFlatU; ++u) {
+            lab[u] = -1;
+            g[u] = 0.0;
+            if (cc[u] >= 0) node_rec(a, cc[u], lab[u], g[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kFlatU; ++u) {
+            const double s_i = __shfl_sync(full, sr, ri[u]);
+            double v = vv[u];
+            if (dia && cc[u] >= 0 && (int64_t)cc[u] == r0 + ri[u]) {
+                v = v + 1.0;
+                dmask |= 1u << ri[u];
+            }
+            const bool ok = cc[u] >= 0 && lab[u] >= 0;
+            const double x = (lap ? v * s_i : v) * g[u];
+            const unsigned key = ok ? (unsigned)(ri[u] * Kp + lab[u]) : 0x80000000u + lane;
+            const unsigned peers = __match_any_sync(full, key);
+            xs[lane] = x;
+            __syncwarp();
+            if (ok && lane == __ffs(peers) - 1) {
+                double sum = 0.0;
+                unsigned m = peers;
+                while (m) {
+                    const int l = __ffs(m) - 1;
+                    m &= m - 1;
+                    sum += xs[l];
+                }
+                zs[key] += sum;
+            }
+            __syncwarp();
+        }
+    }
+    // A+I: the virtual 1.0 of rows without a stored diagonal
+    if (dia) {
+        dmask = __reduce_or_sync(full, dmask);
+        if (lane < nr && !excl && !((dmask >> lane) & 1u) && dlab >= 0) zs[lane * Kp + dlab] += (lap ? sr : 1.0) * dg;
+        __syncwarp();
+    }
+    // correlation: L lanes per row (L = the largest power of two with
+    // L * nr <= 32) fold every L-th column, an L-lane butterfly gives every
+    // one of them the norm, and they rescale their columns in place
+    double rn = 1.0;
+    if (corr) {
+        int L = 32;
+        while (L > 1 && L * nr > 32) L >>= 1;
+        const int i = lane / L, j = lane - i * L;
+        double ss = 0.0;
+        double *zi = zs + i * Kp;
+        if (i < nr)
+            for (int q = j; q < K; q += L) ss = fma(zi[q], zi[q], ss);
+        for (int o = 1; o < L; o <<= 1) ss += __shfl_xor_sync(full, ss, o);
+        const bool live = i < nr && !((exmask >> i) & 1u);
+        int fin = 1;
+        if (live && !isfinite(ss)) {
+            // inf/nan in the row, or a norm beyond the double range
+            // (embedding.py:137-138 checks the entries themselves)
+            for (int q = j; q < K; q += L) fin &= isfinite(zi[q]) ? 1 : 0;
+        }
+        for (int o = 1; o < L; o <<= 1) fin &= __shfl_xor_sync(full, fin, o);
+        if (live) {
+            if (!fin) {
+                if (j == 0) raise_err(a.err, GEE_ERR_NONFINITE);
+            } else {
+                // one division per row; z * (1/nrm) is within 1 ulp of
+                // z / nrm (embedding.py:140 divides; Z's bar is 1e-12)
+                const double nrm = __dsqrt_rn(ss);
+                if (nrm > 0.0) {
+                    rn = __ddiv_rn(1.0, nrm);
+                    // one row per block: the copy below applies rn instead
+                    if (nr > 1)
+                        for (int q = j; q < K; q += L) zi[q] *= rn;
+                }
+            }
+        }
+        __syncwarp();
+    }
+    // the block's Z rows: one contiguous copy when the tile is dense and no
+    // row belongs to another phase, else row by row (others' rows skipped)
+    double *zb = a.z + (r0 - a.row_begin) * a.ldz;
+    if (nr == 1) {
+        rn = __shfl_sync(full, rn, 0);
+        if (!exmask)
+            for (int q = lane; q < K; q += 32) __stcs(zb + q, zs[q] * rn);
+    } else if (exmask == 0 && Kp == K && a.ldz == K) {
+        const int n = nr * K;
+        int e = lane;
+        for (; e + 96 < n; e += 128) {
+            const double v0 = zs[e], v1 = zs[e + 32], v2 = zs[e + 64], v3 = zs[e + 96];
+            __stcs(zb + e, v0);
+            __stcs(zb + e + 32, v1);
+            __stcs(zb + e + 64, v2);
+            __stcs(zb + e + 96, v3);
+        }
+        for (; e < n; e += 32) __stcs(zb + e, zs[e]);
+    } else {
+        for (int i = 0; i < nr; ++i, zb += a.ldz) {
+            if ((exmask >> i) & 1u) continue;
+            const double *zi = zs + i * Kp;
+            for (int q = lane; q < K; q += 32) __stcs(zb + q, zi[q]);
+        }
+    }
+    __syncwarp();
+}
+
+// phase 1.5: rows of (flat_max, kLongRow] entries, one warp each (listed from
+// the back of the long-row list); phase 2: blocks of R consecutive rows
+__device__ void rows_flat(const EmbedArgs &a, double *zs, double *xs) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned n_med = a.n_long[5];
+    const int64_t n_rows = a.row_end - a.row_begin;
+    for (;;) {
+        unsigned tw = 0;
+        if (lane == 0) tw = atomicAdd(&a.work[3], 1u);
+        tw = __shfl_sync(full, tw, 0);
+        if (tw >= n_med) break;
+        flat_block(a, (int64_t)a.long_list[n_rows - 1 - tw], 1, kLongRow, zs, xs);
+    }
+    const int R = a.flat_rows;
+    const int64_t n_chunks = (n_rows + R - 1) / R;
+    unsigned tw = 0;
+    if (lane == 0) tw = atomicAdd(&a.work[1], 1u);
+    int64_t t = __shfl_sync(full, tw, 0);
+    while (t < n_chunks) {
+        // the next block's id is fetched now: its round trip overlaps this block
+        if (lane == 0) tw = atomicAdd(&a.work[1], 1u);
+        const int64_t r0 = a.row_begin + t * R;
+        flat_block(a, r0, (int)min((int64_t)R, a.row_end - r0), a.flat_max, zs, xs);
+        t = __shfl_sync(full, tw, 0);
+    }
+}
+
+template <int KP, bool TAB, int NT, bool FLAT = false>
+__global__ void __launch_bounds__(NT, FLAT ? 3 : 65536 / (NT * 64)) k_embed(EmbedArgs a, int n_tab) {
     constexpr int kWarps = NT / 32;
     // values implicit (all exactly 1.0) when the sort path says so: skip the val stream
     if (a.val_flags && a.val_flags[0] == 0 && a.val_flags[1] == 0) a.val = nullptr;
@@ -444,8 +659,10 @@ __global__ void __launch_bounds__(NT) k_embed(EmbedArgs a, int n_tab) {
     __shared__ double dred[33];
     __shared__ int task;
     const int kt_max = min(a.k, kKTile);
-    double *zsm = reinterpret_cast<double *>(dsm);    // [warps][kt_max]
-    double *xsm = zsm + (size_t)kWarps * kt_max;  // [warps][32]
+    // per-warp tile: a K-vector (kt_max) or a flat block (flat_rows x kp)
+    const int wst = FLAT ? max(kt_max, a.flat_rows * a.kp) : kt_max;
+    double *zsm = reinterpret_cast<double *>(dsm);    // [warps][wst]
+    double *xsm = zsm + (size_t)kWarps * wst;     // [warps][32]
     const int wid = threadIdx.x >> 5;
     NodeTab tab{nullptr, nullptr};
     if (TAB) {
@@ -502,6 +719,10 @@ __global__ void __launch_bounds__(NT) k_embed(EmbedArgs a, int n_tab) {
     // phase 2: every warp grabs its own chunks of rows, one warp per row (no
     // CTA-wide barrier: row lengths vary, so a barrier per chunk would idle
     // the warps that drew short rows)
+    if (FLAT) {
+        rows_flat(a, zsm + (size_t)wid * wst, xsm + wid * 32);
+        return;
+    }
     const int64_t n_rows = a.row_end - a.row_begin;
     const int64_t n_chunks = (n_rows + kRowChunk - 1) / kRowChunk;
     const int lane = threadIdx.x & 31;
@@ -520,31 +741,43 @@ __global__ void __launch_bounds__(NT) k_embed(EmbedArgs a, int n_tab) {
             if (KP > 0)
                 row_regs<(KP > 0 ? KP : 1), TAB>(a, tab, r);
             else
-                row_smem(a, r, zsm + wid * kt_max, xsm + wid * 32);
+                row_smem(a, r, zsm + wid * wst, xsm + wid * 32);
         }
     }
 }
 
 __global__ void k_embed_classify(const int64_t *__restrict__ row_ptr, const unsigned *__restrict__ row_cnt,
-                                 int64_t rb, int64_t re, unsigned *__restrict__ list,
-                                 unsigned *__restrict__ n_list) {
+                                 int64_t rb, int64_t re, int64_t flat_max, unsigned *__restrict__ list,
+                                 unsigned *__restrict__ ctr) {
+    // long rows (> kLongRow) listed from the front (count ctr[0]); with flat
+    // blocks, medium rows (flat_max, kLongRow] from the back (count ctr[5])
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t n = re - rb;
     const int64_t n_round = (n + 31) & ~int64_t(31);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
-        bool lng = false;
+        bool lng = false, med = false;
         int64_t r = rb + i;
         if (i < n) {
             int64_t L = row_cnt ? (int64_t)row_cnt[r] : row_ptr[r + 1] - row_ptr[r];
             lng = L > kLongRow;
+            med = !lng && L > flat_max;
         }
         unsigned m = __ballot_sync(0xffffffffu, lng);
-        if (!m) continue;
-        int leader = __ffs(m) - 1;
-        unsigned base = 0;
-        if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(n_list, __popc(m));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (lng) list[base + __popc(m & lanemask_lt())] = (unsigned)r;
+        if (m) {
+            int leader = __ffs(m) - 1;
+            unsigned base = 0;
+            if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(ctr, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (lng) list[base + __popc(m & lanemask_lt())] = (unsigned)r;
+        }
+        m = __ballot_sync(0xffffffffu, med);
+        if (m) {
+            int leader = __ffs(m) - 1;
+            unsigned base = 0;
+            if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(ctr + 5, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (med) list[n - 1 - (base + __popc(m & lanemask_lt()))] = (unsigned)r;
+        }
     }
 }
 
@@ -572,7 +805,7 @@ struct EmbedScratch {
 
 static EmbedScratch carve_embed(Carver &cv, int64_t n_rows, int64_t n_cols) {
     EmbedScratch s;
-    s.ctr = cv.take<unsigned>(4);
+    s.ctr = cv.take<unsigned>(8);
     s.list = cv.take<unsigned>((size_t)n_rows + 1);
     s.rec = cv.take<double2>((size_t)n_cols + 1);
     const bool small = n_cols <= kTabMax;
@@ -588,6 +821,27 @@ size_t embed_workspace(int64_t n_rows, int64_t n_cols) {
 }
 
 int embed_long_row() { return kLongRow; }
+
+// shared-memory budget of one warp's flat block (bytes); 0 disables the flat
+// phase 2 (test hook GEE_DEBUG_EMBED_FLAT_BYTES)
+static thread_local int t_flat_bytes = 8192;
+constexpr int kFlatBytesMax = 24576;
+
+int set_embed_flat_bytes(int v) {
+    const int old = t_flat_bytes;
+    t_flat_bytes = v < 0 ? 0 : (v > kFlatBytesMax ? kFlatBytesMax : v);
+    return old;
+}
+
+// longest row a flat block takes; longer rows get a warp (or, beyond
+// kLongRow, a CTA) of their own (test hook GEE_DEBUG_EMBED_FLAT_ROWMAX)
+static thread_local int t_flat_max = 256;
+
+int set_embed_flat_rowmax(int v) {
+    const int old = t_flat_max;
+    t_flat_max = v < 1 ? 1 : (v > kLongRow ? kLongRow : v);
+    return old;
+}
 
 void embed_scratch(void *ws, int64_t n_rows, int64_t n_cols, unsigned **ctr, unsigned **list, double2 **rec,
                    double **tab_g, signed char **tab_lab) {
@@ -611,15 +865,25 @@ int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, c
     double2 *rec = sc.rec;
     if (ws_bytes < cv.bytes()) return GEE_E_WORKSPACE;
     if (n <= 0) return GEE_OK;
+    EmbedArgs a;
+    // K > 8: flat blocks of R rows (R x kp doubles within the warp budget)
+    a.kp = k < 32 ? (k | 1) : k;
+    a.flat_rows = 0;
+    a.flat_max = kLongRow;
+    if (k > 8 && k <= kKTile) {
+        // a power of two, so the correlation's lanes-per-row split uses every lane
+        const int r = t_flat_bytes / (8 * a.kp);
+        a.flat_rows = r >= 16 ? 16 : r >= 8 ? 8 : r >= 4 ? 4 : r >= 2 ? 2 : r;
+        if (a.flat_rows > 0) a.flat_max = t_flat_max;
+    }
     if (!prepared) {
-        GEE_CHECK_CUDA(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned), st));
+        GEE_CHECK_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(unsigned), st));
         k_node_rec<<<grid_for(n_cols, 256, 8), 256, 0, st>>>(y32, inv, (flags & GEE_LAPLACIAN) ? scale : nullptr,
                                                               n_cols, rec);
         GEE_CHECK_LAUNCH("k_node_rec");
-        k_embed_classify<<<grid_for(n, 256, 8), 256, 0, st>>>(row_ptr, row_cnt, rb, re, list, ctr);
+        k_embed_classify<<<grid_for(n, 256, 8), 256, 0, st>>>(row_ptr, row_cnt, rb, re, a.flat_max, list, ctr);
         GEE_CHECK_LAUNCH("k_embed_classify");
     }
-    EmbedArgs a;
     a.row_ptr = row_ptr;
     a.row_cnt = row_cnt;
     a.col = col;
@@ -642,16 +906,19 @@ int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, c
     a.tab_g = (prepared && n_cols <= kTabMax) ? sc.tab_g : nullptr;
     a.tab_lab = (prepared && n_cols <= kTabMax) ? sc.tab_lab : nullptr;
     const int kt_max = k < kKTile ? k : kKTile;
+    const int wst = a.flat_rows > 0 ? (kt_max > a.flat_rows * a.kp ? kt_max : a.flat_rows * a.kp) : kt_max;
     // small graphs with K <= 8: node table (9 B/node) staged in shared memory
     // by one 1024-thread CTA per SM (one table copy serves 32 warps)
     const bool tab = k <= 8 && n_cols <= kTabMax;
     const int nt = tab ? kTabThreads : kEmbedThreads;
-    const size_t base_smem = sizeof(double) * (size_t)(nt / 32) * ((size_t)kt_max + 32);
+    const size_t base_smem = sizeof(double) * (size_t)(nt / 32) * ((size_t)wst + 32);
     const size_t smem = base_smem + (tab ? 9 * (size_t)n_cols + 32 : 0);
     static bool attr = false;
     if (!attr) {
-        size_t mx = sizeof(double) * (size_t)kEmbedWarps * ((size_t)kKTile + 32);
+        size_t mx = sizeof(double) * (size_t)kEmbedWarps * ((size_t)kFlatBytesMax / 8 + 32);
         GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<0, false, kEmbedThreads>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
+        GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<0, false, kEmbedThreads, true>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
         const int tmx = (int)(sizeof(double) * (kTabThreads / 32) * (8 + 32) + 9 * kTabMax + 32);
         GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<1, true, kTabThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
@@ -664,12 +931,13 @@ int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, c
     const unsigned grid_cap = (unsigned)num_sms() * 8;
     unsigned grid;
     const int n_tab = tab ? (int)n_cols : 0;
-#define GEE_LAUNCH_EMBED(KP, TB, NT)                                                                         \
+#define GEE_LAUNCH_EMBED(KP, TB, NT, ...)                                                                    \
     do {                                                                                                     \
-        GEE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_embed<KP, TB, NT>, NT, smem));  \
+        GEE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_embed<KP, TB, NT, ##__VA_ARGS__>, \
+                                                                     NT, smem));                             \
         grid = (unsigned)num_sms() * (unsigned)(occ > 0 ? occ : 1);                                          \
         if (grid > grid_cap) grid = grid_cap;                                                                \
-        k_embed<KP, TB, NT><<<grid, NT, smem, st>>>(a, n_tab);                                               \
+        k_embed<KP, TB, NT, ##__VA_ARGS__><<<grid, NT, smem, st>>>(a, n_tab);                                \
     } while (0)
     if (k <= 1) {
         if (tab) GEE_LAUNCH_EMBED(1, true, kTabThreads); else GEE_LAUNCH_EMBED(1, false, kEmbedThreads);
@@ -679,6 +947,8 @@ int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, c
         if (tab) GEE_LAUNCH_EMBED(4, true, kTabThreads); else GEE_LAUNCH_EMBED(4, false, kEmbedThreads);
     } else if (k <= 8) {
         if (tab) GEE_LAUNCH_EMBED(8, true, kTabThreads); else GEE_LAUNCH_EMBED(8, false, kEmbedThreads);
+    } else if (a.flat_rows > 0) {
+        GEE_LAUNCH_EMBED(0, false, kEmbedThreads, true);
     } else {
         GEE_LAUNCH_EMBED(0, false, kEmbedThreads);
     }

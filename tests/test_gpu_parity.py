@@ -431,3 +431,39 @@ def test_long_duplicate_runs_cross_sort_tiles(directed, offset):
         with assembly_path(path):
             _check_against_oracle(n, rows, cols, w, rng.integers(0, 3, n), 3, directed,
                                   combos=[(1, 1, 1), (0, 0, 0)])
+
+
+class embed_flat:
+    """Select the K > 8 embed variant via the library's test hook: the
+    per-warp shared budget of a flat row block (0 = one warp per row)."""
+
+    def __init__(self, nbytes, rowmax=256):
+        self.nbytes, self.rowmax = nbytes, rowmax
+
+    def __enter__(self):
+        from paper_2406_03726_b200 import _lib
+        lib = _lib.load()
+        self.old = (lib.gee_debug_set(_lib.DEBUG_EMBED_FLAT_BYTES, self.nbytes),
+                    lib.gee_debug_set(_lib.DEBUG_EMBED_FLAT_ROWMAX, self.rowmax))
+
+    def __exit__(self, *exc):
+        from paper_2406_03726_b200 import _lib
+        lib = _lib.load()
+        lib.gee_debug_set(_lib.DEBUG_EMBED_FLAT_BYTES, self.old[0])
+        lib.gee_debug_set(_lib.DEBUG_EMBED_FLAT_ROWMAX, self.old[1])
+
+
+@pytest.mark.parametrize("nbytes,rowmax", [(0, 256), (600, 1), (4096, 256), (12288, 16), (24576, 4096)])
+@pytest.mark.parametrize("n,m,k,kind,directed,hub", [
+    (9_000, 60_000, 9, "pos", True, (4, 0.1)),       # K just above the register path, hub > kLongRow
+    (30_000, 120_000, 20, "signed", False, None),    # odd-padded tile rows (K < 32), empty rows
+    (40_000, 300_000, 50, "pos", True, (5, 0.1)),    # cfg3-like K, hub row in phase 1
+    (20_000, 100_000, 1000, "unit", False, (3, 0.2)),  # one row per block
+])
+def test_embed_flat_blocks(nbytes, rowmax, n, m, k, kind, directed, hub):
+    rng = np.random.default_rng(n + k + 7)
+    with embed_flat(nbytes, rowmax):
+        for path in ("default", "buckets"):
+            with assembly_path(path):
+                _check_against_oracle(n, *_graph(rng, n, m, kind, directed, k, dup_runs=True, hub=hub), k,
+                                      directed, combos=[(0, 0, 0), (1, 1, 1), (0, 1, 1), (1, 0, 0)])
