@@ -491,7 +491,11 @@ __device__ void flat_block(const EmbedArgs &a, int64_t r0, int nr, int rmax, dou
     }
     const int pre = lane < nr ? inc - cnt : INT_MAX;
     const int T = __shfl_sync(full, inc, 31);
-    for (int q = lane; q < nr * Kp; q += 32) zs[q] = 0.0;
+    {
+        // the tile is 16-byte aligned with an even stride (wst): clear pairs
+        double2 *z2 = reinterpret_cast<double2 *>(zs);
+        for (int q = lane; 2 * q < nr * Kp; q += 32) z2[q] = make_double2(0.0, 0.0);
+    }
     __syncwarp();
     unsigned dmask = 0;
     for (int f0 = 0; f0 < T; f0 += 32 * kFlatU) {
@@ -566,8 +570,19 @@ __device__ void flat_block(const EmbedArgs &a, int64_t r0, int nr, int rmax, dou
         const int i = lane / L, j = lane - i * L;
         double ss = 0.0;
         double *zi = zs + i * Kp;
-        if (i < nr)
+        if (nr == 1 && !(K & 1)) {
+            // one row: 16-byte shared loads, two independent accumulators
+            const double2 *z2 = reinterpret_cast<const double2 *>(zs);
+            double s1 = 0.0;
+            for (int q = lane; 2 * q < K; q += 32) {
+                const double2 v = z2[q];
+                ss = fma(v.x, v.x, ss);
+                s1 = fma(v.y, v.y, s1);
+            }
+            ss += s1;
+        } else if (i < nr) {
             for (int q = j; q < K; q += L) ss = fma(zi[q], zi[q], ss);
+        }
         for (int o = 1; o < L; o <<= 1) ss += __shfl_xor_sync(full, ss, o);
         const bool live = i < nr && !((exmask >> i) & 1u);
         int fin = 1;
@@ -599,8 +614,18 @@ __device__ void flat_block(const EmbedArgs &a, int64_t r0, int nr, int rmax, dou
     double *zb = a.z + (r0 - a.row_begin) * a.ldz;
     if (nr == 1) {
         rn = __shfl_sync(full, rn, 0);
-        if (!exmask)
-            for (int q = lane; q < K; q += 32) __stcs(zb + q, zs[q] * rn);
+        if (!exmask) {
+            if (!(K & 1) && !(a.ldz & 1) && !(reinterpret_cast<uintptr_t>(a.z) & 15)) {
+                const double2 *z2 = reinterpret_cast<const double2 *>(zs);
+                double2 *o2 = reinterpret_cast<double2 *>(zb);
+                for (int q = lane; 2 * q < K; q += 32) {
+                    const double2 v = z2[q];
+                    __stcs(o2 + q, make_double2(v.x * rn, v.y * rn));
+                }
+            } else {
+                for (int q = lane; q < K; q += 32) __stcs(zb + q, zs[q] * rn);
+            }
+        }
     } else if (exmask == 0 && Kp == K && a.ldz == K) {
         const int n = nr * K;
         int e = lane;
@@ -660,7 +685,7 @@ __global__ void __launch_bounds__(NT, FLAT ? 3 : 65536 / (NT * 64)) k_embed(Embe
     __shared__ int task;
     const int kt_max = min(a.k, kKTile);
     // per-warp tile: a K-vector (kt_max) or a flat block (flat_rows x kp)
-    const int wst = FLAT ? max(kt_max, a.flat_rows * a.kp) : kt_max;
+    const int wst = FLAT ? (max(kt_max, a.flat_rows * a.kp) + 1) & ~1 : kt_max;
     double *zsm = reinterpret_cast<double *>(dsm);    // [warps][wst]
     double *xsm = zsm + (size_t)kWarps * wst;     // [warps][32]
     const int wid = threadIdx.x >> 5;
@@ -906,7 +931,7 @@ int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, c
     a.tab_g = (prepared && n_cols <= kTabMax) ? sc.tab_g : nullptr;
     a.tab_lab = (prepared && n_cols <= kTabMax) ? sc.tab_lab : nullptr;
     const int kt_max = k < kKTile ? k : kKTile;
-    const int wst = a.flat_rows > 0 ? (kt_max > a.flat_rows * a.kp ? kt_max : a.flat_rows * a.kp) : kt_max;
+    const int wst = a.flat_rows > 0 ? ((kt_max > a.flat_rows * a.kp ? kt_max : a.flat_rows * a.kp) + 1) & ~1 : kt_max;
     // small graphs with K <= 8: node table (9 B/node) staged in shared memory
     // by one 1024-thread CTA per SM (one table copy serves 32 warps)
     const bool tab = k <= 8 && n_cols <= kTabMax;
