@@ -184,6 +184,33 @@ int gee_bitmap_shard_encode(const int64_t *rows, const int64_t *cols, int64_t e_
                             unsigned flags, const uint32_t *deg_all, double *z_local, void *ws,
                             size_t ws_bytes, int32_t *err, void *stream);
 
+/* Distributed CSR build: ranks start from contiguous slices
+ * of the ORIGINAL edge list (slice p = stream positions [e_p, e_{p+1}) of
+ * EdgeList(rows, cols, w), graph_io.py:48-92) and shuffle the symmetrised
+ * stream to the P row owners.  Replaces the host-side partition of dist.py
+ * (stream_row_counts / row_ranges / local_stream).
+ *   gee_shuffle_row_hist   adds this slice's stream entries per coarse row
+ *     bucket into hist uint64[n_buckets] (caller zeroes it, then
+ *     all-reduces it); n_buckets = gee_shuffle_buckets(n_nodes);
+ *   gee_shuffle_bounds     bounds int64[world + 1]: contiguous row ranges
+ *     with near-equal stream entries (bucket-granular, as dist.row_ranges);
+ *   gee_partition          stable partition into 2*world send buckets laid
+ *     out [half][dest]: half 0 = originals by their row, half 1 = mirrored
+ *     off-diagonals (undirected) by their column, written as (col, row);
+ *     every bucket keeps slice order; counts uint64[2*world] bucket sizes;
+ *     out_* hold up to 2*n_edges entries; w / out_w in w_type's width.
+ * Exchanging the originals region, then the mirrors region, with one
+ * all-to-all each and concatenating what arrives in source-rank order gives
+ * each rank its slice of the symmetrised stream in stream order. world <= 16. */
+int64_t gee_shuffle_buckets(int64_t n_nodes);
+int gee_shuffle_row_hist(const int64_t *rows, const int64_t *cols, int64_t n_edges, int64_t n_nodes,
+                         int directed, uint64_t *hist, void *stream);
+int gee_shuffle_bounds(const uint64_t *hist, int64_t n_nodes, int world, int64_t *bounds, void *stream);
+int gee_partition_workspace(int64_t n_edges, int world, size_t *ws_bytes);
+int gee_partition(const int64_t *rows, const int64_t *cols, const void *w, int w_type, int64_t n_edges,
+                  int directed, const int64_t *bounds, int world, int64_t *out_rows, int64_t *out_cols,
+                  void *out_w, uint64_t *counts, void *ws, size_t ws_bytes, void *stream);
+
 /* Launch statistics: number of kernels this thread launched through the
  * library since the last reset (for bench.py's gpu_launches). */
 uint64_t gee_launch_count(void);

@@ -55,6 +55,12 @@ SIGNATURES = {
                                         ctypes.c_size_t, _vp, _vp]),
     "gee_bitmap_shard_encode": (_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i32, _u32, _vp, _vp, _vp,
                                        ctypes.c_size_t, _vp, _vp]),
+    "gee_shuffle_buckets": (_i64, [_i64]),
+    "gee_shuffle_row_hist": (_int, [_vp, _vp, _i64, _i64, _int, _vp, _vp]),
+    "gee_shuffle_bounds": (_int, [_vp, _i64, _int, _vp, _vp]),
+    "gee_partition_workspace": (_int, [_i64, _int, _szp]),
+    "gee_partition": (_int, [_vp, _vp, _vp, _int, _i64, _int, _vp, _int, _vp, _vp, _vp, _vp, _vp,
+                             ctypes.c_size_t, _vp]),
     "gee_launch_count": (ctypes.c_uint64, []),
     "gee_reset_launch_count": (None, []),
     "gee_profile_start": (_int, [_vp]),

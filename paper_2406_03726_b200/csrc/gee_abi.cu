@@ -66,6 +66,16 @@ bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed, int w
 int set_force_buckets(int v);
 int set_embed_flat_bytes(int v);
 int set_embed_flat_rowmax(int v);
+size_t partition_workspace(int64_t E, int world);
+int shuffle_row_hist(const int64_t *rows, const int64_t *cols, int64_t E, int64_t n, int directed, int64_t nb,
+                     unsigned long long *hist, cudaStream_t st);
+int shuffle_bounds(const unsigned long long *hist, int64_t nb, int64_t n, int world, int64_t *bounds,
+                   cudaStream_t st);
+int partition(const int64_t *rows, const int64_t *cols, const void *w, int wt, int64_t E, int directed,
+              const int64_t *bounds, int world, int64_t *out_rows, int64_t *out_cols, void *out_w,
+              unsigned long long *counts, void *ws, size_t ws_bytes, cudaStream_t st);
+int shuffle_max_world();
+int64_t shuffle_buckets(int64_t n);
 int sort_csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, int64_t E, int64_t n_rows,
                    int64_t n_cols, int directed, int force_vals, int64_t *row_ptr, int32_t *col, double *val,
                    int64_t *nnz, unsigned deg_flags, double *deg, double *scale, void *ws, size_t ws_bytes,
@@ -388,3 +398,38 @@ int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, in
 }
 
 }  // extern "C"
+
+// ---- distributed CSR build: the edge shuffle (k_shuffle.cu) ----------------
+int64_t gee_shuffle_buckets(int64_t n_nodes) { return n_nodes > 0 ? shuffle_buckets(n_nodes) : 0; }
+
+int gee_shuffle_row_hist(const int64_t *rows, const int64_t *cols, int64_t n_edges, int64_t n_nodes, int directed,
+                         uint64_t *hist, void *stream) {
+    if (n_edges < 0 || n_nodes <= 0 || !hist || (n_edges && (!rows || !cols))) return GEE_E_ARG;
+    return shuffle_row_hist(rows, cols, n_edges, n_nodes, directed, shuffle_buckets(n_nodes),
+                            reinterpret_cast<unsigned long long *>(hist), (cudaStream_t)stream);
+}
+
+int gee_shuffle_bounds(const uint64_t *hist, int64_t n_nodes, int world, int64_t *bounds, void *stream) {
+    if (n_nodes <= 0 || world < 1 || world > shuffle_max_world() || !hist || !bounds) return GEE_E_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    return shuffle_bounds(reinterpret_cast<const unsigned long long *>(hist), shuffle_buckets(n_nodes), n_nodes,
+                          world, bounds, st);
+}
+
+int gee_partition_workspace(int64_t n_edges, int world, size_t *ws_bytes) {
+    if (!ws_bytes || n_edges < 0 || world < 1 || world > shuffle_max_world()) return GEE_E_ARG;
+    *ws_bytes = partition_workspace(n_edges, world);
+    return GEE_OK;
+}
+
+int gee_partition(const int64_t *rows, const int64_t *cols, const void *w, int w_type, int64_t n_edges, int directed,
+                  const int64_t *bounds, int world, int64_t *out_rows, int64_t *out_cols, void *out_w,
+                  uint64_t *counts, void *ws, size_t ws_bytes, void *stream) {
+    if (n_edges < 0 || world < 1 || world > shuffle_max_world() || !bounds || !counts) return GEE_E_ARG;
+    if (w_type != GEE_W_UNIT && w_type != GEE_W_F64 && w_type != GEE_W_F32) return GEE_E_ARG;
+    if (n_edges && (!rows || !cols || !out_rows || !out_cols)) return GEE_E_ARG;
+    if (n_edges && w_type != GEE_W_UNIT && (!w || !out_w)) return GEE_E_ARG;
+    if (!ws && partition_workspace(n_edges, world) > 0 && n_edges) return GEE_E_WORKSPACE;
+    return partition(rows, cols, w, w_type, n_edges, directed, bounds, world, out_rows, out_cols, out_w,
+                     reinterpret_cast<unsigned long long *>(counts), ws, ws_bytes, (cudaStream_t)stream);
+}

@@ -211,6 +211,41 @@ class GpuShardOps:
         return z
 
 
+    # -- edge shuffle (distributed CSR build from edge-list slices) ----------
+    def row_hist(self, rows, cols, n, directed):
+        """Stream entries of this slice per coarse row bucket: int64[B]."""
+        nb = int(self.lib.gee_shuffle_buckets(n))
+        hist = torch.zeros(max(nb, 1), dtype=torch.int64, device=self.dev)
+        _lib.check(self.lib.gee_shuffle_row_hist(_device.ptr(rows), _device.ptr(cols), int(rows.numel()), n,
+                                                 int(bool(directed)), _device.ptr(hist), _device.stream_handle()))
+        return hist[:nb]
+
+    def shuffle_bounds(self, hist, n, world):
+        """Row ranges with near-equal stream entries: int64[world + 1]."""
+        bounds = torch.empty(world + 1, dtype=torch.int64, device=self.dev)
+        _lib.check(self.lib.gee_shuffle_bounds(_device.ptr(hist), n, world, _device.ptr(bounds),
+                                               _device.stream_handle()))
+        return bounds
+
+    def partition(self, rows, cols, w, directed, bounds, world):
+        """Stable partition into [half][dest] send buckets; returns the three
+        send buffers and the 2*world bucket sizes (host ints)."""
+        e = int(rows.numel())
+        cap = max(2 * e, 1)
+        wt = _lib.W_UNIT if w is None else (_lib.W_F32 if w.dtype == torch.float32 else _lib.W_F64)
+        out_r = torch.empty(cap, dtype=torch.int64, device=self.dev)
+        out_c = torch.empty(cap, dtype=torch.int64, device=self.dev)
+        out_w = None if w is None else torch.empty(cap, dtype=w.dtype, device=self.dev)
+        counts = torch.empty(2 * world, dtype=torch.int64, device=self.dev)
+        nb = _lib.size_query(self.lib.gee_partition_workspace, e, world)
+        ws = _device.WORKSPACE.get(max(nb, 256), self.dev)
+        _lib.check(self.lib.gee_partition(
+            _device.ptr(rows), _device.ptr(cols), _device.ptr(w), wt, e, int(bool(directed)), _device.ptr(bounds),
+            world, _device.ptr(out_r), _device.ptr(out_c), _device.ptr(out_w), _device.ptr(counts),
+            _device.ptr(ws), ws.numel(), _device.stream_handle()))
+        return out_r, out_c, out_w, counts.cpu().tolist()
+
+
 # ---------------------------------------------------------------------------
 # orchestration
 # ---------------------------------------------------------------------------
@@ -263,6 +298,100 @@ def encode_sharded(edges, labels, opts=None, group=None, ops=None):
     else:
         z = encode_rows(ops, stream, lab, n, k, flags, ranges, rank, group)
     return z, (rb, re)
+
+
+# ---------------------------------------------------------------------------
+# distributed CSR build: every rank starts from its own slice of the edge list
+# ---------------------------------------------------------------------------
+def shuffle_plan(ops, rows, cols, n, directed, world, group=None):
+    """Row ranges from the ALL-REDUCED coarse row histogram of every rank's
+    slice (device kernels; replaces the host stream_row_counts/row_ranges)."""
+    hist = ops.row_hist(rows, cols, n, directed)
+    dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
+    bounds = ops.shuffle_bounds(hist, n, world)
+    b = bounds.cpu().tolist()
+    return bounds, [(b[p], b[p + 1]) for p in range(world)]
+
+
+def shuffle_stream(ops, rows, cols, w, directed, bounds, world, group=None):
+    """ALL-TO-ALL of the stably partitioned slice: the originals region, then
+    the mirrors region.  Concatenated in source-rank order they are this
+    rank's slice of the symmetrised stream in stream order -- exactly what
+    local_stream() selects from a replicated list (so the CSR is bitwise
+    shard-invariant)."""
+    out_r, out_c, out_w, counts = ops.partition(rows, cols, w, directed, bounds, world)
+    send_o, send_m = counts[:world], counts[world:]
+    dev = out_r.device
+    sizes = torch.tensor([[send_o[d], send_m[d]] for d in range(world)], dtype=torch.int64, device=dev)
+    got = torch.empty_like(sizes)
+    dist.all_to_all_single(got.view(-1), sizes.view(-1), group=group)
+    got = got.cpu().tolist()
+    recv_o, recv_m = [g[0] for g in got], [g[1] for g in got]
+    n_o = sum(send_o)
+
+    def exchange(buf, lo, send, recv):
+        out = torch.empty(sum(recv), dtype=buf.dtype, device=dev)
+        dist.all_to_all_single(out, buf[lo:lo + sum(send)].contiguous(), recv, send, group=group)
+        return out
+
+    parts = []
+    for buf in (out_r, out_c, out_w):
+        if buf is None:
+            parts.append(None)
+            continue
+        parts.append(torch.cat([exchange(buf, 0, send_o, recv_o), exchange(buf, n_o, send_m, recv_m)]))
+    return parts[0], parts[1], parts[2]
+
+
+def encode_distributed(rows, cols, weights, n, directed, labels, k, opts=None, group=None, ops=None):
+    """Row-sharded encode from an edge list PARTITIONED across ranks: rank p
+    passes its contiguous slice (rows, cols, weights: p-th stream range of the
+    original EdgeList, slices in rank order) and the replicated labels.
+    Device row histogram -> ALL-REDUCE -> row ranges -> stable partition ->
+    ALL-TO-ALL edge shuffle -> encode_rows / encode_rows_bitmap.  Returns
+    (z_local, (rb, re))."""
+    from .errors import StructuralError
+    from .graph import options_flags
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    ops = ops or GpuShardOps(_device.require_gpu())
+    dev = ops.dev
+    flags = options_flags(opts)
+    rows = _device.to_device(rows, torch.int64, dev)
+    cols = _device.to_device(cols, torch.int64, dev)
+    if rows.numel() != cols.numel():
+        raise StructuralError("rows and cols of the slice differ in length")
+    if rows.numel():
+        lo = torch.minimum(rows.min(), cols.min())
+        hi = torch.maximum(rows.max(), cols.max())
+        bad = torch.stack([lo < 0, hi >= n]).any().to(torch.int64)
+    else:
+        bad = torch.zeros((), dtype=torch.int64, device=dev)
+    w = None
+    unit = torch.ones((), dtype=torch.int64, device=dev)
+    if weights is not None:
+        w = weights if isinstance(weights, torch.Tensor) else torch.as_tensor(np.asarray(weights))
+        w = w.to(dev)
+        if w.dtype not in (torch.float32, torch.float64):
+            w = w.to(torch.float64)
+        if w.numel():
+            bad = bad | (~torch.isfinite(w)).any().to(torch.int64)
+            unit = (w == 1.0).all().to(torch.int64)
+    flag = torch.stack([bad, 1 - unit])
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)   # any rank bad / any weight != 1.0
+    flag = flag.cpu().tolist()
+    if flag[0]:
+        raise StructuralError("edge endpoints must lie in [0, n) and weights must be finite")
+    if not flag[1]:
+        w = None  # every weight is 1.0 on every rank: the unit-weight paths
+    bounds, ranges = shuffle_plan(ops, rows, cols, n, directed, world, group)
+    stream = shuffle_stream(ops, rows, cols, w, directed, bounds, world, group)
+    lab = _device.to_device(labels.labels if hasattr(labels, "labels") else labels, torch.int64, dev)
+    if ops.bitmap_ok(n, k, w is not None):
+        z = encode_rows_bitmap(ops, stream, lab, n, k, flags, ranges, rank, group)
+    else:
+        z = encode_rows(ops, stream, lab, n, k, flags, ranges, rank, group)
+    return z, ranges[rank]
 
 
 def gather_z(z_local, ranges, group=None):

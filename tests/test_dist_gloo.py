@@ -23,6 +23,59 @@ from paper_2406_03726_b200 import dist as gdist
 LAP, DIAG, CORR = 1, 2, 4
 
 
+def shuffle_hist_np(rows, cols, n, directed, max_buckets=16384):
+    """Stream entries per coarse row bucket floor(r * B / n), B = min(n, 16384)."""
+    nb = min(n, max_buckets)
+    b = (rows.astype(np.int64) * nb) // n
+    h = np.bincount(b, minlength=nb)
+    if not directed:
+        off = rows != cols
+        h = h + np.bincount((cols[off].astype(np.int64) * nb) // n, minlength=nb)
+    return h.astype(np.int64)
+
+
+def shuffle_bounds_np(hist, n, world):
+    """dist.row_ranges on bucket granularity (bucket b starts at row ceil(b n / B))."""
+    nb = len(hist)
+    total = int(hist.sum())
+    bounds = [0]
+    run, b = 0, 0
+    for p in range(1, world):
+        target = total * p // world
+        while b < nb and run < target:
+            run += int(hist[b])
+            b += 1
+        row = min(max(-(-b * n // nb), bounds[-1]), n)
+        bounds.append(row)
+    bounds.append(n)
+    return np.array(bounds, np.int64)
+
+
+def partition_np(rows, cols, w, directed, bounds, world):
+    """Stable [half][dest] partition: originals by row, mirrored off-diagonals
+    (as (col, row)) by column, each bucket in slice order."""
+    dest_o = np.searchsorted(bounds[1:-1], rows, side="right")
+    parts_r, parts_c, parts_w, counts = [], [], [], []
+    for half in (0, 1):
+        if half == 0:
+            rr, cc, ww, dd = rows, cols, w, dest_o
+        else:
+            m = (rows != cols) if not directed else np.zeros(rows.size, bool)
+            rr, cc = cols[m], rows[m]
+            ww = None if w is None else w[m]
+            dd = np.searchsorted(bounds[1:-1], rr, side="right")
+        for d in range(world):
+            sel = dd == d
+            parts_r.append(rr[sel])
+            parts_c.append(cc[sel])
+            if w is not None:
+                parts_w.append(ww[sel])
+            counts.append(int(sel.sum()))
+    cat = lambda xs, dt: np.concatenate(xs) if xs else np.zeros(0, dt)
+    return (cat(parts_r, np.int64), cat(parts_c, np.int64),
+            None if w is None else cat(parts_w, w.dtype), np.array(counts, np.int64))
+
+
 class OracleShardOps:
     """CPU stand-in for GpuShardOps built from the oracle (test only)."""
 
@@ -69,6 +122,24 @@ class OracleShardOps:
     def bm_degrees(self, r, c, n, rb, re, labels, k, flags):
         self._labels = labels.numpy().astype(np.int64)
         return torch.as_tensor(np.bincount(r.numpy() - rb, minlength=re - rb).astype(np.int32))
+
+    @staticmethod
+    def bitmap_ok(n, k, weighted):
+        return not weighted and 1 <= n <= 16384 and 1 <= k <= 8
+
+    # edge shuffle: numpy restatements of k_shuffle.cu (tests/test_gpu_dist.py
+    # pins the kernels against these)
+    def row_hist(self, rows, cols, n, directed):
+        return torch.as_tensor(shuffle_hist_np(rows.numpy(), cols.numpy(), n, directed))
+
+    def shuffle_bounds(self, hist, n, world):
+        return torch.as_tensor(shuffle_bounds_np(hist.numpy(), n, world))
+
+    def partition(self, rows, cols, w, directed, bounds, world):
+        r, c, ww, counts = partition_np(rows.numpy(), cols.numpy(), None if w is None else w.numpy(), directed,
+                                        bounds.numpy(), world)
+        return (torch.as_tensor(r), torch.as_tensor(c), None if ww is None else torch.as_tensor(ww),
+                counts.tolist())
 
     def bm_encode(self, r, c, n, rb, re, k, flags, deg_all, check=True):
         rr = r.numpy()
@@ -184,3 +255,74 @@ def test_local_stream_keeps_stream_order():
     counts = gdist.stream_row_counts(rows, cols, 3, False)
     # 5 originals + 4 reversed off-diagonals (e=2 is a self loop, counted once)
     assert counts.tolist() == [3, 2, 4] and counts.sum() == 9
+
+
+def _slice_worker(rank, world, port, case, flags, cuts, out):
+    """Every rank holds ONLY its contiguous slice of the original edge list."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, rows, cols, w, labels, k, directed = case
+        lo, hi = cuts[rank], cuts[rank + 1]
+        z, (rb, re) = gdist.encode_distributed(torch.as_tensor(rows[lo:hi]), torch.as_tensor(cols[lo:hi]),
+                                               torch.as_tensor(w[lo:hi]), n, directed, torch.as_tensor(labels),
+                                               k, _opts(flags), ops=OracleShardOps())
+        ranges = [None] * world
+        dist.all_gather_object(ranges, (rb, re))
+        full = gdist.gather_z(z, ranges)
+        if rank == 0:
+            out.put(full.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def _opts(flags):
+    from paper_2406_03726_b200.graph import EmbedOptions
+    return EmbedOptions(laplacian=bool(flags & LAP), diagonal=bool(flags & DIAG), correlation=bool(flags & CORR))
+
+
+@pytest.mark.parametrize("weighted,directed,world,flags", [
+    (True, False, 3, LAP | DIAG | CORR), (False, False, 2, LAP | DIAG | CORR),
+    (True, True, 2, LAP), (False, True, 3, LAP | CORR)])
+def test_edge_shuffle_from_partitioned_slices(weighted, directed, world, flags):
+    """Distributed CSR build: ranks start from uneven slices of the edge list
+    (one of them empty in the 3-rank cases); the all-to-all edge shuffle must
+    reproduce the unsharded Z bitwise (weighted: CSR path; unit weights with
+    n <= 16384 and k <= 3: the bitmap path)."""
+    case = _graph(21 + flags + 2 * directed + 4 * weighted, directed=directed, weighted=weighted, k=3)
+    n, rows, cols, w, labels, k, _ = case
+    m = rows.size
+    cuts = [0, m // 3, m] if world == 2 else [0, 700, 700, m]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_slice_worker, args=(world, _free_port(), case, flags, cuts, q), nprocs=world, join=True)
+    z = q.get(timeout=60)
+    st, zr, _ = O.encode_edges(rows, cols, w, n, directed, labels, k, flags)
+    assert st == O.OK
+    assert z.shape == zr.shape and np.array_equal(z, zr)
+
+
+def test_partition_np_matches_local_stream():
+    """The restated partition + exchange order equals local_stream() on every
+    destination (the property the shuffle's bitwise invariance rests on)."""
+    n, rows, cols, w, labels, k, directed = _graph(5, directed=False)
+    cuts = [0, 500, 1200, rows.size]
+    world = 3
+    hist = sum(shuffle_hist_np(rows[a:b], cols[a:b], n, directed) for a, b in zip(cuts, cuts[1:]))
+    bounds = shuffle_bounds_np(hist, n, world)
+    full_counts = gdist.stream_row_counts(rows, cols, n, directed)
+    assert hist.sum() == full_counts.sum()
+    sent = [partition_np(rows[a:b], cols[a:b], w[a:b], directed, bounds, world) for a, b in zip(cuts, cuts[1:])]
+    for d in range(world):
+        got = {0: [], 1: []}
+        for r, c, ww, cnt in sent:
+            off = np.concatenate([[0], np.cumsum(cnt)])
+            for half in (0, 1):
+                b = half * world + d
+                got[half].append((r[off[b]:off[b + 1]], c[off[b]:off[b + 1]], ww[off[b]:off[b + 1]]))
+        seq = got[0] + got[1]
+        r = np.concatenate([x[0] for x in seq])
+        c = np.concatenate([x[1] for x in seq])
+        ww = np.concatenate([x[2] for x in seq])
+        er, ec, ew = gdist.local_stream(rows, cols, w, directed, int(bounds[d]), int(bounds[d + 1]))
+        assert np.array_equal(r, er) and np.array_equal(c, ec) and np.array_equal(ww, ew)

@@ -166,3 +166,99 @@ def test_single_rank_nccl_group_bitmap_path():
         z_close(z.cpu().numpy(), zr, zr_pre=pre)
     finally:
         dist.destroy_process_group()
+
+
+# ---- distributed CSR build: the edge shuffle kernels (k_shuffle.cu) ----------
+from test_dist_gloo import partition_np, shuffle_bounds_np, shuffle_hist_np  # noqa: E402
+
+
+def _shuffle_case(seed, n, m, kind, directed):
+    rng = np.random.default_rng(seed)
+    rows = rng.integers(0, n, m)
+    cols = rng.integers(0, n, m)
+    rows[: m // 10] = 3  # a hub row (R-MAT-like skew) and self loops
+    cols[: m // 50] = 3
+    if kind == "f64":
+        w = 1.0 - rng.random(m)
+    elif kind == "f32":
+        w = (1.0 - rng.random(m, dtype=np.float32)).astype(np.float32)
+    else:
+        w = None
+    return rows, cols, w
+
+
+@pytest.mark.parametrize("n,m,kind,directed,world", [
+    (5000, 60_000, "f64", False, 3), (5000, 60_000, "f32", True, 5), (40_000, 200_000, "unit", False, 8),
+    (100, 0, "f64", False, 2), (20_000, 100_000, "f64", True, 1), (70_000, 50_000, "f32", False, 16)])
+def test_shuffle_kernels_match_restatement(n, m, kind, directed, world):
+    """gee_shuffle_row_hist / gee_shuffle_bounds / gee_partition are bit-exact
+    against the numpy restatements the gloo tests drive the orchestration with,
+    and the per-destination exchange order reproduces local_stream()."""
+    rows, cols, w = _shuffle_case(n + m + world, n, m, kind, directed)
+    ops = gdist.GpuShardOps("cuda")
+    cuts = np.linspace(0, m, world + 1).astype(np.int64)
+    if world > 1:
+        cuts[1] = cuts[0]  # an empty slice
+    dev = torch.device("cuda")
+    hist = None
+    for a, b in zip(cuts, cuts[1:]):
+        r = torch.as_tensor(rows[a:b], device=dev)
+        c = torch.as_tensor(cols[a:b], device=dev)
+        h = ops.row_hist(r, c, n, directed).cpu().numpy()
+        assert np.array_equal(h, shuffle_hist_np(rows[a:b], cols[a:b], n, directed))
+        hist = h if hist is None else hist + h
+    bounds = ops.shuffle_bounds(torch.as_tensor(hist, device=dev), n, world)
+    assert np.array_equal(bounds.cpu().numpy(), shuffle_bounds_np(hist, n, world))
+    sent = []
+    for a, b in zip(cuts, cuts[1:]):
+        r = torch.as_tensor(rows[a:b], device=dev)
+        c = torch.as_tensor(cols[a:b], device=dev)
+        ww = None if w is None else torch.as_tensor(w[a:b], device=dev)
+        gr, gc, gw, cnt = ops.partition(r, c, ww, directed, bounds, world)
+        er, ec, ew, ecnt = partition_np(rows[a:b], cols[a:b], None if w is None else w[a:b], directed,
+                                        bounds.cpu().numpy(), world)
+        tot = int(sum(cnt))
+        assert cnt == ecnt.tolist()
+        assert np.array_equal(gr[:tot].cpu().numpy(), er) and np.array_equal(gc[:tot].cpu().numpy(), ec)
+        if w is not None:
+            assert gw.dtype == ww.dtype and np.array_equal(gw[:tot].cpu().numpy(), ew)
+        sent.append((gr[:tot].cpu().numpy(), gc[:tot].cpu().numpy(),
+                     None if w is None else gw[:tot].cpu().numpy(), np.asarray(cnt)))
+    bnd = bounds.cpu().numpy()
+    for d in range(world):
+        seq = []
+        for half in (0, 1):
+            for r, c, ww, cnt in sent:
+                off = np.concatenate([[0], np.cumsum(cnt)])
+                lo, hi = off[half * world + d], off[half * world + d + 1]
+                seq.append((r[lo:hi], c[lo:hi], None if ww is None else ww[lo:hi]))
+        er, ec, ew = gdist.local_stream(rows, cols, w, directed, int(bnd[d]), int(bnd[d + 1]))
+        assert np.array_equal(np.concatenate([x[0] for x in seq]), er)
+        assert np.array_equal(np.concatenate([x[1] for x in seq]), ec)
+        if w is not None:
+            assert np.array_equal(np.concatenate([x[2] for x in seq]), ew)
+
+
+@pytest.mark.parametrize("kind,k,flags", [("f32", 50, 7), ("unit", 3, 7), ("f64", 20, 1)])
+def test_single_rank_nccl_group_edge_shuffle(kind, k, flags):
+    """encode_distributed through a real NCCL group (all-reduce of the row
+    histogram, all-to-all of the partitioned slice) against the oracle."""
+    import torch.distributed as dist
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        n, m = 3000, 30_000
+        rows, cols, w = _shuffle_case(k + flags, n, m, kind, False)
+        labels = np.random.default_rng(k).integers(-1, k, n)
+        w_in = np.ones(m) if w is None else w
+        z, (rb, re) = gdist.encode_distributed(rows, cols, w_in, n, False, labels, k,
+                                               G.EmbedOptions(bool(flags & 1), bool(flags & 2), bool(flags & 4)))
+        assert (rb, re) == (0, n)
+        st, zr, _ = O.encode_edges(rows, cols, np.asarray(w_in, np.float64), n, False, labels, k, flags)
+        assert st == O.OK
+        z_close(z.cpu().numpy(), zr)
+    finally:
+        dist.destroy_process_group()
