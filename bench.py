@@ -60,6 +60,10 @@ def parse():
                    help="debug: longest row a flat embed block takes (GEE_DEBUG_EMBED_FLAT_ROWMAX)")
     p.add_argument("--force-path", type=int, default=0,
                    help="debug: CSR assembly path hook (gee_debug_set GEE_DEBUG_FORCE_BUCKETS)")
+    p.add_argument("--shuffle", action="store_true",
+                   help="sharded step from per-rank slices of the edge list: device row histogram, "
+                        "all-reduce, partition and all-to-all edge shuffle inside the timed region "
+                        "(dist.encode_distributed; implies --sharded)")
     p.add_argument("--sharded", action="store_true",
                    help="run the row-sharded multi-GPU step even with one rank (exercises dist.py under NCCL)")
     return p.parse_args()
@@ -264,7 +268,7 @@ def run_b200(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1 or args.sharded:
+    if world > 1 or args.sharded or args.shuffle:
         if not dist.is_initialized():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29533")

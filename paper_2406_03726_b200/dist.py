@@ -427,12 +427,28 @@ def bench_sharded(args, rank, world, dev):
     if bool((w == 1.0).all()):
         w = None
     lab = torch.as_tensor(cfg["labels"], device=dev)
-    ranges = shard_plan(rows, cols, n, directed, world)
-    rb, re = ranges[rank]
-    stream = local_stream(rows, cols, w, directed, rb, re)
+    shuffle = bool(getattr(args, "shuffle", False))
+    if shuffle:
+        # distributed CSR build: this rank holds only its contiguous slice of
+        # the original edge list; the whole shuffle is inside the timed region
+        e_all = int(rows.numel())
+        lo, hi = e_all * rank // world, e_all * (rank + 1) // world
+        rs, cs = rows[lo:hi].clone(), cols[lo:hi].clone()
+        ws_ = None if w is None else w[lo:hi].clone()
+        del rows, cols, w
+        ranges = None
+    else:
+        ranges = shard_plan(rows, cols, n, directed, world)
+        rb, re = ranges[rank]
+        stream = local_stream(rows, cols, w, directed, rb, re)
     ops = GpuShardOps(dev)
-    use_bm = ops.bitmap_ok(n, k, w is not None)
-    if use_bm:
+    from .graph import EmbedOptions
+    opts = EmbedOptions(bool(flags & _lib.LAPLACIAN), bool(flags & _lib.DIAGONAL), bool(flags & _lib.CORRELATION))
+    use_bm = (not shuffle) and ops.bitmap_ok(n, k, w is not None)
+    if shuffle:
+        def step():
+            return encode_distributed(rs, cs, ws_, n, directed, lab, k, opts, ops=ops)
+    elif use_bm:
         def step():
             return encode_rows_bitmap(ops, stream, lab, n, k, flags, ranges, rank, check=False)
     else:
@@ -479,7 +495,10 @@ def bench_sharded(args, rank, world, dev):
                 "data": "synthetic (seeded, BASELINE.json shapes)",
                 "config": {"workload": f"configs[{args.config}] {cfg['name']}", "n_nodes": n, "n_edges": e,
                            "k_classes": k,
-                           "parallelism": (f"row-sharded x{world}, bitmap path (NCCL all-gather of degrees)"
+                           "parallelism": (f"edge-list slices x{world}: device row histogram, NCCL all-reduce, "
+                                           "stable partition, NCCL all-to-all edge shuffle, then the row-sharded "
+                                           "encode" if shuffle else
+                                           f"row-sharded x{world}, bitmap path (NCCL all-gather of degrees)"
                                            if use_bm else f"row-sharded x{world} (NCCL all-reduce n_k, "
                                            "all-gather labels + Laplacian scale)"),
                            "cuda_graph": graphed}}
