@@ -73,15 +73,15 @@ __device__ __forceinline__ double fold_row(const int32_t *col, const double *val
     return d;
 }
 
-__global__ void k_degree(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                         const double *__restrict__ val, int64_t n, unsigned flags,
-                         double *__restrict__ deg, double *__restrict__ scale, int32_t *err,
-                         const unsigned *guard, unsigned *__restrict__ hubs, unsigned *__restrict__ n_hubs,
-                         unsigned *__restrict__ work) {
-    if (guard && *guard == 0) return;  // device-side skip (unit-weight graphs use k_degree_stream)
+// skip_hubs: rows over kDegHub belong to hub CTAs (listed beforehand);
+// else, with a hub list, they are appended to it for k_degree_hub
+__device__ __forceinline__ void degree_rows(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                            const double *__restrict__ val, int64_t n, unsigned flags,
+                                            double *__restrict__ deg, double *__restrict__ scale, int32_t *err,
+                                            unsigned *__restrict__ hubs, unsigned *__restrict__ n_hubs,
+                                            unsigned *__restrict__ work, bool skip_hubs, int64_t warp,
+                                            int64_t nwarps) {
     const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const bool diag = (flags & GEE_DIAGONAL) != 0;
     // A warp takes 32 rows at a time, rows c, c + nc, c + 2 nc, ... of chunk c
     // (long rows cluster by id in power-law graphs); lanes fold the short
@@ -107,9 +107,9 @@ __global__ void k_degree(const int64_t *__restrict__ row_ptr, const int32_t *__r
         if (r < n && L <= kDegShort) degree_store(deg, scale, r, fold_row(col, val, r, s, e, diag), err);
         // with a hub list, rows over kDegHub go to k_degree_hub; without one
         // (gee_degree has no workspace) the warp takes them too
-        const bool hub = hubs && L > kDegHub;
+        const bool hub = (hubs || skip_hubs) && L > kDegHub;
         unsigned longer = __ballot_sync(0xffffffffu, r < n && L > kDegShort && !hub);
-        if (r < n && hub) hubs[atomicAdd(n_hubs, 1u)] = (unsigned)r;
+        if (r < n && hub && !skip_hubs) hubs[atomicAdd(n_hubs, 1u)] = (unsigned)r;
         while (longer) {
             const int src = __ffs(longer) - 1;
             longer &= longer - 1;
@@ -150,6 +150,16 @@ __global__ void k_degree(const int64_t *__restrict__ row_ptr, const int32_t *__r
     }
 }
 
+__global__ void k_degree(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                         const double *__restrict__ val, int64_t n, unsigned flags,
+                         double *__restrict__ deg, double *__restrict__ scale, int32_t *err,
+                         const unsigned *guard, unsigned *__restrict__ hubs, unsigned *__restrict__ n_hubs,
+                         unsigned *__restrict__ work) {
+    if (guard && *guard == 0) return;  // device-side skip (unit-weight graphs use k_degree_stream)
+    degree_rows(row_ptr, col, val, n, flags, deg, scale, err, hubs, n_hubs, work, false,
+                ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, ((int64_t)gridDim.x * blockDim.x) >> 5);
+}
+
 // one CTA per hub row: certificate by block reductions, else thread 0 folds
 // while the other warps stage the next 2048 entries in shared memory
 constexpr int kHubThreads = 512, kHubStage = 2048;
@@ -166,20 +176,17 @@ __device__ __forceinline__ double fold_plain(const double *x, int lo, int hi, do
     return d;
 }
 
-__global__ void __launch_bounds__(kHubThreads) k_degree_hub(const int64_t *__restrict__ row_ptr,
-                                                            const int32_t *__restrict__ col,
-                                                            const double *__restrict__ val, unsigned flags,
-                                                            double *__restrict__ deg, double *__restrict__ scale,
-                                                            int32_t *err, const unsigned *guard,
-                                                            const unsigned *__restrict__ hubs,
-                                                            const unsigned *__restrict__ n_hubs) {
-    if (guard && *guard == 0) return;
+__device__ __forceinline__ void degree_hubs(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                            const double *__restrict__ val, unsigned flags,
+                                            double *__restrict__ deg, double *__restrict__ scale, int32_t *err,
+                                            const unsigned *__restrict__ hubs, const unsigned *__restrict__ n_hubs,
+                                            unsigned first, unsigned step) {
     __shared__ double sv[2][kHubStage];
     __shared__ double dred[33];
     __shared__ int ired[33];
     const int tid = threadIdx.x, nt = blockDim.x;
     const bool diag = (flags & GEE_DIAGONAL) != 0;
-    for (unsigned h = blockIdx.x; h < *n_hubs; h += gridDim.x) {
+    for (unsigned h = first; h < *n_hubs; h += step) {
         const int64_t r = hubs[h];
         const int64_t s = row_ptr[r], e = row_ptr[r + 1];
         const int64_t L = e - s;
@@ -258,21 +265,75 @@ __global__ void __launch_bounds__(kHubThreads) k_degree_hub(const int64_t *__res
     }
 }
 
+__global__ void __launch_bounds__(kHubThreads) k_degree_hub(const int64_t *__restrict__ row_ptr,
+                                                            const int32_t *__restrict__ col,
+                                                            const double *__restrict__ val, unsigned flags,
+                                                            double *__restrict__ deg, double *__restrict__ scale,
+                                                            int32_t *err, const unsigned *guard,
+                                                            const unsigned *__restrict__ hubs,
+                                                            const unsigned *__restrict__ n_hubs) {
+    if (guard && *guard == 0) return;
+    degree_hubs(row_ptr, col, val, flags, deg, scale, err, hubs, n_hubs, blockIdx.x, gridDim.x);
+}
+
+// rows over kDegHub entries -> hubs[], count in *n_hubs (warp-aggregated)
+__global__ void k_hub_list(const int64_t *__restrict__ row_ptr, int64_t n, const unsigned *guard,
+                           unsigned *__restrict__ hubs, unsigned *__restrict__ n_hubs) {
+    if (guard && *guard == 0) return;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_round = (n + 31) & ~int64_t(31);
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_round; r += stride) {
+        const bool hub = r < n && row_ptr[r + 1] - row_ptr[r] > kDegHub;
+        const unsigned m = __ballot_sync(0xffffffffu, hub);
+        if (!m) continue;
+        const int leader = __ffs(m) - 1;
+        unsigned base = 0;
+        if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(n_hubs, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (hub) hubs[base + __popc(m & lanemask_lt())] = (unsigned)r;
+    }
+}
+
+// The hub rows' serial folds overlap the other rows: CTAs [0, hub_ctas) take
+// the listed hubs (one CTA per hub, as k_degree_hub), the rest run the
+// warp/lane tiers of k_degree over every other row.
+__global__ void __launch_bounds__(kHubThreads) k_degree_fused(const int64_t *__restrict__ row_ptr,
+                                                              const int32_t *__restrict__ col,
+                                                              const double *__restrict__ val, int64_t n,
+                                                              unsigned flags, double *__restrict__ deg,
+                                                              double *__restrict__ scale, int32_t *err,
+                                                              const unsigned *guard, const unsigned *__restrict__ hubs,
+                                                              const unsigned *__restrict__ n_hubs,
+                                                              unsigned *__restrict__ work, unsigned hub_ctas) {
+    if (guard && *guard == 0) return;
+    if (blockIdx.x < hub_ctas) {
+        degree_hubs(row_ptr, col, val, flags, deg, scale, err, hubs, n_hubs, blockIdx.x, hub_ctas);
+        return;
+    }
+    const int64_t b = blockIdx.x - hub_ctas, nb = gridDim.x - hub_ctas;
+    degree_rows(row_ptr, col, val, n, flags, deg, scale, err, nullptr, nullptr, work, true,
+                (b * blockDim.x + threadIdx.x) >> 5, (nb * blockDim.x) >> 5);
+}
+
 // hub_buf: [1 + nnz / kDegHub] words (count, then row ids) or null
 static int launch_degree(const int64_t *row_ptr, const int32_t *col, const double *val, int64_t n, unsigned flags,
                          double *deg, double *scale, int32_t *err, const unsigned *guard, unsigned *hub_buf,
                          cudaStream_t st) {
     // hub_buf: [0] hub count, [1] chunk counter, [2..] hub rows
-    if (hub_buf) GEE_CHECK_CUDA(cudaMemsetAsync(hub_buf, 0, 2 * sizeof(unsigned), st));
-    k_degree<<<grid_for((n + 31) / 32 * 32, 256, 8), 256, 0, st>>>(row_ptr, col, val, n, flags, deg, scale, err,
-                                                                   guard, hub_buf ? hub_buf + 2 : nullptr, hub_buf,
-                                                                   hub_buf ? hub_buf + 1 : nullptr);
-    GEE_CHECK_LAUNCH("k_degree");
-    if (hub_buf) {
-        k_degree_hub<<<(unsigned)num_sms(), kHubThreads, 0, st>>>(row_ptr, col, val, flags, deg, scale, err, guard,
-                                                                  hub_buf + 2, hub_buf);
-        GEE_CHECK_LAUNCH("k_degree_hub");
+    if (!hub_buf) {
+        k_degree<<<grid_for((n + 31) / 32 * 32, 256, 8), 256, 0, st>>>(row_ptr, col, val, n, flags, deg, scale, err,
+                                                                       guard, nullptr, nullptr, nullptr);
+        GEE_CHECK_LAUNCH("k_degree");
+        return GEE_OK;
     }
+    GEE_CHECK_CUDA(cudaMemsetAsync(hub_buf, 0, 2 * sizeof(unsigned), st));
+    k_hub_list<<<grid_for(n, 256, 8), 256, 0, st>>>(row_ptr, n, guard, hub_buf + 2, hub_buf);
+    GEE_CHECK_LAUNCH("k_hub_list");
+    const unsigned hub_ctas = (unsigned)num_sms();
+    const unsigned rows_ctas = grid_for((n + 31) / 32 * 32, kHubThreads, 4);
+    k_degree_fused<<<hub_ctas + rows_ctas, kHubThreads, 0, st>>>(row_ptr, col, val, n, flags, deg, scale, err, guard,
+                                                                 hub_buf + 2, hub_buf, hub_buf + 1, hub_ctas);
+    GEE_CHECK_LAUNCH("k_degree");
     return GEE_OK;
 }
 
