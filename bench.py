@@ -52,6 +52,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--eager", action="store_true", help="launch kernels one by one instead of a CUDA graph")
     p.add_argument("--flush-mib", type=int, default=512)
+    p.add_argument("--flush-mode", choices=("write", "clean"), default="write",
+                   help="L2 flush between timed steps: write the buffer (default), or write it and then read "
+                        "a second one so the flush's dirty lines are written back before the step")
     p.add_argument("--cpu-budget-s", type=float, default=12.0)
     p.add_argument("--embed-flat-bytes", type=int, default=None,
                    help="debug: per-warp shared budget of the K > 8 embed's flat row blocks "
@@ -298,7 +301,22 @@ def run_b200(args):
     _, w = edges.weight_kind()  # None for unit-weight graphs: never re-read
     opts = G.EmbedOptions(bool(flags & 1), bool(flags & 2), bool(flags & 4))
     enc = G.GeeEncoder(n, e, k, directed, opts, dev)
-    flush = torch.empty(args.flush_mib << 20, dtype=torch.uint8, device=dev)
+    flush_buf = torch.empty(args.flush_mib << 20, dtype=torch.uint8, device=dev)
+    clean_buf = torch.zeros(args.flush_mib << 20 if args.flush_mode == "clean" else 0, dtype=torch.uint8,
+                            device=dev)
+
+    class _Flush:
+        # "write": the flush buffer is written (L2 left full of its dirty lines,
+        # whose write-back then lands inside the next step); "clean": written,
+        # then a second buffer of the same size is read, so the write-back
+        # happens here and the step starts from a cold, clean L2
+        @staticmethod
+        def zero_():
+            flush_buf.zero_()
+            if clean_buf.numel():
+                clean_buf.max()
+
+    flush = _Flush()
     # stream length and unique nnz for the byte model (outside the timed region)
     m_stream = e if directed else e + int((rows != cols).sum().item())
     nnz = edges.to_csr().nnz
@@ -427,7 +445,9 @@ def run_b200(args):
         "vs_baseline_basis": "PAPER.md:93 sparse GEE 0.6 s for SBM 10k/5.6M edges lap+diag+corr "
                              "(laptop i5) = 9.33e6 edges/s" if args.config in PUBLISHED else None,
         "dtype": "f64", "data": "synthetic (seeded, BASELINE.json shapes)",
-        "config": dict(workload_desc(c), l2=(f"flushed: {args.flush_mib} MiB write before every timed step"
+        "config": dict(workload_desc(c), l2=((f"flushed: {args.flush_mib} MiB write before every timed step"
+                                              + (f", then a {args.flush_mib} MiB read (write-backs drained: cold, "
+                                                 "clean L2)" if args.flush_mode == "clean" else ""))
                                              if args.flush_mib > 0 else "not flushed"),
                        stream_entries=m_stream, nnz=nnz,
                        unit_weights=bool(w is None),
