@@ -5,6 +5,8 @@
 #include <limits.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "gee.h"
 
 namespace gee {
@@ -17,6 +19,21 @@ int cuda_status(cudaError_t e);
 int num_sms();
 // bench profiling: when enabled, record an event after each launch
 void profile_mark(const char *name, cudaStream_t st);
+
+// "Done once per device" flag.  Function attributes (e.g. the dynamic
+// shared-memory limit) belong to each device's context, so a process-wide
+// bool would skip them for a second GPU; racing threads may both set the
+// attribute, which is harmless.
+struct PerDevice {
+    std::atomic<unsigned long long> bits{0};
+    static int dev() {
+        int d = 0;
+        if (cudaGetDevice(&d) != cudaSuccess) d = 0;
+        return d & 63;
+    }
+    bool done() const { return (bits.load(std::memory_order_acquire) >> dev()) & 1ull; }
+    void mark() { bits.fetch_or(1ull << dev(), std::memory_order_release); }
+};
 
 // Every launch site uses a stream variable named `st`.
 #define GEE_CHECK_LAUNCH(name)                                  \

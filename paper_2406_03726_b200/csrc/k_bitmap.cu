@@ -1264,11 +1264,11 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 
 template <int NB>
 static int launch_gemm(const BmArgs &a, const int64_t *rows, const int64_t *cols, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    if (!attr.done()) {
         GEE_CHECK_CUDA(cudaFuncSetAttribute(k_bm_gemm<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)gemm_smem<NB>()));
-        attr = true;
+        attr.mark();
     }
     // persistent stream-K grid, one CTA per SM; cooperative so the rare
     // path's grid barrier is safe (a launch error, never a hang)

@@ -1156,13 +1156,13 @@ int csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, i
     if (ws_bytes < need) return GEE_E_WORKSPACE;
     const int threads = 512;
     const bool small_rows = n_rows <= kSmallRows;
-    static bool part_attr = false;
-    if (!part_attr) {
+    static PerDevice part_attr;
+    if (!part_attr.done()) {
         GEE_CHECK_CUDA(cudaFuncSetAttribute(k_count_part, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             kSmallRows * 4));
         GEE_CHECK_CUDA(cudaFuncSetAttribute(k_scatter_part, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             kSmallRows * 4));
-        part_attr = true;
+        part_attr.mark();
     }
     GEE_CHECK_CUDA(cudaMemsetAsync(W.nlist, 0, 16 * sizeof(unsigned), st));
     GEE_CHECK_CUDA(cudaMemsetAsync(W.cnt, 0, sizeof(unsigned) * (size_t)(n_rows + 1), st));
@@ -1228,11 +1228,11 @@ int csr_build(const int64_t *rows, const int64_t *cols, const void *w, int wt, i
         a.err = err;
         a.dense_ok = dense_ok;
         size_t smem = rows_smem(dense_ok, n_cols);
-        static bool attr_set = false;
-        if (!attr_set) {
+        static PerDevice attr_set;
+        if (!attr_set.done()) {
             GEE_CHECK_CUDA(cudaFuncSetAttribute(k_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 16 * kCap + kSmallCols * 4 + 1024));
-            attr_set = true;
+            attr_set.mark();
         }
         k_rows<<<2 * num_sms(), kRowsThreads, smem, st>>>(a);
         GEE_CHECK_LAUNCH("k_rows");

@@ -938,8 +938,8 @@ int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, c
     const int nt = tab ? kTabThreads : kEmbedThreads;
     const size_t base_smem = sizeof(double) * (size_t)(nt / 32) * ((size_t)wst + 32);
     const size_t smem = base_smem + (tab ? 9 * (size_t)n_cols + 32 : 0);
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    if (!attr.done()) {
         size_t mx = sizeof(double) * (size_t)kEmbedWarps * ((size_t)kFlatBytesMax / 8 + 32);
         GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<0, false, kEmbedThreads>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
@@ -950,7 +950,7 @@ int embed(const int64_t *row_ptr, const unsigned *row_cnt, const int32_t *col, c
         GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<2, true, kTabThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
         GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<4, true, kTabThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
         GEE_CHECK_CUDA(cudaFuncSetAttribute(k_embed<8, true, kTabThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, tmx));
-        attr = true;
+        attr.mark();
     }
     int occ = 0;
     const unsigned grid_cap = (unsigned)num_sms() * 8;

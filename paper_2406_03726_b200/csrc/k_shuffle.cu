@@ -257,11 +257,11 @@ int shuffle_row_hist(const int64_t *rows, const int64_t *cols, int64_t E, int64_
                      int64_t nb, unsigned long long *hist, cudaStream_t st) {
     if (E <= 0) return GEE_OK;
     const size_t smem = sizeof(unsigned) * (size_t)nb;
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    if (!attr.done()) {
         GEE_CHECK_CUDA(cudaFuncSetAttribute(k_shuffle_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)(sizeof(unsigned) * kShufBuckets)));
-        attr = true;
+        attr.mark();
     }
     k_shuffle_hist<<<grid_for(E, 512, 2), 512, smem, st>>>(rows, cols, E, n, directed, nb, hist);
     GEE_CHECK_LAUNCH("k_shuffle_hist");

@@ -613,13 +613,13 @@ template <typename K, typename P>
 static int sort_passes(const SortGeom &g, const int64_t *rows, const int64_t *cols, const void *w, int wt,
                        int64_t n_rows, int force_vals, int64_t *row_ptr, int32_t *col, double *val, SortWs &W,
                        cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    if (!attr.done()) {
         GEE_CHECK_CUDA(cudaFuncSetAttribute(k_onesweep<K, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)onesweep_smem<K, P>()));
         GEE_CHECK_CUDA(cudaFuncSetAttribute(k_dedup<K, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)dedup_smem<K, P>()));
-        attr = true;
+        attr.mark();
     }
     const int64_t tiles = W.tiles;
     k_sort_hist<K><<<grid_for(g.Mv, kSortThreads, 4), kSortThreads, 0, st>>>(g, rows, cols, w, wt, W.hist, W.flags);

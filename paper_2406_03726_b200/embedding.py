@@ -190,14 +190,14 @@ def _encode_csr(a: CsrMatrix, labels: LabelVector, flags: int, dev) -> torch.Ten
             deg = torch.empty(n, dtype=torch.float64, device=dev)
             scale = torch.empty(n, dtype=torch.float64, device=dev)
             _lib.check(lib.gee_degree(
-                _device.ptr(a.index_pointers), _device.ptr(a.col_indices), _device.ptr(a.data), n,
+                _device.ptr(a.row_ptr_d), _device.ptr(a.col_d), _device.ptr(a.val_d), n,
                 flags & _lib.DIAGONAL, _device.ptr(deg), _device.ptr(scale), _device.ptr(err),
                 _device.stream_handle()))
         z = torch.empty((n, k), dtype=torch.float64, device=dev)
         nb = _lib.size_query(lib.gee_embed_workspace, n, n)
         ws = _device.WORKSPACE.get(nb, dev)
         _lib.check(lib.gee_embed(
-            _device.ptr(a.index_pointers), None, _device.ptr(a.col_indices), _device.ptr(a.data), 0,
+            _device.ptr(a.row_ptr_d), None, _device.ptr(a.col_d), _device.ptr(a.val_d), 0,
             n, n, _device.ptr(y32), _device.ptr(inv), _device.ptr(scale), k, flags, _device.ptr(z), k,
             _device.ptr(ws), ws.numel(), _device.ptr(err), _device.stream_handle()))
     _device.check_device_errors(err, "encode")

@@ -24,9 +24,34 @@ class CsrMatrix:
                  col_indices: torch.Tensor, data: torch.Tensor):
         self.n_rows = int(n_rows)
         self.n_cols = int(n_cols)
-        self.index_pointers = index_pointers
-        self.col_indices = col_indices
-        self.data = data
+        # device storage (row_ptr int64, col int32, val float64); the
+        # reference-named fields below are host views with the reference's
+        # dtypes (sparse.py:20-27: int64 / int64 / float64 numpy arrays)
+        self.row_ptr_d = index_pointers
+        self.col_d = col_indices
+        self.val_d = data
+        self._host = None
+
+    def _numpy(self):
+        if self._host is None:
+            self._host = (self.row_ptr_d.cpu().numpy().astype(np.int64, copy=False),
+                          self.col_d.cpu().numpy().astype(np.int64),
+                          self.val_d.cpu().numpy())
+            for a in self._host:
+                a.flags.writeable = False
+        return self._host
+
+    @property
+    def index_pointers(self) -> np.ndarray:
+        return self._numpy()[0]
+
+    @property
+    def col_indices(self) -> np.ndarray:
+        return self._numpy()[1]
+
+    @property
+    def data(self) -> np.ndarray:
+        return self._numpy()[2]
 
     # ---- construction ------------------------------------------------------
     @classmethod
@@ -76,32 +101,46 @@ class CsrMatrix:
         r = _device.to_device(rows, torch.int64, dev)
         c = _device.to_device(cols, torch.int64, dev)
         v = _device.to_device(vals, torch.float64, dev)
+        if check and r.shape[0] and not isinstance(rows, np.ndarray):
+            # device inputs get the same checks, on the device (one host sync)
+            bad = (r < 0) | (r >= n_rows) | (c < 0) | (c >= n_cols)
+            nonfin = ~torch.isfinite(v)
+            flags = torch.stack([bad.any(), nonfin.any()]).cpu()
+            if bool(flags[0]):
+                e = int(torch.nonzero(bad)[0])
+                raise StructuralError(
+                    f"triplet ({int(r[e])}, {int(c[e])}, {float(v[e])}) outside {n_rows}x{n_cols} matrix")
+            if bool(flags[1]):
+                e = int(torch.nonzero(nonfin)[0])
+                raise StructuralError(
+                    f"triplet ({int(r[e])}, {int(c[e])}, {float(v[e])}) has a non-finite value")
         return _build(r, c, (_lib.W_F64, v), int(r.shape[0]), n_rows, n_cols, True, dev)
 
     # ---- accessors -----------------------------------------------------------
     @property
     def nnz(self) -> int:
-        return int(self.data.shape[0])
+        return int(self.val_d.shape[0])
 
     @property
     def device(self) -> torch.device:
-        return self.data.device
+        return self.val_d.device
 
     def to_numpy(self):
         """(index_pointers int64, col_indices int64, data float64) on the host."""
-        return (self.index_pointers.cpu().numpy().astype(np.int64, copy=False),
-                self.col_indices.cpu().numpy().astype(np.int64),
-                self.data.cpu().numpy())
+        return self._numpy()
 
     def row_ids(self) -> np.ndarray:
-        ip = self.index_pointers.cpu().numpy()
+        ip = self.index_pointers
         return np.repeat(np.arange(self.n_rows, dtype=np.int64), np.diff(ip))
 
     def row(self, r: int):
         if not 0 <= r < self.n_rows:
             raise IndexError(f"row {r} out of range for {self.n_rows} rows")
-        lo, hi = (int(x) for x in self.index_pointers[r:r + 2].cpu())
+        lo, hi = (int(x) for x in self.index_pointers[r:r + 2])
         return self.col_indices[lo:hi], self.data[lo:hi]
+
+    def to_triplets(self):
+        return self.row_ids(), self.col_indices.copy(), self.data.copy()
 
     def to_dense(self) -> np.ndarray:
         ip, c, d = self.to_numpy()
@@ -177,7 +216,7 @@ def add_identity(a) -> CsrMatrix:
         nb = _lib.size_query(lib.gee_add_identity_workspace, n)
         ws = _device.WORKSPACE.get(nb, dev)
         _lib.check(lib.gee_add_identity(
-            _device.ptr(a.index_pointers), _device.ptr(a.col_indices), _device.ptr(a.data), n,
+            _device.ptr(a.row_ptr_d), _device.ptr(a.col_d), _device.ptr(a.val_d), n,
             _device.ptr(out_ptr), _device.ptr(out_col), _device.ptr(out_val), _device.ptr(nnz),
             _device.ptr(ws), ws.numel(), _device.stream_handle()))
     k = int(nnz.item())
@@ -199,7 +238,7 @@ def degree_vector(a, diagonal: bool = False, with_scale: bool = False):
     err = _device.error_word(dev)
     with torch.cuda.device(dev):
         _lib.check(lib.gee_degree(
-            _device.ptr(a.index_pointers), _device.ptr(a.col_indices), _device.ptr(a.data), n,
+            _device.ptr(a.row_ptr_d), _device.ptr(a.col_d), _device.ptr(a.val_d), n,
             _lib.DIAGONAL if diagonal else 0, _device.ptr(deg), _device.ptr(scale),
             _device.ptr(err), _device.stream_handle()))
     if with_scale:
@@ -229,7 +268,7 @@ def laplacian_normalize(a, degrees) -> CsrMatrix:
         nb = _lib.size_query(lib.gee_laplacian_normalize_workspace, n)
         ws = _device.WORKSPACE.get(nb, dev)
         _lib.check(lib.gee_laplacian_normalize(
-            _device.ptr(a.index_pointers), _device.ptr(a.col_indices), _device.ptr(a.data), n,
+            _device.ptr(a.row_ptr_d), _device.ptr(a.col_d), _device.ptr(a.val_d), n,
             _device.ptr(deg), _device.ptr(out_ptr), _device.ptr(out_col), _device.ptr(out_val),
             _device.ptr(nnz), _device.ptr(ws), ws.numel(), _device.ptr(err),
             _device.stream_handle()))

@@ -371,7 +371,7 @@ def test_full_cfg1_properties():
     csr = edges.to_csr()
     assert csr.nnz == 2 * c["e"]  # SBM: no duplicates or loops, so nnz = 2E
     deg = G.degree_vector(csr, diagonal=True).cpu().numpy()
-    assert same(deg, np.diff(csr.index_pointers.cpu().numpy()).astype(np.float64) + 1.0)
+    assert same(deg, np.diff(csr.index_pointers).astype(np.float64) + 1.0)
     z = G.encode(edges, lab, G.EmbedOptions(True, True, True))
     norms = np.linalg.norm(z, axis=1)
     assert np.abs(norms - 1.0).max() <= 1e-12
