@@ -46,16 +46,29 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--config", type=int, default=1)
+    p.add_argument("--config", type=int, default=3,
+                   help="BASELINE.json configs[C]; default 3, the metric's multi-GPU R-MAT workload "
+                        "(the largest that fits one GPU)")
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--fp32", action="store_true", help="the optional fp32 path: Z stored as float32 (1e-5)")
+    p.add_argument("--stream-variant", type=int, default=0,
+                   help="debug A/B of the stream embed (results wrong by design): 1 no shared atomics, 2 no gathers")
+    p.add_argument("--stream-tile-kb", type=int, default=0, help="debug: KB of the stream encode's Z tile")
+    p.add_argument("--stream-nt", type=int, default=0, help="debug: threads per stream embed CTA (128/256/512)")
+    p.add_argument("--no-stream", action="store_true",
+                   help="debug: disable the bucketed stream encode (gee_debug_set GEE_DEBUG_STREAM=1): exact CSR path")
     p.add_argument("--eager", action="store_true", help="launch kernels one by one instead of a CUDA graph")
     p.add_argument("--flush-mib", type=int, default=512)
     p.add_argument("--flush-mode", choices=("write", "clean"), default="write",
                    help="L2 flush between timed steps: write the buffer (default), or write it and then read "
                         "a second one so the flush's dirty lines are written back before the step")
     p.add_argument("--cpu-budget-s", type=float, default=12.0)
+    p.add_argument("--cpu-sample-edges", type=int, default=1 << 25,
+                   help="cpu_baseline: time the oracle on the first S edges of the workload when it has more")
+    p.add_argument("--ref-budget-s", type=float, default=300.0,
+                   help="--impl reference: stop after this many seconds of timed runs (at least one run)")
     p.add_argument("--embed-flat-bytes", type=int, default=None,
                    help="debug: per-warp shared budget of the K > 8 embed's flat row blocks "
                         "(gee_debug_set GEE_DEBUG_EMBED_FLAT_BYTES; 0 = one warp per row)")
@@ -88,19 +101,23 @@ def workload_desc(c):
         "workload": f"configs[{c['idx']}] {c['name']}",
         "n_nodes": int(c["n"]), "n_edges": int(c["e"]), "k_classes": int(c["k"]),
         "directed": bool(c["directed"]), "options": opts or ["none"],
-        "weights": str(getattr(c["weights"], "dtype", "f64")),
+        "weights": "unit (1.0)" if c.get("wdtype") == "unit" else str(c.get("wdtype")),
         "seed": c["seed"],
-        "step": "device edge list + labels -> Z (to_csr + encode, cli.py:170-180)",
+        "step": "edge list + labels -> Z (EdgeList.to_csr + encode, cli.py:170-180)",
     }
 
 
 def load_config(idx, device):
-    from paper_2406_03726_b200 import synth
+    """Config `idx`: drawn on the GPU by libgee's counter-based generators, or
+    (device "cpu") on the host by their C restatement (oracle/gee_gen.c) --
+    the same arrays bit for bit (tests/test_gpu_gen.py), so both arms time the
+    same graph."""
     import torch
-    dev = device if idx in (3, 4) else "cpu"
-    c = synth.make_config(idx, device=dev)
-    c["idx"] = idx
-    return c
+    if str(device) == "cpu":
+        from oracle import gen
+        return gen.host_config(idx)
+    from paper_2406_03726_b200 import synth
+    return synth.make_config(idx, device=torch.device(device))
 
 
 def host_arrays(c):
@@ -115,9 +132,14 @@ def host_arrays(c):
 # ---------------------------------------------------------------------------
 # CPU reference arm (oracle port of the reference pipeline)
 # ---------------------------------------------------------------------------
-def cpu_reference_time(c, budget_s, min_reps=1, max_reps=5):
+def cpu_reference_time(arrays, c, budget_s, min_reps=1, max_reps=5, sample=None):
+    """Seconds per run of the C restatement of the reference pipeline
+    (encode(EdgeList(...).to_csr(), ...), cli.py:170-180) on these host
+    arrays; `sample` = time only the first S edges (same N, K, options)."""
     from oracle import oracle as O
-    rows, cols, w, labels = host_arrays(c)
+    rows, cols, w, labels = arrays
+    if sample is not None and sample < rows.shape[0]:
+        rows, cols, w = rows[:sample], cols[:sample], w[:sample]
     w = np.asarray(w, dtype=np.float64)  # EdgeList promotes float32 (graph_io.py:61)
     times = []
     t_start = time.perf_counter()
@@ -129,32 +151,39 @@ def cpu_reference_time(c, budget_s, min_reps=1, max_reps=5):
             raise RuntimeError(f"oracle status {st}")
         if len(times) >= min_reps and time.perf_counter() - t_start > budget_s:
             break
-    return times
+    return times, int(rows.shape[0])
 
 
 def run_reference(args):
+    """The reference arm: the CPU reference pipeline (its C restatement,
+    oracle/gee_oracle.c, pinned bitwise to the reference) on the FULL
+    workload of --config, drawn on the host by oracle/gee_gen.c.  The C code
+    has no JIT, so warm-up runs are not needed and none are made; timed runs
+    stop at --steps or once --ref-budget-s has elapsed (at least one), and
+    `steps` reports the runs actually made."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     c = load_config(args.config, "cpu")
-    for _ in range(args.warmup):
-        cpu_reference_time(c, 0.0, 1, 1)
-    times = []
-    for _ in range(args.steps):
-        times.extend(cpu_reference_time(c, 0.0, 1, 1))
+    arrays = host_arrays(c)
+    times, e = cpu_reference_time(arrays, c, args.ref_budget_s, 1, max(1, args.steps))
     t = statistics.mean(times)
-    value = c["e"] / t
+    value = e / t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "n_gpus": args.gpus, "steps": len(times), "steps_requested": args.steps, "warmup": 0,
+        "warmup_requested": args.warmup,
+        "ms_per_step": t * 1e3, "ms_per_step_min": min(times) * 1e3, "higher_is_better": True,
+        "scaling": "strong",
         "vs_baseline": (value / PUBLISHED[args.config]) if args.config in PUBLISHED else None,
-        "dtype": "f64", "data": "synthetic (seeded, BASELINE.json shapes)",
+        "dtype": "f64" + ("; Z stored f32 (--fp32)" if args.fp32 else ""),
+        "data": "synthetic (seeded counter-based generator, BASELINE.json shapes)",
         "config": workload_desc(c),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"full workload, {len(times)} timed runs of the C restatement "
-                                   "of the reference pipeline (oracle/gee_oracle.c; the reference "
-                                   "is single-threaded, numba @njit without parallel)"},
+                         "sample": f"full configs[{args.config}] workload ({e} edges), {len(times)} timed "
+                                   "runs of the C restatement of the reference pipeline "
+                                   "(oracle/gee_oracle.c; the reference is single-threaded, numba @njit "
+                                   "without parallel, so 1 core)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -219,7 +248,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # algorithmic bytes per launch
 # ---------------------------------------------------------------------------
-def kernel_bytes(c, m_stream, nnz, wbytes):
+def kernel_bytes(c, m_stream, nnz, wbytes, zbytes=8):
     """Compulsory bytes each kernel must move once.
     wbytes = bytes per weight actually read (0 for unit-weight graphs, whose
     values are implicit 1.0 and never stored or read)."""
@@ -258,8 +287,29 @@ def kernel_bytes(c, m_stream, nnz, wbytes):
         # per node, the row scale, and Z
         "k_embed": (4 + vb) * nnz + 8 * (n + 1) + 4 * n + 16 * n + (8 * n if lap else 0) + 8 * n * k,
         "k_label_hist": 8 * n + 4 * n,
+        # bucketed stream encode (k_stream.cu): M = stream entries, wbytes the
+        # weight width (0 unit); keys1 8 B, keys2 4 B per entry
+        "k_st_hist1": (8 if directed else 16) * e,
+        "k_st_part1": (16 + wbytes) * e + (8 + wbytes) * m_stream,
+        "k_st_hist2": 8 * m_stream,
+        "k_st_part2": (8 + wbytes) * m_stream + (4 + wbytes) * m_stream,
+        "k_st_degree": ((4 + wbytes) * m_stream + 8 * n if lap else 0) + 4 * n + 8 * n + 16 * n,
+        # the fused SpMM + normalisation kernel: entries once, one node record
+        # per node, the row scales, Z written once
+        "k_st_embed": (4 + wbytes) * m_stream + 16 * n + (8 * n if lap else 0) + zbytes * n * k,
         "k_node_rec": 4 * n + 16 * n + (8 * n if lap else 0),
     }
+
+
+def _traffic(cfg, kernel):
+    """ncu dram__bytes_read.sum + dram__bytes_write.sum per launch for this
+    kernel at this config (profiles/traffic.json, from an ncu --set full
+    capture), or None."""
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(tpath)).get(f"cfg{cfg}", {}).get(kernel)
+    except Exception:
+        return None
 
 
 def run_b200(args):
@@ -285,6 +335,14 @@ def run_b200(args):
     lib = _lib.load()
     if args.force_path:
         lib.gee_debug_set(_lib.DEBUG_FORCE_BUCKETS, args.force_path)
+    if args.no_stream:
+        lib.gee_debug_set(_lib.DEBUG_STREAM, 1)
+    if args.stream_tile_kb:
+        lib.gee_debug_set(5, args.stream_tile_kb)
+    if args.stream_nt:
+        lib.gee_debug_set(6, args.stream_nt)
+    if args.stream_variant:
+        lib.gee_debug_set(_lib.DEBUG_STREAM, 16 + args.stream_variant)
     if args.embed_flat_bytes is not None:
         lib.gee_debug_set(_lib.DEBUG_EMBED_FLAT_BYTES, args.embed_flat_bytes)
     if args.embed_flat_rowmax is not None:
@@ -300,7 +358,8 @@ def run_b200(args):
     edges = G.EdgeList(n, rows, cols, w_in, directed)
     _, w = edges.weight_kind()  # None for unit-weight graphs: never re-read
     opts = G.EmbedOptions(bool(flags & 1), bool(flags & 2), bool(flags & 4))
-    enc = G.GeeEncoder(n, e, k, directed, opts, dev)
+    enc = G.GeeEncoder(n, e, k, directed, opts, dev, nonneg=bool(edges.nonneg),
+                       dtype=torch.float32 if args.fp32 else torch.float64)
     flush_buf = torch.empty(args.flush_mib << 20, dtype=torch.uint8, device=dev)
     clean_buf = torch.zeros(args.flush_mib << 20 if args.flush_mode == "clean" else 0, dtype=torch.uint8,
                             device=dev)
@@ -386,7 +445,7 @@ def run_b200(args):
 
     # roofline of the dominant kernel (largest share of the step)
     hbm, peak_src = peaks()
-    models = kernel_bytes(c, m_stream, nnz, wbytes)
+    models = kernel_bytes(c, m_stream, nnz, wbytes, 4 if args.fp32 else 8)
     ktab = []
     for name, ts in per_kernel.items():
         launches_per_step = len(ts) / args.steps
@@ -397,18 +456,12 @@ def run_b200(args):
                      "alg_bytes": b, "gbs": (b / (t_launch * 1e-3) / 1e9) if b else None})
     ktab.sort(key=lambda r: -r["share"])
     dom = next(r for r in ktab if r["alg_bytes"])
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(f"cfg{args.config}", {}).get(dom["kernel"])
-        except Exception:
-            traffic = None
+    traffic = _traffic(args.config, dom["kernel"])
     roofline = {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["gbs"], "peak": hbm,
                 "peak_source": peak_src, "unit": "GB/s", "frac": dom["gbs"] / hbm,
                 "traffic": traffic, "alg_bytes_per_launch": dom["alg_bytes"]}
-    emb = next((r for r in ktab if r["kernel"] == "k_embed"), None)
-    prod = next((r for r in ktab if r["kernel"] in ("k_bm_gemm", "k_embed")), None)
+    emb = next((r for r in ktab if r["kernel"] in ("k_st_embed", "k_embed")), None)
+    prod = next((r for r in ktab if r["kernel"] in ("k_bm_gemm", "k_st_embed", "k_embed")), None)
 
     # end to end: pinned host in -> Z on host, through the public plan API
     e2e = None
@@ -430,12 +483,14 @@ def run_b200(args):
 
     cpu = None
     if not args.no_cpu_baseline:
-        times = cpu_reference_time(c, args.cpu_budget_s, 1, 5)
-        cpu = {"value": e / statistics.mean(times), "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"full configs[{args.config}] workload, {len(times)} runs of the C "
-                         "restatement (oracle/gee_oracle.c) of encode(EdgeList.to_csr(), ...) on "
-                         f"this host ({os.cpu_count()} cores visible, 1 used: the reference is "
-                         "single-threaded)",
+        arrays = host_arrays(c)
+        times, es = cpu_reference_time(arrays, c, args.cpu_budget_s, 1, 5, sample=args.cpu_sample_edges)
+        what = (f"full configs[{args.config}] workload" if es == e else
+                f"the first {es} of the {e} edges of configs[{args.config}] (same N, K, options)")
+        cpu = {"value": es / statistics.mean(times), "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{what}, {len(times)} runs of the C restatement (oracle/gee_oracle.c) of "
+                         f"encode(EdgeList.to_csr(), ...) on this host ({os.cpu_count()} cores visible, 1 "
+                         "used: the reference is single-threaded)",
                "seconds_per_run": statistics.mean(times)}
 
     line = {
@@ -444,8 +499,10 @@ def run_b200(args):
         "vs_baseline": (value / PUBLISHED[args.config]) if args.config in PUBLISHED else None,
         "vs_baseline_basis": "PAPER.md:93 sparse GEE 0.6 s for SBM 10k/5.6M edges lap+diag+corr "
                              "(laptop i5) = 9.33e6 edges/s" if args.config in PUBLISHED else None,
-        "dtype": "f64", "data": "synthetic (seeded, BASELINE.json shapes)",
-        "config": dict(workload_desc(c), l2=((f"flushed: {args.flush_mib} MiB write before every timed step"
+        "dtype": "f64" + ("; Z stored f32 (--fp32)" if args.fp32 else ""),
+        "data": "synthetic (seeded counter-based generator, BASELINE.json shapes)",
+        "config": workload_desc(c),
+        "workload_detail": dict(l2=((f"flushed: {args.flush_mib} MiB write before every timed step"
                                               + (f", then a {args.flush_mib} MiB read (write-backs drained: cold, "
                                                  "clean L2)" if args.flush_mode == "clean" else ""))
                                              if args.flush_mib > 0 else "not flushed"),
@@ -454,8 +511,9 @@ def run_b200(args):
                        weights_read_per_step="none: EdgeList found every weight == 1.0 at "
                        "construction, values are implicit" if w is None else "yes"),
         "roofline": roofline,
-        "embed_kernel": ({"ms_per_launch": emb["ms_per_launch"], "gbs": emb["gbs"],
-                          "frac": emb["gbs"] / hbm} if emb else None),
+        "embed_kernel": ({"kernel": emb["kernel"], "ms_per_launch": emb["ms_per_launch"], "gbs": emb["gbs"],
+                          "frac": emb["gbs"] / hbm, "alg_bytes_per_launch": emb["alg_bytes"],
+                          "traffic": _traffic(args.config, emb["kernel"])} if emb else None),
         # SURVEY 8(d) scope T1: the product kernel alone (inputs resident); the
         # line's value is T2 (device pipeline) and e2e is T3 (host to host)
         "t1": ({"kernel": prod["kernel"], "ms": prod["ms_per_launch"],

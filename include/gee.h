@@ -60,11 +60,20 @@ extern "C" {
 #define GEE_ERR_LABEL 4
 #define GEE_ERR_EDGE_RANGE 8
 #define GEE_ERR_EDGE_WEIGHT 16
+#define GEE_ERR_NEG_WEIGHT 32 /* GEE_NONNEG was passed but a weight is < 0 */
 
 /* EmbedOptions (embedding.py:74-89) as a bit set */
 #define GEE_LAPLACIAN 1u
 #define GEE_DIAGONAL 2u
 #define GEE_CORRELATION 4u
+/* Caller's assertion that every edge weight is >= 0 (the EdgeList checks it
+ * at construction).  Lets gee_encode_edges take the bucketed stream path,
+ * which sums in any order; a violated assertion sets GEE_ERR_NEG_WEIGHT and
+ * the result must be recomputed without the flag. */
+#define GEE_NONNEG 8u
+/* Output Z as float32 instead of float64 (accumulation stays in f64; the
+ * north_star's optional fp32 path, 1e-5 relative). */
+#define GEE_FP32 16u
 
 /* edge-weight element types */
 #define GEE_W_UNIT 0 /* w == NULL: every weight is 1.0 */
@@ -150,13 +159,17 @@ int gee_embed(const int64_t *row_ptr, const uint32_t *row_cnt, const int32_t *co
               void *stream);
 
 /* The whole reference timed region on the device: edge list + labels ->
- * Z (N x K, f64).  Optionally also returns the uncompacted CSR through
- * the workspace (not exposed).  One stream, no host synchronisation. */
+ * Z (N x K, f64; f32 with GEE_FP32).  One stream, no host synchronisation.
+ * Paths: the L2-resident bitmap + tcgen05 product (unit weights, N <= 16384,
+ * K <= 8); the bucketed stream encode (unit weights, or GEE_NONNEG: no CSR
+ * is built, sums in any order, 1e-12); otherwise the exact CSR assembly
+ * (radix sort or row buckets) + fused embed.  The workspace query covers
+ * every path the arguments allow. */
 int gee_encode_edges_workspace(int64_t n_edges, int64_t n_nodes, int32_t k, int directed,
                                int w_type, size_t *ws_bytes);
 int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, int w_type,
                      int64_t n_edges, int64_t n_nodes, int directed, const int64_t *labels,
-                     int32_t k, unsigned flags, double *z, void *ws, size_t ws_bytes,
+                     int32_t k, unsigned flags, void *z, void *ws, size_t ws_bytes,
                      int32_t *err, void *stream);
 
 /* Row shard of a unit-weight graph (multi-GPU, dist.py; replaces the
@@ -211,6 +224,35 @@ int gee_partition(const int64_t *rows, const int64_t *cols, const void *w, int w
                   int directed, const int64_t *bounds, int world, int64_t *out_rows, int64_t *out_cols,
                   void *out_w, uint64_t *counts, void *ws, size_t ws_bytes, void *stream);
 
+/* On-device synthetic generators (the reference's generator
+ * is sbm.py:52-155, a sequential PCG64 stream).  Counter-based: word t of
+ * stream `key` is splitmix64's output mix64(key + (t+1)*0x9e3779b97f4a7c15),
+ * key = mix64(seed ^ stream_id * 0x9e3779b97f4a7c15), so the C restatement
+ * oracle/gee_gen.c yields identical arrays.  Thresholds are integers
+ * (probability * 2^32, computed by the caller).
+ *   gee_gen_rmat     edge i: word i*16+h gives levels 2h (low 32 bits) and
+ *                    2h+1 (high 32); u < t1 -> (0,0), < t2 -> (0,1),
+ *                    < t3 -> (1,0), else (1,1); w (may be NULL) f32
+ *                    1 - (word_i(wkey) >> 40) * 2^-24.
+ *   gee_gen_chunglu  rows/cols = searchsorted(cdf, (word_i >> 11) * 2^-53,
+ *                    'right') clipped to n-1; w (may be NULL) f64
+ *                    1 - (word_i(wkey) >> 11) * 2^-53.
+ *   gee_gen_pairs    keys[i] for candidate t0+i: a = hi32(lo32 * n),
+ *                    b = hi32(hi32 * n); min*n + max, or -1 when a == b.
+ *   gee_gen_sbm_*    pair (i, j), i < j: edge iff (word_{i*n+j} >> 32) <
+ *                    (labels_i == labels_j ? thr_in : thr_out); counts[i]
+ *                    per row, then the fill at the caller's exclusive
+ *                    offsets, row-major. */
+int gee_gen_rmat(uint64_t key, uint64_t wkey, int scale, int64_t n_edges, uint32_t t1, uint32_t t2, uint32_t t3,
+                 int64_t *rows, int64_t *cols, float *w, void *stream);
+int gee_gen_chunglu(uint64_t rkey, uint64_t ckey, uint64_t wkey, const double *cdf, int64_t n_nodes,
+                    int64_t n_edges, int64_t *rows, int64_t *cols, double *w, void *stream);
+int gee_gen_pairs(uint64_t key, int64_t t0, int64_t count, int64_t n_nodes, int64_t *keys, void *stream);
+int gee_gen_sbm_count(uint64_t key, int64_t n_nodes, const int64_t *labels, uint32_t thr_in, uint32_t thr_out,
+                      int64_t *counts, void *stream);
+int gee_gen_sbm_fill(uint64_t key, int64_t n_nodes, const int64_t *labels, uint32_t thr_in, uint32_t thr_out,
+                     const int64_t *offsets, int64_t *rows, int64_t *cols, void *stream);
+
 /* Launch statistics: number of kernels this thread launched through the
  * library since the last reset (for bench.py's gpu_launches). */
 uint64_t gee_launch_count(void);
@@ -238,6 +280,12 @@ int gee_profile_read(float *ms, const char **names, int cap);
 /* Third hook: the longest row a flat block takes (default 256); longer rows
  * get a warp each, rows over 4096 entries a CTA each. */
 #define GEE_DEBUG_EMBED_FLAT_ROWMAX 3
+/* Fourth hook: the bucketed stream encode: 0 auto, 1 never (tests force the
+ * CSR paths with it). */
+#define GEE_DEBUG_STREAM 4
+/* Fifth hook: KB of the stream encode's shared Z tile (R x K x 8 bytes;
+ * default 104; tests use it to force more, smaller buckets). */
+#define GEE_DEBUG_STREAM_TILE 5
 int gee_debug_set(int key, int value);
 
 #ifdef __cplusplus

@@ -17,7 +17,9 @@ LIB_PATH = os.path.join(_HERE, "libgee.so")
 # synchronous status codes / device error bits / option flags (gee.h)
 GEE_OK, GEE_E_ARG, GEE_E_WORKSPACE, GEE_E_CUDA = 0, 1, 2, 3
 ERR_NEG_DEGREE, ERR_NONFINITE, ERR_LABEL, ERR_EDGE_RANGE, ERR_EDGE_WEIGHT = 1, 2, 4, 8, 16
+ERR_NEG_WEIGHT = 32
 LAPLACIAN, DIAGONAL, CORRELATION = 1, 2, 4
+NONNEG, FP32 = 8, 16  # caller asserts weights >= 0 (stream path) / float32 Z
 W_UNIT, W_F64, W_F32 = 0, 1, 2
 
 _vp = ctypes.c_void_p
@@ -61,6 +63,12 @@ SIGNATURES = {
     "gee_partition_workspace": (_int, [_i64, _int, _szp]),
     "gee_partition": (_int, [_vp, _vp, _vp, _int, _i64, _int, _vp, _int, _vp, _vp, _vp, _vp, _vp,
                              ctypes.c_size_t, _vp]),
+    "gee_gen_rmat": (_int, [ctypes.c_uint64, ctypes.c_uint64, _int, _i64, _u32, _u32, _u32, _vp, _vp, _vp, _vp]),
+    "gee_gen_chunglu": (_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _vp, _i64, _i64, _vp, _vp, _vp,
+                               _vp]),
+    "gee_gen_pairs": (_int, [ctypes.c_uint64, _i64, _i64, _i64, _vp, _vp]),
+    "gee_gen_sbm_count": (_int, [ctypes.c_uint64, _i64, _vp, _u32, _u32, _vp, _vp]),
+    "gee_gen_sbm_fill": (_int, [ctypes.c_uint64, _i64, _vp, _u32, _u32, _vp, _vp, _vp, _vp]),
     "gee_launch_count": (ctypes.c_uint64, []),
     "gee_reset_launch_count": (None, []),
     "gee_profile_start": (_int, [_vp]),
@@ -71,6 +79,8 @@ SIGNATURES = {
 DEBUG_FORCE_BUCKETS = 1  # key; values: 0 default, 1 row buckets, 2 no bitmap path, 3 = 2 + 64-bit sort keys
 DEBUG_EMBED_FLAT_BYTES = 2  # key; per-warp shared bytes of the K > 8 flat embed blocks (0 = warp per row)
 DEBUG_EMBED_FLAT_ROWMAX = 3  # key; longest row a flat embed block takes (longer: a warp each)
+DEBUG_STREAM_TILE = 5  # key; KB of the stream encode's Z tile (default 104)
+DEBUG_STREAM = 4  # key; bucketed stream encode: 0 auto, 1 never (forces the CSR paths)
 
 _lib = None
 
@@ -120,6 +130,8 @@ def raise_device_errors(bits: int, context: str = ""):
         raise NumericalDomainError(f"negative degree under Laplacian normalization{where}")
     if bits & ERR_NONFINITE:
         raise NumericalDomainError(f"non-finite embedding values{where}")
+    if bits & ERR_NEG_WEIGHT:
+        raise StructuralError(f"negative edge weight under the non-negative assertion{where}")
     raise RuntimeError(f"libgee device error bits {bits:#x}{where}")
 
 

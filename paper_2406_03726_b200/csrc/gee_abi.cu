@@ -115,6 +115,14 @@ int bitmap_shard_encode(const int64_t *rows, const int64_t *cols, int64_t E, int
                         int k, unsigned flags, const unsigned *deg_all, double *z_local, void *ws, size_t ws_bytes,
                         int32_t *err, cudaStream_t st);
 int bitmap_max_nodes();
+bool stream_path_ok(int wt, unsigned flags, int64_t E, int64_t N, int directed, int k);
+size_t stream_workspace(int64_t E, int64_t N, int directed, int k, int wt);
+int stream_encode(const int64_t *rows, const int64_t *cols, const void *w, int wt, int64_t E, int64_t N, int directed,
+                  const int64_t *labels, int32_t k, unsigned flags, void *z, void *ws, size_t ws_bytes,
+                  int32_t *err, cudaStream_t st);
+int set_stream_mode(int v);
+int set_stream_tile_kb(int v);
+int set_stream_embed_nt(int v);
 
 static bool index_ok(int64_t x) { return x >= 0 && x < ((int64_t)1 << 31); }
 static bool wt_ok(int wt, const void *w, int64_t n_edges) {
@@ -194,6 +202,9 @@ int gee_profile_start(void *stream) {
 
 int gee_debug_set(int key, int value) {
     if (key == GEE_DEBUG_FORCE_BUCKETS) return set_force_buckets(value);
+    if (key == GEE_DEBUG_STREAM) return set_stream_mode(value);
+    if (key == GEE_DEBUG_STREAM_TILE) return set_stream_tile_kb(value);
+    if (key == 6) return set_stream_embed_nt(value);
     if (key == GEE_DEBUG_EMBED_FLAT_BYTES) return set_embed_flat_bytes(value);
     if (key == GEE_DEBUG_EMBED_FLAT_ROWMAX) return set_embed_flat_rowmax(value);
     return -1;
@@ -351,19 +362,30 @@ int gee_encode_edges_workspace(int64_t n_edges, int64_t n_nodes, int32_t k, int 
     Carver cv(nullptr);
     EncodeWs w;
     *ws_bytes = carve_encode(cv, w, n_edges, n_nodes, k, directed, w_type);
+    const size_t sb = stream_workspace(n_edges, n_nodes, directed, k, w_type);
+    if (sb > *ws_bytes) *ws_bytes = sb;
     return GEE_OK;
 }
 
 int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, int w_type, int64_t n_edges,
-                     int64_t n_nodes, int directed, const int64_t *labels, int32_t k, unsigned flags, double *z,
+                     int64_t n_nodes, int directed, const int64_t *labels, int32_t k, unsigned flags, void *zv,
                      void *ws, size_t ws_bytes, int32_t *err, void *stream) {
-    if (!index_ok(n_edges) || !index_ok(n_nodes) || k < 1 || !wt_ok(w_type, w, n_edges) || !z) return GEE_E_ARG;
+    if (!index_ok(n_edges) || !index_ok(n_nodes) || k < 1 || !wt_ok(w_type, w, n_edges) || !zv) return GEE_E_ARG;
     cudaStream_t st = (cudaStream_t)stream;
+    const bool bitmap = !(flags & GEE_FP32) && bitmap_path_ok(w_type, n_edges, n_nodes, n_nodes, directed, k);
+    if (!bitmap && stream_path_ok(w_type, flags, n_edges, n_nodes, directed, k)) {
+        // non-negative weights: the bucketed stream encode (no CSR)
+        if (!ws) return GEE_E_WORKSPACE;
+        return stream_encode(rows, cols, w, w_type, n_edges, n_nodes, directed, labels, k, flags, zv, ws, ws_bytes,
+                             err, st);
+    }
+    if (flags & GEE_FP32) return GEE_E_ARG;  // float32 output is produced by the stream path only
+    double *z = static_cast<double *>(zv);
     Carver cv(ws);
     EncodeWs W;
     size_t need = carve_encode(cv, W, n_edges, n_nodes, k, directed, w_type);
     if (ws_bytes < need || !ws) return GEE_E_WORKSPACE;
-    if (bitmap_path_ok(w_type, n_edges, n_nodes, n_nodes, directed, k)) {
+    if (bitmap) {
         // unit weights, small node count, K <= 8: labels, an L2-resident N x N
         // adjacency bitmap and Z in three launches (no CSR, no embed pass)
         return bitmap_encode(rows, cols, n_edges, n_nodes, directed, labels, k, flags, W.y32, W.counts, W.inv,

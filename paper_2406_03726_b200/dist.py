@@ -419,7 +419,7 @@ def bench_sharded(args, rank, world, dev):
 
     sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__file__)))
     from . import synth
-    cfg = synth.make_config(args.config, device=dev if args.config in (3, 4) else "cpu")
+    cfg = synth.make_config(args.config, device=dev)
     n, k, directed, flags = cfg["n"], cfg["k"], cfg["directed"], cfg["flags"]
     rows = torch.as_tensor(cfg["rows"], device=dev)
     cols = torch.as_tensor(cfg["cols"], device=dev)

@@ -38,8 +38,18 @@ def _labels_of(labels):
 def _edges_of(edges):
     if isinstance(edges, EdgeList):
         return edges
-    return EdgeList(edges.n_nodes, edges.rows, edges.cols, edges.weights, edges.directed,
-                    validate=False)
+    # a duck-typed (e.g. the reference's) EdgeList: the reference validated it
+    # at construction (graph_io.py:58-72); weights are only checked for sign
+    out = EdgeList(edges.n_nodes, edges.rows, edges.cols, edges.weights, edges.directed, validate=False)
+    w = out.weights
+    if w is not None and out.n_edges:
+        if isinstance(w, np.ndarray):
+            out.unit_weights = bool((w == 1.0).all())
+            out.nonneg = bool((w >= 0).all())
+        else:
+            f = torch.stack([(w == 1.0).all(), (w >= 0).all()]).cpu()
+            out.unit_weights, out.nonneg = bool(f[0]), bool(f[1])
+    return out
 
 
 def label_tables(labels, device=None):
@@ -65,23 +75,39 @@ class GeeEncoder:
 
     Holds the workspace, the error word and the output; ``run`` launches the
     fused pipeline on the current stream without synchronising (check=False)
-    so a caller can time or graph-capture it.
+    so a caller can time or graph-capture it.  ``nonneg=True`` asserts every
+    weight is >= 0 (EdgeList.nonneg), which enables the bucketed stream path;
+    ``dtype=torch.float32`` produces Z in float32 (north_star's optional fp32
+    path: f64 accumulation, f32 storage, 1e-5).
     """
 
     def __init__(self, n_nodes: int, n_edges: int, k_classes: int, directed: bool,
-                 opts: EmbedOptions | None = None, device=None):
+                 opts: EmbedOptions | None = None, device=None, *, nonneg: bool = False,
+                 dtype: torch.dtype = torch.float64):
         self.dev = torch.device(device) if device is not None else _device.require_gpu()
         self.n, self.e, self.k = int(n_nodes), int(n_edges), int(k_classes)
         self.directed = bool(directed)
         self.flags = options_flags(opts)
+        self.nonneg = bool(nonneg)
+        if dtype not in (torch.float64, torch.float32):
+            raise ValueError("dtype must be torch.float64 or torch.float32")
+        self.dtype = dtype
         lib = _lib.load()
         with torch.cuda.device(self.dev):
             # the assembly path (and its workspace) depends on the weight kind
             nb = max(_lib.size_query(lib.gee_encode_edges_workspace, self.e, self.n, self.k,
                                      int(self.directed), wt) for wt in (_lib.W_UNIT, _lib.W_F64))
         self.ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=self.dev)
-        self.z = torch.empty((self.n, self.k), dtype=torch.float64, device=self.dev)
+        self.z = torch.empty((self.n, self.k), dtype=dtype, device=self.dev)
         self.err = _device.error_word(self.dev)
+
+    def run_flags(self, weights) -> int:
+        f = self.flags
+        if self.nonneg or weights is None:
+            f |= _lib.NONNEG
+        if self.dtype == torch.float32:
+            f |= _lib.FP32
+        return f
 
     def run(self, rows, cols, weights, labels, *, check: bool = True, out=None) -> torch.Tensor:
         """rows/cols int64, weights float64/float32/None, labels int64 -- device tensors."""
@@ -92,12 +118,29 @@ class GeeEncoder:
         z = self.z if out is None else out
         if check:
             self.err.zero_()
-        _lib.check(_lib.load().gee_encode_edges(
+        flags = self.run_flags(weights)
+        st = _lib.load().gee_encode_edges(
             _device.ptr(rows), _device.ptr(cols), _device.ptr(weights), wt, self.e, self.n,
-            int(self.directed), _device.ptr(labels), self.k, self.flags, _device.ptr(z),
-            _device.ptr(self.ws), self.ws.numel(), _device.ptr(self.err), _device.stream_handle()))
+            int(self.directed), _device.ptr(labels), self.k, flags, _device.ptr(z),
+            _device.ptr(self.ws), self.ws.numel(), _device.ptr(self.err), _device.stream_handle())
+        if st == _lib.GEE_E_ARG and self.dtype == torch.float32 and not (flags & _lib.NONNEG):
+            # float32 Z comes from the stream path; signed weights take the exact
+            # f64 CSR path and are narrowed once
+            z64 = torch.empty((self.n, self.k), dtype=torch.float64, device=self.dev)
+            _lib.check(_lib.load().gee_encode_edges(
+                _device.ptr(rows), _device.ptr(cols), _device.ptr(weights), wt, self.e, self.n,
+                int(self.directed), _device.ptr(labels), self.k, flags & ~_lib.FP32, _device.ptr(z64),
+                _device.ptr(self.ws), self.ws.numel(), _device.ptr(self.err), _device.stream_handle()))
+            z.copy_(z64)
+        else:
+            _lib.check(st)
         if check:
-            _device.check_device_errors(self.err, "encode")
+            bits = int(self.err.item())
+            if bits & _lib.ERR_NEG_WEIGHT and self.nonneg:
+                # the non-negativity assertion was wrong: recompute on the exact path
+                self.nonneg = False
+                return self.run(rows, cols, weights, labels, check=True, out=out)
+            _lib.raise_device_errors(bits, "encode")
         return z
 
     def capture(self, rows, cols, weights, labels, *, profile: bool = False):
@@ -131,9 +174,9 @@ class GeeEncoder:
             return t.pin_memory()
         self._h = [pin(rows), pin(cols), None if weights is None else pin(weights), pin(labels)]
         self._d = [None if h is None else torch.empty_like(h, device=self.dev) for h in self._h]
-        self._zh = torch.empty((self.n, self.k), dtype=torch.float64).pin_memory()
+        self._zh = torch.empty((self.n, self.k), dtype=self.dtype).pin_memory()
         h2d = sum(h.numel() * h.element_size() for h in self._h if h is not None)
-        return h2d, self._zh.numel() * 8
+        return h2d, self._zh.numel() * self._zh.element_size()
 
     def run_host(self, *, check: bool = True) -> torch.Tensor:
         """Host -> device copies, the fused pipeline, device -> host Z; all
@@ -157,22 +200,43 @@ def _check_shapes(n_rows, n_cols, labels):
         raise StructuralError(f"label count {len(labels)} != node count {n_rows}")
 
 
-def encode(adj, labels, opts=None, *, out: str = "numpy"):
-    """Embed via the sparse pipeline on the GPU; returns a dense (N, K) float64 array."""
+_ENCODERS: dict = {}
+_ENCODER_CACHE = 4
+
+
+def _encoder(n, e, k, directed, flags, nonneg, dtype, dev) -> GeeEncoder:
+    """Per-shape plan cache (workspace + output reused across calls)."""
+    key = (dev, n, e, k, directed, flags, nonneg, dtype)
+    enc = _ENCODERS.pop(key, None)
+    if enc is None:
+        while len(_ENCODERS) >= _ENCODER_CACHE:
+            _ENCODERS.pop(next(iter(_ENCODERS)))
+        enc = GeeEncoder(n, e, k, directed, None, dev, nonneg=nonneg, dtype=dtype)
+        enc.flags = flags
+    _ENCODERS[key] = enc  # most recently used last
+    return enc
+
+
+def encode(adj, labels, opts=None, *, out: str = "numpy", dtype=torch.float64):
+    """Embed via the sparse pipeline on the GPU; returns a dense (N, K) array
+    (float64, or float32 with dtype=torch.float32 -- the optional fp32 path)."""
     labels = _labels_of(labels)
     flags = options_flags(opts)
     dev = _device.require_gpu()
     if hasattr(adj, "index_pointers"):
         z = _encode_csr(CsrMatrix.coerce(adj, dev), labels, flags, dev)
+        if dtype == torch.float32:
+            z = z.to(torch.float32)
     else:
         edges = _edges_of(adj)
         _check_shapes(edges.n_nodes, edges.n_nodes, labels)
         e = edges.to_device(dev)
         lab = _device.to_device(labels.labels, torch.int64, dev)
-        enc = GeeEncoder(e.n_nodes, e.n_edges, labels.k_classes, e.directed, None, dev)
-        enc.flags = flags
         wt_code, w = e.weight_kind()
+        enc = _encoder(e.n_nodes, e.n_edges, labels.k_classes, e.directed, flags, bool(e.nonneg), dtype, dev)
         z = enc.run(e.rows, e.cols, w, lab, check=True)
+        if out == "torch":
+            z = z.clone()  # the plan's output buffer is reused by the next call
     if out == "torch":
         return z
     return z.cpu().numpy()

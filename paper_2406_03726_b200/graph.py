@@ -69,6 +69,10 @@ class EdgeList:
         # device path then never reads the weight array.  Established by the
         # same construction-time scan that checks finiteness (graph_io.py:71).
         self.unit_weights = self.weights is None
+        # True when every weight is >= 0 (established by the same scan; None =
+        # not checked).  Lets encode() take the bucketed stream path, whose
+        # any-order sums are within 1e-12 only without cancellation.
+        self.nonneg = True if self.weights is None else None
         if validate and self.n_edges:
             self._validate()
 
@@ -88,7 +92,8 @@ class EdgeList:
             if bits & _lib.ERR_EDGE_WEIGHT:
                 raise StructuralError("edge weights must be finite")
             if self.weights is not None:
-                self.unit_weights = bool((self.weights == 1.0).all().item())
+                flags = torch.stack([(self.weights == 1.0).all(), (self.weights >= 0).all()]).cpu()
+                self.unit_weights, self.nonneg = bool(flags[0]), bool(flags[1])
             return
         hi = max(int(self.rows.max()), int(self.cols.max()))
         lo = min(int(self.rows.min()), int(self.cols.min()))
@@ -98,6 +103,7 @@ class EdgeList:
             if not np.isfinite(self.weights).all():
                 raise StructuralError("edge weights must be finite")
             self.unit_weights = bool((self.weights == 1.0).all())
+            self.nonneg = bool((self.weights >= 0).all())
 
     @property
     def n_edges(self) -> int:
@@ -127,6 +133,7 @@ class EdgeList:
                        _device.to_device(self.cols, torch.int64, dev), w, self.directed,
                        validate=False)
         out.unit_weights = self.unit_weights
+        out.nonneg = self.nonneg
         return out
 
     def weights_f64(self) -> np.ndarray:

@@ -1,11 +1,16 @@
 """Seeded synthetic inputs for the five BASELINE.json configurations.
 
-The paper's benchmark graphs (Network Repository) are not available; these
-generators stand in for them with the shapes, sizes and value distributions
-BASELINE.json names ("Workloads").  All randomness is seeded;
-numpy generators run on the host, the two largest graphs are drawn with a
-seeded torch generator on the device (then copied to the host only when the
-CPU oracle needs them).
+The paper's benchmark graphs (Network Repository) are not available, and the
+reference ships only its SBM generator (sbm.py:115-155, a sequential numpy
+PCG64 stream).  These generators stand in for them with the shapes, sizes and
+value distributions BASELINE.json names ("Workloads").
+
+Every random word is COUNTER-BASED -- word t of stream s is SplitMix64's
+output for key mix64(seed ^ s * golden) -- so edge arrays are drawn on the
+device by libgee's generator kernels (csrc/k_gen.cu) and the
+reference arm draws the identical arrays on the host with the C restatement
+(oracle/gee_gen.c).  Node-sized tables (labels, the Chung-Lu CDF) are built
+here with numpy, for both arms.
 
   0  SBM       N=10,000  K=3   p_in=0.13 p_out=0.10, undirected, w=1.0   no options
   1  SBM       same graph                                                 lap+diag+corr
@@ -18,7 +23,6 @@ CPU oracle needs them).
 from __future__ import annotations
 
 import numpy as np
-import torch
 
 LAP, DIAG, CORR = 1, 2, 4
 
@@ -35,9 +39,42 @@ CONFIGS = {
             seed=4, flags=LAP | CORR, directed=False),
 }
 
+# stream ids of the counter-based generator
+S_ROW, S_COL, S_W, S_LABEL, S_PERM, S_RMAT, S_PAIRS, S_SBM = 1, 2, 3, 4, 5, 6, 7, 8
+_M64 = (1 << 64) - 1
+_GOLDEN = 0x9E3779B97F4A7C15
+
+
+def _mix64(z: int) -> int:
+    z &= _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def stream_key(seed: int, stream: int) -> int:
+    """mix64(seed ^ stream * golden): the key of one generator stream."""
+    return _mix64(seed ^ ((stream * _GOLDEN) & _M64))
+
+
+def draw_np(key: int, t: np.ndarray) -> np.ndarray:
+    """Words t of stream `key` (uint64), vectorised: mix64(key + (t+1)*golden)."""
+    with np.errstate(over="ignore"):
+        z = np.uint64(key) + (t.astype(np.uint64) + np.uint64(1)) * np.uint64(_GOLDEN)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def uniform_labels(seed: int, n: int, k: int) -> np.ndarray:
+    """labels_i = hi32(word_i >> 32 * k): i.i.d. uniform over {0..k-1}."""
+    hi = draw_np(stream_key(seed, S_LABEL), np.arange(n, dtype=np.uint64)) >> np.uint64(32)
+    return ((hi * np.uint64(k)) >> np.uint64(32)).astype(np.int64)
+
 
 def zipf_counts(n: int, k: int, s: float) -> np.ndarray:
-    """Class sizes proportional to c^-s (c = 1..k), largest-remainder rounding."""
+    """Class sizes proportional to c^-s (c = 1..k), largest-remainder rounding
+    (the apportionment of sbm.py:104-112)."""
     p = np.arange(1, k + 1, dtype=np.float64) ** (-s)
     p /= p.sum()
     raw = p * n
@@ -49,116 +86,142 @@ def zipf_counts(n: int, k: int, s: float) -> np.ndarray:
     return base
 
 
-def sbm(n: int, k: int, p_in: float, p_out: float, seed: int, block: int = 1024):
-    """Undirected SBM: labels i.i.d. uniform; each pair i<j is an edge with
-    p_in (same class) or p_out.  Edges come out in row-major (i, j) order."""
-    rng = np.random.default_rng(seed)
-    labels = rng.integers(0, k, n).astype(np.int64)
-    rows, cols = [], []
-    for i0 in range(0, n - 1, block):
-        i1 = min(n - 1, i0 + block)
-        j0 = i0 + 1
-        u = rng.random((i1 - i0, n - j0))
-        p = np.where(labels[i0:i1, None] == labels[None, j0:], p_in, p_out)
-        hit = u < p
-        hit &= np.arange(j0, n)[None, :] > np.arange(i0, i1)[:, None]
-        r, c = np.nonzero(hit)
-        rows.append(r.astype(np.int64) + i0)
-        cols.append(c.astype(np.int64) + j0)
-    rows = np.concatenate(rows) if rows else np.empty(0, np.int64)
-    cols = np.concatenate(cols) if cols else np.empty(0, np.int64)
-    return rows, cols, labels
+def permuted_labels(seed: int, counts: np.ndarray) -> np.ndarray:
+    """Labels with exactly `counts` members per class, placed by a random
+    permutation (stable argsort of one word per node)."""
+    n = int(counts.sum())
+    lab = np.repeat(np.arange(counts.size, dtype=np.int64), counts)
+    order = np.argsort(draw_np(stream_key(seed, S_PERM), np.arange(n, dtype=np.uint64)), kind="stable")
+    out = np.empty(n, np.int64)
+    out[order] = lab
+    return out
 
 
-def chung_lu(n: int, e: int, gamma: float, seed: int):
-    """E endpoint pairs drawn i.i.d. from p_i ~ (i+1)^(-1/(gamma-1));
-    self-loops and duplicates kept (the reference sums them)."""
-    rng = np.random.default_rng(seed)
+def chunglu_cdf(n: int, gamma: float) -> np.ndarray:
+    """CDF of p_i ~ (i+1)^(-1/(gamma-1)) (numpy cumsum, identical for both arms)."""
     w = (np.arange(n, dtype=np.float64) + 1.0) ** (-1.0 / (gamma - 1.0))
     cdf = np.cumsum(w)
     cdf /= cdf[-1]
-    rows = np.minimum(np.searchsorted(cdf, rng.random(e), side="right"), n - 1).astype(np.int64)
-    cols = np.minimum(np.searchsorted(cdf, rng.random(e), side="right"), n - 1).astype(np.int64)
-    weights = 1.0 - rng.random(e)  # (0, 1]
-    return rows, cols, weights, rng
+    return cdf
 
 
-def rmat(scale: int, e: int, abcd, seed: int, device="cpu", chunk: int = 1 << 26):
-    """R-MAT edges (no noise), directed, duplicates kept; float32 weights in (0, 1]."""
-    a, b, c, _ = abcd
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    rows = torch.empty(e, dtype=torch.int64, device=device)
-    cols = torch.empty(e, dtype=torch.int64, device=device)
-    for s0 in range(0, e, chunk):
-        m = min(chunk, e - s0)
-        r = torch.zeros(m, dtype=torch.int64, device=device)
-        q = torch.zeros(m, dtype=torch.int64, device=device)
-        for _ in range(scale):
-            u = torch.rand(m, generator=g, device=device)
-            rb = (u >= a + b).to(torch.int64)
-            cb = (((u >= a) & (u < a + b)) | (u >= a + b + c)).to(torch.int64)
-            r = r * 2 + rb
-            q = q * 2 + cb
-        rows[s0:s0 + m] = r
-        cols[s0:s0 + m] = q
-    w = 1.0 - torch.rand(e, generator=g, device=device, dtype=torch.float32)
-    return rows, cols, w, g
+def thresholds(probs) -> tuple:
+    """Cumulative probabilities as 32-bit integer thresholds floor(P * 2^32)."""
+    out, acc = [], 0.0
+    for p in probs:
+        acc += p
+        out.append(min(int(acc * 4294967296.0), 0xFFFFFFFF))
+    return tuple(out)
 
 
-def gnm(n: int, m: int, seed: int, device="cpu"):
-    """m distinct unordered pairs {i, j}, i != j, uniformly at random."""
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    keys = torch.empty(0, dtype=torch.int64, device=device)
-    need = m
-    while need > 0:
-        draw = int(need * 1.05) + 1024
-        i = torch.randint(0, n, (draw,), generator=g, device=device)
-        j = torch.randint(0, n, (draw,), generator=g, device=device)
-        ok = i != j
-        lo = torch.minimum(i, j)[ok]
-        hi = torch.maximum(i, j)[ok]
-        keys = torch.unique(torch.cat([keys, lo * n + hi]))
-        need = m - keys.numel()
-    perm = torch.randperm(keys.numel(), generator=g, device=device)[:m]
-    keys = keys[perm]
-    return keys // n, keys % n, g
-
-
-def make_config(idx: int, device="cpu", scale_down: int = 0):
-    """Inputs of config `idx`: dict(rows, cols, weights, labels, n, k, directed,
-    flags, name).  rows/cols/labels int64, weights float64 (float32 for
-    cfg 3).  `scale_down` shrinks configs 2-4 by 2**scale_down (tests)."""
+def spec(idx: int, scale_down: int = 0) -> dict:
+    """Host-side description of config `idx`: sizes, options, labels and the
+    generator parameters.  `scale_down` shrinks configs 2-4 by 2**scale_down
+    in nodes (R-MAT: edges by 4**scale_down) for tests."""
     cfg = dict(CONFIGS[idx])
-    kind = cfg["kind"]
+    kind, seed = cfg["kind"], cfg["seed"]
     if kind == "sbm":
-        rows, cols, labels = sbm(cfg["n"], cfg["k"], cfg["p_in"], cfg["p_out"], cfg["seed"])
         n = cfg["n"]
-        weights = np.ones(rows.shape[0])
+        cfg.update(labels=uniform_labels(seed, n, cfg["k"]), e=None, wdtype="unit",
+                   thr=(min(int(cfg["p_in"] * 4294967296.0), 0xFFFFFFFF),
+                        min(int(cfg["p_out"] * 4294967296.0), 0xFFFFFFFF)),
+                   key=stream_key(seed, S_SBM))
     elif kind == "chunglu":
-        n = cfg["n"] >> scale_down
-        e = cfg["e"] >> scale_down
-        rows, cols, weights, rng = chung_lu(n, e, cfg["gamma"], cfg["seed"])
-        labels = rng.permutation(np.repeat(np.arange(cfg["k"], dtype=np.int64),
-                                           zipf_counts(n, cfg["k"], cfg["zipf"])))
+        n, e = cfg["n"] >> scale_down, cfg["e"] >> scale_down
+        cfg.update(e=e, cdf=chunglu_cdf(n, cfg["gamma"]), wdtype="f64",
+                   labels=permuted_labels(seed, zipf_counts(n, cfg["k"], cfg["zipf"])),
+                   keys=(stream_key(seed, S_ROW), stream_key(seed, S_COL), stream_key(seed, S_W)))
     elif kind == "rmat":
         sc = cfg["scale"] - scale_down
         n = 1 << sc
-        e = cfg["e"] >> (2 * scale_down if scale_down else 0)
-        rows, cols, weights, g = rmat(sc, e, cfg["abcd"], cfg["seed"], device)
-        labels = torch.randint(0, cfg["k"], (n,), generator=g, device=device, dtype=torch.int64)
+        e = cfg["e"] >> (2 * scale_down)
+        cfg.update(scale=sc, e=e, wdtype="f32", thr=thresholds(cfg["abcd"][:3]),
+                   labels=uniform_labels(seed, n, cfg["k"]),
+                   keys=(stream_key(seed, S_RMAT), stream_key(seed, S_W)))
     elif kind == "gnm":
-        n = cfg["n"] >> scale_down
-        e = cfg["e"] >> scale_down
-        rows, cols, g = gnm(n, e, cfg["seed"], device)
-        weights = torch.ones(e, dtype=torch.float64, device=device)
-        counts = zipf_counts(n, cfg["k"], cfg["zipf"])
-        lab = np.repeat(np.arange(cfg["k"], dtype=np.int64), counts)
-        perm = torch.randperm(n, generator=g, device=device)
-        labels = torch.as_tensor(lab, device=device)[perm]
+        n, e = cfg["n"] >> scale_down, cfg["e"] >> scale_down
+        cfg.update(e=e, wdtype="unit", labels=permuted_labels(seed, zipf_counts(n, cfg["k"], cfg["zipf"])),
+                   key=stream_key(seed, S_PAIRS), limit=e + e // 32 + 4096)
     else:
         raise ValueError(kind)
-    cfg.update(rows=rows, cols=cols, weights=weights, labels=labels, n=n,
-               e=int(rows.shape[0]))
+    cfg["n"] = n
+    cfg["idx"] = idx
     return cfg
+
+
+def _device_edges(s: dict, dev):
+    """Edge arrays of spec `s` drawn on the device by libgee (k_gen.cu)."""
+    import torch
+
+    from . import _device, _lib
+    lib = _lib.load()
+    st = _device.stream_handle()
+    kind, n = s["kind"], s["n"]
+    with torch.cuda.device(dev):
+        if kind == "rmat":
+            e = s["e"]
+            rows = torch.empty(e, dtype=torch.int64, device=dev)
+            cols = torch.empty(e, dtype=torch.int64, device=dev)
+            w = torch.empty(e, dtype=torch.float32, device=dev)
+            t1, t2, t3 = s["thr"]
+            _lib.check(lib.gee_gen_rmat(s["keys"][0], s["keys"][1], s["scale"], e, t1, t2, t3,
+                                        _device.ptr(rows), _device.ptr(cols), _device.ptr(w), st))
+        elif kind == "chunglu":
+            e = s["e"]
+            cdf = torch.as_tensor(s["cdf"], device=dev)
+            rows = torch.empty(e, dtype=torch.int64, device=dev)
+            cols = torch.empty(e, dtype=torch.int64, device=dev)
+            w = torch.empty(e, dtype=torch.float64, device=dev)
+            rk, ck, wk = s["keys"]
+            _lib.check(lib.gee_gen_chunglu(rk, ck, wk, _device.ptr(cdf), n, e, _device.ptr(rows),
+                                           _device.ptr(cols), _device.ptr(w), st))
+        elif kind == "gnm":
+            e, lim = s["e"], s["limit"]
+            keys = torch.empty(lim, dtype=torch.int64, device=dev)
+            _lib.check(lib.gee_gen_pairs(s["key"], 0, lim, n, _device.ptr(keys), st))
+            # first occurrence of each pair in candidate order (stable sort by key)
+            sk, perm = torch.sort(keys, stable=True)
+            first = torch.ones_like(sk, dtype=torch.bool)
+            first[1:] = sk[1:] != sk[:-1]
+            first &= sk >= 0
+            keep = torch.zeros_like(first)
+            keep[perm] = first
+            idx = torch.nonzero(keep).flatten()
+            if idx.numel() < e:
+                raise RuntimeError("G(n,m) generator: not enough distinct candidate pairs")
+            kept = keys[idx[:e]]
+            rows, cols = kept // n, kept % n
+            del keys, sk, perm, first, keep, idx, kept
+            w = torch.ones(e, dtype=torch.float64, device=dev)
+        elif kind == "sbm":
+            lab = torch.as_tensor(s["labels"], device=dev)
+            cnt = torch.empty(n, dtype=torch.int64, device=dev)
+            ti, to = s["thr"]
+            _lib.check(lib.gee_gen_sbm_count(s["key"], n, _device.ptr(lab), ti, to, _device.ptr(cnt), st))
+            off = torch.zeros(n, dtype=torch.int64, device=dev)
+            off[1:] = torch.cumsum(cnt, 0)[:-1]
+            e = int((off[-1] + cnt[-1]).item())
+            rows = torch.empty(e, dtype=torch.int64, device=dev)
+            cols = torch.empty(e, dtype=torch.int64, device=dev)
+            _lib.check(lib.gee_gen_sbm_fill(s["key"], n, _device.ptr(lab), ti, to, _device.ptr(off),
+                                            _device.ptr(rows), _device.ptr(cols), st))
+            w = torch.ones(e, dtype=torch.float64, device=dev)
+        else:
+            raise ValueError(kind)
+    return rows, cols, w
+
+
+def make_config(idx: int, device="cuda", scale_down: int = 0) -> dict:
+    """Inputs of config `idx` on a CUDA device: dict(rows, cols, weights,
+    labels, n, e, k, directed, flags, name, ...).  rows/cols/labels int64,
+    weights float64 (float32 for config 3).  The host arrays of the same
+    graph come from oracle/gen.py (C restatement, bit-identical)."""
+    import torch
+    s = spec(idx, scale_down)
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        raise ValueError("make_config draws on a CUDA device; host arrays: oracle.gen.host_config")
+    rows, cols, w = _device_edges(s, dev)
+    s.update(rows=rows, cols=cols, weights=w, labels=torch.as_tensor(s["labels"], device=dev),
+             e=int(rows.shape[0]))
+    return s

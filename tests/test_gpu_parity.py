@@ -38,12 +38,16 @@ class assembly_path:
         self.force = {"default": 0, "sort": 2, "buckets": 1, "sort64": 3}[path]
 
     def __enter__(self):
+        # a forced CSR path also disables the bucketed stream encode, so
+        # encode(EdgeList) runs through the CSR assembly under test
         from paper_2406_03726_b200 import _lib
         self.old = _lib.load().gee_debug_set(_lib.DEBUG_FORCE_BUCKETS, self.force)
+        self.old_stream = _lib.load().gee_debug_set(_lib.DEBUG_STREAM, 1 if self.force else 0)
 
     def __exit__(self, *exc):
         from paper_2406_03726_b200 import _lib
         _lib.load().gee_debug_set(_lib.DEBUG_FORCE_BUCKETS, self.old)
+        _lib.load().gee_debug_set(_lib.DEBUG_STREAM, self.old_stream)
 
 
 def z_close(z, zr, rtol=RTOL, zr_pre=None):
@@ -354,18 +358,17 @@ def test_bitmap_encode_variants(variant):
 # ---- configs -----------------------------------------------------------------
 @pytest.mark.parametrize("idx,scale_down", [(0, 0), (1, 0), (2, 5), (3, 8), (4, 6)])
 def test_configs_vs_oracle(idx, scale_down):
-    from paper_2406_03726_b200 import synth
-    c = synth.make_config(idx, scale_down=scale_down)
-    rows, cols, w, labels = (x.cpu().numpy() if isinstance(x, torch.Tensor) else x
-                             for x in (c["rows"], c["cols"], c["weights"], c["labels"]))
+    from oracle import gen
+    c = gen.host_config(idx, scale_down=scale_down)
+    rows, cols, w, labels = c["rows"], c["cols"], c["weights"], c["labels"]
     f = c["flags"]
     combo = (int(bool(f & 1)), int(bool(f & 2)), int(bool(f & 4)))
     _check_against_oracle(c["n"], rows, cols, w, labels, c["k"], c["directed"], combos=[combo])
 
 
 def test_full_cfg1_properties():
-    from paper_2406_03726_b200 import synth
-    c = synth.make_config(1)
+    from oracle import gen
+    c = gen.host_config(1)
     edges = G.EdgeList(c["n"], c["rows"], c["cols"], c["weights"]).to_device("cuda")
     lab = G.LabelVector(c["labels"], 3)
     csr = edges.to_csr()
@@ -383,8 +386,9 @@ def test_full_cfg1_properties():
 
 
 def test_encoder_plan_and_launch_count():
-    from paper_2406_03726_b200 import _lib, synth
-    c = synth.make_config(1)
+    from paper_2406_03726_b200 import _lib
+    from oracle import gen
+    c = gen.host_config(1)
     dev = torch.device("cuda")
     rows = torch.as_tensor(c["rows"], device=dev)
     cols = torch.as_tensor(c["cols"], device=dev)

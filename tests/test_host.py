@@ -61,21 +61,42 @@ def test_zipf_counts():
 
 
 def test_sbm_config_shape_and_determinism():
-    a = synth.make_config(0)
-    b = synth.make_config(1)
+    from oracle import gen
+    a = gen.host_config(0)
+    b = gen.host_config(1)
     assert np.array_equal(a["rows"], b["rows"]) and np.array_equal(a["cols"], b["cols"])
     assert a["n"] == 10_000 and a["k"] == 3 and not a["directed"]
     assert 5_400_000 < a["e"] < 5_600_000
     assert (a["rows"] < a["cols"]).all()  # i < j, no self loops, no duplicates
     assert b["flags"] == 7 and a["flags"] == 0
+    # row-major order, like the reference's pair sweep
+    key = a["rows"] * a["n"] + a["cols"]
+    assert (np.diff(key) > 0).all()
 
 
 def test_scaled_generators():
-    c2 = synth.make_config(2, scale_down=6)
+    from oracle import gen
+    c2 = gen.host_config(2, scale_down=6)
     assert c2["weights"].dtype == np.float64 and (c2["weights"] > 0).all() and (c2["weights"] <= 1).all()
-    c3 = synth.make_config(3, scale_down=8)
-    assert c3["directed"] and c3["weights"].dtype == torch.float32 and c3["n"] == 1 << 16
+    assert np.bincount(c2["labels"]).tolist() == synth.zipf_counts(c2["n"], 20, 1.1).tolist()
+    c3 = gen.host_config(3, scale_down=8)
+    assert c3["directed"] and c3["weights"].dtype == np.float32 and c3["n"] == 1 << 16
     assert int(c3["rows"].max()) < c3["n"] and int(c3["cols"].max()) < c3["n"]
-    c4 = synth.make_config(4, scale_down=8)
+    assert (c3["weights"] > 0).all() and (c3["weights"] <= 1).all()
+    # R-MAT skew: P(row bit = 1) = c + d = 0.24 per level
+    assert abs((c3["rows"] & 1).mean() - 0.24) < 0.01 and abs((c3["cols"] & 1).mean() - 0.24) < 0.01
+    c4 = gen.host_config(4, scale_down=8)
     keys = c4["rows"] * c4["n"] + c4["cols"]
-    assert torch.unique(keys).numel() == keys.numel() and bool((c4["rows"] < c4["cols"]).all())
+    assert np.unique(keys).size == keys.size and bool((c4["rows"] < c4["cols"]).all())
+
+
+def test_generator_is_counter_based():
+    """Edge i depends only on (seed, i): a prefix of a longer draw is the
+    shorter draw, and python's key derivation equals the C one."""
+    from oracle import gen
+    assert gen._lib().ggen_key(3, synth.S_RMAT) == synth.stream_key(3, synth.S_RMAT)
+    a = gen.pairs(synth.stream_key(4, synth.S_PAIRS), 0, 5000, 1000)
+    b = gen.pairs(synth.stream_key(4, synth.S_PAIRS), 1000, 4000, 1000)
+    assert np.array_equal(a[1000:], b)
+    labs = synth.uniform_labels(9, 100000, 7)
+    assert set(np.unique(labs)) == set(range(7)) and abs(np.bincount(labs).std() / 100000 * 7) < 0.02

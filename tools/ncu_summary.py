@@ -1,11 +1,14 @@
 """Print the headline metrics and stall breakdown of an ncu report (first kernel).
-usage: python tools/ncu_summary.py REPORT.ncu-rep"""
+usage: python tools/ncu_summary.py REPORT.ncu-rep [KERNEL_REGEX]"""
 import csv
 import io
 import subprocess
 import sys
 
-out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+cmd = ["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"]
+if len(sys.argv) > 2:
+    cmd += ["-k", "regex:" + sys.argv[2]]
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(out)))
 h, units, v = r[0], r[1], r[2]
 want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
