@@ -57,12 +57,15 @@ namespace {
 constexpr int kStNT = 512;            // partition / histogram threads
 constexpr int kStTile = 4096;         // entries per partition tile
 constexpr int kStWin = 2048;          // shared bins of the bucket window
-constexpr int kEmbNT = 512;           // degree / embed threads
+constexpr int kEmbNT = 512;           // embed threads (upper bound)
+constexpr int kDegNT = 256;           // degree threads (8 warps, a work item each)
 constexpr int kEmbWarps = kEmbNT / 32;
 constexpr size_t kZTileMax = 104 * 1024;  // bytes of the R x K f64 Z tile (upper bound)
 constexpr size_t kZTileDefault = 64 * 1024;  // default: leaves room for 2 CTAs per SM with the record stages
 constexpr size_t emb_stage_bytes(int nt) { return (size_t)2 * 4 * nt * 16; }  // two stages of 4 records per thread
 int t_emb_nt = 256;  // debug hook: threads of the embed CTA (128 / 256 / 512)
+constexpr unsigned kDegItem = 4096;  // entries per degree work item (one warp)
+constexpr int kScanBlock = 4096;     // buckets per k_st_scan2 block (1024 threads x 4)
 constexpr int kLrowMax = 9;  // at most 512 rows per bucket (per-warp degree copies: 64 KB)
 
 int t_stream_mode = 0;  // debug hook: 0 auto, 1 never, >= 16 embed A/B variant
@@ -129,6 +132,8 @@ struct StWs {
     unsigned long long *keys1;
     void *w1;
     unsigned *hist2, *base2, *cur2, *item_off, *done_deg, *done_emb, *item_bucket, *split_slot;
+    unsigned *ditem_off, *ditem_bucket;  // degree work items (<= kDegItem entries, a warp each)
+    unsigned *scan_part;                 // [blocks][4] partial sums of k_st_scan2a
     double *scratch;  // [max_split][R * K]: f64 partial tiles of split buckets
     uint32_t *keys2;
     void *w2;
@@ -139,7 +144,8 @@ struct StWs {
     double *inv;
     unsigned *label_partial;
 };
-constexpr int kCtlHist1 = 0, kCtlBase1 = 256, kCtlCur1 = 520, kCtlItems = 776, kCtlWork = 777, kCtlLabel = 780;
+constexpr int kCtlHist1 = 0, kCtlBase1 = 256, kCtlCur1 = 520, kCtlItems = 776, kCtlWork = 777, kCtlLabel = 780,
+              kCtlDItems = 781, kCtlSplit = 782;
 constexpr int kCtlWords = 784;
 
 size_t carve(Carver &cv, StWs &w, const StGeo &g) {
@@ -156,6 +162,9 @@ size_t carve(Carver &cv, StWs &w, const StGeo &g) {
     w.done_emb = cv.take<unsigned>((size_t)g.S + 1);
     w.item_bucket = cv.take<unsigned>((size_t)g.max_items);
     w.split_slot = cv.take<unsigned>((size_t)g.S + 1);
+    w.ditem_off = cv.take<unsigned>((size_t)g.S + 1);
+    w.ditem_bucket = cv.take<unsigned>((size_t)g.S + g.Mcap / kDegItem + 1);
+    w.scan_part = cv.take<unsigned>(4 * ((size_t)g.S / kScanBlock + 2));
     w.scratch = cv.take<double>((size_t)g.max_split * ((size_t)1 << g.lrow_bits) * (size_t)g.k);
     w.keys2 = cv.take<uint32_t>(M);
     w.w2 = wb ? (void *)cv.take<char>(M * wb) : nullptr;
@@ -438,38 +447,40 @@ __global__ void __launch_bounds__(kStNT) k_st_hist2(StArgs a) {
     }
 }
 
-// bucket bases, item offsets, split-bucket scratch slots and the item ->
-// bucket table (one CTA; S <= 2^19 buckets)
-__global__ void __launch_bounds__(1024) k_st_scan2(StArgs a) {
-    __shared__ unsigned red[96];
-    const unsigned S = a.S;
-    const unsigned per = (S + 1023) / 1024;
-    const unsigned lo = min(S, threadIdx.x * per), hi = min(S, lo + per);
-    unsigned v[3] = {0u, 0u, 0u};  // entries, items, split buckets
-    for (unsigned b = lo; b < hi; ++b) {
-        const unsigned h = a.ws.hist2[b];
-        const unsigned ni = h ? (h + a.C - 1) / a.C : 1u;
-        v[0] += h;
-        v[1] += ni;
-        v[2] += ni > 1;
-    }
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    unsigned inc[3] = {v[0], v[1], v[2]};
+// Bucket bases, work items and split slots: a three-kernel scan over the S
+// buckets (S <= 2^19).  Channels: entries, embed items (<= C entries each,
+// at least one per bucket), degree items (<= kDegItem), split buckets.
+__device__ __forceinline__ void bucket_channels(const StArgs &a, unsigned b, unsigned (&v)[4]) {
+    const unsigned h = a.ws.hist2[b];
+    const unsigned ni = h ? (h + a.C - 1) / a.C : 1u;
+    v[0] = h;
+    v[1] = ni;
+    v[2] = h ? (h + kDegItem - 1) / kDegItem : 1u;
+    v[3] = ni > 1;
+}
+
+__device__ __forceinline__ void block_scan4(unsigned (&v)[4], unsigned (&excl)[4], unsigned (&tot)[4],
+                                            unsigned *red /* [4][32] */) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned inc[4];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
+    for (int c = 0; c < 4; ++c) inc[c] = v[c];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
+    for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
             const unsigned y = __shfl_up_sync(0xffffffffu, inc[c], o);
             if (lane >= o) inc[c] += y;
         }
-    }
+    __syncthreads();
     if (lane == 31)
-        for (int c = 0; c < 3; ++c) red[32 * c + wid] = inc[c];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) red[32 * c + wid] = inc[c];
     __syncthreads();
     if (wid == 0) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const unsigned x = red[32 * c + lane];
+        for (int c = 0; c < 4; ++c) {
+            const unsigned x = lane < nw ? red[32 * c + lane] : 0u;
             unsigned xi = x;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -477,29 +488,75 @@ __global__ void __launch_bounds__(1024) k_st_scan2(StArgs a) {
                 if (lane >= o) xi += y;
             }
             red[32 * c + lane] = xi - x;
-            if (lane == 31) {
-                if (c == 0) a.ws.base2[S] = xi;
-                if (c == 1) {
-                    a.ws.item_off[S] = xi;
-                    a.ws.ctl[kCtlItems] = xi;
-                }
-            }
+            if (lane == 31) red[128 + c] = xi;
         }
     }
     __syncthreads();
-    unsigned bs = red[wid] + inc[0] - v[0], ib = red[32 + wid] + inc[1] - v[1], sp = red[64 + wid] + inc[2] - v[2];
-    for (unsigned b = lo; b < hi; ++b) {
-        const unsigned h = a.ws.hist2[b];
-        const unsigned ni = h ? (h + a.C - 1) / a.C : 1u;
-        a.ws.base2[b] = bs;
-        a.ws.cur2[b] = bs;
-        a.ws.item_off[b] = ib;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        excl[c] = red[32 * c + wid] + inc[c] - v[c];
+        tot[c] = red[128 + c];
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_st_scan2a(StArgs a) {
+    __shared__ unsigned red[132];
+    const unsigned b0 = blockIdx.x * kScanBlock + threadIdx.x * 4;
+    unsigned v[4] = {0u, 0u, 0u, 0u}, e[4], t[4];
+    for (int j = 0; j < 4; ++j) {
+        if (b0 + j < a.S) {
+            unsigned c[4];
+            bucket_channels(a, b0 + j, c);
+            for (int q = 0; q < 4; ++q) v[q] += c[q];
+        }
+    }
+    block_scan4(v, e, t, red);
+    if (threadIdx.x == 0)
+        for (int q = 0; q < 4; ++q) a.ws.scan_part[4 * blockIdx.x + q] = t[q];
+}
+
+__global__ void __launch_bounds__(1024) k_st_scan2b(StArgs a, unsigned nblk) {
+    __shared__ unsigned red[132];
+    unsigned v[4] = {0u, 0u, 0u, 0u}, e[4], t[4];
+    if (threadIdx.x < nblk)
+        for (int q = 0; q < 4; ++q) v[q] = a.ws.scan_part[4 * threadIdx.x + q];
+    block_scan4(v, e, t, red);
+    if (threadIdx.x < nblk)
+        for (int q = 0; q < 4; ++q) a.ws.scan_part[4 * threadIdx.x + q] = e[q];
+    if (threadIdx.x == 0) {
+        a.ws.base2[a.S] = t[0];
+        a.ws.item_off[a.S] = t[1];
+        a.ws.ditem_off[a.S] = t[2];
+        a.ws.ctl[kCtlItems] = t[1];
+        a.ws.ctl[kCtlDItems] = t[2];
+        a.ws.ctl[kCtlSplit] = t[3];
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_st_scan2c(StArgs a) {
+    __shared__ unsigned red[132];
+    const unsigned b0 = blockIdx.x * kScanBlock + threadIdx.x * 4;
+    unsigned c[4][4], v[4] = {0u, 0u, 0u, 0u}, e[4], t[4];
+    for (int j = 0; j < 4; ++j) {
+        for (int q = 0; q < 4; ++q) c[j][q] = 0;
+        if (b0 + j < a.S) bucket_channels(a, b0 + j, c[j]);
+        for (int q = 0; q < 4; ++q) v[q] += c[j][q];
+    }
+    block_scan4(v, e, t, red);
+    for (int q = 0; q < 4; ++q) e[q] += a.ws.scan_part[4 * blockIdx.x + q];
+    for (int j = 0; j < 4; ++j) {
+        const unsigned b = b0 + j;
+        if (b >= a.S) break;
+        a.ws.base2[b] = e[0];
+        a.ws.cur2[b] = e[0];
+        a.ws.item_off[b] = e[1];
+        a.ws.ditem_off[b] = e[2];
+        a.ws.split_slot[b] = c[j][3] ? e[3] : 0xffffffffu;
         a.ws.done_deg[b] = 0;
         a.ws.done_emb[b] = 0;
-        a.ws.split_slot[b] = ni > 1 ? sp++ : 0xffffffffu;
-        for (unsigned j = 0; j < ni; ++j) a.ws.item_bucket[ib + j] = b;
-        bs += h;
-        ib += ni;
+        for (unsigned i = 0; i < c[j][1]; ++i) a.ws.item_bucket[e[1] + i] = b;
+        for (unsigned i = 0; i < c[j][2]; ++i) a.ws.ditem_bucket[e[2] + i] = b;
+        for (int q = 0; q < 4; ++q) e[q] += c[j][q];
     }
 }
 
@@ -636,94 +693,34 @@ __device__ __forceinline__ void zero_scratch(const StArgs &a, unsigned b, int nr
     for (int64_t i = t; i < nz; i += nt) zs[i] = 0.0;
 }
 
-// CTA per item (buckets of more than 32 rows): per-warp shared degree copies
+// Degrees and node records: a WARP per degree item (<= kDegItem entries of
+// one bucket), so thousands of items are in flight per launch and no CTA
+// barrier is ever taken.  Each warp keeps its bucket's R partial degrees in
+// its own shared slice; a bucket with one item finalises its rows directly,
+// the items of a larger bucket add into deg[] and the last one finalises
+// (and clears the bucket's embed scratch tile when the embed splits it too).
 template <int WT>
-__global__ void __launch_bounds__(kEmbNT) k_st_degree(StArgs a) {
-    extern __shared__ double sdeg[];  // [kEmbWarps][R]
-    __shared__ unsigned s_item, s_last;
-    const int R = 1 << a.lrow_bits;
-    const int wid = threadIdx.x >> 5;
-    const bool lap = (a.flags & GEE_LAPLACIAN) != 0;
-    const unsigned n_items = a.ws.ctl[kCtlItems];
-    const int cb = a.col_bits;
-    constexpr int U = 8;
-    for (;;) {
-        if (threadIdx.x == 0) s_item = atomicAdd(a.ws.ctl + kCtlWork, 1u);
-        __syncthreads();
-        const unsigned item = s_item;
-        if (item >= n_items) break;
-        unsigned b, p0, p1, nitems;
-        item_range(a, item, b, p0, p1, nitems);
-        const int64_t r0 = (int64_t)b << a.lrow_bits;
-        const int nrows = (int)min((int64_t)R, a.N - r0);
-        if (lap) {
-            for (int i = threadIdx.x; i < kEmbWarps * R; i += kEmbNT) sdeg[i] = 0.0;
-            __syncthreads();
-            double *mine = sdeg + wid * R;
-            unsigned p = p0 + threadIdx.x;
-            for (; p + (U - 1) * kEmbNT < p1; p += U * kEmbNT) {
-                unsigned l[U];
-                double x[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) l[u] = __ldcs(a.ws.keys2 + p + u * kEmbNT) >> cb;
-#pragma unroll
-                for (int u = 0; u < U; ++u) x[u] = entry_w<WT>(a, p + u * kEmbNT);
-#pragma unroll
-                for (int u = 0; u < U; ++u) atomicAdd(mine + l[u], x[u]);
-            }
-            for (; p < p1; p += kEmbNT) atomicAdd(mine + (__ldcs(a.ws.keys2 + p) >> cb), entry_w<WT>(a, p));
-            __syncthreads();
-            for (int l = threadIdx.x; l < R; l += kEmbNT) {
-                double d = 0.0;
-                for (int w = 0; w < kEmbWarps; ++w) d += sdeg[w * R + l];
-                sdeg[l] = d;
-            }
-            __syncthreads();
-        }
-        if (nitems == 1) {
-            for (int l = threadIdx.x; l < nrows; l += kEmbNT) finish_node(a, r0 + l, lap ? sdeg[l] : 0.0);
-        } else {
-            if (lap)
-                for (int l = threadIdx.x; l < nrows; l += kEmbNT)
-                    if (sdeg[l] != 0.0) atomicAdd(a.ws.deg + r0 + l, sdeg[l]);
-            __threadfence();
-            __syncthreads();
-            if (threadIdx.x == 0) s_last = atomicAdd(a.ws.done_deg + b, 1u) == nitems - 1;
-            __syncthreads();
-            if (s_last) {
-                __threadfence();
-                for (int l = threadIdx.x; l < nrows; l += kEmbNT)
-                    finish_node(a, r0 + l, lap ? __ldcg(a.ws.deg + r0 + l) : 0.0);
-                zero_scratch(a, b, nrows, threadIdx.x, kEmbNT);
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// Warp per item (buckets of at most 32 rows, e.g. K = 1000): no CTA barriers
-template <int WT>
-__global__ void __launch_bounds__(kEmbNT) k_st_degree_warp(StArgs a) {
-    __shared__ double wdeg[kEmbWarps][32];
+__global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
+    extern __shared__ double wdeg[];  // [kDegNT / 32][R]
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int R = 1 << a.lrow_bits;
     const bool lap = (a.flags & GEE_LAPLACIAN) != 0;
-    const unsigned n_items = a.ws.ctl[kCtlItems];
+    const unsigned n_items = a.ws.ctl[kCtlDItems];
     const int cb = a.col_bits;
-    double *mine = wdeg[wid];
+    double *mine = wdeg + (size_t)wid * R;
     constexpr int U = 8;
-    for (;;) {
-        unsigned item = 0;
-        if (lane == 0) item = atomicAdd(a.ws.ctl + kCtlWork, 1u);
-        item = __shfl_sync(0xffffffffu, item, 0);
-        if (item >= n_items) break;
-        unsigned b, p0, p1, nitems;
-        item_range(a, item, b, p0, p1, nitems);
+    for (unsigned item = (blockIdx.x * kDegNT + threadIdx.x) >> 5; item < n_items;
+         item += (gridDim.x * kDegNT) >> 5) {
+        const unsigned b = a.ws.ditem_bucket[item];
+        const unsigned j = item - a.ws.ditem_off[b];
+        const unsigned nitems = a.ws.ditem_off[b + 1] - a.ws.ditem_off[b];
+        const unsigned s1 = a.ws.base2[b + 1];
+        const unsigned p0 = min(s1, a.ws.base2[b] + j * kDegItem), p1 = min(s1, p0 + kDegItem);
         const int64_t r0 = (int64_t)b << a.lrow_bits;
         const int nrows = (int)min((int64_t)R, a.N - r0);
-        mine[lane] = 0.0;
-        __syncwarp();
         if (lap) {
+            for (int l = lane; l < R; l += 32) mine[l] = 0.0;
+            __syncwarp();
             unsigned p = p0 + lane;
             for (; p + (U - 1) * 32 < p1; p += U * 32) {
                 unsigned l[U];
@@ -739,9 +736,11 @@ __global__ void __launch_bounds__(kEmbNT) k_st_degree_warp(StArgs a) {
             __syncwarp();
         }
         if (nitems == 1) {
-            if (lane < nrows) finish_node(a, r0 + lane, mine[lane]);
+            for (int l = lane; l < nrows; l += 32) finish_node(a, r0 + l, lap ? mine[l] : 0.0);
         } else {
-            if (lap && lane < nrows && mine[lane] != 0.0) atomicAdd(a.ws.deg + r0 + lane, mine[lane]);
+            if (lap)
+                for (int l = lane; l < nrows; l += 32)
+                    if (mine[l] != 0.0) atomicAdd(a.ws.deg + r0 + l, mine[l]);
             __threadfence();
             __syncwarp();
             unsigned last = 0;
@@ -749,8 +748,9 @@ __global__ void __launch_bounds__(kEmbNT) k_st_degree_warp(StArgs a) {
             last = __shfl_sync(0xffffffffu, last, 0);
             if (last) {
                 __threadfence();
-                if (lane < nrows) finish_node(a, r0 + lane, lap ? __ldcg(a.ws.deg + r0 + lane) : 0.0);
-                zero_scratch(a, b, nrows, lane, 32);
+                for (int l = lane; l < nrows; l += 32)
+                    finish_node(a, r0 + l, lap ? __ldcg(a.ws.deg + r0 + l) : 0.0);
+                if (a.ws.split_slot[b] != 0xffffffffu) zero_scratch(a, b, nrows, lane, 32);
             }
         }
         __syncwarp();
@@ -828,22 +828,28 @@ __device__ __forceinline__ void tile_epilogue(const StArgs &a, double *zt, doubl
         for (int64_t i = threadIdx.x; i < n2; i += NT) {
             const unsigned e0 = (unsigned)(2 * i);
             const double2 v = reinterpret_cast<const double2 *>(zt)[i];
+            reinterpret_cast<double2 *>(zt)[i] = make_double2(0.0, 0.0);  // ready for the next bucket
             const double f0 = fac[(e0 * magic) >> 32], f1 = fac[((e0 + 1) * magic) >> 32];
             __stcs(reinterpret_cast<float2 *>(zg) + i, make_float2((float)(v.x * f0), (float)(v.y * f1)));
         }
-        for (int64_t i = 2 * n2 + threadIdx.x; i < n; i += NT)
+        for (int64_t i = 2 * n2 + threadIdx.x; i < n; i += NT) {
             __stcs(zg + i, (float)(zt[i] * fac[((unsigned)i * magic) >> 32]));
+            zt[i] = 0.0;
+        }
     } else {
         double *zg = reinterpret_cast<double *>(a.z) + r0 * K;
         const int64_t n2 = ((uintptr_t)zg & 15) ? 0 : n / 2;
         for (int64_t i = threadIdx.x; i < n2; i += NT) {
             const unsigned e0 = (unsigned)(2 * i);
             const double2 v = reinterpret_cast<const double2 *>(zt)[i];
+            reinterpret_cast<double2 *>(zt)[i] = make_double2(0.0, 0.0);  // ready for the next bucket
             const double f0 = fac[(e0 * magic) >> 32], f1 = fac[((e0 + 1) * magic) >> 32];
             __stcs(reinterpret_cast<double2 *>(zg) + i, make_double2(v.x * f0, v.y * f1));
         }
-        for (int64_t i = 2 * n2 + threadIdx.x; i < n; i += NT)
+        for (int64_t i = 2 * n2 + threadIdx.x; i < n; i += NT) {
             __stcs(zg + i, zt[i] * fac[((unsigned)i * magic) >> 32]);
+            zt[i] = 0.0;
+        }
     }
 }
 
@@ -852,7 +858,7 @@ template <int WT, bool OUT32, int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
     constexpr int U = 4;  // entries per thread per stage; two stages in flight
     extern __shared__ __align__(16) double zt[];  // [R][K], then fac[R], then the record stages
-    __shared__ unsigned s_item, s_last;
+    __shared__ unsigned s_meta[2][4];              // work item {bucket, p0, p1, items of the bucket}
     const int R = 1 << a.lrow_bits;
     const int K = a.k;
     double *fac = zt + (size_t)R * K;
@@ -861,56 +867,69 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
     const unsigned cmask = (1u << a.col_bits) - 1u;
     const int cb = a.col_bits;
     const unsigned step = U * NT;
+    uint32_t kA[U], kB[U];
+    double xA[U], xB[U];
+    // stage s of this thread: the keys of [base, end) are loaded and their node
+    // records requested into the thread's own slots (cp.async, L1 bypassed)
+    auto issue = [&](unsigned base, unsigned end, uint32_t(&kk)[U], double(&x)[U], int s) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const unsigned p = base + u * NT + threadIdx.x;
+            kk[u] = 0xffffffffu;
+            if (p < end) {
+                kk[u] = __ldcs(a.ws.keys2 + p);
+                x[u] = entry_w<WT>(a, p);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (kk[u] != 0xffffffffu) cp_async16(stage + (s * U + u) * NT + threadIdx.x, a.ws.rec + (kk[u] & cmask));
+        cp_async_commit();
+    };
+    auto consume = [&](const uint32_t(&kk)[U], const double(&x)[U], int s) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (kk[u] == 0xffffffffu) continue;
+            const double2 rc = stage[(s * U + u) * NT + threadIdx.x];
+            const int y = rec_label(rc);
+            if (y >= 0) atomicAdd(zt + (kk[u] >> cb) * K + y, x[u] * rc.y);
+        }
+    };
+    auto grab = [&](int slot) {  // thread 0: the next work item into s_meta[slot]
+        const unsigned item = atomicAdd(a.ws.ctl + kCtlWork + 1, 1u);
+        if (item >= n_items) {
+            s_meta[slot][0] = 0xffffffffu;
+            return;
+        }
+        unsigned b, p0, p1, ni;
+        item_range(a, item, b, p0, p1, ni);
+        s_meta[slot][0] = b;
+        s_meta[slot][1] = p0;
+        s_meta[slot][2] = p1;
+        s_meta[slot][3] = ni;
+    };
+    {
+        double2 *z2 = reinterpret_cast<double2 *>(zt);
+        for (int i = threadIdx.x; i < (R * K + 1) / 2; i += NT) z2[i] = make_double2(0.0, 0.0);
+    }
+    if (threadIdx.x == 0) grab(0);
+    __syncthreads();
+    int cur = 0;
+    if (s_meta[0][0] != 0xffffffffu) issue(s_meta[0][1], s_meta[0][2], kA, xA, 0);
     for (;;) {
-        if (threadIdx.x == 0) s_item = atomicAdd(a.ws.ctl + kCtlWork + 1, 1u);
-        __syncthreads();
-        const unsigned item = s_item;
-        if (item >= n_items) break;
-        unsigned b, p0, p1, nitems;
-        item_range(a, item, b, p0, p1, nitems);
+        const unsigned b = s_meta[cur][0];
+        if (b == 0xffffffffu) break;
+        const unsigned p0 = s_meta[cur][1], p1 = s_meta[cur][2], nitems = s_meta[cur][3];
+        // the next item's metadata loads overlap this item's work
+        if (threadIdx.x == 0) grab(cur ^ 1);
         const int64_t r0 = (int64_t)b << a.lrow_bits;
         const int nrows = (int)min((int64_t)R, a.N - r0);
         const int tsz = nrows * K;
-        {
-            double2 *z2 = reinterpret_cast<double2 *>(zt);
-            for (int i = threadIdx.x; i < (tsz + 1) / 2; i += NT) z2[i] = make_double2(0.0, 0.0);
-        }
-        __syncthreads();
-        // two-stage pipeline: the keys of stage s are loaded and their node
-        // records requested (cp.async into this thread's own slots) while the
-        // other stage's records are consumed; no CTA barrier inside the item
-        uint32_t kA[U], kB[U];
-        double xA[U], xB[U];
-        auto issue = [&](unsigned base, uint32_t(&kk)[U], double(&x)[U], int s) {
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const unsigned p = base + u * NT + threadIdx.x;
-                kk[u] = 0xffffffffu;
-                if (p < p1) {
-                    kk[u] = __ldcs(a.ws.keys2 + p);
-                    x[u] = entry_w<WT>(a, p);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (kk[u] != 0xffffffffu)
-                    cp_async16(stage + (s * U + u) * NT + threadIdx.x, a.ws.rec + (kk[u] & cmask));
-            cp_async_commit();
-        };
-        auto consume = [&](const uint32_t(&kk)[U], const double(&x)[U], int s) {
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (kk[u] == 0xffffffffu) continue;
-                const double2 rc = stage[(s * U + u) * NT + threadIdx.x];
-                const int y = rec_label(rc);
-                if (y >= 0) atomicAdd(zt + (kk[u] >> cb) * K + y, x[u] * rc.y);
-            }
-        };
-        if (p0 < p1) issue(p0, kA, xA, 0);
+        // stage A of [p0, p0 + step) was issued before this iteration
         for (unsigned base = p0; base < p1; base += 2 * step) {
             const bool hb = base + step < p1;
             if (hb) {
-                issue(base + step, kB, xB, 1);
+                issue(base + step, p1, kB, xB, 1);
                 cp_async_wait<1>();
             } else {
                 cp_async_wait<0>();
@@ -919,7 +938,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
             if (hb) {
                 const bool ha = base + 2 * step < p1;
                 if (ha) {
-                    issue(base + 2 * step, kA, xA, 0);
+                    issue(base + 2 * step, p1, kA, xA, 0);
                     cp_async_wait<1>();
                 } else {
                     cp_async_wait<0>();
@@ -927,27 +946,34 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
                 consume(kB, xB, 1);
             }
         }
-        __syncthreads();
-        if (a.variant == 3) {
-            // debug A/B: accumulate only
-        } else if (nitems == 1) {
+        __syncthreads();  // tile complete; s_meta[cur ^ 1] visible
+        // the next item's first stage flies while this tile is finished
+        if (s_meta[cur ^ 1][0] != 0xffffffffu) issue(s_meta[cur ^ 1][1], s_meta[cur ^ 1][2], kA, xA, 0);
+        if (nitems == 1) {
             tile_epilogue<OUT32, NT>(a, zt, fac, r0, nrows);
         } else {
             double *zs = a.ws.scratch + (size_t)a.ws.split_slot[b] * ((size_t)R * K);
-            for (int i = threadIdx.x; i < tsz; i += NT)
-                if (zt[i] != 0.0) atomicAdd(zs + i, zt[i]);
+            for (int i = threadIdx.x; i < tsz; i += NT) {
+                const double v = zt[i];
+                if (v != 0.0) {
+                    atomicAdd(zs + i, v);
+                    zt[i] = 0.0;
+                }
+            }
             __threadfence();
             __syncthreads();
-            if (threadIdx.x == 0) s_last = atomicAdd(a.ws.done_emb + b, 1u) == nitems - 1;
+            unsigned *flag = reinterpret_cast<unsigned *>(&s_meta[cur][3]);
+            if (threadIdx.x == 0) *flag = atomicAdd(a.ws.done_emb + b, 1u) == nitems - 1;
             __syncthreads();
-            if (s_last) {
+            if (*flag) {
                 __threadfence();
                 for (int i = threadIdx.x; i < tsz; i += NT) zt[i] = __ldcg(zs + i);
                 __syncthreads();
                 tile_epilogue<OUT32, NT>(a, zt, fac, r0, nrows);
             }
         }
-        __syncthreads();
+        __syncthreads();  // tile zeroed, s_meta[cur] free
+        cur ^= 1;
     }
 }
 
@@ -983,13 +1009,13 @@ int run_stream(const StGeo &g, StArgs &a, cudaStream_t st) {
     static PerDevice attr;
     const size_t p1_smem = (size_t)(8 + WTraits<WT>::bytes) * kStTile;
     const size_t p2_smem = (size_t)(4 + WTraits<WT>::bytes + 2) * kStTile + 3 * sizeof(unsigned) * kStWin;
-    const size_t deg_smem = sizeof(double) * kEmbWarps * ((size_t)1 << g.lrow_bits);
+    const size_t deg_smem = sizeof(double) * (kDegNT / 32) * ((size_t)1 << g.lrow_bits);
     if (!attr.done()) {
         int rc;
         if ((rc = set_smem(k_st_part1<WT, true>, p1_smem))) return rc;
         if ((rc = set_smem(k_st_part1<WT, false>, p1_smem))) return rc;
         if ((rc = set_smem(k_st_part2<WT>, p2_smem))) return rc;
-        if ((rc = set_smem(k_st_degree<WT>, sizeof(double) * kEmbWarps * ((size_t)1 << kLrowMax)))) return rc;
+        if ((rc = set_smem(k_st_degree<WT>, sizeof(double) * (kDegNT / 32) * ((size_t)1 << kLrowMax)))) return rc;
         attr.mark();
     }
     const int sms = num_sms();
@@ -1002,15 +1028,18 @@ int run_stream(const StGeo &g, StArgs &a, cudaStream_t st) {
     GEE_CHECK_LAUNCH("k_st_part1");
     k_st_hist2<<<sms * 4, kStNT, 0, st>>>(a);
     GEE_CHECK_LAUNCH("k_st_hist2");
-    k_st_scan2<<<1, 1024, 0, st>>>(a);
-    GEE_CHECK_LAUNCH("k_st_scan2");
+    {
+        const unsigned nblk = (g.S + kScanBlock - 1) / kScanBlock;
+        k_st_scan2a<<<nblk, 1024, 0, st>>>(a);
+        GEE_CHECK_LAUNCH("k_st_scan2a");
+        k_st_scan2b<<<1, 1024, 0, st>>>(a, nblk);
+        GEE_CHECK_LAUNCH("k_st_scan2b");
+        k_st_scan2c<<<nblk, 1024, 0, st>>>(a);
+        GEE_CHECK_LAUNCH("k_st_scan2c");
+    }
     k_st_part2<WT><<<sms * 3, kStNT, p2_smem, st>>>(a);
     GEE_CHECK_LAUNCH("k_st_part2");
-    if (g.lrow_bits <= 5) {
-        k_st_degree_warp<WT><<<sms * 4, kEmbNT, 0, st>>>(a);
-    } else {
-        k_st_degree<WT><<<sms * 3, kEmbNT, deg_smem, st>>>(a);
-    }
+    k_st_degree<WT><<<sms * 8, kDegNT, deg_smem, st>>>(a);
     GEE_CHECK_LAUNCH("k_st_degree");
     const bool out32 = (a.flags & GEE_FP32) != 0;
     int rc2;

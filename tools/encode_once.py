@@ -16,6 +16,11 @@ cfg = int(sys.argv[1])
 reps = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 2
 if "--no-stream" in sys.argv:
     _lib.load().gee_debug_set(_lib.DEBUG_STREAM, 1)
+for a in sys.argv:
+    if a.startswith("--nt="):
+        _lib.load().gee_debug_set(6, int(a[5:]))
+    if a.startswith("--tile="):
+        _lib.load().gee_debug_set(_lib.DEBUG_STREAM_TILE, int(a[7:]))
 c = synth.make_config(cfg, "cuda")
 edges = G.EdgeList(c["n"], c["rows"], c["cols"], c["weights"], c["directed"])
 _, w = edges.weight_kind()
