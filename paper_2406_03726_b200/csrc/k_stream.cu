@@ -61,9 +61,9 @@ constexpr int kEmbNT = 512;           // embed threads (upper bound)
 constexpr int kDegNT = 256;           // degree threads (8 warps, a work item each)
 constexpr int kEmbWarps = kEmbNT / 32;
 constexpr size_t kZTileMax = 104 * 1024;  // bytes of the R x K f64 Z tile (upper bound)
-constexpr size_t kZTileDefault = 64 * 1024;  // default: leaves room for 2 CTAs per SM with the record stages
+constexpr size_t kZTileDefault = 32 * 1024;  // default (A/B, profiles/r2_stream_ab.txt): several CTAs per SM hide item latency
 constexpr size_t emb_stage_bytes(int nt) { return (size_t)2 * 4 * nt * 16; }  // two stages of 4 records per thread
-int t_emb_nt = 256;  // debug hook: threads of the embed CTA (128 / 256 / 512)
+int t_emb_nt = 128;  // debug hook: threads of the embed CTA (128 / 256 / 512)
 constexpr unsigned kDegItem = 4096;  // entries per degree work item (one warp)
 constexpr int kScanBlock = 4096;     // buckets per k_st_scan2 block (1024 threads x 4)
 constexpr int kLrowMax = 9;  // at most 512 rows per bucket (per-warp degree copies: 64 KB)
@@ -133,6 +133,7 @@ struct StWs {
     void *w1;
     unsigned *hist2, *base2, *cur2, *item_off, *done_deg, *done_emb, *item_bucket, *split_slot;
     unsigned *ditem_off, *ditem_bucket;  // degree work items (<= kDegItem entries, a warp each)
+    uint4 *item_desc;                    // embed work items {bucket, p0, p1, items of the bucket}
     unsigned *scan_part;                 // [blocks][4] partial sums of k_st_scan2a
     double *scratch;  // [max_split][R * K]: f64 partial tiles of split buckets
     uint32_t *keys2;
@@ -163,6 +164,7 @@ size_t carve(Carver &cv, StWs &w, const StGeo &g) {
     w.item_bucket = cv.take<unsigned>((size_t)g.max_items);
     w.split_slot = cv.take<unsigned>((size_t)g.S + 1);
     w.ditem_off = cv.take<unsigned>((size_t)g.S + 1);
+    w.item_desc = cv.take<uint4>((size_t)g.max_items);
     w.ditem_bucket = cv.take<unsigned>((size_t)g.S + g.Mcap / kDegItem + 1);
     w.scan_part = cv.take<unsigned>(4 * ((size_t)g.S / kScanBlock + 2));
     w.scratch = cv.take<double>((size_t)g.max_split * ((size_t)1 << g.lrow_bits) * (size_t)g.k);
@@ -554,7 +556,11 @@ __global__ void __launch_bounds__(1024) k_st_scan2c(StArgs a) {
         a.ws.split_slot[b] = c[j][3] ? e[3] : 0xffffffffu;
         a.ws.done_deg[b] = 0;
         a.ws.done_emb[b] = 0;
-        for (unsigned i = 0; i < c[j][1]; ++i) a.ws.item_bucket[e[1] + i] = b;
+        for (unsigned i = 0; i < c[j][1]; ++i) {
+            a.ws.item_bucket[e[1] + i] = b;
+            const unsigned q0 = e[0] + i * a.C;
+            a.ws.item_desc[e[1] + i] = make_uint4(b, q0, min(e[0] + c[j][0], q0 + a.C), c[j][1]);
+        }
         for (unsigned i = 0; i < c[j][2]; ++i) a.ws.ditem_bucket[e[2] + i] = b;
         for (int q = 0; q < 4; ++q) e[q] += c[j][q];
     }
@@ -766,7 +772,8 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
 //   pass B: one contiguous streaming store of the tile, each element times its
 //     row factor (rows r0 .. r0+nrows are adjacent in Z).
 template <bool OUT32, int NT>
-__device__ __forceinline__ void tile_epilogue(const StArgs &a, double *zt, double *fac, int64_t r0, int nrows) {
+__device__ __forceinline__ void tile_epilogue(const StArgs &a, double *zt, double *fac, const double2 *drec,
+                                              int64_t r0, int nrows) {
     const int K = a.k;
     const unsigned flags = a.flags;
     // lanes per row: a power of two near K / 8, at most 32
@@ -784,13 +791,15 @@ __device__ __forceinline__ void tile_epilogue(const StArgs &a, double *zt, doubl
         double *row = zt + (size_t)l * K;
         double s_r = 1.0;
         if (live) {
-            if (flags & GEE_LAPLACIAN) s_r = a.ws.scale[r];
+            // the row's scale (fac) and record (drec) were loaded when the item started
+            if (flags & GEE_LAPLACIAN) s_r = fac[l];
             if ((flags & GEE_DIAGONAL) && sub == 0) {
-                const double2 rc = a.ws.rec[r];
+                const double2 rc = drec[l];
                 const int y = rec_label(rc);
                 if (y >= 0) row[y] += rc.y;
             }
         }
+        (void)r;
         __syncwarp();
         double f = s_r;
         if (flags & GEE_CORRELATION) {
@@ -816,6 +825,7 @@ __device__ __forceinline__ void tile_epilogue(const StArgs &a, double *zt, doubl
                 }
             }
         }
+        __syncwarp();
         if (live && sub == 0) fac[l] = f;
     }
     __syncthreads();
@@ -862,7 +872,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
     const int R = 1 << a.lrow_bits;
     const int K = a.k;
     double *fac = zt + (size_t)R * K;
-    double2 *stage = reinterpret_cast<double2 *>(fac + R);  // [2][U][NT]
+    double2 *drec = reinterpret_cast<double2 *>(fac + R);  // [R] the rows' own records (A+I term)
+    double2 *stage = drec + R;                             // [2][U][NT]
     const unsigned n_items = a.ws.ctl[kCtlItems];
     const unsigned cmask = (1u << a.col_bits) - 1u;
     const int cb = a.col_bits;
@@ -895,18 +906,13 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
             if (y >= 0) atomicAdd(zt + (kk[u] >> cb) * K + y, x[u] * rc.y);
         }
     };
-    auto grab = [&](int slot) {  // thread 0: the next work item into s_meta[slot]
+    auto grab = [&](int slot) {  // thread 0: the next work item's descriptor into s_meta[slot]
         const unsigned item = atomicAdd(a.ws.ctl + kCtlWork + 1, 1u);
-        if (item >= n_items) {
-            s_meta[slot][0] = 0xffffffffu;
-            return;
-        }
-        unsigned b, p0, p1, ni;
-        item_range(a, item, b, p0, p1, ni);
-        s_meta[slot][0] = b;
-        s_meta[slot][1] = p0;
-        s_meta[slot][2] = p1;
-        s_meta[slot][3] = ni;
+        const uint4 d = item < n_items ? a.ws.item_desc[item] : make_uint4(0xffffffffu, 0, 0, 0);
+        s_meta[slot][0] = d.x;
+        s_meta[slot][1] = d.y;
+        s_meta[slot][2] = d.z;
+        s_meta[slot][3] = d.w;
     };
     {
         double2 *z2 = reinterpret_cast<double2 *>(zt);
@@ -915,42 +921,48 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
     if (threadIdx.x == 0) grab(0);
     __syncthreads();
     int cur = 0;
-    if (s_meta[0][0] != 0xffffffffu) issue(s_meta[0][1], s_meta[0][2], kA, xA, 0);
+    if (s_meta[0][0] != 0xffffffffu) {
+        issue(s_meta[0][1], s_meta[0][2], kA, xA, 0);
+        if (s_meta[0][1] + step < s_meta[0][2]) issue(s_meta[0][1] + step, s_meta[0][2], kB, xB, 1);
+    }
     for (;;) {
         const unsigned b = s_meta[cur][0];
         if (b == 0xffffffffu) break;
         const unsigned p0 = s_meta[cur][1], p1 = s_meta[cur][2], nitems = s_meta[cur][3];
-        // the next item's metadata loads overlap this item's work
+        // the next item's descriptor loads overlap this item's work
         if (threadIdx.x == 0) grab(cur ^ 1);
         const int64_t r0 = (int64_t)b << a.lrow_bits;
         const int nrows = (int)min((int64_t)R, a.N - r0);
         const int tsz = nrows * K;
-        // stage A of [p0, p0 + step) was issued before this iteration
+        // per-row data of the epilogue, loaded now so its latency hides under the accumulation
+        for (int l = threadIdx.x; l < nrows; l += NT) {
+            if (a.flags & GEE_LAPLACIAN) fac[l] = a.ws.scale[r0 + l];
+            if (a.flags & GEE_DIAGONAL) drec[l] = a.ws.rec[r0 + l];
+        }
+        // stages A = [p0, p0 + step) and B = [p0 + step, p0 + 2 step) were issued
+        // before this iteration; each consumed stage is refilled two steps ahead
         for (unsigned base = p0; base < p1; base += 2 * step) {
-            const bool hb = base + step < p1;
-            if (hb) {
-                issue(base + step, p1, kB, xB, 1);
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
-            }
+            const bool hb = base + step < p1, ha = base + 2 * step < p1;
+            if (hb) cp_async_wait<1>();
+            else cp_async_wait<0>();
             consume(kA, xA, 0);
+            if (ha) issue(base + 2 * step, p1, kA, xA, 0);
             if (hb) {
-                const bool ha = base + 2 * step < p1;
-                if (ha) {
-                    issue(base + 2 * step, p1, kA, xA, 0);
-                    cp_async_wait<1>();
-                } else {
-                    cp_async_wait<0>();
-                }
+                if (ha) cp_async_wait<1>();
+                else cp_async_wait<0>();
                 consume(kB, xB, 1);
+                if (base + 3 * step < p1) issue(base + 3 * step, p1, kB, xB, 1);
             }
         }
         __syncthreads();  // tile complete; s_meta[cur ^ 1] visible
-        // the next item's first stage flies while this tile is finished
-        if (s_meta[cur ^ 1][0] != 0xffffffffu) issue(s_meta[cur ^ 1][1], s_meta[cur ^ 1][2], kA, xA, 0);
+        // the next item's first two stages fly while this tile is finished
+        if (s_meta[cur ^ 1][0] != 0xffffffffu) {
+            const unsigned q0 = s_meta[cur ^ 1][1], q1 = s_meta[cur ^ 1][2];
+            issue(q0, q1, kA, xA, 0);
+            if (q0 + step < q1) issue(q0 + step, q1, kB, xB, 1);
+        }
         if (nitems == 1) {
-            tile_epilogue<OUT32, NT>(a, zt, fac, r0, nrows);
+            tile_epilogue<OUT32, NT>(a, zt, fac, drec, r0, nrows);
         } else {
             double *zs = a.ws.scratch + (size_t)a.ws.split_slot[b] * ((size_t)R * K);
             for (int i = threadIdx.x; i < tsz; i += NT) {
@@ -969,7 +981,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
                 __threadfence();
                 for (int i = threadIdx.x; i < tsz; i += NT) zt[i] = __ldcg(zs + i);
                 __syncthreads();
-                tile_epilogue<OUT32, NT>(a, zt, fac, r0, nrows);
+                tile_epilogue<OUT32, NT>(a, zt, fac, drec, r0, nrows);
             }
         }
         __syncthreads();  // tile zeroed, s_meta[cur] free
@@ -987,8 +999,8 @@ template <int WT, int NT>
 int launch_embed(const StGeo &g, const StArgs &a, bool out32, cudaStream_t st) {
     static PerDevice attr;
     const size_t smem =
-        sizeof(double) * ((size_t)1 << g.lrow_bits) * ((size_t)g.k + 1) + emb_stage_bytes(NT);
-    const size_t smax = kZTileMax + 8 * 512 + emb_stage_bytes(NT);
+        sizeof(double) * ((size_t)1 << g.lrow_bits) * ((size_t)g.k + 3) + emb_stage_bytes(NT);
+    const size_t smax = kZTileMax + 24 * 512 + emb_stage_bytes(NT);
     if (!attr.done()) {
         int rc;
         if ((rc = set_smem(k_st_embed<WT, false, NT>, smax))) return rc;
@@ -1061,7 +1073,7 @@ int set_stream_tile_kb(int v) {
 
 int set_stream_embed_nt(int v) {
     const int old = t_emb_nt;
-    t_emb_nt = (v == 128 || v == 512) ? v : 256;
+    t_emb_nt = (v == 256 || v == 512) ? v : 128;
     return old;
 }
 
