@@ -253,6 +253,38 @@ int gee_gen_sbm_count(uint64_t key, int64_t n_nodes, const int64_t *labels, uint
 int gee_gen_sbm_fill(uint64_t key, int64_t n_nodes, const int64_t *labels, uint32_t thr_in, uint32_t thr_out,
                      const int64_t *offsets, int64_t *rows, int64_t *cols, void *stream);
 
+/* Device text parsers (replace graph_io.parse_edge_list /
+ * parse_labels, graph_io.py:95-257).  `text` is the file's bytes in device
+ * memory.  Lines end at \n, \r\n or \r; each is stripped; blank lines and
+ * '#' comments are skipped; the delimiter (0 auto: comma when the first data
+ * line holds one, 1 whitespace, 2 comma) splits the fields; tokens follow
+ * Python's int() / float().  Errors: info[2] = (1-based line << 8 | code) of
+ * the first failing line, -1 if none; the host raises ParseError(line).
+ *   gee_text_count_lines   *n_breaks; parsers take n_lines = n_breaks + 1
+ *   gee_parse_edges        (i, j, w) of the data lines in file order into
+ *                          rows / cols / w (capacity n_lines), shifted by the
+ *                          index base; fallback[slot] = 1 where the weight has
+ *                          more than 19 significant digits (host converts),
+ *                          slot_line (may be NULL) the file line of each slot;
+ *                          info: [0] edges, [1] max index, [2] error,
+ *                          [3] fallbacks, [4] first data line
+ *   gee_parse_labels       per data line: node (-1 in per-line form) and
+ *                          label, slot_line = its file line
+ *   gee_labels_assign      pair form: values[nv] (-1 unmentioned), the
+ *                          conflicting-duplicate error into *err_word */
+int gee_text_workspace(int64_t nbytes, int64_t n_lines, size_t *ws_bytes);
+int gee_text_count_lines(const char *text, int64_t nbytes, int64_t *n_breaks, void *ws, size_t ws_bytes,
+                         void *stream);
+int gee_parse_edges(const char *text, int64_t nbytes, int64_t n_lines, int delim_mode, int index_base,
+                    double default_weight, int64_t n_nodes, int64_t *line_start, int64_t *rows, int64_t *cols,
+                    double *w, unsigned char *fallback, int64_t *slot_line, int64_t *info, void *ws,
+                    size_t ws_bytes, void *stream);
+int gee_parse_labels(const char *text, int64_t nbytes, int64_t n_lines, int delim_mode, int index_base,
+                     int64_t n_nodes, int64_t *line_start, int64_t *node, int64_t *lab, int64_t *slot_line,
+                     int64_t *info, void *ws, size_t ws_bytes, void *stream);
+int gee_labels_assign(const int64_t *node, const int64_t *lab, const int64_t *slot_line, int64_t m, int64_t nv,
+                      uint64_t *first, int64_t *values, uint64_t *err_word, void *stream);
+
 /* Launch statistics: number of kernels this thread launched through the
  * library since the last reset (for bench.py's gpu_launches). */
 uint64_t gee_launch_count(void);

@@ -69,6 +69,13 @@ SIGNATURES = {
     "gee_gen_pairs": (_int, [ctypes.c_uint64, _i64, _i64, _i64, _vp, _vp]),
     "gee_gen_sbm_count": (_int, [ctypes.c_uint64, _i64, _vp, _u32, _u32, _vp, _vp]),
     "gee_gen_sbm_fill": (_int, [ctypes.c_uint64, _i64, _vp, _u32, _u32, _vp, _vp, _vp, _vp]),
+    "gee_text_workspace": (_int, [_i64, _i64, _szp]),
+    "gee_text_count_lines": (_int, [_vp, _i64, _vp, _vp, ctypes.c_size_t, _vp]),
+    "gee_parse_edges": (_int, [_vp, _i64, _i64, _int, _int, ctypes.c_double, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
+                               _vp, _vp, ctypes.c_size_t, _vp]),
+    "gee_parse_labels": (_int, [_vp, _i64, _i64, _int, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t,
+                                _vp]),
+    "gee_labels_assign": (_int, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
     "gee_launch_count": (ctypes.c_uint64, []),
     "gee_reset_launch_count": (None, []),
     "gee_profile_start": (_int, [_vp]),
