@@ -19,6 +19,7 @@ _time_pipeline does (cli.py:170-180); the file parsing stays outside.
 from __future__ import annotations
 
 import argparse
+import pathlib
 import sys
 import time
 from dataclasses import dataclass, field
@@ -26,7 +27,7 @@ from pathlib import Path
 
 import numpy as np
 
-from . import formats as F
+from . import textio as T
 from .errors import GpuUnavailableError, NumericalDomainError, ParseError, StructuralError
 
 EXIT_OK, EXIT_INTERNAL, EXIT_USAGE, EXIT_PARSE, EXIT_SHAPE = 0, 1, 2, 3, 4
@@ -67,15 +68,13 @@ def _tf(flag: bool) -> str:
 
 
 def _read_edges(args):
-    opts = F.ParseOptions(index_base=1 if args.one_based else 0, directed=args.directed)
-    with open(args.edges, encoding="utf-8") as f:
-        return F.parse_edge_list(f, opts, n_nodes=args.nodes)
+    opts = T.ParseOptions(index_base=1 if args.one_based else 0, directed=args.directed)
+    return T.parse_edge_list(pathlib.Path(args.edges), opts, n_nodes=args.nodes)
 
 
 def _read_labels(args, n_nodes):
-    opts = F.ParseOptions(index_base=1 if args.one_based else 0)
-    with open(args.labels, encoding="utf-8") as f:
-        labels = F.parse_labels(f, opts, k_classes=args.classes, n_nodes=n_nodes)
+    opts = T.ParseOptions(index_base=1 if args.one_based else 0)
+    labels = T.parse_labels(pathlib.Path(args.labels), opts, k_classes=args.classes, n_nodes=n_nodes)
     if len(labels) != n_nodes:
         raise StructuralError(f"label file has {len(labels)} entries for {n_nodes} nodes")
     return labels
@@ -157,13 +156,29 @@ def cmd_embed(args) -> int:
     z = np.asarray(encode(edges, labels, opts))
     elapsed = time.perf_counter() - t0
     if args.out == "-":
-        F.write_embedding(z, sys.stdout)
+        T.write_embedding(z, sys.stdout)
     else:
         with open(args.out, "w", encoding="utf-8", newline="") as f:
-            F.write_embedding(z, f)
-    print(f"nodes={edges.n_nodes} edges={edges.n_edges} classes={labels.k_classes} "
-          f"seconds={elapsed:.6f}", file=sys.stderr)
+            T.write_embedding(z, f)
+    # the reference's summary line (cli.py:115-125): stored entries of the CSR
+    # and the undirected edge density 2|E| / (n (n - 1)) of distinct pairs
+    nnz = edges.to_csr().nnz
+    if edges.n_nodes >= 2:
+        density = f"{2.0 * _distinct_pairs(edges) / (edges.n_nodes * (edges.n_nodes - 1.0)):#.5g}"
+    else:
+        density = "n/a"
+    print(f"[embed] nodes={edges.n_nodes} edges={edges.n_edges} classes={labels.k_classes} nnz={nnz} "
+          f"density={density} elapsed={elapsed:.6f}s", file=sys.stderr)
     return EXIT_OK
+
+
+def _distinct_pairs(edges) -> int:
+    """Distinct unordered pairs {i, j}, i != j (graph_io.count_undirected_edges), on the device."""
+    import torch
+    e = edges.to_device()
+    lo, hi = torch.minimum(e.rows, e.cols), torch.maximum(e.rows, e.cols)
+    keep = lo != hi
+    return int(torch.unique(lo[keep] * e.n_nodes + hi[keep]).numel()) if bool(keep.any()) else 0
 
 
 def build_parser():
@@ -197,7 +212,10 @@ def build_parser():
 
 
 def main(argv=None) -> int:
-    args = build_parser().parse_args(argv)
+    try:
+        args = build_parser().parse_args(argv)
+    except SystemExit as exc:  # cli.py:333-336: usage errors exit 2, --help 0
+        return EXIT_USAGE if exc.code else EXIT_OK
     try:
         return args.func(args)
     except ParseError as e:
@@ -206,7 +224,10 @@ def main(argv=None) -> int:
     except (StructuralError, NumericalDomainError) as e:
         print(f"error: {e}", file=sys.stderr)
         return EXIT_SHAPE
-    except (OSError, GpuUnavailableError) as e:
+    except OSError as e:  # cli.py:343-345
+        print(f"error: {e}", file=sys.stderr)
+        return EXIT_PARSE
+    except GpuUnavailableError as e:
         print(f"error: {e}", file=sys.stderr)
         return EXIT_INTERNAL
 
