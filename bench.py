@@ -467,9 +467,10 @@ def run_b200(args):
     e2e = None
     if not args.no_e2e:
         rh, ch, wh, lh = host_arrays(c)
-        h2d, d2h = enc.attach_host(rh, ch, None if w is None else wh, lh)
+        h2d, d2h = enc.attach_host(rh, ch, None if w is None else wh, lh, depth=2)
         enc.run_host(check=True)
         torch.cuda.synchronize()
+        # (1) the synchronous call: copies in, pipeline, Z out, one step at a time
         es = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         ee = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         for i in range(args.steps):
@@ -477,9 +478,32 @@ def run_b200(args):
             enc.run_host(check=False)
             ee[i].record(stream)
         torch.cuda.synchronize()
-        e2e_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(es, ee))
-        e2e = {"value": e / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+        serial_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(es, ee))
+        # (2) a stream of encodes through run_host_async: step i's Z download
+        # overlaps step i+1's input upload (full-duplex PCIe); every step still
+        # copies its inputs up and its Z down inside the timed region
+        for _ in range(2):
+            enc.run_host_async()
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        enc._s_in.wait_stream(stream)
+        last = None
+        for i in range(args.steps):
+            _, last = enc.run_host_async()
+        enc._s_out.wait_event(last)
+        t1.record(enc._s_out)
+        torch.cuda.synchronize()
+        pipe_ms = t0.elapsed_time(t1) / args.steps
+        _device_err2 = int(enc.err.item())
+        e2e = {"value": e / (pipe_ms * 1e-3), "unit": UNIT, "ms_per_step": pipe_ms,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "api": "GeeEncoder.run_host_async (pinned host edge list in, pinned host Z out, "
+                      "double-buffered: step i's D2H overlaps step i+1's H2D)",
+               "serial": {"value": e / (serial_ms * 1e-3), "ms_per_step": serial_ms,
+                          "api": "GeeEncoder.run_host (copies in, pipeline, copy out; one step at a time)"},
+               "device_error_bits": _device_err2}
 
     cpu = None
     if not args.no_cpu_baseline:

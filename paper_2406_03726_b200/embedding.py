@@ -165,32 +165,69 @@ class GeeEncoder:
         self.graph.replay()
         return self.z
 
-    def attach_host(self, rows, cols, weights, labels):
-        """Register host inputs for run_host(): pinned staging copies plus
-        device buffers of the same shapes and a pinned output.  Returns
-        (h2d_bytes, d2h_bytes) per run."""
+    def attach_host(self, rows, cols, weights, labels, *, depth: int = 2):
+        """Register host inputs for run_host() / run_host_async(): pinned
+        staging copies, `depth` sets of device input buffers and outputs, and
+        pinned host outputs.  Returns (h2d_bytes, d2h_bytes) per run."""
         def pin(a):
             t = torch.from_numpy(np.ascontiguousarray(a)) if isinstance(a, np.ndarray) else a.cpu()
             return t.pin_memory()
         self._h = [pin(rows), pin(cols), None if weights is None else pin(weights), pin(labels)]
-        self._d = [None if h is None else torch.empty_like(h, device=self.dev) for h in self._h]
-        self._zh = torch.empty((self.n, self.k), dtype=self.dtype).pin_memory()
+        self._depth = max(1, int(depth))
+        self._d = [[None if h is None else torch.empty_like(h, device=self.dev) for h in self._h]
+                   for _ in range(self._depth)]
+        self._zd = [self.z] + [torch.empty_like(self.z) for _ in range(self._depth - 1)]
+        self._zhs = [torch.empty((self.n, self.k), dtype=self.dtype).pin_memory() for _ in range(self._depth)]
+        self._zh = self._zhs[0]
+        self._s_in = torch.cuda.Stream(self.dev)
+        self._s_out = torch.cuda.Stream(self.dev)
+        mk = lambda: [torch.cuda.Event() for _ in range(self._depth)]  # noqa: E731
+        self._ev_in_free, self._ev_h2d, self._ev_comp, self._ev_out_free = mk(), mk(), mk(), mk()
+        self._step = 0
         h2d = sum(h.numel() * h.element_size() for h in self._h if h is not None)
         return h2d, self._zh.numel() * self._zh.element_size()
 
     def run_host(self, *, check: bool = True) -> torch.Tensor:
         """Host -> device copies, the fused pipeline, device -> host Z; all
-        stream-ordered on the current stream (the end-to-end call)."""
-        for h, d in zip(self._h, self._d):
+        stream-ordered on the current stream (the synchronous end-to-end call)."""
+        d = self._d[0]
+        for h, x in zip(self._h, d):
             if h is not None:
-                d.copy_(h, non_blocking=True)
-        rows, cols, w, lab = self._d
+                x.copy_(h, non_blocking=True)
+        rows, cols, w, lab = d
         z = self.run(rows, cols, w, lab, check=False)
         self._zh.copy_(z, non_blocking=True)
         if check:
             torch.cuda.current_stream().synchronize()
             _device.check_device_errors(self.err, "encode")
         return self._zh
+
+    def run_host_async(self):
+        """One end-to-end step for a stream of encodes: its inputs go up on a
+        copy stream while the previous step computes, its Z comes down on a
+        second copy stream while the next step's inputs go up (PCIe is full
+        duplex).  Buffers rotate over `depth` slots.  Returns (host Z, event):
+        the host Z is valid once the event has completed."""
+        b = self._step % self._depth
+        self._step += 1
+        cs = torch.cuda.current_stream(self.dev)
+        with torch.cuda.stream(self._s_in):
+            self._s_in.wait_event(self._ev_in_free[b])  # the previous compute on slot b read its inputs
+            for h, x in zip(self._h, self._d[b]):
+                if h is not None:
+                    x.copy_(h, non_blocking=True)
+            self._ev_h2d[b].record(self._s_in)
+        cs.wait_event(self._ev_h2d[b])
+        cs.wait_event(self._ev_out_free[b])  # slot b's previous Z has reached the host
+        rows, cols, w, lab = self._d[b]
+        self.run(rows, cols, w, lab, check=False, out=self._zd[b])
+        self._ev_in_free[b].record(cs)
+        self._ev_comp[b].record(cs)
+        with torch.cuda.stream(self._s_out):
+            self._s_out.wait_event(self._ev_comp[b])
+            self._zhs[b].copy_(self._zd[b], non_blocking=True)
+            self._ev_out_free[b].record(self._s_out)
+        return self._zhs[b], self._ev_out_free[b]
 
 
 def _check_shapes(n_rows, n_cols, labels):
