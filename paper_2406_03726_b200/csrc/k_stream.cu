@@ -188,7 +188,8 @@ struct StArgs {
     unsigned flags;
     int lrow_bits, d2_bits, d1_shift, col_bits;
     unsigned S, C;
-    int variant;  // debug A/B (stream mode >= 16): 1 no shared atomics, 2 no gathers
+    int variant;  // debug A/B (stream mode >= 16)
+    int deg_copies;  // partial-sum copies per row in the degree kernel (power of two)
     unsigned long long magic;  // ceil(2^32 / K): row of a tile element by multiply-shift
     StWs ws;
     void *z;  // f64, or f32 under GEE_FP32
@@ -338,20 +339,25 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part1(StArgs a) {
     const int64_t tile_edges = (int64_t)EPT * kStNT;
     const int64_t ntiles = (a.E + tile_edges - 1) / tile_edges;
     int errbits = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    // software pipeline: the next tile's edges are loaded as soon as this
+    // tile's entries sit in shared memory, and fly during the write-out
+    long long r[EPT], c[EPT];
+    WTy wv[EPT];
+    auto load_tile = [&](int64_t tile) {
         const int64_t e0 = tile * tile_edges;
-        long long r[EPT], c[EPT];
-        WTy wv[EPT];
 #pragma unroll
         for (int u = 0; u < EPT; ++u) {
             const int64_t i = e0 + (int64_t)u * kStNT + threadIdx.x;
             r[u] = -2;
-            if (i < a.E) {
+            if (tile < ntiles && i < a.E) {
                 r[u] = __ldcs(reinterpret_cast<const long long *>(a.rows) + i);
                 c[u] = __ldcs(reinterpret_cast<const long long *>(a.cols) + i);
                 if constexpr (WT != GEE_W_UNIT) wv[u] = __ldcs(reinterpret_cast<const WTy *>(a.w) + i);
             }
         }
+    };
+    load_tile(blockIdx.x);
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         if (threadIdx.x < 256) cnt[threadIdx.x] = 0;
         __syncthreads();
         unsigned long long key[EPT][DIR ? 1 : 2];
@@ -408,6 +414,7 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part1(StArgs a) {
                 if constexpr (WT != GEE_W_UNIT) sw[p] = wv[u];
             }
         }
+        load_tile(tile + gridDim.x);
         __syncthreads();
         // coalesced runs out
         for (unsigned t = threadIdx.x; t < total; t += kStNT) {
@@ -582,24 +589,39 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part2(StArgs a) {
     const unsigned ntiles = (M + kStTile - 1) / kStTile;
     const unsigned rmask = (1u << a.lrow_bits) - 1u;
     constexpr int PER = kStTile / kStNT;
-    for (unsigned tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        for (int i = threadIdx.x; i < kStWin; i += kStNT) cnt[i] = 0;
-        __syncthreads();
+    // software pipeline: the next tile's keys and weights are loaded into
+    // registers as soon as this tile's are staged in shared memory, so they
+    // fly while this tile is written out
+    unsigned long long kk[PER];
+    WTy wv[PER];
+    auto load_tile = [&](unsigned tile) {
         const unsigned p0 = tile * kStTile;
-        const unsigned sub0 = (unsigned)((a.ws.keys1[p0] >> 32) >> a.d1_shift) << a.d2_bits;
-        uint32_t k2[PER];
-        unsigned rel[PER], rk[PER];
-        WTy wv[PER];
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
             const unsigned p = p0 + u * kStNT + threadIdx.x;
+            kk[u] = ~0ull;
+            if (tile < ntiles && p < M) {
+                kk[u] = __ldcs(a.ws.keys1 + p);
+                if constexpr (WT != GEE_W_UNIT) wv[u] = __ldcs(reinterpret_cast<const WTy *>(a.ws.w1) + p);
+            }
+        }
+    };
+    __shared__ unsigned s_sub0;
+    load_tile(blockIdx.x);
+    for (unsigned tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int i = threadIdx.x; i < kStWin; i += kStNT) cnt[i] = 0;
+        if (threadIdx.x == 0) s_sub0 = (unsigned)((kk[0] >> 32) >> a.d1_shift) << a.d2_bits;  // entry p0
+        __syncthreads();
+        const unsigned sub0 = s_sub0;
+        uint32_t k2[PER];
+        unsigned rel[PER], rk[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
             rel[u] = 0xffffffffu;
-            if (p < M) {
-                const unsigned long long kk = a.ws.keys1[p];
-                const unsigned r = (unsigned)(kk >> 32), c = (unsigned)kk;
+            if (kk[u] != ~0ull) {
+                const unsigned r = (unsigned)(kk[u] >> 32), c = (unsigned)kk[u];
                 const unsigned sub = r >> a.lrow_bits;
                 k2[u] = ((r & rmask) << a.col_bits) | c;
-                if constexpr (WT != GEE_W_UNIT) wv[u] = reinterpret_cast<const WTy *>(a.ws.w1)[p];
                 const unsigned rl = sub - sub0;
                 if (rl < kStWin) {
                     rel[u] = rl;
@@ -613,10 +635,20 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part2(StArgs a) {
             }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < kStWin; i += kStNT) {
-            const unsigned c = cnt[i];
-            gbase[i] = c ? atomicAdd(a.ws.cur2 + sub0 + i, c) : 0u;
-            off[i] = c;
+        {
+            // all of this thread's reservations in flight at once
+            constexpr int PB = kStWin / kStNT;
+            unsigned cc[PB], gb[PB];
+#pragma unroll
+            for (int j = 0; j < PB; ++j) cc[j] = cnt[threadIdx.x + j * kStNT];
+#pragma unroll
+            for (int j = 0; j < PB; ++j)
+                gb[j] = cc[j] ? atomicAdd(a.ws.cur2 + sub0 + threadIdx.x + j * kStNT, cc[j]) : 0u;
+#pragma unroll
+            for (int j = 0; j < PB; ++j) {
+                gbase[threadIdx.x + j * kStNT] = gb[j];
+                off[threadIdx.x + j * kStNT] = cc[j];
+            }
         }
         __syncthreads();
         block_scan_bins<kStNT>(off, kStWin, red);
@@ -630,6 +662,7 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part2(StArgs a) {
                 if constexpr (WT != GEE_W_UNIT) sw[p] = wv[u];
             }
         }
+        load_tile(tile + gridDim.x);
         __syncthreads();
         // coalesced runs out
         for (unsigned t = threadIdx.x; t < total; t += kStNT) {
@@ -707,13 +740,18 @@ __device__ __forceinline__ void zero_scratch(const StArgs &a, unsigned b, int nr
 // (and clears the bucket's embed scratch tile when the embed splits it too).
 template <int WT>
 __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
-    extern __shared__ double wdeg[];  // [kDegNT / 32][R]
+    extern __shared__ double wdeg[];  // [kDegNT / 32][R][copies]
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int R = 1 << a.lrow_bits;
     const bool lap = (a.flags & GEE_LAPLACIAN) != 0;
     const unsigned n_items = a.ws.ctl[kCtlDItems];
     const int cb = a.col_bits;
-    double *mine = wdeg + (size_t)wid * R;
+    // `copies` interleaved partial sums per row (lane & (copies - 1) picks one):
+    // skewed graphs put many lanes of a warp on the same row, and every lane
+    // colliding on one shared f64 word costs a CAS retry
+    const int copies = a.deg_copies;
+    double *mine = wdeg + (size_t)wid * R * copies;
+    const int cp = lane & (copies - 1);
     constexpr int U = 8;
     for (unsigned item = (blockIdx.x * kDegNT + threadIdx.x) >> 5; item < n_items;
          item += (gridDim.x * kDegNT) >> 5) {
@@ -725,7 +763,7 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
         const int64_t r0 = (int64_t)b << a.lrow_bits;
         const int nrows = (int)min((int64_t)R, a.N - r0);
         if (lap) {
-            for (int l = lane; l < R; l += 32) mine[l] = 0.0;
+            for (int l = lane; l < R * copies; l += 32) mine[l] = 0.0;
             __syncwarp();
             unsigned p = p0 + lane;
             for (; p + (U - 1) * 32 < p1; p += U * 32) {
@@ -736,17 +774,23 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) x[u] = entry_w<WT>(a, p + u * 32);
 #pragma unroll
-                for (int u = 0; u < U; ++u) atomicAdd(mine + l[u], x[u]);
+                for (int u = 0; u < U; ++u) atomicAdd(mine + l[u] * copies + cp, x[u]);
             }
-            for (; p < p1; p += 32) atomicAdd(mine + (__ldcs(a.ws.keys2 + p) >> cb), entry_w<WT>(a, p));
+            for (; p < p1; p += 32) atomicAdd(mine + (__ldcs(a.ws.keys2 + p) >> cb) * copies + cp, entry_w<WT>(a, p));
+            __syncwarp();
+            for (int l = lane; l < R; l += 32) {
+                double d = 0.0;
+                for (int c = 0; c < copies; ++c) d += mine[l * copies + c];
+                mine[l * copies] = d;
+            }
             __syncwarp();
         }
         if (nitems == 1) {
-            for (int l = lane; l < nrows; l += 32) finish_node(a, r0 + l, lap ? mine[l] : 0.0);
+            for (int l = lane; l < nrows; l += 32) finish_node(a, r0 + l, lap ? mine[l * copies] : 0.0);
         } else {
             if (lap)
                 for (int l = lane; l < nrows; l += 32)
-                    if (mine[l] != 0.0) atomicAdd(a.ws.deg + r0 + l, mine[l]);
+                    if (mine[l * copies] != 0.0) atomicAdd(a.ws.deg + r0 + l, mine[l * copies]);
             __threadfence();
             __syncwarp();
             unsigned last = 0;
@@ -1021,13 +1065,13 @@ int run_stream(const StGeo &g, StArgs &a, cudaStream_t st) {
     static PerDevice attr;
     const size_t p1_smem = (size_t)(8 + WTraits<WT>::bytes) * kStTile;
     const size_t p2_smem = (size_t)(4 + WTraits<WT>::bytes + 2) * kStTile + 3 * sizeof(unsigned) * kStWin;
-    const size_t deg_smem = sizeof(double) * (kDegNT / 32) * ((size_t)1 << g.lrow_bits);
+    const size_t deg_smem = sizeof(double) * (kDegNT / 32) * ((size_t)1 << g.lrow_bits) * (size_t)a.deg_copies;
     if (!attr.done()) {
         int rc;
         if ((rc = set_smem(k_st_part1<WT, true>, p1_smem))) return rc;
         if ((rc = set_smem(k_st_part1<WT, false>, p1_smem))) return rc;
         if ((rc = set_smem(k_st_part2<WT>, p2_smem))) return rc;
-        if ((rc = set_smem(k_st_degree<WT>, sizeof(double) * (kDegNT / 32) * ((size_t)1 << kLrowMax)))) return rc;
+        if ((rc = set_smem(k_st_degree<WT>, sizeof(double) * (kDegNT / 32) * 512))) return rc;
         attr.mark();
     }
     const int sms = num_sms();
@@ -1129,6 +1173,8 @@ int stream_encode(const int64_t *rows, const int64_t *cols, const void *w, int w
     a.S = g.S;
     a.C = g.C;
     a.variant = t_stream_mode >= 16 ? t_stream_mode - 16 : 0;
+    // 8 interleaved copies while the per-warp slice stays <= 4 KB (R <= 64), fewer for larger R
+    a.deg_copies = g.lrow_bits <= 6 ? 8 : g.lrow_bits <= 7 ? 4 : g.lrow_bits <= 8 ? 2 : 1;
     a.magic = (0x100000000ull + (unsigned)k - 1) / (unsigned)k;
     a.ws = W;
     a.z = z;
