@@ -44,6 +44,8 @@
 // Every pass is a coalesced stream; the only scattered traffic is the node
 // record gather (L2-resident for skewed graphs) and global atomics at tile /
 // item granularity.  No CUB, no sort library.
+#include <type_traits>
+
 #include "gee_common.cuh"
 
 namespace gee {
@@ -69,6 +71,12 @@ constexpr int kScanBlock = 4096;     // buckets per k_st_scan2 block (1024 threa
 constexpr int kLrowMax = 9;  // at most 512 rows per bucket (per-warp degree copies: 64 KB)
 
 int t_stream_mode = 0;  // debug hook: 0 auto, 1 never, >= 16 embed A/B variant
+
+// debug phase trace of the embed (variant 9): per CTA, clock64 totals of
+// [0] start-of-item wait, [1] accumulation, [2] tile barrier, [3] epilogue,
+// [4] items, [5] entries
+constexpr int kTraceSlots = 8;
+__device__ unsigned long long g_emb_trace[4096 * kTraceSlots];
 size_t t_ztile_bytes = kZTileDefault;  // debug hook: bytes of the R x K Z tile
 
 struct StGeo {
@@ -818,24 +826,25 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
 template <bool OUT32, int NT>
 __device__ __forceinline__ void tile_epilogue(const StArgs &a, double *zt, double *fac, const double2 *drec,
                                               int64_t r0, int nrows) {
+    // One pass per row, L lanes per row (no CTA barrier): the A+I term g_r at
+    // the row's own label, the factor f_r = s_r (Laplacian) times
+    // 1/||s_r z_r|| (correlation; one division per row -- z * (1/nrm) is
+    // within 1 ulp of the reference's z / nrm, embedding.py:140), then the
+    // row leaves as f_r * z_r (each L-lane step writes L adjacent values, whole
+    // 32-byte sectors) and its shared copy is zeroed for the next bucket.
     const int K = a.k;
     const unsigned flags = a.flags;
-    // lanes per row: a power of two near K / 8, at most 32
     const int L = K >= 256 ? 32 : K >= 128 ? 16 : K >= 64 ? 8 : K >= 24 ? 4 : K >= 8 ? 2 : 1;
     const int sub = threadIdx.x % L;
     const unsigned gmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << ((threadIdx.x & 31) & ~(L - 1)));
     const int groups = NT / L;
-    // every group of L lanes takes rows g, g + groups, ...; all lanes of a warp
-    // run the same number of iterations so the shuffles stay converged
-    const int iters = (nrows + groups - 1) / groups;
+    const int iters = (nrows + groups - 1) / groups;  // uniform per warp: shuffles stay converged
     for (int it = 0; it < iters; ++it) {
         const int l = it * groups + (int)threadIdx.x / L;
         const bool live = l < nrows;
-        const int64_t r = r0 + l;
         double *row = zt + (size_t)l * K;
         double s_r = 1.0;
         if (live) {
-            // the row's scale (fac) and record (drec) were loaded when the item started
             if (flags & GEE_LAPLACIAN) s_r = fac[l];
             if ((flags & GEE_DIAGONAL) && sub == 0) {
                 const double2 rc = drec[l];
@@ -843,17 +852,34 @@ __device__ __forceinline__ void tile_epilogue(const StArgs &a, double *zt, doubl
                 if (y >= 0) row[y] += rc.y;
             }
         }
-        (void)r;
         __syncwarp();
         double f = s_r;
         if (flags & GEE_CORRELATION) {
             double ss = 0.0;
             bool fin = true;
             if (live) {
-                for (int c = sub; c < K; c += L) {
-                    const double v = row[c] * s_r;
-                    ss += v * v;
-                    fin &= isfinite(v);
+                // four independent chains (loads first) instead of one serial one
+                double s4[4] = {0.0, 0.0, 0.0, 0.0};
+                int c = sub;
+                for (; c + 3 * L < K; c += 4 * L) {
+                    double v[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v[j] = row[c + j * L];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const double t = v[j] * s_r;
+                        s4[j] += t * t;
+                    }
+                }
+                for (; c < K; c += L) {
+                    const double t = row[c] * s_r;
+                    s4[0] += t * t;
+                }
+                ss = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+                if (!isfinite(ss)) {
+                    // a non-finite element, or finite ones whose squares overflow
+                    // (the reference raises only for the former, embedding.py:137-138)
+                    for (int c2 = sub; c2 < K; c2 += L) fin &= isfinite(row[c2]);
                 }
             }
             for (int o = L >> 1; o > 0; o >>= 1) {
@@ -869,44 +895,47 @@ __device__ __forceinline__ void tile_epilogue(const StArgs &a, double *zt, doubl
                 }
             }
         }
-        __syncwarp();
-        if (live && sub == 0) fac[l] = f;
+        if (live) {
+            const int64_t g0 = (r0 + l) * K;
+            if (OUT32) {
+                float *zg = reinterpret_cast<float *>(a.z) + g0;
+                int c = sub;
+                for (; c + 3 * L < K; c += 4 * L) {
+                    double v[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v[j] = row[c + j * L];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        __stcs(zg + c + j * L, (float)(v[j] * f));
+                        row[c + j * L] = 0.0;
+                    }
+                }
+                for (; c < K; c += L) {
+                    __stcs(zg + c, (float)(row[c] * f));
+                    row[c] = 0.0;
+                }
+            } else {
+                double *zg = reinterpret_cast<double *>(a.z) + g0;
+                int c = sub;
+                for (; c + 3 * L < K; c += 4 * L) {
+                    double v[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v[j] = row[c + j * L];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        __stcs(zg + c + j * L, v[j] * f);
+                        row[c + j * L] = 0.0;
+                    }
+                }
+                for (; c < K; c += L) {
+                    __stcs(zg + c, row[c] * f);
+                    row[c] = 0.0;
+                }
+            }
+        }
     }
-    __syncthreads();
-    const int64_t n = (int64_t)nrows * K;
-    // row of element i: floor(i / K) by a multiply-shift (exact for i < 2^32 / K)
-    const unsigned long long magic = a.magic;
-    if (OUT32) {
-        float *zg = reinterpret_cast<float *>(a.z) + r0 * K;
-        const int64_t n2 = ((uintptr_t)zg & 7) ? 0 : n / 2;
-        for (int64_t i = threadIdx.x; i < n2; i += NT) {
-            const unsigned e0 = (unsigned)(2 * i);
-            const double2 v = reinterpret_cast<const double2 *>(zt)[i];
-            reinterpret_cast<double2 *>(zt)[i] = make_double2(0.0, 0.0);  // ready for the next bucket
-            const double f0 = fac[(e0 * magic) >> 32], f1 = fac[((e0 + 1) * magic) >> 32];
-            __stcs(reinterpret_cast<float2 *>(zg) + i, make_float2((float)(v.x * f0), (float)(v.y * f1)));
-        }
-        for (int64_t i = 2 * n2 + threadIdx.x; i < n; i += NT) {
-            __stcs(zg + i, (float)(zt[i] * fac[((unsigned)i * magic) >> 32]));
-            zt[i] = 0.0;
-        }
-    } else {
-        double *zg = reinterpret_cast<double *>(a.z) + r0 * K;
-        const int64_t n2 = ((uintptr_t)zg & 15) ? 0 : n / 2;
-        for (int64_t i = threadIdx.x; i < n2; i += NT) {
-            const unsigned e0 = (unsigned)(2 * i);
-            const double2 v = reinterpret_cast<const double2 *>(zt)[i];
-            reinterpret_cast<double2 *>(zt)[i] = make_double2(0.0, 0.0);  // ready for the next bucket
-            const double f0 = fac[(e0 * magic) >> 32], f1 = fac[((e0 + 1) * magic) >> 32];
-            __stcs(reinterpret_cast<double2 *>(zg) + i, make_double2(v.x * f0, v.y * f1));
-        }
-        for (int64_t i = 2 * n2 + threadIdx.x; i < n; i += NT) {
-            __stcs(zg + i, zt[i] * fac[((unsigned)i * magic) >> 32]);
-            zt[i] = 0.0;
-        }
-    }
+    (void)fac;
 }
-
 
 template <int WT, bool OUT32, int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
@@ -922,32 +951,44 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
     const unsigned cmask = (1u << a.col_bits) - 1u;
     const int cb = a.col_bits;
     const unsigned step = U * NT;
+    // weights stay in their own type until consumed: a float -> double
+    // conversion right after the load would wait for it
+    using XT = typename std::conditional<WT == GEE_W_UNIT, float, typename WTraits<WT>::T>::type;
     uint32_t kA[U], kB[U];
-    double xA[U], xB[U];
+    XT xA[U], xB[U];
     // stage s of this thread: the keys of [base, end) are loaded and their node
     // records requested into the thread's own slots (cp.async, L1 bypassed)
-    auto issue = [&](unsigned base, unsigned end, uint32_t(&kk)[U], double(&x)[U], int s) {
+    // split in two so the key loads can fly before their record requests:
+    // loadk only issues loads, gather needs the keys (waits for them)
+    auto loadk = [&](unsigned base, unsigned end, uint32_t(&kk)[U], XT(&x)[U]) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const unsigned p = base + u * NT + threadIdx.x;
             kk[u] = 0xffffffffu;
             if (p < end) {
                 kk[u] = __ldcs(a.ws.keys2 + p);
-                x[u] = entry_w<WT>(a, p);
+                if constexpr (WT != GEE_W_UNIT) x[u] = __ldcs(reinterpret_cast<const XT *>(a.ws.w2) + p);
             }
         }
+    };
+    auto gather = [&](const uint32_t(&kk)[U], int s) {
 #pragma unroll
         for (int u = 0; u < U; ++u)
             if (kk[u] != 0xffffffffu) cp_async16(stage + (s * U + u) * NT + threadIdx.x, a.ws.rec + (kk[u] & cmask));
         cp_async_commit();
     };
-    auto consume = [&](const uint32_t(&kk)[U], const double(&x)[U], int s) {
+    auto issue = [&](unsigned base, unsigned end, uint32_t(&kk)[U], XT(&x)[U], int s) {
+        loadk(base, end, kk, x);
+        gather(kk, s);
+    };
+    auto consume = [&](const uint32_t(&kk)[U], const XT(&x)[U], int s) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (kk[u] == 0xffffffffu) continue;
             const double2 rc = stage[(s * U + u) * NT + threadIdx.x];
             const int y = rec_label(rc);
-            if (y >= 0) atomicAdd(zt + (kk[u] >> cb) * K + y, x[u] * rc.y);
+            const double xv = WT == GEE_W_UNIT ? 1.0 : (double)x[u];
+            if (y >= 0) atomicAdd(zt + (kk[u] >> cb) * K + y, xv * rc.y);
         }
     };
     auto grab = [&](int slot) {  // thread 0: the next work item's descriptor into s_meta[slot]
@@ -983,6 +1024,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
             if (a.flags & GEE_LAPLACIAN) fac[l] = a.ws.scale[r0 + l];
             if (a.flags & GEE_DIAGONAL) drec[l] = a.ws.rec[r0 + l];
         }
+        const bool trace = a.variant >= 9 && threadIdx.x == 0 && blockIdx.x < 4096;
+        const long long t1 = trace ? clock64() : 0;
         // stages A = [p0, p0 + step) and B = [p0 + step, p0 + 2 step) were issued
         // before this iteration; each consumed stage is refilled two steps ahead
         for (unsigned base = p0; base < p1; base += 2 * step) {
@@ -998,12 +1041,16 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
                 if (base + 3 * step < p1) issue(base + 3 * step, p1, kB, xB, 1);
             }
         }
+        const long long t2 = trace ? clock64() : 0;
         __syncthreads();  // tile complete; s_meta[cur ^ 1] visible
-        // the next item's first two stages fly while this tile is finished
-        if (s_meta[cur ^ 1][0] != 0xffffffffu) {
-            const unsigned q0 = s_meta[cur ^ 1][1], q1 = s_meta[cur ^ 1][2];
-            issue(q0, q1, kA, xA, 0);
-            if (q0 + step < q1) issue(q0 + step, q1, kB, xB, 1);
+        const long long t3 = trace ? clock64() : 0;
+        // the next item's first two stages: keys requested now, their records
+        // once this tile has been finished (the keys land meanwhile)
+        const bool nxt = s_meta[cur ^ 1][0] != 0xffffffffu;
+        const unsigned nq0 = s_meta[cur ^ 1][1], nq1 = s_meta[cur ^ 1][2];
+        if (nxt) {
+            loadk(nq0, nq1, kA, xA);
+            loadk(nq0 + step, nq1, kB, xB);
         }
         if (nitems == 1) {
             tile_epilogue<OUT32, NT>(a, zt, fac, drec, r0, nrows);
@@ -1028,7 +1075,20 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
                 tile_epilogue<OUT32, NT>(a, zt, fac, drec, r0, nrows);
             }
         }
+        if (nxt) {
+            gather(kA, 0);
+            gather(kB, 1);
+        }
         __syncthreads();  // tile zeroed, s_meta[cur] free
+        if (trace) {
+            const long long t4 = clock64();
+            unsigned long long *tr = g_emb_trace + (size_t)blockIdx.x * kTraceSlots;
+            tr[1] += t2 - t1;
+            tr[2] += t3 - t2;
+            tr[3] += t4 - t3;
+            tr[4] += 1;
+            tr[5] += p1 - p0;
+        }
         cur ^= 1;
     }
 }
@@ -1119,6 +1179,14 @@ int set_stream_embed_nt(int v) {
     const int old = t_emb_nt;
     t_emb_nt = (v == 256 || v == 512) ? v : 128;
     return old;
+}
+
+extern "C" int dbg_stream_trace_read(unsigned long long *out, int cap) {
+    const int n = cap < 4096 * kTraceSlots ? cap : 4096 * kTraceSlots;
+    if (cudaMemcpyFromSymbol(out, g_emb_trace, sizeof(unsigned long long) * (size_t)n) != cudaSuccess) return -1;
+    static unsigned long long zero[4096 * kTraceSlots];
+    cudaMemcpyToSymbol(g_emb_trace, zero, sizeof(zero));
+    return n;
 }
 
 int set_stream_mode(int v) {
