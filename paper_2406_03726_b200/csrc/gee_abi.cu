@@ -62,6 +62,7 @@ int inv_counts(const int64_t *counts, int32_t k, double *inv_nk, cudaStream_t st
 int label_hist_pipeline(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_t *counts, double *inv_nk,
                         unsigned *partial, unsigned *done, int32_t *err, cudaStream_t st);
 size_t csr_build_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
+size_t csr_build_workspace_any(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
 bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed, int wt);
 int set_force_buckets(int v);
 int set_embed_flat_bytes(int v);
@@ -161,8 +162,12 @@ static size_t carve_encode(Carver &cv, EncodeWs &w, int64_t E, int64_t n, int32_
     w.col = cv.take<int32_t>((size_t)(M > 0 ? M : 1));
     w.val = cv.take<double>((size_t)(M > 0 ? M : 1));
     w.label_partial = cv.take<unsigned>(label_partial_words(n, k));
-    w.csr_bytes = bitmap_path_ok(wt, E, n, n, directed, k) ? bitmap_workspace(E, n, directed, k)
-                                                         : csr_build_workspace(E, n, n, directed);
+    // every path the arguments allow (the test hooks switch paths after a plan is sized)
+    w.csr_bytes = csr_build_workspace_any(E, n, n, directed);
+    if (wt == GEE_W_UNIT && n >= 1 && n <= bitmap_max_nodes() && k <= 8) {
+        const size_t b = bitmap_workspace(E, n, directed, k);
+        if (b > w.csr_bytes) w.csr_bytes = b;
+    }
     w.csr_ws = cv.take<char>(w.csr_bytes);
     w.emb_bytes = embed_workspace(n, n);
     w.emb_ws = cv.take<char>(w.emb_bytes);

@@ -6,6 +6,15 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cassert>
+
+// Device-side bounds assertions, compiled in by `make CHECKED=1` (the
+// sanitizer substitute: compute-sanitizer is closed on the GPU pool).
+#ifdef GEE_CHECKED
+#define GEE_DASSERT(c) assert(c)
+#else
+#define GEE_DASSERT(c) ((void)0)
+#endif
 
 #include "gee.h"
 

@@ -1101,6 +1101,18 @@ int sort_csr_build(const int64_t *rows, const int64_t *cols, const void *w, int 
                    unsigned **val_mode, int32_t *err, cudaStream_t st);
 
 // the weight type is not known here: room for whichever path csr_build picks
+bool sort_fits(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
+
+// workspace for any assembly path the test hooks may select (the plan's size
+// must not depend on the hook state at query time)
+size_t csr_build_workspace_any(int64_t E, int64_t n_rows, int64_t n_cols, int directed) {
+    size_t need = sort_fits(E, n_rows, n_cols, directed) ? sort_workspace(E, n_rows, n_cols, directed) : 0;
+    Carver cv(nullptr);
+    CsrWs w;
+    const size_t b = carve_csr(cv, w, E, n_rows, directed);
+    return need > b ? need : b;
+}
+
 size_t csr_build_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int directed) {
     size_t need = 0;
     if (sort_path_ok(E, n_rows, n_cols, directed, -1)) need = sort_workspace(E, n_rows, n_cols, directed);

@@ -537,6 +537,14 @@ int set_force_buckets(int v) {
 int force_path() { return t_force_buckets; }
 
 // wt: the graph's weight type, or -1 when unknown (workspace sizing)
+// the radix sort can assemble this list at all (sizes only; no test hook)
+bool sort_fits(int64_t E, int64_t n_rows, int64_t n_cols, int directed) {
+    const int rb = bitlen(n_rows);
+    const int cb = bitlen(n_cols > 1 ? n_cols - 1 : 1);
+    const int64_t Mv = directed ? E : 2 * E;
+    return Mv < ((int64_t)1 << 30) && n_rows > 0 && n_cols <= ((int64_t)1 << 31) && rb + cb <= 64;
+}
+
 bool sort_path_ok(int64_t E, int64_t n_rows, int64_t n_cols, int directed, int wt) {
     if (t_force_buckets == 1) return false;
     const int rb = bitlen(n_rows);  // rows <= n_rows-1 < 2^rb - 1: keys stay below the sentinel

@@ -429,6 +429,7 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part1(StArgs a) {
             const unsigned long long kk = skey[t];
             const unsigned d = (unsigned)((kk >> 32) >> a.d1_shift);
             const unsigned pos = gbase[d] + (t - off[d]);
+            GEE_DASSERT(d < 256 && pos < a.ws.ctl[kCtlBase1 + d + 1] && pos >= a.ws.ctl[kCtlBase1 + d]);
             a.ws.keys1[pos] = kk;
             if constexpr (WT != GEE_W_UNIT) reinterpret_cast<WTy *>(a.ws.w1)[pos] = sw[t];
         }
@@ -637,6 +638,7 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part2(StArgs a) {
                 } else {
                     // a tile spanning more than the window (tiny buckets): direct slot
                     const unsigned pos = atomicAdd(a.ws.cur2 + sub, 1u);
+                    GEE_DASSERT(sub < a.S && pos < a.ws.base2[sub + 1]);
                     a.ws.keys2[pos] = k2[u];
                     if constexpr (WT != GEE_W_UNIT) reinterpret_cast<WTy *>(a.ws.w2)[pos] = wv[u];
                 }
@@ -676,6 +678,7 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part2(StArgs a) {
         for (unsigned t = threadIdx.x; t < total; t += kStNT) {
             const unsigned lo = srel[t];
             const unsigned pos = gbase[lo] + (t - off[lo]);
+            GEE_DASSERT(sub0 + lo < a.S && pos >= a.ws.base2[sub0 + lo] && pos < a.ws.base2[sub0 + lo + 1]);
             a.ws.keys2[pos] = skey[t];
             if constexpr (WT != GEE_W_UNIT) reinterpret_cast<WTy *>(a.ws.w2)[pos] = sw[t];
         }
@@ -784,7 +787,10 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) atomicAdd(mine + l[u] * copies + cp, x[u]);
             }
-            for (; p < p1; p += 32) atomicAdd(mine + (__ldcs(a.ws.keys2 + p) >> cb) * copies + cp, entry_w<WT>(a, p));
+            for (; p < p1; p += 32) {
+                GEE_DASSERT((int)(a.ws.keys2[p] >> cb) < R);
+                atomicAdd(mine + (__ldcs(a.ws.keys2 + p) >> cb) * copies + cp, entry_w<WT>(a, p));
+            }
             __syncwarp();
             for (int l = lane; l < R; l += 32) {
                 double d = 0.0;
@@ -944,9 +950,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
     __shared__ unsigned s_meta[2][4];              // work item {bucket, p0, p1, items of the bucket}
     const int R = 1 << a.lrow_bits;
     const int K = a.k;
-    double *fac = zt + (size_t)R * K;
-    double2 *drec = reinterpret_cast<double2 *>(fac + R);  // [R] the rows' own records (A+I term)
-    double2 *stage = drec + R;                             // [2][U][NT]
+    // 16-byte aligned sections (R * K may be odd)
+    double *fac = zt + (((size_t)R * K + 1) & ~(size_t)1);
+    double2 *drec = reinterpret_cast<double2 *>(fac + ((R + 1) & ~1));  // [R] the rows' own records (A+I term)
+    double2 *stage = drec + R;                                           // [2][U][NT]
     const unsigned n_items = a.ws.ctl[kCtlItems];
     const unsigned cmask = (1u << a.col_bits) - 1u;
     const int cb = a.col_bits;
@@ -988,6 +995,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
             const double2 rc = stage[(s * U + u) * NT + threadIdx.x];
             const int y = rec_label(rc);
             const double xv = WT == GEE_W_UNIT ? 1.0 : (double)x[u];
+            GEE_DASSERT((int)(kk[u] >> cb) < R && (int64_t)(kk[u] & cmask) < a.N && y < K);
             if (y >= 0) atomicAdd(zt + (kk[u] >> cb) * K + y, xv * rc.y);
         }
     };
@@ -1055,6 +1063,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
         if (nitems == 1) {
             tile_epilogue<OUT32, NT>(a, zt, fac, drec, r0, nrows);
         } else {
+            GEE_DASSERT(a.ws.split_slot[b] < a.ws.ctl[kCtlSplit]);
             double *zs = a.ws.scratch + (size_t)a.ws.split_slot[b] * ((size_t)R * K);
             for (int i = threadIdx.x; i < tsz; i += NT) {
                 const double v = zt[i];
@@ -1103,7 +1112,7 @@ template <int WT, int NT>
 int launch_embed(const StGeo &g, const StArgs &a, bool out32, cudaStream_t st) {
     static PerDevice attr;
     const size_t smem =
-        sizeof(double) * ((size_t)1 << g.lrow_bits) * ((size_t)g.k + 3) + emb_stage_bytes(NT);
+        sizeof(double) * (((size_t)1 << g.lrow_bits) * ((size_t)g.k + 3) + 4) + emb_stage_bytes(NT);
     const size_t smax = kZTileMax + 24 * 512 + emb_stage_bytes(NT);
     if (!attr.done()) {
         int rc;
