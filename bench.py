@@ -312,6 +312,197 @@ def _traffic(cfg, kernel):
         return None
 
 
+def _kernel_table(lib, per_kernel, steps, models, prof_total):
+    import statistics as st_
+    ktab = []
+    for name, ts in per_kernel.items():
+        t_launch = st_.mean(ts)
+        bts = models.get(name)
+        ktab.append({"kernel": name, "ms_per_launch": t_launch, "launches_per_step": len(ts) / steps,
+                     "share": sum(ts) / prof_total, "alg_bytes": bts,
+                     "gbs": (bts / (t_launch * 1e-3) / 1e9) if bts else None})
+    ktab.sort(key=lambda r: -r["share"])
+    return ktab
+
+
+def _profile_steps(lib, fn, steps):
+    """Per-kernel device times of `steps` eager runs of fn (event marks between launches)."""
+    import ctypes
+    import torch
+    cap = 256
+    ms_buf = (ctypes.c_float * cap)()
+    nm_buf = (ctypes.c_char_p * cap)()
+    per_kernel, totals = {}, []
+    for _ in range(steps):
+        lib.gee_profile_start(torch.cuda.current_stream().cuda_stream)
+        fn()
+        lib.gee_profile_stop()
+        got = lib.gee_profile_read(ms_buf, nm_buf, cap)
+        if got < 0:
+            raise RuntimeError("gee_profile_read: " + lib.gee_last_error_string().decode())
+        totals.append(sum(ms_buf[j] for j in range(got)))
+        for j in range(got):
+            per_kernel.setdefault(nm_buf[j].decode(), []).append(ms_buf[j])
+    return per_kernel, sum(totals)
+
+
+def run_sharded(args, rank, world, local, dev):
+    """The row-sharded step on `world` GPUs (one process each, NCCL): every
+    rank draws the same seeded graph and keeps the stream entries of its row
+    range (equal entries per rank; outside the timed region).  Step =
+    partition + degrees of the rank's rows, ALL-GATHER of the degree vector
+    (Laplacian), node table + fused embed of the rank's rows.  value = input
+    edges / max over ranks of the mean step time (strong scaling: the whole
+    graph is split)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_03726_b200 import _lib
+    from paper_2406_03726_b200 import dist as gdist
+    lib = _lib.load()
+    c = load_config(args.config, dev)
+    n, e, k, directed, flags = c["n"], c["e"], c["k"], c["directed"], c["flags"]
+    rows, cols, lab = c["rows"], c["cols"], c["labels"]
+    w = c["weights"]
+    if c.get("wdtype") == "unit":
+        w = None
+    ranges = gdist.shard_plan(rows, cols, n, directed, world)
+    rb, re = ranges[rank]
+    stream = gdist.local_stream(rows, cols, w, directed, rb, re)
+    e_local = int(stream[0].numel())
+    ops = gdist.GpuShardOps(dev)
+    nonneg = gdist.stream_ok(w)
+    use_bm = ops.bitmap_ok(n, k, w is not None)
+    mode = "bitmap" if use_bm else ("stream" if nonneg else "csr")
+    z_out = torch.empty((re - rb, k), dtype=torch.float64, device=dev)
+    if mode == "stream":
+        def step():
+            return gdist.encode_rows_stream(ops, stream, lab, n, k, flags, ranges, rank, check=False, z=z_out)
+    elif mode == "bitmap":
+        def step():
+            return gdist.encode_rows_bitmap(ops, stream, lab, n, k, flags, ranges, rank, check=False)
+    else:
+        def step():
+            return gdist.encode_rows(ops, stream, lab, n, k, flags, ranges, rank)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    run, graphed = step, False
+    if mode != "csr" and not args.eager:
+        try:  # the whole rank step, kernels and the NCCL all-gather, as one CUDA graph
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step()
+            run, graphed = g.replay, True
+            run()
+            torch.cuda.synchronize()
+        except Exception as ex:
+            print(f"[rank {rank}] CUDA graph capture failed ({ex}); timing eager launches", file=sys.stderr)
+            run, graphed = step, False
+    lib.gee_reset_launch_count()
+    step()
+    torch.cuda.synchronize()
+    launches_per_step = int(lib.gee_launch_count())
+    sampler = ClockSampler(local) if rank == 0 else None
+    times = []
+    if sampler:
+        sampler.__enter__()
+    for _ in range(args.steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        run()
+        s1.record()
+        torch.cuda.synchronize()
+        times.append(s0.elapsed_time(s1))
+    if sampler:
+        sampler.__exit__()
+    dist.barrier()
+    if mode == "stream":
+        ops.st_check()
+    elif mode == "bitmap":
+        _lib.raise_device_errors(int(ops._bm_err.item()), "sharded bitmap encode")
+    ms_t = torch.tensor([statistics.mean(times)], device=dev)
+    dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t)
+    # per-kernel breakdown of this rank's step (eager, event marks between launches)
+    per_kernel, prof_total = _profile_steps(lib, step, max(1, min(args.steps, 5)))
+    m_local = e_local
+    models = kernel_bytes(dict(c, n=n, e=e_local, directed=True), m_local, m_local,
+                          0 if w is None else w.element_size())
+    # the rank's embed covers only its rows: Z bytes of (re - rb) rows, node records of all n
+    if "k_st_embed" in models:
+        wb = 0 if w is None else w.element_size()
+        lap = bool(flags & 1)
+        models["k_st_embed"] = (4 + wb) * m_local + 16 * n + (8 * n if lap else 0) + 8 * (re - rb) * k
+    ktab = _kernel_table(lib, per_kernel, max(1, min(args.steps, 5)), models, prof_total)
+    hbm, peak_src = peaks()
+    emb = next((r for r in ktab if r["kernel"] in ("k_st_embed", "k_embed")), None)
+    dom = next((r for r in ktab if r["alg_bytes"]), None)
+    # end to end: this rank's pinned host entries up, its step, its Z rows down
+    e2e = None
+    if not args.no_e2e:
+        hs = [None if x is None else x.cpu().pin_memory() for x in stream]
+        zh = torch.empty((re - rb, k), dtype=torch.float64).pin_memory()
+        ds = list(stream)
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(args.steps):
+            for h, d in zip(hs, ds):
+                if h is not None:
+                    d.copy_(h, non_blocking=True)
+            zz = step()
+            zh.copy_(zz, non_blocking=True)
+        t1.record()
+        torch.cuda.synchronize()
+        e2e_t = torch.tensor([t0.elapsed_time(t1) / args.steps], device=dev)
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        h2d = sum(h.numel() * h.element_size() for h in hs if h is not None)
+        e2e = {"value": e / (float(e2e_t) * 1e-3), "unit": UNIT, "ms_per_step": float(e2e_t),
+               "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(zh.numel() * 8) * world,
+               "api": "per rank: pinned host stream slice in, the rank step, its Z rows out (max over ranks)"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        arrays = host_arrays(c)
+        tms, es = cpu_reference_time(arrays, c, args.cpu_budget_s, 1, 5, sample=args.cpu_sample_edges)
+        cpu = {"value": es / statistics.mean(tms), "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"the first {es} of the {e} edges of configs[{args.config}], C restatement, 1 core"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": e / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": (e / (ms * 1e-3) / PUBLISHED[args.config]) if args.config in PUBLISHED else None,
+            "dtype": "f64", "data": "synthetic (seeded counter-based generator, BASELINE.json shapes)",
+            "config": workload_desc(c),
+            "workload_detail": {"parallelism": f"row-sharded x{world} ({mode} path): equal stream entries per "
+                                               "rank; NCCL all-gather of the degree vector (Laplacian)",
+                                "rank0_rows": [rb, re], "rank0_entries": e_local, "cuda_graph": graphed},
+            "roofline": ({"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["gbs"], "peak": hbm,
+                          "peak_source": peak_src, "unit": "GB/s", "frac": dom["gbs"] / hbm,
+                          "traffic": _traffic(args.config, dom["kernel"]), "alg_bytes_per_launch": dom["alg_bytes"],
+                          "scope": "rank 0's kernels"} if dom else None),
+            "embed_kernel": ({"kernel": emb["kernel"], "ms_per_launch": emb["ms_per_launch"], "gbs": emb["gbs"],
+                              "frac": emb["gbs"] / hbm} if emb and emb["gbs"] else None),
+            "kernels": ktab,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "launch_mode": "cuda_graph (kernels + NCCL, one replay per step)" if graphed else "eager",
+            "clocks": sampler.summary() if sampler else None,
+        }
+        sys.stdout.flush()
+        os.write(_REAL_STDOUT if _REAL_STDOUT is not None else 1, (json.dumps(line) + "\n").encode())
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
+_REAL_STDOUT = None
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -322,12 +513,19 @@ def run_b200(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1 or args.sharded or args.shuffle:
+        # NCCL may print its banner on stdout: keep stdout for the JSON line only
+        global _REAL_STDOUT
+        sys.stdout.flush()
+        _REAL_STDOUT = os.dup(1)
+        os.dup2(2, 1)
         if not dist.is_initialized():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29533")
             dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
-        from paper_2406_03726_b200 import dist as gdist
-        return gdist.bench_sharded(args, rank, world, dev)
+        if args.shuffle:
+            from paper_2406_03726_b200 import dist as gdist
+            return gdist.bench_sharded(args, rank, world, dev)
+        return run_sharded(args, rank, world, local, dev)
 
     import paper_2406_03726_b200 as G
     from paper_2406_03726_b200 import _lib

@@ -197,6 +197,28 @@ int gee_bitmap_shard_encode(const int64_t *rows, const int64_t *cols, int64_t e_
                             unsigned flags, const uint32_t *deg_all, double *z_local, void *ws,
                             size_t ws_bytes, int32_t *err, void *stream);
 
+/* Row shard through the bucketed stream encode (multi-GPU, dist.py; unit or
+ * GEE_NONNEG weights).  The shard owns rows [row_begin, row_end); rows / cols
+ * / w hold its e_local stream entries (row in the range, any column: the
+ * symmetrised list's entries of those rows), labels all n_nodes labels.
+ *   gee_stream_shard_degrees -> deg_local f64[row_end - row_begin]: the raw
+ *     weighted degrees of the local rows (without the A+I 1); the entries stay
+ *     partitioned in the workspace;
+ *   the caller all-gathers them into deg_all f64[n_nodes] (Laplacian only);
+ *   gee_stream_shard_encode -> z_local (f64, or f32 under GEE_FP32)
+ *     [(row_end - row_begin) x k]: node table of every node, then the embed.
+ * Both calls take the same arguments and workspace.  Out-of-range entries set
+ * GEE_ERR_EDGE_RANGE. */
+int gee_stream_shard_workspace(int64_t e_local, int64_t n_nodes, int64_t row_begin, int64_t row_end, int32_t k,
+                               int w_type, unsigned flags, size_t *ws_bytes);
+int gee_stream_shard_degrees(const int64_t *rows, const int64_t *cols, const void *w, int w_type, int64_t e_local,
+                             int64_t n_nodes, int64_t row_begin, int64_t row_end, const int64_t *labels, int32_t k,
+                             unsigned flags, double *deg_local, void *ws, size_t ws_bytes, int32_t *err,
+                             void *stream);
+int gee_stream_shard_encode(int w_type, int64_t e_local, int64_t n_nodes, int64_t row_begin, int64_t row_end,
+                            int32_t k, unsigned flags, const double *deg_all, void *z_local, void *ws,
+                            size_t ws_bytes, int32_t *err, void *stream);
+
 /* Distributed CSR build: ranks start from contiguous slices
  * of the ORIGINAL edge list (slice p = stream positions [e_p, e_{p+1}) of
  * EdgeList(rows, cols, w), graph_io.py:48-92) and shuffle the symmetrised

@@ -76,6 +76,11 @@ SIGNATURES = {
     "gee_parse_labels": (_int, [_vp, _i64, _i64, _int, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t,
                                 _vp]),
     "gee_labels_assign": (_int, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "gee_stream_shard_workspace": (_int, [_i64, _i64, _i64, _i64, _i32, _int, _u32, _szp]),
+    "gee_stream_shard_degrees": (_int, [_vp, _vp, _vp, _int, _i64, _i64, _i64, _i64, _vp, _i32, _u32, _vp, _vp,
+                                        ctypes.c_size_t, _vp, _vp]),
+    "gee_stream_shard_encode": (_int, [_int, _i64, _i64, _i64, _i64, _i32, _u32, _vp, _vp, _vp, ctypes.c_size_t,
+                                       _vp, _vp]),
     "gee_launch_count": (ctypes.c_uint64, []),
     "gee_reset_launch_count": (None, []),
     "gee_profile_start": (_int, [_vp]),

@@ -122,6 +122,14 @@ int stream_encode(const int64_t *rows, const int64_t *cols, const void *w, int w
                   const int64_t *labels, int32_t k, unsigned flags, void *z, void *ws, size_t ws_bytes,
                   int32_t *err, cudaStream_t st);
 int set_stream_mode(int v);
+bool stream_shard_ok(int wt, unsigned flags, int64_t e_local, int64_t N, int64_t rb, int64_t re, int k);
+size_t stream_shard_workspace(int64_t e_local, int64_t N, int64_t rb, int64_t re, int k, int wt);
+int stream_shard_degrees(const int64_t *rows, const int64_t *cols, const void *w, int wt, int64_t e_local, int64_t N,
+                         int64_t rb, int64_t re, const int64_t *labels, int32_t k, unsigned flags, double *deg_local,
+                         void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st);
+int stream_shard_encode(int wt, int64_t e_local, int64_t N, int64_t rb, int64_t re, int32_t k, unsigned flags,
+                        const double *deg_all, void *z_local, void *ws, size_t ws_bytes, int32_t *err,
+                        cudaStream_t st);
 int set_stream_tile_kb(int v);
 int set_stream_embed_nt(int v);
 
@@ -422,6 +430,39 @@ int gee_encode_edges(const int64_t *rows, const int64_t *cols, const void *w, in
     if (rc) return rc;
     return embed(W.row_ptr, W.row_cnt, W.col, W.val, nullptr, nullptr, 0, n_nodes, n_nodes, W.y32, W.inv, sc, k,
                  flags, z, k, W.emb_ws, W.emb_bytes, err, st);
+}
+
+}  // extern "C"
+
+// ---- row shards through the stream encode (k_stream.cu) --------------------
+extern "C" {
+
+int gee_stream_shard_workspace(int64_t e_local, int64_t n_nodes, int64_t row_begin, int64_t row_end, int32_t k,
+                               int w_type, unsigned flags, size_t *ws_bytes) {
+    if (!ws_bytes || !stream_shard_ok(w_type, flags, e_local, n_nodes, row_begin, row_end, k)) return GEE_E_ARG;
+    *ws_bytes = stream_shard_workspace(e_local, n_nodes, row_begin, row_end, k, w_type);
+    return GEE_OK;
+}
+
+int gee_stream_shard_degrees(const int64_t *rows, const int64_t *cols, const void *w, int w_type, int64_t e_local,
+                             int64_t n_nodes, int64_t row_begin, int64_t row_end, const int64_t *labels, int32_t k,
+                             unsigned flags, double *deg_local, void *ws, size_t ws_bytes, int32_t *err,
+                             void *stream) {
+    if (!stream_shard_ok(w_type, flags, e_local, n_nodes, row_begin, row_end, k) || !labels || !deg_local ||
+        (e_local && (!rows || !cols || (w_type != GEE_W_UNIT && !w))))
+        return GEE_E_ARG;
+    return stream_shard_degrees(rows, cols, w, w_type, e_local, n_nodes, row_begin, row_end, labels, k, flags,
+                                deg_local, ws, ws_bytes, err, (cudaStream_t)stream);
+}
+
+int gee_stream_shard_encode(int w_type, int64_t e_local, int64_t n_nodes, int64_t row_begin, int64_t row_end,
+                            int32_t k, unsigned flags, const double *deg_all, void *z_local, void *ws,
+                            size_t ws_bytes, int32_t *err, void *stream) {
+    if (!stream_shard_ok(w_type, flags, e_local, n_nodes, row_begin, row_end, k) || !z_local ||
+        ((flags & GEE_LAPLACIAN) && !deg_all))
+        return GEE_E_ARG;
+    return stream_shard_encode(w_type, e_local, n_nodes, row_begin, row_end, k, flags, deg_all, z_local, ws,
+                               ws_bytes, err, (cudaStream_t)stream);
 }
 
 }  // extern "C"

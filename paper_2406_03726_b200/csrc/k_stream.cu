@@ -81,6 +81,7 @@ size_t t_ztile_bytes = kZTileDefault;  // debug hook: bytes of the R x K Z tile
 
 struct StGeo {
     int64_t E, N;
+    int64_t nloc;  // rows this call owns (row shard), N for a whole graph
     int directed, wt, k;
     unsigned flags;
     int lrow_bits, sub_bits, d1_bits, d2_bits, d1_shift, col_bits;
@@ -100,15 +101,17 @@ __host__ __device__ __forceinline__ int bitlen64(int64_t x) {
     return b;
 }
 
-bool make_geo(StGeo &g, int64_t E, int64_t N, int directed, int wt, int k, unsigned flags) {
+bool make_geo(StGeo &g, int64_t E, int64_t N, int directed, int wt, int k, unsigned flags, int64_t nloc = -1) {
     g.E = E;
     g.N = N;
+    g.nloc = nloc < 0 ? N : nloc;
+    if (g.nloc < 1) return false;
     g.directed = directed;
     g.wt = wt;
     g.k = k;
     g.flags = flags;
-    const int rb = bitlen64(N - 1) > 0 ? bitlen64(N - 1) : 1;
-    g.col_bits = rb;
+    const int rb = bitlen64(g.nloc - 1) > 0 ? bitlen64(g.nloc - 1) : 1;  // local row bits
+    g.col_bits = bitlen64(N - 1) > 0 ? bitlen64(N - 1) : 1;
     int lr = 0;
     while (lr < rb && lr < kLrowMax && (size_t)(2ll << lr) * (size_t)k * 8 <= t_ztile_bytes) ++lr;
     if ((size_t)(1ll << lr) * (size_t)k * 8 > t_ztile_bytes) return false;  // K too large for one row
@@ -123,7 +126,7 @@ bool make_geo(StGeo &g, int64_t E, int64_t N, int directed, int wt, int k, unsig
     if ((1 << g.d2_bits) > kStWin) return false;
     g.d1_shift = g.lrow_bits + g.d2_bits;
     if (g.lrow_bits + g.col_bits > 32) return false;
-    g.S = (unsigned)(((N - 1) >> g.lrow_bits) + 1);
+    g.S = (unsigned)(((g.nloc - 1) >> g.lrow_bits) + 1);
     g.Mcap = directed ? E : 2 * E;
     const int64_t per = g.Mcap / ((int64_t)num_sms() * 4);
     int64_t c = 4096;
@@ -178,7 +181,7 @@ size_t carve(Carver &cv, StWs &w, const StGeo &g) {
     w.scratch = cv.take<double>((size_t)g.max_split * ((size_t)1 << g.lrow_bits) * (size_t)g.k);
     w.keys2 = cv.take<uint32_t>(M);
     w.w2 = wb ? (void *)cv.take<char>(M * wb) : nullptr;
-    w.deg = cv.take<double>((size_t)g.N);
+    w.deg = cv.take<double>((size_t)g.nloc);
     w.scale = cv.take<double>((size_t)g.N);
     w.rec = cv.take<double2>((size_t)g.N);
     w.y32 = cv.take<int32_t>((size_t)g.N + 1);
@@ -192,6 +195,8 @@ struct StArgs {
     const int64_t *rows, *cols;
     const void *w;
     int64_t E, N;
+    int64_t row0, nloc;  // the rows [row0, row0 + nloc) this call owns
+    double *deg_out;     // row-shard phase 1: raw local degrees (else nullptr)
     int directed, k;
     unsigned flags;
     int lrow_bits, d2_bits, d1_shift, col_bits;
@@ -236,6 +241,16 @@ __device__ __forceinline__ int64_t fix_index(int64_t x, int64_t N, bool &bad) {
 }
 
 // A non-finite weight (graph_io.py:71-72) is raised and stored as 0.
+// a row of this call's range -> its local index (out of range: raised, 0)
+__device__ __forceinline__ int64_t fix_row(int64_t r, const StArgs &a, bool &bad) {
+    r -= a.row0;
+    if (r < 0 || r >= a.nloc) {
+        bad = true;
+        return 0;
+    }
+    return r;
+}
+
 template <int WT>
 __device__ __forceinline__ void load_weight(const StArgs &a, int64_t i, typename WTraits<WT>::T &w, bool &badw,
                                             bool &neg) {
@@ -258,7 +273,7 @@ __global__ void __launch_bounds__(kStNT) k_st_hist1(StArgs a) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.E; i += stride) {
         bool bad = false;
-        int64_t r = fix_index(__ldg(a.rows + i), a.N, bad);
+        int64_t r = a.directed ? fix_row(__ldg(a.rows + i), a, bad) : fix_index(__ldg(a.rows + i), a.N, bad);
         if (a.directed) {
             atomicAdd(cnt + (unsigned)(r >> a.d1_shift), 1u);
         } else {
@@ -376,7 +391,8 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part1(StArgs a) {
             if (!DIR) rk[u][DIR ? 0 : 1] = 0xffffffffu;
             if (r[u] == -2) continue;
             bool bad = false;
-            long long rr = fix_index(r[u], a.N, bad), cc = fix_index(c[u], a.N, bad);
+            long long rr = DIR ? fix_row(r[u], a, bad) : fix_index(r[u], a.N, bad);
+            long long cc = fix_index(c[u], a.N, bad);
             if constexpr (WT != GEE_W_UNIT) {
                 if (!isfinite((double)wv[u])) {
                     errbits |= GEE_ERR_EDGE_WEIGHT;
@@ -698,11 +714,11 @@ __device__ __forceinline__ void item_range(const StArgs &a, unsigned item, unsig
     if (p0 > s1) p0 = s1;
 }
 
+// node r (global id): s_r = 1/sqrt(d_r (+1 under A+I)) and its record
 __device__ __forceinline__ void finish_node(const StArgs &a, int64_t r, double d) {
     double s = 1.0;
     if (a.flags & GEE_LAPLACIAN) {
         if (a.flags & GEE_DIAGONAL) d = d + 1.0;
-        a.ws.deg[r] = d;
         s = laplacian_scale(d, a.err);
     }
     a.ws.scale[r] = s;
@@ -771,8 +787,8 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
         const unsigned nitems = a.ws.ditem_off[b + 1] - a.ws.ditem_off[b];
         const unsigned s1 = a.ws.base2[b + 1];
         const unsigned p0 = min(s1, a.ws.base2[b] + j * kDegItem), p1 = min(s1, p0 + kDegItem);
-        const int64_t r0 = (int64_t)b << a.lrow_bits;
-        const int nrows = (int)min((int64_t)R, a.N - r0);
+        const int64_t r0 = (int64_t)b << a.lrow_bits;  // local row of the bucket
+        const int nrows = (int)min((int64_t)R, a.nloc - r0);
         if (lap) {
             for (int l = lane; l < R * copies; l += 32) mine[l] = 0.0;
             __syncwarp();
@@ -800,7 +816,11 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
             __syncwarp();
         }
         if (nitems == 1) {
-            for (int l = lane; l < nrows; l += 32) finish_node(a, r0 + l, lap ? mine[l * copies] : 0.0);
+            for (int l = lane; l < nrows; l += 32) {
+                const double d = lap ? mine[l * copies] : 0.0;
+                if (a.deg_out) a.deg_out[r0 + l] = d;
+                else finish_node(a, a.row0 + r0 + l, d);
+            }
         } else {
             if (lap)
                 for (int l = lane; l < nrows; l += 32)
@@ -812,13 +832,23 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
             last = __shfl_sync(0xffffffffu, last, 0);
             if (last) {
                 __threadfence();
-                for (int l = lane; l < nrows; l += 32)
-                    finish_node(a, r0 + l, lap ? __ldcg(a.ws.deg + r0 + l) : 0.0);
+                for (int l = lane; l < nrows; l += 32) {
+                    const double d = lap ? __ldcg(a.ws.deg + r0 + l) : 0.0;
+                    if (a.deg_out) a.deg_out[r0 + l] = d;
+                    else finish_node(a, a.row0 + r0 + l, d);
+                }
                 if (a.ws.split_slot[b] != 0xffffffffu) zero_scratch(a, b, nrows, lane, 32);
             }
         }
         __syncwarp();
     }
+}
+
+// Row-shard phase 2: the node table of every node from the all-gathered
+// degrees (deg_all may be null without the Laplacian)
+__global__ void k_st_nodes(StArgs a, const double *deg_all) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.N; j += (int64_t)gridDim.x * blockDim.x)
+        finish_node(a, j, deg_all ? deg_all[j] : 0.0);
 }
 
 // ---- the fused embed ------------------------------------------------------------
@@ -1024,13 +1054,13 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
         const unsigned p0 = s_meta[cur][1], p1 = s_meta[cur][2], nitems = s_meta[cur][3];
         // the next item's descriptor loads overlap this item's work
         if (threadIdx.x == 0) grab(cur ^ 1);
-        const int64_t r0 = (int64_t)b << a.lrow_bits;
-        const int nrows = (int)min((int64_t)R, a.N - r0);
+        const int64_t r0 = (int64_t)b << a.lrow_bits;  // local row (Z row) of the bucket
+        const int nrows = (int)min((int64_t)R, a.nloc - r0);
         const int tsz = nrows * K;
         // per-row data of the epilogue, loaded now so its latency hides under the accumulation
         for (int l = threadIdx.x; l < nrows; l += NT) {
-            if (a.flags & GEE_LAPLACIAN) fac[l] = a.ws.scale[r0 + l];
-            if (a.flags & GEE_DIAGONAL) drec[l] = a.ws.rec[r0 + l];
+            if (a.flags & GEE_LAPLACIAN) fac[l] = a.ws.scale[a.row0 + r0 + l];
+            if (a.flags & GEE_DIAGONAL) drec[l] = a.ws.rec[a.row0 + r0 + l];
         }
         const bool trace = a.variant >= 9 && threadIdx.x == 0 && blockIdx.x < 4096;
         const long long t1 = trace ? clock64() : 0;
@@ -1129,8 +1159,10 @@ int launch_embed(const StGeo &g, const StArgs &a, bool out32, cudaStream_t st) {
     return GEE_OK;
 }
 
+// phase 1: partition the entries into row buckets and compute the degrees
+// (node records, or the raw local degrees of a row shard)
 template <int WT>
-int run_stream(const StGeo &g, StArgs &a, cudaStream_t st) {
+int run_phase1(const StGeo &g, StArgs &a, cudaStream_t st) {
     static PerDevice attr;
     const size_t p1_smem = (size_t)(8 + WTraits<WT>::bytes) * kStTile;
     const size_t p2_smem = (size_t)(4 + WTraits<WT>::bytes + 2) * kStTile + 3 * sizeof(unsigned) * kStWin;
@@ -1166,6 +1198,16 @@ int run_stream(const StGeo &g, StArgs &a, cudaStream_t st) {
     GEE_CHECK_LAUNCH("k_st_part2");
     k_st_degree<WT><<<sms * 8, kDegNT, deg_smem, st>>>(a);
     GEE_CHECK_LAUNCH("k_st_degree");
+    return GEE_OK;
+}
+
+// phase 2: the fused embed (+ the node table of a row shard from deg_all)
+template <int WT>
+int run_phase2(const StGeo &g, StArgs &a, const double *deg_all, bool shard, cudaStream_t st) {
+    if (shard) {
+        k_st_nodes<<<grid_for(g.N, 256, 8), 256, 0, st>>>(a, deg_all);
+        GEE_CHECK_LAUNCH("k_st_nodes");
+    }
     const bool out32 = (a.flags & GEE_FP32) != 0;
     int rc2;
     if (t_emb_nt == 128) rc2 = launch_embed<WT, 128>(g, a, out32, st);
@@ -1174,6 +1216,12 @@ int run_stream(const StGeo &g, StArgs &a, cudaStream_t st) {
     if (rc2) return rc2;
     GEE_CHECK_LAUNCH("k_st_embed");
     return GEE_OK;
+}
+
+template <int WT>
+int run_stream(const StGeo &g, StArgs &a, cudaStream_t st) {
+    const int rc = run_phase1<WT>(g, a, st);
+    return rc ? rc : run_phase2<WT>(g, a, nullptr, false, st);
 }
 
 }  // namespace
@@ -1221,28 +1269,19 @@ size_t stream_workspace(int64_t E, int64_t N, int directed, int k, int wt) {
     return carve(cv, w, g);
 }
 
-int stream_encode(const int64_t *rows, const int64_t *cols, const void *w, int wt, int64_t E, int64_t N, int directed,
-                  const int64_t *labels, int32_t k, unsigned flags, void *z, void *ws, size_t ws_bytes,
-                  int32_t *err, cudaStream_t st) {
-    StGeo g;
-    if (!make_geo(g, E, N, directed, wt, k, flags)) return GEE_E_ARG;
-    Carver cv(ws);
-    StWs W;
-    if (carve(cv, W, g) > ws_bytes) return GEE_E_WORKSPACE;
-    GEE_CHECK_CUDA(cudaMemsetAsync(W.ctl, 0, sizeof(unsigned) * kCtlWords, st));
-    GEE_CHECK_CUDA(cudaMemsetAsync(W.hist2, 0, sizeof(unsigned) * ((size_t)g.S + 1), st));
-    if (flags & GEE_LAPLACIAN) GEE_CHECK_CUDA(cudaMemsetAsync(W.deg, 0, sizeof(double) * (size_t)N, st));
-    int rc = label_hist_pipeline(labels, N, k, W.y32, W.counts, W.inv, W.label_partial, W.ctl + kCtlLabel, err, st);
-    if (rc) return rc;
-    StArgs a;
+static void fill_args(StArgs &a, const StGeo &g, const StWs &W, const int64_t *rows, const int64_t *cols,
+                      const void *w, int64_t row0, void *z, int32_t *err) {
     a.rows = rows;
     a.cols = cols;
     a.w = w;
-    a.E = E;
-    a.N = N;
-    a.directed = directed;
-    a.k = k;
-    a.flags = flags;
+    a.E = g.E;
+    a.N = g.N;
+    a.row0 = row0;
+    a.nloc = g.nloc;
+    a.deg_out = nullptr;
+    a.directed = g.directed;
+    a.k = g.k;
+    a.flags = g.flags;
     a.lrow_bits = g.lrow_bits;
     a.d2_bits = g.d2_bits;
     a.d1_shift = g.d1_shift;
@@ -1252,14 +1291,87 @@ int stream_encode(const int64_t *rows, const int64_t *cols, const void *w, int w
     a.variant = t_stream_mode >= 16 ? t_stream_mode - 16 : 0;
     // 8 interleaved copies while the per-warp slice stays <= 4 KB (R <= 64), fewer for larger R
     a.deg_copies = g.lrow_bits <= 6 ? 8 : g.lrow_bits <= 7 ? 4 : g.lrow_bits <= 8 ? 2 : 1;
-    a.magic = (0x100000000ull + (unsigned)k - 1) / (unsigned)k;
+    a.magic = (0x100000000ull + (unsigned)g.k - 1) / (unsigned)g.k;
     a.ws = W;
     a.z = z;
     a.err = err;
+}
+
+static int setup(StGeo &g, StWs &W, void *ws, size_t ws_bytes, const int64_t *labels, cudaStream_t st,
+                 int32_t *err) {
+    Carver cv(ws);
+    if (carve(cv, W, g) > ws_bytes || !ws) return GEE_E_WORKSPACE;
+    GEE_CHECK_CUDA(cudaMemsetAsync(W.ctl, 0, sizeof(unsigned) * kCtlWords, st));
+    GEE_CHECK_CUDA(cudaMemsetAsync(W.hist2, 0, sizeof(unsigned) * ((size_t)g.S + 1), st));
+    if (g.flags & GEE_LAPLACIAN) GEE_CHECK_CUDA(cudaMemsetAsync(W.deg, 0, sizeof(double) * (size_t)g.nloc, st));
+    return label_hist_pipeline(labels, g.N, g.k, W.y32, W.counts, W.inv, W.label_partial, W.ctl + kCtlLabel, err, st);
+}
+
+int stream_encode(const int64_t *rows, const int64_t *cols, const void *w, int wt, int64_t E, int64_t N, int directed,
+                  const int64_t *labels, int32_t k, unsigned flags, void *z, void *ws, size_t ws_bytes,
+                  int32_t *err, cudaStream_t st) {
+    StGeo g;
+    if (!make_geo(g, E, N, directed, wt, k, flags)) return GEE_E_ARG;
+    StWs W;
+    int rc = setup(g, W, ws, ws_bytes, labels, st, err);
+    if (rc) return rc;
+    StArgs a;
+    fill_args(a, g, W, rows, cols, w, 0, z, err);
     switch (wt) {
         case GEE_W_UNIT: return run_stream<GEE_W_UNIT>(g, a, st);
         case GEE_W_F32: return run_stream<GEE_W_F32>(g, a, st);
         default: return run_stream<GEE_W_F64>(g, a, st);
+    }
+}
+
+// ---- row shards (multi-GPU, dist.py) ----------------------------------------------
+bool stream_shard_ok(int wt, unsigned flags, int64_t e_local, int64_t N, int64_t rb, int64_t re, int k) {
+    if (wt != GEE_W_UNIT && !(flags & GEE_NONNEG)) return false;
+    if (e_local < 0 || e_local >= (int64_t)0xffffffffll || rb < 0 || re <= rb || re > N) return false;
+    StGeo g;
+    return make_geo(g, e_local, N, 1, wt, k, flags, re - rb);
+}
+
+size_t stream_shard_workspace(int64_t e_local, int64_t N, int64_t rb, int64_t re, int k, int wt) {
+    StGeo g;
+    if (!make_geo(g, e_local, N, 1, wt, k, 0, re - rb)) return 0;
+    Carver cv(nullptr);
+    StWs w;
+    return carve(cv, w, g);
+}
+
+int stream_shard_degrees(const int64_t *rows, const int64_t *cols, const void *w, int wt, int64_t e_local, int64_t N,
+                         int64_t rb, int64_t re, const int64_t *labels, int32_t k, unsigned flags, double *deg_local,
+                         void *ws, size_t ws_bytes, int32_t *err, cudaStream_t st) {
+    StGeo g;
+    if (!make_geo(g, e_local, N, 1, wt, k, flags, re - rb)) return GEE_E_ARG;
+    StWs W;
+    int rc = setup(g, W, ws, ws_bytes, labels, st, err);
+    if (rc) return rc;
+    StArgs a;
+    fill_args(a, g, W, rows, cols, w, rb, nullptr, err);
+    a.deg_out = deg_local;
+    switch (wt) {
+        case GEE_W_UNIT: return run_phase1<GEE_W_UNIT>(g, a, st);
+        case GEE_W_F32: return run_phase1<GEE_W_F32>(g, a, st);
+        default: return run_phase1<GEE_W_F64>(g, a, st);
+    }
+}
+
+int stream_shard_encode(int wt, int64_t e_local, int64_t N, int64_t rb, int64_t re, int32_t k, unsigned flags,
+                        const double *deg_all, void *z_local, void *ws, size_t ws_bytes, int32_t *err,
+                        cudaStream_t st) {
+    StGeo g;
+    if (!make_geo(g, e_local, N, 1, wt, k, flags, re - rb)) return GEE_E_ARG;
+    Carver cv(ws);
+    StWs W;
+    if (carve(cv, W, g) > ws_bytes || !ws) return GEE_E_WORKSPACE;
+    StArgs a;
+    fill_args(a, g, W, nullptr, nullptr, nullptr, rb, z_local, err);
+    switch (wt) {
+        case GEE_W_UNIT: return run_phase2<GEE_W_UNIT>(g, a, deg_all, true, st);
+        case GEE_W_F32: return run_phase2<GEE_W_F32>(g, a, deg_all, true, st);
+        default: return run_phase2<GEE_W_F64>(g, a, deg_all, true, st);
     }
 }
 

@@ -175,6 +175,41 @@ class GpuShardOps:
         _lib.raise_device_errors(bits, "sharded encode")
         return z
 
+    # -- stream path (unit or non-negative weights; k_stream.cu) -------------
+    def st_prepare(self, r, c, w, n, rb, re, k, flags):
+        """Plan the row shard's stream encode (workspace sized once)."""
+        e = int(r.numel())
+        wt = _lib.W_UNIT if w is None else (_lib.W_F32 if w.dtype == torch.float32 else _lib.W_F64)
+        f = flags | _lib.NONNEG
+        nb = _lib.size_query(self.lib.gee_stream_shard_workspace, e, n, rb, re, k, wt, f)
+        self._st = dict(e=e, wt=wt, n=n, rb=rb, re=re, k=k, flags=f,
+                        ws=torch.empty(max(nb, 256), dtype=torch.uint8, device=self.dev),
+                        deg=torch.empty(max(re - rb, 1), dtype=torch.float64, device=self.dev),
+                        err=_device.error_word(self.dev))
+        return self._st
+
+    def st_degrees(self, r, c, w, labels):
+        """Phase 1: partition the shard's entries, degrees of its rows (raw, f64)."""
+        p = self._st
+        _lib.check(self.lib.gee_stream_shard_degrees(
+            _device.ptr(r), _device.ptr(c), _device.ptr(w), p["wt"], p["e"], p["n"], p["rb"], p["re"],
+            _device.ptr(labels), p["k"], p["flags"], _device.ptr(p["deg"]), _device.ptr(p["ws"]), p["ws"].numel(),
+            _device.ptr(p["err"]), _device.stream_handle()))
+        return p["deg"][: p["re"] - p["rb"]]
+
+    def st_encode(self, deg_all, z=None):
+        """Phase 2: node table from the gathered degrees, Z of the shard's rows."""
+        p = self._st
+        if z is None:
+            z = torch.empty((p["re"] - p["rb"], p["k"]), dtype=torch.float64, device=self.dev)
+        _lib.check(self.lib.gee_stream_shard_encode(
+            p["wt"], p["e"], p["n"], p["rb"], p["re"], p["k"], p["flags"], _device.ptr(deg_all), _device.ptr(z),
+            _device.ptr(p["ws"]), p["ws"].numel(), _device.ptr(p["err"]), _device.stream_handle()))
+        return z
+
+    def st_check(self):
+        _lib.raise_device_errors(int(self._st["err"].item()), "sharded stream encode")
+
     # -- bitmap path (unit weights, n <= 16384, k <= 8) ----------------------
     BITMAP_MAX_NODES = 16384
 
@@ -267,6 +302,29 @@ def encode_rows(ops, stream, labels, n, k, flags, ranges, rank, group=None):
     return ops.embed(csr, rb, re, n, y32, inv, scale, k, flags)
 
 
+def encode_rows_stream(ops, stream, labels, n, k, flags, ranges, rank, group=None, check=True, z=None):
+    """Stream path for rank `rank` (unit or non-negative weights): partition
+    its entries and compute its rows' degrees, ALL-GATHER of the degree
+    vector (f64, N; Laplacian only -- labels are replicated, so n_k needs no
+    collective), then the node table and Z[rb:re].  No host synchronisation
+    unless `check`."""
+    rb, re = ranges[rank]
+    r, c, w = stream
+    if getattr(ops, "_st", None) is None or ops._st["e"] != int(r.numel()) or ops._st["rb"] != rb:
+        ops.st_prepare(r, c, w, n, rb, re, k, flags)
+    deg_local = ops.st_degrees(r, c, w, labels)
+    deg_all = all_gather_ranges(deg_local, ranges, group) if flags & _lib.LAPLACIAN else None
+    z = ops.st_encode(deg_all, z)
+    if check:
+        ops.st_check()
+    return z
+
+
+def stream_ok(w) -> bool:
+    """The stream path applies: unit weights, or weights all >= 0."""
+    return w is None or bool((w >= 0).all())
+
+
 def encode_rows_bitmap(ops, stream, labels, n, k, flags, ranges, rank, group=None, check=True):
     """Bitmap path for rank `rank` (unit weights): degrees of the local rows,
     ALL-GATHER of the degree vector (Laplacian only), then Z[rb:re]."""
@@ -293,8 +351,11 @@ def encode_sharded(edges, labels, opts=None, group=None, ops=None):
     _, w = e.weight_kind()
     stream = local_stream(e.rows, e.cols, w, edges.directed, rb, re)
     lab = _device.to_device(labels.labels, torch.int64, dev)
+    nonneg = w is None or bool(e.nonneg)
     if ops.bitmap_ok(n, k, w is not None):
         z = encode_rows_bitmap(ops, stream, lab, n, k, flags, ranges, rank, group)
+    elif nonneg and hasattr(ops, "st_prepare"):
+        z = encode_rows_stream(ops, stream, lab, n, k, flags, ranges, rank, group)
     else:
         z = encode_rows(ops, stream, lab, n, k, flags, ranges, rank, group)
     return z, (rb, re)

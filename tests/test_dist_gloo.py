@@ -123,6 +123,44 @@ class OracleShardOps:
         self._labels = labels.numpy().astype(np.int64)
         return torch.as_tensor(np.bincount(r.numpy() - rb, minlength=re - rb).astype(np.int32))
 
+    # stream path: phase 1 = raw degrees of the local rows, phase 2 = Z rows
+    # from the gathered degree vector (the oracle's CSR of the local stream)
+    def st_prepare(self, r, c, w, n, rb, re, k, flags):
+        self._st = dict(e=int(r.numel()), rb=rb, re=re, n=n, k=k, flags=flags, stream=(r, c, w))
+        return self._st
+
+    def st_degrees(self, r, c, w, labels):
+        p = self._st
+        self._labels = labels.numpy().astype(np.int64)
+        w64 = np.ones(r.numel()) if w is None else w.numpy().astype(np.float64)
+        ip, cc, cv = O.coo_to_csr(r.numpy(), c.numpy(), w64, p["n"], p["n"])
+        p["csr"] = (ip, cc, cv)
+        return torch.as_tensor(O.degree(ip, cv, p["n"])[p["rb"]:p["re"]])
+
+    def st_encode(self, deg_all, z=None):
+        p = self._st
+        n, k, flags = p["n"], p["k"], p["flags"]
+        scale = None
+        if flags & LAP:
+            if flags & DIAG:
+                ip, cc, cv = p["csr"]
+                aug = O.add_identity(ip, cc, cv, n)
+                local = O.degree(aug[0], aug[2], n)[p["rb"]:p["re"]]
+                deg = deg_all.numpy().astype(np.float64).copy()
+                # the gathered degrees are raw; A+I adds the diagonal term as the
+                # reference merges it (v_rr + 1.0 at its sorted position)
+                deg = np.where(np.arange(n) >= 0, deg + 1.0, deg)
+                deg[p["rb"]:p["re"]] = local
+            else:
+                deg = deg_all.numpy().astype(np.float64)
+            scale = torch.as_tensor(np.where(deg > 0, 1.0 / np.sqrt(np.where(deg > 0, deg, 1.0)), 0.0))
+        y32 = torch.as_tensor(self._labels.astype(np.int32))
+        inv = self.inv_counts(torch.as_tensor(O.class_counts(self._labels, k)))
+        return self.embed(p["csr"], p["rb"], p["re"], n, y32, inv, scale, k, flags)
+
+    def st_check(self):
+        pass
+
     @staticmethod
     def bitmap_ok(n, k, weighted):
         return not weighted and 1 <= n <= 16384 and 1 <= k <= 8
@@ -326,3 +364,39 @@ def test_partition_np_matches_local_stream():
         ww = np.concatenate([x[2] for x in seq])
         er, ec, ew = gdist.local_stream(rows, cols, w, directed, int(bounds[d]), int(bounds[d + 1]))
         assert np.array_equal(r, er) and np.array_equal(c, ec) and np.array_equal(ww, ew)
+
+
+def _st_worker(rank, world, port, case, flags, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, rows, cols, w, labels, k, directed = case
+        ranges = gdist.shard_plan(rows, cols, n, directed, world)
+        stream = gdist.local_stream(torch.as_tensor(rows), torch.as_tensor(cols), torch.as_tensor(w), directed,
+                                    *ranges[rank])
+        z = gdist.encode_rows_stream(OracleShardOps(), stream, torch.as_tensor(labels), n, k, flags, ranges, rank)
+        full = gdist.gather_z(z, ranges)
+        if rank == 0:
+            out.put(full.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("flags", [LAP | DIAG | CORR, LAP | CORR, 0])
+def test_stream_path_degree_allgather(world, flags):
+    """Stream path orchestration: phase 1 per rank, ALL-GATHER of the f64
+    degree vector, phase 2 per rank; Z assembled from the shards matches the
+    unsharded oracle within the north_star's 1e-12 (the gathered degrees are
+    raw sums; A+I's 1.0 is added after the exchange, which the reference
+    merges into the diagonal entry instead -- a rounding-level difference)."""
+    case = _graph(21 + flags + world, directed=True)
+    n, rows, cols, w, labels, k, directed = case
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_st_worker, args=(world, _free_port(), case, flags, q), nprocs=world, join=True)
+    z = q.get(timeout=60)
+    st, zr, _ = O.encode_edges(rows, cols, w, n, directed, labels, k, flags)
+    assert st == O.OK
+    rown = np.sqrt((zr * zr).sum(axis=1, keepdims=True))
+    assert z.shape == zr.shape and (np.abs(z - zr) <= 1e-12 * np.maximum(np.abs(zr), rown) + 1e-15).all()

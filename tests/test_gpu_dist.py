@@ -262,3 +262,68 @@ def test_single_rank_nccl_group_edge_shuffle(kind, k, flags):
         z_close(z.cpu().numpy(), zr)
     finally:
         dist.destroy_process_group()
+
+
+# ---- the stream path per row shard (gee_stream_shard_*) ---------------------
+@pytest.mark.parametrize("shards", [1, 2, 5])
+@pytest.mark.parametrize("flags,directed,kind", [(7, False, "f64"), (5, True, "f32"), (3, False, "unit"),
+                                                 (0, True, "f64")])
+def test_stream_shards_match_oracle(shards, flags, directed, kind):
+    """Every shard runs phase 1 (its rows' degrees), the degree vectors are
+    concatenated by hand (the all-gather), then phase 2 per shard."""
+    rng = np.random.default_rng(shards * 100 + flags)
+    n, m, k = 5000, 60_000, 20
+    rows = rng.integers(0, n, m)
+    cols = rng.integers(0, n, m)
+    rows[:3000] = 11  # a hub: split buckets in its shard
+    w = np.ones(m) if kind == "unit" else (1.0 - rng.random(m))
+    if kind == "f32":
+        w = w.astype(np.float32)
+    labels = rng.integers(-1, k, n)
+    dev = torch.device("cuda")
+    ranges = gdist.shard_plan(rows, cols, n, directed, shards)
+    tr, tc = torch.as_tensor(rows, device=dev), torch.as_tensor(cols, device=dev)
+    tw = None if kind == "unit" else torch.as_tensor(w, device=dev)
+    lab = torch.as_tensor(labels, device=dev)
+    opss, streams, degs = [], [], []
+    for rb, re in ranges:
+        ops = gdist.GpuShardOps(dev)
+        st = gdist.local_stream(tr, tc, tw, directed, rb, re)
+        ops.st_prepare(*st, n, rb, re, k, flags)
+        degs.append(ops.st_degrees(*st, lab).clone())
+        opss.append(ops)
+        streams.append(st)
+    deg_all = torch.cat(degs)                              # all-gather
+    z = torch.cat([ops.st_encode(deg_all if flags & 1 else None) for ops in opss])
+    for ops in opss:
+        ops.st_check()
+    st_, zr, _ = O.encode_edges(rows, cols, np.asarray(w, np.float64), n, directed, labels, k, flags)
+    assert st_ == O.OK
+    z_close(z.cpu().numpy(), zr)
+
+
+def test_single_rank_nccl_group_stream_path():
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    try:
+        rng = np.random.default_rng(3)
+        n, m, k = 20000, 100_000, 50
+        rows = rng.integers(0, n, m)
+        cols = rng.integers(0, n, m)
+        w = (1.0 - rng.random(m)).astype(np.float32)
+        labels = rng.integers(0, k, n)
+        e = G.EdgeList(n, rows, cols, w, directed=True)
+        lab = G.LabelVector(labels, k)
+        opts = G.EmbedOptions(True, True, True)
+        z, (rb, re) = gdist.encode_sharded(e, lab, opts)
+        assert (rb, re) == (0, n)
+        st, zr, _ = O.encode_edges(rows, cols, w.astype(np.float64), n, True, labels, k, 7)
+        z_close(z.cpu().numpy(), zr)
+    finally:
+        dist.destroy_process_group()
