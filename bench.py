@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--fp32", action="store_true", help="the optional fp32 path: Z stored as float32 (1e-5)")
+    p.add_argument("--permute-edges", action="store_true", help="side measurement: seeded random edge order")
+    p.add_argument("--weighted", action="store_true", help="side measurement: U(0,1] f64 weights instead of 1.0")
     p.add_argument("--stream-variant", type=int, default=0,
                    help="debug A/B of the stream embed (results wrong by design): 1 no shared atomics, 2 no gathers")
     p.add_argument("--stream-tile-kb", type=int, default=0, help="debug: KB of the stream encode's Z tile")
@@ -118,6 +120,31 @@ def load_config(idx, device):
         return gen.host_config(idx)
     from paper_2406_03726_b200 import synth
     return synth.make_config(idx, device=torch.device(device))
+
+
+def apply_variant(c, args):
+    """Workload variants for the side measurements (never the default line):
+    --permute-edges: the same edge list in a seeded random order (the SBM
+    generator emits row-major order); --weighted: U(0,1] float64 weights
+    instead of 1.0 (the general weighted paths instead of the unit-weight ones)."""
+    import torch
+    if not (args.permute_edges or args.weighted):
+        return c
+    c = dict(c)
+    e = int(c["e"])
+    if args.permute_edges:
+        g = torch.Generator(device=c["rows"].device).manual_seed(12345)
+        perm = torch.randperm(e, generator=g, device=c["rows"].device)
+        c["rows"], c["cols"] = c["rows"][perm], c["cols"][perm]
+        if c["weights"] is not None:
+            c["weights"] = c["weights"][perm]
+    if args.weighted:
+        g = torch.Generator(device=c["rows"].device).manual_seed(54321)
+        c["weights"] = 1.0 - torch.rand(e, generator=g, device=c["rows"].device, dtype=torch.float64)
+        c["wdtype"] = "f64"
+    c["variant"] = ",".join(v for v, on in (("permuted edge order", args.permute_edges),
+                                            ("U(0,1] f64 weights", args.weighted)) if on)
+    return c
 
 
 def host_arrays(c):
@@ -545,7 +572,7 @@ def run_b200(args):
         lib.gee_debug_set(_lib.DEBUG_EMBED_FLAT_BYTES, args.embed_flat_bytes)
     if args.embed_flat_rowmax is not None:
         lib.gee_debug_set(_lib.DEBUG_EMBED_FLAT_ROWMAX, args.embed_flat_rowmax)
-    c = load_config(args.config, dev)
+    c = apply_variant(load_config(args.config, dev), args)
     n, e, k, directed, flags = c["n"], c["e"], c["k"], c["directed"], c["flags"]
     rows = torch.as_tensor(c["rows"], device=dev)
     cols = torch.as_tensor(c["cols"], device=dev)
@@ -724,7 +751,7 @@ def run_b200(args):
         "dtype": "f64" + ("; Z stored f32 (--fp32)" if args.fp32 else ""),
         "data": "synthetic (seeded counter-based generator, BASELINE.json shapes)",
         "config": workload_desc(c),
-        "workload_detail": dict(l2=((f"flushed: {args.flush_mib} MiB write before every timed step"
+        "workload_detail": dict(variant=c.get("variant"), l2=((f"flushed: {args.flush_mib} MiB write before every timed step"
                                               + (f", then a {args.flush_mib} MiB read (write-backs drained: cold, "
                                                  "clean L2)" if args.flush_mode == "clean" else ""))
                                              if args.flush_mib > 0 else "not flushed"),

@@ -792,8 +792,10 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
         if (lap) {
             for (int l = lane; l < R * copies; l += 32) mine[l] = 0.0;
             __syncwarp();
-            unsigned p = p0 + lane;
-            for (; p + (U - 1) * 32 < p1; p += U * 32) {
+            // warp-uniform trip count (the shuffles below need every lane)
+            unsigned base = p0;
+            for (; base + U * 32 <= p1; base += U * 32) {
+                const unsigned p = base + lane;
                 unsigned l[U];
                 double x[U];
 #pragma unroll
@@ -801,9 +803,19 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) x[u] = entry_w<WT>(a, p + u * 32);
 #pragma unroll
-                for (int u = 0; u < U; ++u) atomicAdd(mine + l[u] * copies + cp, x[u]);
+                for (int u = 0; u < U; ++u) {
+                    // a row-sorted input gives a warp 32 entries of one row: one
+                    // shuffle reduction and a single add instead of 32 colliding CAS
+                    const unsigned l0 = __shfl_sync(0xffffffffu, l[u], 0);
+                    if (__all_sync(0xffffffffu, l[u] == l0)) {
+                        const double sum = warp_sum(x[u]);
+                        if (lane == 0) atomicAdd(mine + l0 * copies, sum);
+                    } else {
+                        atomicAdd(mine + l[u] * copies + cp, x[u]);
+                    }
+                }
             }
-            for (; p < p1; p += 32) {
+            for (unsigned p = base + lane; p < p1; p += 32) {
                 GEE_DASSERT((int)(a.ws.keys2[p] >> cb) < R);
                 atomicAdd(mine + (__ldcs(a.ws.keys2 + p) >> cb) * copies + cp, entry_w<WT>(a, p));
             }
@@ -1021,6 +1033,21 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
     auto consume = [&](const uint32_t(&kk)[U], const XT(&x)[U], int s) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+            if (K <= 8 && __all_sync(0xffffffffu, kk[u] != 0xffffffffu)) {
+                // few classes and a row-sorted input: every lane of the warp
+                // on one row collides on K words -- reduce per class instead
+                const unsigned lr0 = __shfl_sync(0xffffffffu, kk[u] >> cb, 0);
+                if (__all_sync(0xffffffffu, (kk[u] >> cb) == lr0)) {
+                    const double2 rc = stage[(s * U + u) * NT + threadIdx.x];
+                    const int y = rec_label(rc);
+                    const double v = (WT == GEE_W_UNIT ? 1.0 : (double)x[u]) * rc.y;
+                    for (int c = 0; c < K; ++c) {
+                        const double t = warp_sum(y == c ? v : 0.0);
+                        if ((threadIdx.x & 31) == 0 && t != 0.0) atomicAdd(zt + lr0 * K + c, t);
+                    }
+                    continue;
+                }
+            }
             if (kk[u] == 0xffffffffu) continue;
             const double2 rc = stage[(s * U + u) * NT + threadIdx.x];
             const int y = rec_label(rc);

@@ -260,7 +260,8 @@ def encode(adj, labels, opts=None, *, out: str = "numpy", dtype=torch.float64):
     labels = _labels_of(labels)
     flags = options_flags(opts)
     dev = _device.require_gpu()
-    if hasattr(adj, "index_pointers"):
+    # (a CsrMatrix's reference-named fields are host copies: never touch them here)
+    if isinstance(adj, CsrMatrix) or (not isinstance(adj, EdgeList) and hasattr(adj, "index_pointers")):
         z = _encode_csr(CsrMatrix.coerce(adj, dev), labels, flags, dev)
         if dtype == torch.float32:
             z = z.to(torch.float32)
