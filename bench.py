@@ -58,7 +58,8 @@ def parse():
     p.add_argument("--stream-variant", type=int, default=0,
                    help="debug A/B of the stream embed (results wrong by design): 1 no shared atomics, 2 no gathers")
     p.add_argument("--stream-tile-kb", type=int, default=0, help="debug: KB of the stream encode's Z tile")
-    p.add_argument("--stream-nt", type=int, default=0, help="debug: threads per stream embed CTA (128/256/512)")
+    p.add_argument("--stream-nt", type=int, default=None,
+                   help="debug: stream embed kernel: 0 warp-specialised, else threads per CTA (128/256/512)")
     p.add_argument("--no-stream", action="store_true",
                    help="debug: disable the bucketed stream encode (gee_debug_set GEE_DEBUG_STREAM=1): exact CSR path")
     p.add_argument("--eager", action="store_true", help="launch kernels one by one instead of a CUDA graph")
@@ -564,7 +565,7 @@ def run_b200(args):
         lib.gee_debug_set(_lib.DEBUG_STREAM, 1)
     if args.stream_tile_kb:
         lib.gee_debug_set(5, args.stream_tile_kb)
-    if args.stream_nt:
+    if args.stream_nt is not None:
         lib.gee_debug_set(6, args.stream_nt)
     if args.stream_variant:
         lib.gee_debug_set(_lib.DEBUG_STREAM, 16 + args.stream_variant)

@@ -157,8 +157,12 @@ struct StWs {
     unsigned *label_partial;
 };
 constexpr int kCtlHist1 = 0, kCtlBase1 = 256, kCtlCur1 = 520, kCtlItems = 776, kCtlWork = 777, kCtlLabel = 780,
-              kCtlDItems = 781, kCtlSplit = 782;
-constexpr int kCtlWords = 784;
+              kCtlDItems = 781, kCtlSplit = 782, kCtlWLow = 783, kCtlWHigh = 784;
+// kCtlWLow / kCtlWHigh: min over nonzero weights of the exponent of the lowest
+// set bit, and max of ilogb(w) + 1 (both + kExpBias, so unsigned atomicMin/Max
+// order them): every weight is a multiple of 2^low and below 2^high
+constexpr int kCtlWords = 788;
+constexpr int kExpBias = 4096;
 
 size_t carve(Carver &cv, StWs &w, const StGeo &g) {
     const size_t wb = g.wt == GEE_W_F64 ? 8 : g.wt == GEE_W_F32 ? 4 : 0;
@@ -265,6 +269,24 @@ __device__ __forceinline__ void load_weight(const StArgs &a, int64_t i, typename
     }
 }
 
+// Exponent of the lowest set bit of |w| and an exclusive power-of-two bound
+// (|w| < 2^hi), from the bits (w finite, nonzero).
+__device__ __forceinline__ void weight_exponents(float w, int &lo, int &hi) {
+    const unsigned b = __float_as_uint(w) & 0x7fffffffu;
+    const int e = (int)(b >> 23);
+    const unsigned m = b & 0x7fffffu;
+    lo = e == 0 ? -150 + __ffs(m) : e - 151 + __ffs(m | 0x800000u);
+    hi = e == 0 ? -126 : e - 126;
+}
+__device__ __forceinline__ void weight_exponents(double w, int &lo, int &hi) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(w) & 0x7fffffffffffffffull;
+    const int e = (int)(b >> 52);
+    const unsigned long long m = b & ((1ull << 52) - 1);
+    lo = e == 0 ? -1075 + __ffsll((long long)m) : e - 1076 + __ffsll((long long)(m | (1ull << 52)));
+    hi = e == 0 ? -1022 : e - 1022;
+}
+__device__ __forceinline__ void weight_exponents(char, int &lo, int &hi) { lo = hi = 0; }
+
 // ---- pass H: 8-bit MSD digit histogram --------------------------------------
 __global__ void __launch_bounds__(kStNT) k_st_hist1(StArgs a) {
     __shared__ unsigned cnt[256];
@@ -362,6 +384,7 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part1(StArgs a) {
     const int64_t tile_edges = (int64_t)EPT * kStNT;
     const int64_t ntiles = (a.E + tile_edges - 1) / tile_edges;
     int errbits = 0;
+    int elow = INT_MAX / 2, ehigh = -INT_MAX / 2;  // weight exponent range (k_st_degree's integer mode)
     // software pipeline: the next tile's edges are loaded as soon as this
     // tile's entries sit in shared memory, and fly during the write-out
     long long r[EPT], c[EPT];
@@ -399,6 +422,12 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part1(StArgs a) {
                     wv[u] = 0;
                 } else if (wv[u] < 0 && (a.flags & GEE_NONNEG)) {
                     errbits |= GEE_ERR_NEG_WEIGHT;
+                }
+                if (wv[u] != 0) {
+                    int lo, hi;
+                    weight_exponents(wv[u], lo, hi);
+                    elow = min(elow, lo);
+                    ehigh = max(ehigh, hi);
                 }
             }
             if (bad) {
@@ -452,6 +481,16 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part1(StArgs a) {
         __syncthreads();
     }
     if (errbits) raise_err(a.err, errbits);
+    if constexpr (WT != GEE_W_UNIT) {
+        for (int o = 16; o > 0; o >>= 1) {
+            elow = min(elow, __shfl_xor_sync(0xffffffffu, elow, o));
+            ehigh = max(ehigh, __shfl_xor_sync(0xffffffffu, ehigh, o));
+        }
+        if ((threadIdx.x & 31) == 0 && ehigh > -INT_MAX / 2) {
+            atomicMin(a.ws.ctl + kCtlWLow, (unsigned)(elow + kExpBias));
+            atomicMax(a.ws.ctl + kCtlWHigh, (unsigned)(ehigh + kExpBias));
+        }
+    }
 }
 
 // ---- bucket histogram over the digit-ordered list ---------------------------
@@ -767,18 +806,47 @@ __device__ __forceinline__ void zero_scratch(const StArgs &a, unsigned b, int nr
 // (and clears the bucket's embed scratch tile when the embed splits it too).
 template <int WT>
 __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
-    extern __shared__ double wdeg[];  // [kDegNT / 32][R][copies]
+    extern __shared__ double wdeg[];  // [kDegNT / 32][R][copies] f64, or [kDegNT / 32][2][R] u32 (integer mode)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int R = 1 << a.lrow_bits;
     const bool lap = (a.flags & GEE_LAPLACIAN) != 0;
     const unsigned n_items = a.ws.ctl[kCtlDItems];
     const int cb = a.col_bits;
-    // `copies` interleaved partial sums per row (lane & (copies - 1) picks one):
-    // skewed graphs put many lanes of a warp on the same row, and every lane
-    // colliding on one shared f64 word costs a CAS retry
-    const int copies = a.deg_copies;
+    // Integer mode: when every weight is a multiple of 2^low and the total of
+    // all entries stays below 2^62 after scaling by 2^-low (unit weights;
+    // configs[3]'s float32 weights are multiples of 2^-24), degrees are exact
+    // 64-bit fixed-point sums kept as two native 32-bit shared atomics per
+    // add (lo, and hi on a carry) -- no CAS retries on hot rows, and the
+    // reference's fold bits whenever the total fits 53 bits.
+    int q = 0;
+    bool imode = WT == GEE_W_UNIT;
+    if constexpr (WT != GEE_W_UNIT) {
+        const unsigned lo = a.ws.ctl[kCtlWLow], hi = a.ws.ctl[kCtlWHigh];
+        const unsigned M = a.ws.ctl[kCtlBase1 + 256];
+        if (lo == 0xffffffffu) {
+            imode = true;  // no nonzero weight
+        } else {
+            const int elow = (int)lo - kExpBias, ehigh = (int)hi - kExpBias;
+            int mbits = 0;
+            while ((1u << mbits) < M && mbits < 32) ++mbits;
+            imode = elow > -1000 && ehigh - elow + mbits <= 62;
+            q = -elow;
+        }
+    }
+    const int copies = imode ? 1 : a.deg_copies;
     double *mine = wdeg + (size_t)wid * R * copies;
+    unsigned *ilo = reinterpret_cast<unsigned *>(wdeg) + (size_t)wid * 2 * R, *ihi = ilo + R;
     const int cp = lane & (copies - 1);
+    unsigned long long *gdeg = reinterpret_cast<unsigned long long *>(a.ws.deg);
+    auto to_fixed = [&](double x) -> unsigned long long { return (unsigned long long)ldexp(x, q); };
+    auto iadd = [&](unsigned l, unsigned long long v) {
+        const unsigned vlo = (unsigned)v, vhi = (unsigned)(v >> 32);
+        const unsigned old = atomicAdd(ilo + l, vlo);
+        const unsigned carry = (old + vlo) < old;
+        if (vhi + carry) atomicAdd(ihi + l, vhi + carry);
+    };
+    auto ival = [&](int l) -> unsigned long long { return ((unsigned long long)ihi[l] << 32) + ilo[l]; };
+    auto fdeg = [&](unsigned long long v) -> double { return ldexp((double)v, -q); };
     constexpr int U = 8;
     for (unsigned item = (blockIdx.x * kDegNT + threadIdx.x) >> 5; item < n_items;
          item += (gridDim.x * kDegNT) >> 5) {
@@ -790,7 +858,11 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
         const int64_t r0 = (int64_t)b << a.lrow_bits;  // local row of the bucket
         const int nrows = (int)min((int64_t)R, a.nloc - r0);
         if (lap) {
-            for (int l = lane; l < R * copies; l += 32) mine[l] = 0.0;
+            if (imode) {
+                for (int l = lane; l < 2 * R; l += 32) ilo[l] = 0u;
+            } else {
+                for (int l = lane; l < R * copies; l += 32) mine[l] = 0.0;
+            }
             __syncwarp();
             // warp-uniform trip count (the shuffles below need every lane)
             unsigned base = p0;
@@ -805,9 +877,18 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     // a row-sorted input gives a warp 32 entries of one row: one
-                    // shuffle reduction and a single add instead of 32 colliding CAS
+                    // shuffle reduction and a single add instead of 32 colliding adds
                     const unsigned l0 = __shfl_sync(0xffffffffu, l[u], 0);
-                    if (__all_sync(0xffffffffu, l[u] == l0)) {
+                    const bool uni = __all_sync(0xffffffffu, l[u] == l0);
+                    if (imode) {
+                        unsigned long long v = to_fixed(x[u]);
+                        if (uni) {
+                            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                            if (lane == 0) iadd(l0, v);
+                        } else {
+                            iadd(l[u], v);
+                        }
+                    } else if (uni) {
                         const double sum = warp_sum(x[u]);
                         if (lane == 0) atomicAdd(mine + l0 * copies, sum);
                     } else {
@@ -816,27 +897,38 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
                 }
             }
             for (unsigned p = base + lane; p < p1; p += 32) {
-                GEE_DASSERT((int)(a.ws.keys2[p] >> cb) < R);
-                atomicAdd(mine + (__ldcs(a.ws.keys2 + p) >> cb) * copies + cp, entry_w<WT>(a, p));
+                const unsigned l = __ldcs(a.ws.keys2 + p) >> cb;
+                GEE_DASSERT((int)l < R);
+                if (imode) iadd(l, to_fixed(entry_w<WT>(a, p)));
+                else atomicAdd(mine + l * copies + cp, entry_w<WT>(a, p));
             }
             __syncwarp();
-            for (int l = lane; l < R; l += 32) {
-                double d = 0.0;
-                for (int c = 0; c < copies; ++c) d += mine[l * copies + c];
-                mine[l * copies] = d;
+            if (!imode) {
+                for (int l = lane; l < R; l += 32) {
+                    double d = 0.0;
+                    for (int c = 0; c < copies; ++c) d += mine[l * copies + c];
+                    mine[l * copies] = d;
+                }
+                __syncwarp();
             }
-            __syncwarp();
         }
         if (nitems == 1) {
             for (int l = lane; l < nrows; l += 32) {
-                const double d = lap ? mine[l * copies] : 0.0;
+                const double d = !lap ? 0.0 : imode ? fdeg(ival(l)) : mine[l * copies];
                 if (a.deg_out) a.deg_out[r0 + l] = d;
                 else finish_node(a, a.row0 + r0 + l, d);
             }
         } else {
-            if (lap)
-                for (int l = lane; l < nrows; l += 32)
-                    if (mine[l * copies] != 0.0) atomicAdd(a.ws.deg + r0 + l, mine[l * copies]);
+            if (lap) {
+                for (int l = lane; l < nrows; l += 32) {
+                    if (imode) {
+                        const unsigned long long v = ival(l);
+                        if (v) atomicAdd(gdeg + r0 + l, v);
+                    } else if (mine[l * copies] != 0.0) {
+                        atomicAdd(a.ws.deg + r0 + l, mine[l * copies]);
+                    }
+                }
+            }
             __threadfence();
             __syncwarp();
             unsigned last = 0;
@@ -845,7 +937,7 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
             if (last) {
                 __threadfence();
                 for (int l = lane; l < nrows; l += 32) {
-                    const double d = lap ? __ldcg(a.ws.deg + r0 + l) : 0.0;
+                    const double d = !lap ? 0.0 : imode ? fdeg(__ldcg(gdeg + r0 + l)) : __ldcg(a.ws.deg + r0 + l);
                     if (a.deg_out) a.deg_out[r0 + l] = d;
                     else finish_node(a, a.row0 + r0 + l, d);
                 }
@@ -873,7 +965,8 @@ __global__ void k_st_nodes(StArgs a, const double *deg_all) {
 //     row factor (rows r0 .. r0+nrows are adjacent in Z).
 template <bool OUT32, int NT>
 __device__ __forceinline__ void tile_epilogue(const StArgs &a, double *zt, double *fac, const double2 *drec,
-                                              int64_t r0, int nrows) {
+                                              int64_t r0, int nrows, int tid = -1) {
+    if (tid < 0) tid = threadIdx.x;  // thread index inside the NT threads doing the epilogue
     // One pass per row, L lanes per row (no CTA barrier): the A+I term g_r at
     // the row's own label, the factor f_r = s_r (Laplacian) times
     // 1/||s_r z_r|| (correlation; one division per row -- z * (1/nrm) is
@@ -883,12 +976,12 @@ __device__ __forceinline__ void tile_epilogue(const StArgs &a, double *zt, doubl
     const int K = a.k;
     const unsigned flags = a.flags;
     const int L = K >= 256 ? 32 : K >= 128 ? 16 : K >= 64 ? 8 : K >= 24 ? 4 : K >= 8 ? 2 : 1;
-    const int sub = threadIdx.x % L;
-    const unsigned gmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << ((threadIdx.x & 31) & ~(L - 1)));
+    const int sub = tid % L;
+    const unsigned gmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << ((tid & 31) & ~(L - 1)));
     const int groups = NT / L;
     const int iters = (nrows + groups - 1) / groups;  // uniform per warp: shuffles stay converged
     for (int it = 0; it < iters; ++it) {
-        const int l = it * groups + (int)threadIdx.x / L;
+        const int l = it * groups + tid / L;
         const bool live = l < nrows;
         double *row = zt + (size_t)l * K;
         double s_r = 1.0;
@@ -1165,6 +1258,239 @@ int set_smem(T *kern, size_t bytes) {
     return e == cudaSuccess ? GEE_OK : cuda_status(e);
 }
 
+// ---- warp-specialised embed ------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    unsigned ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P1;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void group_sync(int id) { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
+
+constexpr int kWsNT = 256;  // warps 0-3 accumulate, warps 4-7 run the epilogue
+
+// The fused embed, warp-specialised: four warps accumulate bucket i into one
+// of two shared Z tiles while the other four finish bucket i-1 from the
+// other tile (factors, streaming stores, zeroing), handing tiles over with
+// mbarriers (FULL: accumulated, EMPTY: zeroed).  The accumulating warps
+// stream entries through the two-stage record pipeline of k_st_embed and
+// request the next bucket's first stages as soon as they hand a tile over.
+template <int WT, bool OUT32>
+__global__ void __launch_bounds__(kWsNT, 2) k_st_embed_ws(StArgs a) {
+    constexpr int U = 4, NA = 128;
+    using XT = typename std::conditional<WT == GEE_W_UNIT, float, typename WTraits<WT>::T>::type;
+    extern __shared__ __align__(16) double wsm[];
+    __shared__ unsigned long long full_bar[2], empty_bar[2];
+    __shared__ unsigned meta[2][4];  // bucket, p0, p1, items of the bucket (~0: no more work)
+    __shared__ unsigned s_next[4];
+    __shared__ unsigned s_flag;
+    const int R = 1 << a.lrow_bits;
+    const int K = a.k;
+    const size_t ts = ((size_t)R * K + 1) & ~(size_t)1;
+    const size_t r2 = ((size_t)R + 1) & ~(size_t)1;
+    // per-buffer sections, selected with ternaries (no local-memory arrays)
+    double *const tile0 = wsm, *const tile1 = wsm + ts;
+    double *const fac0 = wsm + 2 * ts, *const fac1 = wsm + 2 * ts + r2;
+    double2 *const drec0 = reinterpret_cast<double2 *>(wsm + 2 * ts + 2 * r2), *const drec1 = drec0 + R;
+    double2 *stage = reinterpret_cast<double2 *>(wsm + 2 * ts + 2 * r2) + 2 * R;  // [2][U][NA]
+    const unsigned n_items = a.ws.ctl[kCtlItems];
+    const unsigned cmask = (1u << a.col_bits) - 1u;
+    const int cb = a.col_bits;
+    for (size_t i = threadIdx.x; i < ts; i += kWsNT) {
+        tile0[i] = 0.0;
+        tile1[i] = 0.0;
+    }
+    if (threadIdx.x == 0) {
+        mbar_init(&full_bar[0], NA);
+        mbar_init(&full_bar[1], NA);
+        mbar_init(&empty_bar[0], kWsNT - NA);
+        mbar_init(&empty_bar[1], kWsNT - NA);
+    }
+    __syncthreads();
+    if (threadIdx.x < NA) {
+        // ------------------------------------------------ accumulating warps
+        const int t = threadIdx.x;
+        const unsigned step = U * NA;
+        uint32_t kA[U], kB[U];
+        XT xA[U], xB[U];
+        auto loadk = [&](unsigned base, unsigned end, uint32_t(&kk)[U], XT(&x)[U]) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const unsigned p = base + u * NA + t;
+                kk[u] = 0xffffffffu;
+                if (p < end) {
+                    kk[u] = __ldcs(a.ws.keys2 + p);
+                    if constexpr (WT != GEE_W_UNIT) x[u] = __ldcs(reinterpret_cast<const XT *>(a.ws.w2) + p);
+                }
+            }
+        };
+        auto gather = [&](const uint32_t(&kk)[U], int s) {
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (kk[u] != 0xffffffffu) cp_async16(stage + (s * U + u) * NA + t, a.ws.rec + (kk[u] & cmask));
+            cp_async_commit();
+        };
+        auto consume = [&](double *zt, const uint32_t(&kk)[U], const XT(&x)[U], int s) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (kk[u] == 0xffffffffu) continue;
+                const double2 rc = stage[(s * U + u) * NA + t];
+                const int y = rec_label(rc);
+                const double xv = WT == GEE_W_UNIT ? 1.0 : (double)x[u];
+                GEE_DASSERT((int)(kk[u] >> cb) < R && y < K);
+                if (y >= 0) atomicAdd(zt + (kk[u] >> cb) * K + y, xv * rc.y);
+            }
+        };
+        auto grab = [&]() {  // thread 0: next item's descriptor into s_next
+            const unsigned item = atomicAdd(a.ws.ctl + kCtlWork + 1, 1u);
+            const uint4 d = item < n_items ? a.ws.item_desc[item] : make_uint4(0xffffffffu, 0, 0, 0);
+            s_next[0] = d.x;
+            s_next[1] = d.y;
+            s_next[2] = d.z;
+            s_next[3] = d.w;
+        };
+        if (t == 0) grab();
+        group_sync(1);
+        unsigned cur[4] = {s_next[0], s_next[1], s_next[2], s_next[3]};
+        group_sync(1);
+        if (cur[0] != 0xffffffffu) {
+            loadk(cur[1], cur[2], kA, xA);
+            loadk(cur[1] + step, cur[2], kB, xB);
+            gather(kA, 0);
+            gather(kB, 1);
+        }
+        for (unsigned it = 0;; ++it) {
+            const int b = it & 1;
+            if (it >= 2) mbar_wait(&empty_bar[b], ((it >> 1) - 1) & 1);  // tile b zeroed
+            if (cur[0] == 0xffffffffu) {
+                if (t == 0) meta[b][0] = 0xffffffffu;
+                mbar_arrive(&full_bar[b]);
+                break;
+            }
+            if (t == 0) grab();  // its loads overlap this bucket's accumulation
+            const unsigned p0 = cur[1], p1 = cur[2];
+            double *zt = b ? tile1 : tile0;
+            for (unsigned base = p0; base < p1; base += 2 * step) {
+                const bool hb = base + step < p1, ha = base + 2 * step < p1;
+                if (hb) cp_async_wait<1>();
+                else cp_async_wait<0>();
+                consume(zt, kA, xA, 0);
+                if (ha) {
+                    loadk(base + 2 * step, p1, kA, xA);
+                    gather(kA, 0);
+                }
+                if (hb) {
+                    if (ha) cp_async_wait<1>();
+                    else cp_async_wait<0>();
+                    consume(zt, kB, xB, 1);
+                    if (base + 3 * step < p1) {
+                        loadk(base + 3 * step, p1, kB, xB);
+                        gather(kB, 1);
+                    }
+                }
+            }
+            if (t == 0) {
+                meta[b][0] = cur[0];
+                meta[b][1] = cur[1];
+                meta[b][2] = cur[2];
+                meta[b][3] = cur[3];
+            }
+            group_sync(1);  // every accumulation into tile b done; s_next visible
+            mbar_arrive(&full_bar[b]);
+            for (int q = 0; q < 4; ++q) cur[q] = s_next[q];
+            group_sync(1);  // s_next read before thread 0 overwrites it
+            if (cur[0] != 0xffffffffu) {
+                loadk(cur[1], cur[2], kA, xA);
+                loadk(cur[1] + step, cur[2], kB, xB);
+                gather(kA, 0);
+                gather(kB, 1);
+            }
+        }
+        cp_async_wait<0>();
+    } else {
+        // ------------------------------------------------ epilogue warps
+        const int t = threadIdx.x - NA;
+        for (unsigned it = 0;; ++it) {
+            const int b = it & 1;
+            mbar_wait(&full_bar[b], (it >> 1) & 1);
+            const unsigned bk = meta[b][0];
+            if (bk == 0xffffffffu) break;
+            const unsigned nitems = meta[b][3];
+            const int64_t r0 = (int64_t)bk << a.lrow_bits;
+            const int nrows = (int)min((int64_t)R, a.nloc - r0);
+            const int tsz = nrows * K;
+            double *const fb = b ? fac1 : fac0;
+            double2 *const db = b ? drec1 : drec0;
+            for (int l = t; l < nrows; l += kWsNT - NA) {
+                if (a.flags & GEE_LAPLACIAN) fb[l] = a.ws.scale[a.row0 + r0 + l];
+                if (a.flags & GEE_DIAGONAL) db[l] = a.ws.rec[a.row0 + r0 + l];
+            }
+            group_sync(2);
+            double *zt = b ? tile1 : tile0;
+            if (nitems == 1) {
+                tile_epilogue<OUT32, kWsNT - NA>(a, zt, fb, db, r0, nrows, t);
+            } else {
+                GEE_DASSERT(a.ws.split_slot[bk] < a.ws.ctl[kCtlSplit]);
+                double *zs = a.ws.scratch + (size_t)a.ws.split_slot[bk] * ((size_t)R * K);
+                for (int i = t; i < tsz; i += kWsNT - NA) {
+                    const double v = zt[i];
+                    if (v != 0.0) {
+                        atomicAdd(zs + i, v);
+                        zt[i] = 0.0;
+                    }
+                }
+                __threadfence();
+                group_sync(2);
+                if (t == 0) s_flag = atomicAdd(a.ws.done_emb + bk, 1u) == nitems - 1;
+                group_sync(2);
+                if (s_flag) {
+                    __threadfence();
+                    for (int i = t; i < tsz; i += kWsNT - NA) zt[i] = __ldcg(zs + i);
+                    group_sync(2);
+                    tile_epilogue<OUT32, kWsNT - NA>(a, zt, fb, db, r0, nrows, t);
+                }
+            }
+            group_sync(2);  // tile b zeroed, fac/drec of b read
+            mbar_arrive(&empty_bar[b]);
+        }
+    }
+}
+
+template <int WT>
+int launch_embed_ws(const StGeo &g, const StArgs &a, bool out32, cudaStream_t st) {
+    static PerDevice attr;
+    const size_t R = (size_t)1 << g.lrow_bits;
+    const size_t ts = (R * (size_t)g.k + 1) & ~(size_t)1, r2 = (R + 1) & ~(size_t)1;
+    const size_t smem = sizeof(double) * (2 * ts + 2 * r2) + 2 * R * 16 + (size_t)2 * 4 * 128 * 16;
+    const size_t smax = 226 * 1024;  // per-CTA maximum less the static barriers; the launch uses `smem`
+    if (!attr.done()) {
+        int rc;
+        if ((rc = set_smem(k_st_embed_ws<WT, false>, smax))) return rc;
+        if ((rc = set_smem(k_st_embed_ws<WT, true>, smax))) return rc;
+        attr.mark();
+    }
+    int occ = 1;
+    if (out32) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_st_embed_ws<WT, true>, kWsNT, smem);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_st_embed_ws<WT, false>, kWsNT, smem);
+    if (occ < 1) occ = 1;
+    if (out32) k_st_embed_ws<WT, true><<<num_sms() * occ, kWsNT, smem, st>>>(a);
+    else k_st_embed_ws<WT, false><<<num_sms() * occ, kWsNT, smem, st>>>(a);
+    return GEE_OK;
+}
+
 template <int WT, int NT>
 int launch_embed(const StGeo &g, const StArgs &a, bool out32, cudaStream_t st) {
     static PerDevice attr;
@@ -1237,7 +1563,8 @@ int run_phase2(const StGeo &g, StArgs &a, const double *deg_all, bool shard, cud
     }
     const bool out32 = (a.flags & GEE_FP32) != 0;
     int rc2;
-    if (t_emb_nt == 128) rc2 = launch_embed<WT, 128>(g, a, out32, st);
+    if (t_emb_nt == 0) rc2 = launch_embed_ws<WT>(g, a, out32, st);
+    else if (t_emb_nt == 128) rc2 = launch_embed<WT, 128>(g, a, out32, st);
     else if (t_emb_nt == 512) rc2 = launch_embed<WT, 512>(g, a, out32, st);
     else rc2 = launch_embed<WT, 256>(g, a, out32, st);
     if (rc2) return rc2;
@@ -1261,7 +1588,7 @@ int set_stream_tile_kb(int v) {
 
 int set_stream_embed_nt(int v) {
     const int old = t_emb_nt;
-    t_emb_nt = (v == 256 || v == 512) ? v : 128;
+    t_emb_nt = (v == 0 || v == 256 || v == 512) ? v : 128;  // 0: warp-specialised
     return old;
 }
 
@@ -1329,6 +1656,7 @@ static int setup(StGeo &g, StWs &W, void *ws, size_t ws_bytes, const int64_t *la
     Carver cv(ws);
     if (carve(cv, W, g) > ws_bytes || !ws) return GEE_E_WORKSPACE;
     GEE_CHECK_CUDA(cudaMemsetAsync(W.ctl, 0, sizeof(unsigned) * kCtlWords, st));
+    GEE_CHECK_CUDA(cudaMemsetAsync(W.ctl + kCtlWLow, 0xff, sizeof(unsigned), st));
     GEE_CHECK_CUDA(cudaMemsetAsync(W.hist2, 0, sizeof(unsigned) * ((size_t)g.S + 1), st));
     if (g.flags & GEE_LAPLACIAN) GEE_CHECK_CUDA(cudaMemsetAsync(W.deg, 0, sizeof(double) * (size_t)g.nloc, st));
     return label_hist_pipeline(labels, g.N, g.k, W.y32, W.counts, W.inv, W.label_partial, W.ctl + kCtlLabel, err, st);
