@@ -818,8 +818,11 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
     // 64-bit fixed-point sums kept as two native 32-bit shared atomics per
     // add (lo, and hi on a carry) -- no CAS retries on hot rows, and the
     // reference's fold bits whenever the total fits 53 bits.
+    // When every scaled weight is below 2^16 (unit weights) an item's sum
+    // (<= kDegItem entries) stays below 2^28, so one native non-returning
+    // 32-bit reduction per add is exact.
     int q = 0;
-    bool imode = WT == GEE_W_UNIT;
+    bool imode = WT == GEE_W_UNIT, small = WT == GEE_W_UNIT;
     if constexpr (WT != GEE_W_UNIT) {
         const unsigned lo = a.ws.ctl[kCtlWLow], hi = a.ws.ctl[kCtlWHigh];
         const unsigned M = a.ws.ctl[kCtlBase1 + 256];
@@ -831,6 +834,7 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
             while ((1u << mbits) < M && mbits < 32) ++mbits;
             imode = elow > -1000 && ehigh - elow + mbits <= 62;
             q = -elow;
+            small = ehigh - elow <= 16;
         }
     }
     const int copies = imode ? 1 : a.deg_copies;
@@ -840,12 +844,18 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
     unsigned long long *gdeg = reinterpret_cast<unsigned long long *>(a.ws.deg);
     auto to_fixed = [&](double x) -> unsigned long long { return (unsigned long long)ldexp(x, q); };
     auto iadd = [&](unsigned l, unsigned long long v) {
+        if (small) {
+            atomicAdd(ilo + l, (unsigned)v);  // result unused: a reduction
+            return;
+        }
         const unsigned vlo = (unsigned)v, vhi = (unsigned)(v >> 32);
         const unsigned old = atomicAdd(ilo + l, vlo);
         const unsigned carry = (old + vlo) < old;
         if (vhi + carry) atomicAdd(ihi + l, vhi + carry);
     };
-    auto ival = [&](int l) -> unsigned long long { return ((unsigned long long)ihi[l] << 32) + ilo[l]; };
+    auto ival = [&](int l) -> unsigned long long {
+        return small ? (unsigned long long)ilo[l] : ((unsigned long long)ihi[l] << 32) + ilo[l];
+    };
     auto fdeg = [&](unsigned long long v) -> double { return ldexp((double)v, -q); };
     constexpr int U = 8;
     for (unsigned item = (blockIdx.x * kDegNT + threadIdx.x) >> 5; item < n_items;
@@ -1078,6 +1088,143 @@ __device__ __forceinline__ void tile_epilogue(const StArgs &a, double *zt, doubl
     (void)fac;
 }
 
+// Epilogue geometry of a CTA, fixed for the kernel: L = 2^lgL lanes per row
+// in the factor pass; in the flat store pass thread t starts at element V*t
+// of the tile (row t0r, column t0c) and steps NT*V elements (dq rows + dr
+// columns) per iteration.
+struct EpiGeo {
+    int lgL, t0r, t0c, dq, dr;
+};
+template <int NT>
+__device__ __forceinline__ EpiGeo epi_geo(int K, int tid) {
+    EpiGeo g;
+    g.lgL = K >= 256 ? 5 : K >= 128 ? 4 : K >= 64 ? 3 : K >= 24 ? 2 : K >= 8 ? 1 : 0;
+    g.t0r = (2 * tid) / K;
+    g.t0c = 2 * tid - g.t0r * K;
+    g.dq = (2 * NT) / K;
+    g.dr = 2 * NT - g.dq * K;
+    return g;
+}
+
+// The fused epilogue of one R x K tile in two passes (NT threads, the caller
+// provides the CTA barrier `sync`):
+//  1. factor pass, L lanes per row: the A+I term g_r at the row's own label,
+//     f_r = s_r (Laplacian) times 1/||s_r z_r|| (correlation; one division
+//     per row -- z * (1/nrm) is within 1 ulp of the reference's z / nrm,
+//     embedding.py:140) into fac[r];
+//  2. flat store pass: the tile is rows r0 .. r0+nrows-1 of Z, one contiguous
+//     run of nrows*K elements in global memory, so every thread moves 16-byte
+//     units (two elements, their row tracked incrementally) from shared
+//     memory to Z with coalesced streaming stores and zeroes them behind.
+template <bool OUT32, int NT, class Sync>
+__device__ __forceinline__ void tile_epilogue_flat(const StArgs &a, double *zt, double *fac, const double2 *drec,
+                                                   int64_t r0, int nrows, const EpiGeo &eg, int tid, Sync sync) {
+    const int K = a.k;
+    const unsigned flags = a.flags;
+    const bool lap = (flags & GEE_LAPLACIAN) != 0, corr = (flags & GEE_CORRELATION) != 0;
+    const int L = 1 << eg.lgL;
+    const int sub = tid & (L - 1);
+    const unsigned gmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << ((tid & 31) & ~(L - 1)));
+    for (int l = tid >> eg.lgL; l < nrows; l += NT >> eg.lgL) {  // a group's L lanes share l
+        double *row = zt + (size_t)l * K;
+        const double s_r = lap ? fac[l] : 1.0;
+        if ((flags & GEE_DIAGONAL) && sub == 0) {
+            const double2 rc = drec[l];
+            const int y = rec_label(rc);
+            if (y >= 0) row[y] += rc.y;
+        }
+        if (!corr) {
+            if (!lap && sub == 0) fac[l] = 1.0;
+            continue;
+        }
+        __syncwarp(gmask);
+        // four independent chains (loads first) instead of one serial one
+        double s4[4] = {0.0, 0.0, 0.0, 0.0};
+        int c = sub;
+        for (; c + 3 * L < K; c += 4 * L) {
+            double v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = row[c + j * L];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const double t = v[j] * s_r;
+                s4[j] = fma(t, t, s4[j]);
+            }
+        }
+        for (; c < K; c += L) {
+            const double t = row[c] * s_r;
+            s4[0] = fma(t, t, s4[0]);
+        }
+        double ss = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+        bool fin = true;
+        if (!isfinite(ss)) {
+            // a non-finite element, or finite ones whose squares overflow
+            // (the reference raises only for the former, embedding.py:137-138)
+            for (int c2 = sub; c2 < K; c2 += L) fin &= isfinite(row[c2]);
+        }
+        for (int o = L >> 1; o > 0; o >>= 1) {
+            ss += __shfl_xor_sync(gmask, ss, o);
+            fin &= __shfl_xor_sync(gmask, (int)fin, o) != 0;
+        }
+        if (sub == 0) {
+            double f = s_r;
+            if (!fin) {
+                raise_err(a.err, GEE_ERR_NONFINITE);
+            } else {
+                const double nrm = __dsqrt_rn(ss);
+                if (nrm > 0.0) f = s_r * __ddiv_rn(1.0, nrm);
+            }
+            fac[l] = f;
+        }
+    }
+    sync();
+    const int tsz = nrows * K;
+    const int64_t zoff = r0 * K;
+    // 16-byte units need an even element offset into Z (r0 * K is even unless
+    // K and r0 are both odd) and a 16-byte aligned Z (any torch allocation)
+    const bool vec = ((reinterpret_cast<uintptr_t>(a.z) + (uintptr_t)zoff * (OUT32 ? 4 : 8)) & (OUT32 ? 7 : 15)) == 0;
+    if (vec) {
+        const int n = tsz >> 1;
+        int row = eg.t0r, col = eg.t0c;
+        for (int j = tid; j < n; j += NT) {
+            const int e = 2 * j;
+            const double f0 = fac[row];
+            const double f1 = col + 1 < K ? f0 : fac[row + 1];
+            double2 *zp = reinterpret_cast<double2 *>(zt + e);
+            const double2 v = *zp;
+            if (OUT32) {
+                __stcs(reinterpret_cast<float2 *>(reinterpret_cast<float *>(a.z) + zoff + e),
+                       make_float2((float)(v.x * f0), (float)(v.y * f1)));
+            } else {
+                __stcs(reinterpret_cast<double2 *>(reinterpret_cast<double *>(a.z) + zoff + e),
+                       make_double2(v.x * f0, v.y * f1));
+            }
+            *zp = make_double2(0.0, 0.0);
+            row += eg.dq;
+            col += eg.dr;
+            if (col >= K) {
+                col -= K;
+                ++row;
+            }
+        }
+        if ((tsz & 1) && tid == 0) {
+            const int e = tsz - 1;
+            const double v = zt[e] * fac[nrows - 1];
+            if (OUT32) __stcs(reinterpret_cast<float *>(a.z) + zoff + e, (float)v);
+            else __stcs(reinterpret_cast<double *>(a.z) + zoff + e, v);
+            zt[e] = 0.0;
+        }
+    } else {
+        for (int e = tid; e < tsz; e += NT) {
+            const int l = e / K;
+            const double v = zt[e] * fac[l];
+            if (OUT32) __stcs(reinterpret_cast<float *>(a.z) + zoff + e, (float)v);
+            else __stcs(reinterpret_cast<double *>(a.z) + zoff + e, v);
+            zt[e] = 0.0;
+        }
+    }
+}
+
 template <int WT, bool OUT32, int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
     constexpr int U = 4;  // entries per thread per stage; two stages in flight
@@ -1093,6 +1240,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
     const unsigned cmask = (1u << a.col_bits) - 1u;
     const int cb = a.col_bits;
     const unsigned step = U * NT;
+    const EpiGeo eg = epi_geo<NT>(K, threadIdx.x);
     // weights stay in their own type until consumed: a float -> double
     // conversion right after the load would wait for it
     using XT = typename std::conditional<WT == GEE_W_UNIT, float, typename WTraits<WT>::T>::type;
@@ -1211,7 +1359,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
             loadk(nq0 + step, nq1, kB, xB);
         }
         if (nitems == 1) {
-            tile_epilogue<OUT32, NT>(a, zt, fac, drec, r0, nrows);
+            tile_epilogue_flat<OUT32, NT>(a, zt, fac, drec, r0, nrows, eg, threadIdx.x, [] { __syncthreads(); });
         } else {
             GEE_DASSERT(a.ws.split_slot[b] < a.ws.ctl[kCtlSplit]);
             double *zs = a.ws.scratch + (size_t)a.ws.split_slot[b] * ((size_t)R * K);
@@ -1231,7 +1379,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
                 __threadfence();
                 for (int i = threadIdx.x; i < tsz; i += NT) zt[i] = __ldcg(zs + i);
                 __syncthreads();
-                tile_epilogue<OUT32, NT>(a, zt, fac, drec, r0, nrows);
+                tile_epilogue_flat<OUT32, NT>(a, zt, fac, drec, r0, nrows, eg, threadIdx.x, [] { __syncthreads(); });
             }
         }
         if (nxt) {
