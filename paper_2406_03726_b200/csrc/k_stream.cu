@@ -72,7 +72,7 @@ constexpr int kLrowMax = 9;  // at most 512 rows per bucket (per-warp degree cop
 
 int t_stream_mode = 0;  // debug hook: 0 auto, 1 never, >= 16 embed A/B variant
 
-// debug phase trace of the embed (variant 9): per CTA, clock64 totals of
+// debug phase trace of the embed (variant bit 16): per CTA, clock64 totals of
 // [0] start-of-item wait, [1] accumulation, [2] tile barrier, [3] epilogue,
 // [4] items, [5] entries
 constexpr int kTraceSlots = 8;
@@ -151,6 +151,7 @@ struct StWs {
     void *w2;
     double *deg, *scale;
     double2 *rec;   // node record {bits of Y_r (-1 unlabeled), g_r = s_r / n_{Y_r}}
+    double *zeros;  // a zeroed Z tile: source of the embed's bulk re-zeroing
     int32_t *y32;
     int64_t *counts;
     double *inv;
@@ -188,6 +189,7 @@ size_t carve(Carver &cv, StWs &w, const StGeo &g) {
     w.deg = cv.take<double>((size_t)g.nloc);
     w.scale = cv.take<double>((size_t)g.N);
     w.rec = cv.take<double2>((size_t)g.N);
+    w.zeros = cv.take<double>(((size_t)1 << g.lrow_bits) * (size_t)g.k + 2);
     w.y32 = cv.take<int32_t>((size_t)g.N + 1);
     w.counts = cv.take<int64_t>((size_t)g.k);
     w.inv = cv.take<double>((size_t)g.k);
@@ -1088,325 +1090,6 @@ __device__ __forceinline__ void tile_epilogue(const StArgs &a, double *zt, doubl
     (void)fac;
 }
 
-// Epilogue geometry of a CTA, fixed for the kernel: L = 2^lgL lanes per row
-// in the factor pass; in the flat store pass thread t starts at element V*t
-// of the tile (row t0r, column t0c) and steps NT*V elements (dq rows + dr
-// columns) per iteration.
-struct EpiGeo {
-    int lgL, t0r, t0c, dq, dr;
-};
-template <int NT>
-__device__ __forceinline__ EpiGeo epi_geo(int K, int tid) {
-    EpiGeo g;
-    g.lgL = K >= 256 ? 5 : K >= 128 ? 4 : K >= 64 ? 3 : K >= 24 ? 2 : K >= 8 ? 1 : 0;
-    g.t0r = (2 * tid) / K;
-    g.t0c = 2 * tid - g.t0r * K;
-    g.dq = (2 * NT) / K;
-    g.dr = 2 * NT - g.dq * K;
-    return g;
-}
-
-// The fused epilogue of one R x K tile in two passes (NT threads, the caller
-// provides the CTA barrier `sync`):
-//  1. factor pass, L lanes per row: the A+I term g_r at the row's own label,
-//     f_r = s_r (Laplacian) times 1/||s_r z_r|| (correlation; one division
-//     per row -- z * (1/nrm) is within 1 ulp of the reference's z / nrm,
-//     embedding.py:140) into fac[r];
-//  2. flat store pass: the tile is rows r0 .. r0+nrows-1 of Z, one contiguous
-//     run of nrows*K elements in global memory, so every thread moves 16-byte
-//     units (two elements, their row tracked incrementally) from shared
-//     memory to Z with coalesced streaming stores and zeroes them behind.
-template <bool OUT32, int NT, class Sync>
-__device__ __forceinline__ void tile_epilogue_flat(const StArgs &a, double *zt, double *fac, const double2 *drec,
-                                                   int64_t r0, int nrows, const EpiGeo &eg, int tid, Sync sync) {
-    const int K = a.k;
-    const unsigned flags = a.flags;
-    const bool lap = (flags & GEE_LAPLACIAN) != 0, corr = (flags & GEE_CORRELATION) != 0;
-    const int L = 1 << eg.lgL;
-    const int sub = tid & (L - 1);
-    const unsigned gmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << ((tid & 31) & ~(L - 1)));
-    for (int l = tid >> eg.lgL; l < nrows; l += NT >> eg.lgL) {  // a group's L lanes share l
-        double *row = zt + (size_t)l * K;
-        const double s_r = lap ? fac[l] : 1.0;
-        if ((flags & GEE_DIAGONAL) && sub == 0) {
-            const double2 rc = drec[l];
-            const int y = rec_label(rc);
-            if (y >= 0) row[y] += rc.y;
-        }
-        if (!corr) {
-            if (!lap && sub == 0) fac[l] = 1.0;
-            continue;
-        }
-        __syncwarp(gmask);
-        // four independent chains (loads first) instead of one serial one
-        double s4[4] = {0.0, 0.0, 0.0, 0.0};
-        int c = sub;
-        for (; c + 3 * L < K; c += 4 * L) {
-            double v[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) v[j] = row[c + j * L];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const double t = v[j] * s_r;
-                s4[j] = fma(t, t, s4[j]);
-            }
-        }
-        for (; c < K; c += L) {
-            const double t = row[c] * s_r;
-            s4[0] = fma(t, t, s4[0]);
-        }
-        double ss = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-        bool fin = true;
-        if (!isfinite(ss)) {
-            // a non-finite element, or finite ones whose squares overflow
-            // (the reference raises only for the former, embedding.py:137-138)
-            for (int c2 = sub; c2 < K; c2 += L) fin &= isfinite(row[c2]);
-        }
-        for (int o = L >> 1; o > 0; o >>= 1) {
-            ss += __shfl_xor_sync(gmask, ss, o);
-            fin &= __shfl_xor_sync(gmask, (int)fin, o) != 0;
-        }
-        if (sub == 0) {
-            double f = s_r;
-            if (!fin) {
-                raise_err(a.err, GEE_ERR_NONFINITE);
-            } else {
-                const double nrm = __dsqrt_rn(ss);
-                if (nrm > 0.0) f = s_r * __ddiv_rn(1.0, nrm);
-            }
-            fac[l] = f;
-        }
-    }
-    sync();
-    const int tsz = nrows * K;
-    const int64_t zoff = r0 * K;
-    // 16-byte units need an even element offset into Z (r0 * K is even unless
-    // K and r0 are both odd) and a 16-byte aligned Z (any torch allocation)
-    const bool vec = ((reinterpret_cast<uintptr_t>(a.z) + (uintptr_t)zoff * (OUT32 ? 4 : 8)) & (OUT32 ? 7 : 15)) == 0;
-    if (vec) {
-        const int n = tsz >> 1;
-        int row = eg.t0r, col = eg.t0c;
-        for (int j = tid; j < n; j += NT) {
-            const int e = 2 * j;
-            const double f0 = fac[row];
-            const double f1 = col + 1 < K ? f0 : fac[row + 1];
-            double2 *zp = reinterpret_cast<double2 *>(zt + e);
-            const double2 v = *zp;
-            if (OUT32) {
-                __stcs(reinterpret_cast<float2 *>(reinterpret_cast<float *>(a.z) + zoff + e),
-                       make_float2((float)(v.x * f0), (float)(v.y * f1)));
-            } else {
-                __stcs(reinterpret_cast<double2 *>(reinterpret_cast<double *>(a.z) + zoff + e),
-                       make_double2(v.x * f0, v.y * f1));
-            }
-            *zp = make_double2(0.0, 0.0);
-            row += eg.dq;
-            col += eg.dr;
-            if (col >= K) {
-                col -= K;
-                ++row;
-            }
-        }
-        if ((tsz & 1) && tid == 0) {
-            const int e = tsz - 1;
-            const double v = zt[e] * fac[nrows - 1];
-            if (OUT32) __stcs(reinterpret_cast<float *>(a.z) + zoff + e, (float)v);
-            else __stcs(reinterpret_cast<double *>(a.z) + zoff + e, v);
-            zt[e] = 0.0;
-        }
-    } else {
-        for (int e = tid; e < tsz; e += NT) {
-            const int l = e / K;
-            const double v = zt[e] * fac[l];
-            if (OUT32) __stcs(reinterpret_cast<float *>(a.z) + zoff + e, (float)v);
-            else __stcs(reinterpret_cast<double *>(a.z) + zoff + e, v);
-            zt[e] = 0.0;
-        }
-    }
-}
-
-template <int WT, bool OUT32, int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) k_st_embed(StArgs a) {
-    constexpr int U = 4;  // entries per thread per stage; two stages in flight
-    extern __shared__ __align__(16) double zt[];  // [R][K], then fac[R], then the record stages
-    __shared__ unsigned s_meta[2][4];              // work item {bucket, p0, p1, items of the bucket}
-    const int R = 1 << a.lrow_bits;
-    const int K = a.k;
-    // 16-byte aligned sections (R * K may be odd)
-    double *fac = zt + (((size_t)R * K + 1) & ~(size_t)1);
-    double2 *drec = reinterpret_cast<double2 *>(fac + ((R + 1) & ~1));  // [R] the rows' own records (A+I term)
-    double2 *stage = drec + R;                                           // [2][U][NT]
-    const unsigned n_items = a.ws.ctl[kCtlItems];
-    const unsigned cmask = (1u << a.col_bits) - 1u;
-    const int cb = a.col_bits;
-    const unsigned step = U * NT;
-    const EpiGeo eg = epi_geo<NT>(K, threadIdx.x);
-    // weights stay in their own type until consumed: a float -> double
-    // conversion right after the load would wait for it
-    using XT = typename std::conditional<WT == GEE_W_UNIT, float, typename WTraits<WT>::T>::type;
-    uint32_t kA[U], kB[U];
-    XT xA[U], xB[U];
-    // stage s of this thread: the keys of [base, end) are loaded and their node
-    // records requested into the thread's own slots (cp.async, L1 bypassed)
-    // split in two so the key loads can fly before their record requests:
-    // loadk only issues loads, gather needs the keys (waits for them)
-    auto loadk = [&](unsigned base, unsigned end, uint32_t(&kk)[U], XT(&x)[U]) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const unsigned p = base + u * NT + threadIdx.x;
-            kk[u] = 0xffffffffu;
-            if (p < end) {
-                kk[u] = __ldcs(a.ws.keys2 + p);
-                if constexpr (WT != GEE_W_UNIT) x[u] = __ldcs(reinterpret_cast<const XT *>(a.ws.w2) + p);
-            }
-        }
-    };
-    auto gather = [&](const uint32_t(&kk)[U], int s) {
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (kk[u] != 0xffffffffu) cp_async16(stage + (s * U + u) * NT + threadIdx.x, a.ws.rec + (kk[u] & cmask));
-        cp_async_commit();
-    };
-    auto issue = [&](unsigned base, unsigned end, uint32_t(&kk)[U], XT(&x)[U], int s) {
-        loadk(base, end, kk, x);
-        gather(kk, s);
-    };
-    auto consume = [&](const uint32_t(&kk)[U], const XT(&x)[U], int s) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (K <= 8 && __all_sync(0xffffffffu, kk[u] != 0xffffffffu)) {
-                // few classes and a row-sorted input: every lane of the warp
-                // on one row collides on K words -- reduce per class instead
-                const unsigned lr0 = __shfl_sync(0xffffffffu, kk[u] >> cb, 0);
-                if (__all_sync(0xffffffffu, (kk[u] >> cb) == lr0)) {
-                    const double2 rc = stage[(s * U + u) * NT + threadIdx.x];
-                    const int y = rec_label(rc);
-                    const double v = (WT == GEE_W_UNIT ? 1.0 : (double)x[u]) * rc.y;
-                    for (int c = 0; c < K; ++c) {
-                        const double t = warp_sum(y == c ? v : 0.0);
-                        if ((threadIdx.x & 31) == 0 && t != 0.0) atomicAdd(zt + lr0 * K + c, t);
-                    }
-                    continue;
-                }
-            }
-            if (kk[u] == 0xffffffffu) continue;
-            const double2 rc = stage[(s * U + u) * NT + threadIdx.x];
-            const int y = rec_label(rc);
-            const double xv = WT == GEE_W_UNIT ? 1.0 : (double)x[u];
-            GEE_DASSERT((int)(kk[u] >> cb) < R && (int64_t)(kk[u] & cmask) < a.N && y < K);
-            if (y >= 0) atomicAdd(zt + (kk[u] >> cb) * K + y, xv * rc.y);
-        }
-    };
-    auto grab = [&](int slot) {  // thread 0: the next work item's descriptor into s_meta[slot]
-        const unsigned item = atomicAdd(a.ws.ctl + kCtlWork + 1, 1u);
-        const uint4 d = item < n_items ? a.ws.item_desc[item] : make_uint4(0xffffffffu, 0, 0, 0);
-        s_meta[slot][0] = d.x;
-        s_meta[slot][1] = d.y;
-        s_meta[slot][2] = d.z;
-        s_meta[slot][3] = d.w;
-    };
-    {
-        double2 *z2 = reinterpret_cast<double2 *>(zt);
-        for (int i = threadIdx.x; i < (R * K + 1) / 2; i += NT) z2[i] = make_double2(0.0, 0.0);
-    }
-    if (threadIdx.x == 0) grab(0);
-    __syncthreads();
-    int cur = 0;
-    if (s_meta[0][0] != 0xffffffffu) {
-        issue(s_meta[0][1], s_meta[0][2], kA, xA, 0);
-        if (s_meta[0][1] + step < s_meta[0][2]) issue(s_meta[0][1] + step, s_meta[0][2], kB, xB, 1);
-    }
-    for (;;) {
-        const unsigned b = s_meta[cur][0];
-        if (b == 0xffffffffu) break;
-        const unsigned p0 = s_meta[cur][1], p1 = s_meta[cur][2], nitems = s_meta[cur][3];
-        // the next item's descriptor loads overlap this item's work
-        if (threadIdx.x == 0) grab(cur ^ 1);
-        const int64_t r0 = (int64_t)b << a.lrow_bits;  // local row (Z row) of the bucket
-        const int nrows = (int)min((int64_t)R, a.nloc - r0);
-        const int tsz = nrows * K;
-        // per-row data of the epilogue, loaded now so its latency hides under the accumulation
-        for (int l = threadIdx.x; l < nrows; l += NT) {
-            if (a.flags & GEE_LAPLACIAN) fac[l] = a.ws.scale[a.row0 + r0 + l];
-            if (a.flags & GEE_DIAGONAL) drec[l] = a.ws.rec[a.row0 + r0 + l];
-        }
-        const bool trace = a.variant >= 9 && threadIdx.x == 0 && blockIdx.x < 4096;
-        const long long t1 = trace ? clock64() : 0;
-        // stages A = [p0, p0 + step) and B = [p0 + step, p0 + 2 step) were issued
-        // before this iteration; each consumed stage is refilled two steps ahead
-        for (unsigned base = p0; base < p1; base += 2 * step) {
-            const bool hb = base + step < p1, ha = base + 2 * step < p1;
-            if (hb) cp_async_wait<1>();
-            else cp_async_wait<0>();
-            consume(kA, xA, 0);
-            if (ha) issue(base + 2 * step, p1, kA, xA, 0);
-            if (hb) {
-                if (ha) cp_async_wait<1>();
-                else cp_async_wait<0>();
-                consume(kB, xB, 1);
-                if (base + 3 * step < p1) issue(base + 3 * step, p1, kB, xB, 1);
-            }
-        }
-        const long long t2 = trace ? clock64() : 0;
-        __syncthreads();  // tile complete; s_meta[cur ^ 1] visible
-        const long long t3 = trace ? clock64() : 0;
-        // the next item's first two stages: keys requested now, their records
-        // once this tile has been finished (the keys land meanwhile)
-        const bool nxt = s_meta[cur ^ 1][0] != 0xffffffffu;
-        const unsigned nq0 = s_meta[cur ^ 1][1], nq1 = s_meta[cur ^ 1][2];
-        if (nxt) {
-            loadk(nq0, nq1, kA, xA);
-            loadk(nq0 + step, nq1, kB, xB);
-        }
-        if (nitems == 1) {
-            tile_epilogue_flat<OUT32, NT>(a, zt, fac, drec, r0, nrows, eg, threadIdx.x, [] { __syncthreads(); });
-        } else {
-            GEE_DASSERT(a.ws.split_slot[b] < a.ws.ctl[kCtlSplit]);
-            double *zs = a.ws.scratch + (size_t)a.ws.split_slot[b] * ((size_t)R * K);
-            for (int i = threadIdx.x; i < tsz; i += NT) {
-                const double v = zt[i];
-                if (v != 0.0) {
-                    atomicAdd(zs + i, v);
-                    zt[i] = 0.0;
-                }
-            }
-            __threadfence();
-            __syncthreads();
-            unsigned *flag = reinterpret_cast<unsigned *>(&s_meta[cur][3]);
-            if (threadIdx.x == 0) *flag = atomicAdd(a.ws.done_emb + b, 1u) == nitems - 1;
-            __syncthreads();
-            if (*flag) {
-                __threadfence();
-                for (int i = threadIdx.x; i < tsz; i += NT) zt[i] = __ldcg(zs + i);
-                __syncthreads();
-                tile_epilogue_flat<OUT32, NT>(a, zt, fac, drec, r0, nrows, eg, threadIdx.x, [] { __syncthreads(); });
-            }
-        }
-        if (nxt) {
-            gather(kA, 0);
-            gather(kB, 1);
-        }
-        __syncthreads();  // tile zeroed, s_meta[cur] free
-        if (trace) {
-            const long long t4 = clock64();
-            unsigned long long *tr = g_emb_trace + (size_t)blockIdx.x * kTraceSlots;
-            tr[1] += t2 - t1;
-            tr[2] += t3 - t2;
-            tr[3] += t4 - t3;
-            tr[4] += 1;
-            tr[5] += p1 - p0;
-        }
-        cur ^= 1;
-    }
-}
-
-template <class T>
-int set_smem(T *kern, size_t bytes) {
-    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    return e == cudaSuccess ? GEE_OK : cuda_status(e);
-}
-
-// ---- warp-specialised embed ------------------------------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -1426,6 +1109,463 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
             : "memory");
     }
 }
+// Bulk (TMA) copies between shared and global memory, no tensor map: the Z
+// tile of a bucket is one contiguous run of Z, so one instruction stores it.
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_store_s2g(void *g, const void *s, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(smem_u32(s)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_load_g2s(void *s, const void *g, unsigned bytes, unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(s)),
+                 "l"(g), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// Factor pass of the epilogue, L = 2^lgL lanes per row (L * R = NT when
+// R <= NT, so every lane works): the A+I term g_r at the row's own label,
+// f_r = s_r (Laplacian) times 1/||s_r z_r|| (correlation; one division per
+// row -- z * (1/nrm) is within 1 ulp of the reference's z / nrm,
+// embedding.py:140), then the row is scaled by f_r in place, each lane
+// rescaling the V-element units it summed.  Rows start 16-byte aligned when
+// K is even (V = 2: 16-byte shared loads and stores).
+template <int NT, int V>
+__device__ __forceinline__ void epi_rows(const StArgs &a, double *zt, const double *fac, const double2 *drec,
+                                         int nrows, int lgL, int tid) {
+    const int K = a.k;
+    const unsigned flags = a.flags;
+    const bool lap = (flags & GEE_LAPLACIAN) != 0, corr = (flags & GEE_CORRELATION) != 0;
+    const int L = 1 << lgL;
+    const int sub = tid & (L - 1);
+    const int KU = K / V;  // units per row
+    using VT = typename std::conditional<V == 2, double2, double>::type;
+    const int R = 1 << a.lrow_bits;
+    for (int l0 = 0; l0 < R && l0 < nrows; l0 += NT >> lgL) {  // uniform: the shuffles need whole warps
+        const int l = l0 + (tid >> lgL);
+        const bool live = l < nrows;
+        double *row = zt + (size_t)(live ? l : 0) * K;
+        VT *rv = reinterpret_cast<VT *>(row);
+        const double s_r = lap && live ? fac[l] : 1.0;
+        if ((flags & GEE_DIAGONAL) && live && sub == 0) {
+            const double2 rc = drec[l];
+            const int y = rec_label(rc);
+            if (y >= 0) row[y] += rc.y;
+        }
+        __syncwarp();  // the diagonal term lands before the row is read
+        double f = s_r;
+        if (corr) {
+            double s4[4] = {0.0, 0.0, 0.0, 0.0};
+            if (live) {
+                int c = sub;
+                for (; c + 3 * L < KU; c += 4 * L) {
+                    VT v[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v[j] = rv[c + j * L];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if constexpr (V == 2) {
+                            const double t0 = v[j].x * s_r, t1 = v[j].y * s_r;
+                            s4[j] = fma(t0, t0, s4[j]);
+                            s4[j] = fma(t1, t1, s4[j]);
+                        } else {
+                            const double t = v[j] * s_r;
+                            s4[j] = fma(t, t, s4[j]);
+                        }
+                    }
+                }
+                for (; c < KU; c += L) {
+                    const VT v = rv[c];
+                    if constexpr (V == 2) {
+                        const double t0 = v.x * s_r, t1 = v.y * s_r;
+                        s4[0] = fma(t0, t0, s4[0]);
+                        s4[1] = fma(t1, t1, s4[1]);
+                    } else {
+                        const double t = v * s_r;
+                        s4[0] = fma(t, t, s4[0]);
+                    }
+                }
+            }
+            double ss = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+            bool fin = true;
+            if (live && !isfinite(ss)) {
+                // a non-finite element, or finite ones whose squares overflow
+                // (the reference raises only for the former, embedding.py:137-138)
+                for (int c2 = sub; c2 < K; c2 += L) fin &= isfinite(row[c2]);
+            }
+            for (int o = L >> 1; o > 0; o >>= 1) {
+                ss += __shfl_xor_sync(0xffffffffu, ss, o);
+                fin &= __shfl_xor_sync(0xffffffffu, (int)fin, o) != 0;
+            }
+            if (live) {
+                if (!fin) {
+                    if (sub == 0) raise_err(a.err, GEE_ERR_NONFINITE);
+                } else {
+                    const double nrm = __dsqrt_rn(ss);
+                    if (nrm > 0.0) f = s_r * __ddiv_rn(1.0, nrm);
+                }
+            }
+        }
+        if (live && f != 1.0) {
+            for (int c = sub; c < KU; c += L) {
+                VT v = rv[c];
+                if constexpr (V == 2) {
+                    v.x *= f;
+                    v.y *= f;
+                } else {
+                    v *= f;
+                }
+                rv[c] = v;
+            }
+        }
+    }
+}
+
+// The scaled tile (nrows * K elements, one contiguous run of Z at zoff) to Z:
+// f64 output from a 16-byte aligned address leaves by one bulk copy issued by
+// thread 0, and the tile is re-zeroed by a bulk copy from the zero page that
+// completes on `zbar` (returns true: the caller waits on zbar before the next
+// accumulation); otherwise the threads convert / store / zero it themselves.
+template <bool OUT32, int NT>
+__device__ __forceinline__ bool epi_store(const StArgs &a, double *zt, int64_t zoff, int tsz, int tid,
+                                          unsigned long long *zbar, bool bulk) {
+    if (!OUT32) {
+        double *zg = reinterpret_cast<double *>(a.z) + zoff;
+        if ((reinterpret_cast<uintptr_t>(zg) & 15) == 0 && !bulk) {
+            double2 *z2 = reinterpret_cast<double2 *>(zt);
+            double2 *g2 = reinterpret_cast<double2 *>(zg);
+            for (int j = tid; j < (tsz >> 1); j += NT) {
+                __stcs(g2 + j, z2[j]);
+                z2[j] = make_double2(0.0, 0.0);
+            }
+            if ((tsz & 1) && tid == 0) {
+                __stcs(zg + tsz - 1, zt[tsz - 1]);
+                zt[tsz - 1] = 0.0;
+            }
+            return false;
+        }
+        if ((reinterpret_cast<uintptr_t>(zg) & 15) == 0) {
+            if (tid == 0) {
+                const unsigned bytes = (unsigned)(tsz & ~1) * 8u;
+                if (bytes) bulk_store_s2g(zg, zt, bytes);
+                if (tsz & 1) __stcs(zg + tsz - 1, zt[tsz - 1]);
+                bulk_wait_read_all();  // the tile may be overwritten
+                bulk_load_g2s(zt, a.ws.zeros, (unsigned)((tsz + 1) & ~1) * 8u, zbar);
+            }
+            return true;
+        }
+    }
+    if (OUT32 && ((reinterpret_cast<uintptr_t>(reinterpret_cast<float *>(a.z) + zoff) & 7) == 0)) {
+        float2 *zg = reinterpret_cast<float2 *>(reinterpret_cast<float *>(a.z) + zoff);
+        double2 *z2 = reinterpret_cast<double2 *>(zt);
+        for (int j = tid; j < (tsz >> 1); j += NT) {
+            const double2 v = z2[j];
+            __stcs(zg + j, make_float2((float)v.x, (float)v.y));
+            z2[j] = make_double2(0.0, 0.0);
+        }
+        if ((tsz & 1) && tid == 0) {
+            __stcs(reinterpret_cast<float *>(a.z) + zoff + tsz - 1, (float)zt[tsz - 1]);
+            zt[tsz - 1] = 0.0;
+        }
+        return false;
+    }
+    for (int e = tid; e < tsz; e += NT) {
+        if (OUT32) __stcs(reinterpret_cast<float *>(a.z) + zoff + e, (float)zt[e]);
+        else __stcs(reinterpret_cast<double *>(a.z) + zoff + e, zt[e]);
+        zt[e] = 0.0;
+    }
+    return false;
+}
+
+// The fused embed.  A CTA owns one R x K f64 Z tile in shared memory and
+// pulls work items (<= C entries of one bucket) off a global counter.  The
+// entries of the CTA's successive items form ONE stream of stages (U entries
+// per thread); per thread the stream is a three-deep pipeline that never
+// stops at an item boundary:
+//   stage t     its node records (16-byte cp.async.cg gathers, L1 bypassed)
+//               have landed in shared slot t&1: consumed -- one shared f64
+//               add of w * g_j into the tile per entry;
+//   stage t+1   records in flight (slot (t+1)&1);
+//   stage t+2   keys + weights in registers (their loads in flight).
+// Consuming stage t requests the records of t+2 and the keys of t+3, so when
+// an item's last stage is consumed, the first stages of the items after it
+// are already on their way and the epilogue (factor pass, bulk store of the
+// tile, bulk re-zeroing) runs while they land.  The stage cursor reads the
+// descriptors of up to three items ahead from a ring that thread 0 refills
+// (one item per item consumed); an empty bucket's item has no stage, and a
+// position the cursor cannot fill yet is a bubble.
+template <int WT, bool OUT32, int NT>
+__global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(StArgs a) {
+    constexpr int U = 4;       // entries per thread per stage
+    constexpr int kRing = 8;   // work item descriptors {bucket, p0, p1, items of the bucket}
+    constexpr int kAhead = 3;  // the cursor stays within this many items of the consumer
+    extern __shared__ __align__(16) double zt[];  // [R][K], then fac[R], drec[R], the record slots
+    __shared__ uint4 s_meta[kRing];
+    __shared__ unsigned s_flag;
+    __shared__ unsigned long long s_zbar;  // completes the bulk re-zeroing of the tile
+    const int R = 1 << a.lrow_bits;
+    const int K = a.k;
+    double *fac = zt + (((size_t)R * K + 1) & ~(size_t)1);
+    double2 *drec = reinterpret_cast<double2 *>(fac + ((R + 1) & ~1));  // [R] the rows' own records (A+I term)
+    double2 *stage = drec + R;                                           // [2][U][NT]
+    const unsigned n_items = a.ws.ctl[kCtlItems];
+    const unsigned cmask = (1u << a.col_bits) - 1u;
+    const int cb = a.col_bits;
+    const unsigned step = U * NT;
+    // epilogue: L = NT / R lanes per row (1..32), 16-byte units when K is even
+    const int lgL = max(0, min(5, __ffs(NT) - 1 - a.lrow_bits));
+    const bool kv2 = (K & 1) == 0;
+    const bool bulk = (a.variant & 15) != 1;  // debug A/B: threads store the tile
+    bool zpending = false;
+    unsigned zphase = 0;
+    // weights stay in their own type while loading (kC / xC); they are
+    // converted when the stage's keys move to kA / kB (the gather has waited
+    // for that load batch by then)
+    using XT = typename std::conditional<WT == GEE_W_UNIT, float, typename WTraits<WT>::T>::type;
+    uint32_t kA[U], kB[U], kC[U];
+    XT xC[U];
+    double xA[U], xB[U];  // converted when a stage's keys move out of kC
+    auto loadk = [&](unsigned base, unsigned end, uint32_t(&kk)[U], XT(&x)[U]) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const unsigned p = base + u * NT + threadIdx.x;
+            kk[u] = 0xffffffffu;
+            if (p < end) {
+                kk[u] = __ldcs(a.ws.keys2 + p);
+                if constexpr (WT != GEE_W_UNIT) x[u] = __ldcs(reinterpret_cast<const XT *>(a.ws.w2) + p);
+            }
+        }
+    };
+    auto gather = [&](const uint32_t(&kk)[U], int s) {  // one commit group per call, possibly empty
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (kk[u] != 0xffffffffu) cp_async16(stage + (s * U + u) * NT + threadIdx.x, a.ws.rec + (kk[u] & cmask));
+        cp_async_commit();
+    };
+    auto consume = [&](const uint32_t(&kk)[U], const double(&x)[U], int s) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (K <= 8 && __all_sync(0xffffffffu, kk[u] != 0xffffffffu)) {
+                // few classes and a row-sorted input: every lane of the warp
+                // on one row collides on K words -- reduce per class instead
+                const unsigned lr0 = __shfl_sync(0xffffffffu, kk[u] >> cb, 0);
+                if (__all_sync(0xffffffffu, (kk[u] >> cb) == lr0)) {
+                    const double2 rc = stage[(s * U + u) * NT + threadIdx.x];
+                    const int y = rec_label(rc);
+                    const double v = (WT == GEE_W_UNIT ? 1.0 : x[u]) * rc.y;
+                    for (int c = 0; c < K; ++c) {
+                        const double t = warp_sum(y == c ? v : 0.0);
+                        if ((threadIdx.x & 31) == 0 && t != 0.0) atomicAdd(zt + lr0 * K + c, t);
+                    }
+                    continue;
+                }
+            }
+            if (kk[u] == 0xffffffffu) continue;
+            const double2 rc = stage[(s * U + u) * NT + threadIdx.x];
+            const int y = rec_label(rc);
+            const double xv = WT == GEE_W_UNIT ? 1.0 : x[u];
+            GEE_DASSERT((int)(kk[u] >> cb) < R && (int64_t)(kk[u] & cmask) < a.N && y < K);
+            if ((a.variant & 15) == 4) {  // debug diagnostics only: plain add instead of the atomic
+                if (y >= 0) zt[(kk[u] >> cb) * K + y] += xv * rc.y;
+            } else if (y >= 0) {
+                atomicAdd(zt + (kk[u] >> cb) * K + y, xv * rc.y);
+            }
+        }
+    };
+    auto grab = [&](unsigned n) {  // thread 0: the CTA's n-th work item into the ring
+        const unsigned item = atomicAdd(a.ws.ctl + kCtlWork + 1, 1u);
+        s_meta[n % kRing] = item < n_items ? a.ws.item_desc[item] : make_uint4(0xffffffffu, 0, 0, 0);
+    };
+    auto epilogue = [&](int64_t r0, int nrows) {
+        if ((a.variant & 15) != 2 && (a.variant & 15) != 3) {
+            if (kv2) epi_rows<NT, 2>(a, zt, fac, drec, nrows, lgL, threadIdx.x);
+            else epi_rows<NT, 1>(a, zt, fac, drec, nrows, lgL, threadIdx.x);
+        }
+        fence_proxy_async_smem();  // the scaled tile is visible to the bulk copy
+        __syncthreads();
+        if ((a.variant & 15) == 3) {  // debug diagnostics only: the tile is zeroed, Z not written
+            for (int i = threadIdx.x; i < nrows * K; i += NT) zt[i] = 0.0;
+            return;
+        }
+        if (epi_store<OUT32, NT>(a, zt, r0 * K, nrows * K, threadIdx.x, &s_zbar, bulk)) zpending = true;
+    };
+    // the stage cursor (uniform across the CTA): item qi of the CTA, next entry qb
+    unsigned ci = 0, qi = 0, qb = 0xffffffffu;
+    auto cursor = [&](unsigned &base, unsigned &end) -> bool {
+        for (;;) {
+            if (qi > ci + kAhead) return false;  // descriptor not published yet: a bubble
+            const uint4 d = s_meta[qi % kRing];
+            if (d.x == 0xffffffffu) return false;  // no more work
+            if (qb == 0xffffffffu) qb = d.y;
+            if (qb < d.z) {
+                base = qb;
+                end = d.z;
+                qb += step;
+                return true;
+            }
+            ++qi;
+            qb = 0xffffffffu;
+        }
+    };
+    {
+        double2 *z2 = reinterpret_cast<double2 *>(zt);
+        for (int i = threadIdx.x; i < (R * K + 1) / 2; i += NT) z2[i] = make_double2(0.0, 0.0);
+    }
+    if (threadIdx.x == 0) {
+        for (unsigned n = 0; n <= (unsigned)kAhead; ++n) grab(n);
+        mbar_init(&s_zbar, 1);
+    }
+    __syncthreads();
+    // prologue: stages 0 and 1 gathered, stage 2's keys loading
+    unsigned vbits = 0;  // bit j: stream position t + j holds a stage (not a bubble)
+    {
+        // every load lands in kC / xC and reaches kA / kB by a register move,
+        // as in the loop: a consumed operand is then never the destination of
+        // an outstanding load, so its use does not wait on a scoreboard the
+        // newest key loads share
+        unsigned b0, e0;
+        for (int j = 0; j < 3; ++j) {
+            const bool ok = cursor(b0, e0);
+            loadk(ok ? b0 : 0u, ok ? e0 : 0u, kC, xC);
+            vbits |= ok ? 1u << j : 0u;
+            if (j < 2) {
+                gather(kC, j);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (j == 0) {
+                        kA[u] = kC[u];
+                        xA[u] = WT == GEE_W_UNIT ? 1.0 : (double)xC[u];
+                    } else {
+                        kB[u] = kC[u];
+                        xB[u] = WT == GEE_W_UNIT ? 1.0 : (double)xC[u];
+                    }
+                }
+            }
+        }
+    }
+    int par = 0;  // slot / register set of stream position t
+    // one stream position: consume it (if it is a stage), gather t + 2 into its
+    // slot, rotate the key registers, load the keys of t + 3
+    const bool trace0 = (a.variant & 16) && threadIdx.x == 0 && blockIdx.x < 4096;
+    long long tw = 0, tc = 0, tg = 0;  // debug trace: wait / consume / refill cycles
+    auto advance = [&](bool live) {
+        const long long c0 = trace0 ? clock64() : 0;
+        cp_async_wait<1>();
+        const long long c1 = trace0 ? clock64() : 0;
+        long long c2 = 0;
+        unsigned b0 = 0, e0 = 0;
+        if (par == 0) {
+            if (live) consume(kA, xA, 0);
+            if (trace0) c2 = clock64();
+            gather(kC, 0);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                kA[u] = kC[u];
+                xA[u] = WT == GEE_W_UNIT ? 1.0 : (double)xC[u];
+            }
+        } else {
+            if (live) consume(kB, xB, 1);
+            if (trace0) c2 = clock64();
+            gather(kC, 1);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                kB[u] = kC[u];
+                xB[u] = WT == GEE_W_UNIT ? 1.0 : (double)xC[u];
+            }
+        }
+        const bool ok = cursor(b0, e0);
+        loadk(ok ? b0 : 0u, ok ? e0 : 0u, kC, xC);
+        vbits = (vbits >> 1) | (ok ? 4u : 0u);
+        par ^= 1;
+        if (trace0) {
+            const long long c3 = clock64();
+            tw += c1 - c0;
+            tc += c2 - c1;
+            tg += c3 - c2;
+        }
+    };
+    for (;; ++ci) {
+        const uint4 d = s_meta[ci % kRing];
+        const unsigned b = d.x;
+        if (b == 0xffffffffu) break;
+        const unsigned p0 = d.y, p1 = d.z, nitems = d.w;
+        if (threadIdx.x == 0) grab(ci + kAhead + 1);  // published by the tile barrier below
+        const int64_t r0 = (int64_t)b << a.lrow_bits;  // local row (Z row) of the bucket
+        const int nrows = (int)min((int64_t)R, a.nloc - r0);
+        const int tsz = nrows * K;
+        // per-row data of the epilogue, loaded now so its latency hides under the accumulation
+        for (int l = threadIdx.x; l < nrows; l += NT) {
+            if (a.flags & GEE_LAPLACIAN) fac[l] = a.ws.scale[a.row0 + r0 + l];
+            if (a.flags & GEE_DIAGONAL) drec[l] = a.ws.rec[a.row0 + r0 + l];
+        }
+        if (zpending) {  // the previous tile's bulk re-zeroing
+            mbar_wait(&s_zbar, zphase);
+            zphase ^= 1;
+            zpending = false;
+        }
+        const bool trace = (a.variant & 16) && threadIdx.x == 0 && blockIdx.x < 4096;
+        const long long t1 = trace ? clock64() : 0;
+        for (unsigned left = (p1 - p0 + step - 1) / step; left > 0;) {
+            const bool live = vbits & 1u;
+            advance(live);
+            if (live) --left;
+        }
+        const long long t2 = trace ? clock64() : 0;
+        __syncthreads();  // tile complete; the descriptor grabbed above visible
+        const long long t3 = trace ? clock64() : 0;
+        if (nitems == 1) {
+            epilogue(r0, nrows);
+        } else {
+            GEE_DASSERT(a.ws.split_slot[b] < a.ws.ctl[kCtlSplit]);
+            double *zs = a.ws.scratch + (size_t)a.ws.split_slot[b] * ((size_t)R * K);
+            for (int i = threadIdx.x; i < tsz; i += NT) {
+                const double v = zt[i];
+                if (v != 0.0) {
+                    atomicAdd(zs + i, v);
+                    zt[i] = 0.0;
+                }
+            }
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) s_flag = atomicAdd(a.ws.done_emb + b, 1u) == nitems - 1;
+            __syncthreads();
+            if (s_flag) {
+                __threadfence();
+                for (int i = threadIdx.x; i < tsz; i += NT) zt[i] = __ldcg(zs + i);
+                __syncthreads();
+                epilogue(r0, nrows);
+            }
+        }
+        __syncthreads();  // tile zeroed (or its re-zeroing issued); s_flag free
+        if (trace) {
+            const long long t4 = clock64();
+            unsigned long long *tr = g_emb_trace + (size_t)blockIdx.x * kTraceSlots;
+            tr[1] += t2 - t1;
+            tr[2] += t3 - t2;
+            tr[3] += t4 - t3;
+            tr[4] += 1;
+            tr[5] += p1 - p0;
+            tr[0] = tw;
+            tr[6] = tc;
+            tr[7] = tg;
+        }
+    }
+    cp_async_wait<0>();
+    if (zpending) mbar_wait(&s_zbar, zphase);  // no bulk copy outlives the CTA
+    if (threadIdx.x == 0) bulk_wait_all();
+}
+
+template <class T>
+int set_smem(T *kern, size_t bytes) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    return e == cudaSuccess ? GEE_OK : cuda_status(e);
+}
+
+// ---- warp-specialised embed ------------------------------------------------------
 __device__ __forceinline__ void group_sync(int id) { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
 
 constexpr int kWsNT = 256;  // warps 0-3 accumulate, warps 4-7 run the epilogue
@@ -1806,6 +1946,7 @@ static int setup(StGeo &g, StWs &W, void *ws, size_t ws_bytes, const int64_t *la
     GEE_CHECK_CUDA(cudaMemsetAsync(W.ctl, 0, sizeof(unsigned) * kCtlWords, st));
     GEE_CHECK_CUDA(cudaMemsetAsync(W.ctl + kCtlWLow, 0xff, sizeof(unsigned), st));
     GEE_CHECK_CUDA(cudaMemsetAsync(W.hist2, 0, sizeof(unsigned) * ((size_t)g.S + 1), st));
+    GEE_CHECK_CUDA(cudaMemsetAsync(W.zeros, 0, sizeof(double) * (((size_t)1 << g.lrow_bits) * (size_t)g.k + 2), st));
     if (g.flags & GEE_LAPLACIAN) GEE_CHECK_CUDA(cudaMemsetAsync(W.deg, 0, sizeof(double) * (size_t)g.nloc, st));
     return label_hist_pipeline(labels, g.N, g.k, W.y32, W.counts, W.inv, W.label_partial, W.ctl + kCtlLabel, err, st);
 }

@@ -1,4 +1,4 @@
-"""Phase trace of the stream embed (debug variant 9): clock64 totals per CTA.
+"""Phase trace of the stream embed (debug variant 16 + diagnostics): clock64 totals per CTA.
   python tools/embed_trace.py CONFIG [--nt=128] [--tile=32]"""
 import ctypes
 import os
@@ -28,7 +28,7 @@ enc.run(edges.rows, edges.cols, w, c["labels"], check=True)
 buf = (ctypes.c_ulonglong * (4096 * 8))()
 lib.dbg_stream_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
 lib.dbg_stream_trace_read(buf, 4096 * 8)
-lib.gee_debug_set(4, 16 + int(os.environ.get("VARIANT", "9")))
+lib.gee_debug_set(4, 16 + int(os.environ.get("VARIANT", "16")))
 enc.run(edges.rows, edges.cols, w, c["labels"], check=False)
 torch.cuda.synchronize()
 lib.dbg_stream_trace_read(buf, 4096 * 8)
@@ -36,6 +36,9 @@ t = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 8).astype(np.float64)
 t = t[t[:, 4] > 0]
 tot = t[:, :4].sum(axis=1)
 print(f"CTAs {t.shape[0]}  items/CTA {t[:,4].mean():.0f}  entries/CTA {t[:,5].mean():.0f}")
+if t.shape[1] >= 8:
+    print("in accumulate, per item: record wait %.0f  consume %.0f  refill (gather + keys) %.0f" %
+          tuple(t[:, [0, 6, 7]].mean(axis=0) / t[:, 4].mean()))
 print("mean cycles per CTA: wait-K0 %.0f  accumulate %.0f  tile-barrier %.0f  epilogue %.0f  total %.0f" %
       tuple(list(t[:, :4].mean(axis=0)) + [tot.mean()]))
 print("per item: wait-K0 %.0f  accumulate %.0f  barrier %.0f  epilogue %.0f" %
