@@ -823,8 +823,11 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
     // When every scaled weight is below 2^16 (unit weights) an item's sum
     // (<= kDegItem entries) stays below 2^28, so one native non-returning
     // 32-bit reduction per add is exact.
+    // When every scaled weight is below 2^32 (configs[3]'s f32 weights span
+    // 25 bits), each is split into 16-bit limbs added by two non-returning
+    // reductions: an item's sums of either limb stay below 2^28.
     int q = 0;
-    bool imode = WT == GEE_W_UNIT, small = WT == GEE_W_UNIT;
+    bool imode = WT == GEE_W_UNIT, small = WT == GEE_W_UNIT, limb2 = false;
     if constexpr (WT != GEE_W_UNIT) {
         const unsigned lo = a.ws.ctl[kCtlWLow], hi = a.ws.ctl[kCtlWHigh];
         const unsigned M = a.ws.ctl[kCtlBase1 + 256];
@@ -837,6 +840,7 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
             imode = elow > -1000 && ehigh - elow + mbits <= 62;
             q = -elow;
             small = ehigh - elow <= 16;
+            limb2 = !small && ehigh - elow <= 32;
         }
     }
     const int copies = imode ? 1 : a.deg_copies;
@@ -850,13 +854,20 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
             atomicAdd(ilo + l, (unsigned)v);  // result unused: a reduction
             return;
         }
+        if (limb2) {  // v < 2^37 (a warp's sum): limbs of the item total < 2^44 stay below 2^28
+            atomicAdd(ilo + l, (unsigned)v & 0xffffu);
+            atomicAdd(ihi + l, (unsigned)(v >> 16));
+            return;
+        }
         const unsigned vlo = (unsigned)v, vhi = (unsigned)(v >> 32);
         const unsigned old = atomicAdd(ilo + l, vlo);
         const unsigned carry = (old + vlo) < old;
         if (vhi + carry) atomicAdd(ihi + l, vhi + carry);
     };
     auto ival = [&](int l) -> unsigned long long {
-        return small ? (unsigned long long)ilo[l] : ((unsigned long long)ihi[l] << 32) + ilo[l];
+        return small   ? (unsigned long long)ilo[l]
+               : limb2 ? ((unsigned long long)ihi[l] << 16) + ilo[l]
+                       : ((unsigned long long)ihi[l] << 32) + ilo[l];
     };
     auto fdeg = [&](unsigned long long v) -> double { return ldexp((double)v, -q); };
     constexpr int U = 8;
@@ -1281,6 +1292,81 @@ __device__ __forceinline__ bool epi_store(const StArgs &a, double *zt, int64_t z
     return false;
 }
 
+// Epilogue of long rows (K even, K >= kEpiDirectK), a warp per row: the A+I
+// term, the row's sum of squares from one read of the tile (16-byte units,
+// consecutive lanes), the factor f_r = s_r / ||s_r z_r|| (correlation; one
+// division per row, within 1 ulp of the reference's z / nrm,
+// embedding.py:140), then every unit is read, zeroed and leaves as a
+// streaming 16-byte store of f_r * z: 24 shared bytes per element against
+// the 40 of epi_rows' in-place scaling + bulk store + bulk re-zeroing
+// (configs[4]: 3.12 -> 2.69 ms).  Short rows keep the bulk path, where this
+// one measured slower (configs[3]: 3.73 -> 3.99 ms).
+constexpr int kEpiDirectK = 128;
+template <int NT, bool OUT32>
+__device__ __forceinline__ void epi_direct(const StArgs &a, double *zt, const double *fac, const double2 *drec,
+                                           int64_t r0, int nrows) {
+    const int K = a.k, KU = K >> 1;
+    const unsigned flags = a.flags;
+    const bool lap = (flags & GEE_LAPLACIAN) != 0, corr = (flags & GEE_CORRELATION) != 0;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int W = NT / 32;
+    for (int l = wid; l < nrows; l += W) {
+        double *row = zt + (size_t)l * K;
+        double2 *rv = reinterpret_cast<double2 *>(row);
+        const double s_r = lap ? fac[l] : 1.0;
+        if ((flags & GEE_DIAGONAL) && lane == 0) {
+            const double2 rc = drec[l];
+            const int y = rec_label(rc);
+            if (y >= 0) row[y] += rc.y;
+        }
+        __syncwarp();  // the diagonal term lands before the row is read
+        double f = s_r;
+        if (corr) {
+            double s4[4] = {0.0, 0.0, 0.0, 0.0};
+            int c = lane;
+            for (; c + 32 < KU; c += 64) {
+                const double2 p = rv[c], q = rv[c + 32];
+                const double t0 = p.x * s_r, t1 = p.y * s_r, t2 = q.x * s_r, t3 = q.y * s_r;
+                s4[0] = fma(t0, t0, s4[0]);
+                s4[1] = fma(t1, t1, s4[1]);
+                s4[2] = fma(t2, t2, s4[2]);
+                s4[3] = fma(t3, t3, s4[3]);
+            }
+            if (c < KU) {
+                const double2 p = rv[c];
+                const double t0 = p.x * s_r, t1 = p.y * s_r;
+                s4[0] = fma(t0, t0, s4[0]);
+                s4[1] = fma(t1, t1, s4[1]);
+            }
+            double ss = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+            bool fin = true;
+            if (!isfinite(ss))  // a non-finite element, or finite ones whose squares overflow
+                for (int e = lane; e < K; e += 32) fin &= isfinite(row[e]);  // (the reference raises only for the former)
+            ss = warp_sum(ss);
+            fin = __all_sync(0xffffffffu, fin);
+            if (!fin) {
+                if (lane == 0) raise_err(a.err, GEE_ERR_NONFINITE);
+            } else {
+                const double nrm = __dsqrt_rn(ss);
+                if (nrm > 0.0) f = s_r * __ddiv_rn(1.0, nrm);
+            }
+        }
+        const int64_t g0 = (r0 + l) * K;
+        for (int c = lane; c < KU; c += 32) {
+            const double2 p = rv[c];
+            rv[c] = make_double2(0.0, 0.0);
+            if (OUT32) {
+                __stcs(reinterpret_cast<float2 *>(reinterpret_cast<float *>(a.z) + g0) + c,
+                       make_float2((float)(p.x * f), (float)(p.y * f)));
+            } else {
+                asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(reinterpret_cast<double *>(a.z) + g0 + 2 * c),
+                             "d"(p.x * f), "d"(p.y * f)
+                             : "memory");
+            }
+        }
+    }
+}
+
 // The fused embed.  A CTA owns one R x K f64 Z tile in shared memory and
 // pulls work items (<= C entries of one bucket) off a global counter.  The
 // entries of the CTA's successive items form ONE stream of stages (U entries
@@ -1380,7 +1466,12 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
         const unsigned item = atomicAdd(a.ws.ctl + kCtlWork + 1, 1u);
         s_meta[n % kRing] = item < n_items ? a.ws.item_desc[item] : make_uint4(0xffffffffu, 0, 0, 0);
     };
+    const bool direct_epi = kv2 && K >= kEpiDirectK && !(a.variant & 32) && (a.variant & 15) == 0;
     auto epilogue = [&](int64_t r0, int nrows) {
+        if (direct_epi) {
+            epi_direct<NT, OUT32>(a, zt, fac, drec, r0, nrows);
+            return;  // the tile's zeroing is ordered by the item's closing barrier
+        }
         if ((a.variant & 15) != 2 && (a.variant & 15) != 3) {
             if (kv2) epi_rows<NT, 2>(a, zt, fac, drec, nrows, lgL, threadIdx.x);
             else epi_rows<NT, 1>(a, zt, fac, drec, nrows, lgL, threadIdx.x);
@@ -1418,6 +1509,7 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
     if (threadIdx.x == 0) {
         for (unsigned n = 0; n <= (unsigned)kAhead; ++n) grab(n);
         mbar_init(&s_zbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // init visible to the bulk copies
     }
     __syncthreads();
     // prologue: stages 0 and 1 gathered, stage 2's keys loading
@@ -1494,6 +1586,16 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
         if (b == 0xffffffffu) break;
         const unsigned p0 = d.y, p1 = d.z, nitems = d.w;
         if (threadIdx.x == 0) grab(ci + kAhead + 1);  // published by the tile barrier below
+        // Empty items take no stage, so the consumer passes them without a
+        // cursor call and the cursor can fall behind it; its descriptors
+        // would then come from ring slots already refilled with later items
+        // (a stage-count mismatch: the item loop below spun forever on
+        // bubbles).  Every item before ci is fully enumerated, so the cursor
+        // restarts at ci.
+        if (qi < ci) {
+            qi = ci;
+            qb = 0xffffffffu;
+        }
         const int64_t r0 = (int64_t)b << a.lrow_bits;  // local row (Z row) of the bucket
         const int nrows = (int)min((int64_t)R, a.nloc - r0);
         const int tsz = nrows * K;
@@ -1799,6 +1901,7 @@ int launch_embed(const StGeo &g, const StArgs &a, bool out32, cudaStream_t st) {
     else k_st_embed<WT, false, NT><<<num_sms() * occ, NT, smem, st>>>(a);
     return GEE_OK;
 }
+
 
 // phase 1: partition the entries into row buckets and compute the degrees
 // (node records, or the raw local degrees of a row shard)

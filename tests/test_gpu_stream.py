@@ -152,6 +152,32 @@ def test_stream_empty_rows_and_unlabeled():
     _check(n, rows, cols, np.ones(2000), labels, 4, False)
 
 
+@pytest.mark.timeout(600, method="thread")
+def test_stream_runs_of_empty_items():
+    """Runs of empty buckets between non-empty ones: a CTA passes empty work
+    items without calling its stage cursor, which must not fall behind the
+    descriptor ring (the R-MAT tail of configs[3] hung the embed in ~40% of
+    bench runs before the cursor restarted at the current item).  Repeated
+    encodes, each against the oracle."""
+    rng = np.random.default_rng(11)
+    n, k = 1 << 21, 50  # 64-row buckets: 32768 buckets
+    bands = np.arange(0, n, 64 * 37)  # one populated bucket in 37
+    rows = np.concatenate([rng.integers(0, 4096, 300000),  # a dense head (many stages)
+                           (bands[rng.integers(0, bands.size, 200000)] + rng.integers(0, 64, 200000))])
+    cols = rng.integers(0, n, rows.size)
+    w = (1.0 - rng.random(rows.size)).astype(np.float32)
+    labels = rng.integers(0, k, n)
+    combo = (1, 1, 1)
+    st, zr = _oracle_z(n, rows, cols, w, labels, k, True, combo)
+    assert st == O.OK
+    _, pre = _oracle_z(n, rows, cols, w, labels, k, True, (1, 1, 0))
+    edges = G.EdgeList(n, rows.astype(np.int64), cols.astype(np.int64), w, True)
+    lab = G.LabelVector(labels, k)
+    for _ in range(12):
+        z = G.encode(edges, lab, G.EmbedOptions(True, True, True))
+        z_close(z, zr, zr_pre=pre)
+
+
 @pytest.mark.parametrize("idx,scale_down", [(2, 3), (3, 5), (4, 4)])
 def test_stream_configs_reduced(idx, scale_down):
     from oracle import gen
