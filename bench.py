@@ -59,7 +59,7 @@ def parse():
                    help="debug A/B of the stream embed (results wrong by design): 1 no shared atomics, 2 no gathers")
     p.add_argument("--stream-tile-kb", type=int, default=0, help="debug: KB of the stream encode's Z tile")
     p.add_argument("--stream-nt", type=int, default=None,
-                   help="debug: stream embed kernel: 0 warp-specialised, else threads per CTA (128/256/512)")
+                   help="retired debug knob (the stream embed is built for 128-thread CTAs only)")
     p.add_argument("--no-stream", action="store_true",
                    help="debug: disable the bucketed stream encode (gee_debug_set GEE_DEBUG_STREAM=1): exact CSR path")
     p.add_argument("--eager", action="store_true", help="launch kernels one by one instead of a CUDA graph")

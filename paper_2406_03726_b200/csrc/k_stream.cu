@@ -65,7 +65,7 @@ constexpr int kEmbWarps = kEmbNT / 32;
 constexpr size_t kZTileMax = 104 * 1024;  // bytes of the R x K f64 Z tile (upper bound)
 constexpr size_t kZTileDefault = 32 * 1024;  // default (A/B, profiles/r2_stream_ab.txt): several CTAs per SM hide item latency
 constexpr size_t emb_stage_bytes(int nt) { return (size_t)2 * 4 * nt * 16; }  // two stages of 4 records per thread
-int t_emb_nt = 128;  // debug hook: threads of the embed CTA (128 / 256 / 512)
+int t_emb_nt = 128;  // threads of the embed CTA (the debug hook that chose 256 / 512 is retired)
 constexpr unsigned kDegItem = 4096;  // entries per degree work item (one warp)
 constexpr int kScanBlock = 4096;     // buckets per k_st_scan2 block (1024 threads x 4)
 constexpr int kLrowMax = 9;  // at most 512 rows per bucket (per-warp degree copies: 64 KB)
@@ -777,6 +777,22 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
                  "l"(gmem)
                  : "memory");
 }
+__device__ __forceinline__ void cp_async16_hint(void *smem, const void *gmem, unsigned long long pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ unsigned long long l2_policy_evict_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long l2_policy_evict_first() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -979,128 +995,6 @@ __global__ void k_st_nodes(StArgs a, const double *deg_all) {
 }
 
 // ---- the fused embed ------------------------------------------------------------
-// Epilogue of one bucket's R x K tile held in shared memory (zt):
-//   pass A (L lanes per row): the A+I diagonal term g_r at the row's own label,
-//     then the row factor f_r = s_r (Laplacian) times 1/||s_r * z_r||
-//     (correlation; one division per row -- z * (1/nrm) is within 1 ulp of the
-//     reference's z / nrm, embedding.py:140, against the 1e-12 bar);
-//   pass B: one contiguous streaming store of the tile, each element times its
-//     row factor (rows r0 .. r0+nrows are adjacent in Z).
-template <bool OUT32, int NT>
-__device__ __forceinline__ void tile_epilogue(const StArgs &a, double *zt, double *fac, const double2 *drec,
-                                              int64_t r0, int nrows, int tid = -1) {
-    if (tid < 0) tid = threadIdx.x;  // thread index inside the NT threads doing the epilogue
-    // One pass per row, L lanes per row (no CTA barrier): the A+I term g_r at
-    // the row's own label, the factor f_r = s_r (Laplacian) times
-    // 1/||s_r z_r|| (correlation; one division per row -- z * (1/nrm) is
-    // within 1 ulp of the reference's z / nrm, embedding.py:140), then the
-    // row leaves as f_r * z_r (each L-lane step writes L adjacent values, whole
-    // 32-byte sectors) and its shared copy is zeroed for the next bucket.
-    const int K = a.k;
-    const unsigned flags = a.flags;
-    const int L = K >= 256 ? 32 : K >= 128 ? 16 : K >= 64 ? 8 : K >= 24 ? 4 : K >= 8 ? 2 : 1;
-    const int sub = tid % L;
-    const unsigned gmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << ((tid & 31) & ~(L - 1)));
-    const int groups = NT / L;
-    const int iters = (nrows + groups - 1) / groups;  // uniform per warp: shuffles stay converged
-    for (int it = 0; it < iters; ++it) {
-        const int l = it * groups + tid / L;
-        const bool live = l < nrows;
-        double *row = zt + (size_t)l * K;
-        double s_r = 1.0;
-        if (live) {
-            if (flags & GEE_LAPLACIAN) s_r = fac[l];
-            if ((flags & GEE_DIAGONAL) && sub == 0) {
-                const double2 rc = drec[l];
-                const int y = rec_label(rc);
-                if (y >= 0) row[y] += rc.y;
-            }
-        }
-        __syncwarp();
-        double f = s_r;
-        if (flags & GEE_CORRELATION) {
-            double ss = 0.0;
-            bool fin = true;
-            if (live) {
-                // four independent chains (loads first) instead of one serial one
-                double s4[4] = {0.0, 0.0, 0.0, 0.0};
-                int c = sub;
-                for (; c + 3 * L < K; c += 4 * L) {
-                    double v[4];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) v[j] = row[c + j * L];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const double t = v[j] * s_r;
-                        s4[j] += t * t;
-                    }
-                }
-                for (; c < K; c += L) {
-                    const double t = row[c] * s_r;
-                    s4[0] += t * t;
-                }
-                ss = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-                if (!isfinite(ss)) {
-                    // a non-finite element, or finite ones whose squares overflow
-                    // (the reference raises only for the former, embedding.py:137-138)
-                    for (int c2 = sub; c2 < K; c2 += L) fin &= isfinite(row[c2]);
-                }
-            }
-            for (int o = L >> 1; o > 0; o >>= 1) {
-                ss += __shfl_xor_sync(gmask, ss, o);
-                fin &= __shfl_xor_sync(gmask, (int)fin, o) != 0;
-            }
-            if (live) {
-                if (!fin) {
-                    if (sub == 0) raise_err(a.err, GEE_ERR_NONFINITE);
-                } else {
-                    const double nrm = __dsqrt_rn(ss);
-                    if (nrm > 0.0) f = s_r * __ddiv_rn(1.0, nrm);
-                }
-            }
-        }
-        if (live) {
-            const int64_t g0 = (r0 + l) * K;
-            if (OUT32) {
-                float *zg = reinterpret_cast<float *>(a.z) + g0;
-                int c = sub;
-                for (; c + 3 * L < K; c += 4 * L) {
-                    double v[4];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) v[j] = row[c + j * L];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        __stcs(zg + c + j * L, (float)(v[j] * f));
-                        row[c + j * L] = 0.0;
-                    }
-                }
-                for (; c < K; c += L) {
-                    __stcs(zg + c, (float)(row[c] * f));
-                    row[c] = 0.0;
-                }
-            } else {
-                double *zg = reinterpret_cast<double *>(a.z) + g0;
-                int c = sub;
-                for (; c + 3 * L < K; c += 4 * L) {
-                    double v[4];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) v[j] = row[c + j * L];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        __stcs(zg + c + j * L, v[j] * f);
-                        row[c + j * L] = 0.0;
-                    }
-                }
-                for (; c < K; c += L) {
-                    __stcs(zg + c, row[c] * f);
-                    row[c] = 0.0;
-                }
-            }
-        }
-    }
-    (void)fac;
-}
-
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -1125,6 +1019,14 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void bulk_store_s2g(void *g, const void *s, unsigned bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(smem_u32(s)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// the same with an L2 eviction policy (Z is written once: evict first, so the
+// node records stay resident)
+__device__ __forceinline__ void bulk_store_s2g_hint(void *g, const void *s, unsigned bytes, unsigned long long pol) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(g),
+                 "r"(smem_u32(s)), "r"(bytes), "l"(pol)
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -1243,7 +1145,7 @@ __device__ __forceinline__ void epi_rows(const StArgs &a, double *zt, const doub
 // accumulation); otherwise the threads convert / store / zero it themselves.
 template <bool OUT32, int NT>
 __device__ __forceinline__ bool epi_store(const StArgs &a, double *zt, int64_t zoff, int tsz, int tid,
-                                          unsigned long long *zbar, bool bulk) {
+                                          unsigned long long *zbar, bool bulk, unsigned long long zpol) {
     if (!OUT32) {
         double *zg = reinterpret_cast<double *>(a.z) + zoff;
         if ((reinterpret_cast<uintptr_t>(zg) & 15) == 0 && !bulk) {
@@ -1262,7 +1164,10 @@ __device__ __forceinline__ bool epi_store(const StArgs &a, double *zt, int64_t z
         if ((reinterpret_cast<uintptr_t>(zg) & 15) == 0) {
             if (tid == 0) {
                 const unsigned bytes = (unsigned)(tsz & ~1) * 8u;
-                if (bytes) bulk_store_s2g(zg, zt, bytes);
+                if (bytes) {
+                    if (a.variant & 64) bulk_store_s2g(zg, zt, bytes);  // debug A/B: no L2 hint
+                    else bulk_store_s2g_hint(zg, zt, bytes, zpol);
+                }
                 if (tsz & 1) __stcs(zg + tsz - 1, zt[tsz - 1]);
                 bulk_wait_read_all();  // the tile may be overwritten
                 bulk_load_g2s(zt, a.ws.zeros, (unsigned)((tsz + 1) & ~1) * 8u, zbar);
@@ -1408,6 +1313,9 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
     const bool bulk = (a.variant & 15) != 1;  // debug A/B: threads store the tile
     bool zpending = false;
     unsigned zphase = 0;
+    // L2 policies: node records (the gather target) evict last, Z evict first
+    const bool hints = !(a.variant & 64);
+    const unsigned long long rpol = l2_policy_evict_last(), zpol = l2_policy_evict_first();
     // weights stay in their own type while loading (kC / xC); they are
     // converted when the stage's keys move to kA / kB (the gather has waited
     // for that load batch by then)
@@ -1428,10 +1336,15 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
     };
     auto gather = [&](const uint32_t(&kk)[U], int s) {  // one commit group per call, possibly empty
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (kk[u] != 0xffffffffu) cp_async16(stage + (s * U + u) * NT + threadIdx.x, a.ws.rec + (kk[u] & cmask));
+        for (int u = 0; u < U; ++u) {
+            if (kk[u] == 0xffffffffu) continue;
+            const void *src = a.ws.rec + (kk[u] & cmask);
+            if (hints) cp_async16_hint(stage + (s * U + u) * NT + threadIdx.x, src, rpol);
+            else cp_async16(stage + (s * U + u) * NT + threadIdx.x, src);
+        }
         cp_async_commit();
     };
+    auto record = [&](int s, int u) -> double2 { return stage[(s * U + u) * NT + threadIdx.x]; };
     auto consume = [&](const uint32_t(&kk)[U], const double(&x)[U], int s) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -1440,7 +1353,7 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
                 // on one row collides on K words -- reduce per class instead
                 const unsigned lr0 = __shfl_sync(0xffffffffu, kk[u] >> cb, 0);
                 if (__all_sync(0xffffffffu, (kk[u] >> cb) == lr0)) {
-                    const double2 rc = stage[(s * U + u) * NT + threadIdx.x];
+                    const double2 rc = record(s, u);
                     const int y = rec_label(rc);
                     const double v = (WT == GEE_W_UNIT ? 1.0 : x[u]) * rc.y;
                     for (int c = 0; c < K; ++c) {
@@ -1451,7 +1364,7 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
                 }
             }
             if (kk[u] == 0xffffffffu) continue;
-            const double2 rc = stage[(s * U + u) * NT + threadIdx.x];
+            const double2 rc = record(s, u);
             const int y = rec_label(rc);
             const double xv = WT == GEE_W_UNIT ? 1.0 : x[u];
             GEE_DASSERT((int)(kk[u] >> cb) < R && (int64_t)(kk[u] & cmask) < a.N && y < K);
@@ -1482,7 +1395,7 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
             for (int i = threadIdx.x; i < nrows * K; i += NT) zt[i] = 0.0;
             return;
         }
-        if (epi_store<OUT32, NT>(a, zt, r0 * K, nrows * K, threadIdx.x, &s_zbar, bulk)) zpending = true;
+        if (epi_store<OUT32, NT>(a, zt, r0 * K, nrows * K, threadIdx.x, &s_zbar, bulk, zpol)) zpending = true;
     };
     // the stage cursor (uniform across the CTA): item qi of the CTA, next entry qb
     unsigned ci = 0, qi = 0, qb = 0xffffffffu;
@@ -1667,220 +1580,6 @@ int set_smem(T *kern, size_t bytes) {
     return e == cudaSuccess ? GEE_OK : cuda_status(e);
 }
 
-// ---- warp-specialised embed ------------------------------------------------------
-__device__ __forceinline__ void group_sync(int id) { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
-
-constexpr int kWsNT = 256;  // warps 0-3 accumulate, warps 4-7 run the epilogue
-
-// The fused embed, warp-specialised: four warps accumulate bucket i into one
-// of two shared Z tiles while the other four finish bucket i-1 from the
-// other tile (factors, streaming stores, zeroing), handing tiles over with
-// mbarriers (FULL: accumulated, EMPTY: zeroed).  The accumulating warps
-// stream entries through the two-stage record pipeline of k_st_embed and
-// request the next bucket's first stages as soon as they hand a tile over.
-template <int WT, bool OUT32>
-__global__ void __launch_bounds__(kWsNT, 2) k_st_embed_ws(StArgs a) {
-    constexpr int U = 4, NA = 128;
-    using XT = typename std::conditional<WT == GEE_W_UNIT, float, typename WTraits<WT>::T>::type;
-    extern __shared__ __align__(16) double wsm[];
-    __shared__ unsigned long long full_bar[2], empty_bar[2];
-    __shared__ unsigned meta[2][4];  // bucket, p0, p1, items of the bucket (~0: no more work)
-    __shared__ unsigned s_next[4];
-    __shared__ unsigned s_flag;
-    const int R = 1 << a.lrow_bits;
-    const int K = a.k;
-    const size_t ts = ((size_t)R * K + 1) & ~(size_t)1;
-    const size_t r2 = ((size_t)R + 1) & ~(size_t)1;
-    // per-buffer sections, selected with ternaries (no local-memory arrays)
-    double *const tile0 = wsm, *const tile1 = wsm + ts;
-    double *const fac0 = wsm + 2 * ts, *const fac1 = wsm + 2 * ts + r2;
-    double2 *const drec0 = reinterpret_cast<double2 *>(wsm + 2 * ts + 2 * r2), *const drec1 = drec0 + R;
-    double2 *stage = reinterpret_cast<double2 *>(wsm + 2 * ts + 2 * r2) + 2 * R;  // [2][U][NA]
-    const unsigned n_items = a.ws.ctl[kCtlItems];
-    const unsigned cmask = (1u << a.col_bits) - 1u;
-    const int cb = a.col_bits;
-    for (size_t i = threadIdx.x; i < ts; i += kWsNT) {
-        tile0[i] = 0.0;
-        tile1[i] = 0.0;
-    }
-    if (threadIdx.x == 0) {
-        mbar_init(&full_bar[0], NA);
-        mbar_init(&full_bar[1], NA);
-        mbar_init(&empty_bar[0], kWsNT - NA);
-        mbar_init(&empty_bar[1], kWsNT - NA);
-    }
-    __syncthreads();
-    if (threadIdx.x < NA) {
-        // ------------------------------------------------ accumulating warps
-        const int t = threadIdx.x;
-        const unsigned step = U * NA;
-        uint32_t kA[U], kB[U];
-        XT xA[U], xB[U];
-        auto loadk = [&](unsigned base, unsigned end, uint32_t(&kk)[U], XT(&x)[U]) {
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const unsigned p = base + u * NA + t;
-                kk[u] = 0xffffffffu;
-                if (p < end) {
-                    kk[u] = __ldcs(a.ws.keys2 + p);
-                    if constexpr (WT != GEE_W_UNIT) x[u] = __ldcs(reinterpret_cast<const XT *>(a.ws.w2) + p);
-                }
-            }
-        };
-        auto gather = [&](const uint32_t(&kk)[U], int s) {
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (kk[u] != 0xffffffffu) cp_async16(stage + (s * U + u) * NA + t, a.ws.rec + (kk[u] & cmask));
-            cp_async_commit();
-        };
-        auto consume = [&](double *zt, const uint32_t(&kk)[U], const XT(&x)[U], int s) {
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (kk[u] == 0xffffffffu) continue;
-                const double2 rc = stage[(s * U + u) * NA + t];
-                const int y = rec_label(rc);
-                const double xv = WT == GEE_W_UNIT ? 1.0 : (double)x[u];
-                GEE_DASSERT((int)(kk[u] >> cb) < R && y < K);
-                if (y >= 0) atomicAdd(zt + (kk[u] >> cb) * K + y, xv * rc.y);
-            }
-        };
-        auto grab = [&]() {  // thread 0: next item's descriptor into s_next
-            const unsigned item = atomicAdd(a.ws.ctl + kCtlWork + 1, 1u);
-            const uint4 d = item < n_items ? a.ws.item_desc[item] : make_uint4(0xffffffffu, 0, 0, 0);
-            s_next[0] = d.x;
-            s_next[1] = d.y;
-            s_next[2] = d.z;
-            s_next[3] = d.w;
-        };
-        if (t == 0) grab();
-        group_sync(1);
-        unsigned cur[4] = {s_next[0], s_next[1], s_next[2], s_next[3]};
-        group_sync(1);
-        if (cur[0] != 0xffffffffu) {
-            loadk(cur[1], cur[2], kA, xA);
-            loadk(cur[1] + step, cur[2], kB, xB);
-            gather(kA, 0);
-            gather(kB, 1);
-        }
-        for (unsigned it = 0;; ++it) {
-            const int b = it & 1;
-            if (it >= 2) mbar_wait(&empty_bar[b], ((it >> 1) - 1) & 1);  // tile b zeroed
-            if (cur[0] == 0xffffffffu) {
-                if (t == 0) meta[b][0] = 0xffffffffu;
-                mbar_arrive(&full_bar[b]);
-                break;
-            }
-            if (t == 0) grab();  // its loads overlap this bucket's accumulation
-            const unsigned p0 = cur[1], p1 = cur[2];
-            double *zt = b ? tile1 : tile0;
-            for (unsigned base = p0; base < p1; base += 2 * step) {
-                const bool hb = base + step < p1, ha = base + 2 * step < p1;
-                if (hb) cp_async_wait<1>();
-                else cp_async_wait<0>();
-                consume(zt, kA, xA, 0);
-                if (ha) {
-                    loadk(base + 2 * step, p1, kA, xA);
-                    gather(kA, 0);
-                }
-                if (hb) {
-                    if (ha) cp_async_wait<1>();
-                    else cp_async_wait<0>();
-                    consume(zt, kB, xB, 1);
-                    if (base + 3 * step < p1) {
-                        loadk(base + 3 * step, p1, kB, xB);
-                        gather(kB, 1);
-                    }
-                }
-            }
-            if (t == 0) {
-                meta[b][0] = cur[0];
-                meta[b][1] = cur[1];
-                meta[b][2] = cur[2];
-                meta[b][3] = cur[3];
-            }
-            group_sync(1);  // every accumulation into tile b done; s_next visible
-            mbar_arrive(&full_bar[b]);
-            for (int q = 0; q < 4; ++q) cur[q] = s_next[q];
-            group_sync(1);  // s_next read before thread 0 overwrites it
-            if (cur[0] != 0xffffffffu) {
-                loadk(cur[1], cur[2], kA, xA);
-                loadk(cur[1] + step, cur[2], kB, xB);
-                gather(kA, 0);
-                gather(kB, 1);
-            }
-        }
-        cp_async_wait<0>();
-    } else {
-        // ------------------------------------------------ epilogue warps
-        const int t = threadIdx.x - NA;
-        for (unsigned it = 0;; ++it) {
-            const int b = it & 1;
-            mbar_wait(&full_bar[b], (it >> 1) & 1);
-            const unsigned bk = meta[b][0];
-            if (bk == 0xffffffffu) break;
-            const unsigned nitems = meta[b][3];
-            const int64_t r0 = (int64_t)bk << a.lrow_bits;
-            const int nrows = (int)min((int64_t)R, a.nloc - r0);
-            const int tsz = nrows * K;
-            double *const fb = b ? fac1 : fac0;
-            double2 *const db = b ? drec1 : drec0;
-            for (int l = t; l < nrows; l += kWsNT - NA) {
-                if (a.flags & GEE_LAPLACIAN) fb[l] = a.ws.scale[a.row0 + r0 + l];
-                if (a.flags & GEE_DIAGONAL) db[l] = a.ws.rec[a.row0 + r0 + l];
-            }
-            group_sync(2);
-            double *zt = b ? tile1 : tile0;
-            if (nitems == 1) {
-                tile_epilogue<OUT32, kWsNT - NA>(a, zt, fb, db, r0, nrows, t);
-            } else {
-                GEE_DASSERT(a.ws.split_slot[bk] < a.ws.ctl[kCtlSplit]);
-                double *zs = a.ws.scratch + (size_t)a.ws.split_slot[bk] * ((size_t)R * K);
-                for (int i = t; i < tsz; i += kWsNT - NA) {
-                    const double v = zt[i];
-                    if (v != 0.0) {
-                        atomicAdd(zs + i, v);
-                        zt[i] = 0.0;
-                    }
-                }
-                __threadfence();
-                group_sync(2);
-                if (t == 0) s_flag = atomicAdd(a.ws.done_emb + bk, 1u) == nitems - 1;
-                group_sync(2);
-                if (s_flag) {
-                    __threadfence();
-                    for (int i = t; i < tsz; i += kWsNT - NA) zt[i] = __ldcg(zs + i);
-                    group_sync(2);
-                    tile_epilogue<OUT32, kWsNT - NA>(a, zt, fb, db, r0, nrows, t);
-                }
-            }
-            group_sync(2);  // tile b zeroed, fac/drec of b read
-            mbar_arrive(&empty_bar[b]);
-        }
-    }
-}
-
-template <int WT>
-int launch_embed_ws(const StGeo &g, const StArgs &a, bool out32, cudaStream_t st) {
-    static PerDevice attr;
-    const size_t R = (size_t)1 << g.lrow_bits;
-    const size_t ts = (R * (size_t)g.k + 1) & ~(size_t)1, r2 = (R + 1) & ~(size_t)1;
-    const size_t smem = sizeof(double) * (2 * ts + 2 * r2) + 2 * R * 16 + (size_t)2 * 4 * 128 * 16;
-    const size_t smax = 226 * 1024;  // per-CTA maximum less the static barriers; the launch uses `smem`
-    if (!attr.done()) {
-        int rc;
-        if ((rc = set_smem(k_st_embed_ws<WT, false>, smax))) return rc;
-        if ((rc = set_smem(k_st_embed_ws<WT, true>, smax))) return rc;
-        attr.mark();
-    }
-    int occ = 1;
-    if (out32) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_st_embed_ws<WT, true>, kWsNT, smem);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_st_embed_ws<WT, false>, kWsNT, smem);
-    if (occ < 1) occ = 1;
-    if (out32) k_st_embed_ws<WT, true><<<num_sms() * occ, kWsNT, smem, st>>>(a);
-    else k_st_embed_ws<WT, false><<<num_sms() * occ, kWsNT, smem, st>>>(a);
-    return GEE_OK;
-}
-
 template <int WT, int NT>
 int launch_embed(const StGeo &g, const StArgs &a, bool out32, cudaStream_t st) {
     static PerDevice attr;
@@ -1901,6 +1600,7 @@ int launch_embed(const StGeo &g, const StArgs &a, bool out32, cudaStream_t st) {
     else k_st_embed<WT, false, NT><<<num_sms() * occ, NT, smem, st>>>(a);
     return GEE_OK;
 }
+
 
 
 // phase 1: partition the entries into row buckets and compute the degrees
@@ -1938,9 +1638,12 @@ int run_phase1(const StGeo &g, StArgs &a, cudaStream_t st) {
         k_st_scan2c<<<nblk, 1024, 0, st>>>(a);
         GEE_CHECK_LAUNCH("k_st_scan2c");
     }
-    k_st_part2<WT><<<sms * 3, kStNT, p2_smem, st>>>(a);
+    // as many CTAs as are resident (64 registers x 512 threads: two per SM);
+    // the tiles are grid-strided, so a third CTA per SM ran as a second,
+    // half-occupied wave
+    k_st_part2<WT><<<sms * 2, kStNT, p2_smem, st>>>(a);
     GEE_CHECK_LAUNCH("k_st_part2");
-    k_st_degree<WT><<<sms * 8, kDegNT, deg_smem, st>>>(a);
+    k_st_degree<WT><<<sms * (a.variant & 512 ? 8 : 4), kDegNT, deg_smem, st>>>(a);  // resident CTAs (A/B: bit 512 two waves)
     GEE_CHECK_LAUNCH("k_st_degree");
     return GEE_OK;
 }
@@ -1954,10 +1657,7 @@ int run_phase2(const StGeo &g, StArgs &a, const double *deg_all, bool shard, cud
     }
     const bool out32 = (a.flags & GEE_FP32) != 0;
     int rc2;
-    if (t_emb_nt == 0) rc2 = launch_embed_ws<WT>(g, a, out32, st);
-    else if (t_emb_nt == 128) rc2 = launch_embed<WT, 128>(g, a, out32, st);
-    else if (t_emb_nt == 512) rc2 = launch_embed<WT, 512>(g, a, out32, st);
-    else rc2 = launch_embed<WT, 256>(g, a, out32, st);
+    rc2 = launch_embed<WT, 128>(g, a, out32, st);
     if (rc2) return rc2;
     GEE_CHECK_LAUNCH("k_st_embed");
     return GEE_OK;
@@ -1979,7 +1679,7 @@ int set_stream_tile_kb(int v) {
 
 int set_stream_embed_nt(int v) {
     const int old = t_emb_nt;
-    t_emb_nt = (v == 0 || v == 256 || v == 512) ? v : 128;  // 0: warp-specialised
+    (void)v;  // only 128-thread embed CTAs are built
     return old;
 }
 
@@ -2035,7 +1735,7 @@ static void fill_args(StArgs &a, const StGeo &g, const StWs &W, const int64_t *r
     a.C = g.C;
     a.variant = t_stream_mode >= 16 ? t_stream_mode - 16 : 0;
     // 8 interleaved copies while the per-warp slice stays <= 4 KB (R <= 64), fewer for larger R
-    a.deg_copies = g.lrow_bits <= 6 ? 8 : g.lrow_bits <= 7 ? 4 : g.lrow_bits <= 8 ? 2 : 1;
+    a.deg_copies = g.lrow_bits <= 6 ? 8 : g.lrow_bits <= 7 ? 4 : g.lrow_bits <= 8 ? 2 : 1;  // <= 4 KB per warp
     a.magic = (0x100000000ull + (unsigned)g.k - 1) / (unsigned)g.k;
     a.ws = W;
     a.z = z;
