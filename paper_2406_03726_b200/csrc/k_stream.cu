@@ -640,31 +640,31 @@ __global__ void __launch_bounds__(1024) k_st_scan2c(StArgs a) {
 }
 
 // ---- pass P2: partition into buckets ----------------------------------------
-template <int WT>
-__global__ void __launch_bounds__(kStNT, 2) k_st_part2(StArgs a) {
+template <int WT, int NT, int TILE>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_st_part2(StArgs a) {
     using WTy = typename WTraits<WT>::T;
     extern __shared__ __align__(16) unsigned char sm[];
     uint32_t *skey = reinterpret_cast<uint32_t *>(sm);
-    WTy *sw = reinterpret_cast<WTy *>(sm + 4 * kStTile);
-    unsigned *cnt = reinterpret_cast<unsigned *>(sm + (4 + WTraits<WT>::bytes) * kStTile);
+    WTy *sw = reinterpret_cast<WTy *>(sm + 4 * TILE);
+    unsigned *cnt = reinterpret_cast<unsigned *>(sm + (4 + WTraits<WT>::bytes) * TILE);
     unsigned *off = cnt + kStWin;
     unsigned *gbase = off + kStWin;
     unsigned short *srel = reinterpret_cast<unsigned short *>(gbase + kStWin);
     __shared__ unsigned red[32];
     const unsigned M = a.ws.ctl[kCtlBase1 + 256];
-    const unsigned ntiles = (M + kStTile - 1) / kStTile;
+    const unsigned ntiles = (M + TILE - 1) / TILE;
     const unsigned rmask = (1u << a.lrow_bits) - 1u;
-    constexpr int PER = kStTile / kStNT;
+    constexpr int PER = TILE / NT;
     // software pipeline: the next tile's keys and weights are loaded into
     // registers as soon as this tile's are staged in shared memory, so they
     // fly while this tile is written out
     unsigned long long kk[PER];
     WTy wv[PER];
     auto load_tile = [&](unsigned tile) {
-        const unsigned p0 = tile * kStTile;
+        const unsigned p0 = tile * TILE;
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
-            const unsigned p = p0 + u * kStNT + threadIdx.x;
+            const unsigned p = p0 + u * NT + threadIdx.x;
             kk[u] = ~0ull;
             if (tile < ntiles && p < M) {
                 kk[u] = __ldcs(a.ws.keys1 + p);
@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part2(StArgs a) {
     __shared__ unsigned s_sub0;
     load_tile(blockIdx.x);
     for (unsigned tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        for (int i = threadIdx.x; i < kStWin; i += kStNT) cnt[i] = 0;
+        for (int i = threadIdx.x; i < kStWin; i += NT) cnt[i] = 0;
         if (threadIdx.x == 0) s_sub0 = (unsigned)((kk[0] >> 32) >> a.d1_shift) << a.d2_bits;  // entry p0
         __syncthreads();
         const unsigned sub0 = s_sub0;
@@ -704,21 +704,21 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part2(StArgs a) {
         __syncthreads();
         {
             // all of this thread's reservations in flight at once
-            constexpr int PB = kStWin / kStNT;
+            constexpr int PB = kStWin / NT;
             unsigned cc[PB], gb[PB];
 #pragma unroll
-            for (int j = 0; j < PB; ++j) cc[j] = cnt[threadIdx.x + j * kStNT];
+            for (int j = 0; j < PB; ++j) cc[j] = cnt[threadIdx.x + j * NT];
 #pragma unroll
             for (int j = 0; j < PB; ++j)
-                gb[j] = cc[j] ? atomicAdd(a.ws.cur2 + sub0 + threadIdx.x + j * kStNT, cc[j]) : 0u;
+                gb[j] = cc[j] ? atomicAdd(a.ws.cur2 + sub0 + threadIdx.x + j * NT, cc[j]) : 0u;
 #pragma unroll
             for (int j = 0; j < PB; ++j) {
-                gbase[threadIdx.x + j * kStNT] = gb[j];
-                off[threadIdx.x + j * kStNT] = cc[j];
+                gbase[threadIdx.x + j * NT] = gb[j];
+                off[threadIdx.x + j * NT] = cc[j];
             }
         }
         __syncthreads();
-        block_scan_bins<kStNT>(off, kStWin, red);
+        block_scan_bins<NT>(off, kStWin, red);
         const unsigned total = off[kStWin - 1] + cnt[kStWin - 1];
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
@@ -732,7 +732,7 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part2(StArgs a) {
         load_tile(tile + gridDim.x);
         __syncthreads();
         // coalesced runs out
-        for (unsigned t = threadIdx.x; t < total; t += kStNT) {
+        for (unsigned t = threadIdx.x; t < total; t += NT) {
             const unsigned lo = srel[t];
             const unsigned pos = gbase[lo] + (t - off[lo]);
             GEE_DASSERT(sub0 + lo < a.S && pos >= a.ws.base2[sub0 + lo] && pos < a.ws.base2[sub0 + lo + 1]);
@@ -1609,13 +1609,17 @@ template <int WT>
 int run_phase1(const StGeo &g, StArgs &a, cudaStream_t st) {
     static PerDevice attr;
     const size_t p1_smem = (size_t)(8 + WTraits<WT>::bytes) * kStTile;
-    const size_t p2_smem = (size_t)(4 + WTraits<WT>::bytes + 2) * kStTile + 3 * sizeof(unsigned) * kStWin;
+    // part2: 1024-thread CTAs over 8192-entry tiles (one per SM; bucket runs
+    // twice as long as with 4096) unless the debug A/B bit 1024 asks for 512 / 4096
+    const bool p2big = !(a.variant & 1024);
+    const size_t p2_smem = (size_t)(4 + WTraits<WT>::bytes + 2) * (p2big ? 8192 : kStTile) + 3 * sizeof(unsigned) * kStWin;
     const size_t deg_smem = sizeof(double) * (kDegNT / 32) * ((size_t)1 << g.lrow_bits) * (size_t)a.deg_copies;
     if (!attr.done()) {
         int rc;
         if ((rc = set_smem(k_st_part1<WT, true>, p1_smem))) return rc;
         if ((rc = set_smem(k_st_part1<WT, false>, p1_smem))) return rc;
-        if ((rc = set_smem(k_st_part2<WT>, p2_smem))) return rc;
+        if ((rc = set_smem(k_st_part2<WT, 1024, 8192>, (size_t)(4 + WTraits<WT>::bytes + 2) * 8192 + 3 * sizeof(unsigned) * kStWin))) return rc;
+        if ((rc = set_smem(k_st_part2<WT, kStNT, kStTile>, (size_t)(4 + WTraits<WT>::bytes + 2) * kStTile + 3 * sizeof(unsigned) * kStWin))) return rc;
         if ((rc = set_smem(k_st_degree<WT>, sizeof(double) * (kDegNT / 32) * 512))) return rc;
         attr.mark();
     }
@@ -1641,9 +1645,10 @@ int run_phase1(const StGeo &g, StArgs &a, cudaStream_t st) {
     // as many CTAs as are resident (64 registers x 512 threads: two per SM);
     // the tiles are grid-strided, so a third CTA per SM ran as a second,
     // half-occupied wave
-    k_st_part2<WT><<<sms * 2, kStNT, p2_smem, st>>>(a);
+    if (p2big) k_st_part2<WT, 1024, 8192><<<sms, 1024, p2_smem, st>>>(a);
+    else k_st_part2<WT, kStNT, kStTile><<<sms * 2, kStNT, p2_smem, st>>>(a);
     GEE_CHECK_LAUNCH("k_st_part2");
-    k_st_degree<WT><<<sms * (a.variant & 512 ? 8 : 4), kDegNT, deg_smem, st>>>(a);  // resident CTAs (A/B: bit 512 two waves)
+    k_st_degree<WT><<<sms * 8, kDegNT, deg_smem, st>>>(a);
     GEE_CHECK_LAUNCH("k_st_degree");
     return GEE_OK;
 }
