@@ -290,25 +290,50 @@ __device__ __forceinline__ void weight_exponents(double w, int &lo, int &hi) {
 __device__ __forceinline__ void weight_exponents(char, int &lo, int &hi) { lo = hi = 0; }
 
 // ---- pass H: 8-bit MSD digit histogram --------------------------------------
+// Eight sub-histograms (by warp) against the contention of a skewed digit
+// (R-MAT: 11% of configs[3]'s entries share digit 0); 16-byte loads of row
+// pairs for directed lists.
 __global__ void __launch_bounds__(kStNT) k_st_hist1(StArgs a) {
-    __shared__ unsigned cnt[256];
-    if (threadIdx.x < 256) cnt[threadIdx.x] = 0;
+    __shared__ unsigned cnt[8][256];
+    for (int i = threadIdx.x; i < 8 * 256; i += kStNT) (&cnt[0][0])[i] = 0;
     __syncthreads();
+    unsigned *mine = cnt[(threadIdx.x >> 5) & 7];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.E; i += stride) {
-        bool bad = false;
-        int64_t r = a.directed ? fix_row(__ldg(a.rows + i), a, bad) : fix_index(__ldg(a.rows + i), a.N, bad);
-        if (a.directed) {
-            atomicAdd(cnt + (unsigned)(r >> a.d1_shift), 1u);
-        } else {
-            int64_t c = fix_index(__ldg(a.cols + i), a.N, bad);
-            if (bad) r = c = 0;
-            atomicAdd(cnt + (unsigned)(r >> a.d1_shift), 1u);
-            if (r != c) atomicAdd(cnt + (unsigned)(c >> a.d1_shift), 1u);
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (a.directed && (reinterpret_cast<uintptr_t>(a.rows) & 15) == 0) {
+        const longlong2 *r2 = reinterpret_cast<const longlong2 *>(a.rows);
+        const int64_t npair = a.E >> 1;
+        for (int64_t i = t0; i < npair; i += stride) {
+            const longlong2 rv = __ldcs(r2 + i);
+            bool bad = false;
+            const int64_t r0 = fix_row(rv.x, a, bad), r1 = fix_row(rv.y, a, bad);
+            atomicAdd(mine + (unsigned)(r0 >> a.d1_shift), 1u);
+            atomicAdd(mine + (unsigned)(r1 >> a.d1_shift), 1u);
+        }
+        if ((a.E & 1) && t0 == 0) {
+            bool bad = false;
+            atomicAdd(mine + (unsigned)(fix_row(__ldg(a.rows + a.E - 1), a, bad) >> a.d1_shift), 1u);
+        }
+    } else {
+        for (int64_t i = t0; i < a.E; i += stride) {
+            bool bad = false;
+            int64_t r = a.directed ? fix_row(__ldg(a.rows + i), a, bad) : fix_index(__ldg(a.rows + i), a.N, bad);
+            if (a.directed) {
+                atomicAdd(mine + (unsigned)(r >> a.d1_shift), 1u);
+            } else {
+                int64_t c = fix_index(__ldg(a.cols + i), a.N, bad);
+                if (bad) r = c = 0;
+                atomicAdd(mine + (unsigned)(r >> a.d1_shift), 1u);
+                if (r != c) atomicAdd(mine + (unsigned)(c >> a.d1_shift), 1u);
+            }
         }
     }
     __syncthreads();
-    if (threadIdx.x < 256 && cnt[threadIdx.x]) atomicAdd(a.ws.ctl + kCtlHist1 + threadIdx.x, cnt[threadIdx.x]);
+    if (threadIdx.x < 256) {
+        unsigned t = 0;
+        for (int w = 0; w < 8; ++w) t += cnt[w][threadIdx.x];
+        if (t) atomicAdd(a.ws.ctl + kCtlHist1 + threadIdx.x, t);
+    }
 }
 
 __global__ void k_st_scan1(StArgs a) {
@@ -496,23 +521,36 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part1(StArgs a) {
 }
 
 // ---- bucket histogram over the digit-ordered list ---------------------------
+// 16384-entry tiles (four times the partition tile): a tile still lies within
+// the 2048-bucket window (one digit region spans 2^d2_bits <= 1024 buckets),
+// and its non-zero bins -- about one flush atomic per bucket of the region --
+// amortise over four times the entries; 16-byte loads of entry pairs.
+constexpr int kH2Tile = 16384;
 __global__ void __launch_bounds__(kStNT) k_st_hist2(StArgs a) {
     __shared__ unsigned cnt[kStWin];
     const unsigned M = a.ws.ctl[kCtlBase1 + 256];
-    const unsigned ntiles = (M + kStTile - 1) / kStTile;
+    const unsigned ntiles = (M + kH2Tile - 1) / kH2Tile;
+    const ulonglong2 *k2 = reinterpret_cast<const ulonglong2 *>(a.ws.keys1);
     for (unsigned tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         for (int i = threadIdx.x; i < kStWin; i += kStNT) cnt[i] = 0;
         __syncthreads();
-        const unsigned p0 = tile * kStTile;
+        const unsigned p0 = tile * kH2Tile;
         const unsigned sub0 = (unsigned)((a.ws.keys1[p0] >> 32) >> a.d1_shift) << a.d2_bits;
+        auto count = [&](unsigned long long key) {
+            const unsigned sub = (unsigned)((key >> 32) >> a.lrow_bits);
+            const unsigned rel = sub - sub0;
+            if (rel < kStWin) atomicAdd(cnt + rel, 1u);
+            else atomicAdd(a.ws.hist2 + sub, 1u);
+        };
 #pragma unroll 4
-        for (int u = 0; u < kStTile / kStNT; ++u) {
-            const unsigned p = p0 + u * kStNT + threadIdx.x;
-            if (p < M) {
-                const unsigned sub = (unsigned)((a.ws.keys1[p] >> 32) >> a.lrow_bits);
-                const unsigned rel = sub - sub0;
-                if (rel < kStWin) atomicAdd(cnt + rel, 1u);
-                else atomicAdd(a.ws.hist2 + sub, 1u);
+        for (int u = 0; u < kH2Tile / (2 * kStNT); ++u) {
+            const unsigned p = p0 + 2 * (u * kStNT + threadIdx.x);  // even: keys1 is 256-byte aligned
+            if (p + 1 < M) {
+                const ulonglong2 kv = __ldcs(k2 + (p >> 1));
+                count(kv.x);
+                count(kv.y);
+            } else if (p < M) {
+                count(a.ws.keys1[p]);
             }
         }
         __syncthreads();
