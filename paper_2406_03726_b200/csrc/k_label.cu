@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(1024) k_label_small(const int64_t *__restrict_
 }
 
 constexpr int64_t kLabelSmall = 1 << 18;
+constexpr int kLabelWarpHistK = 384;  // 32 warp histograms of <= 384 classes: <= 48 KB
 constexpr int kLabelMaxBlocks = 1024;
 
 // Pipeline variant: each CTA histograms a contiguous slice into its own row
@@ -112,7 +113,12 @@ __global__ void __launch_bounds__(1024) k_label_multi(const int64_t *__restrict_
                                                       int32_t *err) {
     extern __shared__ unsigned sh_hist[];
     __shared__ bool last;
-    for (int c = threadIdx.x; c < k; c += blockDim.x) sh_hist[c] = 0;
+    // few classes: one sub-histogram per warp and plain shared atomics (no
+    // __match_any_sync); more: one histogram with warp-aggregated updates
+    const bool per_warp = k <= kLabelWarpHistK;
+    const int nh = per_warp ? (int)(blockDim.x >> 5) : 1;
+    unsigned *mine = sh_hist + (per_warp ? (threadIdx.x >> 5) * k : 0);
+    for (int c = threadIdx.x; c < nh * k; c += blockDim.x) sh_hist[c] = 0;
     __syncthreads();
     const int64_t i0 = (int64_t)blockIdx.x * per_block;
     const int64_t i1 = min(n, i0 + per_block);
@@ -136,13 +142,21 @@ __global__ void __launch_bounds__(1024) k_label_multi(const int64_t *__restrict_
                 lab = (int)x;
                 y32[i] = lab;
             }
-            const unsigned key = lab >= 0 ? (unsigned)lab : 0xffffffffu;
-            const unsigned peers = __match_any_sync(0xffffffffu, key);
-            if (lab >= 0 && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh_hist[lab], __popc(peers));
+            if (per_warp) {
+                if (lab >= 0) atomicAdd(mine + lab, 1u);
+            } else {
+                const unsigned key = lab >= 0 ? (unsigned)lab : 0xffffffffu;
+                const unsigned peers = __match_any_sync(0xffffffffu, key);
+                if (lab >= 0 && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh_hist[lab], __popc(peers));
+            }
         }
     }
     __syncthreads();
-    for (int c = threadIdx.x; c < k; c += blockDim.x) partial[(size_t)blockIdx.x * k + c] = sh_hist[c];
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+        unsigned t = 0;
+        for (int h = 0; h < nh; ++h) t += sh_hist[h * k + c];
+        partial[(size_t)blockIdx.x * k + c] = t;
+    }
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
@@ -207,7 +221,8 @@ int label_hist_pipeline(const int64_t *labels, int64_t n, int32_t k, int32_t *y3
     if (k > kHistSmemMax || n <= 0) return label_hist(labels, n, k, y32, counts, inv_nk, err, st);
     const int64_t per = n > 2048 * (int64_t)kLabelMaxBlocks ? (n + kLabelMaxBlocks - 1) / kLabelMaxBlocks : 2048;
     const unsigned nb = (unsigned)((n + per - 1) / per);
-    k_label_multi<<<nb, 1024, sizeof(unsigned) * (size_t)k, st>>>(labels, n, k, per, y32, partial,
+    const size_t smem = sizeof(unsigned) * (size_t)k * (k <= kLabelWarpHistK ? 32 : 1);
+    k_label_multi<<<nb, 1024, smem, st>>>(labels, n, k, per, y32, partial,
                                                                  reinterpret_cast<long long *>(counts), inv_nk,
                                                                  done, err);
     GEE_CHECK_LAUNCH("k_label_hist");

@@ -902,7 +902,10 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
     unsigned *ilo = reinterpret_cast<unsigned *>(wdeg) + (size_t)wid * 2 * R, *ihi = ilo + R;
     const int cp = lane & (copies - 1);
     unsigned long long *gdeg = reinterpret_cast<unsigned long long *>(a.ws.deg);
-    auto to_fixed = [&](double x) -> unsigned long long { return (unsigned long long)ldexp(x, q); };
+    // x * 2^q is an integer below 2^62 with x's significant bits: the
+    // multiplication by the power of two is exact (and far cheaper than ldexp)
+    const double up = ldexp(1.0, q), down = ldexp(1.0, -q);
+    auto to_fixed = [&](double x) -> unsigned long long { return (unsigned long long)(x * up); };
     auto iadd = [&](unsigned l, unsigned long long v) {
         if (small) {
             atomicAdd(ilo + l, (unsigned)v);  // result unused: a reduction
@@ -923,7 +926,7 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
                : limb2 ? ((unsigned long long)ihi[l] << 16) + ilo[l]
                        : ((unsigned long long)ihi[l] << 32) + ilo[l];
     };
-    auto fdeg = [&](unsigned long long v) -> double { return ldexp((double)v, -q); };
+    auto fdeg = [&](unsigned long long v) -> double { return (double)v * down; };
     constexpr int U = 8;
     for (unsigned item = (blockIdx.x * kDegNT + threadIdx.x) >> 5; item < n_items;
          item += (gridDim.x * kDegNT) >> 5) {
