@@ -831,6 +831,10 @@ __device__ __forceinline__ unsigned long long l2_policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -1211,9 +1215,15 @@ __device__ __forceinline__ bool epi_store(const StArgs &a, double *zt, int64_t z
                 }
                 if (tsz & 1) __stcs(zg + tsz - 1, zt[tsz - 1]);
                 bulk_wait_read_all();  // the tile may be overwritten
-                bulk_load_g2s(zt, a.ws.zeros, (unsigned)((tsz + 1) & ~1) * 8u, zbar);
+                if (!(a.variant & 128)) bulk_load_g2s(zt, a.ws.zeros, (unsigned)((tsz + 1) & ~1) * 8u, zbar);
             }
-            return true;
+            if (!(a.variant & 128)) return true;
+            // debug A/B: re-zeroed by the threads once the bulk copy has read
+            // the tile (measured 1% slower than the bulk re-zeroing)
+            __syncthreads();
+            double2 *z2 = reinterpret_cast<double2 *>(zt);
+            for (int j = tid; j < ((tsz + 1) >> 1); j += NT) z2[j] = make_double2(0.0, 0.0);
+            return false;
         }
     }
     if (OUT32 && ((reinterpret_cast<uintptr_t>(reinterpret_cast<float *>(a.z) + zoff) & 7) == 0)) {
@@ -1553,10 +1563,21 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
         const int64_t r0 = (int64_t)b << a.lrow_bits;  // local row (Z row) of the bucket
         const int nrows = (int)min((int64_t)R, a.nloc - r0);
         const int tsz = nrows * K;
-        // per-row data of the epilogue, loaded now so its latency hides under the accumulation
-        for (int l = threadIdx.x; l < nrows; l += NT) {
-            if (a.flags & GEE_LAPLACIAN) fac[l] = a.ws.scale[a.row0 + r0 + l];
-            if (a.flags & GEE_DIAGONAL) drec[l] = a.ws.rec[a.row0 + r0 + l];
+        // per-row data of the epilogue: asynchronous copies in a commit group
+        // of their own, complete by the epilogue (every group but the newest
+        // is; an item without stages waits for all) -- no load latency at
+        // the start of the item
+        if (a.variant & 256) {  // debug A/B: synchronous loads
+            for (int l = threadIdx.x; l < nrows; l += NT) {
+                if (a.flags & GEE_LAPLACIAN) fac[l] = a.ws.scale[a.row0 + r0 + l];
+                if (a.flags & GEE_DIAGONAL) drec[l] = a.ws.rec[a.row0 + r0 + l];
+            }
+        } else {
+            for (int l = threadIdx.x; l < nrows; l += NT) {
+                if (a.flags & GEE_LAPLACIAN) cp_async8(fac + l, a.ws.scale + a.row0 + r0 + l);
+                if (a.flags & GEE_DIAGONAL) cp_async16(drec + l, a.ws.rec + a.row0 + r0 + l);
+            }
+            cp_async_commit();
         }
         if (zpending) {  // the previous tile's bulk re-zeroing
             mbar_wait(&s_zbar, zphase);
@@ -1571,7 +1592,9 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
             if (live) --left;
         }
         const long long t2 = trace ? clock64() : 0;
-        __syncthreads();  // tile complete; the descriptor grabbed above visible
+        if (p1 == p0) cp_async_wait<0>();  // the item's fac / drec copies (see above)
+        else cp_async_wait<1>();
+        __syncthreads();  // tile complete; the descriptor grabbed above visible; fac / drec landed
         const long long t3 = trace ? clock64() : 0;
         if (nitems == 1) {
             epilogue(r0, nrows);
