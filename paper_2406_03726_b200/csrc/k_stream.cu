@@ -128,9 +128,13 @@ bool make_geo(StGeo &g, int64_t E, int64_t N, int directed, int wt, int k, unsig
     if (g.lrow_bits + g.col_bits > 32) return false;
     g.S = (unsigned)(((g.nloc - 1) >> g.lrow_bits) + 1);
     g.Mcap = directed ? E : 2 * E;
-    const int64_t per = g.Mcap / ((int64_t)num_sms() * 4);
+    // work items of <= C entries, C ~ M / (16 SMs): a hub bucket (power-law
+    // rows) splits over enough CTAs to finish with the rest (A/B: C / 4 took
+    // configs[2]'s embed 0.41 -> 0.25 ms and configs[3]'s 3.43 -> 3.34 ms;
+    // C / 16 lost again to the split-tile reductions)
+    const int64_t per = g.Mcap / ((int64_t)num_sms() * 16);
     int64_t c = 4096;
-    while (c < per && c < (1 << 18)) c <<= 1;
+    while (c < per && c < (1 << 16)) c <<= 1;
     g.C = (unsigned)c;
     g.max_items = (int64_t)g.S + g.Mcap / g.C + 1;
     g.max_split = g.Mcap / g.C + 1;
