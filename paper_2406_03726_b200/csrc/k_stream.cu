@@ -936,8 +936,17 @@ __global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
     };
     auto fdeg = [&](unsigned long long v) -> double { return (double)v * down; };
     constexpr int U = 8;
-    for (unsigned item = (blockIdx.x * kDegNT + threadIdx.x) >> 5; item < n_items;
-         item += (gridDim.x * kDegNT) >> 5) {
+    // items claimed dynamically, a warp at a time (their sizes range from an
+    // empty bucket to 4096 entries of a hub row); debug A/B: variant bit 512
+    // keeps the static warp-strided assignment
+    const bool dyn = !(a.variant & 512);
+    auto claim = [&](unsigned prev) -> unsigned {
+        if (!dyn) return prev == 0xffffffffu ? (blockIdx.x * kDegNT + threadIdx.x) >> 5 : prev + ((gridDim.x * kDegNT) >> 5);
+        unsigned it = 0;
+        if (lane == 0) it = atomicAdd(a.ws.ctl + kCtlWork + 2, 1u);
+        return __shfl_sync(0xffffffffu, it, 0);
+    };
+    for (unsigned item = claim(0xffffffffu); item < n_items; item = claim(item)) {
         const unsigned b = a.ws.ditem_bucket[item];
         const unsigned j = item - a.ws.ditem_off[b];
         const unsigned nitems = a.ws.ditem_off[b + 1] - a.ws.ditem_off[b];
