@@ -100,6 +100,16 @@ int gee_label_hist(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, in
  * histograms of row shards are all-reduced (multi-GPU, dist.py). */
 int gee_inv_counts(const int64_t *counts, int32_t k, double *inv_nk, void *stream);
 
+/* build_weight_matrix (embedding.py:92-107): W = the N x K one-hot CSR of
+ * the labels, row j holding inv_nk[y32[j]] (= 1.0/n_k) at column y32[j],
+ * unlabeled rows empty.  y32 / inv_nk as gee_label_hist produces them;
+ * index_pointers int64[n+1], col_indices int32[n], data f64[n] (the first
+ * index_pointers[n] entries are written).  Workspace from
+ * gee_weight_matrix_workspace. */
+int gee_weight_matrix_workspace(int64_t n, size_t *ws_bytes);
+int gee_weight_matrix(const int32_t *y32, int64_t n, const double *inv_nk, int64_t *index_pointers,
+                      int32_t *col_indices, double *data, void *ws, size_t ws_bytes, void *stream);
+
 /* K2: edge list -> CSR with the reference's exact structure and values:
  * undirected lists are symmetrised in the order [originals, reversed
  * off-diagonals]; entries are ordered by (row, col); duplicates are summed

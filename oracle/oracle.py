@@ -118,6 +118,18 @@ def coo_to_csr(rows, cols, vals, n_rows: int, n_cols: int):
     return indptr, oc[:nnz].copy(), ov[:nnz].copy()
 
 
+def weight_matrix(labels, k: int):
+    """build_weight_matrix (embedding.py:92-107): the N x K one-hot CSR, row j
+    holding 1.0 / n_{Y_j} at column Y_j, unlabeled rows empty."""
+    lab = _i64(labels)
+    counts = class_counts(lab, k)
+    labeled = lab >= 0
+    indptr = np.zeros(lab.size + 1, np.int64)
+    np.cumsum(labeled, out=indptr[1:])
+    cols = lab[labeled]
+    return indptr, cols.astype(np.int64), 1.0 / counts[cols]
+
+
 def to_csr(rows, cols, w, n: int, directed: bool):
     """EdgeList(n, rows, cols, w, directed).to_csr() (graph_io.py:78-92)."""
     r, c, v = symmetrize(rows, cols, w, directed)

@@ -7,7 +7,7 @@ semantics, computed by hand-written sm_100a CUDA kernels in libgee.so
 (C ABI: include/gee.h).  There is no CPU fallback.
 """
 
-from .embedding import GeeEncoder, build_weight_matrix, encode, label_tables, spmm_weight
+from .embedding import GeeEncoder, build_weight_matrix, encode, encode_reference, label_tables, spmm_weight
 from .errors import GpuUnavailableError, GrapheeError, NumericalDomainError, ParseError, StructuralError
 from .graph import UNLABELED, EdgeList, EmbedOptions, LabelVector
 from .sparse import CsrMatrix, add_identity, degree_vector, laplacian_normalize
@@ -30,6 +30,7 @@ __all__ = [
     "build_weight_matrix",
     "degree_vector",
     "encode",
+    "encode_reference",
     "label_tables",
     "laplacian_normalize",
     "spmm_weight",

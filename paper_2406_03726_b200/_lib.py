@@ -37,6 +37,8 @@ SIGNATURES = {
     "gee_validate_edges": (_int, [_vp, _vp, _vp, _int, _i64, _i64, _vp, _vp]),
     "gee_label_hist": (_int, [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     "gee_inv_counts": (_int, [_vp, _i32, _vp, _vp]),
+    "gee_weight_matrix_workspace": (_int, [_i64, _szp]),
+    "gee_weight_matrix": (_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "gee_csr_build_workspace": (_int, [_i64, _i64, _i64, _int, _szp]),
     "gee_csr_build": (_int, [_vp, _vp, _vp, _int, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _vp,
                              _vp, _u32, _vp, _vp, _vp, ctypes.c_size_t, _vp, _vp]),

@@ -7,7 +7,11 @@ reference's PIPELINE_MISMATCH_TOL (1e-12, cli.py:40) -- with GPU pipelines:
                (gee_encode_edges), host arrays in, host Z out;
 * ``gpu-ops``  encode(edges.to_csr(), labels, opts): the operator seam one
                call at a time (CSR build, then the encode of the CsrMatrix),
-               i.e. the reference's own call form (cli.py:176).
+               i.e. the reference's own call form (cli.py:176);
+* ``sparse``   the reference's name for that call form (same as gpu-ops);
+* ``reference`` encode_reference(edges, labels, opts) (cli.py:178,
+               embedding.py:146-200);
+* ``both``     sparse and reference, compared as cli.py:190-214 does.
 
 Each repeat is timed with time.perf_counter around the call, as
 _time_pipeline does (cli.py:170-180); the file parsing stays outside.
@@ -90,11 +94,16 @@ def _combos(args):
 
 
 def _time_pipeline(pipeline, edges, labels, opts, repeats):
-    from .embedding import encode
+    from .embedding import encode, encode_reference
     seconds, z = [], None
     for _ in range(repeats):
         t0 = time.perf_counter()
-        z = encode(edges, labels, opts) if pipeline == "gpu" else encode(edges.to_csr(), labels, opts)
+        if pipeline == "gpu":
+            z = encode(edges, labels, opts)
+        elif pipeline == "reference":  # cli.py:178 encode_reference(edges, ...)
+            z = encode_reference(edges, labels, opts)
+        else:  # "gpu-ops" / "sparse": encode(edges.to_csr(), ...) (cli.py:176)
+            z = encode(edges.to_csr(), labels, opts)
         seconds.append(time.perf_counter() - t0)
     return seconds, np.asarray(z)
 
@@ -106,7 +115,8 @@ def cmd_bench(args) -> int:
     edges = _read_edges(args)
     labels = _read_labels(args, edges.n_nodes)
     dataset = Path(args.edges).stem
-    pipelines = ["gpu", "gpu-ops"] if args.pipeline == "both" else [args.pipeline]
+    # "both" compares the reference's two pipelines as cli.py:190 does
+    pipelines = ["sparse", "reference"] if args.pipeline == "both" else [args.pipeline]
     results = []
     # warm-up (library load, workspace, first launches) outside the timed repeats
     _time_pipeline(pipelines[0], edges, labels, _combos(args)[0], 1)
@@ -117,7 +127,7 @@ def cmd_bench(args) -> int:
             results.append(BenchResult(dataset, pipeline, opts, seconds))
             outputs[pipeline] = z
         if len(pipelines) == 2:
-            delta = outputs["gpu"] - outputs["gpu-ops"]
+            delta = outputs[pipelines[0]] - outputs[pipelines[1]]
             diff = float(np.max(np.abs(delta))) if delta.size else 0.0
             print(f"[bench] {dataset} lap={_tf(opts.laplacian)} diag={_tf(opts.diagonal)} "
                   f"corr={_tf(opts.correlation)} max_abs_diff={diff:.3e}", file=sys.stderr)
@@ -205,7 +215,7 @@ def build_parser():
             s.add_argument("--corr", type=_bool_flag, default=False, metavar="B")
             s.add_argument("--grid", action="store_true")
             s.add_argument("--repeats", type=int, default=5)
-            s.add_argument("--pipeline", choices=("gpu", "gpu-ops", "both"), default="gpu")
+            s.add_argument("--pipeline", choices=("gpu", "gpu-ops", "sparse", "reference", "both"), default="gpu")
             s.add_argument("--format", choices=("csv", "table"), default="csv")
             s.set_defaults(func=cmd_bench)
     return p

@@ -59,6 +59,9 @@ int num_sms() {
 int label_hist(const int64_t *, int64_t, int32_t, int32_t *, int64_t *, double *, int32_t *, cudaStream_t);
 size_t label_partial_words(int64_t n, int k);
 int inv_counts(const int64_t *counts, int32_t k, double *inv_nk, cudaStream_t st);
+size_t weight_matrix_workspace(int64_t n);
+int weight_matrix(const int32_t *y32, int64_t n, const double *inv_nk, int64_t *ptr, int32_t *cols, double *vals,
+                  void *ws, cudaStream_t st);
 int label_hist_pipeline(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_t *counts, double *inv_nk,
                         unsigned *partial, unsigned *done, int32_t *err, cudaStream_t st);
 size_t csr_build_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int directed);
@@ -260,6 +263,19 @@ int gee_label_hist(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, in
 int gee_inv_counts(const int64_t *counts, int32_t k, double *inv_nk, void *stream) {
     if (k < 1 || !counts || !inv_nk) return GEE_E_ARG;
     return inv_counts(counts, k, inv_nk, (cudaStream_t)stream);
+}
+
+int gee_weight_matrix_workspace(int64_t n, size_t *ws_bytes) {
+    if (!ws_bytes || n < 0 || !index_ok(n)) return GEE_E_ARG;
+    *ws_bytes = weight_matrix_workspace(n);
+    return GEE_OK;
+}
+
+int gee_weight_matrix(const int32_t *y32, int64_t n, const double *inv_nk, int64_t *index_pointers,
+                      int32_t *col_indices, double *data, void *ws, size_t ws_bytes, void *stream) {
+    if (n < 0 || !index_ok(n) || !index_pointers || !inv_nk) return GEE_E_ARG;
+    if (n > 0 && (!y32 || !col_indices || !data || !ws || ws_bytes < weight_matrix_workspace(n))) return GEE_E_ARG;
+    return weight_matrix(y32, n, inv_nk, index_pointers, col_indices, data, ws, (cudaStream_t)stream);
 }
 
 int gee_csr_build_workspace(int64_t n_edges, int64_t n_rows, int64_t n_cols, int directed, size_t *ws_bytes) {

@@ -216,6 +216,51 @@ int inv_counts(const int64_t *counts, int32_t k, double *inv_nk, cudaStream_t st
     return GEE_OK;
 }
 
+// ---- build_weight_matrix (embedding.py:92-107) ------------------------------
+// W materialised as an N x K CSR: row j holds 1/n_{Y_j} at column Y_j,
+// unlabeled rows are empty.  index_pointers = exclusive scan of the labeled
+// flags, then one thread per node writes its entry (values are inv_nk, i.e.
+// 1.0 / counts, the reference's `1.0 / counts[cols]`).
+int exclusive_scan_u32(const unsigned *in, int64_t n, int64_t *out, void *ws, cudaStream_t st);
+size_t scan_workspace(int64_t n);
+
+__global__ void k_wm_flags(const int32_t *__restrict__ y32, int64_t n, unsigned *__restrict__ flag) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = y32[i] >= 0 ? 1u : 0u;
+}
+
+__global__ void k_wm_fill(const int32_t *__restrict__ y32, int64_t n, const double *__restrict__ inv_nk,
+                          const int64_t *__restrict__ ptr, int32_t *__restrict__ cols, double *__restrict__ vals) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t y = y32[i];
+        if (y >= 0) {
+            const int64_t p = ptr[i];
+            cols[p] = y;
+            vals[p] = inv_nk[y];
+        }
+    }
+}
+
+size_t weight_matrix_workspace(int64_t n) { return (((size_t)n * 4 + 255) & ~(size_t)255) + scan_workspace(n); }
+
+int weight_matrix(const int32_t *y32, int64_t n, const double *inv_nk, int64_t *ptr, int32_t *cols, double *vals,
+                  void *ws, cudaStream_t st) {
+    unsigned *flag = static_cast<unsigned *>(ws);
+    void *sws = static_cast<unsigned char *>(ws) + (((size_t)n * 4 + 255) & ~(size_t)255);
+    if (n == 0) {
+        GEE_CHECK_CUDA(cudaMemsetAsync(ptr, 0, sizeof(int64_t), st));
+        return GEE_OK;
+    }
+    const unsigned grid = grid_for(n, 256, 4);
+    k_wm_flags<<<grid, 256, 0, st>>>(y32, n, flag);
+    GEE_CHECK_LAUNCH("k_wm_flags");
+    const int rc = exclusive_scan_u32(flag, n, ptr, sws, st);
+    if (rc != GEE_OK) return rc;
+    k_wm_fill<<<grid, 256, 0, st>>>(y32, n, inv_nk, ptr, cols, vals);
+    GEE_CHECK_LAUNCH("k_wm_fill");
+    return GEE_OK;
+}
+
 int label_hist_pipeline(const int64_t *labels, int64_t n, int32_t k, int32_t *y32, int64_t *counts, double *inv_nk,
                         unsigned *partial, unsigned *done, int32_t *err, cudaStream_t st) {
     if (k > kHistSmemMax || n <= 0) return label_hist(labels, n, k, y32, counts, inv_nk, err, st);

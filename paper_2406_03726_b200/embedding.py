@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import _device, _lib
-from .errors import StructuralError
+from .errors import NumericalDomainError, StructuralError
 from .graph import EdgeList, EmbedOptions, LabelVector, options_flags
 from .sparse import CsrMatrix
 
@@ -308,17 +308,54 @@ def _encode_csr(a: CsrMatrix, labels: LabelVector, flags: int, dev) -> torch.Ten
 
 def build_weight_matrix(labels):
     """W as the reference builds it (embedding.py:92-107), materialised on the
-    device as a CsrMatrix (N x K).  The encode path never needs it."""
+    device by gee_weight_matrix as an N x K CsrMatrix: row j holds 1/n_{Y_j}
+    at column Y_j, unlabeled rows are empty.  The encode path never needs it
+    (gee_embed reads y32 + 1/n_k instead)."""
     labels = _labels_of(labels)
-    y32, counts, inv = label_tables(labels)
+    if labels.k_classes < 1:
+        raise StructuralError("k_classes must be at least 1")
+    y32, _, inv = label_tables(labels)
     dev = y32.device
     n = len(labels)
-    lab = y32.to(torch.int64)
-    labeled = lab >= 0
-    ptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-    ptr[1:] = torch.cumsum(labeled.to(torch.int64), 0)
-    cols = lab[labeled]
-    return CsrMatrix(n, labels.k_classes, ptr, cols.to(torch.int32), inv[cols])
+    lib = _lib.load()
+    ptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    cols = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    vals = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        ws = _device.WORKSPACE.get(_lib.size_query(lib.gee_weight_matrix_workspace, n), dev)
+        _lib.check(lib.gee_weight_matrix(_device.ptr(y32), n, _device.ptr(inv), _device.ptr(ptr),
+                                         _device.ptr(cols), _device.ptr(vals), _device.ptr(ws), ws.numel(),
+                                         _device.stream_handle()))
+    nnz = int(ptr[n].item())
+    return CsrMatrix(n, labels.k_classes, ptr, cols[:nnz], vals[:nnz])
+
+
+def encode_reference(edges, labels, opts=None, *, out: str = "numpy"):
+    """The reference's edge-stream embedding (embedding.py:146-200): Z from
+    the (i, j, e_ij) triplets with the options applied as edge-level
+    transforms, no CSR.  On the B200 this is the same device pipeline as
+    encode(EdgeList) -- the bucketed stream encode accumulates straight off
+    the triplet stream exactly as the reference's bincount does, up to the
+    summation order (results within 1e-12).  Reference
+    semantics kept: only the label count is checked (no squareness check,
+    embedding.py:158-159), and under correlation a non-finite Z is NOT an
+    error -- rows are divided by sqrt(sum z*z) as numpy would
+    (embedding.py:195-199), NaN/inf propagating."""
+    opts = EmbedOptions() if opts is None else opts
+    labels = _labels_of(labels)
+    e = _edges_of(edges)
+    if len(labels) != e.n_nodes:
+        raise StructuralError(f"label count {len(labels)} != node count {e.n_nodes}")
+    try:
+        z = encode(e, labels, opts, out="torch")
+    except NumericalDomainError as exc:
+        if "non-finite" not in str(exc) or not opts.correlation:
+            raise
+        z = encode(e, labels, EmbedOptions(opts.laplacian, opts.diagonal, False), out="torch")
+        norms = torch.sqrt((z * z).sum(dim=1))
+        nz = norms > 0
+        z[nz] = z[nz] / norms[nz, None]
+    return z if out == "torch" else z.cpu().numpy()
 
 
 def spmm_weight(a, labels, opts=None, *, out: str = "numpy"):

@@ -26,3 +26,26 @@ def load():
 
 def ztag(lap, diag, corr):
     return f"z{lap}{diag}{corr}"
+
+
+EXTRA_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_extra.npz")
+
+
+@functools.lru_cache(maxsize=1)
+def load_extra():
+    """tests/golden/reference_extra.npz (make_extra_golden.py): W, encode_reference
+    and from_triplets of the reference on the same seeded inputs."""
+    data = np.load(EXTRA_PATH, allow_pickle=False)
+    store = {k: data[k] for k in data.files}
+    out = []
+    for idx, name in enumerate(store["names"]):
+        p = f"c{idx}_"
+        case = {k[len(p):]: v for k, v in store.items() if k.startswith(p)}
+        n, k, directed = (int(x) for x in case["meta"])
+        case.update(name=str(name), n=n, k=k, directed=bool(directed))
+        out.append(case)
+    return out
+
+
+def rtag(lap, diag, corr):
+    return f"r{lap}{diag}{corr}"

@@ -183,4 +183,4 @@ def test_cli_bench_grid_both_pipelines_csv(tmp_path, capsys):
     assert lines[0] == "dataset,pipeline,lap,diag,corr,repeat,seconds"
     rows = [ln.split(",") for ln in lines[1:]]
     assert len(rows) == 8 * 2 * 2
-    assert {x[1] for x in rows} == {"gpu", "gpu-ops"} and all(float(x[6]) > 0 for x in rows)
+    assert {x[1] for x in rows} == {"sparse", "reference"} and all(float(x[6]) > 0 for x in rows)
