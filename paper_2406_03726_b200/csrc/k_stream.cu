@@ -1444,10 +1444,38 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
         s_meta[n % kRing] = item < n_items ? a.ws.item_desc[item] : make_uint4(0xffffffffu, 0, 0, 0);
     };
     const bool direct_epi = kv2 && K >= kEpiDirectK && !(a.variant & 32) && (a.variant & 15) == 0;
+    // Per-warp tile segments (short rows, R <= NT): the factor pass gives each
+    // warp 32/L whole consecutive rows, i.e. one contiguous run of the tile and
+    // of Z, so each warp stores its run with its own bulk copy and re-zeroes
+    // it, with no CTA barrier between the factor pass and the store (the
+    // re-zeroing copies of all warps complete on s_zbar, waited before the
+    // next accumulation).  Debug A/B bit 2048: the whole-tile store.
+    const bool seg_epi = !OUT32 && !direct_epi && kv2 && bulk && (a.variant & 15) == 0 && !(a.variant & 2048) &&
+                         R <= NT && R * 32 >= NT && (reinterpret_cast<uintptr_t>(a.z) & 15) == 0;
     auto epilogue = [&](int64_t r0, int nrows) {
         if (direct_epi) {
             epi_direct<NT, OUT32>(a, zt, fac, drec, r0, nrows);
             return;  // the tile's zeroing is ordered by the item's closing barrier
+        }
+        if (seg_epi) {
+            epi_rows<NT, 2>(a, zt, fac, drec, nrows, lgL, threadIdx.x);
+            fence_proxy_async_smem();  // this lane's scaled units are visible to the bulk copy
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) {
+                const int rw = 32 >> lgL;
+                const int l0 = (threadIdx.x >> 5) * rw;
+                const int nr = max(0, min(rw, nrows - l0));
+                if (nr > 0) {
+                    const unsigned bytes = (unsigned)(nr * K) * 8u;
+                    bulk_store_s2g_hint(reinterpret_cast<double *>(a.z) + (r0 + l0) * K, zt + (size_t)l0 * K, bytes, zpol);
+                    bulk_wait_read_all();  // the segment may be overwritten
+                    bulk_load_g2s(zt + (size_t)l0 * K, a.ws.zeros, bytes, &s_zbar);
+                } else {
+                    mbar_arrive(&s_zbar);
+                }
+            }
+            zpending = true;
+            return;
         }
         if ((a.variant & 15) != 2 && (a.variant & 15) != 3) {
             if (kv2) epi_rows<NT, 2>(a, zt, fac, drec, nrows, lgL, threadIdx.x);
@@ -1485,7 +1513,7 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
     }
     if (threadIdx.x == 0) {
         for (unsigned n = 0; n <= (unsigned)kAhead; ++n) grab(n);
-        mbar_init(&s_zbar, 1);
+        mbar_init(&s_zbar, seg_epi ? NT / 32 : 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // init visible to the bulk copies
     }
     __syncthreads();
@@ -1648,7 +1676,7 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
     }
     cp_async_wait<0>();
     if (zpending) mbar_wait(&s_zbar, zphase);  // no bulk copy outlives the CTA
-    if (threadIdx.x == 0) bulk_wait_all();
+    if (threadIdx.x == 0 || (seg_epi && (threadIdx.x & 31) == 0)) bulk_wait_all();
 }
 
 template <class T>
