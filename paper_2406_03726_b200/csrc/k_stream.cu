@@ -400,6 +400,35 @@ __device__ __forceinline__ void block_scan_bins(unsigned *cnt, int n, unsigned *
     __syncthreads();
 }
 
+// block-wide exclusive scan of cnt[0..n) in place for n <= blockDim (one bin
+// per thread: fewer live registers than block_scan_bins, whose peak made
+// k_st_part1 spill its ranks and keys)
+template <int NT>
+__device__ __forceinline__ void block_scan_small(unsigned *cnt, int n, unsigned *red) {
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const unsigned v = t < n ? cnt[t] : 0u;
+    unsigned incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) red[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        unsigned x = lane < NT / 32 ? red[lane] : 0u, xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += y;
+        }
+        if (lane < NT / 32) red[lane] = xi - x;
+    }
+    __syncthreads();
+    if (t < n) cnt[t] = red[wid] + incl - v;
+    __syncthreads();
+}
+
 // ---- pass P1: partition by the MSD digit ------------------------------------
 // Each thread owns EPT edges of the tile (8 entries: directed 8 edges, an
 // undirected list 4 edges and their mirrors); all loads are issued before the
@@ -484,7 +513,7 @@ __global__ void __launch_bounds__(kStNT, 2) k_st_part1(StArgs a) {
             off[threadIdx.x] = n;
         }
         __syncthreads();
-        block_scan_bins<kStNT>(off, 256, red);
+        block_scan_small<kStNT>(off, 256, red);
         const unsigned total = off[255] + cnt[255];
         // reorder in shared memory by digit
 #pragma unroll
