@@ -113,7 +113,10 @@ bool make_geo(StGeo &g, int64_t E, int64_t N, int directed, int wt, int k, unsig
     const int rb = bitlen64(g.nloc - 1) > 0 ? bitlen64(g.nloc - 1) : 1;  // local row bits
     g.col_bits = bitlen64(N - 1) > 0 ? bitlen64(N - 1) : 1;
     int lr = 0;
-    while (lr < rb && lr < kLrowMax && (size_t)(2ll << lr) * (size_t)k * 8 <= t_ztile_bytes) ++lr;
+    // row-in-bucket + column fit 31 bits: 0xffffffff is the embed's "no entry" key
+    if (g.col_bits > 31) return false;
+    const int lr_cap = kLrowMax < 31 - g.col_bits ? kLrowMax : 31 - g.col_bits;
+    while (lr < rb && lr < lr_cap && (size_t)(2ll << lr) * (size_t)k * 8 <= t_ztile_bytes) ++lr;
     if ((size_t)(1ll << lr) * (size_t)k * 8 > t_ztile_bytes) return false;  // K too large for one row
     g.lrow_bits = lr;
     g.sub_bits = rb - lr;
@@ -125,7 +128,7 @@ bool make_geo(StGeo &g, int64_t E, int64_t N, int directed, int wt, int k, unsig
     g.d2_bits = g.sub_bits - g.d1_bits;
     if ((1 << g.d2_bits) > kStWin) return false;
     g.d1_shift = g.lrow_bits + g.d2_bits;
-    if (g.lrow_bits + g.col_bits > 32) return false;
+    if (g.lrow_bits + g.col_bits > 31) return false;
     g.S = (unsigned)(((g.nloc - 1) >> g.lrow_bits) + 1);
     g.Mcap = directed ? E : 2 * E;
     // work items of <= C entries, C ~ M / (16 SMs): a hub bucket (power-law

@@ -264,3 +264,17 @@ def test_stream_matches_csr_path():
         z2 = G.encode(edges, lab, opts)
     rown = np.sqrt((z2 * z2).sum(axis=1, keepdims=True))
     assert (np.abs(z1 - z2) <= 2e-12 * np.maximum(np.abs(z2), rown) + 1e-14).all()
+
+
+def test_stream_all_ones_key():
+    """N = 2^23 with K <= 8: 512-row buckets and 23 column bits would make the
+    entry (row % 512 == 511, col == N - 1) the 32-bit key 0xffffffff, which is
+    the embed's "no entry" marker.  The geometry keeps row-in-bucket + column
+    within 31 bits, so the entry counts (it was dropped before)."""
+    n, k = 1 << 23, 4
+    rng = np.random.default_rng(5)
+    rows = np.concatenate([np.array([511, 1023, n - 1, 511]), rng.integers(0, n, 5000)]).astype(np.int64)
+    cols = np.concatenate([np.array([n - 1, n - 1, n - 1, 7]), rng.integers(0, n, 5000)]).astype(np.int64)
+    w = 1.0 - rng.random(rows.size)
+    labels = rng.integers(0, k, n)
+    _check(n, rows, cols, w, labels, k, True, combos=[(0, 0, 0), (1, 1, 1)])

@@ -8,4 +8,4 @@ for f in sys.argv[1:]:
     except (IndexError, OSError):
         print(f, "missing")
         continue
-    print(f"{f:36s} {d['ms_per_step']:8.3f} ms", " ".join(f"{k['kernel']}={k['ms_per_launch']:.3f}" for k in d["kernels"][:4]))
+    print(f"{f:36s} {d['ms_per_step']:8.3f} ms", " ".join(f"{k['kernel']}={k['ms_per_launch']:.3f}" for k in d["kernels"][:8]))
