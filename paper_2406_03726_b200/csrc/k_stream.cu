@@ -77,6 +77,14 @@ int t_stream_mode = 0;  // debug hook: 0 auto, 1 never, >= 16 embed A/B variant
 // [4] items, [5] entries
 constexpr int kTraceSlots = 8;
 __device__ unsigned long long g_emb_trace[4096 * kTraceSlots];
+// The trace is compiled in only with -DGEE_EMBED_TRACE (make EXTRA=-DGEE_EMBED_TRACE):
+// its running totals cost the embed ~8 registers it does not have (96 at 5 CTAs
+// per SM; a spill of 48 bytes took configs[3]'s embed from 3.25 to 5.6 ms).
+#ifdef GEE_EMBED_TRACE
+#define GEE_TRACE_ON(x) (x)
+#else
+#define GEE_TRACE_ON(x) false
+#endif
 size_t t_ztile_bytes = kZTileDefault;  // debug hook: bytes of the R x K Z tile
 
 struct StGeo {
@@ -1228,6 +1236,95 @@ __device__ __forceinline__ void epi_rows(const StArgs &a, double *zt, const doub
     }
 }
 
+// The factor pass for K even (16-byte units), free of shared-memory bank
+// conflicts for any number of lanes per row.  A 16-byte shared access is served a
+// quarter-warp (8 lanes) at a time, conflict-free when the 8 lanes touch 8
+// different 16-byte bank groups, i.e. different (unit address mod 8).  With
+// lanes (row, sub) reading unit `c = sub, sub + L, ...` of rows whose stride is
+// K / 2 units (25 at configs[3]: consecutive rows are one group apart) the
+// lanes (r, 1) and (r + 1, 0) met in one group: every access of the three
+// passes cost two wavefronts instead of one (ncu: 7.7 per instruction, ideal
+// 3.85).  Here a row is walked in blocks of 8 units; in step m of a block the
+// lane reads unit 8 b + ((sub * G + c_r + m) mod 8), G = 8 / L rows per
+// quarter-warp, c_r = (row-in-quarter - row * K/2) mod G: the 8 lanes of a
+// quarter-warp then cover all 8 groups, and the L lanes of a row all 8 units.
+template <int NT>
+__device__ __forceinline__ void epi_rows_q(const StArgs &a, double *zt, const double *fac, const double2 *drec,
+                                           int nrows, int lgL, int tid) {
+    // 8 or more lanes per row (wide): consecutive units, conflict-free as is --
+    // blocks of L units, one step each
+    const bool wide = lgL >= 3;
+    const int L = 1 << lgL, G = wide ? 1 : 8 >> lgL;
+    const int bstep = wide ? L : 8, msk = bstep - 1;
+    const int K = a.k, KU = K >> 1;
+    const unsigned flags = a.flags;
+    const bool lap = (flags & GEE_LAPLACIAN) != 0, corr = (flags & GEE_CORRELATION) != 0;
+    const int sub = tid & (L - 1);
+    const int R = 1 << a.lrow_bits;
+    for (int l0 = 0; l0 < R && l0 < nrows; l0 += NT >> lgL) {  // uniform: the shuffles need whole warps
+        const int l = l0 + (tid >> lgL);
+        const bool live = l < nrows;
+        const int lr = live ? l : 0;
+        double *row = zt + (size_t)lr * K;
+        double2 *rv = reinterpret_cast<double2 *>(row);
+        const int rot = wide ? sub : sub * G + ((((tid >> lgL) & (G - 1)) - lr * KU) & (G - 1));
+        const double s_r = lap && live ? fac[l] : 1.0;
+        if ((flags & GEE_DIAGONAL) && live && sub == 0) {
+            const double2 rc = drec[l];
+            const int y = rec_label(rc);
+            if (y >= 0) row[y] += rc.y;
+        }
+        __syncwarp();  // the diagonal term lands before the row is read
+        double f = s_r;
+        if (corr) {
+            double sq0 = 0.0, sq1 = 0.0;
+            if (live) {
+                for (int b = 0; b < KU; b += bstep) {
+                    for (int m = 0; m < G; ++m) {
+                        const int u = b + ((rot + m) & msk);
+                        if (u < KU) {
+                            const double2 v = rv[u];
+                            const double t0 = v.x * s_r, t1 = v.y * s_r;
+                            sq0 = fma(t0, t0, sq0);
+                            sq1 = fma(t1, t1, sq1);
+                        }
+                    }
+                }
+            }
+            double ss = sq0 + sq1;
+            bool fin = true;
+            if (live && !isfinite(ss)) {
+                // a non-finite element, or finite ones whose squares overflow
+                // (the reference raises only for the former, embedding.py:137-138)
+                for (int c2 = sub; c2 < K; c2 += L) fin &= isfinite(row[c2]);
+            }
+            for (int o = L >> 1; o > 0; o >>= 1) {
+                ss += __shfl_xor_sync(0xffffffffu, ss, o);
+                fin &= __shfl_xor_sync(0xffffffffu, (int)fin, o) != 0;
+            }
+            if (live) {
+                if (!fin) {
+                    if (sub == 0) raise_err(a.err, GEE_ERR_NONFINITE);
+                } else {
+                    const double nrm = __dsqrt_rn(ss);
+                    if (nrm > 0.0) f = s_r * __ddiv_rn(1.0, nrm);
+                }
+            }
+        }
+        if (live && f != 1.0) {
+            for (int b = 0; b < KU; b += bstep) {
+                for (int m = 0; m < G; ++m) {
+                    const int u = b + ((rot + m) & msk);
+                    if (u < KU) {
+                        const double2 v = rv[u];
+                        rv[u] = make_double2(v.x * f, v.y * f);
+                    }
+                }
+            }
+        }
+    }
+}
+
 // The scaled tile (nrows * K elements, one contiguous run of Z at zoff) to Z:
 // f64 output from a 16-byte aligned address leaves by one bulk copy issued by
 // thread 0, and the tile is re-zeroed by a bulk copy from the zero page that
@@ -1490,7 +1587,7 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
             return;  // the tile's zeroing is ordered by the item's closing barrier
         }
         if (seg_epi) {
-            epi_rows<NT, 2>(a, zt, fac, drec, nrows, lgL, threadIdx.x);
+            epi_rows_q<NT>(a, zt, fac, drec, nrows, lgL, threadIdx.x);
             fence_proxy_async_smem();  // this lane's scaled units are visible to the bulk copy
             __syncwarp();
             if ((threadIdx.x & 31) == 0) {
@@ -1510,7 +1607,7 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
             return;
         }
         if ((a.variant & 15) != 2 && (a.variant & 15) != 3) {
-            if (kv2) epi_rows<NT, 2>(a, zt, fac, drec, nrows, lgL, threadIdx.x);
+            if (kv2) epi_rows_q<NT>(a, zt, fac, drec, nrows, lgL, threadIdx.x);
             else epi_rows<NT, 1>(a, zt, fac, drec, nrows, lgL, threadIdx.x);
         }
         fence_proxy_async_smem();  // the scaled tile is visible to the bulk copy
@@ -1579,7 +1676,7 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
     int par = 0;  // slot / register set of stream position t
     // one stream position: consume it (if it is a stage), gather t + 2 into its
     // slot, rotate the key registers, load the keys of t + 3
-    const bool trace0 = (a.variant & 16) && threadIdx.x == 0 && blockIdx.x < 4096;
+    const bool trace0 = GEE_TRACE_ON((a.variant & 16) && threadIdx.x == 0 && blockIdx.x < 4096);
     long long tw = 0, tc = 0, tg = 0;  // debug trace: wait / consume / refill cycles
     auto advance = [&](bool live) {
         const long long c0 = trace0 ? clock64() : 0;
@@ -1657,7 +1754,7 @@ __global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(St
             zphase ^= 1;
             zpending = false;
         }
-        const bool trace = (a.variant & 16) && threadIdx.x == 0 && blockIdx.x < 4096;
+        const bool trace = GEE_TRACE_ON((a.variant & 16) && threadIdx.x == 0 && blockIdx.x < 4096);
         const long long t1 = trace ? clock64() : 0;
         for (unsigned left = (p1 - p0 + step - 1) / step; left > 0;) {
             const bool live = vbits & 1u;
