@@ -64,7 +64,7 @@ constexpr int kDegNT = 256;           // degree threads (8 warps, a work item ea
 constexpr int kEmbWarps = kEmbNT / 32;
 constexpr size_t kZTileMax = 104 * 1024;  // bytes of the R x K f64 Z tile (upper bound)
 constexpr size_t kZTileDefault = 32 * 1024;  // default (A/B, profiles/r2_stream_ab.txt): several CTAs per SM hide item latency
-constexpr size_t emb_stage_bytes(int nt) { return (size_t)2 * 4 * nt * 16; }  // two stages of 4 records per thread
+constexpr size_t emb_stage_bytes(int nt, int u = 4) { return (size_t)2 * u * nt * 16; }  // two stages of u records per thread
 int t_emb_nt = 128;  // threads of the embed CTA (the debug hook that chose 256 / 512 is retired)
 constexpr unsigned kDegItem = 4096;  // entries per degree work item (one warp)
 constexpr int kScanBlock = 4096;     // buckets per k_st_scan2 block (1024 threads x 4)
@@ -1482,9 +1482,8 @@ __device__ __forceinline__ void epi_direct(const StArgs &a, double *zt, const do
 // descriptors of up to three items ahead from a ring that thread 0 refills
 // (one item per item consumed); an empty bucket's item has no stage, and a
 // position the cursor cannot fill yet is a bubble.
-template <int WT, bool OUT32, int NT>
-__global__ void __launch_bounds__(NT, 640 / NT > 0 ? 640 / NT : 1) k_st_embed(StArgs a) {
-    constexpr int U = 4;       // entries per thread per stage
+template <int WT, bool OUT32, int NT, int U = 4>  // U entries per thread per stage
+__global__ void __launch_bounds__(NT, (U == 1 ? 896 : U == 2 ? 768 : 640) / NT > 0 ? (U == 1 ? 896 : U == 2 ? 768 : 640) / NT : 1) k_st_embed(StArgs a) {
     constexpr int kRing = 8;   // work item descriptors {bucket, p0, p1, items of the bucket}
     constexpr int kAhead = 3;  // the cursor stays within this many items of the consumer
     extern __shared__ __align__(16) double zt[];  // [R][K], then fac[R], drec[R], the record slots
@@ -1814,28 +1813,26 @@ int set_smem(T *kern, size_t bytes) {
     return e == cudaSuccess ? GEE_OK : cuda_status(e);
 }
 
-template <int WT, int NT>
+template <int WT, int NT, int U>
 int launch_embed(const StGeo &g, const StArgs &a, bool out32, cudaStream_t st) {
     static PerDevice attr;
     const size_t smem =
-        sizeof(double) * (((size_t)1 << g.lrow_bits) * ((size_t)g.k + 3) + 4) + emb_stage_bytes(NT);
-    const size_t smax = kZTileMax + 24 * 512 + emb_stage_bytes(NT);
+        sizeof(double) * (((size_t)1 << g.lrow_bits) * ((size_t)g.k + 3) + 4) + emb_stage_bytes(NT, U);
+    const size_t smax = kZTileMax + 24 * 512 + emb_stage_bytes(NT, U);
     if (!attr.done()) {
         int rc;
-        if ((rc = set_smem(k_st_embed<WT, false, NT>, smax))) return rc;
-        if ((rc = set_smem(k_st_embed<WT, true, NT>, smax))) return rc;
+        if ((rc = set_smem(k_st_embed<WT, false, NT, U>, smax))) return rc;
+        if ((rc = set_smem(k_st_embed<WT, true, NT, U>, smax))) return rc;
         attr.mark();
     }
     int occ = 1;
-    if (out32) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_st_embed<WT, true, NT>, NT, smem);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_st_embed<WT, false, NT>, NT, smem);
+    if (out32) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_st_embed<WT, true, NT, U>, NT, smem);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_st_embed<WT, false, NT, U>, NT, smem);
     if (occ < 1) occ = 1;
-    if (out32) k_st_embed<WT, true, NT><<<num_sms() * occ, NT, smem, st>>>(a);
-    else k_st_embed<WT, false, NT><<<num_sms() * occ, NT, smem, st>>>(a);
+    if (out32) k_st_embed<WT, true, NT, U><<<num_sms() * occ, NT, smem, st>>>(a);
+    else k_st_embed<WT, false, NT, U><<<num_sms() * occ, NT, smem, st>>>(a);
     return GEE_OK;
 }
-
-
 
 // phase 1: partition the entries into row buckets and compute the degrees
 // (node records, or the raw local degrees of a row shard)
@@ -1896,7 +1893,20 @@ int run_phase2(const StGeo &g, StArgs &a, const double *deg_all, bool shard, cud
     }
     const bool out32 = (a.flags & GEE_FP32) != 0;
     int rc2;
-    rc2 = launch_embed<WT, 128>(g, a, out32, st);
+    // Entries per thread and stage (U): fewer mean fewer registers and less stage
+    // memory, so more resident CTAs whose epilogues and accumulations overlap --
+    // U = 4: 96 registers, 5 CTAs/SM; U = 2: 80, 6 CTAs; U = 1: 72, 7 CTAs (the
+    // gathers in flight per SM, 7 x 256, still cover DRAM latency at this rate).
+    // Measured (profiles/r2_session3_ab.txt): configs[3] 3.17 / 3.12 / 3.52 ms,
+    // configs[4] 2.71 / 2.48 / 2.40 ms, configs[2] 0.246 / 0.249 / 0.265 ms for
+    // U = 4 / 2 / 1: U = 1 where buckets are small next to their tile (the
+    // epilogue dominates), else U = 2.  Debug A/B bits: 16384 forces U = 4,
+    // 32768 U = 1, both U = 2.
+    const int force = (a.variant >> 14) & 3;
+    const int u = force == 1 ? 4 : force == 2 ? 1 : force == 3 ? 2 : (g.Mcap / (int64_t)(g.S ? g.S : 1) < 768 ? 1 : 2);
+    rc2 = u == 1   ? launch_embed<WT, 128, 1>(g, a, out32, st)
+          : u == 2 ? launch_embed<WT, 128, 2>(g, a, out32, st)
+                   : launch_embed<WT, 128, 4>(g, a, out32, st);
     if (rc2) return rc2;
     GEE_CHECK_LAUNCH("k_st_embed");
     return GEE_OK;
