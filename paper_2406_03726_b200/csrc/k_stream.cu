@@ -909,7 +909,7 @@ __device__ __forceinline__ void zero_scratch(const StArgs &a, unsigned b, int nr
 // the items of a larger bucket add into deg[] and the last one finalises
 // (and clears the bucket's embed scratch tile when the embed splits it too).
 template <int WT>
-__global__ void __launch_bounds__(kDegNT) k_st_degree(StArgs a) {
+__global__ void __launch_bounds__(kDegNT, 5) k_st_degree(StArgs a) {  // 48 registers: a fifth CTA per SM
     extern __shared__ double wdeg[];  // [kDegNT / 32][R][copies] f64, or [kDegNT / 32][2][R] u32 (integer mode)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int R = 1 << a.lrow_bits;
