@@ -163,10 +163,31 @@ __global__ void __launch_bounds__(1024) k_label_multi(const int64_t *__restrict_
     __syncthreads();
     if (!last) return;
     __threadfence();
-    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    // the last block sums the per-block rows with all of its threads: class c's
+    // blocks are split over blockDim / k slices (one thread per class did 1024
+    // dependent L2 round trips at configs[3]) and the slices meet in counts[c]
+    const int nsl = (int)blockDim.x / k;
+    if (nsl < 2) {  // more classes than half the block: a thread per class (configs[4]: 0.06 ms; sliced 0.13)
+        for (int c = threadIdx.x; c < k; c += blockDim.x) {
+            unsigned long long m = 0;
+            for (unsigned b = 0; b < gridDim.x; ++b) m += __ldcg(partial + (size_t)b * k + c);
+            counts[c] = (long long)m;
+            inv_nk[c] = m ? __ddiv_rn(1.0, (double)m) : 0.0;
+        }
+        if (threadIdx.x == 0) *done = 0;
+        return;
+    }
+    for (int c = threadIdx.x; c < k; c += blockDim.x) counts[c] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < nsl * k; t += blockDim.x) {
+        const int c = t % k, sl = t / k;
         unsigned long long m = 0;
-        for (unsigned b = 0; b < gridDim.x; ++b) m += __ldcg(partial + (size_t)b * k + c);
-        counts[c] = (long long)m;
+        for (unsigned b = sl; b < gridDim.x; b += nsl) m += __ldcg(partial + (size_t)b * k + c);
+        if (m) atomicAdd(reinterpret_cast<unsigned long long *>(counts) + c, m);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+        const unsigned long long m = (unsigned long long)__ldcg(counts + c);  // the atomics' result, from L2
         inv_nk[c] = m ? __ddiv_rn(1.0, (double)m) : 0.0;
     }
     if (threadIdx.x == 0) *done = 0;
