@@ -1,4 +1,6 @@
 """Phase trace of the stream embed (debug variant 16 + diagnostics): clock64 totals per CTA.
+Needs a library built with the trace compiled in: make -C paper_2406_03726_b200/csrc EXTRA=-DGEE_EMBED_TRACE
+(the normal build leaves it out: its counters cost the embed registers it does not have).
   python tools/embed_trace.py CONFIG [--nt=128] [--tile=32]"""
 import ctypes
 import os
